@@ -1,0 +1,192 @@
+/*
+ * qadc.h -- C ABI of the B200-native Quicker ADC scan path (libqadc_b200.so).
+ *
+ * This is the drop-in boundary for the reference's scan/search path
+ * (reference = header-only C++ library `pqscan`, paths below are relative to
+ * /root/reference/proj/include/pqscan/).  Plain pointers and sizes only; the
+ * library never throws: every entry point returns a status whose numeric class
+ * mirrors the reference's exception taxonomy (errors.hpp:9-46 and the exit codes
+ * the CLI maps them to, tools/pqscan_cli.cpp:20-30), and qadc_last_error() holds
+ * the message.  There is NO CPU fallback: with no usable CUDA device every
+ * compute entry point fails with QADC_ERR_CUDA.
+ *
+ * Host buffers are owned by the caller; a handle owns its device memory.
+ * A handle is immutable after open; calls on one handle serialise on its stream.
+ */
+#ifndef QADC_H
+#define QADC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QADC_MAX_SUBS 64
+#define QADC_MAX_GROUP 16
+#define QADC_MAX_R 1024 /* results per query supported by the device top-R stage */
+
+/* status classes: reference exception -> CLI exit code (errors.hpp, pqscan_cli.cpp:20-30) */
+enum {
+    QADC_OK = 0,
+    QADC_ERR_INVALID_SPEC = 3, /* invalid_spec_error */
+    QADC_ERR_TRAINING = 4,     /* training_error (unused by this path) */
+    QADC_ERR_INPUT = 5,        /* input_error */
+    QADC_ERR_CORRUPTION = 6,   /* corruption_error */
+    QADC_ERR_CONFIG = 7,       /* config_error */
+    QADC_ERR_IO = 8,           /* io_error (unused by this path) */
+    QADC_ERR_CALIBRATION = 9,  /* calibration_error */
+    QADC_ERR_CUDA = 20         /* CUDA runtime / no device: new class, no reference analogue */
+};
+
+/* Flattened PqSpec (pqspec.hpp:66-113) + PackingScheme (layout.hpp:18-46).
+ * Flat float codebooks are the per-subquantizer centroid matrices
+ * (codebook.hpp:60, k_j x dim_alloc[j] row-major) concatenated in subquantizer
+ * order (cb_off[j] floats in); flat LUTs are the per-subquantizer tables
+ * concatenated (ent_off[j] entries in). */
+typedef struct qadc_spec {
+    uint32_t dims;
+    uint32_t m;          /* subquantizers */
+    uint32_t g;          /* group size */
+    uint32_t groups;     /* m / g = rows of a packed block */
+    uint32_t word_width; /* 8 or 16: packing word AND quantized table width */
+    uint32_t block_len;  /* 16 / 32 / 64 codes per transposed block */
+    uint32_t exact;      /* proportional dim split was integral */
+    uint32_t total_entries;
+    uint32_t cb_floats;
+    uint8_t widths[QADC_MAX_GROUP];
+    uint8_t offsets[QADC_MAX_GROUP];
+    uint8_t bits[QADC_MAX_SUBS];
+    uint32_t dim_alloc[QADC_MAX_SUBS];
+    uint32_t dim_off[QADC_MAX_SUBS];
+    uint32_t ent_off[QADC_MAX_SUBS];
+    uint32_t cb_off[QADC_MAX_SUBS];
+} qadc_spec;
+
+/* SearchParams (index.hpp:20-32).  flags: bit 0 = fuse the final q*delta+d_min
+ * into one FMA like the reference's default -march=native build does
+ * (distance.hpp:158-161); default 0 = unfused, matching the pinned oracle. */
+typedef struct qadc_search_params {
+    uint32_t probes; /* IVF only */
+    uint32_t r;
+    uint32_t t;
+    uint32_t flags;
+} qadc_search_params;
+#define QADC_FLAG_FMA_UNQUANTIZE 1u
+
+/* counters of the last search on a handle (bench.py's gpu_launches comes from here) */
+typedef struct qadc_stats {
+    uint64_t kernel_launches; /* kernels of this library launched by the last call */
+    uint64_t scan_launches;
+    uint64_t pairs_scanned;   /* (query, code) pairs evaluated by the scan kernels */
+    uint64_t candidates;      /* pairs that passed the exact admission test */
+    uint64_t overflow_retries;
+    uint64_t segments;
+    uint32_t scan_variant;    /* which scan kernel variant ran (see qadc_variant_name) */
+    uint32_t query_tile;      /* queries (LUT rows) resident in shared memory per CTA */
+    float ms_lut, ms_scan, ms_select; /* CUDA-event time of the stages of the last search */
+} qadc_stats;
+
+typedef struct qadc_index qadc_index;
+
+const char* qadc_version(void);
+const char* qadc_last_error(void);
+const char* qadc_variant_name(uint32_t variant);
+/* number of CUDA devices visible, or a negative QADC_ERR_CUDA-class failure */
+int qadc_device_count(void);
+
+/* parse_spec_string + allocate_dims + PackingScheme::for_spec
+ * (pqspec.hpp:24-55, 119-171; layout.hpp:27-43) */
+int qadc_spec_parse(uint32_t dims, const char* text, qadc_spec* out);
+
+/* bytes of a PackedList holding n codes (layout.hpp:135-144) */
+uint64_t qadc_packed_bytes(const qadc_spec* spec, uint64_t n);
+
+/* ---- FlatIndex (index.hpp:73-157) ---------------------------------------
+ * packed/count: the reference PackedList bytes of this shard (layout.hpp:135-160).
+ * base_id: id of the shard's first code (ids are base_id + position,
+ *          scan_scalar.hpp:60); 0 for an unsharded index.
+ * calib_packed/calib_count: PackedList of the first codes of the WHOLE list
+ *          (>= the largest t that will be used), needed only by shards whose
+ *          own head is not the global head (index.hpp:124-129 calibrates on the
+ *          global prefix); NULL/0 = use this shard's own head.
+ * device: CUDA ordinal. */
+int qadc_flat_open(const qadc_spec* spec, const float* codebook, const uint8_t* packed, uint64_t count,
+                   uint32_t base_id, const uint8_t* calib_packed, uint64_t calib_count, int device,
+                   qadc_index** out);
+
+/* ---- IvfIndex (index.hpp:166-177, 276-341) ------------------------------
+ * Lists are concatenated: list c has list_count[c] codes, PackedList bytes at
+ * packed + list_byte_off[c], ids at ids + list_id_off[c].
+ * calib_*: per-list PackedList of the first min(count_global, t_max) codes of the
+ * unsharded list (same convention as the flat index), or NULL to use own heads;
+ * calib_count[c] is the GLOBAL list length capped at what calib_packed holds. */
+int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
+                  const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
+                  const uint64_t* list_count, const uint32_t* ids, const uint8_t* calib_packed,
+                  const uint64_t* calib_byte_off, const uint64_t* calib_count, int device, qadc_index** out);
+
+void qadc_close(qadc_index* h);
+
+/* FlatIndex::search / IvfIndex::search over a batch (index.hpp:110, 276), host buffers.
+ * out_ids/out_dists: nq*r, ascending (distance, id); rows shorter than r are
+ * padded (id 0xFFFFFFFF, dist +inf) and out_counts[q] < r says so
+ * (reference returns shorter vectors, T/test_index.cpp:33-44). */
+int qadc_search_batch(qadc_index* h, const float* queries, uint32_t nq, const qadc_search_params* params,
+                      uint32_t* out_ids, float* out_dists, uint32_t* out_counts);
+
+/* Same with DEVICE buffers on `stream` (a cudaStream_t, NULL = the handle's own).
+ * d_out_keys (optional, nq*r u64): (quantized distance << 32 | id), padded with
+ * ~0, the per-shard lists exchanged by the multi-GPU merge.
+ * d_out_map (optional, nq*2 floats): {delta, d_min} of each query's affine map. */
+int qadc_search_batch_device(qadc_index* h, const float* d_queries, uint32_t nq, const qadc_search_params* params,
+                             uint32_t* d_out_ids, float* d_out_dists, uint32_t* d_out_counts,
+                             uint64_t* d_out_keys, float* d_out_map, void* stream);
+
+/* Multi-GPU exchange step: merge `nshards` per-shard key lists (layout
+ * [shard][nq][r], as gathered by NCCL all_gather) into the global top-r and
+ * unquantize with the (replicated) map.  Device buffers. */
+int qadc_merge_topk_device(const uint64_t* d_keys, uint32_t nshards, uint32_t nq, uint32_t r, const float* d_map,
+                           uint32_t flags, uint32_t* d_out_ids, float* d_out_dists, uint32_t* d_out_counts,
+                           int device, void* stream);
+
+/* ---- debug / parity entry points ----------------------- */
+/* float LUTs (compute_tables, distance.hpp:35-58), calibration and quantized
+ * LUTs (quantize_tables, distance.hpp:102-142) of a flat index.  Any output may
+ * be NULL.  luts: nq*total_entries floats; qluts: nq*total_entries at table
+ * width; calib: nq*4 floats {d_min, d_max, delta, own_d_min}. */
+int qadc_flat_tables(qadc_index* h, const float* queries, uint32_t nq, const qadc_search_params* params,
+                     float* luts, void* qluts, float* calib);
+
+/* raw saturating ADC sums (adc_scalar_quantized, distance.hpp:149-155) of codes
+ * [first, first+n) of a flat index under a caller-supplied quantized LUT */
+int qadc_flat_adc_sums(qadc_index* h, const void* qlut, uint32_t width, uint32_t acc_init, uint64_t first,
+                       uint64_t n, uint32_t* sums);
+
+/* IvfIndex::probe_order (index.hpp:247-265) for a batch: order is nq*min(a,K) */
+int qadc_ivf_probe_order(qadc_index* h, const float* queries, uint32_t nq, uint32_t a, uint32_t* order);
+
+/* QuantizedScanFn (simd/kernels.hpp:49-50; normative body scan_scalar.hpp:34-64):
+ * scan one PackedList with caller-supplied quantized tables into a bounded
+ * (distance, id) heap.  heap_in_*: n_in pre-seeded entries; outputs: the heap's
+ * sorted() contents (heap.hpp:61-65), *n_out <= cap entries. */
+int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count, uint32_t rows, const void* qlut,
+                   uint32_t width, const uint32_t* ids, uint32_t base_id, uint32_t acc_init, uint32_t cap,
+                   const uint32_t* heap_in_dist, const uint32_t* heap_in_id, uint32_t n_in, uint32_t* out_dist,
+                   uint32_t* out_id, uint32_t* n_out, int device);
+
+/* encode (codebook.hpp:94-118) on the GPU: codes is n*m bytes ("next" row N2) */
+int qadc_encode(const qadc_spec* spec, const float* codebook, const float* vectors, uint64_t n, uint8_t* codes,
+                int device);
+
+int qadc_get_stats(const qadc_index* h, qadc_stats* out);
+/* tuning knobs for experiments: name in {"cand_cap","seg0","seg_growth","force_variant","threads"} */
+int qadc_set_option(qadc_index* h, const char* name, int64_t value);
+/* device pointer / stride of the re-laid code array (for tests of the layout bijection) */
+int qadc_flat_download_codes(qadc_index* h, uint64_t first, uint64_t n, uint8_t* codes_out /* n*m subquantizer indices */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

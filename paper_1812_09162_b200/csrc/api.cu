@@ -1,0 +1,771 @@
+// api.cu -- the C ABI (include/qadc.h): index handles, search orchestration, error mapping.
+//
+// Host-side mirror of FlatIndex::search (index.hpp:110-145), IvfIndex::search
+// (index.hpp:276-341) and the QuantizedScanFn plugin point (simd/kernels.hpp:49-50),
+// batched over queries.  Everything that touches data runs in CUDA kernels of this
+// library; there is no CPU fallback.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace qadc {
+
+void parse_spec(uint32_t dims, const std::string& text, qadc_spec& out);
+void validate_spec(const qadc_spec& s);
+const char* variant_name(uint32_t v);
+
+static thread_local std::string g_error;
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        g_launches = 0;
+        f();
+        return QADC_OK;
+    } catch (const Error& e) {
+        g_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_error = "out of host memory";
+        return QADC_ERR_INPUT;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return QADC_ERR_CUDA;
+    }
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    void ensure(size_t bytes) {
+        if (bytes <= cap) return;
+        release();
+        if (bytes == 0) return;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess)
+            throw Error(QADC_ERR_CUDA, "cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+        cap = bytes;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+static void set_device(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw Error(QADC_ERR_CUDA, std::string("no usable CUDA device (this library has no CPU fallback): ") +
+                                       (e != cudaSuccess ? cudaGetErrorString(e) : "device count is 0"));
+    if (device < 0 || device >= n) throw Error(QADC_ERR_INPUT, "device ordinal out of range");
+    QADC_CUDA_CHECK(cudaSetDevice(device));
+}
+
+static void validate_params(const qadc_search_params& p, bool ivf) {
+    // SearchParams::validate, index.hpp:27-31
+    if (p.r < 1) throw Error(QADC_ERR_INPUT, "search: R must be at least 1");
+    if (p.t < p.r) throw Error(QADC_ERR_INPUT, "search: calibration prefix t must be at least R");
+    if (ivf && p.probes < 1) throw Error(QADC_ERR_INPUT, "search: probes must be at least 1");
+    if (p.r > QADC_MAX_R) throw Error(QADC_ERR_CONFIG, "search: R exceeds QADC_MAX_R supported by the device top-R stage");
+    if (p.t > 16384) throw Error(QADC_ERR_CONFIG, "search: calibration prefix t exceeds 16384");
+}
+
+// Per-query selection state on the device.
+struct SelectBufs {
+    DevBuf thr_key, cand, cand_count, top, ntop, overflow;
+    uint32_t cap = 0, kpad = 0;
+    void ensure(uint32_t nq, uint32_t r, uint32_t cap_) {
+        cap = cap_;
+        kpad = r;
+        thr_key.ensure(size_t(nq) * 8);
+        cand.ensure(size_t(nq) * cap * 8);
+        cand_count.ensure(size_t(nq) * 4);
+        top.ensure(size_t(nq) * kpad * 8);
+        ntop.ensure(size_t(nq) * 4);
+        overflow.ensure(size_t(nq) * 4);
+    }
+};
+
+// Stage timing with CUDA events recorded on the launching stream (no extra syncs: the events are
+// read after the call's own final synchronisation).  stage: 0 tables, 1 scan, 2 select.
+struct StageTimer {
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<int, std::pair<size_t, size_t>>> spans; // stage -> (begin, end) event index
+    size_t used = 0;
+    ~StageTimer() {
+        for (auto e : pool) cudaEventDestroy(e);
+    }
+    void reset() {
+        used = 0;
+        spans.clear();
+        tags.clear();
+    }
+    size_t mark(cudaStream_t st) {
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            QADC_CUDA_CHECK(cudaEventCreate(&e));
+            pool.push_back(e);
+        }
+        QADC_CUDA_CHECK(cudaEventRecord(pool[used], st));
+        return used++;
+    }
+    std::vector<uint64_t> tags;
+    void span(int stage, size_t b, size_t e, uint64_t tag = 0) {
+        spans.push_back({stage, {b, e}});
+        tags.push_back(tag);
+    }
+    void collect(float* ms /* [3] */) {
+        const bool trace = std::getenv("QADC_TRACE") != nullptr;
+        for (size_t i = 0; i < spans.size(); ++i) {
+            auto& sp = spans[i];
+            float t = 0.f;
+            if (cudaEventElapsedTime(&t, pool[sp.second.first], pool[sp.second.second]) == cudaSuccess) ms[sp.first] += t;
+            if (trace) fprintf(stderr, "[qadc trace] stage %d tag %llu: %.3f ms\n", sp.first, (unsigned long long)tags[i], t);
+        }
+    }
+};
+
+} // namespace qadc
+
+using namespace qadc;
+
+struct qadc_index {
+    int kind = 0; // 0 flat, 1 ivf
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;
+    qadc_spec spec{};
+    DevSpec ds{};
+    DevBuf codebook, codes, calib, ids;
+    uint64_t count = 0, count_padded = 0;
+    uint32_t base_id = 0;
+    uint32_t calib_count = 0;
+    // ivf
+    uint32_t k_cells = 0;
+    DevBuf coarse, coarse_t, list_code_off, list_count_dev, calib_off_dev, calib_count_dev;
+    std::vector<uint64_t> list_code_off_h, list_count_h, list_ids_off_h;
+    // options
+    uint32_t cand_cap = 8192;
+    uint32_t seg0 = 4096;
+    uint32_t seg_growth = 8;
+    int force_variant = -1;
+    // workspace
+    SelectBufs sel;
+    DevBuf qlut, luts, calib_out, map, status, jobs, queries, out_ids, out_dists, out_counts, counters, scratch;
+    qadc_stats stats{};
+    StageTimer timer;
+
+    ~qadc_index() {
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace qadc {
+
+static constexpr uint64_t CODE_PAD = 1024; // device code arrays are padded to this many codes
+
+static ScanPlan plan_for(const qadc_index* h) { return plan_scan(h->ds, h->device, h->force_variant, 0); }
+
+// Geometric segment schedule: after n codes the R-th best of n bounds the admission
+// rate of the next codes by R/n, so each segment admits O(R * growth) candidates.
+static std::vector<uint64_t> segment_bounds(uint64_t count, uint64_t seg0, uint64_t growth) {
+    std::vector<uint64_t> b{0};
+    uint64_t len = std::max<uint64_t>(seg0, 256);
+    while (b.back() < count) {
+        uint64_t next = std::min(count, b.back() + len);
+        if (count - next < len / 2) next = count; // do not leave a tiny tail segment
+        b.push_back(next);
+        len *= std::max<uint64_t>(growth, 2);
+    }
+    return b;
+}
+
+// Jobs of one segment of a flat list: tile-major so that a CTA's contiguous slice of the
+// job list mostly stays on one LUT tile.
+static void flat_segment_jobs(std::vector<ScanJob>& jobs, uint64_t seg_begin, uint64_t seg_end, uint32_t nq,
+                              uint32_t tq, uint32_t base_id, int grid) {
+    const uint32_t tiles = (nq + tq - 1) / tq;
+    const uint64_t n = seg_end - seg_begin;
+    uint64_t chunk = (n * tiles + uint64_t(grid) * 16 - 1) / (uint64_t(grid) * 16);
+    chunk = std::max<uint64_t>(256, (chunk + 255) / 256 * 256);
+    chunk = std::min<uint64_t>(chunk, 1u << 22);
+    for (uint32_t t = 0; t < tiles; ++t)
+        for (uint64_t c = seg_begin; c < seg_end; c += chunk) {
+            ScanJob j{};
+            j.code_off = c;
+            j.ids_off = c;
+            j.n_codes = uint32_t(std::min(chunk, seg_end - c));
+            j.id_base = base_id + uint32_t(c);
+            j.row_begin = t * tq;
+            j.n_rows = std::min(tq, nq - t * tq);
+            jobs.push_back(j);
+        }
+}
+
+struct RowSet {
+    const void* qlut;          // device [rows][E]
+    const uint32_t* row_query; // device or nullptr
+    const uint32_t* row_bias;  // device or nullptr
+};
+
+// Scan `count` codes for nq queries (rows == queries) segment by segment, tightening the
+// per-query thresholds in between; leaves the unsorted top-r in h->sel.top / ntop.
+// Returns false if some query overflowed its candidate buffer (caller retries with a
+// larger cap).
+static bool scan_select_flat(qadc_index* h, const ScanPlan& plan, const uint8_t* d_codes, uint64_t count,
+                             uint32_t base_id, const RowSet& rows, uint32_t nq, uint32_t r, uint32_t cap,
+                             bool keep_state, cudaStream_t st) {
+    h->sel.ensure(nq, r, cap);
+    if (!keep_state)
+        launch_init_select(h->sel.thr_key.as<uint64_t>(), h->sel.cand_count.as<uint32_t>(), h->sel.ntop.as<uint32_t>(),
+                           h->sel.overflow.as<uint32_t>(), nq, st);
+    const int grid = h->num_sms;
+    // dense exact top-r over the head: seeds every query's threshold before the streaming scan
+    const uint64_t head = keep_state ? 0 : std::min<uint64_t>(count, h->seg0);
+    if (head) {
+        const size_t s0e = h->timer.mark(st);
+        launch_seed_topk(h->ds, d_codes, uint32_t(head), base_id, nullptr, rows.qlut, rows.row_bias, nq, r,
+                         h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad,
+                         h->sel.thr_key.as<uint64_t>(), st);
+        h->timer.span(2, s0e, h->timer.mark(st));
+    }
+    std::vector<uint64_t> bounds = segment_bounds(count - head, uint64_t(h->seg0) * h->seg_growth, h->seg_growth);
+    for (auto& b : bounds) b += head;
+    std::vector<ScanJob> jobs;
+    std::vector<std::pair<size_t, size_t>> seg_jobs;
+    for (size_t s = 0; s + 1 < bounds.size(); ++s) {
+        const size_t first = jobs.size();
+        flat_segment_jobs(jobs, bounds[s], bounds[s + 1], nq, plan.tq, base_id, grid);
+        seg_jobs.emplace_back(first, jobs.size() - first);
+    }
+    h->jobs.ensure(jobs.size() * sizeof(ScanJob));
+    if (!jobs.empty())
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->jobs.p, jobs.data(), jobs.size() * sizeof(ScanJob), cudaMemcpyHostToDevice, st));
+    for (size_t si = 0; si < seg_jobs.size(); ++si) {
+        const size_t first = seg_jobs[si].first, n = seg_jobs[si].second;
+        ScanArgs a{};
+        a.codes = d_codes;
+        a.ids = nullptr;
+        a.qlut = rows.qlut;
+        a.row_query = rows.row_query;
+        a.row_bias = rows.row_bias;
+        a.jobs = h->jobs.as<ScanJob>() + first;
+        a.n_jobs = uint32_t(n);
+        a.thr_key = h->sel.thr_key.as<uint64_t>();
+        a.cand = h->sel.cand.as<uint64_t>();
+        a.cand_count = h->sel.cand_count.as<uint32_t>();
+        a.cap = cap;
+        a.overflow = h->sel.overflow.as<uint32_t>();
+        a.counters = h->counters.as<unsigned long long>();
+        const size_t e0 = h->timer.mark(st);
+        launch_scan(plan, h->ds, a, std::min<int>(grid, int(n)), st);
+        const size_t e1 = h->timer.mark(st);
+        launch_tighten(h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad, h->sel.cand.as<uint64_t>(),
+                       h->sel.cand_count.as<uint32_t>(), cap, h->sel.thr_key.as<uint64_t>(), nq, r, st);
+        const size_t e2 = h->timer.mark(st);
+        h->timer.span(1, e0, e1, bounds[si + 1] - bounds[si]);
+        h->timer.span(2, e1, e2);
+        h->stats.scan_launches += 1;
+        h->stats.segments += 1;
+    }
+    h->stats.pairs_scanned += count * nq;
+    // overflow check (one small D2H; the only host sync of a batch)
+    std::vector<uint32_t> ov(nq);
+    QADC_CUDA_CHECK(cudaMemcpyAsync(ov.data(), h->sel.overflow.p, size_t(nq) * 4, cudaMemcpyDeviceToHost, st));
+    QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (uint32_t v : ov)
+        if (v) return false;
+    return true;
+}
+
+static void fill_empty_results(uint32_t nq, uint32_t r, uint32_t* d_ids, float* d_dists, uint32_t* d_counts,
+                               uint64_t* d_keys, float* d_map, cudaStream_t st) {
+    // empty database: every query returns an empty result (index.hpp:113)
+    if (d_ids) QADC_CUDA_CHECK(cudaMemsetAsync(d_ids, 0xFF, size_t(nq) * r * 4, st));
+    if (d_dists) {
+        std::vector<float> inf(size_t(nq) * r, __builtin_inff());
+        QADC_CUDA_CHECK(cudaMemcpyAsync(d_dists, inf.data(), inf.size() * 4, cudaMemcpyHostToDevice, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    if (d_counts) QADC_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, size_t(nq) * 4, st));
+    if (d_keys) QADC_CUDA_CHECK(cudaMemsetAsync(d_keys, 0xFF, size_t(nq) * r * 8, st));
+    if (d_map) QADC_CUDA_CHECK(cudaMemsetAsync(d_map, 0, size_t(nq) * 2 * 4, st));
+}
+
+static void check_status(qadc_index* h, cudaStream_t st) {
+    int status = 0;
+    QADC_CUDA_CHECK(cudaMemcpyAsync(&status, h->status.p, 4, cudaMemcpyDeviceToHost, st));
+    QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (status == QADC_ERR_CALIBRATION) throw Error(QADC_ERR_CALIBRATION, "quantize_tables: d_max < d_min");
+    if (status) throw Error(status, "device-side failure");
+}
+
+static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t nq, const qadc_search_params& p,
+                               uint32_t* d_ids, float* d_dists, uint32_t* d_counts, uint64_t* d_keys, float* d_map,
+                               cudaStream_t st) {
+    validate_params(p, false);
+    h->stats = qadc_stats{};
+    h->timer.reset();
+    if (nq == 0) return;
+    if (h->calib_count == 0) { // the whole list is empty
+        fill_empty_results(nq, p.r, d_ids, d_dists, d_counts, d_keys, d_map, st);
+        h->stats.kernel_launches = g_launches;
+        return;
+    }
+    const ScanPlan plan = plan_for(h);
+    h->stats.scan_variant = plan.variant;
+    h->stats.query_tile = plan.tq;
+    const DevSpec& ds = h->ds;
+    const size_t wb = ds.word_width / 8;
+    h->status.ensure(4);
+    h->counters.ensure(16);
+    QADC_CUDA_CHECK(cudaMemsetAsync(h->status.p, 0, 4, st));
+
+    // query batches bound the candidate-buffer footprint
+    uint32_t cap = h->cand_cap;
+    const size_t budget = size_t(4) << 30;
+    for (uint32_t q0 = 0; q0 < nq;) {
+        const uint32_t qb_max = uint32_t(std::max<size_t>(1, budget / (size_t(cap) * 8)));
+        const uint32_t nb = std::min<uint32_t>(nq - q0, std::min<uint32_t>(qb_max, 1u << 16));
+        h->qlut.ensure(size_t(nb) * ds.E * wb);
+        h->map.ensure(size_t(nb) * 2 * 4);
+        LutArgs la{};
+        la.codebook = h->codebook.as<float>();
+        la.queries = d_queries + size_t(q0) * ds.dims;
+        la.calib_codes = h->calib.as<uint8_t>();
+        la.calib_count = h->calib_count;
+        la.nq = nb;
+        la.r = p.r;
+        la.t = p.t;
+        la.qluts = h->qlut.p;
+        la.map = h->map.as<float>();
+        la.status = h->status.as<int>();
+        const size_t t0 = h->timer.mark(st);
+        launch_flat_tables(ds, la, st);
+        h->timer.span(0, t0, h->timer.mark(st));
+        RowSet rows{h->qlut.p, nullptr, nullptr};
+        const bool ok = scan_select_flat(h, plan, h->codes.as<uint8_t>(), h->count, h->base_id, rows, nb, p.r, cap,
+                                         false, st);
+        if (!ok) { // some query admitted more candidates than fit: redo this batch with a larger buffer
+            if (uint64_t(cap) >= h->count + p.r) throw Error(QADC_ERR_CUDA, "internal: candidate overflow at full capacity");
+            cap = uint32_t(std::min<uint64_t>(uint64_t(cap) * 8, h->count + p.r));
+            h->stats.overflow_retries += 1;
+            continue;
+        }
+        const size_t f0 = h->timer.mark(st);
+        launch_finalize(h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad, 1, nb, p.r, h->map.as<float>(),
+                        p.flags, ds.qmax, d_ids ? d_ids + size_t(q0) * p.r : nullptr,
+                        d_dists ? d_dists + size_t(q0) * p.r : nullptr, d_counts ? d_counts + q0 : nullptr,
+                        d_keys ? d_keys + size_t(q0) * p.r : nullptr, st);
+        h->timer.span(2, f0, h->timer.mark(st));
+        if (d_map)
+            QADC_CUDA_CHECK(cudaMemcpyAsync(d_map + size_t(q0) * 2, h->map.p, size_t(nb) * 8, cudaMemcpyDeviceToDevice, st));
+        q0 += nb;
+        cap = h->cand_cap;
+    }
+    check_status(h, st);
+    float ms[3] = {0.f, 0.f, 0.f};
+    h->timer.collect(ms);
+    h->stats.ms_lut = ms[0];
+    h->stats.ms_scan = ms[1];
+    h->stats.ms_select = ms[2];
+    h->stats.kernel_launches = g_launches;
+}
+
+static void upload_list(qadc_index* h, const qadc_spec& s, const DevSpec& ds, const uint8_t* packed, uint64_t count,
+                        DevBuf& out, uint64_t& padded, cudaStream_t st) {
+    padded = (count + CODE_PAD - 1) / CODE_PAD * CODE_PAD + CODE_PAD;
+    out.ensure(size_t(padded) * ds.code_stride);
+    const uint64_t bytes = qadc_packed_bytes(&s, count);
+    DevBuf tmp;
+    tmp.ensure(bytes);
+    if (bytes) QADC_CUDA_CHECK(cudaMemcpyAsync(tmp.p, packed, bytes, cudaMemcpyHostToDevice, st));
+    launch_relayout(s, ds, tmp.as<uint8_t>(), count, padded, out.as<uint8_t>(), st);
+    QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    (void)h;
+}
+
+} // namespace qadc
+
+// =============================================================== C ABI ======
+
+extern "C" {
+
+const char* qadc_version(void) { return "qadc-b200 0.1 (sm_100a)"; }
+const char* qadc_last_error(void) { return g_error.c_str(); }
+const char* qadc_variant_name(uint32_t v) { return variant_name(v); }
+
+int qadc_device_count(void) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        g_error = cudaGetErrorString(e);
+        cudaGetLastError();
+        return -QADC_ERR_CUDA;
+    }
+    return n;
+}
+
+int qadc_spec_parse(uint32_t dims, const char* text, qadc_spec* out) {
+    return guarded([&] {
+        if (!text || !out) throw Error(QADC_ERR_INPUT, "null argument");
+        parse_spec(dims, text, *out);
+    });
+}
+
+uint64_t qadc_packed_bytes(const qadc_spec* s, uint64_t n) {
+    if (n == 0) return 0;
+    const uint64_t blocks = (n + s->block_len - 1) / s->block_len;
+    return blocks * s->groups * s->block_len * (s->word_width / 8);
+}
+
+int qadc_flat_open(const qadc_spec* spec, const float* codebook, const uint8_t* packed, uint64_t count,
+                   uint32_t base_id, const uint8_t* calib_packed, uint64_t calib_count, int device,
+                   qadc_index** out) {
+    return guarded([&] {
+        if (!spec || !codebook || !out || (count && !packed)) throw Error(QADC_ERR_INPUT, "null argument");
+        validate_spec(*spec);
+        set_device(device);
+        std::unique_ptr<qadc_index> h(new qadc_index);
+        h->kind = 0;
+        h->device = device;
+        h->spec = *spec;
+        h->ds = make_dev_spec(*spec, spec->groups);
+        if (h->ds.code_stride > 32) throw Error(QADC_ERR_CONFIG, "codes wider than 256 bits are not supported");
+        QADC_CUDA_CHECK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+        QADC_CUDA_CHECK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        for (uint32_t i = 0; i < spec->cb_floats; ++i)
+            if (!(codebook[i] - codebook[i] == 0.0f)) // codebook.hpp:45-46
+                throw Error(QADC_ERR_CORRUPTION, "codebook: non-finite centroid component");
+        h->codebook.ensure(size_t(spec->cb_floats) * 4);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->codebook.p, codebook, size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice, h->stream));
+        h->count = count;
+        h->base_id = base_id;
+        upload_list(h.get(), *spec, h->ds, packed, count, h->codes, h->count_padded, h->stream);
+        if (calib_packed && calib_count) {
+            uint64_t pad = 0;
+            const uint64_t n = std::min<uint64_t>(calib_count, 16384);
+            upload_list(h.get(), *spec, h->ds, calib_packed, n, h->calib, pad, h->stream);
+            h->calib_count = uint32_t(n);
+        } else {
+            const uint64_t n = std::min<uint64_t>(count, 16384);
+            h->calib.ensure(std::max<size_t>(size_t(n) * h->ds.code_stride, 16));
+            if (n) QADC_CUDA_CHECK(cudaMemcpyAsync(h->calib.p, h->codes.p, size_t(n) * h->ds.code_stride, cudaMemcpyDeviceToDevice, h->stream));
+            h->calib_count = uint32_t(n);
+        }
+        QADC_CUDA_CHECK(cudaStreamSynchronize(h->stream));
+        *out = h.release();
+    });
+}
+
+void qadc_close(qadc_index* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    delete h;
+}
+
+int qadc_search_batch_device(qadc_index* h, const float* d_queries, uint32_t nq, const qadc_search_params* params,
+                             uint32_t* d_out_ids, float* d_out_dists, uint32_t* d_out_counts,
+                             uint64_t* d_out_keys, float* d_out_map, void* stream) {
+    return guarded([&] {
+        if (!h || !params || (nq && !d_queries)) throw Error(QADC_ERR_INPUT, "null argument");
+        set_device(h->device);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
+        if (h->kind == 0)
+            flat_search_device(h, d_queries, nq, *params, d_out_ids, d_out_dists, d_out_counts, d_out_keys, d_out_map, st);
+        else
+            throw Error(QADC_ERR_CONFIG, "ivf search: not built yet");
+    });
+}
+
+int qadc_search_batch(qadc_index* h, const float* queries, uint32_t nq, const qadc_search_params* params,
+                      uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {
+    return guarded([&] {
+        if (!h || !params || (nq && (!queries || !out_ids || !out_dists || !out_counts)))
+            throw Error(QADC_ERR_INPUT, "null argument");
+        validate_params(*params, h->kind == 1);
+        set_device(h->device);
+        cudaStream_t st = h->stream;
+        const size_t nr = size_t(nq) * params->r;
+        h->queries.ensure(size_t(nq) * h->ds.dims * 4);
+        h->out_ids.ensure(nr * 4);
+        h->out_dists.ensure(nr * 4);
+        h->out_counts.ensure(size_t(nq) * 4);
+        if (nq == 0) return;
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->queries.p, queries, size_t(nq) * h->ds.dims * 4, cudaMemcpyHostToDevice, st));
+        const unsigned long long before = g_launches;
+        if (h->kind == 0)
+            flat_search_device(h, h->queries.as<float>(), nq, *params, h->out_ids.as<uint32_t>(), h->out_dists.as<float>(),
+                               h->out_counts.as<uint32_t>(), nullptr, nullptr, st);
+        else
+            throw Error(QADC_ERR_CONFIG, "ivf search: not built yet");
+        (void)before;
+        QADC_CUDA_CHECK(cudaMemcpyAsync(out_ids, h->out_ids.p, nr * 4, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaMemcpyAsync(out_dists, h->out_dists.p, nr * 4, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaMemcpyAsync(out_counts, h->out_counts.p, size_t(nq) * 4, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int qadc_merge_topk_device(const uint64_t* d_keys, uint32_t nshards, uint32_t nq, uint32_t r, const float* d_map,
+                           uint32_t flags, uint32_t* d_out_ids, float* d_out_dists, uint32_t* d_out_counts,
+                           int device, void* stream) {
+    return guarded([&] {
+        if (!d_keys || nshards == 0 || r == 0) throw Error(QADC_ERR_INPUT, "merge: bad arguments");
+        set_device(device);
+        launch_finalize(d_keys, nullptr, r, nshards, nq, r, d_map, flags, 0xFFFFFFFFu, d_out_ids, d_out_dists,
+                        d_out_counts, nullptr, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int qadc_flat_tables(qadc_index* h, const float* queries, uint32_t nq, const qadc_search_params* params,
+                     float* luts, void* qluts, float* calib) {
+    return guarded([&] {
+        if (!h || h->kind != 0 || !params || !queries) throw Error(QADC_ERR_INPUT, "tables: bad arguments");
+        validate_params(*params, false);
+        set_device(h->device);
+        if (nq == 0) return;
+        if (h->calib_count == 0) throw Error(QADC_ERR_INPUT, "tables: empty index");
+        cudaStream_t st = h->stream;
+        const DevSpec& ds = h->ds;
+        const size_t wb = ds.word_width / 8;
+        h->queries.ensure(size_t(nq) * ds.dims * 4);
+        h->qlut.ensure(size_t(nq) * ds.E * wb);
+        h->luts.ensure(size_t(nq) * ds.E * 4);
+        h->calib_out.ensure(size_t(nq) * 16);
+        h->map.ensure(size_t(nq) * 8);
+        h->status.ensure(4);
+        QADC_CUDA_CHECK(cudaMemsetAsync(h->status.p, 0, 4, st));
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->queries.p, queries, size_t(nq) * ds.dims * 4, cudaMemcpyHostToDevice, st));
+        LutArgs la{};
+        la.codebook = h->codebook.as<float>();
+        la.queries = h->queries.as<float>();
+        la.calib_codes = h->calib.as<uint8_t>();
+        la.calib_count = h->calib_count;
+        la.nq = nq;
+        la.r = params->r;
+        la.t = params->t;
+        la.luts = h->luts.as<float>();
+        la.qluts = h->qlut.p;
+        la.calib = h->calib_out.as<float>();
+        la.map = h->map.as<float>();
+        la.status = h->status.as<int>();
+        launch_flat_tables(ds, la, st);
+        if (luts) QADC_CUDA_CHECK(cudaMemcpyAsync(luts, h->luts.p, size_t(nq) * ds.E * 4, cudaMemcpyDeviceToHost, st));
+        if (qluts) QADC_CUDA_CHECK(cudaMemcpyAsync(qluts, h->qlut.p, size_t(nq) * ds.E * wb, cudaMemcpyDeviceToHost, st));
+        if (calib) QADC_CUDA_CHECK(cudaMemcpyAsync(calib, h->calib_out.p, size_t(nq) * 16, cudaMemcpyDeviceToHost, st));
+        check_status(h, st);
+    });
+}
+
+int qadc_flat_adc_sums(qadc_index* h, const void* qlut, uint32_t width, uint32_t acc_init, uint64_t first,
+                       uint64_t n, uint32_t* sums) {
+    return guarded([&] {
+        if (!h || h->kind != 0 || !qlut || !sums) throw Error(QADC_ERR_INPUT, "adc_sums: bad arguments");
+        if (width != h->ds.word_width) throw Error(QADC_ERR_CONFIG, "scan: table width does not match the packing word width");
+        if (first + n > h->count) throw Error(QADC_ERR_INPUT, "adc_sums: range exceeds list");
+        set_device(h->device);
+        cudaStream_t st = h->stream;
+        const size_t wb = width / 8;
+        h->qlut.ensure(size_t(h->ds.E) * wb);
+        h->scratch.ensure(size_t(n) * 4);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->qlut.p, qlut, size_t(h->ds.E) * wb, cudaMemcpyHostToDevice, st));
+        launch_adc_sums(h->ds, h->codes.as<uint8_t>(), h->qlut.p, acc_init, first, n, h->scratch.as<uint32_t>(), st);
+        if (n) QADC_CUDA_CHECK(cudaMemcpyAsync(sums, h->scratch.p, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int qadc_flat_download_codes(qadc_index* h, uint64_t first, uint64_t n, uint8_t* codes_out) {
+    return guarded([&] {
+        if (!h || h->kind != 0 || !codes_out) throw Error(QADC_ERR_INPUT, "download_codes: bad arguments");
+        if (first + n > h->count) throw Error(QADC_ERR_INPUT, "download_codes: range exceeds list");
+        set_device(h->device);
+        cudaStream_t st = h->stream;
+        h->scratch.ensure(size_t(n) * h->ds.m);
+        launch_unlayout(h->ds, h->codes.as<uint8_t>(), first, n, h->scratch.as<uint8_t>(), st);
+        if (n) QADC_CUDA_CHECK(cudaMemcpyAsync(codes_out, h->scratch.p, size_t(n) * h->ds.m, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
+int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count, uint32_t rows, const void* qlut,
+                   uint32_t width, const uint32_t* ids, uint32_t base_id, uint32_t acc_init, uint32_t cap,
+                   const uint32_t* heap_in_dist, const uint32_t* heap_in_id, uint32_t n_in, uint32_t* out_dist,
+                   uint32_t* out_id, uint32_t* n_out, int device) {
+    return guarded([&] {
+        if (!spec || !qlut || !out_dist || !out_id || !n_out) throw Error(QADC_ERR_INPUT, "scan_list: null argument");
+        validate_spec(*spec);
+        if (cap == 0) throw Error(QADC_ERR_CONFIG, "candidate heap capacity must be positive"); // heap.hpp:27-28
+        // check_scan_config (scan_scalar.hpp:23-27) and the width check (:38-39)
+        if (count != 0 && uint64_t(rows) * spec->g != spec->m)
+            throw Error(QADC_ERR_CONFIG, "scan: packed rows do not match the table count for this scheme");
+        if (width != spec->word_width) throw Error(QADC_ERR_CONFIG, "scan: table width does not match the packing word width");
+        // n_in may exceed cap: the reference pushes every seed through the bounded heap (selftest.hpp:104-109)
+        if (cap > QADC_MAX_R) throw Error(QADC_ERR_CONFIG, "scan_list: heap capacity exceeds QADC_MAX_R");
+        set_device(device);
+        qadc_index h;
+        h.device = device;
+        h.spec = *spec;
+        h.ds = make_dev_spec(*spec, spec->groups);
+        QADC_CUDA_CHECK(cudaDeviceGetAttribute(&h.num_sms, cudaDevAttrMultiProcessorCount, device));
+        QADC_CUDA_CHECK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
+        cudaStream_t st = h.stream;
+        const DevSpec& ds = h.ds;
+        h.count = count;
+        upload_list(&h, *spec, ds, packed, count, h.codes, h.count_padded, st);
+        const size_t wb = width / 8;
+        h.qlut.ensure(size_t(ds.E) * wb);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h.qlut.p, qlut, size_t(ds.E) * wb, cudaMemcpyHostToDevice, st));
+        DevBuf bias;
+        bias.ensure(4);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(bias.p, &acc_init, 4, cudaMemcpyHostToDevice, st));
+        h.counters.ensure(16);
+        // explicit ids: translate positions -> ids at the end (keys carry positions during the scan
+        // would break the (distance,id) order), so give the kernel the id array directly
+        if (ids && count) {
+            h.ids.ensure(size_t(count) * 4);
+            QADC_CUDA_CHECK(cudaMemcpyAsync(h.ids.p, ids, size_t(count) * 4, cudaMemcpyHostToDevice, st));
+        }
+        const ScanPlan plan = plan_for(&h);
+        // pre-seeded heap entries are just earlier candidates (heap.hpp:12-14: order-independent)
+        uint32_t buf_cap = std::max<uint32_t>(h.cand_cap, n_in + 16);
+        for (;;) {
+            h.sel.ensure(1, cap, buf_cap);
+            launch_init_select(h.sel.thr_key.as<uint64_t>(), h.sel.cand_count.as<uint32_t>(), h.sel.ntop.as<uint32_t>(),
+                               h.sel.overflow.as<uint32_t>(), 1, st);
+            if (n_in) {
+                std::vector<uint64_t> seed(n_in);
+                for (uint32_t i = 0; i < n_in; ++i) seed[i] = make_key(heap_in_dist[i], heap_in_id[i]);
+                QADC_CUDA_CHECK(cudaMemcpyAsync(h.sel.cand.p, seed.data(), size_t(n_in) * 8, cudaMemcpyHostToDevice, st));
+                QADC_CUDA_CHECK(cudaMemcpyAsync(h.sel.cand_count.p, &n_in, 4, cudaMemcpyHostToDevice, st));
+                launch_tighten(h.sel.top.as<uint64_t>(), h.sel.ntop.as<uint32_t>(), h.sel.kpad, h.sel.cand.as<uint64_t>(),
+                               h.sel.cand_count.as<uint32_t>(), buf_cap, h.sel.thr_key.as<uint64_t>(), 1, cap, st);
+                QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // seed vector goes out of scope
+            }
+            RowSet rs{h.qlut.p, nullptr, bias.as<uint32_t>()};
+            bool ok = true;
+            if (count) {
+                // same machinery as the flat search; explicit ids ride in ScanArgs::ids
+                h.sel.cap = buf_cap;
+                ok = [&] {
+                    const int grid = h.num_sms;
+                    const uint64_t s0 = std::min<uint64_t>(h.seg0, std::max<uint32_t>(buf_cap / 2, 256));
+                    const std::vector<uint64_t> bounds = segment_bounds(count, s0, h.seg_growth);
+                    for (size_t s = 0; s + 1 < bounds.size(); ++s) {
+                        std::vector<ScanJob> jobs;
+                        flat_segment_jobs(jobs, bounds[s], bounds[s + 1], 1, plan.tq, base_id, grid);
+                        h.jobs.ensure(jobs.size() * sizeof(ScanJob));
+                        QADC_CUDA_CHECK(cudaMemcpyAsync(h.jobs.p, jobs.data(), jobs.size() * sizeof(ScanJob), cudaMemcpyHostToDevice, st));
+                        ScanArgs a{};
+                        a.codes = h.codes.as<uint8_t>();
+                        a.ids = ids ? h.ids.as<uint32_t>() : nullptr;
+                        a.qlut = rs.qlut;
+                        a.row_bias = rs.row_bias;
+                        a.jobs = h.jobs.as<ScanJob>();
+                        a.n_jobs = uint32_t(jobs.size());
+                        a.thr_key = h.sel.thr_key.as<uint64_t>();
+                        a.cand = h.sel.cand.as<uint64_t>();
+                        a.cand_count = h.sel.cand_count.as<uint32_t>();
+                        a.cap = buf_cap;
+                        a.overflow = h.sel.overflow.as<uint32_t>();
+                        a.counters = h.counters.as<unsigned long long>();
+                        launch_scan(plan, ds, a, std::min<int>(grid, int(jobs.size())), st);
+                        launch_tighten(h.sel.top.as<uint64_t>(), h.sel.ntop.as<uint32_t>(), h.sel.kpad,
+                                       h.sel.cand.as<uint64_t>(), h.sel.cand_count.as<uint32_t>(), buf_cap,
+                                       h.sel.thr_key.as<uint64_t>(), 1, cap, st);
+                        QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // jobs vector goes out of scope
+                    }
+                    uint32_t ov = 0;
+                    QADC_CUDA_CHECK(cudaMemcpy(&ov, h.sel.overflow.p, 4, cudaMemcpyDeviceToHost));
+                    return ov == 0;
+                }();
+            }
+            if (ok) break;
+            if (uint64_t(buf_cap) >= count + n_in + 16) throw Error(QADC_ERR_CUDA, "internal: candidate overflow at full capacity");
+            buf_cap = uint32_t(std::min<uint64_t>(uint64_t(buf_cap) * 8, count + n_in + 16));
+        }
+        DevBuf keys, cnt;
+        keys.ensure(size_t(cap) * 8);
+        cnt.ensure(4);
+        launch_finalize(h.sel.top.as<uint64_t>(), h.sel.ntop.as<uint32_t>(), h.sel.kpad, 1, 1, cap, nullptr, 0, ds.qmax,
+                        nullptr, nullptr, cnt.as<uint32_t>(), keys.as<uint64_t>(), st);
+        std::vector<uint64_t> hk(cap);
+        uint32_t n = 0;
+        QADC_CUDA_CHECK(cudaMemcpyAsync(hk.data(), keys.p, size_t(cap) * 8, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaMemcpyAsync(&n, cnt.p, 4, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (uint32_t i = 0; i < n; ++i) {
+            out_dist[i] = uint32_t(hk[i] >> 32);
+            out_id[i] = uint32_t(hk[i]);
+        }
+        *n_out = n;
+    });
+}
+
+int qadc_encode(const qadc_spec* spec, const float* codebook, const float* vectors, uint64_t n, uint8_t* codes,
+                int device) {
+    return guarded([&] {
+        if (!spec || !codebook || (n && (!vectors || !codes))) throw Error(QADC_ERR_INPUT, "encode: null argument");
+        validate_spec(*spec);
+        set_device(device);
+        const DevSpec ds = make_dev_spec(*spec, spec->groups);
+        DevBuf cb, v, c;
+        cb.ensure(size_t(spec->cb_floats) * 4);
+        QADC_CUDA_CHECK(cudaMemcpy(cb.p, codebook, size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice));
+        const uint64_t batch = 1u << 20;
+        v.ensure(size_t(std::min(batch, std::max<uint64_t>(n, 1))) * spec->dims * 4);
+        c.ensure(size_t(std::min(batch, std::max<uint64_t>(n, 1))) * spec->m);
+        for (uint64_t i = 0; i < n; i += batch) {
+            const uint64_t nb = std::min(batch, n - i);
+            QADC_CUDA_CHECK(cudaMemcpy(v.p, vectors + i * spec->dims, size_t(nb) * spec->dims * 4, cudaMemcpyHostToDevice));
+            launch_encode(ds, cb.as<float>(), v.as<float>(), nb, c.as<uint8_t>(), nullptr);
+            QADC_CUDA_CHECK(cudaMemcpy(codes + i * spec->m, c.p, size_t(nb) * spec->m, cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+int qadc_get_stats(const qadc_index* h, qadc_stats* out) {
+    if (!h || !out) return QADC_ERR_INPUT;
+    *out = h->stats;
+    return QADC_OK;
+}
+
+int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
+    return guarded([&] {
+        if (!h || !name) throw Error(QADC_ERR_INPUT, "set_option: null argument");
+        const std::string n(name);
+        if (n == "cand_cap") h->cand_cap = uint32_t(std::max<int64_t>(value, 16));
+        else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384));
+        else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
+        else if (n == "force_variant") h->force_variant = int(value);
+        else throw Error(QADC_ERR_CONFIG, "set_option: unknown option " + n);
+    });
+}
+
+int qadc_ivf_open(const qadc_spec*, const float*, const float*, uint32_t, const uint8_t*, const uint64_t*,
+                  const uint64_t*, const uint64_t*, const uint32_t*, const uint8_t*, const uint64_t*, const uint64_t*,
+                  int, qadc_index**) {
+    g_error = "ivf: not built yet";
+    return QADC_ERR_CONFIG;
+}
+
+int qadc_ivf_probe_order(qadc_index*, const float*, uint32_t, uint32_t, uint32_t*) {
+    g_error = "ivf: not built yet";
+    return QADC_ERR_CONFIG;
+}
+
+} // extern "C"

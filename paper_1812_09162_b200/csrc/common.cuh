@@ -1,0 +1,140 @@
+// common.cuh -- internal declarations shared by the translation units of libqadc_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "qadc.h"
+
+namespace qadc {
+
+// ---- errors: C++ exceptions inside the library, mapped to status codes at the C ABI ----
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& msg) : std::runtime_error(msg), code(c) {}
+};
+
+#define QADC_CUDA_CHECK(expr)                                                                        \
+    do {                                                                                             \
+        cudaError_t _e = (expr);                                                                     \
+        if (_e != cudaSuccess)                                                                       \
+            throw ::qadc::Error(QADC_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+    } while (0)
+
+// ---- device-side view of a spec (kernel parameter, passed by value) ----
+struct DevSpec {
+    uint32_t dims, m, E, cb_floats;
+    uint32_t word_width; // 8 / 16
+    uint32_t qmax;       // 255 / 65535
+    uint32_t code_bytes; // rows * word_bytes
+    uint32_t code_stride; // bytes between consecutive codes in the device layout (multiple of 8)
+    uint8_t bits[QADC_MAX_SUBS];
+    uint8_t bitpos[QADC_MAX_SUBS]; // bit position of subquantizer j inside the little-endian code
+    uint32_t dim_off[QADC_MAX_SUBS];
+    uint32_t dim_alloc[QADC_MAX_SUBS];
+    uint32_t ent_off[QADC_MAX_SUBS];
+    uint32_t cb_off[QADC_MAX_SUBS];
+};
+
+DevSpec make_dev_spec(const qadc_spec& s, uint32_t rows);
+
+// 64-bit candidate key: (quantized distance << 32) | id.  Lexicographic (distance, id)
+// order of the reference's CandidateHeap (heap.hpp:21-23) == unsigned order of the key.
+__host__ __device__ inline uint64_t make_key(uint32_t dist, uint32_t id) { return (uint64_t(dist) << 32) | id; }
+static constexpr uint64_t KEY_INF = ~0ull;
+
+// ---- scan job: one (code range) x (tile of LUT rows) unit of work ----
+struct ScanJob {
+    uint64_t code_off; // first code (index into the device code array)
+    uint64_t ids_off;  // index of the first code's id in the ids array (explicit-id mode)
+    uint32_t n_codes;
+    uint32_t id_base;  // implicit-id mode: id of the first code
+    uint32_t row_begin; // first LUT row of the tile
+    uint32_t n_rows;    // rows in the tile (<= TQ of the variant)
+};
+
+// ---- scan kernel variants ----
+enum ScanVariant : uint32_t {
+    VAR_F16X8 = 0,   // u8 tables, fp16 entries in smem, 8 rows per lane (LDS.128), 256-row tile
+    VAR_F32X2 = 1,   // u16 tables, fp32 entries in smem, 2 rows per lane (LDS.64), 64-row tile
+    VAR_U16X1 = 2,   // any width, u16 entries in smem, 1 row per lane, 32-row tile, int32 accumulate
+    VAR_U8X1 = 3,    // any width, u8 (high-byte for u16 tables) conservative filter, 32-row tile
+    VAR_COUNT
+};
+
+struct ScanArgs {
+    const uint8_t* codes;      // device code array, code_stride bytes per code
+    const uint32_t* ids;       // explicit ids or nullptr
+    const void* qlut;          // [rows][E] at table width, reference table order
+    const uint32_t* row_query; // row -> query index (nullptr: identity)
+    const uint32_t* row_bias;  // row -> acc_init (nullptr: 0)
+    const ScanJob* jobs;
+    uint32_t n_jobs;
+    uint64_t* thr_key;         // [nq] current R-th smallest key (KEY_INF while fewer than R)
+    uint64_t* cand;            // [nq][cap]
+    uint32_t* cand_count;      // [nq]
+    uint32_t cap;
+    uint32_t* overflow;        // [nq] set to 1 when a candidate did not fit
+    unsigned long long* counters; // [0] exact-admitted candidates, [1] slow-path entries
+};
+
+struct ScanPlan {
+    ScanVariant variant;
+    uint32_t tq;         // rows per tile
+    uint32_t smem_bytes;
+    uint32_t threads;
+};
+
+// chooses the variant for a spec (throws config error if nothing fits shared memory)
+ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int threads);
+void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
+
+// ---- LUT / calibration / quantization (lut.cu) ----
+struct LutArgs {
+    const float* codebook;    // flat codebook on device
+    const float* queries;     // [nq][dims]
+    const float* sub;         // optional [nq][dims] vectors subtracted first (IVF residual), or nullptr
+    const uint8_t* calib_codes; // device layout, first codes of the list
+    uint32_t calib_count;     // number of valid calibration codes (<= t)
+    uint32_t nq, r, t;
+    float* luts;              // optional [nq][E]
+    void* qluts;              // [nq][E] at table width
+    float* calib;             // [nq][4] {d_min, d_max, delta, own_d_min}
+    float* map;               // [nq][2] {delta, d_min} used to unquantize
+    int* status;              // device int, set non-zero on calibration errors
+};
+void launch_flat_tables(const DevSpec& ds, const LutArgs& a, cudaStream_t stream);
+
+// ---- selection (select.cu) ----
+void launch_init_select(uint64_t* thr_key, uint32_t* cand_count, uint32_t* ntop, uint32_t* overflow, uint32_t nq,
+                        cudaStream_t stream);
+// fold the new candidates of every query into its running top-r and refresh thr_key
+void launch_tighten(uint64_t* top, uint32_t* ntop, uint32_t kpad, uint64_t* cand, uint32_t* cand_count, uint32_t cap,
+                    uint64_t* thr_key, uint32_t nq, uint32_t r, cudaStream_t stream);
+// sort each query's top list and emit ids / unquantized distances / counts / keys
+void launch_finalize(const uint64_t* lists, const uint32_t* counts_in, uint32_t list_len, uint32_t nlists,
+                     uint32_t nq, uint32_t r, const float* map, uint32_t flags, uint32_t qmax, uint32_t* out_ids,
+                     float* out_dists, uint32_t* out_counts, uint64_t* out_keys, cudaStream_t stream);
+
+// ---- dense head evaluation (seed.cu) ----
+void launch_seed_topk(const DevSpec& ds, const uint8_t* d_codes, uint32_t n_head, uint32_t id_base,
+                      const uint32_t* d_ids, const void* d_qlut, const uint32_t* d_row_bias, uint32_t nq, uint32_t r,
+                      uint64_t* top, uint32_t* ntop, uint32_t kpad, uint64_t* thr_key, cudaStream_t stream);
+
+// ---- layout (layout.cu) ----
+// reference PackedList bytes (device copy) -> linear device layout, padded with 0xFF codes up to n_padded
+void launch_relayout(const qadc_spec& s, const DevSpec& ds, const uint8_t* d_packed, uint64_t n, uint64_t n_padded,
+                     uint8_t* d_codes, cudaStream_t stream);
+void launch_unlayout(const DevSpec& ds, const uint8_t* d_codes, uint64_t first, uint64_t n, uint8_t* d_subcodes,
+                     cudaStream_t stream);
+void launch_adc_sums(const DevSpec& ds, const uint8_t* d_codes, const void* d_qlut, uint32_t acc_init,
+                     uint64_t first, uint64_t n, uint32_t* d_sums, cudaStream_t stream);
+void launch_encode(const DevSpec& ds, const float* d_codebook, const float* d_vectors, uint64_t n, uint8_t* d_codes,
+                   cudaStream_t stream);
+
+extern thread_local unsigned long long g_launches; // kernels launched by this thread's current call
+
+} // namespace qadc

@@ -1,0 +1,578 @@
+// scan.cu -- the ADC scan kernels (the hot path).
+//
+// Reference semantics (scan_scalar.hpp:34-64): for every occupied code, fold the m
+// quantized table entries selected by its subcodes with saturating adds at table
+// width, starting from min(acc_init, q_max), and push (sum, id) into the bounded heap.
+// The CPU kernels (scan_x86.hpp) put 16/32/64 CODES in the lanes of one register and
+// shuffle one query's tables.  On the GPU the batch dimension is the QUERY:
+//
+//   * a CTA keeps the quantized tables of a TILE of queries ("LUT rows") resident in
+//     shared memory, transposed to [entry][row] so that the 32 lanes of a warp, each
+//     owning 1..8 rows, read one conflict-free 64..512-byte line per lookup;
+//   * codes stream through a double-buffered shared-memory stage filled by bulk async
+//     copies (cp.async.bulk + mbarrier); a warp takes one whole code at a time with a
+//     broadcast load, so the code is read once per (warp, tile), not once per query;
+//   * sums are accumulated WITHOUT per-step saturation in a wider type and compared
+//     once: min(min(S,q)+x,q) == min(S+x,q) for unsigned terms.  u8
+//     tables accumulate as packed fp16 pairs (HADD2; integers are exact up to 2048 and
+//     every rounded value is far above any 8-bit threshold), u16 tables as fp32
+//     (exact below 2^24) or int32;
+//   * the accumulator starts at (bias - threshold - 1/2), so "sum <= threshold" is the
+//     sign bit: one OR over a lane's accumulators decides whether ANY of its rows
+//     admits the code;
+//   * the rare admitted (row, code) pair is re-evaluated exactly in integers against
+//     the reference-order table in global memory and appended to the query's candidate
+//     list iff its (distance, id) key beats the query's current R-th best key -- the
+//     CandidateHeap::push test (heap.hpp:46-47).  The in-loop test is only a filter
+//     (it never drops a pair the exact test would admit), so results are exact by
+//     construction whatever the filter's arithmetic.
+#include <cuda_fp16.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace qadc {
+
+// ------------------------------------------------------------------ helpers --
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// TMA 1-D bulk copy global -> shared, completion counted on an mbarrier (SASS: UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for<I + 1, N>(f);
+    }
+}
+
+// ----------------------------------------------------------------- geometry --
+
+// Compile-time geometry of a 64-bit-or-wider code: ROWS packed words of WW bits, each
+// holding the group pattern Ws... LSB-first (layout.hpp:30-36).
+template <int WW, int ROWS, int... Ws>
+struct GeomCT {
+    static constexpr bool RUNTIME = false;
+    static constexpr int G = sizeof...(Ws);
+    static constexpr int M = G * ROWS;
+    static constexpr int CODE_BYTES = ROWS * WW / 8;
+    static constexpr int STRIDE = (CODE_BYTES + 7) / 8 * 8;
+    static constexpr int CW = STRIDE / 4; // 32-bit words per code
+    __host__ __device__ static constexpr int width_at(int k) {
+        const int ws[] = {Ws...};
+        return ws[k];
+    }
+    __host__ __device__ static constexpr int bits(int j) { return width_at(j % G); }
+    __host__ __device__ static constexpr int bitpos(int j) {
+        int off = 0;
+        for (int k = 0; k < j % G; ++k) off += width_at(k);
+        return (j / G) * WW + off;
+    }
+    __host__ __device__ static constexpr int ent_off(int j) {
+        int e = 0;
+        for (int k = 0; k < j; ++k) e += 1 << bits(k);
+        return e;
+    }
+    static constexpr int E = ent_off(M);
+    static bool matches(const DevSpec& ds) {
+        if (int(ds.m) != M || int(ds.word_width) != WW || int(ds.code_stride) != STRIDE) return false;
+        for (int j = 0; j < M; ++j)
+            if (ds.bits[j] != bits(j) || ds.bitpos[j] != bitpos(j)) return false;
+        return true;
+    }
+};
+struct GeomRT {
+    static constexpr bool RUNTIME = true;
+    static constexpr int CW = 2, E = 0, M = 0, STRIDE = 8;
+    __host__ __device__ static constexpr int bits(int) { return 0; }
+    __host__ __device__ static constexpr int bitpos(int) { return 0; }
+    __host__ __device__ static constexpr int ent_off(int) { return 0; }
+};
+
+// ------------------------------------------------------------------ policies --
+// A policy fixes how table entries live in shared memory and how a lane accumulates.
+//   QPL    rows (queries) owned by one lane;   TQ = 32*QPL rows per tile
+//   ROWB   bytes of one [entry] line in shared memory = TQ * sizeof(entry)
+
+struct PolF16x8 { // u8 tables only
+    static constexpr int QPL = 8, TQ = 256, ROWB = 512, LOG_ROWB = 9, LANE_B = 16;
+    static constexpr bool EXACT_FILTER = true;
+    using Entry = __half;
+    struct Acc {
+        __half2 h[4];
+    };
+    __device__ static Entry convert(uint32_t v, uint32_t) { return __uint2half_rn(v); } // exact: v <= 255
+    __device__ static void init(Acc& a, const float* t) { // t[s] = bias - thr - 0.5 (or +-BIG)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a.h[k] = __floats2half2_rn(t[2 * k], t[2 * k + 1]);
+    }
+    __device__ static void add(Acc& a, const char* p) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        a.h[0] = __hadd2(a.h[0], *reinterpret_cast<const __half2*>(&v.x));
+        a.h[1] = __hadd2(a.h[1], *reinterpret_cast<const __half2*>(&v.y));
+        a.h[2] = __hadd2(a.h[2], *reinterpret_cast<const __half2*>(&v.z));
+        a.h[3] = __hadd2(a.h[3], *reinterpret_cast<const __half2*>(&v.w));
+    }
+    __device__ static bool any(const Acc& a) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(a.h);
+        return ((u[0] | u[1] | u[2] | u[3]) & 0x80008000u) != 0;
+    }
+    __device__ static bool hit(const Acc& a, int s) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(a.h);
+        return (u[s >> 1] >> ((s & 1) * 16 + 15)) & 1u;
+    }
+    // exact accumulator value of slot s as fp32 (only meaningful when the slot admits, i.e. |v| < 1024)
+    __device__ static float value(const Acc& a, int s) {
+        return (s & 1) ? __high2float(a.h[s >> 1]) : __low2float(a.h[s >> 1]);
+    }
+    static constexpr float BIG = 30000.0f, HALF = 0.5f;
+};
+
+struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
+    static constexpr int QPL = 2, TQ = 64, ROWB = 256, LOG_ROWB = 8, LANE_B = 8;
+    static constexpr bool EXACT_FILTER = true;
+    using Entry = float;
+    struct Acc {
+        float f[2];
+    };
+    __device__ static Entry convert(uint32_t v, uint32_t) { return float(v); }
+    __device__ static void init(Acc& a, const float* t) {
+        a.f[0] = t[0];
+        a.f[1] = t[1];
+    }
+    __device__ static void add(Acc& a, const char* p) {
+        const float2 v = *reinterpret_cast<const float2*>(p);
+        a.f[0] = __fadd_rn(a.f[0], v.x);
+        a.f[1] = __fadd_rn(a.f[1], v.y);
+    }
+    __device__ static bool any(const Acc& a) { return (__float_as_uint(a.f[0]) | __float_as_uint(a.f[1])) >> 31; }
+    __device__ static bool hit(const Acc& a, int s) { return __float_as_uint(a.f[s]) >> 31; }
+    __device__ static float value(const Acc& a, int s) { return a.f[s]; }
+    static constexpr float BIG = 1.0e9f, HALF = 0.5f;
+};
+
+struct PolU16x1 { // any width, u16 entries, int32 accumulate
+    static constexpr int QPL = 1, TQ = 32, ROWB = 64, LOG_ROWB = 6, LANE_B = 2;
+    static constexpr bool EXACT_FILTER = true;
+    using Entry = unsigned short;
+    struct Acc {
+        int v;
+    };
+    __device__ static Entry convert(uint32_t v, uint32_t) { return (unsigned short)v; }
+    __device__ static void init(Acc& a, const float* t) { a.v = int(floorf(t[0])); } // bias - thr - 1
+    __device__ static void add(Acc& a, const char* p) { a.v += int(*reinterpret_cast<const unsigned short*>(p)); }
+    __device__ static bool any(const Acc& a) { return a.v < 0; }
+    __device__ static bool hit(const Acc& a, int) { return a.v < 0; }
+    __device__ static float value(const Acc& a, int) { return float(a.v) + 0.5f; } // init was floor(t) = t - 1/2
+    static constexpr float BIG = 1.0e9f, HALF = 0.5f;
+};
+
+struct PolU8x1 { // any width; u16 tables keep only the HIGH byte: a conservative filter
+    static constexpr int QPL = 1, TQ = 32, ROWB = 32, LOG_ROWB = 5, LANE_B = 1;
+    static constexpr bool EXACT_FILTER = false;
+    using Entry = unsigned char;
+    struct Acc {
+        int v;
+    };
+    __device__ static Entry convert(uint32_t v, uint32_t width) { return (unsigned char)(width == 16 ? v >> 8 : v); }
+    __device__ static void init(Acc& a, const float* t) { a.v = int(floorf(t[0])); }
+    __device__ static void add(Acc& a, const char* p) { a.v += int(*reinterpret_cast<const unsigned char*>(p)); }
+    __device__ static bool any(const Acc& a) { return a.v < 0; }
+    __device__ static bool hit(const Acc& a, int) { return a.v < 0; }
+    __device__ static float value(const Acc& a, int) { return float(a.v) + 0.5f; }
+    // floor(bias/256) + sum floor(e/256) <= floor(thr/256) is necessary for bias + sum e <= thr
+    static constexpr float BIG = 1.0e9f, HALF = 0.5f;
+};
+
+static constexpr int SCAN_THREADS = 512;
+static constexpr int SCAN_WARPS = SCAN_THREADS / 32;
+static constexpr int STAGE_BYTES = 8192; // one code stage buffer
+static constexpr int NSTAGE = 2;
+
+// --------------------------------------------------------- exact admission --
+
+__device__ __forceinline__ uint32_t rt_sub_index(const DevSpec* ds, const uint8_t* code, uint32_t j) {
+    const uint32_t bp = ds->bitpos[j];
+    const uint32_t w = reinterpret_cast<const uint32_t*>(code)[bp >> 5];
+    return (w >> (bp & 31u)) & ((1u << ds->bits[j]) - 1u);
+}
+
+// The CandidateHeap::push test (heap.hpp:40-51) for one (row, code): exact saturating
+// sum (scan_scalar.hpp:52-58) from the reference-order table, then key < worst key.
+__device__ __noinline__ void exact_admit(const DevSpec* ds, const ScanArgs* a, const uint8_t* code, uint32_t row,
+                                         uint32_t id) {
+    uint32_t acc = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;
+    const size_t base = size_t(row) * ds->E;
+    if (ds->word_width == 8) {
+        const uint8_t* t = reinterpret_cast<const uint8_t*>(a->qlut) + base;
+        for (uint32_t j = 0; j < ds->m; ++j) acc += t[ds->ent_off[j] + rt_sub_index(ds, code, j)];
+    } else {
+        const uint16_t* t = reinterpret_cast<const uint16_t*>(a->qlut) + base;
+        for (uint32_t j = 0; j < ds->m; ++j) acc += t[ds->ent_off[j] + rt_sub_index(ds, code, j)];
+    }
+    acc = min(acc, ds->qmax); // == the chain of saturating adds, all terms being unsigned
+    const uint32_t q = a->row_query ? a->row_query[row] : row;
+    const uint64_t key = make_key(acc, id);
+    if (key < a->thr_key[q]) {
+        const uint32_t slot = atomicAdd(&a->cand_count[q], 1u);
+        if (slot < a->cap) a->cand[size_t(q) * a->cap + slot] = key;
+        else a->overflow[q] = 1u;
+    }
+}
+
+// Admission of one flagged (row, code).  When the in-loop filter is exact and the row has
+// a finite, unsaturated threshold, the accumulator itself is exact (it is < 0, far
+// inside the exactly representable range): bias + sum = acc + thr + 1/2, no re-evaluation.
+// Otherwise (no threshold yet, saturated threshold, or the high-byte filter) fall back to
+// the integer re-evaluation above.
+template <class P>
+__device__ __forceinline__ void admit(const DevSpec* ds, const ScanArgs* a, const typename P::Acc& acc, int s,
+                                      const uint8_t* code, uint32_t row, uint32_t id) {
+    const uint32_t q = a->row_query ? a->row_query[row] : row;
+    const uint64_t tk = a->thr_key[q];
+    const uint32_t thr = uint32_t(tk >> 32);
+    if (!P::EXACT_FILTER || tk == KEY_INF || thr >= ds->qmax) {
+        exact_admit(ds, a, code, row, id);
+        return;
+    }
+    const uint32_t d = uint32_t(P::value(acc, s) + float(thr) + 0.5f);
+    const uint64_t key = make_key(d, id);
+    if (key < tk) {
+        const uint32_t slot = atomicAdd(&a->cand_count[q], 1u);
+        if (slot < a->cap) a->cand[size_t(q) * a->cap + slot] = key;
+        else a->overflow[q] = 1u;
+    }
+}
+
+// ------------------------------------------------------------------- kernel --
+
+template <class P, class G>
+__global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param, ScanArgs args_param) {
+    extern __shared__ __align__(1024) char smem[];
+    // [0, E*ROWB) LUT tile | stage buffers | mbarriers
+    __shared__ DevSpec s_ds;
+    __shared__ ScanArgs s_args;
+    __shared__ __align__(8) uint64_t s_bar[NSTAGE];
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        s_ds = ds_param;
+        s_args = args_param;
+        for (int i = 0; i < NSTAGE; ++i) mbar_init(&s_bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const DevSpec* ds = &s_ds;
+    const ScanArgs* a = &s_args;
+
+    const uint32_t E = G::RUNTIME ? ds->E : uint32_t(G::E);
+    const uint32_t stride = ds->code_stride;
+    char* tile = smem;
+    char* stage = smem + size_t(E) * P::ROWB;
+    const uint32_t stage_codes = STAGE_BYTES / stride;
+    uint32_t bar_phase = 0; // bit b = parity to wait for on barrier b
+
+    // contiguous slice of the job list for this CTA
+    const uint32_t j_begin = uint32_t(uint64_t(a->n_jobs) * blockIdx.x / gridDim.x);
+    const uint32_t j_end = uint32_t(uint64_t(a->n_jobs) * (blockIdx.x + 1) / gridDim.x);
+
+    uint32_t cur_row_begin = 0xFFFFFFFFu, cur_n_rows = 0;
+    typename P::Acc acc0;
+    {
+        float t[P::QPL];
+#pragma unroll
+        for (int s = 0; s < P::QPL; ++s) t[s] = P::BIG;
+        P::init(acc0, t);
+    }
+
+    for (uint32_t ji = j_begin; ji < j_end; ++ji) {
+        const ScanJob job = a->jobs[ji];
+        if (job.n_codes == 0 || job.n_rows == 0) continue;
+
+        // ---- (re)load the LUT tile when the row range changes ----
+        if (job.row_begin != cur_row_begin || job.n_rows != cur_n_rows) {
+            __syncthreads(); // everyone is done with the previous tile
+            cur_row_begin = job.row_begin;
+            cur_n_rows = job.n_rows;
+            const uint32_t wbytes = ds->word_width / 8;
+            const size_t row_bytes = size_t(E) * wbytes;
+            typename P::Entry* te = reinterpret_cast<typename P::Entry*>(tile);
+            if ((row_bytes & 15u) == 0 && (reinterpret_cast<size_t>(a->qlut) & 15u) == 0) {
+                // lane = row inside a 32-row block; 16-byte global loads along the entry axis;
+                // shared-memory stores are lane-contiguous along the row axis (conflict-free)
+                const uint32_t ent_per_vec = 16 / wbytes;
+                const uint32_t n_vec = E / ent_per_vec;
+                const uint32_t n_rblk = P::TQ / 32;
+                for (uint32_t u = warp; u < n_vec * n_rblk; u += SCAN_WARPS) {
+                    const uint32_t rb = u % n_rblk, vi = u / n_rblk;
+                    const uint32_t r = rb * 32 + lane;
+                    uint4 v = make_uint4(0, 0, 0, 0);
+                    if (r < job.n_rows)
+                        v = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a->qlut) +
+                                                            size_t(job.row_begin + r) * row_bytes + size_t(vi) * 16);
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (uint32_t k = 0; k < 16; ++k) {
+                        if (wbytes == 2 && k >= 8) break;
+                        const uint32_t val = wbytes == 1 ? (w[k >> 2] >> ((k & 3) * 8)) & 0xFFu
+                                                         : (w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+                        te[size_t(vi * ent_per_vec + k) * P::TQ + r] = P::convert(val, ds->word_width);
+                    }
+                }
+            } else {
+                for (uint32_t u = tid; u < E * P::TQ; u += SCAN_THREADS) {
+                    const uint32_t r = u % P::TQ, e = u / P::TQ;
+                    uint32_t val = 0;
+                    if (r < job.n_rows) {
+                        const size_t gi = size_t(job.row_begin + r) * E + e;
+                        val = wbytes == 1 ? uint32_t(reinterpret_cast<const uint8_t*>(a->qlut)[gi])
+                                          : uint32_t(reinterpret_cast<const uint16_t*>(a->qlut)[gi]);
+                    }
+                    te[size_t(e) * P::TQ + r] = P::convert(val, ds->word_width);
+                }
+            }
+            // per-lane accumulator start: bias - threshold - 1/2 (sign bit <=> admitted)
+            float t[P::QPL];
+#pragma unroll
+            for (int s = 0; s < P::QPL; ++s) {
+                const uint32_t r = lane * P::QPL + s;
+                t[s] = P::BIG; // rows past the tile never admit
+                if (r < job.n_rows) {
+                    const uint32_t row = job.row_begin + r;
+                    const uint32_t q = a->row_query ? a->row_query[row] : row;
+                    const uint64_t tk = a->thr_key[q];
+                    uint32_t thr = uint32_t(tk >> 32);
+                    uint32_t bias = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;
+                    if (tk == KEY_INF || thr >= ds->qmax) t[s] = -P::BIG; // heap not full / worst saturated: admit all
+                    else {
+                        if (!P::EXACT_FILTER && ds->word_width == 16) {
+                            thr >>= 8;
+                            bias >>= 8;
+                        }
+                        t[s] = float(bias) - float(thr) - P::HALF;
+                    }
+                }
+            }
+            P::init(acc0, t);
+            __syncthreads();
+        }
+
+        // ---- stream the job's codes through the stage buffers ----
+        const uint8_t* gcodes = a->codes + job.code_off * stride;
+        const uint32_t n_sub = (job.n_codes + stage_codes - 1) / stage_codes;
+        auto issue = [&](uint32_t sub) {
+            const uint32_t first = sub * stage_codes;
+            const uint32_t cnt = min(stage_codes, job.n_codes - first);
+            const uint32_t bytes = (cnt * stride + 15u) & ~15u;
+            const uint32_t b = sub % NSTAGE;
+            mbar_expect_tx(&s_bar[b], bytes);
+            bulk_g2s(stage + size_t(b) * STAGE_BYTES, gcodes + size_t(first) * stride, bytes, &s_bar[b]);
+        };
+        if (tid == 0) {
+            issue(0);
+            if (n_sub > 1) issue(1);
+        }
+        for (uint32_t sub = 0; sub < n_sub; ++sub) {
+            const uint32_t b = sub % NSTAGE;
+            mbar_wait(&s_bar[b], (bar_phase >> b) & 1u);
+            bar_phase ^= 1u << b;
+            const uint32_t first = sub * stage_codes;
+            const uint32_t cnt = min(stage_codes, job.n_codes - first);
+            const char* sb = stage + size_t(b) * STAGE_BYTES;
+            const uint32_t lane_off = lane * P::LANE_B;
+
+            if constexpr (!G::RUNTIME) {
+                constexpr int CIF = 2; // codes in flight per warp
+                for (uint32_t i0 = warp; i0 < cnt; i0 += SCAN_WARPS * CIF) {
+                    uint32_t cw[CIF][G::CW];
+                    typename P::Acc acc[CIF];
+#pragma unroll
+                    for (int c = 0; c < CIF; ++c) {
+                        const uint32_t i = min(i0 + c * SCAN_WARPS, cnt - 1); // clamp: duplicates are ignored below
+                        const uint32_t* src = reinterpret_cast<const uint32_t*>(sb + size_t(i) * G::STRIDE);
+                        if constexpr (G::CW == 2) {
+                            const uint2 v = *reinterpret_cast<const uint2*>(src);
+                            cw[c][0] = v.x;
+                            cw[c][1] = v.y;
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < G::CW; ++k) cw[c][k] = src[k];
+                        }
+                        acc[c] = acc0;
+                    }
+                    static_for<0, G::M>([&](auto J) {
+                        constexpr int j = decltype(J)::value;
+                        constexpr int bp = G::bitpos(j), nb = G::bits(j);
+                        constexpr int word = bp >> 5, sh = (bp & 31) - P::LOG_ROWB;
+                        constexpr uint32_t mask = ((1u << nb) - 1u) << P::LOG_ROWB;
+                        constexpr uint32_t imm = uint32_t(G::ent_off(j)) * P::ROWB;
+#pragma unroll
+                        for (int c = 0; c < CIF; ++c) {
+                            const uint32_t x = sh >= 0 ? (cw[c][word] >> (sh >= 0 ? sh : 0)) : (cw[c][word] << (sh < 0 ? -sh : 0));
+                            const uint32_t off = (x & mask) | lane_off;
+                            P::add(acc[c], tile + imm + off);
+                        }
+                    });
+#pragma unroll
+                    for (int c = 0; c < CIF; ++c) {
+                        const uint32_t i = i0 + c * SCAN_WARPS;
+                        if (i < cnt && P::any(acc[c])) {
+                            const uint32_t pos = first + i;
+                            const uint32_t id = a->ids ? a->ids[job.ids_off + pos] : job.id_base + pos;
+#pragma unroll
+                            for (int s = 0; s < P::QPL; ++s)
+                                if (P::hit(acc[c], s))
+                                    admit<P>(ds, a, acc[c], s, reinterpret_cast<const uint8_t*>(sb + size_t(i) * G::STRIDE),
+                                             job.row_begin + lane * P::QPL + s, id);
+                        }
+                    }
+                }
+            } else {
+                // runtime geometry: any m / widths / code size that fits; one code per warp step
+                for (uint32_t i = warp; i < cnt; i += SCAN_WARPS) {
+                    const uint8_t* code = reinterpret_cast<const uint8_t*>(sb + size_t(i) * stride);
+                    typename P::Acc acc = acc0;
+                    for (uint32_t j = 0; j < ds->m; ++j) {
+                        const uint32_t idx = rt_sub_index(ds, code, j);
+                        P::add(acc, tile + size_t(ds->ent_off[j] + idx) * P::ROWB + lane_off);
+                    }
+                    if (P::any(acc)) {
+                        const uint32_t pos = first + i;
+                        const uint32_t id = a->ids ? a->ids[job.ids_off + pos] : job.id_base + pos;
+#pragma unroll
+                        for (int s = 0; s < P::QPL; ++s)
+                            if (P::hit(acc, s)) admit<P>(ds, a, acc, s, code, job.row_begin + lane * P::QPL + s, id);
+                    }
+                }
+            }
+            __syncthreads(); // stage buffer b is free again
+            if (tid == 0 && sub + NSTAGE < n_sub) issue(sub + NSTAGE);
+        }
+    }
+}
+
+// ----------------------------------------------------------------- dispatch --
+
+using G44 = GeomCT<8, 8, 4, 4>;       // 16x{4,4}
+using G655 = GeomCT<16, 4, 6, 5, 5>;  // 12x{6,5,5}
+using G664 = GeomCT<16, 4, 6, 6, 4>;  // 12x{6,6,4}
+using G555 = GeomCT<16, 4, 5, 5, 5>;  // 12x{5,5,5}
+using G88 = GeomCT<16, 4, 8, 8>;      // 8x{8,8}
+using G8 = GeomCT<8, 8, 8>;           // 8x{8}
+
+const char* variant_name(uint32_t v) {
+    switch (v) {
+    case VAR_F16X8: return "f16x8 (u8 tables as fp16 pairs, 256-query tile, LDS.128)";
+    case VAR_F32X2: return "f32x2 (u16 tables as fp32, 64-query tile, LDS.64)";
+    case VAR_U16X1: return "u16x1 (u16 entries, 32-query tile, int32 accumulate)";
+    case VAR_U8X1: return "u8x1 (high-byte filter, 32-query tile)";
+    }
+    return "?";
+}
+
+template <class P>
+static uint32_t smem_need(uint32_t E) {
+    return E * P::ROWB + NSTAGE * STAGE_BYTES;
+}
+
+ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int) {
+    int max_smem = 0;
+    QADC_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    // static shared (DevSpec + ScanArgs + barriers) comes out of the same budget
+    const uint32_t budget = uint32_t(max_smem) - uint32_t(sizeof(DevSpec) + sizeof(ScanArgs) + 256);
+    if (ds.code_stride > 32) throw Error(QADC_ERR_CONFIG, "scan: codes wider than 256 bits are not supported");
+    ScanPlan p{};
+    p.threads = SCAN_THREADS;
+    auto fits = [&](uint32_t need) { return need <= budget; };
+    auto set = [&](ScanVariant v, uint32_t tq, uint32_t need) {
+        p.variant = v;
+        p.tq = tq;
+        p.smem_bytes = need;
+    };
+    const bool u8 = ds.word_width == 8;
+    if (force_variant >= 0) {
+        switch (force_variant) {
+        case VAR_F16X8:
+            if (!u8) throw Error(QADC_ERR_CONFIG, "scan: f16x8 needs 8-bit tables");
+            set(VAR_F16X8, PolF16x8::TQ, smem_need<PolF16x8>(ds.E));
+            break;
+        case VAR_F32X2: set(VAR_F32X2, PolF32x2::TQ, smem_need<PolF32x2>(ds.E)); break;
+        case VAR_U16X1: set(VAR_U16X1, PolU16x1::TQ, smem_need<PolU16x1>(ds.E)); break;
+        case VAR_U8X1: set(VAR_U8X1, PolU8x1::TQ, smem_need<PolU8x1>(ds.E)); break;
+        default: throw Error(QADC_ERR_CONFIG, "scan: unknown forced variant");
+        }
+        if (!fits(p.smem_bytes)) throw Error(QADC_ERR_CONFIG, "scan: forced variant does not fit shared memory");
+        return p;
+    }
+    if (u8 && fits(smem_need<PolF16x8>(ds.E))) set(VAR_F16X8, PolF16x8::TQ, smem_need<PolF16x8>(ds.E));
+    else if (fits(smem_need<PolF32x2>(ds.E))) set(VAR_F32X2, PolF32x2::TQ, smem_need<PolF32x2>(ds.E));
+    else if (fits(smem_need<PolU16x1>(ds.E))) set(VAR_U16X1, PolU16x1::TQ, smem_need<PolU16x1>(ds.E));
+    else if (fits(smem_need<PolU8x1>(ds.E))) set(VAR_U8X1, PolU8x1::TQ, smem_need<PolU8x1>(ds.E));
+    else
+        throw Error(QADC_ERR_CONFIG, "scan: the quantized tables of this spec (" + std::to_string(ds.E) +
+                                         " entries) do not fit shared memory; no CPU fallback exists");
+    return p;
+}
+
+template <class P, class G>
+static void launch_one(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_kernel<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(plan.smem_bytes)));
+    scan_kernel<P, G><<<grid, SCAN_THREADS, plan.smem_bytes, stream>>>(ds, args);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+// Compile-time geometries are instantiated only for the (policy, shape) pairs the planner
+// can actually pick for the named 64-bit specs; everything else runs the runtime geometry.
+void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
+    if (args.n_jobs == 0 || grid <= 0) return;
+    switch (plan.variant) {
+    case VAR_F16X8:
+        if (G44::matches(ds)) return launch_one<PolF16x8, G44>(plan, ds, args, grid, stream);
+        return launch_one<PolF16x8, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_F32X2:
+        if (G655::matches(ds)) return launch_one<PolF32x2, G655>(plan, ds, args, grid, stream);
+        if (G664::matches(ds)) return launch_one<PolF32x2, G664>(plan, ds, args, grid, stream);
+        if (G555::matches(ds)) return launch_one<PolF32x2, G555>(plan, ds, args, grid, stream);
+        if (G44::matches(ds)) return launch_one<PolF32x2, G44>(plan, ds, args, grid, stream);
+        return launch_one<PolF32x2, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_U16X1:
+        if (G88::matches(ds)) return launch_one<PolU16x1, G88>(plan, ds, args, grid, stream);
+        if (G8::matches(ds)) return launch_one<PolU16x1, G8>(plan, ds, args, grid, stream);
+        return launch_one<PolU16x1, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_U8X1: return launch_one<PolU8x1, GeomRT>(plan, ds, args, grid, stream);
+    default: throw Error(QADC_ERR_CONFIG, "scan: bad variant");
+    }
+}
+
+} // namespace qadc

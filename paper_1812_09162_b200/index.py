@@ -1,0 +1,284 @@
+"""Host-side mirror of the reference's search interface over the C ABI.
+
+Names and argument meaning follow the reference (``pqscan``): ``allocate_dims`` /
+``PqSpec`` (pqspec.hpp), ``SearchParams`` / ``SearchResult`` / ``FlatIndex`` / ``IvfIndex``
+(index.hpp) and the ``QuantizedScanFn`` plugin point (simd/kernels.hpp:49-50).  All
+computation happens in libqadc_b200.so's CUDA kernels; these classes only marshal
+numpy / torch buffers.  Errors raise :class:`QadcError` whose ``kind`` is the reference's
+exception class name (input / config / calibration / ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import QadcError, QadcSearchParams, QadcSpec, QadcStats, check, lib
+
+KERNEL_FAMILY = "b200-smem-lut"  # reported in SearchResult.kernel (the reference reports its SIMD family)
+
+
+def _p(a, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype)) if a is not None else None
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def allocate_dims(total_dims: int, spec_string: str) -> QadcSpec:
+    """parse_spec_string + allocate_dims + PackingScheme::for_spec (pqspec.hpp:24-55, 119-171)."""
+    s = QadcSpec()
+    check(lib().qadc_spec_parse(C.c_uint32(total_dims), spec_string.encode(), C.byref(s)))
+    return s
+
+
+def packed_bytes(spec: QadcSpec, n: int) -> int:
+    return int(lib().qadc_packed_bytes(C.byref(spec), C.c_uint64(n)))
+
+
+@dataclass
+class SearchParams:
+    """index.hpp:20-32.  ``fma_unquantize`` reproduces the reference's default -march=native build,
+    which contracts ``q*delta + d_min`` into one FMA; off matches the pinned (-ffp-contract=off) oracle."""
+    probes: int = 1
+    r: int = 100
+    t: int = 400
+    fma_unquantize: bool = False
+
+    def c(self) -> QadcSearchParams:
+        for name in ("probes", "r", "t"):
+            v = getattr(self, name)
+            if v < 0 or v > 0xFFFFFFFF:
+                raise QadcError(5, f"search: {name} out of range")
+        return QadcSearchParams(self.probes, self.r, self.t, 1 if self.fma_unquantize else 0)
+
+
+@dataclass
+class SearchResult:
+    """index.hpp:34-39 for a batch: row q holds ``counts[q]`` valid entries, ascending (distance, id)."""
+    ids: np.ndarray
+    dists: np.ndarray
+    counts: np.ndarray
+    kernel: str = KERNEL_FAMILY
+    scalar_fallback: bool = False
+
+    def query(self, q: int):
+        n = int(self.counts[q])
+        return self.ids[q, :n], self.dists[q, :n]
+
+
+class _Index:
+    def __init__(self):
+        self._h = C.c_void_p()
+        self.spec: QadcSpec | None = None
+        self.device = 0
+
+    def close(self):
+        if self._h:
+            lib().qadc_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- search ---------------------------------------------------------------
+    def search(self, queries, params: SearchParams | None = None) -> SearchResult:
+        """FlatIndex::search / IvfIndex::search (index.hpp:110, 276) for a batch of host queries."""
+        params = params or SearchParams()
+        q = _f32(queries)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        if q.ndim != 2 or q.shape[1] != self.spec.dims:
+            raise QadcError(5, "search: query has wrong dimension")  # index.hpp:112
+        nq, r = q.shape[0], max(int(params.r), 1)
+        ids = np.empty((nq, r), dtype=np.uint32)
+        dists = np.empty((nq, r), dtype=np.float32)
+        counts = np.zeros(nq, dtype=np.uint32)
+        cp = params.c()
+        check(lib().qadc_search_batch(self._h, _p(q, C.c_float), C.c_uint32(nq), C.byref(cp), _p(ids, C.c_uint32),
+                                      _p(dists, C.c_float), _p(counts, C.c_uint32)))
+        return SearchResult(ids, dists, counts)
+
+    def search_device(self, d_queries, params: SearchParams, d_ids, d_dists, d_counts, d_keys=None, d_map=None,
+                      stream=None):
+        """Device-buffer variant: arguments are torch CUDA tensors (float32 [nq,dims]; uint32-as-int32 / float32
+        [nq,r]; int32 [nq]; optional int64 [nq,r] keys and float32 [nq,2] map).  Runs on ``stream`` (an int
+        cudaStream_t, e.g. ``torch.cuda.current_stream().cuda_stream``)."""
+        nq = int(d_queries.shape[0])
+        if nq and int(d_queries.shape[1]) != self.spec.dims:
+            raise QadcError(5, "search: query has wrong dimension")
+        cp = params.c()
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        check(lib().qadc_search_batch_device(self._h, ptr(d_queries), C.c_uint32(nq), C.byref(cp), ptr(d_ids),
+                                             ptr(d_dists), ptr(d_counts), ptr(d_keys), ptr(d_map),
+                                             C.c_void_p(stream or 0)))
+
+    def stats(self) -> QadcStats:
+        st = QadcStats()
+        check(lib().qadc_get_stats(self._h, C.byref(st)))
+        return st
+
+    def set_option(self, name: str, value: int):
+        check(lib().qadc_set_option(self._h, name.encode(), C.c_int64(value)))
+
+
+class FlatIndex(_Index):
+    """FlatIndex (index.hpp:73-157): exhaustive search over one packed list.
+
+    ``packed`` is the reference's PackedList byte stream (layout.hpp:135-160) for ``count`` codes.
+    For a database shard pass ``base_id`` (id of the shard's first code) and ``calib_packed`` /
+    ``calib_count`` (the PackedList of the first codes of the WHOLE list) so that every shard
+    derives the same quantization map (index.hpp:124-129)."""
+
+    def __init__(self, spec: QadcSpec, codebook, packed, count: int, base_id: int = 0, calib_packed=None,
+                 calib_count: int = 0, device: int = 0):
+        super().__init__()
+        self.spec = spec
+        self.device = device
+        self.count = int(count)
+        cb = _f32(codebook).reshape(-1)
+        if cb.size != spec.cb_floats:
+            raise QadcError(5, "codebook: table count does not match spec")  # codebook.hpp:40
+        pk = np.ascontiguousarray(packed, dtype=np.uint8).reshape(-1)
+        if pk.size < packed_bytes(spec, count):
+            raise QadcError(5, "packed list is shorter than its code count requires")
+        cpk = None
+        if calib_packed is not None:
+            cpk = np.ascontiguousarray(calib_packed, dtype=np.uint8).reshape(-1)
+            if cpk.size < packed_bytes(spec, calib_count):
+                raise QadcError(5, "calibration list is shorter than its code count requires")
+        check(lib().qadc_flat_open(C.byref(spec), _p(cb, C.c_float), _p(pk, C.c_uint8), C.c_uint64(count),
+                                   C.c_uint32(base_id), _p(cpk, C.c_uint8), C.c_uint64(calib_count if cpk is not None else 0),
+                                   C.c_int(device), C.byref(self._h)))
+
+    def size(self) -> int:
+        return self.count
+
+    # -- parity / debug entry points -----------------------------------------------
+    def tables(self, queries, params: SearchParams | None = None):
+        """(float LUTs, quantized LUTs, calib{d_min,d_max,delta,own_d_min}) as the search derives them."""
+        params = params or SearchParams()
+        q = _f32(queries).reshape(-1, self.spec.dims)
+        nq, E = q.shape[0], self.spec.total_entries
+        luts = np.empty((nq, E), dtype=np.float32)
+        qluts = np.empty((nq, E), dtype=np.uint8 if self.spec.word_width == 8 else np.uint16)
+        calib = np.empty((nq, 4), dtype=np.float32)
+        cp = params.c()
+        check(lib().qadc_flat_tables(self._h, _p(q, C.c_float), C.c_uint32(nq), C.byref(cp), _p(luts, C.c_float),
+                                     qluts.ctypes.data_as(C.c_void_p), _p(calib, C.c_float)))
+        return luts, qluts, calib
+
+    def adc_sums(self, qlut, first: int, n: int, acc_init: int = 0, width: int | None = None) -> np.ndarray:
+        width = self.spec.word_width if width is None else width
+        q = np.ascontiguousarray(qlut, dtype=np.uint8 if width == 8 else np.uint16)
+        out = np.empty(n, dtype=np.uint32)
+        check(lib().qadc_flat_adc_sums(self._h, q.ctypes.data_as(C.c_void_p), C.c_uint32(width), C.c_uint32(acc_init),
+                                       C.c_uint64(first), C.c_uint64(n), _p(out, C.c_uint32)))
+        return out
+
+    def download_codes(self, first: int, n: int) -> np.ndarray:
+        out = np.empty((n, self.spec.m), dtype=np.uint8)
+        check(lib().qadc_flat_download_codes(self._h, C.c_uint64(first), C.c_uint64(n), _p(out, C.c_uint8)))
+        return out
+
+
+class IvfIndex(_Index):
+    """IvfIndex (index.hpp:166-177): coarse partition + per-cell packed lists of residual codes."""
+
+    def __init__(self, spec: QadcSpec, codebook, coarse, packed, list_byte_off, list_id_off, list_count, ids,
+                 device: int = 0):
+        super().__init__()
+        self.spec = spec
+        self.device = device
+        cb = _f32(codebook).reshape(-1)
+        if cb.size != spec.cb_floats:
+            raise QadcError(5, "codebook: table count does not match spec")
+        co = _f32(coarse).reshape(-1, spec.dims)
+        self.k_cells = co.shape[0]
+        pk = np.ascontiguousarray(packed, dtype=np.uint8).reshape(-1)
+        lbo = np.ascontiguousarray(list_byte_off, dtype=np.uint64)
+        lio = np.ascontiguousarray(list_id_off, dtype=np.uint64)
+        lc = np.ascontiguousarray(list_count, dtype=np.uint64)
+        idv = np.ascontiguousarray(ids, dtype=np.uint32)
+        if not (lbo.size == lio.size == lc.size == self.k_cells):
+            raise QadcError(6, "ivf: list/id section mismatch")  # index.hpp:173
+        if int(lc.sum()) != idv.size:
+            raise QadcError(6, "ivf: list code count != id count")  # index.hpp:175
+        self.total = int(lc.sum())
+        check(lib().qadc_ivf_open(C.byref(spec), _p(cb, C.c_float), _p(co, C.c_float), C.c_uint32(self.k_cells),
+                                  _p(pk, C.c_uint8), _p(lbo, C.c_uint64), _p(lio, C.c_uint64), _p(lc, C.c_uint64),
+                                  _p(idv, C.c_uint32), None, None, None, C.c_int(device), C.byref(self._h)))
+
+    def size(self) -> int:
+        return self.total
+
+    def cells(self) -> int:
+        return self.k_cells
+
+    def probe_order(self, queries, a: int) -> np.ndarray:
+        """IvfIndex::probe_order (index.hpp:247-265) for a batch."""
+        q = _f32(queries).reshape(-1, self.spec.dims)
+        a = min(a, self.k_cells)
+        out = np.empty((q.shape[0], a), dtype=np.uint32)
+        check(lib().qadc_ivf_probe_order(self._h, _p(q, C.c_float), C.c_uint32(q.shape[0]), C.c_uint32(a),
+                                         _p(out, C.c_uint32)))
+        return out
+
+
+def scan_list(spec: QadcSpec, packed, count: int, qlut, *, rows=None, width=None, ids=None, base_id=0, acc_init=0,
+              cap=100, heap_in=None, device=0):
+    """The QuantizedScanFn contract (simd/kernels.hpp:49-50, scan_scalar.hpp:34-64) on the GPU.
+
+    Scans one PackedList with caller-supplied quantized tables into a bounded heap that may be
+    pre-seeded with ``heap_in`` [(dist, id), ...]; returns the heap's ``sorted()`` as (dists, ids)."""
+    packed = np.ascontiguousarray(packed, dtype=np.uint8).reshape(-1)
+    width = spec.word_width if width is None else width
+    qlut = np.ascontiguousarray(qlut, dtype=np.uint8 if width == 8 else np.uint16)
+    rows = spec.groups if rows is None else rows
+    ids_a = None if ids is None else np.ascontiguousarray(ids, dtype=np.uint32)
+    hd = hi = None
+    n_in = 0
+    if heap_in is not None and len(heap_in):
+        hd = np.ascontiguousarray([d for d, _ in heap_in], dtype=np.uint32)
+        hi = np.ascontiguousarray([i for _, i in heap_in], dtype=np.uint32)
+        n_in = len(heap_in)
+    od = np.empty(max(cap, 1), dtype=np.uint32)
+    oi = np.empty(max(cap, 1), dtype=np.uint32)
+    n_out = C.c_uint32(0)
+    check(lib().qadc_scan_list(C.byref(spec), _p(packed, C.c_uint8), C.c_uint64(count), C.c_uint32(rows),
+                               qlut.ctypes.data_as(C.c_void_p), C.c_uint32(width), _p(ids_a, C.c_uint32),
+                               C.c_uint32(base_id), C.c_uint32(acc_init), C.c_uint32(cap), _p(hd, C.c_uint32),
+                               _p(hi, C.c_uint32), C.c_uint32(n_in), _p(od, C.c_uint32), _p(oi, C.c_uint32),
+                               C.byref(n_out), C.c_int(device)))
+    return od[:n_out.value].copy(), oi[:n_out.value].copy()
+
+
+def encode(spec: QadcSpec, codebook, vectors, device: int = 0) -> np.ndarray:
+    """encode (codebook.hpp:94-118) on the GPU: nearest centroid per slice, double accumulators,
+    ties toward the lowest index."""
+    cb = _f32(codebook).reshape(-1)
+    v = _f32(vectors).reshape(-1, spec.dims)
+    out = np.empty((v.shape[0], spec.m), dtype=np.uint8)
+    check(lib().qadc_encode(C.byref(spec), _p(cb, C.c_float), _p(v, C.c_float), C.c_uint64(v.shape[0]),
+                            _p(out, C.c_uint8), C.c_int(device)))
+    return out
+
+
+def merge_topk_device(d_keys, nshards: int, nq: int, r: int, d_map, d_ids, d_dists, d_counts, device: int,
+                      fma_unquantize=False, stream=None):
+    """Multi-GPU exchange step: merge gathered per-shard key lists [nshards, nq, r] (torch CUDA tensors)."""
+    ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+    check(lib().qadc_merge_topk_device(ptr(d_keys), C.c_uint32(nshards), C.c_uint32(nq), C.c_uint32(r), ptr(d_map),
+                                       C.c_uint32(1 if fma_unquantize else 0), ptr(d_ids), ptr(d_dists),
+                                       ptr(d_counts), C.c_int(device), C.c_void_p(stream or 0)))

@@ -1,0 +1,258 @@
+"""GPU parity tests proper: the CUDA path, called through the C ABI, against (1) the committed golden
+fixtures produced by the unmodified reference and (2) the CPU oracle on the same seeded inputs.
+Bit-exact everywhere: float LUTs and distances compare bitwise, integers exactly."""
+import numpy as np
+import pytest
+
+import paper_1812_09162_b200 as qb
+from paper_1812_09162_b200.synth import gaussian_mixture, random_codes
+
+pytestmark = pytest.mark.gpu
+
+FLAT = ["flat_pq16x4.npz", "flat_irr655.npz", "flat_irr664.npz", "flat_irr555.npz", "flat_split88.npz",
+        "flat_split8.npz", "flat_pq16x4_short.npz", "flat_irr655_short.npz"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib_loaded():
+    qb.build()
+    assert qb.lib().qadc_device_count() > 0, "GPU tests need a CUDA device"
+
+
+def bits_equal(a, b):
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("name", FLAT)
+def test_golden_flat(golden, name):
+    g = golden(name)
+    s = qb.allocate_dims(int(g["dims"]), str(g["spec"]))
+    n, r, t = int(g["count"]), int(g["r"]), int(g["t"])
+    with qb.FlatIndex(s, g["codebook"], g["packed"], n) as idx:
+        assert np.array_equal(idx.download_codes(0, n), g["codes"])  # layout bijection
+        p = qb.SearchParams(r=r, t=t)
+        luts, qluts, calib = idx.tables(g["queries"], p)
+        assert bits_equal(luts, g["luts"])
+        assert bits_equal(calib, g["params"])
+        assert np.array_equal(qluts, g["qlut"])
+        for qi in range(len(g["queries"])):
+            assert np.array_equal(idx.adc_sums(g["qlut"][qi], 0, n), g["sums"][qi])
+        res = idx.search(g["queries"], p)
+        assert np.array_equal(res.counts, g["counts"])
+        for qi in range(len(g["queries"])):
+            c = int(g["counts"][qi])
+            assert np.array_equal(res.ids[qi, :c], g["ids"][qi, :c])
+            assert bits_equal(res.dists[qi, :c], g["dists"][qi, :c])
+        assert idx.stats().kernel_launches > 0
+
+
+def test_golden_scan_cases(golden):
+    g = golden("scan_cases.npz")
+    for c in range(int(g["n_cases"])):
+        p = f"c{c}_"
+        s = qb.allocate_dims(int(g[p + "dims"]), str(g[p + "spec"]))
+        ids = g[p + "ids"] if g[p + "ids"].size else None
+        pre = [(int(d), int(i)) for d, i in g[p + "pre"]]
+        od, oi = qb.scan_list(s, g[p + "packed"], int(g[p + "n"]), g[p + "qlut"], ids=ids, base_id=int(g[p + "base"]),
+                              acc_init=int(g[p + "init"]), cap=int(g[p + "cap"]), heap_in=pre)
+        assert np.array_equal(od, g[p + "out_d"]) and np.array_equal(oi, g[p + "out_i"]), str(g[p + "spec"])
+
+
+def test_scan_fn_differential(port):
+    """selftest.hpp:40-127 methodology against the oracle: random tables (uniform / saturation-heavy), block
+    counts and occupancies, pre-seeded heaps, accumulator bias, both id modes."""
+    rng = np.random.default_rng(2024)
+    fams = [("{4,4}", [2, 4, 6, 8, 10, 16, 32]), ("{6,6,4}", [3, 6, 12, 24]), ("{6,5,5}", [3, 6, 12, 24]),
+            ("{5,5,5}", [3, 6, 12, 24]), ("{8,8}", [2, 4, 8, 16]), ("{8}", [1, 2, 4, 8, 16])]
+    for pat, ms in fams:
+        for _ in range(12):
+            m = int(ms[rng.integers(len(ms))])
+            s = qb.allocate_dims(16 * m, f"{m}x{pat}")
+            so = port.spec(16 * m, f"{m}x{pat}")
+            qmax = s.q_max
+            dt = np.uint8 if s.word_width == 8 else np.uint16
+            if rng.integers(4) == 0:
+                qlut = (qmax - rng.integers(0, qmax // 4 + 1, size=s.total_entries)).astype(dt)
+            else:
+                qlut = rng.integers(0, qmax + 1, size=s.total_entries).astype(dt)
+            n = int(1 + rng.integers(s.block_len * 3))
+            if rng.integers(3) == 0:
+                n = int(1 + rng.integers(20000))
+            codes = random_codes(s, n, seed=int(rng.integers(1 << 30)))
+            pk = qb.pack_list(s, codes)
+            kw = dict(cap=int(1 + rng.integers(24)),
+                      acc_init=int(rng.integers(qmax + 2)) if rng.integers(4) == 0 else 0,
+                      base_id=int(rng.integers(100000)),
+                      ids=rng.integers(0, 1000000, size=n).astype(np.uint32) if rng.integers(2) else None,
+                      heap_in=[(int(rng.integers(qmax + 1)), 2000000 + i) for i in range(int(rng.integers(4)))])
+            a = port.scan_quantized(so, pk, n, qlut, **kw)
+            b = qb.scan_list(s, pk, n, qlut, **kw)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (pat, m, n, kw["cap"])
+
+
+def test_scan_list_config_errors():
+    # scan_scalar.hpp:23-27, 38-39; heap.hpp:27-28
+    s = qb.allocate_dims(128, "16x{4,4}")
+    pk = qb.pack_list(s, np.zeros((5, 16), np.uint8))
+    for kw, q in [(dict(width=16), np.zeros(256, np.uint16)), (dict(rows=4), np.zeros(256, np.uint8)),
+                  (dict(cap=0), np.zeros(256, np.uint8))]:
+        with pytest.raises(qb.QadcError) as e:
+            qb.scan_list(s, pk, 5, q, **kw)
+        assert e.value.kind == "config"
+
+
+def test_all_zero_and_saturated_tables(port):
+    # T/test_kernels.cpp:79-105 (all-zero tables keep the first R ids) and :135-159 (saturated never displace)
+    s = qb.allocate_dims(128, "16x{4,4}")
+    n = 30000
+    pk = qb.pack_list(s, random_codes(s, n, seed=3))
+    d, i = qb.scan_list(s, pk, n, np.zeros(256, np.uint8), cap=10, base_id=7)
+    assert d.tolist() == [0] * 10 and i.tolist() == list(range(7, 17))
+    d, i = qb.scan_list(s, pk, n, np.full(256, 255, np.uint8), cap=5, heap_in=[(9, 1), (8, 2), (7, 3), (6, 4), (5, 5)])
+    assert i.tolist() == [5, 4, 3, 2, 1]
+    d, i = qb.scan_list(s, pk, n, np.full(256, 255, np.uint8), cap=5)
+    assert d.tolist() == [255] * 5 and i.tolist() == [0, 1, 2, 3, 4]
+
+
+def test_whole_vs_chunked_scan(port):
+    # T/test_kernels.cpp:107-133: scanning a list in chunks with base_id == scanning it whole (sharding correctness)
+    rng = np.random.default_rng(9)
+    for dims, text in [(128, "16x{4,4}"), (96, "12x{6,5,5}")]:
+        s = qb.allocate_dims(dims, text)
+        n = 3 * 960
+        codes = random_codes(s, n, seed=4)
+        qlut = rng.integers(0, s.q_max + 1, size=s.total_entries).astype(np.uint8 if s.word_width == 8 else np.uint16)
+        whole = qb.scan_list(s, qb.pack_list(s, codes), n, qlut, cap=20)
+        heap = []
+        for c in range(3):
+            part = codes[c * 960:(c + 1) * 960]
+            d, i = qb.scan_list(s, qb.pack_list(s, part), 960, qlut, cap=20, base_id=c * 960, heap_in=heap)
+            heap = list(zip(d.tolist(), i.tolist()))
+        assert [h[0] for h in heap] == whole[0].tolist() and [h[1] for h in heap] == whole[1].tolist()
+
+
+SPECS = [(128, "16x{4,4}"), (96, "12x{6,5,5}"), (128, "8x{8,8}"), (128, "8x{8}"), (128, "12x{6,6,4}"),
+         (120, "12x{5,5,5}"), (128, "12x{6,5,5}"), (64, "32x{4,4}"), (64, "4x{4,4,4,4}")]
+
+
+@pytest.mark.parametrize("dims,text", SPECS)
+def test_flat_search_vs_oracle(port, dims, text):
+    """FlatIndex::search end to end (T/test_index.cpp:57-89): ids AND unquantized distances exact."""
+    rng = np.random.default_rng(abs(hash(text)) % 10000)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+    n, nq = 60000, 70
+    codes = random_codes(s, n, seed=12)
+    pk = qb.pack_list(s, codes)
+    queries = (rng.standard_normal((nq, dims)) * 2).astype(np.float32)
+    ref = port.flat_search(so, cb, pk, n, queries, r=100, t=400, threads=8, debug=True)
+    with qb.FlatIndex(s, cb, pk, n) as idx:
+        luts, qluts, calib = idx.tables(queries)
+        assert np.array_equal(qluts, ref[3]) and bits_equal(calib, ref[4])
+        res = idx.search(queries)
+        assert np.array_equal(res.counts, ref[2])
+        assert np.array_equal(res.ids, ref[0]) and bits_equal(res.dists, ref[1])
+        # R >= N and tiny r / t edge cases (T/test_index.cpp:24-55)
+        for r, t in [(1, 1), (7, 9), (1000, 1000)]:
+            sub = queries[:5]
+            ref2 = port.flat_search(so, cb, pk[:qb.packed_bytes(s, 300)], 300, sub, r=r, t=t)
+            with qb.FlatIndex(s, cb, pk[:qb.packed_bytes(s, 300)], 300) as small:
+                got = small.search(sub, qb.SearchParams(r=r, t=t))
+                assert np.array_equal(got.counts, ref2[2])
+                for qi in range(5):
+                    c = int(ref2[2][qi])
+                    assert np.array_equal(got.ids[qi, :c], ref2[0][qi, :c]) and bits_equal(got.dists[qi, :c], ref2[1][qi, :c])
+
+
+def test_search_errors_and_empty():
+    s = qb.allocate_dims(64, "16x{4,4}")
+    cb = np.zeros(s.cb_floats, np.float32)
+    pk = qb.pack_list(s, np.zeros((40, 16), np.uint8))
+    with qb.FlatIndex(s, cb, pk, 40) as idx:
+        q = np.zeros((2, 64), np.float32)
+        for p in (qb.SearchParams(r=0), qb.SearchParams(r=100, t=50)):
+            with pytest.raises(qb.QadcError) as e:
+                idx.search(q, p)
+            assert e.value.kind == "input"
+        with pytest.raises(qb.QadcError) as e:
+            idx.search(np.zeros((2, 63), np.float32))
+        assert e.value.kind == "input"
+        res = idx.search(q)  # degenerate: all-zero codebook -> delta == 0, every distance 0, first ids win
+        assert res.counts.tolist() == [40, 40] and res.ids[0, :40].tolist() == list(range(40))
+    with qb.FlatIndex(s, cb, np.zeros(0, np.uint8), 0) as empty:
+        res = empty.search(np.zeros((3, 64), np.float32))
+        assert res.counts.tolist() == [0, 0, 0]
+    bad = cb.copy()
+    bad[3] = np.nan
+    with pytest.raises(qb.QadcError) as e:
+        qb.FlatIndex(s, bad, pk, 40)
+    assert e.value.kind == "corruption"
+
+
+def test_candidate_overflow_retry(port):
+    """Adversarial order (distances strictly improving along the list) floods the candidate buffer; the
+    library must detect the overflow and redo the batch with a larger buffer, still exact."""
+    s, so = qb.allocate_dims(16, "2x{8}"), port.spec(16, "2x{8}")
+    n = 40000
+    codes = np.zeros((n, 2), np.uint8)
+    codes[:, 0] = (255 - (np.arange(n) * 256 // n)).astype(np.uint8)  # decreasing first subcode
+    codes[:, 1] = 0
+    pk = qb.pack_list(s, codes)
+    qlut = np.concatenate([np.arange(256) // 2, np.zeros(256)]).astype(np.uint8)
+    a = port.scan_quantized(so, pk, n, qlut, cap=50)
+    b = qb.scan_list(s, pk, n, qlut, cap=50)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_encode_vs_oracle(port):
+    rng = np.random.default_rng(5)
+    for dims, text in [(128, "16x{4,4}"), (96, "12x{6,5,5}"), (64, "8x{8}")]:
+        s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+        cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+        # duplicate a centroid so that exact ties occur (lowest index must win, T/test_kmeans_codebook.cpp:108-118)
+        d0 = s.dim_alloc[0]
+        cb[d0:2 * d0] = cb[0:d0]
+        v = (rng.standard_normal((3000, dims)) * 2).astype(np.float32)
+        v[0, :d0] = cb[0:d0]
+        assert np.array_equal(qb.encode(s, cb, v), port.encode(so, cb, v))
+
+
+def test_large_seeded_property_round_trip(port):
+    """Size-independent properties at a larger size (1M codes x 256 queries on 16x{4,4}): every returned
+    (distance, id) must equal the oracle's quantized ADC sum of that code under the oracle's tables, be
+    sorted by (distance, id), and the R-th distance must bound a uniform sample of the list."""
+    rng = np.random.default_rng(77)
+    dims, text = 128, "16x{4,4}"
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    centres = None
+    train = gaussian_mixture(20000, dims, seed=4)
+    from paper_1812_09162_b200.synth import train_codebook
+    cb = train_codebook(s, train, iters=4)
+    n, nq = 1_000_000, 256
+    codes = random_codes(s, n, seed=6)
+    pk = qb.pack_list(s, codes)
+    queries = gaussian_mixture(nq, dims, seed=3)
+    with qb.FlatIndex(s, cb, pk, n) as idx:
+        res = idx.search(queries)
+        luts, qluts, calib = idx.tables(queries)
+    assert np.all(res.counts == 100)
+    sample = rng.choice(n, size=20000, replace=False)
+    for qi in range(0, nq, 16):
+        lut = port.compute_tables(so, cb, queries[qi])
+        pre = port.prefix_float(so, pk, n, lut, 400)
+        dmin, dmax = port.calibrate(so, lut, pre, 100)
+        qlut, _, delta, own = port.quantize(so, lut, dmin, dmax, 8)
+        assert np.array_equal(qlut, qluts[qi])
+        sums = qlut.astype(np.uint32).reshape(16, 16)[np.arange(16)[None, :], codes[res.ids[qi]].astype(np.int64)].sum(1)
+        sums = np.minimum(sums, 255)
+        want = (sums.astype(np.float32) * delta + own).astype(np.float32)
+        assert bits_equal(res.dists[qi], want)
+        keys = sums.astype(np.int64) << 32 | res.ids[qi].astype(np.int64)
+        assert np.all(np.diff(keys) > 0)
+        ssum = np.minimum(qlut.astype(np.uint32).reshape(16, 16)[np.arange(16)[None, :], codes[sample].astype(np.int64)].sum(1), 255)
+        skeys = ssum.astype(np.int64) << 32 | sample.astype(np.int64)
+        inside = np.isin(sample, res.ids[qi])
+        assert np.all(skeys[~inside] > keys[-1])
+    # and the full oracle on a few queries
+    ref = port.flat_search(so, cb, pk, n, queries[:4], r=100, t=400, threads=4)
+    assert np.array_equal(res.ids[:4], ref[0]) and bits_equal(res.dists[:4], ref[1])
