@@ -162,9 +162,10 @@ struct qadc_index {
     uint32_t seg0 = 4096;
     uint32_t seg_growth = 8;
     int force_variant = -1;
+    int cif = 2;
     // workspace
     SelectBufs sel;
-    DevBuf qlut, luts, calib_out, map, status, jobs, queries, out_ids, out_dists, out_counts, counters, scratch;
+    DevBuf qlut, tile_lut, luts, calib_out, map, status, jobs, queries, out_ids, out_dists, out_counts, counters, scratch;
     qadc_stats stats{};
     StageTimer timer;
 
@@ -177,7 +178,7 @@ namespace qadc {
 
 static constexpr uint64_t CODE_PAD = 1024; // device code arrays are padded to this many codes
 
-static ScanPlan plan_for(const qadc_index* h) { return plan_scan(h->ds, h->device, h->force_variant, 0); }
+static ScanPlan plan_for(const qadc_index* h) { return plan_scan(h->ds, h->device, h->force_variant, h->cif); }
 
 // Geometric segment schedule: after n codes the R-th best of n bounds the admission
 // rate of the next codes by R/n, so each segment admits O(R * growth) candidates.
@@ -217,6 +218,7 @@ static void flat_segment_jobs(std::vector<ScanJob>& jobs, uint64_t seg_begin, ui
 
 struct RowSet {
     const void* qlut;          // device [rows][E]
+    const void* tile_lut;      // device [tile][E][TQ] (tilepack.cu)
     const uint32_t* row_query; // device or nullptr
     const uint32_t* row_bias;  // device or nullptr
 };
@@ -260,6 +262,7 @@ static bool scan_select_flat(qadc_index* h, const ScanPlan& plan, const uint8_t*
         a.codes = d_codes;
         a.ids = nullptr;
         a.qlut = rows.qlut;
+        a.tile_lut = rows.tile_lut;
         a.row_query = rows.row_query;
         a.row_bias = rows.row_bias;
         a.jobs = h->jobs.as<ScanJob>() + first;
@@ -355,8 +358,11 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
         la.status = h->status.as<int>();
         const size_t t0 = h->timer.mark(st);
         launch_flat_tables(ds, la, st);
+        const uint32_t ntiles = (nb + plan.tq - 1) / plan.tq;
+        h->tile_lut.ensure(size_t(ntiles) * ds.E * plan.tq * tile_entry_bytes(plan.variant));
+        launch_pack_tiles(plan.variant, h->qlut.p, ds.word_width, ds.E, nb, plan.tq, h->tile_lut.p, st);
         h->timer.span(0, t0, h->timer.mark(st));
-        RowSet rows{h->qlut.p, nullptr, nullptr};
+        RowSet rows{h->qlut.p, h->tile_lut.p, nullptr, nullptr};
         const bool ok = scan_select_flat(h, plan, h->codes.as<uint8_t>(), h->count, h->base_id, rows, nb, p.r, cap,
                                          false, st);
         if (!ok) { // some query admitted more candidates than fit: redo this batch with a larger buffer
@@ -656,7 +662,9 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
                                h.sel.cand_count.as<uint32_t>(), buf_cap, h.sel.thr_key.as<uint64_t>(), 1, cap, st);
                 QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // seed vector goes out of scope
             }
-            RowSet rs{h.qlut.p, nullptr, bias.as<uint32_t>()};
+            h.tile_lut.ensure(size_t(ds.E) * plan.tq * tile_entry_bytes(plan.variant));
+            launch_pack_tiles(plan.variant, h.qlut.p, ds.word_width, ds.E, 1, plan.tq, h.tile_lut.p, st);
+            RowSet rs{h.qlut.p, h.tile_lut.p, nullptr, bias.as<uint32_t>()};
             bool ok = true;
             if (count) {
                 // same machinery as the flat search; explicit ids ride in ScanArgs::ids
@@ -674,6 +682,7 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
                         a.codes = h.codes.as<uint8_t>();
                         a.ids = ids ? h.ids.as<uint32_t>() : nullptr;
                         a.qlut = rs.qlut;
+                        a.tile_lut = rs.tile_lut;
                         a.row_bias = rs.row_bias;
                         a.jobs = h.jobs.as<ScanJob>();
                         a.n_jobs = uint32_t(jobs.size());
@@ -752,6 +761,7 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384));
         else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
         else if (n == "force_variant") h->force_variant = int(value);
+        else if (n == "cif") h->cif = int(value);
         else throw Error(QADC_ERR_CONFIG, "set_option: unknown option " + n);
     });
 }

@@ -62,13 +62,15 @@ enum ScanVariant : uint32_t {
     VAR_F32X2 = 1,   // u16 tables, fp32 entries in smem, 2 rows per lane (LDS.64), 64-row tile
     VAR_U16X1 = 2,   // any width, u16 entries in smem, 1 row per lane, 32-row tile, int32 accumulate
     VAR_U8X1 = 3,    // any width, u8 (high-byte for u16 tables) conservative filter, 32-row tile
+    VAR_F16X4H = 4,  // u16 tables, fp16 HIGH-BYTE conservative filter, 4 rows per lane (LDS.64), 128-row tile
     VAR_COUNT
 };
 
 struct ScanArgs {
     const uint8_t* codes;      // device code array, code_stride bytes per code
     const uint32_t* ids;       // explicit ids or nullptr
-    const void* qlut;          // [rows][E] at table width, reference table order
+    const void* qlut;          // [rows][E] at table width, reference table order (exact re-evaluation)
+    const void* tile_lut;      // [tile][E][TQ] in the variant's entry type (tilepack.cu); tile = row / TQ
     const uint32_t* row_query; // row -> query index (nullptr: identity)
     const uint32_t* row_bias;  // row -> acc_init (nullptr: 0)
     const ScanJob* jobs;
@@ -86,6 +88,7 @@ struct ScanPlan {
     uint32_t tq;         // rows per tile
     uint32_t smem_bytes;
     uint32_t threads;
+    uint32_t cif; // codes in flight per warp (1, 2 or 4)
 };
 
 // chooses the variant for a spec (throws config error if nothing fits shared memory)
@@ -118,6 +121,11 @@ void launch_tighten(uint64_t* top, uint32_t* ntop, uint32_t kpad, uint64_t* cand
 void launch_finalize(const uint64_t* lists, const uint32_t* counts_in, uint32_t list_len, uint32_t nlists,
                      uint32_t nq, uint32_t r, const float* map, uint32_t flags, uint32_t qmax, uint32_t* out_ids,
                      float* out_dists, uint32_t* out_counts, uint64_t* out_keys, cudaStream_t stream);
+
+// ---- tile-layout tables (tilepack.cu) ----
+size_t tile_entry_bytes(ScanVariant v);
+void launch_pack_tiles(ScanVariant v, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
+                       void* out, cudaStream_t stream);
 
 // ---- dense head evaluation (seed.cu) ----
 void launch_seed_topk(const DevSpec& ds, const uint8_t* d_codes, uint32_t n_head, uint32_t id_base,

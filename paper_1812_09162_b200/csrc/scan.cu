@@ -59,6 +59,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     } while (!done);
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() { // named barrier over the consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(16 * 32) : "memory");
+}
 // TMA 1-D bulk copy global -> shared, completion counted on an mbarrier (SASS: UBLKCP)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -130,7 +136,6 @@ struct PolF16x8 { // u8 tables only
     struct Acc {
         __half2 h[4];
     };
-    __device__ static Entry convert(uint32_t v, uint32_t) { return __uint2half_rn(v); } // exact: v <= 255
     __device__ static void init(Acc& a, const float* t) { // t[s] = bias - thr - 0.5 (or +-BIG)
 #pragma unroll
         for (int k = 0; k < 4; ++k) a.h[k] = __floats2half2_rn(t[2 * k], t[2 * k + 1]);
@@ -164,7 +169,6 @@ struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
     struct Acc {
         float f[2];
     };
-    __device__ static Entry convert(uint32_t v, uint32_t) { return float(v); }
     __device__ static void init(Acc& a, const float* t) {
         a.f[0] = t[0];
         a.f[1] = t[1];
@@ -180,6 +184,34 @@ struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
     static constexpr float BIG = 1.0e9f, HALF = 0.5f;
 };
 
+struct PolF16x4H { // u16 tables: fp16 image of the HIGH byte of every entry; conservative filter
+    static constexpr int QPL = 4, TQ = 128, ROWB = 256, LOG_ROWB = 8, LANE_B = 8;
+    static constexpr bool EXACT_FILTER = false;
+    using Entry = __half;
+    struct Acc {
+        __half2 h[2];
+    };
+    __device__ static void init(Acc& a, const float* t) {
+        a.h[0] = __floats2half2_rn(t[0], t[1]);
+        a.h[1] = __floats2half2_rn(t[2], t[3]);
+    }
+    __device__ static void add(Acc& a, const char* p) {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        a.h[0] = __hadd2(a.h[0], *reinterpret_cast<const __half2*>(&v.x));
+        a.h[1] = __hadd2(a.h[1], *reinterpret_cast<const __half2*>(&v.y));
+    }
+    __device__ static bool any(const Acc& a) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(a.h);
+        return ((u[0] | u[1]) & 0x80008000u) != 0;
+    }
+    __device__ static bool hit(const Acc& a, int s) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(a.h);
+        return (u[s >> 1] >> ((s & 1) * 16 + 15)) & 1u;
+    }
+    __device__ static float value(const Acc&, int) { return 0.f; } // never used: the filter is not exact
+    static constexpr float BIG = 30000.0f, HALF = 0.5f;
+};
+
 struct PolU16x1 { // any width, u16 entries, int32 accumulate
     static constexpr int QPL = 1, TQ = 32, ROWB = 64, LOG_ROWB = 6, LANE_B = 2;
     static constexpr bool EXACT_FILTER = true;
@@ -187,7 +219,6 @@ struct PolU16x1 { // any width, u16 entries, int32 accumulate
     struct Acc {
         int v;
     };
-    __device__ static Entry convert(uint32_t v, uint32_t) { return (unsigned short)v; }
     __device__ static void init(Acc& a, const float* t) { a.v = int(floorf(t[0])); } // bias - thr - 1
     __device__ static void add(Acc& a, const char* p) { a.v += int(*reinterpret_cast<const unsigned short*>(p)); }
     __device__ static bool any(const Acc& a) { return a.v < 0; }
@@ -203,7 +234,6 @@ struct PolU8x1 { // any width; u16 tables keep only the HIGH byte: a conservativ
     struct Acc {
         int v;
     };
-    __device__ static Entry convert(uint32_t v, uint32_t width) { return (unsigned char)(width == 16 ? v >> 8 : v); }
     __device__ static void init(Acc& a, const float* t) { a.v = int(floorf(t[0])); }
     __device__ static void add(Acc& a, const char* p) { a.v += int(*reinterpret_cast<const unsigned char*>(p)); }
     __device__ static bool any(const Acc& a) { return a.v < 0; }
@@ -213,10 +243,13 @@ struct PolU8x1 { // any width; u16 tables keep only the HIGH byte: a conservativ
     static constexpr float BIG = 1.0e9f, HALF = 0.5f;
 };
 
-static constexpr int SCAN_THREADS = 512;
-static constexpr int SCAN_WARPS = SCAN_THREADS / 32;
-static constexpr int STAGE_BYTES = 8192; // one code stage buffer
-static constexpr int NSTAGE = 2;
+static constexpr int SCAN_WARPS = 16;                      // consumer warps
+static constexpr int SCAN_CONSUMERS = SCAN_WARPS * 32;     // consumer threads
+static constexpr int SCAN_THREADS = SCAN_CONSUMERS + 32;   // + one producer warp (TMA issue)
+static constexpr int STAGE_BYTES = 8192;                   // one code stage buffer
+static constexpr int NSTAGE = 4;
+static constexpr int WQ_CAP = 64;                          // per-warp queue of flagged (row, code) pairs
+static constexpr int WQ_BYTES = SCAN_WARPS * WQ_CAP * 12;  // row, stage index, accumulator value
 
 // --------------------------------------------------------- exact admission --
 
@@ -228,7 +261,7 @@ __device__ __forceinline__ uint32_t rt_sub_index(const DevSpec* ds, const uint8_
 
 // The CandidateHeap::push test (heap.hpp:40-51) for one (row, code): exact saturating
 // sum (scan_scalar.hpp:52-58) from the reference-order table, then key < worst key.
-__device__ __noinline__ void exact_admit(const DevSpec* ds, const ScanArgs* a, const uint8_t* code, uint32_t row,
+__device__ __forceinline__ void exact_admit(const DevSpec* ds, const ScanArgs* a, const uint8_t* code, uint32_t row,
                                          uint32_t id) {
     uint32_t acc = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;
     const size_t base = size_t(row) * ds->E;
@@ -249,14 +282,15 @@ __device__ __noinline__ void exact_admit(const DevSpec* ds, const ScanArgs* a, c
     }
 }
 
-// Admission of one flagged (row, code).  When the in-loop filter is exact and the row has
+// Admission of one flagged (row, code), run by one lane of a warp-wide flush (32 entries
+// resolved at once, all lanes active).  When the in-loop filter is exact and the row has
 // a finite, unsaturated threshold, the accumulator itself is exact (it is < 0, far
 // inside the exactly representable range): bias + sum = acc + thr + 1/2, no re-evaluation.
 // Otherwise (no threshold yet, saturated threshold, or the high-byte filter) fall back to
 // the integer re-evaluation above.
 template <class P>
-__device__ __forceinline__ void admit(const DevSpec* ds, const ScanArgs* a, const typename P::Acc& acc, int s,
-                                      const uint8_t* code, uint32_t row, uint32_t id) {
+__device__ __forceinline__ void admit_entry(const DevSpec* ds, const ScanArgs* a, float val, const uint8_t* code,
+                                            uint32_t row, uint32_t id) {
     const uint32_t q = a->row_query ? a->row_query[row] : row;
     const uint64_t tk = a->thr_key[q];
     const uint32_t thr = uint32_t(tk >> 32);
@@ -264,7 +298,7 @@ __device__ __forceinline__ void admit(const DevSpec* ds, const ScanArgs* a, cons
         exact_admit(ds, a, code, row, id);
         return;
     }
-    const uint32_t d = uint32_t(P::value(acc, s) + float(thr) + 0.5f);
+    const uint32_t d = uint32_t(val + float(thr) + 0.5f);
     const uint64_t key = make_key(d, id);
     if (key < tk) {
         const uint32_t slot = atomicAdd(&a->cand_count[q], 1u);
@@ -275,19 +309,24 @@ __device__ __forceinline__ void admit(const DevSpec* ds, const ScanArgs* a, cons
 
 // ------------------------------------------------------------------- kernel --
 
-template <class P, class G>
+template <class P, class G, int CIF>
 __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param, ScanArgs args_param) {
     extern __shared__ __align__(1024) char smem[];
-    // [0, E*ROWB) LUT tile | stage buffers | mbarriers
+    // dynamic smem: [0, E*ROWB) LUT tile | NSTAGE code stage buffers
     __shared__ DevSpec s_ds;
     __shared__ ScanArgs s_args;
-    __shared__ __align__(8) uint64_t s_bar[NSTAGE];
+    __shared__ __align__(8) uint64_t s_full[NSTAGE], s_empty[NSTAGE];
+    __shared__ __align__(8) uint64_t s_tbar; // LUT tile arrival
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         s_ds = ds_param;
         s_args = args_param;
-        for (int i = 0; i < NSTAGE; ++i) mbar_init(&s_bar[i], 1);
+        for (int i = 0; i < NSTAGE; ++i) {
+            mbar_init(&s_full[i], 1);           // the producer's arrive.expect_tx
+            mbar_init(&s_empty[i], SCAN_WARPS); // one arrival per consumer warp
+        }
+        mbar_init(&s_tbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -299,13 +338,36 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     char* tile = smem;
     char* stage = smem + size_t(E) * P::ROWB;
     const uint32_t stage_codes = STAGE_BYTES / stride;
-    uint32_t bar_phase = 0; // bit b = parity to wait for on barrier b
 
     // contiguous slice of the job list for this CTA
     const uint32_t j_begin = uint32_t(uint64_t(a->n_jobs) * blockIdx.x / gridDim.x);
     const uint32_t j_end = uint32_t(uint64_t(a->n_jobs) * (blockIdx.x + 1) / gridDim.x);
 
+    // ============================ producer warp: stream codes with TMA bulk copies ==========
+    if (warp == SCAN_WARPS) {
+        if (lane != 0) return;
+        uint32_t it = 0; // running stage-fill counter, mirrored by the consumers
+        for (uint32_t ji = j_begin; ji < j_end; ++ji) {
+            const ScanJob job = a->jobs[ji];
+            if (job.n_codes == 0 || job.n_rows == 0) continue;
+            const uint8_t* gcodes = a->codes + job.code_off * stride;
+            const uint32_t n_sub = (job.n_codes + stage_codes - 1) / stage_codes;
+            for (uint32_t sub = 0; sub < n_sub; ++sub, ++it) {
+                const uint32_t b = it % NSTAGE;
+                mbar_wait(&s_empty[b], ((it / NSTAGE) & 1u) ^ 1u); // first lap passes immediately
+                const uint32_t first = sub * stage_codes;
+                const uint32_t cnt = min(stage_codes, job.n_codes - first);
+                const uint32_t bytes = (cnt * stride + 15u) & ~15u;
+                mbar_expect_tx(&s_full[b], bytes);
+                bulk_g2s(stage + size_t(b) * STAGE_BYTES, gcodes + size_t(first) * stride, bytes, &s_full[b]);
+            }
+        }
+        return;
+    }
+
+    // ============================ consumer warps ==============================================
     uint32_t cur_row_begin = 0xFFFFFFFFu, cur_n_rows = 0;
+    uint32_t tile_phase = 0, it = 0;
     typename P::Acc acc0;
     {
         float t[P::QPL];
@@ -313,6 +375,13 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
         for (int s = 0; s < P::QPL; ++s) t[s] = P::BIG;
         P::init(acc0, t);
     }
+    const uint32_t lane_off = lane * P::LANE_B;
+    // per-warp queue of flagged pairs: ballot-compacted in the hot loop, resolved 32 at a time
+    uint32_t* wq_row = reinterpret_cast<uint32_t*>(stage + NSTAGE * STAGE_BYTES) + warp * (WQ_CAP * 3);
+    uint32_t* wq_idx = wq_row + WQ_CAP;
+    float* wq_val = reinterpret_cast<float*>(wq_idx + WQ_CAP);
+    uint32_t qn = 0; // warp-uniform fill level
+    const uint32_t lanemask_lt = (1u << lane) - 1u;
 
     for (uint32_t ji = j_begin; ji < j_end; ++ji) {
         const ScanJob job = a->jobs[ji];
@@ -320,45 +389,16 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
 
         // ---- (re)load the LUT tile when the row range changes ----
         if (job.row_begin != cur_row_begin || job.n_rows != cur_n_rows) {
-            __syncthreads(); // everyone is done with the previous tile
+            consumer_sync(); // every consumer is done with the previous tile
             cur_row_begin = job.row_begin;
             cur_n_rows = job.n_rows;
-            const uint32_t wbytes = ds->word_width / 8;
-            const size_t row_bytes = size_t(E) * wbytes;
-            typename P::Entry* te = reinterpret_cast<typename P::Entry*>(tile);
-            if ((row_bytes & 15u) == 0 && (reinterpret_cast<size_t>(a->qlut) & 15u) == 0) {
-                // lane = row inside a 32-row block; 16-byte global loads along the entry axis;
-                // shared-memory stores are lane-contiguous along the row axis (conflict-free)
-                const uint32_t ent_per_vec = 16 / wbytes;
-                const uint32_t n_vec = E / ent_per_vec;
-                const uint32_t n_rblk = P::TQ / 32;
-                for (uint32_t u = warp; u < n_vec * n_rblk; u += SCAN_WARPS) {
-                    const uint32_t rb = u % n_rblk, vi = u / n_rblk;
-                    const uint32_t r = rb * 32 + lane;
-                    uint4 v = make_uint4(0, 0, 0, 0);
-                    if (r < job.n_rows)
-                        v = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a->qlut) +
-                                                            size_t(job.row_begin + r) * row_bytes + size_t(vi) * 16);
-                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (uint32_t k = 0; k < 16; ++k) {
-                        if (wbytes == 2 && k >= 8) break;
-                        const uint32_t val = wbytes == 1 ? (w[k >> 2] >> ((k & 3) * 8)) & 0xFFu
-                                                         : (w[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
-                        te[size_t(vi * ent_per_vec + k) * P::TQ + r] = P::convert(val, ds->word_width);
-                    }
-                }
-            } else {
-                for (uint32_t u = tid; u < E * P::TQ; u += SCAN_THREADS) {
-                    const uint32_t r = u % P::TQ, e = u / P::TQ;
-                    uint32_t val = 0;
-                    if (r < job.n_rows) {
-                        const size_t gi = size_t(job.row_begin + r) * E + e;
-                        val = wbytes == 1 ? uint32_t(reinterpret_cast<const uint8_t*>(a->qlut)[gi])
-                                          : uint32_t(reinterpret_cast<const uint16_t*>(a->qlut)[gi]);
-                    }
-                    te[size_t(e) * P::TQ + r] = P::convert(val, ds->word_width);
-                }
+            // the tile image [entry][row] was prepared by tilepack.cu: bulk async copies, 32 KB each
+            if (tid == 0) {
+                const uint32_t tile_bytes = E * P::ROWB;
+                const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / P::TQ) * tile_bytes;
+                mbar_expect_tx(&s_tbar, tile_bytes);
+                for (uint32_t off = 0; off < tile_bytes; off += 32768u)
+                    bulk_g2s(tile + off, src + off, min(32768u, tile_bytes - off), &s_tbar);
             }
             // per-lane accumulator start: bias - threshold - 1/2 (sign bit <=> admitted)
             float t[P::QPL];
@@ -383,35 +423,55 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                 }
             }
             P::init(acc0, t);
-            __syncthreads();
+            mbar_wait(&s_tbar, tile_phase); // every thread observes the tile's arrival itself
+            tile_phase ^= 1u;
         }
 
-        // ---- stream the job's codes through the stage buffers ----
-        const uint8_t* gcodes = a->codes + job.code_off * stride;
+        // ---- consume the job's codes stage by stage ----
         const uint32_t n_sub = (job.n_codes + stage_codes - 1) / stage_codes;
-        auto issue = [&](uint32_t sub) {
-            const uint32_t first = sub * stage_codes;
-            const uint32_t cnt = min(stage_codes, job.n_codes - first);
-            const uint32_t bytes = (cnt * stride + 15u) & ~15u;
-            const uint32_t b = sub % NSTAGE;
-            mbar_expect_tx(&s_bar[b], bytes);
-            bulk_g2s(stage + size_t(b) * STAGE_BYTES, gcodes + size_t(first) * stride, bytes, &s_bar[b]);
-        };
-        if (tid == 0) {
-            issue(0);
-            if (n_sub > 1) issue(1);
-        }
-        for (uint32_t sub = 0; sub < n_sub; ++sub) {
-            const uint32_t b = sub % NSTAGE;
-            mbar_wait(&s_bar[b], (bar_phase >> b) & 1u);
-            bar_phase ^= 1u << b;
+        for (uint32_t sub = 0; sub < n_sub; ++sub, ++it) {
+            const uint32_t b = it % NSTAGE;
+            mbar_wait(&s_full[b], (it / NSTAGE) & 1u);
             const uint32_t first = sub * stage_codes;
             const uint32_t cnt = min(stage_codes, job.n_codes - first);
             const char* sb = stage + size_t(b) * STAGE_BYTES;
-            const uint32_t lane_off = lane * P::LANE_B;
+            auto flush = [&]() {
+                __syncwarp();
+                for (uint32_t base = 0; base < qn; base += 32) {
+                    const uint32_t e = base + lane;
+                    if (e < qn) {
+                        const uint32_t i = wq_idx[e];
+                        const uint32_t pos = first + i;
+                        const uint32_t id = a->ids ? a->ids[job.ids_off + pos] : job.id_base + pos;
+                        admit_entry<P>(ds, a, wq_val[e], reinterpret_cast<const uint8_t*>(sb + size_t(i) * stride),
+                                       wq_row[e], id);
+                    }
+                }
+                __syncwarp();
+                qn = 0;
+            };
+            auto flag = [&](const typename P::Acc& acc, bool live, uint32_t i) {
+                const bool h = live && P::any(acc);
+                if (__any_sync(0xffffffffu, h)) {
+#pragma unroll
+                    for (int sl = 0; sl < P::QPL; ++sl) {
+                        const bool hs = h && P::hit(acc, sl);
+                        const uint32_t m = __ballot_sync(0xffffffffu, hs);
+                        if (m) {
+                            if (qn + 32 > WQ_CAP) flush();
+                            if (hs) {
+                                const uint32_t slot = qn + __popc(m & lanemask_lt);
+                                wq_row[slot] = job.row_begin + lane * P::QPL + sl;
+                                wq_idx[slot] = i;
+                                wq_val[slot] = P::value(acc, sl);
+                            }
+                            qn += __popc(m);
+                        }
+                    }
+                }
+            };
 
             if constexpr (!G::RUNTIME) {
-                constexpr int CIF = 2; // codes in flight per warp
                 for (uint32_t i0 = warp; i0 < cnt; i0 += SCAN_WARPS * CIF) {
                     uint32_t cw[CIF][G::CW];
                     typename P::Acc acc[CIF];
@@ -443,18 +503,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                         }
                     });
 #pragma unroll
-                    for (int c = 0; c < CIF; ++c) {
-                        const uint32_t i = i0 + c * SCAN_WARPS;
-                        if (i < cnt && P::any(acc[c])) {
-                            const uint32_t pos = first + i;
-                            const uint32_t id = a->ids ? a->ids[job.ids_off + pos] : job.id_base + pos;
-#pragma unroll
-                            for (int s = 0; s < P::QPL; ++s)
-                                if (P::hit(acc[c], s))
-                                    admit<P>(ds, a, acc[c], s, reinterpret_cast<const uint8_t*>(sb + size_t(i) * G::STRIDE),
-                                             job.row_begin + lane * P::QPL + s, id);
-                        }
-                    }
+                    for (int c = 0; c < CIF; ++c) flag(acc[c], i0 + c * SCAN_WARPS < cnt, i0 + c * SCAN_WARPS);
                 }
             } else {
                 // runtime geometry: any m / widths / code size that fits; one code per warp step
@@ -465,17 +514,11 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                         const uint32_t idx = rt_sub_index(ds, code, j);
                         P::add(acc, tile + size_t(ds->ent_off[j] + idx) * P::ROWB + lane_off);
                     }
-                    if (P::any(acc)) {
-                        const uint32_t pos = first + i;
-                        const uint32_t id = a->ids ? a->ids[job.ids_off + pos] : job.id_base + pos;
-#pragma unroll
-                        for (int s = 0; s < P::QPL; ++s)
-                            if (P::hit(acc, s)) admit<P>(ds, a, acc, s, code, job.row_begin + lane * P::QPL + s, id);
-                    }
+                    flag(acc, true, i);
                 }
             }
-            __syncthreads(); // stage buffer b is free again
-            if (tid == 0 && sub + NSTAGE < n_sub) issue(sub + NSTAGE);
+            flush(); // queued pairs reference this stage buffer: resolve them before releasing it
+            if (lane == 0) mbar_arrive(&s_empty[b]); // this warp is done with stage buffer b
         }
     }
 }
@@ -495,16 +538,17 @@ const char* variant_name(uint32_t v) {
     case VAR_F32X2: return "f32x2 (u16 tables as fp32, 64-query tile, LDS.64)";
     case VAR_U16X1: return "u16x1 (u16 entries, 32-query tile, int32 accumulate)";
     case VAR_U8X1: return "u8x1 (high-byte filter, 32-query tile)";
+    case VAR_F16X4H: return "f16x4h (u16 tables, fp16 high-byte filter + exact re-evaluation, 128-query tile, LDS.64)";
     }
     return "?";
 }
 
 template <class P>
 static uint32_t smem_need(uint32_t E) {
-    return E * P::ROWB + NSTAGE * STAGE_BYTES;
+    return E * P::ROWB + NSTAGE * STAGE_BYTES + WQ_BYTES;
 }
 
-ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int) {
+ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int cif) {
     int max_smem = 0;
     QADC_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     // static shared (DevSpec + ScanArgs + barriers) comes out of the same budget
@@ -512,6 +556,7 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int) {
     if (ds.code_stride > 32) throw Error(QADC_ERR_CONFIG, "scan: codes wider than 256 bits are not supported");
     ScanPlan p{};
     p.threads = SCAN_THREADS;
+    p.cif = (cif == 1 || cif == 4) ? cif : 2;
     auto fits = [&](uint32_t need) { return need <= budget; };
     auto set = [&](ScanVariant v, uint32_t tq, uint32_t need) {
         p.variant = v;
@@ -528,12 +573,17 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int) {
         case VAR_F32X2: set(VAR_F32X2, PolF32x2::TQ, smem_need<PolF32x2>(ds.E)); break;
         case VAR_U16X1: set(VAR_U16X1, PolU16x1::TQ, smem_need<PolU16x1>(ds.E)); break;
         case VAR_U8X1: set(VAR_U8X1, PolU8x1::TQ, smem_need<PolU8x1>(ds.E)); break;
+        case VAR_F16X4H:
+            if (u8) throw Error(QADC_ERR_CONFIG, "scan: f16x4h is the 16-bit-table filter");
+            set(VAR_F16X4H, PolF16x4H::TQ, smem_need<PolF16x4H>(ds.E));
+            break;
         default: throw Error(QADC_ERR_CONFIG, "scan: unknown forced variant");
         }
         if (!fits(p.smem_bytes)) throw Error(QADC_ERR_CONFIG, "scan: forced variant does not fit shared memory");
         return p;
     }
     if (u8 && fits(smem_need<PolF16x8>(ds.E))) set(VAR_F16X8, PolF16x8::TQ, smem_need<PolF16x8>(ds.E));
+    else if (!u8 && fits(smem_need<PolF16x4H>(ds.E))) set(VAR_F16X4H, PolF16x4H::TQ, smem_need<PolF16x4H>(ds.E));
     else if (fits(smem_need<PolF32x2>(ds.E))) set(VAR_F32X2, PolF32x2::TQ, smem_need<PolF32x2>(ds.E));
     else if (fits(smem_need<PolU16x1>(ds.E))) set(VAR_U16X1, PolU16x1::TQ, smem_need<PolU16x1>(ds.E));
     else if (fits(smem_need<PolU8x1>(ds.E))) set(VAR_U8X1, PolU8x1::TQ, smem_need<PolU8x1>(ds.E));
@@ -543,13 +593,22 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int) {
     return p;
 }
 
-template <class P, class G>
-static void launch_one(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
-    QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_kernel<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <class P, class G, int CIF>
+static void launch_cif(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_kernel<P, G, CIF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(plan.smem_bytes)));
-    scan_kernel<P, G><<<grid, SCAN_THREADS, plan.smem_bytes, stream>>>(ds, args);
+    scan_kernel<P, G, CIF><<<grid, SCAN_THREADS, plan.smem_bytes, stream>>>(ds, args);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
+}
+template <class P, class G>
+static void launch_one(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
+    if constexpr (G::RUNTIME) return launch_cif<P, G, 1>(plan, ds, args, grid, stream);
+    else {
+        if (plan.cif == 4) return launch_cif<P, G, 4>(plan, ds, args, grid, stream);
+        if (plan.cif == 1) return launch_cif<P, G, 1>(plan, ds, args, grid, stream);
+        return launch_cif<P, G, 2>(plan, ds, args, grid, stream);
+    }
 }
 
 // Compile-time geometries are instantiated only for the (policy, shape) pairs the planner
@@ -571,6 +630,11 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, 
         if (G8::matches(ds)) return launch_one<PolU16x1, G8>(plan, ds, args, grid, stream);
         return launch_one<PolU16x1, GeomRT>(plan, ds, args, grid, stream);
     case VAR_U8X1: return launch_one<PolU8x1, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_F16X4H:
+        if (G655::matches(ds)) return launch_one<PolF16x4H, G655>(plan, ds, args, grid, stream);
+        if (G664::matches(ds)) return launch_one<PolF16x4H, G664>(plan, ds, args, grid, stream);
+        if (G555::matches(ds)) return launch_one<PolF16x4H, G555>(plan, ds, args, grid, stream);
+        return launch_one<PolF16x4H, GeomRT>(plan, ds, args, grid, stream);
     default: throw Error(QADC_ERR_CONFIG, "scan: bad variant");
     }
 }

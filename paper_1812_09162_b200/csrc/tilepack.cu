@@ -1,0 +1,96 @@
+// tilepack.cu -- quantized tables in the scan kernel's shared-memory layout.
+//
+// quantize_tables (lut.cu) emits the reference layout [row][entry] at table width.  The scan
+// kernel wants, per tile of TQ rows, the transposed image [entry][row] already converted to the
+// variant's entry type (fp16 / fp32 / u16 / u8), so that loading a tile is a handful of bulk
+// async copies (TMA, UBLKCP) instead of a strided gather.  One CTA transposes a
+// (64 entries x TQ rows) panel through shared memory: reads are contiguous along the entry
+// axis, writes along the row axis.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace qadc {
+
+template <class Entry>
+__device__ __forceinline__ Entry tile_convert(uint32_t v, uint32_t width, bool high_byte);
+template <>
+__device__ __forceinline__ __half tile_convert<__half>(uint32_t v, uint32_t width, bool hb) {
+    return __uint2half_rn(hb && width == 16 ? v >> 8 : v); // exact: value <= 255 whenever a half entry is used
+}
+template <>
+__device__ __forceinline__ float tile_convert<float>(uint32_t v, uint32_t, bool) { return float(v); }
+template <>
+__device__ __forceinline__ unsigned short tile_convert<unsigned short>(uint32_t v, uint32_t, bool) {
+    return (unsigned short)v;
+}
+template <>
+__device__ __forceinline__ unsigned char tile_convert<unsigned char>(uint32_t v, uint32_t width, bool) {
+    return (unsigned char)(width == 16 ? v >> 8 : v);
+}
+
+static constexpr int PACK_E = 64;
+
+// grid = (ntiles, ceil(E / PACK_E)); block = 256.  rows [tile*TQ, tile*TQ + TQ) clipped to n_rows.
+template <class Entry>
+__global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width, uint32_t E, uint32_t n_rows,
+                                  uint32_t tq, bool high_byte, Entry* __restrict__ out) {
+    extern __shared__ unsigned short panel[]; // [PACK_E][tq + 1]
+    const uint32_t tile = blockIdx.x, e0 = blockIdx.y * PACK_E;
+    const uint32_t ne = min(uint32_t(PACK_E), E - e0);
+    const uint32_t pitch = tq + 1;
+    for (uint32_t u = threadIdx.x; u < tq * PACK_E; u += blockDim.x) {
+        const uint32_t el = u % PACK_E, r = u / PACK_E;
+        const uint32_t row = tile * tq + r;
+        uint32_t v = 0;
+        if (el < ne && row < n_rows) {
+            const size_t gi = size_t(row) * E + e0 + el;
+            v = width == 8 ? uint32_t(reinterpret_cast<const uint8_t*>(qlut)[gi])
+                           : uint32_t(reinterpret_cast<const uint16_t*>(qlut)[gi]);
+        }
+        panel[el * pitch + r] = (unsigned short)v;
+    }
+    __syncthreads();
+    Entry* dst = out + (size_t(tile) * E + e0) * tq;
+    for (uint32_t u = threadIdx.x; u < ne * tq; u += blockDim.x) {
+        const uint32_t r = u % tq, el = u / tq;
+        dst[size_t(el) * tq + r] = tile_convert<Entry>(panel[el * pitch + r], width, high_byte);
+    }
+}
+
+template <class Entry>
+static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq, bool hb,
+                        void* out, cudaStream_t stream) {
+    const uint32_t ntiles = (n_rows + tq - 1) / tq;
+    if (ntiles == 0) return;
+    const dim3 grid(ntiles, (E + PACK_E - 1) / PACK_E);
+    const size_t smem = size_t(PACK_E) * (tq + 1) * sizeof(unsigned short);
+    pack_tiles_kernel<Entry><<<grid, 256, smem, stream>>>(qlut, width, E, n_rows, tq, hb, static_cast<Entry*>(out));
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+size_t tile_entry_bytes(ScanVariant v) {
+    switch (v) {
+    case VAR_F16X8:
+    case VAR_F16X4H: return 2;
+    case VAR_F32X2: return 4;
+    case VAR_U16X1: return 2;
+    case VAR_U8X1: return 1;
+    default: return 4;
+    }
+}
+
+void launch_pack_tiles(ScanVariant v, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
+                       void* out, cudaStream_t stream) {
+    switch (v) {
+    case VAR_F16X8: return launch_pack<__half>(qlut, width, E, n_rows, tq, false, out, stream);
+    case VAR_F16X4H: return launch_pack<__half>(qlut, width, E, n_rows, tq, true, out, stream);
+    case VAR_F32X2: return launch_pack<float>(qlut, width, E, n_rows, tq, false, out, stream);
+    case VAR_U16X1: return launch_pack<unsigned short>(qlut, width, E, n_rows, tq, false, out, stream);
+    case VAR_U8X1: return launch_pack<unsigned char>(qlut, width, E, n_rows, tq, false, out, stream);
+    default: throw Error(QADC_ERR_CONFIG, "pack_tiles: bad variant");
+    }
+}
+
+} // namespace qadc
