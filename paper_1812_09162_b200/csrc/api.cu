@@ -155,8 +155,12 @@ struct qadc_index {
     uint32_t calib_count = 0;
     // ivf
     uint32_t k_cells = 0;
-    DevBuf coarse, coarse_t, list_code_off, list_count_dev, calib_off_dev, calib_count_dev;
-    std::vector<uint64_t> list_code_off_h, list_count_h, list_ids_off_h;
+    DevBuf coarse, coarse_t, list_code_off, list_count_dev;
+    std::vector<uint64_t> list_code_off_h, list_count_h;
+    uint64_t total_codes = 0;
+    uint32_t ivf_round0 = 512; // list positions scanned in the first round (then x seg_growth per round)
+    // ivf workspace
+    DevBuf order, pmin, own_min, qparams, cell_npairs, pair_rank, pair_slot, tile_base, row_query, row_bias, cta_begin;
     // options
     uint32_t cand_cap = 8192;
     uint32_t seg0 = 4096;
@@ -391,6 +395,214 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
     h->stats.kernel_launches = g_launches;
 }
 
+// ------------------------------------------------------------------ IVF search --
+
+static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq, const qadc_search_params& p,
+                              uint32_t* d_ids, float* d_dists, uint32_t* d_counts, uint64_t* d_keys, float* d_map,
+                              cudaStream_t st) {
+    validate_params(p, true);
+    h->stats = qadc_stats{};
+    h->timer.reset();
+    if (nq == 0) return;
+    const DevSpec& ds = h->ds;
+    const uint32_t K = h->k_cells;
+    const uint32_t a = std::min(p.probes, K); // index.hpp:250
+    if (K == 0 || h->total_codes == 0) {
+        fill_empty_results(nq, p.r, d_ids, d_dists, d_counts, d_keys, d_map, st);
+        h->stats.kernel_launches = g_launches;
+        return;
+    }
+    const ScanPlan plan = plan_for(h);
+    h->stats.scan_variant = plan.variant;
+    h->stats.query_tile = plan.tq;
+    const size_t wb = ds.word_width / 8;
+    const uint32_t tq = plan.tq;
+    h->status.ensure(4);
+    h->counters.ensure(16);
+    QADC_CUDA_CHECK(cudaMemsetAsync(h->status.p, 0, 4, st));
+    const int grid = h->num_sms;
+
+    uint32_t cap = h->cand_cap;
+    // query batches bound the float-table and candidate footprints (~2 GB each)
+    const size_t pair_bytes = size_t(a) * ds.E * 4;
+    for (uint32_t q0 = 0; q0 < nq;) {
+        uint32_t nb = uint32_t(std::min<size_t>(nq - q0, std::max<size_t>(1, (size_t(2) << 30) / pair_bytes)));
+        nb = uint32_t(std::min<size_t>(nb, std::max<size_t>(1, (size_t(4) << 30) / (size_t(cap) * 8))));
+        const uint32_t n_pairs = nb * a;
+        const float* dq = d_queries + size_t(q0) * ds.dims;
+        h->order.ensure(size_t(n_pairs) * 4);
+        h->luts.ensure(size_t(n_pairs) * ds.E * 4);
+        h->pmin.ensure(size_t(n_pairs) * ds.m * 4);
+        h->own_min.ensure(size_t(n_pairs) * 4);
+        h->qparams.ensure(size_t(nb) * 16);
+        h->map.ensure(size_t(nb) * 8);
+        h->cell_npairs.ensure(size_t(K) * 4);
+        h->pair_rank.ensure(size_t(n_pairs) * 4);
+        h->pair_slot.ensure(size_t(n_pairs) * 4);
+        h->tile_base.ensure(size_t(K) * 4);
+        QADC_CUDA_CHECK(cudaMemsetAsync(h->cell_npairs.p, 0, size_t(K) * 4, st));
+
+        const size_t t0 = h->timer.mark(st);
+        launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->order.as<uint32_t>(), st);
+        launch_ivf_tables(ds, h->codebook.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(), n_pairs, a,
+                          h->luts.as<float>(), h->pmin.as<float>(), h->own_min.as<float>(), st);
+        launch_ivf_calib(ds, h->codes.as<uint8_t>(), h->list_code_off.as<uint64_t>(), h->list_count_dev.as<uint64_t>(),
+                         h->order.as<uint32_t>(), nb, a, h->luts.as<float>(), h->own_min.as<float>(), p.r, p.t,
+                         h->qparams.as<float>(), h->map.as<float>(), h->cell_npairs.as<uint32_t>(),
+                         h->pair_rank.as<uint32_t>(), st);
+        // rows are grouped by cell: the host lays the cells' tiles out back to back
+        std::vector<uint32_t> npairs(K), tile_base(K);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(npairs.data(), h->cell_npairs.p, size_t(K) * 4, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+        uint32_t ntiles = 0;
+        for (uint32_t c = 0; c < K; ++c) {
+            tile_base[c] = ntiles;
+            ntiles += (npairs[c] + tq - 1) / tq;
+        }
+        const size_t nslots = size_t(ntiles) * tq;
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->tile_base.p, tile_base.data(), size_t(K) * 4, cudaMemcpyHostToDevice, st));
+        h->qlut.ensure(std::max<size_t>(nslots * ds.E * wb, 16));
+        h->row_query.ensure(std::max<size_t>(nslots * 4, 16));
+        h->row_bias.ensure(std::max<size_t>(nslots * 4, 16));
+        h->tile_lut.ensure(std::max<size_t>(nslots * ds.E * tile_entry_bytes(plan.variant), 16));
+        if (nslots) {
+            QADC_CUDA_CHECK(cudaMemsetAsync(h->row_query.p, 0xFF, nslots * 4, st));
+            QADC_CUDA_CHECK(cudaMemsetAsync(h->row_bias.p, 0, nslots * 4, st));
+            QADC_CUDA_CHECK(cudaMemsetAsync(h->qlut.p, 0, nslots * ds.E * wb, st));
+        }
+        launch_ivf_quantize(ds, h->order.as<uint32_t>(), n_pairs, a, h->luts.as<float>(), h->pmin.as<float>(),
+                            h->own_min.as<float>(), h->qparams.as<float>(), h->pair_rank.as<uint32_t>(),
+                            h->tile_base.as<uint32_t>(), tq, h->qlut.p, h->row_query.as<uint32_t>(),
+                            h->row_bias.as<uint32_t>(), h->pair_slot.as<uint32_t>(), st);
+        launch_pack_tiles(plan.variant, h->qlut.p, ds.word_width, ds.E, uint32_t(nslots), tq, h->tile_lut.p, st);
+        h->timer.span(0, t0, h->timer.mark(st));
+
+        h->sel.ensure(nb, p.r, cap);
+        launch_init_select(h->sel.thr_key.as<uint64_t>(), h->sel.cand_count.as<uint32_t>(), h->sel.ntop.as<uint32_t>(),
+                           h->sel.overflow.as<uint32_t>(), nb, st);
+        const size_t s0 = h->timer.mark(st);
+        launch_ivf_seed(ds, h->codes.as<uint8_t>(), h->ids.as<uint32_t>(), h->list_code_off.as<uint64_t>(),
+                        h->list_count_dev.as<uint64_t>(), h->order.as<uint32_t>(), nb, a, h->pair_slot.as<uint32_t>(),
+                        h->qlut.p, h->row_bias.as<uint32_t>(), p.r, std::max<uint32_t>(std::min<uint32_t>(h->seg0, 2048), p.r), 
+                        h->sel.thr_key.as<uint64_t>(), st);
+        h->timer.span(2, s0, h->timer.mark(st));
+
+        // rounds over list positions [lo, hi): the thresholds tighten between rounds
+        uint64_t lo = 0, len = std::max<uint32_t>(h->ivf_round0, 64);
+        uint64_t longest = 0;
+        for (uint32_t c = 0; c < K; ++c)
+            if (npairs[c]) longest = std::max(longest, h->list_count_h[c]);
+        uint64_t pairs_scanned = 0;
+        while (lo < longest) {
+            uint64_t hi = lo + len;
+            if (longest - hi < len) hi = longest; // fold a short tail into this round
+            if (hi >= longest) hi = ~0ull;
+            std::vector<ScanJob> jobs;
+            std::vector<uint64_t> cost;
+            const uint64_t max_chunk = 32768;
+            for (uint32_t c = 0; c < K; ++c) {
+                const uint64_t cnt = h->list_count_h[c];
+                if (!npairs[c] || cnt <= lo) continue;
+                const uint64_t end = std::min(cnt, hi);
+                const uint32_t tiles = (npairs[c] + tq - 1) / tq;
+                for (uint32_t t = 0; t < tiles; ++t)
+                    for (uint64_t b = lo; b < end; b += max_chunk) {
+                        ScanJob j{};
+                        j.code_off = h->list_code_off_h[c] + b;
+                        j.ids_off = j.code_off;
+                        j.n_codes = uint32_t(std::min(max_chunk, end - b));
+                        j.id_base = 0;
+                        j.row_begin = (tile_base[c] + t) * tq;
+                        j.n_rows = std::min(tq, npairs[c] - t * tq);
+                        jobs.push_back(j);
+                        cost.push_back(uint64_t(j.n_codes) + 1024); // + the tile load
+                        pairs_scanned += uint64_t(j.n_codes) * j.n_rows;
+                    }
+            }
+            if (!jobs.empty()) {
+                // cost-balanced contiguous slices of the job list, one per CTA
+                const int g = int(std::min<size_t>(size_t(grid), jobs.size()));
+                uint64_t total = 0;
+                for (uint64_t cst : cost) total += cst;
+                std::vector<uint32_t> begin(size_t(g) + 1, uint32_t(jobs.size()));
+                uint64_t acc = 0;
+                int cta = 0;
+                begin[0] = 0;
+                for (size_t j = 0; j < jobs.size(); ++j) {
+                    while (cta + 1 < g && acc >= total * uint64_t(cta + 1) / uint64_t(g)) begin[++cta] = uint32_t(j);
+                    acc += cost[j];
+                }
+                while (cta + 1 < g) begin[++cta] = uint32_t(jobs.size());
+                begin[g] = uint32_t(jobs.size());
+                h->jobs.ensure(jobs.size() * sizeof(ScanJob));
+                h->cta_begin.ensure((size_t(g) + 1) * 4);
+                QADC_CUDA_CHECK(cudaMemcpyAsync(h->jobs.p, jobs.data(), jobs.size() * sizeof(ScanJob), cudaMemcpyHostToDevice, st));
+                QADC_CUDA_CHECK(cudaMemcpyAsync(h->cta_begin.p, begin.data(), (size_t(g) + 1) * 4, cudaMemcpyHostToDevice, st));
+                ScanArgs sa{};
+                sa.codes = h->codes.as<uint8_t>();
+                sa.ids = h->ids.as<uint32_t>();
+                sa.qlut = h->qlut.p;
+                sa.tile_lut = h->tile_lut.p;
+                sa.row_query = h->row_query.as<uint32_t>();
+                sa.row_bias = h->row_bias.as<uint32_t>();
+                sa.jobs = h->jobs.as<ScanJob>();
+                sa.n_jobs = uint32_t(jobs.size());
+                sa.cta_begin = h->cta_begin.as<uint32_t>();
+                sa.thr_key = h->sel.thr_key.as<uint64_t>();
+                sa.cand = h->sel.cand.as<uint64_t>();
+                sa.cand_count = h->sel.cand_count.as<uint32_t>();
+                sa.cap = cap;
+                sa.overflow = h->sel.overflow.as<uint32_t>();
+                sa.counters = h->counters.as<unsigned long long>();
+                const size_t e0 = h->timer.mark(st);
+                launch_scan(plan, ds, sa, g, st);
+                const size_t e1 = h->timer.mark(st);
+                launch_tighten(h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad,
+                               h->sel.cand.as<uint64_t>(), h->sel.cand_count.as<uint32_t>(), cap,
+                               h->sel.thr_key.as<uint64_t>(), nb, p.r, st);
+                const size_t e2 = h->timer.mark(st);
+                h->timer.span(1, e0, e1, jobs.size());
+                h->timer.span(2, e1, e2);
+                h->stats.scan_launches += 1;
+                h->stats.segments += 1;
+                QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // job vectors go out of scope
+            }
+            if (hi == ~0ull) break;
+            lo = hi;
+            len *= std::max<uint32_t>(h->seg_growth, 2);
+        }
+        std::vector<uint32_t> ov(nb);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(ov.data(), h->sel.overflow.p, size_t(nb) * 4, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+        bool overflowed = false;
+        for (uint32_t v : ov) overflowed |= v != 0;
+        if (overflowed) {
+            if (uint64_t(cap) >= h->total_codes + p.r) throw Error(QADC_ERR_CUDA, "internal: candidate overflow at full capacity");
+            cap = uint32_t(std::min<uint64_t>(uint64_t(cap) * 8, h->total_codes + p.r));
+            h->stats.overflow_retries += 1;
+            continue;
+        }
+        h->stats.pairs_scanned += pairs_scanned;
+        const size_t f0 = h->timer.mark(st);
+        launch_finalize(h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad, 1, nb, p.r, h->map.as<float>(),
+                        p.flags, ds.qmax, d_ids ? d_ids + size_t(q0) * p.r : nullptr,
+                        d_dists ? d_dists + size_t(q0) * p.r : nullptr, d_counts ? d_counts + q0 : nullptr,
+                        d_keys ? d_keys + size_t(q0) * p.r : nullptr, st);
+        h->timer.span(2, f0, h->timer.mark(st));
+        if (d_map)
+            QADC_CUDA_CHECK(cudaMemcpyAsync(d_map + size_t(q0) * 2, h->map.p, size_t(nb) * 8, cudaMemcpyDeviceToDevice, st));
+        q0 += nb;
+        cap = h->cand_cap;
+    }
+    check_status(h, st);
+    float ms[3] = {0.f, 0.f, 0.f};
+    h->timer.collect(ms);
+    h->stats.ms_lut = ms[0];
+    h->stats.ms_scan = ms[1];
+    h->stats.ms_select = ms[2];
+    h->stats.kernel_launches = g_launches;
+}
+
 static void upload_list(qadc_index* h, const qadc_spec& s, const DevSpec& ds, const uint8_t* packed, uint64_t count,
                         DevBuf& out, uint64_t& padded, cudaStream_t st) {
     padded = (count + CODE_PAD - 1) / CODE_PAD * CODE_PAD + CODE_PAD;
@@ -493,7 +705,7 @@ int qadc_search_batch_device(qadc_index* h, const float* d_queries, uint32_t nq,
         if (h->kind == 0)
             flat_search_device(h, d_queries, nq, *params, d_out_ids, d_out_dists, d_out_counts, d_out_keys, d_out_map, st);
         else
-            throw Error(QADC_ERR_CONFIG, "ivf search: not built yet");
+            ivf_search_device(h, d_queries, nq, *params, d_out_ids, d_out_dists, d_out_counts, d_out_keys, d_out_map, st);
     });
 }
 
@@ -517,7 +729,8 @@ int qadc_search_batch(qadc_index* h, const float* queries, uint32_t nq, const qa
             flat_search_device(h, h->queries.as<float>(), nq, *params, h->out_ids.as<uint32_t>(), h->out_dists.as<float>(),
                                h->out_counts.as<uint32_t>(), nullptr, nullptr, st);
         else
-            throw Error(QADC_ERR_CONFIG, "ivf search: not built yet");
+            ivf_search_device(h, h->queries.as<float>(), nq, *params, h->out_ids.as<uint32_t>(), h->out_dists.as<float>(),
+                              h->out_counts.as<uint32_t>(), nullptr, nullptr, st);
         (void)before;
         QADC_CUDA_CHECK(cudaMemcpyAsync(out_ids, h->out_ids.p, nr * 4, cudaMemcpyDeviceToHost, st));
         QADC_CUDA_CHECK(cudaMemcpyAsync(out_dists, h->out_dists.p, nr * 4, cudaMemcpyDeviceToHost, st));
@@ -762,20 +975,103 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
         else if (n == "force_variant") h->force_variant = int(value);
         else if (n == "cif") h->cif = int(value);
+        else if (n == "ivf_round0") h->ivf_round0 = uint32_t(std::max<int64_t>(value, 64));
         else throw Error(QADC_ERR_CONFIG, "set_option: unknown option " + n);
     });
 }
 
-int qadc_ivf_open(const qadc_spec*, const float*, const float*, uint32_t, const uint8_t*, const uint64_t*,
-                  const uint64_t*, const uint64_t*, const uint32_t*, const uint8_t*, const uint64_t*, const uint64_t*,
-                  int, qadc_index**) {
-    g_error = "ivf: not built yet";
-    return QADC_ERR_CONFIG;
+int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
+                  const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
+                  const uint64_t* list_count, const uint32_t* ids, const uint8_t* calib_packed,
+                  const uint64_t* calib_byte_off, const uint64_t* calib_count, int device, qadc_index** out) {
+    return guarded([&] {
+        if (!spec || !codebook || !out || (k_cells && (!coarse || !list_byte_off || !list_id_off || !list_count)))
+            throw Error(QADC_ERR_INPUT, "null argument");
+        if (calib_packed || calib_byte_off || calib_count)
+            throw Error(QADC_ERR_CONFIG, "ivf: sharded lists with replicated calibration heads are not supported yet");
+        validate_spec(*spec);
+        set_device(device);
+        std::unique_ptr<qadc_index> h(new qadc_index);
+        h->kind = 1;
+        h->device = device;
+        h->spec = *spec;
+        h->ds = make_dev_spec(*spec, spec->groups);
+        h->k_cells = k_cells;
+        if (h->ds.code_stride > 32) throw Error(QADC_ERR_CONFIG, "codes wider than 256 bits are not supported");
+        QADC_CUDA_CHECK(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device));
+        QADC_CUDA_CHECK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        cudaStream_t st = h->stream;
+        for (uint32_t i = 0; i < spec->cb_floats; ++i)
+            if (!(codebook[i] - codebook[i] == 0.0f)) throw Error(QADC_ERR_CORRUPTION, "codebook: non-finite centroid component");
+        h->codebook.ensure(size_t(spec->cb_floats) * 4);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->codebook.p, codebook, size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice, st));
+        const uint32_t d = spec->dims;
+        // coarse centroids: row-major for the residuals, transposed [dims][K] for the probe kernel
+        std::vector<float> ct(size_t(k_cells) * d);
+        for (uint32_t c = 0; c < k_cells; ++c)
+            for (uint32_t j = 0; j < d; ++j) ct[size_t(j) * k_cells + c] = coarse[size_t(c) * d + j];
+        h->coarse.ensure(std::max<size_t>(ct.size() * 4, 16));
+        h->coarse_t.ensure(std::max<size_t>(ct.size() * 4, 16));
+        if (k_cells) {
+            QADC_CUDA_CHECK(cudaMemcpyAsync(h->coarse.p, coarse, ct.size() * 4, cudaMemcpyHostToDevice, st));
+            QADC_CUDA_CHECK(cudaMemcpyAsync(h->coarse_t.p, ct.data(), ct.size() * 4, cudaMemcpyHostToDevice, st));
+        }
+        // every list starts on a 16-code boundary of the device array (bulk copies need 16-byte alignment)
+        const uint64_t LIST_ALIGN = 16;
+        h->list_code_off_h.resize(k_cells);
+        h->list_count_h.assign(list_count, list_count + k_cells);
+        uint64_t run = 0, packed_total = 0, n_ids = 0;
+        for (uint32_t c = 0; c < k_cells; ++c) {
+            h->list_code_off_h[c] = run;
+            run += (list_count[c] + LIST_ALIGN - 1) / LIST_ALIGN * LIST_ALIGN;
+            packed_total = std::max<uint64_t>(packed_total, list_byte_off[c] + qadc_packed_bytes(spec, list_count[c]));
+            n_ids += list_count[c];
+        }
+        h->total_codes = n_ids;
+        if (n_ids && (!packed || !ids)) throw Error(QADC_ERR_INPUT, "null argument");
+        const uint64_t total_padded = run + CODE_PAD;
+        h->count_padded = total_padded;
+        h->codes.ensure(size_t(total_padded) * h->ds.code_stride);
+        h->list_code_off.ensure(std::max<size_t>(size_t(k_cells) * 8, 16));
+        h->list_count_dev.ensure(std::max<size_t>(size_t(k_cells) * 8, 16));
+        DevBuf tmp, boff;
+        tmp.ensure(std::max<uint64_t>(packed_total, 16));
+        boff.ensure(std::max<size_t>(size_t(k_cells) * 8, 16));
+        if (k_cells) {
+            QADC_CUDA_CHECK(cudaMemcpyAsync(h->list_code_off.p, h->list_code_off_h.data(), size_t(k_cells) * 8, cudaMemcpyHostToDevice, st));
+            QADC_CUDA_CHECK(cudaMemcpyAsync(h->list_count_dev.p, list_count, size_t(k_cells) * 8, cudaMemcpyHostToDevice, st));
+            QADC_CUDA_CHECK(cudaMemcpyAsync(boff.p, list_byte_off, size_t(k_cells) * 8, cudaMemcpyHostToDevice, st));
+        }
+        if (packed_total) QADC_CUDA_CHECK(cudaMemcpyAsync(tmp.p, packed, packed_total, cudaMemcpyHostToDevice, st));
+        if (k_cells)
+            launch_ivf_relayout(*spec, h->ds, tmp.as<uint8_t>(), boff.as<uint64_t>(), h->list_code_off.as<uint64_t>(),
+                                h->list_count_dev.as<uint64_t>(), k_cells, total_padded, h->codes.as<uint8_t>(), st);
+        // ids ride in the same index space as the device codes
+        std::vector<uint32_t> ids_padded(total_padded, 0xFFFFFFFFu);
+        for (uint32_t c = 0; c < k_cells; ++c)
+            std::copy(ids + list_id_off[c], ids + list_id_off[c] + list_count[c], ids_padded.begin() + h->list_code_off_h[c]);
+        h->ids.ensure(size_t(total_padded) * 4);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->ids.p, ids_padded.data(), size_t(total_padded) * 4, cudaMemcpyHostToDevice, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+        *out = h.release();
+    });
 }
 
-int qadc_ivf_probe_order(qadc_index*, const float*, uint32_t, uint32_t, uint32_t*) {
-    g_error = "ivf: not built yet";
-    return QADC_ERR_CONFIG;
+int qadc_ivf_probe_order(qadc_index* h, const float* queries, uint32_t nq, uint32_t a, uint32_t* order) {
+    return guarded([&] {
+        if (!h || h->kind != 1 || (nq && (!queries || !order))) throw Error(QADC_ERR_INPUT, "probe_order: bad arguments");
+        set_device(h->device);
+        a = std::min(a, h->k_cells);
+        if (nq == 0 || a == 0) return;
+        cudaStream_t st = h->stream;
+        h->queries.ensure(size_t(nq) * h->ds.dims * 4);
+        h->order.ensure(size_t(nq) * a * 4);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(h->queries.p, queries, size_t(nq) * h->ds.dims * 4, cudaMemcpyHostToDevice, st));
+        launch_ivf_probe(h->queries.as<float>(), h->coarse_t.as<float>(), h->ds.dims, h->k_cells, nq, a,
+                         h->order.as<uint32_t>(), st);
+        QADC_CUDA_CHECK(cudaMemcpyAsync(order, h->order.p, size_t(nq) * a * 4, cudaMemcpyDeviceToHost, st));
+        QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
 }
 
 } // extern "C"

@@ -75,6 +75,7 @@ struct ScanArgs {
     const uint32_t* row_bias;  // row -> acc_init (nullptr: 0)
     const ScanJob* jobs;
     uint32_t n_jobs;
+    const uint32_t* cta_begin; // optional [grid + 1]: job slice of every CTA (cost-balanced); nullptr = equal counts
     uint64_t* thr_key;         // [nq] current R-th smallest key (KEY_INF while fewer than R)
     uint64_t* cand;            // [nq][cap]
     uint32_t* cand_count;      // [nq]
@@ -131,6 +132,28 @@ void launch_pack_tiles(ScanVariant v, const void* qlut, uint32_t width, uint32_t
 void launch_seed_topk(const DevSpec& ds, const uint8_t* d_codes, uint32_t n_head, uint32_t id_base,
                       const uint32_t* d_ids, const void* d_qlut, const uint32_t* d_row_bias, uint32_t nq, uint32_t r,
                       uint64_t* top, uint32_t* ntop, uint32_t kpad, uint64_t* thr_key, cudaStream_t stream);
+
+// ---- IVF stages (ivf.cu) ----
+void launch_ivf_relayout(const qadc_spec& s, const DevSpec& ds, const uint8_t* d_packed, const uint64_t* d_byte_off,
+                         const uint64_t* d_code_off, const uint64_t* d_count, uint32_t k_cells, uint64_t total_padded,
+                         uint8_t* d_codes, cudaStream_t stream);
+void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t dims, uint32_t k_cells, uint32_t nq,
+                      uint32_t a, uint32_t* d_order, cudaStream_t stream);
+void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* d_queries, const float* d_coarse,
+                       const uint32_t* d_order, uint32_t n_pairs, uint32_t a, float* d_luts, float* d_pmin,
+                       float* d_own_min, cudaStream_t stream);
+void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_codes, const uint64_t* d_list_code_off,
+                      const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq, uint32_t a,
+                      const float* d_luts, const float* d_own_min, uint32_t r, uint32_t t, float* d_qparams,
+                      float* d_map, uint32_t* d_cell_npairs, uint32_t* d_pair_rank, cudaStream_t stream);
+void launch_ivf_quantize(const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a, const float* d_luts,
+                         const float* d_pmin, const float* d_own_min, const float* d_qparams,
+                         const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base, uint32_t tq, void* d_qluts,
+                         uint32_t* d_row_query, uint32_t* d_row_bias, uint32_t* d_pair_slot, cudaStream_t stream);
+void launch_ivf_seed(const DevSpec& ds, const uint8_t* d_codes, const uint32_t* d_ids, const uint64_t* d_list_code_off,
+                     const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq, uint32_t a,
+                     const uint32_t* d_pair_slot, const void* d_qluts, const uint32_t* d_row_bias, uint32_t r,
+                     uint32_t head, uint64_t* d_thr_key, cudaStream_t stream);
 
 // ---- layout (layout.cu) ----
 // reference PackedList bytes (device copy) -> linear device layout, padded with 0xFF codes up to n_padded

@@ -1,2 +1,404 @@
-// ivf.cu -- placeholder translation unit; the IVF path lands here.
-#include "common.cuh"
+// ivf.cu -- device stages of IvfIndex::search (index.hpp:276-341) in front of the shared scan kernel.
+//
+//   probe_order      index.hpp:247-265  K serial fp32 squared distances, first a by (dist, cell)
+//   residual tables  index.hpp:282-288  one compute_tables per (query, probed cell)
+//   shared map       index.hpp:299-316  d_min_global = min over probed cells of min_total();
+//                                       prefix over cells in probe order until t distances;
+//                                       d_max = r_eff-th smallest; delta = (d_max - d_min_global)/q_max
+//   per cell         index.hpp:319-329  quantize against the SHARED bounds, bias =
+//                                       floor((own_d_min - d_min_global)/delta) in fp32, scan with ids
+//
+// The CPU loops query -> cell -> code.  On the GPU the loop is inverted: all (query, cell)
+// pairs that probe the same cell are grouped into tiles of LUT rows, so a cell's codes are
+// streamed once per tile and reused by every query probing it -- the same scan kernel as the
+// flat index, with per-row bias, a row -> query map and explicit ids.
+// Every float that feeds the quantizer follows the reference's operation order with explicitly
+// rounded fp32 ops (see lut.cu); the file is compiled with --fmad=false.
+#include "select_common.cuh"
+
+namespace qadc {
+
+// ------------------------------------------------------------------ list layout --
+
+// One thread per (padded) device code slot: find its list by binary search over the padded
+// offsets and gather its words from the list's transposed blocks (layout.hpp:105-125).
+__global__ void ivf_relayout_kernel(const uint8_t* __restrict__ packed, const uint64_t* __restrict__ byte_off,
+                                    const uint64_t* __restrict__ code_off, const uint64_t* __restrict__ count,
+                                    uint32_t k_cells, uint64_t total_padded, uint32_t rows, uint32_t wb,
+                                    uint32_t block_len, uint32_t stride, uint8_t* __restrict__ out) {
+    const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+    if (i >= total_padded) return;
+    uint32_t lo = 0, hi = k_cells; // last list with code_off <= i
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (code_off[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    const uint64_t p = i - code_off[lo];
+    uint8_t* dst = out + i * stride;
+    if (p >= count[lo]) {
+        for (uint32_t b = 0; b < stride; ++b) dst[b] = 0xFF;
+        return;
+    }
+    const uint64_t bb = uint64_t(rows) * block_len * wb;
+    const uint8_t* blk = packed + byte_off[lo] + (p / block_len) * bb;
+    const uint32_t s = uint32_t(p % block_len);
+    for (uint32_t r = 0; r < rows; ++r)
+        for (uint32_t b = 0; b < wb; ++b) dst[r * wb + b] = blk[(uint64_t(r) * block_len + s) * wb + b];
+    for (uint32_t b = rows * wb; b < stride; ++b) dst[b] = 0xFF;
+}
+
+void launch_ivf_relayout(const qadc_spec& s, const DevSpec& ds, const uint8_t* d_packed, const uint64_t* d_byte_off,
+                         const uint64_t* d_code_off, const uint64_t* d_count, uint32_t k_cells, uint64_t total_padded,
+                         uint8_t* d_codes, cudaStream_t stream) {
+    if (total_padded == 0) return;
+    ivf_relayout_kernel<<<unsigned((total_padded + 255) / 256), 256, 0, stream>>>(
+        d_packed, d_byte_off, d_code_off, d_count, k_cells, total_padded, s.groups, s.word_width / 8, s.block_len,
+        ds.code_stride, d_codes);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ probe order --
+
+// One CTA (256 threads) per query.  coarse_t is the centroid matrix transposed to [dims][K] so
+// that lanes (= cells) read contiguously while each thread walks the dims serially.
+// dynamic smem: K keys (u64) + dims floats.
+__global__ void __launch_bounds__(256)
+ivf_probe_kernel(const float* __restrict__ queries, const float* __restrict__ coarse_t, uint32_t dims,
+                 uint32_t k_cells, uint32_t a, uint32_t* __restrict__ order) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(sm_raw);
+    float* q = reinterpret_cast<float*>(keys + k_cells);
+    uint64_t* best = reinterpret_cast<uint64_t*>(q + ((dims + 1) & ~1u)); // a keys, then sorted in place
+    __shared__ SelectScratch sc;
+    const uint32_t qi = blockIdx.x;
+    for (uint32_t d = threadIdx.x; d < dims; d += blockDim.x) q[d] = queries[size_t(qi) * dims + d];
+    __syncthreads();
+    for (uint32_t c = threadIdx.x; c < k_cells; c += blockDim.x) {
+        float acc = 0.0f;
+        for (uint32_t j = 0; j < dims; ++j) {
+            const float diff = __fsub_rn(q[j], coarse_t[size_t(j) * k_cells + c]);
+            acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+        }
+        keys[c] = (uint64_t(__float_as_uint(acc)) << 32) | c; // acc >= +0: float order == bit order
+    }
+    __syncthreads();
+    auto key_at = [&](uint32_t i) -> uint64_t { return keys[i]; };
+    uint32_t pow2 = 1;
+    while (pow2 < a) pow2 <<= 1;
+    if (a < k_cells) {
+        uint32_t eq;
+        const uint64_t kth = block_select_kth(key_at, k_cells, a, 64, &sc, &eq);
+        block_keep_smallest(key_at, k_cells, a, kth, eq, &sc, best);
+    } else {
+        for (uint32_t i = threadIdx.x; i < k_cells; i += blockDim.x) best[i] = keys[i];
+    }
+    for (uint32_t i = a + threadIdx.x; i < pow2; i += blockDim.x) best[i] = KEY_INF;
+    __syncthreads();
+    for (uint32_t size = 2; size <= pow2; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < pow2 / 2; i += blockDim.x) {
+                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t x = best[lo], y = best[hi];
+                if ((x > y) == up) {
+                    best[lo] = y;
+                    best[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = threadIdx.x; i < a; i += blockDim.x) order[size_t(qi) * a + i] = uint32_t(best[i]);
+}
+
+void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t dims, uint32_t k_cells, uint32_t nq,
+                      uint32_t a, uint32_t* d_order, cudaStream_t stream) {
+    if (nq == 0 || a == 0) return;
+    uint32_t pow2 = 1;
+    while (pow2 < a) pow2 <<= 1;
+    const size_t smem = size_t(k_cells) * 8 + size_t((dims + 1) & ~1u) * 4 + size_t(pow2) * 8;
+    if (smem > 200 * 1024)
+        throw Error(QADC_ERR_CONFIG, "ivf probe: coarse quantizer too large for the shared-memory selection "
+                                     "(K*8 + probes*8 bytes must fit 200 KB)");
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ivf_probe_kernel<<<nq, 256, smem, stream>>>(d_queries, d_coarse_t, dims, k_cells, a, d_order);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------- residual tables --
+
+// One CTA per (query, probe) pair: residual = q - centroid (index.hpp:286), compute_tables,
+// per-table minima and their table-order sum (DistanceTables::min_total, distance.hpp:28-32).
+__global__ void __launch_bounds__(256)
+ivf_tables_kernel(DevSpec ds, const float* __restrict__ codebook, const float* __restrict__ queries,
+                  const float* __restrict__ coarse, const uint32_t* __restrict__ order, uint32_t a,
+                  float* __restrict__ luts, float* __restrict__ pmin_out, float* __restrict__ own_min) {
+    extern __shared__ float smf[];
+    float* res = smf;
+    float* lut = res + ds.dims;
+    float* pmin = lut + ds.E;
+    const uint32_t pair = blockIdx.x;
+    const uint32_t qi = pair / a;
+    const uint32_t cell = order[pair];
+    for (uint32_t d = threadIdx.x; d < ds.dims; d += blockDim.x)
+        res[d] = __fsub_rn(queries[size_t(qi) * ds.dims + d], coarse[size_t(cell) * ds.dims + d]);
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x) {
+        uint32_t j = 0;
+        while (j + 1 < ds.m && ds.ent_off[j + 1] <= e) ++j;
+        const uint32_t dsub = ds.dim_alloc[j];
+        const float* c = codebook + ds.cb_off[j] + size_t(e - ds.ent_off[j]) * dsub;
+        const float* qq = res + ds.dim_off[j];
+        float acc = 0.0f;
+        for (uint32_t t = 0; t < dsub; ++t) {
+            const float d = __fsub_rn(qq[t], c[t]);
+            acc = __fadd_rn(acc, __fmul_rn(d, d));
+        }
+        lut[e] = acc;
+        luts[size_t(pair) * ds.E + e] = acc;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < ds.m; j += blockDim.x) {
+        float mn = __int_as_float(0x7f800000);
+        const float* t = lut + ds.ent_off[j];
+        for (uint32_t i = 0; i < (1u << ds.bits[j]); ++i) mn = (t[i] < mn) ? t[i] : mn;
+        pmin[j] = mn;
+        pmin_out[size_t(pair) * ds.m + j] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.0f;
+        for (uint32_t j = 0; j < ds.m; ++j) s = __fadd_rn(s, pmin[j]);
+        own_min[pair] = s;
+    }
+}
+
+void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* d_queries, const float* d_coarse,
+                       const uint32_t* d_order, uint32_t n_pairs, uint32_t a, float* d_luts, float* d_pmin,
+                       float* d_own_min, cudaStream_t stream) {
+    if (n_pairs == 0) return;
+    const size_t smem = sizeof(float) * (size_t(ds.dims) + ds.E + ds.m);
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ivf_tables_kernel<<<n_pairs, 256, smem, stream>>>(ds, d_codebook, d_queries, d_coarse, d_order, a, d_luts, d_pmin,
+                                                      d_own_min);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------- calibration --
+
+// One CTA per query.  Also counts the (query, cell) pairs per cell for the row grouping and
+// records each pair's rank inside its cell.  dynamic smem: t floats + a uint32 (prefix starts).
+// qparams[q] = {d_min_global, d_max, delta, n_prefix}
+__global__ void __launch_bounds__(256)
+ivf_calib_kernel(DevSpec ds, const uint8_t* __restrict__ codes, const uint64_t* __restrict__ list_code_off,
+                 const uint64_t* __restrict__ list_count, const uint32_t* __restrict__ order, uint32_t a,
+                 const float* __restrict__ luts, const float* __restrict__ own_min, uint32_t r, uint32_t t,
+                 float* __restrict__ qparams, float* __restrict__ map, uint32_t* __restrict__ cell_npairs,
+                 uint32_t* __restrict__ pair_rank) {
+    extern __shared__ float smf[];
+    float* prefix = smf;
+    uint32_t* start = reinterpret_cast<uint32_t*>(prefix + t); // a + 1 entries
+    __shared__ float s_dmin, s_dmax;
+    __shared__ uint32_t s_np;
+    const uint32_t qi = blockIdx.x;
+    const uint32_t* ord = order + size_t(qi) * a;
+    if (threadIdx.x == 0) {
+        float dmin = __int_as_float(0x7f800000); // index.hpp:301-302
+        uint32_t taken = 0;
+        for (uint32_t i = 0; i < a; ++i) {
+            const float mt = own_min[size_t(qi) * a + i];
+            dmin = (mt < dmin) ? mt : dmin;
+            start[i] = taken;
+            const uint64_t cnt = list_count[ord[i]];
+            taken += uint32_t(min(cnt, uint64_t(t - taken))); // index.hpp:305-306
+        }
+        start[a] = taken;
+        s_dmin = dmin;
+        s_np = taken;
+    }
+    // row grouping: every probed, non-empty cell gets this pair as one LUT row
+    for (uint32_t i = threadIdx.x; i < a; i += blockDim.x) {
+        const uint32_t cell = ord[i];
+        pair_rank[size_t(qi) * a + i] = list_count[cell] ? atomicAdd(&cell_npairs[cell], 1u) : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    const uint32_t np = s_np;
+    for (uint32_t p = threadIdx.x; p < np; p += blockDim.x) {
+        uint32_t i = 0;
+        while (start[i + 1] <= p) ++i; // the probe this prefix position falls into
+        const uint8_t* code = codes + (list_code_off[ord[i]] + (p - start[i])) * ds.code_stride;
+        const float* lut = luts + (size_t(qi) * a + i) * ds.E;
+        float acc = 0.0f;
+        for (uint32_t j = 0; j < ds.m; ++j) acc = __fadd_rn(acc, lut[ds.ent_off[j] + code_field(ds, code, j)]);
+        prefix[p] = acc;
+    }
+    __syncthreads();
+    float d_max = 0.0f;
+    if (np) {
+        const uint32_t r_eff = min(r, np); // index.hpp:308
+        for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
+            const float v = prefix[i];
+            uint32_t less = 0, leq = 0;
+            for (uint32_t k = 0; k < np; ++k) {
+                less += prefix[k] < v;
+                leq += prefix[k] <= v;
+            }
+            if (less <= r_eff - 1 && r_eff - 1 < leq) s_dmax = v;
+        }
+        __syncthreads();
+        d_max = s_dmax;
+    }
+    if (threadIdx.x == 0) {
+        float* o = qparams + size_t(qi) * 4;
+        o[0] = s_dmin;
+        o[1] = d_max;
+        o[2] = np ? __fdiv_rn(__fsub_rn(d_max, s_dmin), float(ds.qmax)) : 0.0f; // index.hpp:316
+        o[3] = __uint_as_float(np);
+        map[size_t(qi) * 2 + 0] = o[2];   // unquantize: float(sum) * delta + d_min_global (index.hpp:337)
+        map[size_t(qi) * 2 + 1] = s_dmin;
+    }
+}
+
+void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_codes, const uint64_t* d_list_code_off,
+                      const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq, uint32_t a,
+                      const float* d_luts, const float* d_own_min, uint32_t r, uint32_t t, float* d_qparams,
+                      float* d_map, uint32_t* d_cell_npairs, uint32_t* d_pair_rank, cudaStream_t stream) {
+    if (nq == 0) return;
+    const size_t smem = size_t(t) * 4 + size_t(a + 1) * 4;
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_calib_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ivf_calib_kernel<<<nq, 256, smem, stream>>>(ds, d_codes, d_list_code_off, d_list_count, d_order, a, d_luts,
+                                                d_own_min, r, t, d_qparams, d_map, d_cell_npairs, d_pair_rank);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ quantization --
+
+__device__ __forceinline__ uint32_t ivf_quantize_entry(float p, float pmin, float d_min, float d_max, float delta,
+                                                       uint32_t qmax) { // distance.hpp:117-124
+    if (delta <= 0.0f) return p == pmin ? 0u : qmax;
+    if (__fsub_rn(p, pmin) >= __fsub_rn(d_max, d_min)) return qmax;
+    const double q = floor(__ddiv_rn(__dsub_rn(double(p), double(pmin)), double(delta)));
+    if (q >= double(qmax)) return qmax;
+    return uint32_t(q);
+}
+
+// One CTA per (query, probe) pair with a non-empty list: quantize its tables against the query's
+// shared bounds into LUT row `slot`, and derive the row's bias (index.hpp:322-328).
+__global__ void __launch_bounds__(256)
+ivf_quantize_kernel(DevSpec ds, const uint32_t* __restrict__ order, uint32_t a, const float* __restrict__ luts,
+                    const float* __restrict__ pmin, const float* __restrict__ own_min,
+                    const float* __restrict__ qparams, const uint32_t* __restrict__ pair_rank,
+                    const uint32_t* __restrict__ cell_tile_base, uint32_t tq, void* __restrict__ qluts,
+                    uint32_t* __restrict__ row_query, uint32_t* __restrict__ row_bias,
+                    uint32_t* __restrict__ pair_slot) {
+    const uint32_t pair = blockIdx.x;
+    const uint32_t rank = pair_rank[pair];
+    if (rank == 0xFFFFFFFFu) { // empty list: skipped by the search loop (index.hpp:321)
+        if (threadIdx.x == 0) pair_slot[pair] = 0xFFFFFFFFu;
+        return;
+    }
+    const uint32_t qi = pair / a;
+    const uint32_t slot = cell_tile_base[order[pair]] * tq + rank;
+    const float d_min = qparams[size_t(qi) * 4 + 0], d_max = qparams[size_t(qi) * 4 + 1];
+    const float delta = qparams[size_t(qi) * 4 + 2];
+    const float* lut = luts + size_t(pair) * ds.E;
+    for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x) {
+        uint32_t j = 0;
+        while (j + 1 < ds.m && ds.ent_off[j + 1] <= e) ++j;
+        const uint32_t qv = ivf_quantize_entry(lut[e], pmin[size_t(pair) * ds.m + j], d_min, d_max, delta, ds.qmax);
+        if (ds.word_width == 8) reinterpret_cast<uint8_t*>(qluts)[size_t(slot) * ds.E + e] = uint8_t(qv);
+        else reinterpret_cast<uint16_t*>(qluts)[size_t(slot) * ds.E + e] = uint16_t(qv);
+    }
+    if (threadIdx.x == 0) {
+        uint32_t bias = 0;
+        if (delta > 0.0f) { // float math, index.hpp:325-327
+            const float b = floorf(__fdiv_rn(__fsub_rn(own_min[pair], d_min), delta));
+            bias = b >= float(ds.qmax) ? ds.qmax : uint32_t(b);
+        }
+        row_query[slot] = qi;
+        row_bias[slot] = bias;
+        pair_slot[pair] = slot;
+    }
+}
+
+void launch_ivf_quantize(const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a, const float* d_luts,
+                         const float* d_pmin, const float* d_own_min, const float* d_qparams,
+                         const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base, uint32_t tq, void* d_qluts,
+                         uint32_t* d_row_query, uint32_t* d_row_bias, uint32_t* d_pair_slot, cudaStream_t stream) {
+    if (n_pairs == 0) return;
+    ivf_quantize_kernel<<<n_pairs, 256, 0, stream>>>(ds, d_order, a, d_luts, d_pmin, d_own_min, d_qparams, d_pair_rank,
+                                                     d_cell_tile_base, tq, d_qluts, d_row_query, d_row_bias, d_pair_slot);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------- threshold seeding --
+
+// One CTA per query: exact quantized sums of the head of the first probed list that holds at
+// least r codes; thr_key = (r-th smallest key) + 1.  The codes are real candidates that the
+// streaming scan will meet again, so this is a valid (exclusive) upper bound on the final
+// r-th key; nothing is kept, only the bound.  dynamic smem: head keys + table (u16).
+__global__ void __launch_bounds__(256)
+ivf_seed_kernel(DevSpec ds, const uint8_t* __restrict__ codes, const uint32_t* __restrict__ ids,
+                const uint64_t* __restrict__ list_code_off, const uint64_t* __restrict__ list_count,
+                const uint32_t* __restrict__ order, uint32_t a, const uint32_t* __restrict__ pair_slot,
+                const void* __restrict__ qluts, const uint32_t* __restrict__ row_bias, uint32_t r, uint32_t head,
+                uint64_t* __restrict__ thr_key) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(sm_raw);
+    uint16_t* table = reinterpret_cast<uint16_t*>(keys + head);
+    __shared__ SelectScratch sc;
+    __shared__ uint32_t s_probe;
+    const uint32_t qi = blockIdx.x;
+    if (threadIdx.x == 0) {
+        uint32_t pick = 0xFFFFFFFFu;
+        for (uint32_t i = 0; i < a; ++i)
+            if (list_count[order[size_t(qi) * a + i]] >= r) {
+                pick = i;
+                break;
+            }
+        s_probe = pick;
+    }
+    __syncthreads();
+    if (s_probe == 0xFFFFFFFFu) return; // no list with r codes: the scan starts unbounded
+    const uint32_t pair = qi * a + s_probe;
+    const uint32_t cell = order[pair];
+    const uint32_t slot = pair_slot[pair];
+    const uint32_t n = uint32_t(min(list_count[cell], uint64_t(head)));
+    for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x)
+        table[e] = ds.word_width == 8 ? uint16_t(reinterpret_cast<const uint8_t*>(qluts)[size_t(slot) * ds.E + e])
+                                      : reinterpret_cast<const uint16_t*>(qluts)[size_t(slot) * ds.E + e];
+    __syncthreads();
+    const uint32_t bias = min(row_bias[slot], ds.qmax);
+    const uint64_t base = list_code_off[cell];
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint8_t* code = codes + (base + i) * ds.code_stride;
+        uint32_t acc = bias;
+        for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + code_field(ds, code, j)];
+        keys[i] = make_key(min(acc, ds.qmax), ids[base + i]);
+    }
+    __syncthreads();
+    auto key_at = [&](uint32_t i) -> uint64_t { return keys[i]; };
+    uint32_t eq;
+    const uint64_t kth = block_select_kth(key_at, n, r, 48, &sc, &eq);
+    if (threadIdx.x == 0) thr_key[qi] = kth + 1; // exclusive bound: the seed codes themselves re-enter via the scan
+}
+
+void launch_ivf_seed(const DevSpec& ds, const uint8_t* d_codes, const uint32_t* d_ids, const uint64_t* d_list_code_off,
+                     const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq, uint32_t a,
+                     const uint32_t* d_pair_slot, const void* d_qluts, const uint32_t* d_row_bias, uint32_t r,
+                     uint32_t head, uint64_t* d_thr_key, cudaStream_t stream) {
+    if (nq == 0 || head < r) return;
+    const size_t smem = size_t(head) * 8 + size_t(ds.E) * 2;
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ivf_seed_kernel<<<nq, 256, smem, stream>>>(ds, d_codes, d_ids, d_list_code_off, d_list_count, d_order, a,
+                                               d_pair_slot, d_qluts, d_row_bias, r, head, d_thr_key);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+} // namespace qadc

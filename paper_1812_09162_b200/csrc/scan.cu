@@ -340,8 +340,8 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     const uint32_t stage_codes = STAGE_BYTES / stride;
 
     // contiguous slice of the job list for this CTA
-    const uint32_t j_begin = uint32_t(uint64_t(a->n_jobs) * blockIdx.x / gridDim.x);
-    const uint32_t j_end = uint32_t(uint64_t(a->n_jobs) * (blockIdx.x + 1) / gridDim.x);
+    const uint32_t j_begin = a->cta_begin ? a->cta_begin[blockIdx.x] : uint32_t(uint64_t(a->n_jobs) * blockIdx.x / gridDim.x);
+    const uint32_t j_end = a->cta_begin ? a->cta_begin[blockIdx.x + 1] : uint32_t(uint64_t(a->n_jobs) * (blockIdx.x + 1) / gridDim.x);
 
     // ============================ producer warp: stream codes with TMA bulk copies ==========
     if (warp == SCAN_WARPS) {
@@ -409,6 +409,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                 if (r < job.n_rows) {
                     const uint32_t row = job.row_begin + r;
                     const uint32_t q = a->row_query ? a->row_query[row] : row;
+                    if (q == 0xFFFFFFFFu) continue; // padding row of a partially filled tile
                     const uint64_t tk = a->thr_key[q];
                     uint32_t thr = uint32_t(tk >> 32);
                     uint32_t bias = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;

@@ -8,17 +8,11 @@
 // radix-selects the R smallest (distance, id) keys and stores them as the query's
 // running top-R with thr_key = the R-th key.  After S0 codes the admission rate of the
 // streaming scan is already R/S0 (2.4 % at R=100), and it falls as 1/n from there.
-#include "common.cuh"
+#include "select_common.cuh"
 
 namespace qadc {
 
 static constexpr int SEED_THREADS = 256;
-
-__device__ __forceinline__ uint32_t seed_sub_index(const DevSpec& ds, const uint8_t* code, uint32_t j) {
-    const uint32_t bp = ds.bitpos[j];
-    const uint32_t w = reinterpret_cast<const uint32_t*>(code)[bp >> 5];
-    return (w >> (bp & 31u)) & ((1u << ds.bits[j]) - 1u);
-}
 
 // dynamic smem: keys[n_head] (u64) | table[E] (u16)
 __global__ void __launch_bounds__(SEED_THREADS)
@@ -29,9 +23,7 @@ seed_topk_kernel(DevSpec ds, const uint8_t* __restrict__ codes, uint32_t n_head,
     extern __shared__ __align__(16) unsigned char sm_raw[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(sm_raw);
     uint16_t* table = reinterpret_cast<uint16_t*>(keys + n_head);
-    __shared__ uint32_t hist[256];
-    __shared__ uint64_t s_prefix;
-    __shared__ uint32_t s_rank, s_cnt_less, s_cnt_eq;
+    __shared__ SelectScratch sc;
 
     const uint32_t q = blockIdx.x;
     for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x)
@@ -42,7 +34,7 @@ seed_topk_kernel(DevSpec ds, const uint8_t* __restrict__ codes, uint32_t n_head,
     for (uint32_t i = threadIdx.x; i < n_head; i += blockDim.x) {
         const uint8_t* code = codes + size_t(i) * ds.code_stride;
         uint32_t acc = bias;
-        for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + seed_sub_index(ds, code, j)];
+        for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + code_field(ds, code, j)];
         acc = min(acc, ds.qmax); // == the chain of saturating adds (all terms unsigned)
         keys[i] = make_key(acc, ids ? ids[i] : id_base + i);
     }
@@ -67,64 +59,10 @@ seed_topk_kernel(DevSpec ds, const uint8_t* __restrict__ codes, uint32_t n_head,
         if (threadIdx.x == 0) ntop[q] = n_head;
         return;
     }
-    // MSB-first radix select of the r-th smallest key (48 significant bits)
-    if (threadIdx.x == 0) {
-        s_prefix = 0;
-        s_rank = r;
-    }
-    for (int shift = 40; shift >= 0; shift -= 8) {
-        hist[threadIdx.x] = 0;
-        __syncthreads();
-        const uint64_t prefix = s_prefix;
-        const uint64_t himask = ~0ull << (shift + 8);
-        for (uint32_t i = threadIdx.x; i < n_head; i += blockDim.x) {
-            const uint64_t k = keys[i];
-            if ((k & himask) == (prefix & himask)) atomicAdd(&hist[(k >> shift) & 255u], 1u);
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            uint32_t loc[8], sum = 0;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                loc[b] = hist[threadIdx.x * 8 + b];
-                sum += loc[b];
-            }
-            uint32_t incl = sum;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (int(threadIdx.x) >= o) incl += v;
-            }
-            uint32_t excl = incl - sum;
-            const uint32_t rank = s_rank;
-            if (rank > excl && rank <= incl) {
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    if (rank > excl && rank <= excl + loc[b]) {
-                        s_prefix = prefix | (uint64_t(threadIdx.x * 8 + b) << shift);
-                        s_rank = rank - excl;
-                    }
-                    excl += loc[b];
-                }
-            }
-        }
-        __syncthreads();
-    }
-    const uint64_t kth = s_prefix;
-    const uint32_t eq_needed = s_rank;
-    const uint32_t less = r - eq_needed;
-    if (threadIdx.x == 0) {
-        s_cnt_less = 0;
-        s_cnt_eq = 0;
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < n_head; i += blockDim.x) {
-        const uint64_t k = keys[i];
-        if (k < kth) my_top[atomicAdd(&s_cnt_less, 1u)] = k;
-        else if (k == kth) {
-            const uint32_t e = atomicAdd(&s_cnt_eq, 1u);
-            if (e < eq_needed) my_top[less + e] = k;
-        }
-    }
+    auto key_at = [&](uint32_t i) -> uint64_t { return keys[i]; };
+    uint32_t eq_needed;
+    const uint64_t kth = block_select_kth(key_at, n_head, r, 48, &sc, &eq_needed);
+    block_keep_smallest(key_at, n_head, r, kth, eq_needed, &sc, my_top);
     if (threadIdx.x == 0) {
         ntop[q] = r;
         thr_key[q] = kth;

@@ -12,7 +12,7 @@
 // which is what the heap's worst() does continuously on the CPU.  `finalize` sorts
 // the survivors (bitonic, shared memory) and applies the affine map
 // (unquantize, distance.hpp:158-161 / index.hpp:335-338).
-#include "common.cuh"
+#include "select_common.cuh"
 
 namespace qadc {
 
@@ -41,9 +41,7 @@ __global__ void __launch_bounds__(TIGHTEN_THREADS)
 tighten_kernel(uint64_t* __restrict__ top, uint32_t* __restrict__ ntop, uint32_t kpad, uint64_t* __restrict__ cand,
                uint32_t* __restrict__ cand_count, uint32_t cap, uint64_t* __restrict__ thr_key, uint32_t r) {
     extern __shared__ uint64_t keep[];
-    __shared__ uint32_t hist[256];
-    __shared__ uint64_t s_prefix;
-    __shared__ uint32_t s_rank, s_cnt_less, s_cnt_eq;
+    __shared__ SelectScratch sc;
 
     const uint32_t q = blockIdx.x;
     const uint32_t n = min(cand_count[q], cap);
@@ -77,67 +75,10 @@ tighten_kernel(uint64_t* __restrict__ top, uint32_t* __restrict__ ntop, uint32_t
     }
 
     auto key_at = [&](uint32_t i) -> uint64_t { return i < nt ? my_top[i] : my_cand[i - nt]; };
-
     // MSB-first radix select of the r-th smallest key (48 significant bits: 16 distance + 32 id)
-    if (threadIdx.x == 0) {
-        s_prefix = 0;
-        s_rank = r; // 1-based rank still to locate inside the current prefix bucket
-    }
-    for (int shift = 40; shift >= 0; shift -= 8) {
-        hist[threadIdx.x] = 0; // TIGHTEN_THREADS == 256
-        __syncthreads();
-        const uint64_t prefix = s_prefix;
-        const uint64_t himask = shift + 8 >= 64 ? 0ull : (~0ull << (shift + 8));
-        for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
-            const uint64_t k = key_at(i);
-            if ((k & himask) == (prefix & himask)) atomicAdd(&hist[(k >> shift) & 255u], 1u);
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            // lane l owns bins 8l..8l+7
-            uint32_t loc[8], sum = 0;
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                loc[b] = hist[threadIdx.x * 8 + b];
-                sum += loc[b];
-            }
-            uint32_t incl = sum;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (int(threadIdx.x) >= o) incl += v;
-            }
-            uint32_t excl = incl - sum;
-            const uint32_t rank = s_rank;
-            if (rank > excl && rank <= incl) {
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    if (rank > excl && rank <= excl + loc[b]) {
-                        s_prefix = prefix | (uint64_t(threadIdx.x * 8 + b) << shift);
-                        s_rank = rank - excl;
-                    }
-                    excl += loc[b];
-                }
-            }
-        }
-        __syncthreads();
-    }
-    const uint64_t kth = s_prefix;       // the r-th smallest key
-    const uint32_t eq_needed = s_rank;   // copies of kth to keep (1 unless ids repeat)
-    const uint32_t less = r - eq_needed; // keys strictly below kth
-    if (threadIdx.x == 0) {
-        s_cnt_less = 0;
-        s_cnt_eq = 0;
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
-        const uint64_t k = key_at(i);
-        if (k < kth) keep[atomicAdd(&s_cnt_less, 1u)] = k;
-        else if (k == kth) {
-            const uint32_t e = atomicAdd(&s_cnt_eq, 1u);
-            if (e < eq_needed) keep[less + e] = k;
-        }
-    }
-    __syncthreads();
+    uint32_t eq_needed;
+    const uint64_t kth = block_select_kth(key_at, total, r, 48, &sc, &eq_needed);
+    block_keep_smallest(key_at, total, r, kth, eq_needed, &sc, keep);
     for (uint32_t i = threadIdx.x; i < r; i += blockDim.x) my_top[i] = keep[i];
     if (threadIdx.x == 0) {
         ntop[q] = r;

@@ -256,3 +256,91 @@ def test_large_seeded_property_round_trip(port):
     # and the full oracle on a few queries
     ref = port.flat_search(so, cb, pk, n, queries[:4], r=100, t=400, threads=4)
     assert np.array_equal(res.ids[:4], ref[0]) and bits_equal(res.dists[:4], ref[1])
+
+
+# ------------------------------------------------------------------------- IVF --
+
+def _ivf_lists(rng, s, k_cells, n, empty=()):
+    """Random IVF partition: list sizes, packed lists (reference layout, concatenated), ids."""
+    assign = rng.integers(0, k_cells, size=n)
+    for c in empty:
+        assign[assign == c] = (c + 1) % k_cells
+    codes = random_codes(s, n, seed=int(rng.integers(1 << 30)))
+    packed, ids, boff, ioff, counts = [], [], [], [], []
+    b = i = 0
+    for c in range(k_cells):
+        members = np.nonzero(assign == c)[0].astype(np.uint32)
+        rng.shuffle(members)
+        pk = qb.pack_list(s, codes[members]) if len(members) else np.zeros(0, np.uint8)
+        boff.append(b); ioff.append(i); counts.append(len(members))
+        packed.append(pk); ids.append(members)
+        b += pk.size; i += len(members)
+    return (np.concatenate(packed), np.array(boff, np.uint64), np.array(ioff, np.uint64),
+            np.array(counts, np.uint64), np.concatenate(ids).astype(np.uint32))
+
+
+@pytest.mark.parametrize("name", ["ivf_irr655.npz", "ivf_pq16x4.npz"])
+def test_golden_ivf(golden, name):
+    g = golden(name)
+    s = qb.allocate_dims(int(g["dims"]), str(g["spec"]))
+    with qb.IvfIndex(s, g["codebook"], g["coarse"], g["packed"], g["list_byte_off"], g["list_id_off"],
+                     g["list_count"], g["list_ids"]) as idx:
+        probes_mid = int(g["probe_list"][1])
+        assert np.array_equal(idx.probe_order(g["queries"], probes_mid), g["order"])
+        for pr in g["probe_list"]:
+            res = idx.search(g["queries"], qb.SearchParams(probes=int(pr), r=int(g["r"]), t=int(g["t"])))
+            assert np.array_equal(res.counts, g[f"counts_p{pr}"])
+            for qi in range(len(g["queries"])):
+                c = int(res.counts[qi])
+                assert np.array_equal(res.ids[qi, :c], g[f"ids_p{pr}"][qi, :c]), (name, int(pr), qi)
+                assert bits_equal(res.dists[qi, :c], g[f"dists_p{pr}"][qi, :c])
+
+
+@pytest.mark.parametrize("dims,text,k_cells,n,probes", [(128, "12x{6,5,5}", 64, 150000, 8), (64, "16x{4,4}", 40, 60000, 5),
+                                                        (64, "8x{8,8}", 16, 30000, 16), (48, "12x{6,6,4}", 300, 90000, 32)])
+def test_ivf_search_vs_oracle(port, dims, text, k_cells, n, probes):
+    """IvfIndex::search (shared map + per-cell bias + explicit ids) against the oracle, including empty cells,
+    lists shorter than t and R, and probes > non-empty cells."""
+    rng = np.random.default_rng(abs(hash((text, k_cells))) % 10000)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 1.5).astype(np.float32)
+    coarse = (rng.standard_normal((k_cells, dims)) * 3).astype(np.float32)
+    packed, boff, ioff, counts, ids = _ivf_lists(rng, s, k_cells, n, empty=(1, k_cells - 2))
+    queries = (rng.standard_normal((50, dims)) * 3).astype(np.float32)
+    with qb.IvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids) as idx:
+        for pr, r, t in [(probes, 100, 400), (1, 10, 10), (k_cells + 5, 100, 5000)]:
+            want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=pr, r=r, t=t, threads=8)
+            got = idx.search(queries, qb.SearchParams(probes=pr, r=r, t=t))
+            assert np.array_equal(got.counts, want[2]), (pr, r, t)
+            for qi in range(len(queries)):
+                c = int(want[2][qi])
+                assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]), (pr, r, t, qi)
+                assert bits_equal(got.dists[qi, :c], want[1][qi, :c])
+        a = min(probes, k_cells)
+        order = idx.probe_order(queries, a)
+        for qi in range(0, 50, 7):
+            assert np.array_equal(order[qi], port.probe_order(dims, coarse, queries[qi], a))
+        with pytest.raises(qb.QadcError) as e:
+            idx.search(queries, qb.SearchParams(probes=0))
+        assert e.value.kind == "input"
+
+
+def test_ivf_all_lists_empty_or_tiny(port):
+    dims, text = 64, "16x{4,4}"
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    rng = np.random.default_rng(4)
+    cb = rng.standard_normal(s.cb_floats).astype(np.float32)
+    coarse = rng.standard_normal((8, dims)).astype(np.float32)
+    queries = rng.standard_normal((6, dims)).astype(np.float32)
+    z64 = np.zeros(8, np.uint64)
+    with qb.IvfIndex(s, cb, coarse, np.zeros(0, np.uint8), z64, z64, z64, np.zeros(0, np.uint32)) as idx:
+        res = idx.search(queries, qb.SearchParams(probes=3))
+        assert res.counts.tolist() == [0] * 6
+    packed, boff, ioff, counts, ids = _ivf_lists(rng, s, 8, 30)
+    with qb.IvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids) as idx:
+        want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=8, r=100, t=400)
+        got = idx.search(queries, qb.SearchParams(probes=8))
+        assert np.array_equal(got.counts, want[2])
+        for qi in range(6):
+            c = int(want[2][qi])
+            assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]) and bits_equal(got.dists[qi, :c], want[1][qi, :c])
