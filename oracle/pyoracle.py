@@ -81,6 +81,9 @@ def build(force: bool = False) -> None:
     if (ref_inc / "pqscan").is_dir():
         if force or not REF_SO.exists() or REF_SO.stat().st_mtime < (HERE / "ref_shim.cpp").stat().st_mtime:
             subprocess.check_call(["make", "-C", str(HERE), "ref", f"REF={ref_inc}"], stdout=subprocess.DEVNULL)
+        # the C++ integration test (reference types -> include/qadc.hpp -> libqadc_b200.so); make skips it
+        # quietly when the product library has not been built yet
+        subprocess.check_call(["make", "-C", str(HERE), "integration", f"REF={ref_inc}"], stdout=subprocess.DEVNULL)
 
 
 def _p(a, ctype):

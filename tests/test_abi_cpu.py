@@ -86,3 +86,17 @@ def test_product_does_not_link_the_oracle(L):
     assert "oracle" not in out and "pqscan" not in out
     syms = subprocess.run(["nm", "-D", str(_lib.SO_PATH)], capture_output=True, text=True).stdout
     assert " orc_" not in syms
+
+
+def test_cpp_binding_fails_loudly_without_gpu(L):
+    """The reference-side C++ binding (include/qadc.hpp) must surface the missing device as an error, not emulate."""
+    import subprocess
+    from pathlib import Path
+    if L.qadc_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    exe = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "integration_test"
+    if not exe.exists():
+        pytest.skip("integration binary not built")
+    out = subprocess.run([str(exe), "1"], capture_output=True, text=True, timeout=120)
+    assert out.returncode != 0
+    assert "no usable CUDA device" in out.stderr

@@ -344,3 +344,61 @@ def test_ivf_all_lists_empty_or_tiny(port):
         for qi in range(6):
             c = int(want[2][qi])
             assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]) and bits_equal(got.dists[qi, :c], want[1][qi, :c])
+
+
+# ------------------------------------------------------------------ sharded (1 GPU) --
+
+@pytest.mark.parametrize("dims,text,n,world", [(128, "16x{4,4}", 100000, 4), (96, "12x{6,5,5}", 50000, 3), (128, "8x{8,8}", 300, 8)])
+def test_sharded_device_path_equals_unsharded(port, dims, text, n, world):
+    """The multi-GPU data path on one device: every 'rank' is a FlatIndex over its block-aligned shard opened
+    with base_id and the global calibration head; their device key lists are stacked as all_gather would and
+    merged by the CUDA merge kernel.  Ranks run one after the other (nothing waits on another kernel)."""
+    import torch
+    from paper_1812_09162_b200.dist import global_head, shard_ranges, slice_packed
+    rng = np.random.default_rng(3)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+    packed = qb.pack_list(s, random_codes(s, n, seed=8))
+    queries = (rng.standard_normal((33, dims)) * 2).astype(np.float32)
+    r, t = 100, 400
+    want = port.flat_search(so, cb, packed, n, queries, r=r, t=t, threads=8)
+    dev = torch.device("cuda", 0)
+    d_q = torch.from_numpy(queries).to(dev)
+    head, head_n = global_head(s, packed, n)
+    keys = torch.empty((world, len(queries), r), dtype=torch.int64, device=dev)
+    qmap = torch.empty((len(queries), 2), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    params = qb.SearchParams(r=r, t=t)
+    for rank, rg in enumerate(shard_ranges(n, world, s.block_len)):
+        with qb.FlatIndex(s, cb, slice_packed(s, packed, rg), rg.count, base_id=rg.start, calib_packed=head,
+                          calib_count=head_n) as shard:
+            shard.search_device(d_q, params, None, None, None, d_keys=keys[rank], d_map=qmap, stream=stream)
+            torch.cuda.synchronize()
+    d_ids = torch.empty((len(queries), r), dtype=torch.int32, device=dev)
+    d_dists = torch.empty((len(queries), r), dtype=torch.float32, device=dev)
+    d_counts = torch.empty((len(queries),), dtype=torch.int32, device=dev)
+    qb.merge_topk_device(keys, world, len(queries), r, qmap, d_ids, d_dists, d_counts, 0, stream=stream)
+    torch.cuda.synchronize()
+    counts = d_counts.cpu().numpy().astype(np.uint32)
+    ids = d_ids.cpu().numpy().view(np.uint32)
+    dists = d_dists.cpu().numpy()
+    assert np.array_equal(counts, want[2])
+    for qi in range(len(queries)):
+        c = int(want[2][qi])
+        assert np.array_equal(ids[qi, :c], want[0][qi, :c]) and bits_equal(dists[qi, :c], want[1][qi, :c])
+
+
+# ------------------------------------------------ reference-side C++ binding (qadc.hpp) --
+
+def test_cpp_integration_binary():
+    """The reference's own C++ types (FlatIndex, IvfIndex, QuantizedScanFn, CandidateHeap) against the GPU path
+    through include/qadc.hpp.  The binary is compiled in the build container against the unmodified reference
+    headers (oracle/Makefile `integration`) and travels with the snapshot; it is absent only if that build never ran."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "integration_test"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/integration_test was not built (no reference tree at build time)")
+    out = subprocess.run([str(exe), "25"], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "INTEGRATION OK" in out.stdout
