@@ -17,9 +17,10 @@ Workloads (BASELINE.json configs; seeded synthetic inputs with the named shapes 
 SIFT/Deep-like data, see paper_1812_09162_b200/synth.py):
   c1  16x{4,4}    d=128  N=1e6   Q=1e3     c3  8x{8,8}   d=128  N=1e7  Q=1e4
   c2  12x{6,5,5}  d=96   N=1e7   Q=1e4     c4  16x{4,4}  d=128  N=2e8  Q=1e4 (uniform random codes)
+  c5  IVF K=16384, 12x{6,5,5} residual codes, d=128, N=6.25e7 per GPU (5e8 / 8), nprobe=64, Q=1e4
 Default c2 (configs[1]).  With --gpus N > 1 (torchrun, one rank per GPU) every rank holds one database
 shard of the per-GPU size above (weak scaling), queries are replicated and the per-query top-R lists are
-merged after one NCCL all_gather.
+merged after one NCCL all_gather (flat workloads; the IVF workload runs on one GPU in this round).
 """
 from __future__ import annotations
 
@@ -38,10 +39,12 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 WORKLOADS = {
-    "c1": dict(spec="16x{4,4}", dims=128, n=1_000_000, nq=1_000, data="encoded"),
-    "c2": dict(spec="12x{6,5,5}", dims=96, n=10_000_000, nq=10_000, data="encoded"),
-    "c3": dict(spec="8x{8,8}", dims=128, n=10_000_000, nq=10_000, data="encoded"),
-    "c4": dict(spec="16x{4,4}", dims=128, n=200_000_000, nq=10_000, data="random"),
+    "c1": dict(kind="flat", spec="16x{4,4}", dims=128, n=1_000_000, nq=1_000, data="encoded"),
+    "c2": dict(kind="flat", spec="12x{6,5,5}", dims=96, n=10_000_000, nq=10_000, data="encoded"),
+    "c3": dict(kind="flat", spec="8x{8,8}", dims=128, n=10_000_000, nq=10_000, data="encoded"),
+    "c4": dict(kind="flat", spec="16x{4,4}", dims=128, n=200_000_000, nq=10_000, data="random"),
+    "c5": dict(kind="ivf", spec="12x{6,5,5}", dims=128, n=62_500_000, nq=10_000, data="random", k_cells=16384,
+               probes=64),
 }
 R, T = 100, 400
 
@@ -52,7 +55,7 @@ def log(*a):
 
 # ----------------------------------------------------------------------------- data --
 
-def make_database(qb, spec, wl, rank, have_gpu):
+def make_flat(qb, spec, wl, rank, have_gpu):
     """Packed shard for this rank (seeded by rank) + the global head (rank 0's first codes)."""
     from paper_1812_09162_b200 import synth
     dims, n = wl["dims"], wl["n"]
@@ -69,19 +72,13 @@ def make_database(qb, spec, wl, rank, have_gpu):
         o = Oracle("port")
         return o.encode(o.spec(dims, wl["spec"]), cb, vecs)
 
-    def shard_codes(r, count, first_only=None):
-        if wl["data"] == "random":
-            return None
-        parts, done, batch = [], 0, 500_000
-        b = 0
+    def shard_codes(r, count):
+        parts, done, batch, b = [], 0, 500_000, 0
         while done < count:
             nb = min(batch, count - done)
-            vecs = synth.gaussian_mixture(nb, dims, seed=2 + 1000 * r + b, centres=centres)
-            parts.append(encode(vecs))
+            parts.append(encode(synth.gaussian_mixture(nb, dims, seed=2 + 1000 * r + b, centres=centres)))
             done += nb
             b += 1
-            if first_only and done >= first_only:
-                break
         return np.concatenate(parts)
 
     t0 = time.time()
@@ -97,11 +94,57 @@ def make_database(qb, spec, wl, rank, have_gpu):
         codes = shard_codes(rank, n)
         packed = qb.pack_list(spec, codes)
         head_n = min(4096, n)
-        head_codes = codes[:head_n] if rank == 0 else shard_codes(0, head_n, first_only=head_n)[:head_n]
+        head_codes = codes[:head_n] if rank == 0 else shard_codes(0, min(head_n, 500_000))[:head_n]
         head = qb.pack_list(spec, head_codes)
     log(f"[bench] rank {rank}: database shard of {n} codes ready in {time.time() - t0:.1f}s")
     queries = synth.gaussian_mixture(wl["nq"], dims, seed=3, centres=centres)
-    return cb, packed, head, head_n, queries
+    return dict(cb=cb, packed=packed, head=head, head_n=head_n, queries=queries)
+
+
+def make_ivf(qb, spec, wl, have_gpu):
+    """Config 5 stand-in: coarse centroids from Lloyd iterations on mixture samples, list sizes from the
+    assignment histogram of a mixture sample scaled to N, uniform random residual codes, ids = positions."""
+    from paper_1812_09162_b200 import synth
+    import torch
+    dims, n, K = wl["dims"], wl["n"], wl["k_cells"]
+    dev = torch.device("cuda", 0) if have_gpu else torch.device("cpu")
+    centres = synth.mixture_centres(dims, seed=1)
+    t0 = time.time()
+    sample = torch.from_numpy(synth.gaussian_mixture(max(4 * K, 300_000), dims, seed=7, centres=centres)).to(dev)
+    g = torch.Generator(device="cpu").manual_seed(8)
+    coarse = sample[torch.randperm(sample.shape[0], generator=g)[:K].to(dev)].clone()
+
+    def assign(x):
+        out = torch.empty(x.shape[0], dtype=torch.long, device=dev)
+        for i in range(0, x.shape[0], 16384):
+            xb = x[i:i + 16384]
+            d = (xb * xb).sum(1, keepdim=True) - 2.0 * xb @ coarse.T + (coarse * coarse).sum(1)[None, :]
+            out[i:i + 16384] = d.argmin(1)
+        return out
+
+    for _ in range(2 if have_gpu else 1):  # Lloyd steps (input preparation, not the timed path)
+        a = assign(sample)
+        sums = torch.zeros_like(coarse).index_add_(0, a, sample)
+        cnt = torch.bincount(a, minlength=K).clamp(min=1).unsqueeze(1)
+        coarse = sums / cnt
+    a = assign(sample)
+    hist = torch.bincount(a, minlength=K).double().cpu().numpy() + 0.25
+    resid = (sample - coarse[a])[:100_000].cpu().numpy()
+    coarse = coarse.cpu().numpy().astype(np.float32)
+    counts = np.floor(hist / hist.sum() * n).astype(np.uint64)
+    counts[: int(n - counts.sum())] += 1
+    cb = synth.train_codebook(spec, resid, iters=6, seed=5)
+    log(f"[bench] coarse quantizer (K={K}) + residual codebook in {time.time() - t0:.1f}s; "
+        f"list sizes min/median/max = {counts.min()}/{int(np.median(counts))}/{counts.max()}")
+    t0 = time.time()
+    pbytes = np.array([qb.packed_bytes(spec, int(c)) for c in counts], dtype=np.uint64)
+    boff = np.concatenate([[0], np.cumsum(pbytes)[:-1]]).astype(np.uint64)
+    ioff = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
+    packed = np.random.default_rng(6).integers(0, 256, size=int(pbytes.sum()), dtype=np.uint8)
+    ids = np.arange(n, dtype=np.uint32)
+    queries = synth.gaussian_mixture(wl["nq"], dims, seed=3, centres=centres)
+    log(f"[bench] {n} residual codes in {K} lists ready in {time.time() - t0:.1f}s")
+    return dict(cb=cb, coarse=coarse, packed=packed, boff=boff, ioff=ioff, counts=counts, ids=ids, queries=queries)
 
 
 # --------------------------------------------------------------------------- clocks --
@@ -154,29 +197,49 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- cpu baseline --
 
-def cpu_reference_rate(wl, cb, packed, queries, budget_s=12.0, max_queries=None):
-    """The reference's CPU search on the host cores (query-parallel pool, all cores), bounded sample."""
-    from oracle.pyoracle import Oracle, build
-    build()
-    kind = "reference" if Oracle.available("reference") else "port"
-    o = Oracle(kind)
-    s = o.spec(wl["dims"], wl["spec"])
-    cores = os.cpu_count() or 1
-    fam = 1  # auto: the natural SIMD family when the host supports it
-    n = wl["n"]
-    probe = min(len(queries), cores)
-    t0 = time.perf_counter()
-    o.flat_search(s, cb, packed, n, queries[:probe], r=R, t=T, family=fam, threads=cores)
-    dt = max(time.perf_counter() - t0, 1e-4)
-    nq = int(min(len(queries), max(probe, budget_s / dt * probe)))
-    if max_queries:
-        nq = min(nq, max_queries)
-    t0 = time.perf_counter()
-    o.flat_search(s, cb, packed, n, queries[:nq], r=R, t=T, family=fam, threads=cores)
-    dt = time.perf_counter() - t0
-    family = o.auto_family(s) if kind == "reference" else "scalar-quantized (C port)"
-    return {"value": n * nq / dt, "unit": "codes/s", "cores": cores, "kind": kind,
-            "sample": f"{nq} of {len(queries)} queries x {n} codes, kernel {family}, {dt:.2f}s"}, nq, dt
+class CpuReference:
+    """The reference's CPU search on the host cores: query-parallel pool on all cores
+    (tools/pqscan_cli.cpp:141-166), kernel family chosen by the reference (auto)."""
+
+    def __init__(self, wl, data):
+        from oracle.pyoracle import Oracle, build
+        build()
+        self.kind = "reference" if Oracle.available("reference") else "port"
+        self.o = Oracle(self.kind)
+        self.wl = wl
+        self.s = self.o.spec(wl["dims"], wl["spec"])
+        self.cores = os.cpu_count() or 1
+        self.queries = data["queries"]
+        if wl["kind"] == "ivf":
+            self.h = self.o.ivf_open(self.s, data["cb"], data["coarse"], data["packed"], data["boff"], data["ioff"],
+                                     data["counts"], data["ids"])
+        else:
+            self.h = self.o.flat_open(self.s, data["cb"], data["packed"], wl["n"])
+        self.family = self.o.auto_family(self.s) if self.kind == "reference" else "scalar-quantized (C port)"
+
+    def run(self, nq):
+        t0 = time.perf_counter()
+        self.o.search_h(self.h, self.queries[:nq], probes=self.wl.get("probes", 1), r=R, t=T, family=1,
+                        threads=self.cores)
+        return time.perf_counter() - t0
+
+    def sized_sample(self, budget_s, cap=None):
+        probe = min(len(self.queries), self.cores)
+        dt = max(self.run(probe), 1e-4)
+        nq = int(min(len(self.queries), max(probe, budget_s / dt * probe)))
+        return min(nq, cap) if cap else nq
+
+    def pairs_per_query(self, data, nq_sample):
+        """flat: every query scans the whole list; IVF: mean total length of the probed lists."""
+        if self.wl["kind"] != "ivf":
+            return float(self.wl["n"])
+        lens = data["counts"].astype(np.float64)
+        qs = data["queries"][:min(64, nq_sample)]
+        return float(np.mean([lens[self.o.probe_order(self.wl["dims"], data["coarse"], q, self.wl["probes"])].sum()
+                              for q in qs]))
+
+    def close(self):
+        self.o.close_h(self.h)
 
 
 # ------------------------------------------------------------------------------ main --
@@ -193,7 +256,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--option", action="append", default=[], help="name=value passed to qadc_set_option")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "ours":
+        args.warmup = max(args.warmup, 3)
 
     wl = dict(WORKLOADS[args.workload])
     if args.n:
@@ -203,6 +267,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    ivf = wl["kind"] == "ivf"
 
     if args.impl == "reference" and rank != 0:
         return 0
@@ -211,56 +276,70 @@ def main():
     qb.build()
     have_gpu = qb.lib().qadc_device_count() > 0
     spec = qb.allocate_dims(wl["dims"], wl["spec"])
-    config = {"workload": f"{args.workload}: {wl['spec']} d={wl['dims']} N={wl['n']}/GPU Q={wl['nq']} R={R} t={T}",
+    dtype = "u16" if spec.word_width == 16 else "u8"
+    config = {"workload": f"{args.workload}: " + (f"IVF K={wl['k_cells']} nprobe={wl['probes']} " if ivf else "") +
+                          f"{wl['spec']} d={wl['dims']} N={wl['n']}/GPU Q={wl['nq']} R={R} t={T}",
               "spec": wl["spec"], "dims": wl["dims"], "codes_per_gpu": wl["n"], "queries": wl["nq"], "r": R, "t": T,
               "database": "gaussian-mixture vectors encoded with k-means codebooks" if wl["data"] == "encoded"
               else "uniform random codes", "sharding": f"db{world}" if world > 1 else "none"}
 
     # -------------------------------------------------------------- reference arm --
     if args.impl == "reference":
-        cb, packed, head, head_n, queries = make_database(qb, spec, wl, 0, have_gpu)
-        per_step = []
-        base = None
-        nq_step = None
+        data = make_ivf(qb, spec, wl, have_gpu) if ivf else make_flat(qb, spec, wl, 0, have_gpu)
+        cpu = CpuReference(wl, data)
+        nq_step = cpu.sized_sample(6.0)
+        ppq = cpu.pairs_per_query(data, nq_step)
+        times = []
         for i in range(args.warmup + args.steps):
-            base, nq_used, dt = cpu_reference_rate(wl, cb, packed, queries, budget_s=8.0, max_queries=nq_step)
-            nq_step = nq_used
+            dt = cpu.run(nq_step)
             if i >= args.warmup:
-                per_step.append((nq_used, dt))
-        tot_pairs = sum(n for n, _ in per_step) * wl["n"]
-        tot_t = sum(t for _, t in per_step)
-        value = tot_pairs / tot_t
-        base["value"] = value
+                times.append(dt)
+        tot_t = sum(times)
+        value = ppq * nq_step * len(times) / tot_t
         print(json.dumps({
             "impl": "reference", "metric": "ADC codes scanned/s", "value": value, "unit": "codes/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / max(args.steps, 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16" if spec.word_width == 16 else "u8",
-            "data": "synthetic", "config": config, "cpu_baseline": base,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / max(len(times), 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": config,
+            "cpu_baseline": {"value": value, "unit": "codes/s", "cores": cpu.cores, "kind": cpu.kind,
+                             "sample": f"each step: {nq_step} of {wl['nq']} queries, kernel {cpu.family}"},
             "e2e": {"value": value, "unit": "codes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        cpu.close()
         return 0
 
     # --------------------------------------------------------------------- our arm --
     import torch
     if not have_gpu:
         raise SystemExit("bench.py: no CUDA device; the product has no CPU path (use --impl reference for the CPU arm)")
+    if ivf and world > 1:
+        raise SystemExit("bench.py: the IVF workload (c5) runs on one GPU in this round (IVF sharding is not built yet)")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    cb, packed, head, head_n, queries = make_database(qb, spec, wl, rank, have_gpu)
-
-    from paper_1812_09162_b200.dist import ShardedFlatIndex, ShardRange
+    params = qb.SearchParams(probes=wl.get("probes", 1), r=R, t=T)
     t0 = time.time()
-    sharded = ShardedFlatIndex(spec, cb, packed, ShardRange(rank * wl["n"], wl["n"]), head, head_n, local_rank)
-    idx = sharded.index
+    if ivf:
+        data = make_ivf(qb, spec, wl, have_gpu)
+        t0 = time.time()
+        idx = qb.IvfIndex(spec, data["cb"], data["coarse"], data["packed"], data["boff"], data["ioff"],
+                          data["counts"], data["ids"], device=local_rank)
+        sharded = None
+    else:
+        from paper_1812_09162_b200.dist import ShardedFlatIndex, ShardRange
+        data = make_flat(qb, spec, wl, rank, have_gpu)
+        t0 = time.time()
+        sharded = ShardedFlatIndex(spec, data["cb"], data["packed"], ShardRange(rank * wl["n"], wl["n"]), data["head"],
+                                   data["head_n"], local_rank)
+        idx = sharded.index
     for opt in args.option:
         k, v = opt.split("=")
         idx.set_option(k, int(v))
     log(f"[bench] rank {rank}: index open (upload + re-layout) {time.time() - t0:.1f}s")
 
+    queries = data["queries"]
     nq = wl["nq"]
-    params = qb.SearchParams(r=R, t=T)
     d_q = torch.from_numpy(queries).to(dev)
     d_ids = torch.empty((nq, R), dtype=torch.int32, device=dev)
     d_dists = torch.empty((nq, R), dtype=torch.float32, device=dev)
@@ -270,7 +349,10 @@ def main():
 
     def step():
         flush.zero_()  # evict the code array / tables from L2 between steps
-        sharded.search_device(d_q, params, d_ids, d_dists, d_counts, stream=stream)
+        if sharded is not None:
+            sharded.search_device(d_q, params, d_ids, d_dists, d_counts, stream=stream)
+        else:
+            idx.search_device(d_q, params, d_ids, d_dists, d_counts, stream=stream)
 
     def barrier():
         if world > 1:
@@ -297,7 +379,7 @@ def main():
             st_acc["ms_scan"] += st.ms_scan
             st_acc["ms_lut"] += st.ms_lut
             st_acc["ms_select"] += st.ms_select
-            st_acc["launches"] += st.kernel_launches + (1 if True else 0)  # + the merge kernel
+            st_acc["launches"] += st.kernel_launches + (1 if sharded is not None else 0)  # + the merge kernel
             st_acc["scan_launches"] += st.scan_launches
             st_acc["pairs"] += st.pairs_scanned
         ev1.record()
@@ -309,12 +391,12 @@ def main():
         tmax = torch.tensor([ms], device=dev)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         ms = float(tmax.item())
-    total_pairs = float(wl["n"]) * nq * world * args.steps
+    pairs_per_step = st_acc["pairs"] / args.steps  # flat: N*Q per rank; IVF: sum of probed list lengths
+    total_pairs = pairs_per_step * world * args.steps
     value = total_pairs / (ms * 1e-3)
 
     # ---- e2e: the host-buffer C-ABI call (H2D + D2H inside), same metric ----
     h_q = torch.from_numpy(queries).pin_memory()
-    e2e_ms = None
     if world == 1:
         qn = h_q.numpy()
         idx.search(qn, params)  # warm the host path (its workspace is sized on first use)
@@ -322,10 +404,9 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.steps):
             flush.zero_()
-            res = idx.search(qn, params)
+            idx.search(qn, params)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3
-        e2e_value = float(wl["n"]) * nq * args.steps / (e2e_ms * 1e-3)
     else:
         # multi-GPU e2e: pinned host queries -> device, sharded search + merge, results back to pinned host
         h_ids = torch.empty((nq, R), dtype=torch.int32).pin_memory()
@@ -346,7 +427,7 @@ def main():
         tmax = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         e2e_ms = float(tmax.item())
-        e2e_value = total_pairs / (e2e_ms * 1e-3)
+    e2e_value = total_pairs / (e2e_ms * 1e-3)
 
     if rank == 0:
         peaks_path = ROOT / "MEASURED_PEAKS.json"
@@ -356,26 +437,37 @@ def main():
             peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
         scan_s = st_acc["ms_scan"] * 1e-3
         achieved = (st_acc["pairs"] * 8.0 / scan_s) / 1e9 if scan_s > 0 else None
+        traffic = None
+        tpath = ROOT / "profiles" / "traffic.json"  # dram__bytes_read+write of the dominant launch, from ncu --set full
+        if tpath.exists():
+            traffic = json.loads(tpath.read_text()).get(args.workload)
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak if achieved else None, "traffic": None, "peak_source": peak_src,
+                    "frac": achieved / peak if achieved else None, "traffic": traffic, "peak_source": peak_src,
                     "kernel": "scan_kernel (" + qb.lib().qadc_variant_name(idx.stats().scan_variant).decode() + ")",
                     "algorithmic_bytes_per_pair": 8,
                     "avg_launch_ms": st_acc["ms_scan"] / max(st_acc["scan_launches"], 1),
                     "stage_ms_per_step": {k: st_acc[k] / args.steps for k in ("ms_lut", "ms_scan", "ms_select")},
-                    "note": "codes are reused across the query tile from shared memory/L2, so algorithmic bytes exceed DRAM traffic"}
-        cpu = None
+                    "note": "codes are streamed once per query tile and reused from shared memory, so algorithmic bytes "
+                            "exceed DRAM traffic; the kernel's real ceiling is the shared-memory pipe (profiles/)"}
+        cpu_out = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu, _, _ = cpu_reference_rate(wl, cb, packed, queries)
+            cpu = CpuReference(wl, data)
+            nq_s = cpu.sized_sample(12.0)
+            dt = cpu.run(nq_s)
+            cpu_out = {"value": pairs_per_step / nq * nq_s / dt, "unit": "codes/s", "cores": cpu.cores, "kind": cpu.kind,
+                       "sample": f"{nq_s} of {nq} queries, kernel {cpu.family}, {dt:.2f}s"}
+            cpu.close()
         out = {
             "metric": "ADC codes scanned/s", "value": value, "unit": "codes/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u16" if spec.word_width == 16 else "u8", "data": "synthetic",
-            "config": dict(config, l2="flushed between steps (256 MiB write inside the timed region); the code array "
-                                      "is also re-streamed once per query tile"),
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": dict(config, pairs_per_step=pairs_per_step * world,
+                           l2="flushed between steps (256 MiB write inside the timed region); the code array "
+                              "is also re-streamed once per query tile"),
             "clocks": clk, "gpu_launches": int(st_acc["launches"]),
             "e2e": {"value": e2e_value, "unit": "codes/s", "h2d_bytes_per_step": int(nq * wl["dims"] * 4),
                     "d2h_bytes_per_step": int(nq * R * 8 + nq * 4), "ms_per_step": e2e_ms / args.steps},
-            "roofline": roofline, "cpu_baseline": cpu,
+            "roofline": roofline, "cpu_baseline": cpu_out,
             "per_gpu_value": value / world,
         }
         print(json.dumps(out))

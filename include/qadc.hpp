@@ -90,7 +90,7 @@ inline void gpu_scan_list(const pqscan::PackedList& list, const pqscan::PackingS
     if (list.count == 0) return;
     const uint32_t m = static_cast<uint32_t>(qt.num_subs());
     pqscan::SpecPattern pat{m, scheme.widths};
-    const qadc_spec s = to_abi(pqscan::allocate_dims(m, pat)); // dims are irrelevant to the scan
+    const qadc_spec s = to_abi(pqscan::allocate_dims(16 * m, pat)); // dims are irrelevant to the scan (selftest.hpp:57)
     std::vector<uint8_t> q8;
     std::vector<uint16_t> q16;
     const void* qptr;

@@ -278,6 +278,47 @@ class Oracle:
             _p(out_ids, C.c_uint32), _p(out_d, C.c_float), _p(counts, C.c_uint32)))
         return out_ids, out_d, counts
 
+    # -- handle-based search (index built once; used by bench.py's CPU baseline) ----------------
+    def flat_open(self, s: OrcSpec, codebook, packed, count: int):
+        self.lib.orc_flat_create.restype = C.c_void_p
+        keep = (_f32(codebook), np.ascontiguousarray(packed, dtype=np.uint8))
+        h = self.lib.orc_flat_create(C.byref(s), _p(keep[0], C.c_float), _p(keep[1], C.c_uint8), C.c_uint64(count))
+        if not h:
+            raise OracleError(1, self.lib.orc_last_error().decode())
+        return {"h": C.c_void_p(h), "keep": keep, "dims": s.dims, "ivf": False}
+
+    def ivf_open(self, s: OrcSpec, codebook, coarse, packed, list_byte_off, list_id_off, list_count, ids):
+        self.lib.orc_ivf_create.restype = C.c_void_p
+        keep = (_f32(codebook), _f32(coarse).reshape(-1, s.dims), np.ascontiguousarray(packed, dtype=np.uint8),
+                np.ascontiguousarray(list_byte_off, dtype=np.uint64), np.ascontiguousarray(list_id_off, dtype=np.uint64),
+                np.ascontiguousarray(list_count, dtype=np.uint64), np.ascontiguousarray(ids, dtype=np.uint32))
+        h = self.lib.orc_ivf_create(C.byref(s), _p(keep[0], C.c_float), _p(keep[1], C.c_float),
+                                    C.c_uint32(keep[1].shape[0]), _p(keep[2], C.c_uint8), _p(keep[3], C.c_uint64),
+                                    _p(keep[4], C.c_uint64), _p(keep[5], C.c_uint64), _p(keep[6], C.c_uint32))
+        if not h:
+            raise OracleError(1, self.lib.orc_last_error().decode())
+        return {"h": C.c_void_p(h), "keep": keep, "dims": s.dims, "ivf": True}
+
+    def search_h(self, handle, queries, probes=1, r=100, t=400, family=0, threads=1):
+        q = _f32(queries).reshape(-1, handle["dims"])
+        nq = q.shape[0]
+        ids = np.zeros((nq, r), dtype=np.uint32)
+        dists = np.zeros((nq, r), dtype=np.float32)
+        counts = np.zeros(nq, dtype=np.uint32)
+        if handle["ivf"]:
+            rc = self.lib.orc_ivf_search_h(handle["h"], _p(q, C.c_float), C.c_uint32(nq), C.c_uint32(probes),
+                                           C.c_uint32(r), C.c_uint32(t), C.c_int(family), C.c_int(threads),
+                                           _p(ids, C.c_uint32), _p(dists, C.c_float), _p(counts, C.c_uint32))
+        else:
+            rc = self.lib.orc_flat_search_h(handle["h"], _p(q, C.c_float), C.c_uint32(nq), C.c_uint32(r), C.c_uint32(t),
+                                            C.c_int(family), C.c_int(threads), _p(ids, C.c_uint32),
+                                            _p(dists, C.c_float), _p(counts, C.c_uint32))
+        self._check(rc)
+        return ids, dists, counts
+
+    def close_h(self, handle):
+        (self.lib.orc_ivf_destroy if handle["ivf"] else self.lib.orc_flat_destroy)(handle["h"])
+
     # -- reference-only helpers ---------------------------------------------
     def train_codebook(self, s: OrcSpec, vectors, iters=25, seed=0) -> np.ndarray:
         assert self.kind == "reference"

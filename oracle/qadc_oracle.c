@@ -715,3 +715,57 @@ int orc_ivf_search(const orc_spec* s, const float* codebook, const float* coarse
     J.is_ivf = 1;
     return run_pool(&J, threads);
 }
+
+/* ---------------------------------------------------------- handle variants -- */
+
+typedef struct {
+    int is_ivf;
+    orc_spec s;
+    const float* cb;
+    const uint8_t* packed;
+    uint64_t count;
+    const float* coarse;
+    uint32_t k_cells;
+    const uint64_t *lbo, *lio, *lc;
+    const uint32_t* ids;
+} handle_t;
+
+void* orc_flat_create(const orc_spec* s, const float* codebook, const uint8_t* packed, uint64_t count) {
+    handle_t* h = (handle_t*)calloc(1, sizeof *h);
+    h->s = *s;
+    h->cb = codebook;
+    h->packed = packed;
+    h->count = count;
+    return h;
+}
+int orc_flat_search_h(void* hv, const float* queries, uint32_t nq, uint32_t r, uint32_t t, int family, int threads,
+                      uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {
+    handle_t* h = (handle_t*)hv;
+    return orc_flat_search(&h->s, h->cb, h->packed, h->count, queries, nq, r, t, family, threads, out_ids, out_dists,
+                           out_counts, NULL, NULL);
+}
+void orc_flat_destroy(void* h) { free(h); }
+
+void* orc_ivf_create(const orc_spec* s, const float* codebook, const float* coarse, uint32_t k_cells,
+                     const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
+                     const uint64_t* list_count, const uint32_t* ids) {
+    handle_t* h = (handle_t*)calloc(1, sizeof *h);
+    h->is_ivf = 1;
+    h->s = *s;
+    h->cb = codebook;
+    h->coarse = coarse;
+    h->k_cells = k_cells;
+    h->packed = packed;
+    h->lbo = list_byte_off;
+    h->lio = list_id_off;
+    h->lc = list_count;
+    h->ids = ids;
+    return h;
+}
+int orc_ivf_search_h(void* hv, const float* queries, uint32_t nq, uint32_t probes, uint32_t r, uint32_t t, int family,
+                     int threads, uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {
+    handle_t* h = (handle_t*)hv;
+    return orc_ivf_search(&h->s, h->cb, h->coarse, h->k_cells, h->packed, h->lbo, h->lio, h->lc, h->ids, queries, nq,
+                          probes, r, t, family, threads, out_ids, out_dists, out_counts);
+}
+void orc_ivf_destroy(void* h) { free(h); }

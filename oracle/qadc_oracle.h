@@ -135,6 +135,20 @@ int orc_ivf_search(const orc_spec* s, const float* codebook, const float* coarse
                    uint32_t probes, uint32_t r, uint32_t t, int family, int threads, uint32_t* out_ids,
                    float* out_dists, uint32_t* out_counts);
 
+/* Handle-based variants for timing (bench.py cpu_baseline): the index is built once, searches reuse it.
+ * The port keeps pointers into the caller's arrays (they must stay alive); the reference shim builds a
+ * pqscan::FlatIndex / pqscan::IvfIndex once. */
+void* orc_flat_create(const orc_spec* s, const float* codebook, const uint8_t* packed, uint64_t count);
+int orc_flat_search_h(void* h, const float* queries, uint32_t nq, uint32_t r, uint32_t t, int family, int threads,
+                      uint32_t* out_ids, float* out_dists, uint32_t* out_counts);
+void orc_flat_destroy(void* h);
+void* orc_ivf_create(const orc_spec* s, const float* codebook, const float* coarse, uint32_t k_cells,
+                     const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
+                     const uint64_t* list_count, const uint32_t* ids);
+int orc_ivf_search_h(void* h, const float* queries, uint32_t nq, uint32_t probes, uint32_t r, uint32_t t, int family,
+                     int threads, uint32_t* out_ids, float* out_dists, uint32_t* out_counts);
+void orc_ivf_destroy(void* h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -407,6 +407,101 @@ int orc_ivf_search(const orc_spec* s, const float* codebook, const float* coarse
     });
 }
 
+// ---- handle variants: build the reference index once, search many times ----
+
+struct RefFlat {
+    PqSpec spec;
+    FlatIndex index;
+    uint32_t dims;
+};
+struct RefIvf {
+    PqSpec spec;
+    IvfIndex index;
+    uint32_t dims;
+};
+
+void* orc_flat_create(const orc_spec* s, const float* codebook, const uint8_t* packed, uint64_t count) {
+    try {
+        return new RefFlat{spec_of(s), FlatIndex(codebook_of(s, codebook), list_of(s, packed, count, s->groups)), s->dims};
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+int orc_flat_search_h(void* hv, const float* queries, uint32_t nq, uint32_t r, uint32_t t, int family, int threads,
+                      uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {
+    return guarded([&] {
+        RefFlat* h = static_cast<RefFlat*>(hv);
+        SearchParams params;
+        params.r = r;
+        params.t = t;
+        params.forced_kernel = family_of(h->spec, family);
+        params.validate();
+        std::atomic<int> failed{0};
+        std::string err;
+        parallel_queries(nq, threads, [&](uint32_t q) {
+            try {
+                SearchResult res = h->index.search({queries + size_t{q} * h->dims, h->dims}, params);
+                out_counts[q] = static_cast<uint32_t>(res.ids.size());
+                std::copy(res.ids.begin(), res.ids.end(), out_ids + size_t{q} * r);
+                std::copy(res.dists.begin(), res.dists.end(), out_dists + size_t{q} * r);
+            } catch (const std::exception& e) {
+                if (!failed.exchange(1)) err = e.what();
+            }
+        });
+        if (failed) throw calibration_error(err);
+    });
+}
+void orc_flat_destroy(void* h) { delete static_cast<RefFlat*>(h); }
+
+void* orc_ivf_create(const orc_spec* s, const float* codebook, const float* coarse, uint32_t k_cells,
+                     const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
+                     const uint64_t* list_count, const uint32_t* ids) {
+    try {
+        std::vector<PackedList> lists(k_cells);
+        std::vector<std::vector<uint32_t>> lids(k_cells);
+        for (uint32_t c = 0; c < k_cells; ++c) {
+            lists[c] = list_of(s, packed + list_byte_off[c], list_count[c], s->groups);
+            lids[c].assign(ids + list_id_off[c], ids + list_id_off[c] + list_count[c]);
+        }
+        return new RefIvf{spec_of(s),
+                          IvfIndex(codebook_of(s, codebook), std::vector<float>(coarse, coarse + size_t{k_cells} * s->dims),
+                                   std::move(lists), std::move(lids)),
+                          s->dims};
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+int orc_ivf_search_h(void* hv, const float* queries, uint32_t nq, uint32_t probes, uint32_t r, uint32_t t, int family,
+                     int threads, uint32_t* out_ids, float* out_dists, uint32_t* out_counts) {
+    return guarded([&] {
+        RefIvf* h = static_cast<RefIvf*>(hv);
+        SearchParams params;
+        params.probes = probes;
+        params.r = r;
+        params.t = t;
+        params.forced_kernel = family_of(h->spec, family);
+        params.validate();
+        std::atomic<int> failed{0};
+        std::string err;
+        parallel_queries(nq, threads, [&](uint32_t q) {
+            try {
+                SearchResult res = h->index.search({queries + size_t{q} * h->dims, h->dims}, params);
+                out_counts[q] = static_cast<uint32_t>(res.ids.size());
+                std::copy(res.ids.begin(), res.ids.end(), out_ids + size_t{q} * r);
+                std::copy(res.dists.begin(), res.dists.end(), out_dists + size_t{q} * r);
+            } catch (const std::exception& e) {
+                if (!failed.exchange(1)) err = e.what();
+            }
+        });
+        if (failed) throw calibration_error(err);
+    });
+}
+void orc_ivf_destroy(void* h) { delete static_cast<RefIvf*>(h); }
+
 // ---- reference-only helpers (fixture generation; not part of the port) ----
 
 // train_codebook (codebook.hpp:66-91) -> flat codebook of s->cb_floats floats

@@ -43,6 +43,9 @@ static int guarded(F&& f) {
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
         if (p) cudaFree(p);
@@ -155,7 +158,8 @@ struct qadc_index {
     uint32_t calib_count = 0;
     // ivf
     uint32_t k_cells = 0;
-    DevBuf coarse, coarse_t, list_code_off, list_count_dev;
+    DevBuf coarse, coarse_t, list_code_off, list_count_dev, calib_code_off, calib_count_dev;
+    bool own_heads = true; // calibration heads alias the lists themselves (unsharded index)
     std::vector<uint64_t> list_code_off_h, list_count_h;
     uint64_t total_codes = 0;
     uint32_t ivf_round0 = 512; // list positions scanned in the first round (then x seg_growth per round)
@@ -443,13 +447,19 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         QADC_CUDA_CHECK(cudaMemsetAsync(h->cell_npairs.p, 0, size_t(K) * 4, st));
 
         const size_t t0 = h->timer.mark(st);
-        launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->order.as<uint32_t>(), st);
+        h->scratch.ensure(size_t(nb) * K * 4);
+        launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->scratch.as<float>(), h->order.as<uint32_t>(), st);
+        const size_t t1 = h->timer.mark(st);
         launch_ivf_tables(ds, h->codebook.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(), n_pairs, a,
                           h->luts.as<float>(), h->pmin.as<float>(), h->own_min.as<float>(), st);
-        launch_ivf_calib(ds, h->codes.as<uint8_t>(), h->list_code_off.as<uint64_t>(), h->list_count_dev.as<uint64_t>(),
-                         h->order.as<uint32_t>(), nb, a, h->luts.as<float>(), h->own_min.as<float>(), p.r, p.t,
+        const size_t t2 = h->timer.mark(st);
+        launch_ivf_calib(ds, h->own_heads ? h->codes.as<uint8_t>() : h->calib.as<uint8_t>(),
+                         h->own_heads ? h->list_code_off.as<uint64_t>() : h->calib_code_off.as<uint64_t>(),
+                         h->own_heads ? h->list_count_dev.as<uint64_t>() : h->calib_count_dev.as<uint64_t>(),
+                         h->list_count_dev.as<uint64_t>(), h->order.as<uint32_t>(), nb, a, h->luts.as<float>(), h->own_min.as<float>(), p.r, p.t,
                          h->qparams.as<float>(), h->map.as<float>(), h->cell_npairs.as<uint32_t>(),
                          h->pair_rank.as<uint32_t>(), st);
+        const size_t t3 = h->timer.mark(st);
         // rows are grouped by cell: the host lays the cells' tiles out back to back
         std::vector<uint32_t> npairs(K), tile_base(K);
         QADC_CUDA_CHECK(cudaMemcpyAsync(npairs.data(), h->cell_npairs.p, size_t(K) * 4, cudaMemcpyDeviceToHost, st));
@@ -470,12 +480,20 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
             QADC_CUDA_CHECK(cudaMemsetAsync(h->row_bias.p, 0, nslots * 4, st));
             QADC_CUDA_CHECK(cudaMemsetAsync(h->qlut.p, 0, nslots * ds.E * wb, st));
         }
+        const size_t t4 = h->timer.mark(st);
         launch_ivf_quantize(ds, h->order.as<uint32_t>(), n_pairs, a, h->luts.as<float>(), h->pmin.as<float>(),
                             h->own_min.as<float>(), h->qparams.as<float>(), h->pair_rank.as<uint32_t>(),
                             h->tile_base.as<uint32_t>(), tq, h->qlut.p, h->row_query.as<uint32_t>(),
                             h->row_bias.as<uint32_t>(), h->pair_slot.as<uint32_t>(), st);
+        const size_t t5 = h->timer.mark(st);
         launch_pack_tiles(plan.variant, h->qlut.p, ds.word_width, ds.E, uint32_t(nslots), tq, h->tile_lut.p, st);
-        h->timer.span(0, t0, h->timer.mark(st));
+        const size_t t6 = h->timer.mark(st);
+        h->timer.span(0, t0, t1, 101); // probe order
+        h->timer.span(0, t1, t2, 102); // residual tables
+        h->timer.span(0, t2, t3, 103); // calibration + grouping
+        h->timer.span(0, t3, t4, 104); // host: tile layout, memsets
+        h->timer.span(0, t4, t5, 105); // quantize
+        h->timer.span(0, t5, t6, 106); // tile pack
 
         h->sel.ensure(nb, p.r, cap);
         launch_init_select(h->sel.thr_key.as<uint64_t>(), h->sel.cand_count.as<uint32_t>(), h->sel.ntop.as<uint32_t>(),
@@ -493,6 +511,10 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         for (uint32_t c = 0; c < K; ++c)
             if (npairs[c]) longest = std::max(longest, h->list_count_h[c]);
         uint64_t pairs_scanned = 0;
+        std::vector<std::vector<ScanJob>> keep_jobs;        // host staging must outlive the async copies
+        std::vector<std::vector<uint32_t>> keep_begin;
+        std::vector<DevBuf> round_jobs(8), round_begin(8);  // one device buffer per round (no reuse hazards)
+        size_t round_no = 0;
         while (lo < longest) {
             uint64_t hi = lo + len;
             if (longest - hi < len) hi = longest; // fold a short tail into this round
@@ -534,10 +556,22 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                 }
                 while (cta + 1 < g) begin[++cta] = uint32_t(jobs.size());
                 begin[g] = uint32_t(jobs.size());
-                h->jobs.ensure(jobs.size() * sizeof(ScanJob));
-                h->cta_begin.ensure((size_t(g) + 1) * 4);
-                QADC_CUDA_CHECK(cudaMemcpyAsync(h->jobs.p, jobs.data(), jobs.size() * sizeof(ScanJob), cudaMemcpyHostToDevice, st));
-                QADC_CUDA_CHECK(cudaMemcpyAsync(h->cta_begin.p, begin.data(), (size_t(g) + 1) * 4, cudaMemcpyHostToDevice, st));
+                if (round_no >= round_jobs.size()) {
+                    QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+                    round_no = 0;
+                }
+                DevBuf& jb = round_jobs[round_no];
+                DevBuf& bb = round_begin[round_no];
+                ++round_no;
+                keep_jobs.push_back(std::move(jobs));
+                keep_begin.push_back(std::move(begin));
+                const std::vector<ScanJob>& jobs_h = keep_jobs.back();
+                const std::vector<uint32_t>& begin_h = keep_begin.back();
+                const size_t n_jobs = jobs_h.size();
+                jb.ensure(n_jobs * sizeof(ScanJob));
+                bb.ensure((size_t(g) + 1) * 4);
+                QADC_CUDA_CHECK(cudaMemcpyAsync(jb.p, jobs_h.data(), n_jobs * sizeof(ScanJob), cudaMemcpyHostToDevice, st));
+                QADC_CUDA_CHECK(cudaMemcpyAsync(bb.p, begin_h.data(), (size_t(g) + 1) * 4, cudaMemcpyHostToDevice, st));
                 ScanArgs sa{};
                 sa.codes = h->codes.as<uint8_t>();
                 sa.ids = h->ids.as<uint32_t>();
@@ -545,9 +579,9 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                 sa.tile_lut = h->tile_lut.p;
                 sa.row_query = h->row_query.as<uint32_t>();
                 sa.row_bias = h->row_bias.as<uint32_t>();
-                sa.jobs = h->jobs.as<ScanJob>();
-                sa.n_jobs = uint32_t(jobs.size());
-                sa.cta_begin = h->cta_begin.as<uint32_t>();
+                sa.jobs = jb.as<ScanJob>();
+                sa.n_jobs = uint32_t(n_jobs);
+                sa.cta_begin = bb.as<uint32_t>();
                 sa.thr_key = h->sel.thr_key.as<uint64_t>();
                 sa.cand = h->sel.cand.as<uint64_t>();
                 sa.cand_count = h->sel.cand_count.as<uint32_t>();
@@ -561,11 +595,10 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                                h->sel.cand.as<uint64_t>(), h->sel.cand_count.as<uint32_t>(), cap,
                                h->sel.thr_key.as<uint64_t>(), nb, p.r, st);
                 const size_t e2 = h->timer.mark(st);
-                h->timer.span(1, e0, e1, jobs.size());
+                h->timer.span(1, e0, e1, n_jobs);
                 h->timer.span(2, e1, e2);
                 h->stats.scan_launches += 1;
                 h->stats.segments += 1;
-                QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // job vectors go out of scope
             }
             if (hi == ~0ull) break;
             lo = hi;
@@ -987,8 +1020,9 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
     return guarded([&] {
         if (!spec || !codebook || !out || (k_cells && (!coarse || !list_byte_off || !list_id_off || !list_count)))
             throw Error(QADC_ERR_INPUT, "null argument");
-        if (calib_packed || calib_byte_off || calib_count)
-            throw Error(QADC_ERR_CONFIG, "ivf: sharded lists with replicated calibration heads are not supported yet");
+        const bool have_heads = calib_packed || calib_byte_off || calib_count;
+        if (have_heads && (!calib_byte_off || !calib_count))
+            throw Error(QADC_ERR_INPUT, "ivf: calib_byte_off and calib_count must be given together");
         validate_spec(*spec);
         set_device(device);
         std::unique_ptr<qadc_index> h(new qadc_index);
@@ -1046,6 +1080,35 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
         if (k_cells)
             launch_ivf_relayout(*spec, h->ds, tmp.as<uint8_t>(), boff.as<uint64_t>(), h->list_code_off.as<uint64_t>(),
                                 h->list_count_dev.as<uint64_t>(), k_cells, total_padded, h->codes.as<uint8_t>(), st);
+        if (have_heads) {
+            // replicated heads of the unsharded lists (first min(count, t_max) codes each): calibration input
+            h->own_heads = false;
+            std::vector<uint64_t> coff(k_cells);
+            uint64_t crun = 0, cbytes = 0;
+            for (uint32_t c = 0; c < k_cells; ++c) {
+                coff[c] = crun;
+                crun += (calib_count[c] + LIST_ALIGN - 1) / LIST_ALIGN * LIST_ALIGN;
+                if (calib_count[c]) cbytes = std::max<uint64_t>(cbytes, calib_byte_off[c] + qadc_packed_bytes(spec, calib_count[c]));
+            }
+            if (cbytes && !calib_packed) throw Error(QADC_ERR_INPUT, "null argument");
+            const uint64_t cpad = crun + CODE_PAD;
+            h->calib.ensure(size_t(cpad) * h->ds.code_stride);
+            h->calib_code_off.ensure(std::max<size_t>(size_t(k_cells) * 8, 16));
+            h->calib_count_dev.ensure(std::max<size_t>(size_t(k_cells) * 8, 16));
+            DevBuf ctmp, cboff;
+            ctmp.ensure(std::max<uint64_t>(cbytes, 16));
+            cboff.ensure(std::max<size_t>(size_t(k_cells) * 8, 16));
+            if (k_cells) {
+                QADC_CUDA_CHECK(cudaMemcpyAsync(h->calib_code_off.p, coff.data(), size_t(k_cells) * 8, cudaMemcpyHostToDevice, st));
+                QADC_CUDA_CHECK(cudaMemcpyAsync(h->calib_count_dev.p, calib_count, size_t(k_cells) * 8, cudaMemcpyHostToDevice, st));
+                QADC_CUDA_CHECK(cudaMemcpyAsync(cboff.p, calib_byte_off, size_t(k_cells) * 8, cudaMemcpyHostToDevice, st));
+            }
+            if (cbytes) QADC_CUDA_CHECK(cudaMemcpyAsync(ctmp.p, calib_packed, cbytes, cudaMemcpyHostToDevice, st));
+            if (k_cells)
+                launch_ivf_relayout(*spec, h->ds, ctmp.as<uint8_t>(), cboff.as<uint64_t>(), h->calib_code_off.as<uint64_t>(),
+                                    h->calib_count_dev.as<uint64_t>(), k_cells, cpad, h->calib.as<uint8_t>(), st);
+            QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // coff / temporaries go out of scope
+        }
         // ids ride in the same index space as the device codes
         std::vector<uint32_t> ids_padded(total_padded, 0xFFFFFFFFu);
         for (uint32_t c = 0; c < k_cells; ++c)
@@ -1067,8 +1130,9 @@ int qadc_ivf_probe_order(qadc_index* h, const float* queries, uint32_t nq, uint3
         h->queries.ensure(size_t(nq) * h->ds.dims * 4);
         h->order.ensure(size_t(nq) * a * 4);
         QADC_CUDA_CHECK(cudaMemcpyAsync(h->queries.p, queries, size_t(nq) * h->ds.dims * 4, cudaMemcpyHostToDevice, st));
+        h->scratch.ensure(size_t(nq) * h->k_cells * 4);
         launch_ivf_probe(h->queries.as<float>(), h->coarse_t.as<float>(), h->ds.dims, h->k_cells, nq, a,
-                         h->order.as<uint32_t>(), st);
+                         h->scratch.as<float>(), h->order.as<uint32_t>(), st);
         QADC_CUDA_CHECK(cudaMemcpyAsync(order, h->order.p, size_t(nq) * a * 4, cudaMemcpyDeviceToHost, st));
         QADC_CUDA_CHECK(cudaStreamSynchronize(st));
     });

@@ -138,12 +138,13 @@ void launch_ivf_relayout(const qadc_spec& s, const DevSpec& ds, const uint8_t* d
                          const uint64_t* d_code_off, const uint64_t* d_count, uint32_t k_cells, uint64_t total_padded,
                          uint8_t* d_codes, cudaStream_t stream);
 void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t dims, uint32_t k_cells, uint32_t nq,
-                      uint32_t a, uint32_t* d_order, cudaStream_t stream);
+                      uint32_t a, float* d_dist_scratch /* [nq][K] */, uint32_t* d_order, cudaStream_t stream);
 void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* d_queries, const float* d_coarse,
                        const uint32_t* d_order, uint32_t n_pairs, uint32_t a, float* d_luts, float* d_pmin,
                        float* d_own_min, cudaStream_t stream);
-void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_codes, const uint64_t* d_list_code_off,
-                      const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq, uint32_t a,
+void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_calib_codes, const uint64_t* d_calib_code_off,
+                      const uint64_t* d_calib_count, const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq,
+                      uint32_t a,
                       const float* d_luts, const float* d_own_min, uint32_t r, uint32_t t, float* d_qparams,
                       float* d_map, uint32_t* d_cell_npairs, uint32_t* d_pair_rank, cudaStream_t stream);
 void launch_ivf_quantize(const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a, const float* d_luts,

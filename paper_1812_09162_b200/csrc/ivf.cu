@@ -61,28 +61,58 @@ void launch_ivf_relayout(const qadc_spec& s, const DevSpec& ds, const uint8_t* d
 
 // ------------------------------------------------------------------ probe order --
 
-// One CTA (256 threads) per query.  coarse_t is the centroid matrix transposed to [dims][K] so
-// that lanes (= cells) read contiguously while each thread walks the dims serially.
-// dynamic smem: K keys (u64) + dims floats.
+// Coarse distances, register-tiled: a CTA owns 256 cells (one per thread) x PROBE_QT queries.  Each
+// thread walks the dims SERIALLY for every (query, cell) pair -- the reference's operation order,
+// index.hpp:254-258 -- but loads each centroid component once for all PROBE_QT queries (from the
+// transposed [dims][K] matrix, coalesced across cells), so the 8 MB matrix is read nq/16 times from
+// L2 instead of nq times.  Queries sit in shared memory as [dim][query] for 128-bit broadcast loads.
+static constexpr int PROBE_QT = 16;
+
 __global__ void __launch_bounds__(256)
-ivf_probe_kernel(const float* __restrict__ queries, const float* __restrict__ coarse_t, uint32_t dims,
-                 uint32_t k_cells, uint32_t a, uint32_t* __restrict__ order) {
+ivf_coarse_dist_kernel(const float* __restrict__ queries, const float* __restrict__ coarse_t, uint32_t dims,
+                       uint32_t k_cells, uint32_t nq, float* __restrict__ dist /* [nq][K] */) {
+    extern __shared__ __align__(16) float qs[]; // [dims][PROBE_QT]
+    const uint32_t q0 = blockIdx.y * PROBE_QT;
+    for (uint32_t u = threadIdx.x; u < dims * PROBE_QT; u += blockDim.x) {
+        const uint32_t qi = u % PROBE_QT, j = u / PROBE_QT;
+        qs[u] = q0 + qi < nq ? queries[size_t(q0 + qi) * dims + j] : 0.0f;
+    }
+    __syncthreads();
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= k_cells) return;
+    float acc[PROBE_QT];
+#pragma unroll
+    for (int i = 0; i < PROBE_QT; ++i) acc[i] = 0.0f;
+    for (uint32_t j = 0; j < dims; ++j) {
+        const float ctr = coarse_t[size_t(j) * k_cells + c];
+        const float4* qv = reinterpret_cast<const float4*>(qs + j * PROBE_QT);
+#pragma unroll
+        for (int v = 0; v < PROBE_QT / 4; ++v) {
+            const float4 x = qv[v];
+            float d;
+            d = __fsub_rn(x.x, ctr); acc[4 * v + 0] = __fadd_rn(acc[4 * v + 0], __fmul_rn(d, d));
+            d = __fsub_rn(x.y, ctr); acc[4 * v + 1] = __fadd_rn(acc[4 * v + 1], __fmul_rn(d, d));
+            d = __fsub_rn(x.z, ctr); acc[4 * v + 2] = __fadd_rn(acc[4 * v + 2], __fmul_rn(d, d));
+            d = __fsub_rn(x.w, ctr); acc[4 * v + 3] = __fadd_rn(acc[4 * v + 3], __fmul_rn(d, d));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < PROBE_QT; ++i)
+        if (q0 + i < nq) dist[size_t(q0 + i) * k_cells + c] = acc[i];
+}
+
+// One CTA (256 threads) per query: first a cells by (distance, cell) -- partial_sort on pairs,
+// index.hpp:261.  key = float bits << 32 | cell (distance >= +0, so float order == bit order).
+// dynamic smem: K keys (u64) + pow2(a) keys.
+__global__ void __launch_bounds__(256)
+ivf_probe_select_kernel(const float* __restrict__ dist, uint32_t k_cells, uint32_t a, uint32_t* __restrict__ order) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(sm_raw);
-    float* q = reinterpret_cast<float*>(keys + k_cells);
-    uint64_t* best = reinterpret_cast<uint64_t*>(q + ((dims + 1) & ~1u)); // a keys, then sorted in place
+    uint64_t* best = keys + k_cells;
     __shared__ SelectScratch sc;
     const uint32_t qi = blockIdx.x;
-    for (uint32_t d = threadIdx.x; d < dims; d += blockDim.x) q[d] = queries[size_t(qi) * dims + d];
-    __syncthreads();
-    for (uint32_t c = threadIdx.x; c < k_cells; c += blockDim.x) {
-        float acc = 0.0f;
-        for (uint32_t j = 0; j < dims; ++j) {
-            const float diff = __fsub_rn(q[j], coarse_t[size_t(j) * k_cells + c]);
-            acc = __fadd_rn(acc, __fmul_rn(diff, diff));
-        }
-        keys[c] = (uint64_t(__float_as_uint(acc)) << 32) | c; // acc >= +0: float order == bit order
-    }
+    for (uint32_t c = threadIdx.x; c < k_cells; c += blockDim.x)
+        keys[c] = (uint64_t(__float_as_uint(dist[size_t(qi) * k_cells + c])) << 32) | c;
     __syncthreads();
     auto key_at = [&](uint32_t i) -> uint64_t { return keys[i]; };
     uint32_t pow2 = 1;
@@ -113,65 +143,79 @@ ivf_probe_kernel(const float* __restrict__ queries, const float* __restrict__ co
 }
 
 void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t dims, uint32_t k_cells, uint32_t nq,
-                      uint32_t a, uint32_t* d_order, cudaStream_t stream) {
+                      uint32_t a, float* d_dist_scratch, uint32_t* d_order, cudaStream_t stream) {
     if (nq == 0 || a == 0) return;
     uint32_t pow2 = 1;
     while (pow2 < a) pow2 <<= 1;
-    const size_t smem = size_t(k_cells) * 8 + size_t((dims + 1) & ~1u) * 4 + size_t(pow2) * 8;
-    if (smem > 200 * 1024)
+    const size_t smem_sel = size_t(k_cells) * 8 + size_t(pow2) * 8;
+    if (smem_sel > 200 * 1024)
         throw Error(QADC_ERR_CONFIG, "ivf probe: coarse quantizer too large for the shared-memory selection "
                                      "(K*8 + probes*8 bytes must fit 200 KB)");
-    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    ivf_probe_kernel<<<nq, 256, smem, stream>>>(d_queries, d_coarse_t, dims, k_cells, a, d_order);
+    const size_t smem_d = size_t(dims) * PROBE_QT * 4;
+    if (smem_d > 200 * 1024) throw Error(QADC_ERR_CONFIG, "ivf probe: dims too large");
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_coarse_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_d)));
+    const dim3 grid((k_cells + 255) / 256, (nq + PROBE_QT - 1) / PROBE_QT);
+    ivf_coarse_dist_kernel<<<grid, 256, smem_d, stream>>>(d_queries, d_coarse_t, dims, k_cells, nq, d_dist_scratch);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_probe_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_sel)));
+    ivf_probe_select_kernel<<<nq, 256, smem_sel, stream>>>(d_dist_scratch, k_cells, a, d_order);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
 // ------------------------------------------------------------- residual tables --
 
-// One CTA per (query, probe) pair: residual = q - centroid (index.hpp:286), compute_tables,
-// per-table minima and their table-order sum (DistanceTables::min_total, distance.hpp:28-32).
+// One CTA walks IVF_PAIRS_PER_CTA consecutive (query, probe) pairs: residual = q - centroid
+// (index.hpp:286), compute_tables, per-table minima and their table-order sum
+// (DistanceTables::min_total, distance.hpp:28-32).
+static constexpr uint32_t IVF_PAIRS_PER_CTA = 8;
+
 __global__ void __launch_bounds__(256)
 ivf_tables_kernel(DevSpec ds, const float* __restrict__ codebook, const float* __restrict__ queries,
-                  const float* __restrict__ coarse, const uint32_t* __restrict__ order, uint32_t a,
+                  const float* __restrict__ coarse, const uint32_t* __restrict__ order, uint32_t a, uint32_t n_pairs,
                   float* __restrict__ luts, float* __restrict__ pmin_out, float* __restrict__ own_min) {
     extern __shared__ float smf[];
     float* res = smf;
     float* lut = res + ds.dims;
     float* pmin = lut + ds.E;
-    const uint32_t pair = blockIdx.x;
-    const uint32_t qi = pair / a;
-    const uint32_t cell = order[pair];
-    for (uint32_t d = threadIdx.x; d < ds.dims; d += blockDim.x)
-        res[d] = __fsub_rn(queries[size_t(qi) * ds.dims + d], coarse[size_t(cell) * ds.dims + d]);
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x) {
-        uint32_t j = 0;
-        while (j + 1 < ds.m && ds.ent_off[j + 1] <= e) ++j;
-        const uint32_t dsub = ds.dim_alloc[j];
-        const float* c = codebook + ds.cb_off[j] + size_t(e - ds.ent_off[j]) * dsub;
-        const float* qq = res + ds.dim_off[j];
-        float acc = 0.0f;
-        for (uint32_t t = 0; t < dsub; ++t) {
-            const float d = __fsub_rn(qq[t], c[t]);
-            acc = __fadd_rn(acc, __fmul_rn(d, d));
+    for (uint32_t k = 0; k < IVF_PAIRS_PER_CTA; ++k) {
+        const uint32_t pair = blockIdx.x * IVF_PAIRS_PER_CTA + k;
+        if (pair >= n_pairs) return;
+        const uint32_t qi = pair / a;
+        const uint32_t cell = order[pair];
+        __syncthreads(); // previous pair's shared data is no longer read
+        for (uint32_t d = threadIdx.x; d < ds.dims; d += blockDim.x)
+            res[d] = __fsub_rn(queries[size_t(qi) * ds.dims + d], coarse[size_t(cell) * ds.dims + d]);
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x) {
+            uint32_t j = 0;
+            while (j + 1 < ds.m && ds.ent_off[j + 1] <= e) ++j;
+            const uint32_t dsub = ds.dim_alloc[j];
+            const float* c = codebook + ds.cb_off[j] + size_t(e - ds.ent_off[j]) * dsub;
+            const float* qq = res + ds.dim_off[j];
+            float acc = 0.0f;
+            for (uint32_t t = 0; t < dsub; ++t) {
+                const float d = __fsub_rn(qq[t], c[t]);
+                acc = __fadd_rn(acc, __fmul_rn(d, d));
+            }
+            lut[e] = acc;
+            luts[size_t(pair) * ds.E + e] = acc;
         }
-        lut[e] = acc;
-        luts[size_t(pair) * ds.E + e] = acc;
-    }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < ds.m; j += blockDim.x) {
-        float mn = __int_as_float(0x7f800000);
-        const float* t = lut + ds.ent_off[j];
-        for (uint32_t i = 0; i < (1u << ds.bits[j]); ++i) mn = (t[i] < mn) ? t[i] : mn;
-        pmin[j] = mn;
-        pmin_out[size_t(pair) * ds.m + j] = mn;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float s = 0.0f;
-        for (uint32_t j = 0; j < ds.m; ++j) s = __fadd_rn(s, pmin[j]);
-        own_min[pair] = s;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < ds.m; j += blockDim.x) {
+            float mn = __int_as_float(0x7f800000);
+            const float* t = lut + ds.ent_off[j];
+            for (uint32_t i = 0; i < (1u << ds.bits[j]); ++i) mn = (t[i] < mn) ? t[i] : mn;
+            pmin[j] = mn;
+            pmin_out[size_t(pair) * ds.m + j] = mn;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float s = 0.0f;
+            for (uint32_t j = 0; j < ds.m; ++j) s = __fadd_rn(s, pmin[j]);
+            own_min[pair] = s;
+        }
     }
 }
 
@@ -181,8 +225,8 @@ void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* 
     if (n_pairs == 0) return;
     const size_t smem = sizeof(float) * (size_t(ds.dims) + ds.E + ds.m);
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    ivf_tables_kernel<<<n_pairs, 256, smem, stream>>>(ds, d_codebook, d_queries, d_coarse, d_order, a, d_luts, d_pmin,
-                                                      d_own_min);
+    ivf_tables_kernel<<<(n_pairs + IVF_PAIRS_PER_CTA - 1) / IVF_PAIRS_PER_CTA, 256, smem, stream>>>(
+        ds, d_codebook, d_queries, d_coarse, d_order, a, n_pairs, d_luts, d_pmin, d_own_min);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
@@ -192,9 +236,14 @@ void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* 
 // One CTA per query.  Also counts the (query, cell) pairs per cell for the row grouping and
 // records each pair's rank inside its cell.  dynamic smem: t floats + a uint32 (prefix starts).
 // qparams[q] = {d_min_global, d_max, delta, n_prefix}
+// calib_codes / calib_off / calib_count describe the HEADS of the unsharded lists (first min(count, t_max)
+// codes each): for an unsharded index they alias the lists themselves; a shard gets replicated heads so
+// that every rank derives the same map.  list_count is the LOCAL length (rows are only grouped for
+// lists this rank actually holds codes of).
 __global__ void __launch_bounds__(256)
 ivf_calib_kernel(DevSpec ds, const uint8_t* __restrict__ codes, const uint64_t* __restrict__ list_code_off,
-                 const uint64_t* __restrict__ list_count, const uint32_t* __restrict__ order, uint32_t a,
+                 const uint64_t* __restrict__ calib_count, const uint64_t* __restrict__ list_count,
+                 const uint32_t* __restrict__ order, uint32_t a,
                  const float* __restrict__ luts, const float* __restrict__ own_min, uint32_t r, uint32_t t,
                  float* __restrict__ qparams, float* __restrict__ map, uint32_t* __restrict__ cell_npairs,
                  uint32_t* __restrict__ pair_rank) {
@@ -212,7 +261,7 @@ ivf_calib_kernel(DevSpec ds, const uint8_t* __restrict__ codes, const uint64_t* 
             const float mt = own_min[size_t(qi) * a + i];
             dmin = (mt < dmin) ? mt : dmin;
             start[i] = taken;
-            const uint64_t cnt = list_count[ord[i]];
+            const uint64_t cnt = calib_count[ord[i]];
             taken += uint32_t(min(cnt, uint64_t(t - taken))); // index.hpp:305-306
         }
         start[a] = taken;
@@ -263,13 +312,14 @@ ivf_calib_kernel(DevSpec ds, const uint8_t* __restrict__ codes, const uint64_t* 
 }
 
 void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_codes, const uint64_t* d_list_code_off,
-                      const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq, uint32_t a,
+                      const uint64_t* d_calib_count, const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq,
+                      uint32_t a,
                       const float* d_luts, const float* d_own_min, uint32_t r, uint32_t t, float* d_qparams,
                       float* d_map, uint32_t* d_cell_npairs, uint32_t* d_pair_rank, cudaStream_t stream) {
     if (nq == 0) return;
     const size_t smem = size_t(t) * 4 + size_t(a + 1) * 4;
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_calib_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    ivf_calib_kernel<<<nq, 256, smem, stream>>>(ds, d_codes, d_list_code_off, d_list_count, d_order, a, d_luts,
+    ivf_calib_kernel<<<nq, 256, smem, stream>>>(ds, d_codes, d_list_code_off, d_calib_count, d_list_count, d_order, a, d_luts,
                                                 d_own_min, r, t, d_qparams, d_map, d_cell_npairs, d_pair_rank);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());

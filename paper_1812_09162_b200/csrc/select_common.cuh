@@ -9,6 +9,7 @@ struct SelectScratch {
     uint64_t prefix;
     uint32_t rank;
     uint32_t cnt_less, cnt_eq;
+    uint32_t bucket; // population of the bucket the r-th key fell into after the last pass
 };
 
 // Finds the r-th smallest (1-based) of key_at(0..total) whose significant bits are
@@ -51,12 +52,26 @@ __device__ uint64_t block_select_kth(KeyAt key_at, uint32_t total, uint32_t r, i
                     if (rank > excl && rank <= excl + loc[b]) {
                         sc->prefix = prefix | (uint64_t(threadIdx.x * 8 + b) << shift);
                         sc->rank = rank - excl;
+                        sc->bucket = loc[b];
                     }
                     excl += loc[b];
                 }
             }
         }
         __syncthreads();
+        if (sc->bucket == 1 && shift > 0) {
+            // the bucket holds exactly one key: it IS the r-th smallest; fetch its low bits and stop
+            const uint64_t pfx = sc->prefix;
+            const uint64_t hm = ~0ull << shift;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
+                const uint64_t k = key_at(i);
+                if ((k & hm) == (pfx & hm)) sc->prefix = k;
+            }
+            __syncthreads();
+            *eq_needed = 1;
+            return sc->prefix;
+        }
     }
     *eq_needed = sc->rank;
     return sc->prefix;

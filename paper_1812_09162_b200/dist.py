@@ -89,6 +89,38 @@ class ShardedFlatIndex:
         self.index.close()
 
 
+def shard_ivf_lists(spec: QadcSpec, packed, list_byte_off, list_id_off, list_count, ids, rank: int, world: int,
+                    t_max: int = 4096):
+    """IVF sharding: EVERY list is split evenly (on packed-block boundaries) across the ranks --
+    ids are explicit, so any split is legal (scan_scalar.hpp:60) -- and the first min(count, t_max) codes of every
+    unsharded list are replicated as calibration heads, so probe order, tables, d_min_global, d_max, delta and the
+    biases come out identical on every rank.  Returns the keyword arguments for :class:`IvfIndex`."""
+    packed = np.ascontiguousarray(packed, dtype=np.uint8)
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    k = len(list_count)
+    s_packed, s_ids, s_boff, s_ioff, s_cnt = [], [], [], [], []
+    c_packed, c_boff, c_cnt = [], [], []
+    b = i = cb = 0
+    for c in range(k):
+        n = int(list_count[c])
+        lp = packed[int(list_byte_off[c]): int(list_byte_off[c]) + packed_bytes(spec, n)]
+        rg = shard_ranges(n, world, spec.block_len)[rank]
+        sp = slice_packed(spec, lp, rg)
+        s_boff.append(b); s_ioff.append(i); s_cnt.append(rg.count)
+        s_packed.append(sp)
+        s_ids.append(ids[int(list_id_off[c]) + rg.start: int(list_id_off[c]) + rg.start + rg.count])
+        b += sp.size; i += rg.count
+        hn = min(n, t_max)
+        hp = lp[: packed_bytes(spec, hn)]
+        c_boff.append(cb); c_cnt.append(hn); c_packed.append(hp)
+        cb += hp.size
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs and sum(x.size for x in xs) else np.zeros(0, dt)  # noqa: E731
+    return dict(packed=cat(s_packed, np.uint8), list_byte_off=np.array(s_boff, np.uint64),
+                list_id_off=np.array(s_ioff, np.uint64), list_count=np.array(s_cnt, np.uint64),
+                ids=cat(s_ids, np.uint32), calib_packed=cat(c_packed, np.uint8),
+                calib_byte_off=np.array(c_boff, np.uint64), calib_count=np.array(c_cnt, np.uint64))
+
+
 def merge_keys_numpy(gathered: np.ndarray, r: int) -> np.ndarray:
     """Reference merge for tests: [world, nq, r] uint64 keys (padding = 2^64-1) -> [nq, r] smallest keys."""
     world, nq, _ = gathered.shape

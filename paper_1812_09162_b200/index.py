@@ -197,7 +197,9 @@ class IvfIndex(_Index):
     """IvfIndex (index.hpp:166-177): coarse partition + per-cell packed lists of residual codes."""
 
     def __init__(self, spec: QadcSpec, codebook, coarse, packed, list_byte_off, list_id_off, list_count, ids,
-                 device: int = 0):
+                 device: int = 0, calib_packed=None, calib_byte_off=None, calib_count=None):
+        """For a shard (every list split across ranks) pass ``calib_*``: the PackedLists of the first
+        min(count, t_max) codes of the UNSHARDED lists, so that every rank derives the same quantization map."""
         super().__init__()
         self.spec = spec
         self.device = device
@@ -216,9 +218,17 @@ class IvfIndex(_Index):
         if int(lc.sum()) != idv.size:
             raise QadcError(6, "ivf: list code count != id count")  # index.hpp:175
         self.total = int(lc.sum())
+        cpk = cbo = cc = None
+        if calib_packed is not None:
+            cpk = np.ascontiguousarray(calib_packed, dtype=np.uint8).reshape(-1)
+            cbo = np.ascontiguousarray(calib_byte_off, dtype=np.uint64)
+            cc = np.ascontiguousarray(calib_count, dtype=np.uint64)
+            if not (cbo.size == cc.size == self.k_cells):
+                raise QadcError(6, "ivf: calibration head section mismatch")
         check(lib().qadc_ivf_open(C.byref(spec), _p(cb, C.c_float), _p(co, C.c_float), C.c_uint32(self.k_cells),
                                   _p(pk, C.c_uint8), _p(lbo, C.c_uint64), _p(lio, C.c_uint64), _p(lc, C.c_uint64),
-                                  _p(idv, C.c_uint32), None, None, None, C.c_int(device), C.byref(self._h)))
+                                  _p(idv, C.c_uint32), _p(cpk, C.c_uint8), _p(cbo, C.c_uint64), _p(cc, C.c_uint64),
+                                  C.c_int(device), C.byref(self._h)))
 
     def size(self) -> int:
         return self.total

@@ -402,3 +402,45 @@ def test_cpp_integration_binary():
     out = subprocess.run([str(exe), "25"], capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "INTEGRATION OK" in out.stdout
+
+
+@pytest.mark.parametrize("world", [2, 5])
+def test_sharded_ivf_equals_unsharded(port, world):
+    """IVF sharding on one device: every list split across `world` ranks, heads replicated for calibration;
+    per-rank key lists merged by the CUDA merge kernel must equal the unsharded IvfIndex::search."""
+    import torch
+    from paper_1812_09162_b200.dist import shard_ivf_lists
+    dims, text, k_cells, n = 64, "12x{6,5,5}", 30, 40000
+    rng = np.random.default_rng(21)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 1.5).astype(np.float32)
+    coarse = (rng.standard_normal((k_cells, dims)) * 3).astype(np.float32)
+    packed, boff, ioff, counts, ids = _ivf_lists(rng, s, k_cells, n, empty=(3,))
+    queries = (rng.standard_normal((24, dims)) * 3).astype(np.float32)
+    probes, r, t = 7, 60, 300
+    want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=probes, r=r, t=t, threads=8)
+    dev = torch.device("cuda", 0)
+    d_q = torch.from_numpy(queries).to(dev)
+    keys = torch.empty((world, len(queries), r), dtype=torch.int64, device=dev)
+    qmap = torch.empty((len(queries), 2), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    params = qb.SearchParams(probes=probes, r=r, t=t)
+    for rank in range(world):
+        kw = shard_ivf_lists(s, packed, boff, ioff, counts, ids, rank, world, t_max=512)
+        with qb.IvfIndex(s, cb, coarse, kw["packed"], kw["list_byte_off"], kw["list_id_off"], kw["list_count"],
+                         kw["ids"], calib_packed=kw["calib_packed"], calib_byte_off=kw["calib_byte_off"],
+                         calib_count=kw["calib_count"]) as shard:
+            shard.search_device(d_q, params, None, None, None, d_keys=keys[rank], d_map=qmap, stream=stream)
+            torch.cuda.synchronize()
+    d_ids = torch.empty((len(queries), r), dtype=torch.int32, device=dev)
+    d_dists = torch.empty((len(queries), r), dtype=torch.float32, device=dev)
+    d_counts = torch.empty((len(queries),), dtype=torch.int32, device=dev)
+    qb.merge_topk_device(keys, world, len(queries), r, qmap, d_ids, d_dists, d_counts, 0, stream=stream)
+    torch.cuda.synchronize()
+    counts_g = d_counts.cpu().numpy().astype(np.uint32)
+    ids_g = d_ids.cpu().numpy().view(np.uint32)
+    dists_g = d_dists.cpu().numpy()
+    assert np.array_equal(counts_g, want[2])
+    for qi in range(len(queries)):
+        c = int(want[2][qi])
+        assert np.array_equal(ids_g[qi, :c], want[0][qi, :c]) and bits_equal(dists_g[qi, :c], want[1][qi, :c])
