@@ -20,7 +20,7 @@ SIFT/Deep-like data, see paper_1812_09162_b200/synth.py):
   c5  IVF K=16384, 12x{6,5,5} residual codes, d=128, N=6.25e7 per GPU (5e8 / 8), nprobe=64, Q=1e4
 Default c2 (configs[1]).  With --gpus N > 1 (torchrun, one rank per GPU) every rank holds one database
 shard of the per-GPU size above (weak scaling), queries are replicated and the per-query top-R lists are
-merged after one NCCL all_gather (flat workloads; the IVF workload runs on one GPU in this round).
+merged after one NCCL all_gather (IVF: every list is split across the ranks, list heads are replicated).
 """
 from __future__ import annotations
 
@@ -101,13 +101,13 @@ def make_flat(qb, spec, wl, rank, have_gpu):
     return dict(cb=cb, packed=packed, head=head, head_n=head_n, queries=queries)
 
 
-def make_ivf(qb, spec, wl, have_gpu):
+def make_ivf(qb, spec, wl, have_gpu, rank=0, world=1):
     """Config 5 stand-in: coarse centroids from Lloyd iterations on mixture samples, list sizes from the
     assignment histogram of a mixture sample scaled to N, uniform random residual codes, ids = positions."""
     from paper_1812_09162_b200 import synth
     import torch
     dims, n, K = wl["dims"], wl["n"], wl["k_cells"]
-    dev = torch.device("cuda", 0) if have_gpu else torch.device("cpu")
+    dev = torch.device("cuda", torch.cuda.current_device()) if have_gpu else torch.device("cpu")
     centres = synth.mixture_centres(dims, seed=1)
     t0 = time.time()
     sample = torch.from_numpy(synth.gaussian_mixture(max(4 * K, 300_000), dims, seed=7, centres=centres)).to(dev)
@@ -140,11 +140,22 @@ def make_ivf(qb, spec, wl, have_gpu):
     pbytes = np.array([qb.packed_bytes(spec, int(c)) for c in counts], dtype=np.uint64)
     boff = np.concatenate([[0], np.cumsum(pbytes)[:-1]]).astype(np.uint64)
     ioff = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
-    packed = np.random.default_rng(6).integers(0, 256, size=int(pbytes.sum()), dtype=np.uint8)
-    ids = np.arange(n, dtype=np.uint32)
-    queries = synth.gaussian_mixture(wl["nq"], dims, seed=3, centres=centres)
-    log(f"[bench] {n} residual codes in {K} lists ready in {time.time() - t0:.1f}s")
-    return dict(cb=cb, coarse=coarse, packed=packed, boff=boff, ioff=ioff, counts=counts, ids=ids, queries=queries)
+    packed0 = np.random.default_rng(6).integers(0, 256, size=int(pbytes.sum()), dtype=np.uint8)
+    packed = packed0 if rank == 0 else np.random.default_rng(6 + 1000 * rank).integers(
+        0, 256, size=int(pbytes.sum()), dtype=np.uint8)
+    ids = np.arange(n, dtype=np.uint32) + np.uint32(rank * n)
+    out = dict(cb=cb, coarse=coarse, packed=packed, boff=boff, ioff=ioff, counts=counts, ids=ids)
+    if world > 1:
+        # weak scaling: rank r holds the r-th slice of EVERY list (same slice lengths on every rank); the heads of
+        # the unsharded lists are rank 0's first codes, regenerated from rank 0's stream on every rank
+        hc = np.minimum(counts, 512).astype(np.uint64)
+        hbytes = np.array([qb.packed_bytes(spec, int(c)) for c in hc], dtype=np.uint64)
+        hoff = np.concatenate([[0], np.cumsum(hbytes)[:-1]]).astype(np.uint64)
+        heads = np.concatenate([packed0[int(b): int(b) + int(hb)] for b, hb in zip(boff, hbytes)])
+        out.update(calib_packed=heads, calib_byte_off=hoff, calib_count=hc)
+    out["queries"] = synth.gaussian_mixture(wl["nq"], dims, seed=3, centres=centres)
+    log(f"[bench] rank {rank}: {n} residual codes in {K} lists ready in {time.time() - t0:.1f}s")
+    return out
 
 
 # --------------------------------------------------------------------------- clocks --
@@ -311,8 +322,6 @@ def main():
     import torch
     if not have_gpu:
         raise SystemExit("bench.py: no CUDA device; the product has no CPU path (use --impl reference for the CPU arm)")
-    if ivf and world > 1:
-        raise SystemExit("bench.py: the IVF workload (c5) runs on one GPU in this round (IVF sharding is not built yet)")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
@@ -321,11 +330,13 @@ def main():
     params = qb.SearchParams(probes=wl.get("probes", 1), r=R, t=T)
     t0 = time.time()
     if ivf:
-        data = make_ivf(qb, spec, wl, have_gpu)
+        from paper_1812_09162_b200.dist import ShardedIndex
+        data = make_ivf(qb, spec, wl, have_gpu, rank, world)
         t0 = time.time()
         idx = qb.IvfIndex(spec, data["cb"], data["coarse"], data["packed"], data["boff"], data["ioff"],
-                          data["counts"], data["ids"], device=local_rank)
-        sharded = None
+                          data["counts"], data["ids"], device=local_rank, calib_packed=data.get("calib_packed"),
+                          calib_byte_off=data.get("calib_byte_off"), calib_count=data.get("calib_count"))
+        sharded = ShardedIndex(idx, local_rank) if world > 1 else None
     else:
         from paper_1812_09162_b200.dist import ShardedFlatIndex, ShardRange
         data = make_flat(qb, spec, wl, rank, have_gpu)

@@ -5,6 +5,7 @@
 // batched over queries.  Everything that touches data runs in CUDA kernels of this
 // library; there is no CPU fallback.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -164,7 +165,7 @@ struct qadc_index {
     uint64_t total_codes = 0;
     uint32_t ivf_round0 = 512; // list positions scanned in the first round (then x seg_growth per round)
     // ivf workspace
-    DevBuf order, pmin, own_min, qparams, cell_npairs, pair_rank, pair_slot, tile_base, row_query, row_bias, cta_begin;
+    DevBuf order, pmin, own_min, qparams, cell_npairs, pair_rank, pair_slot, tile_base, row_query, row_bias, cta_begin, round_begin;
     // options
     uint32_t cand_cap = 8192;
     uint32_t seg0 = 4096;
@@ -416,11 +417,9 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         h->stats.kernel_launches = g_launches;
         return;
     }
-    const ScanPlan plan = plan_for(h);
-    h->stats.scan_variant = plan.variant;
-    h->stats.query_tile = plan.tq;
+    ScanPlan plan = plan_for(h);
     const size_t wb = ds.word_width / 8;
-    const uint32_t tq = plan.tq;
+    uint32_t tq = plan.tq;
     h->status.ensure(4);
     h->counters.ensure(16);
     QADC_CUDA_CHECK(cudaMemsetAsync(h->status.p, 0, 4, st));
@@ -448,7 +447,9 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
 
         const size_t t0 = h->timer.mark(st);
         h->scratch.ensure(size_t(nb) * K * 4);
-        launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->scratch.as<float>(), h->order.as<uint32_t>(), st);
+        h->cta_begin.ensure(size_t(nb) * 4); // reused as the probe-selection redo flags
+        launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->scratch.as<float>(), h->cta_begin.as<uint32_t>(),
+                         h->order.as<uint32_t>(), st);
         const size_t t1 = h->timer.mark(st);
         launch_ivf_tables(ds, h->codebook.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(), n_pairs, a,
                           h->luts.as<float>(), h->pmin.as<float>(), h->own_min.as<float>(), st);
@@ -464,6 +465,28 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         std::vector<uint32_t> npairs(K), tile_base(K);
         QADC_CUDA_CHECK(cudaMemcpyAsync(npairs.data(), h->cell_npairs.p, size_t(K) * 4, cudaMemcpyDeviceToHost, st));
         QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (h->force_variant < 0 && plan.variant >= VAR_F16X4H && plan.variant <= VAR_F16X4H_C4) {
+            // rows per cell are known now: pick the tile height (128 / 64 / 32 rows, i.e. 1 / 2 / 4 codes per
+            // warp step) that minimises padded work = sum over cells of tiles * tile_rows * list_length
+            const ScanVariant cand[3] = {VAR_F16X4H, VAR_F16X4H_C2, VAR_F16X4H_C4};
+            const uint32_t rows[3] = {128, 64, 32};
+            double best = -1.0;
+            int pick = 0;
+            for (int v = 0; v < 3; ++v) {
+                double cost = 0.0;
+                for (uint32_t c = 0; c < K; ++c)
+                    if (npairs[c])
+                        cost += double((npairs[c] + rows[v] - 1) / rows[v]) * rows[v] * (double(h->list_count_h[c]) + 2048.0);
+                if (best < 0.0 || cost < best * 0.97) { // prefer the taller tile unless the gain is real
+                    best = cost;
+                    pick = v;
+                }
+            }
+            plan = plan_scan(ds, h->device, int(cand[pick]), h->cif);
+            tq = plan.tq;
+        }
+        h->stats.scan_variant = plan.variant;
+        h->stats.query_tile = plan.tq;
         uint32_t ntiles = 0;
         for (uint32_t c = 0; c < K; ++c) {
             tile_base[c] = ntiles;
@@ -505,104 +528,106 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                         h->sel.thr_key.as<uint64_t>(), st);
         h->timer.span(2, s0, h->timer.mark(st));
 
-        // rounds over list positions [lo, hi): the thresholds tighten between rounds
-        uint64_t lo = 0, len = std::max<uint32_t>(h->ivf_round0, 64);
+        // rounds over list positions [lo, hi): the thresholds tighten between rounds.  All rounds' jobs are
+        // built before the first launch and uploaded once (a pageable async copy would otherwise stall the host
+        // behind the previous round's kernels).
         uint64_t longest = 0;
         for (uint32_t c = 0; c < K; ++c)
             if (npairs[c]) longest = std::max(longest, h->list_count_h[c]);
+        struct Round {
+            size_t job_first, n_jobs, begin_first;
+            int grid;
+        };
+        std::vector<Round> rounds;
+        std::vector<ScanJob> jobs;
+        std::vector<uint32_t> begins;
+        std::vector<uint64_t> cost;
         uint64_t pairs_scanned = 0;
-        std::vector<std::vector<ScanJob>> keep_jobs;        // host staging must outlive the async copies
-        std::vector<std::vector<uint32_t>> keep_begin;
-        std::vector<DevBuf> round_jobs(8), round_begin(8);  // one device buffer per round (no reuse hazards)
-        size_t round_no = 0;
-        while (lo < longest) {
-            uint64_t hi = lo + len;
-            if (longest - hi < len) hi = longest; // fold a short tail into this round
-            if (hi >= longest) hi = ~0ull;
-            std::vector<ScanJob> jobs;
-            std::vector<uint64_t> cost;
+        {
+            uint64_t lo = 0, len = std::max<uint32_t>(h->ivf_round0, 64);
             const uint64_t max_chunk = 32768;
-            for (uint32_t c = 0; c < K; ++c) {
-                const uint64_t cnt = h->list_count_h[c];
-                if (!npairs[c] || cnt <= lo) continue;
-                const uint64_t end = std::min(cnt, hi);
-                const uint32_t tiles = (npairs[c] + tq - 1) / tq;
-                for (uint32_t t = 0; t < tiles; ++t)
-                    for (uint64_t b = lo; b < end; b += max_chunk) {
-                        ScanJob j{};
-                        j.code_off = h->list_code_off_h[c] + b;
-                        j.ids_off = j.code_off;
-                        j.n_codes = uint32_t(std::min(max_chunk, end - b));
-                        j.id_base = 0;
-                        j.row_begin = (tile_base[c] + t) * tq;
-                        j.n_rows = std::min(tq, npairs[c] - t * tq);
-                        jobs.push_back(j);
-                        cost.push_back(uint64_t(j.n_codes) + 1024); // + the tile load
-                        pairs_scanned += uint64_t(j.n_codes) * j.n_rows;
+            while (lo < longest) {
+                uint64_t hi = lo + len;
+                if (longest - hi < len) hi = longest; // fold a short tail into this round
+                if (hi >= longest) hi = ~0ull;
+                const size_t first = jobs.size();
+                cost.clear();
+                for (uint32_t c = 0; c < K; ++c) {
+                    const uint64_t cnt = h->list_count_h[c];
+                    if (!npairs[c] || cnt <= lo) continue;
+                    const uint64_t end = std::min(cnt, hi);
+                    const uint32_t tiles = (npairs[c] + tq - 1) / tq;
+                    for (uint32_t t = 0; t < tiles; ++t)
+                        for (uint64_t bpos = lo; bpos < end; bpos += max_chunk) {
+                            ScanJob j{};
+                            j.code_off = h->list_code_off_h[c] + bpos;
+                            j.ids_off = j.code_off;
+                            j.n_codes = uint32_t(std::min(max_chunk, end - bpos));
+                            j.id_base = 0;
+                            j.row_begin = (tile_base[c] + t) * tq;
+                            j.n_rows = std::min(tq, npairs[c] - t * tq);
+                            jobs.push_back(j);
+                            cost.push_back(uint64_t(j.n_codes) + 1024); // + the tile load
+                            pairs_scanned += uint64_t(j.n_codes) * j.n_rows;
+                        }
+                }
+                const size_t n = jobs.size() - first;
+                if (n) {
+                    // cost-balanced contiguous slices of the round's job list, one per CTA
+                    const int g = int(std::min<size_t>(size_t(grid), n));
+                    uint64_t total = 0;
+                    for (uint64_t cst : cost) total += cst;
+                    const size_t bfirst = begins.size();
+                    begins.resize(bfirst + size_t(g) + 1, uint32_t(n));
+                    uint64_t acc = 0;
+                    int cta = 0;
+                    begins[bfirst] = 0;
+                    for (size_t j = 0; j < n; ++j) {
+                        while (cta + 1 < g && acc >= total * uint64_t(cta + 1) / uint64_t(g)) begins[bfirst + size_t(++cta)] = uint32_t(j);
+                        acc += cost[j];
                     }
-            }
-            if (!jobs.empty()) {
-                // cost-balanced contiguous slices of the job list, one per CTA
-                const int g = int(std::min<size_t>(size_t(grid), jobs.size()));
-                uint64_t total = 0;
-                for (uint64_t cst : cost) total += cst;
-                std::vector<uint32_t> begin(size_t(g) + 1, uint32_t(jobs.size()));
-                uint64_t acc = 0;
-                int cta = 0;
-                begin[0] = 0;
-                for (size_t j = 0; j < jobs.size(); ++j) {
-                    while (cta + 1 < g && acc >= total * uint64_t(cta + 1) / uint64_t(g)) begin[++cta] = uint32_t(j);
-                    acc += cost[j];
+                    while (cta + 1 < g) begins[bfirst + size_t(++cta)] = uint32_t(n);
+                    begins[bfirst + size_t(g)] = uint32_t(n);
+                    rounds.push_back(Round{first, n, bfirst, g});
                 }
-                while (cta + 1 < g) begin[++cta] = uint32_t(jobs.size());
-                begin[g] = uint32_t(jobs.size());
-                if (round_no >= round_jobs.size()) {
-                    QADC_CUDA_CHECK(cudaStreamSynchronize(st));
-                    round_no = 0;
-                }
-                DevBuf& jb = round_jobs[round_no];
-                DevBuf& bb = round_begin[round_no];
-                ++round_no;
-                keep_jobs.push_back(std::move(jobs));
-                keep_begin.push_back(std::move(begin));
-                const std::vector<ScanJob>& jobs_h = keep_jobs.back();
-                const std::vector<uint32_t>& begin_h = keep_begin.back();
-                const size_t n_jobs = jobs_h.size();
-                jb.ensure(n_jobs * sizeof(ScanJob));
-                bb.ensure((size_t(g) + 1) * 4);
-                QADC_CUDA_CHECK(cudaMemcpyAsync(jb.p, jobs_h.data(), n_jobs * sizeof(ScanJob), cudaMemcpyHostToDevice, st));
-                QADC_CUDA_CHECK(cudaMemcpyAsync(bb.p, begin_h.data(), (size_t(g) + 1) * 4, cudaMemcpyHostToDevice, st));
-                ScanArgs sa{};
-                sa.codes = h->codes.as<uint8_t>();
-                sa.ids = h->ids.as<uint32_t>();
-                sa.qlut = h->qlut.p;
-                sa.tile_lut = h->tile_lut.p;
-                sa.row_query = h->row_query.as<uint32_t>();
-                sa.row_bias = h->row_bias.as<uint32_t>();
-                sa.jobs = jb.as<ScanJob>();
-                sa.n_jobs = uint32_t(n_jobs);
-                sa.cta_begin = bb.as<uint32_t>();
-                sa.thr_key = h->sel.thr_key.as<uint64_t>();
-                sa.cand = h->sel.cand.as<uint64_t>();
-                sa.cand_count = h->sel.cand_count.as<uint32_t>();
-                sa.cap = cap;
-                sa.overflow = h->sel.overflow.as<uint32_t>();
-                sa.counters = h->counters.as<unsigned long long>();
-                const size_t e0 = h->timer.mark(st);
-                launch_scan(plan, ds, sa, g, st);
-                const size_t e1 = h->timer.mark(st);
-                launch_tighten(h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad,
-                               h->sel.cand.as<uint64_t>(), h->sel.cand_count.as<uint32_t>(), cap,
-                               h->sel.thr_key.as<uint64_t>(), nb, p.r, st);
-                const size_t e2 = h->timer.mark(st);
-                h->timer.span(1, e0, e1, n_jobs);
-                h->timer.span(2, e1, e2);
-                h->stats.scan_launches += 1;
-                h->stats.segments += 1;
+                if (hi == ~0ull) break;
+                lo = hi;
+                len *= std::max<uint32_t>(h->seg_growth, 2);
             }
-            if (hi == ~0ull) break;
-            lo = hi;
-            len *= std::max<uint32_t>(h->seg_growth, 2);
+        }
+        h->jobs.ensure(std::max<size_t>(jobs.size() * sizeof(ScanJob), 16));
+        h->round_begin.ensure(std::max<size_t>(begins.size() * 4, 16));
+        if (!jobs.empty()) {
+            QADC_CUDA_CHECK(cudaMemcpyAsync(h->jobs.p, jobs.data(), jobs.size() * sizeof(ScanJob), cudaMemcpyHostToDevice, st));
+            QADC_CUDA_CHECK(cudaMemcpyAsync(h->round_begin.p, begins.data(), begins.size() * 4, cudaMemcpyHostToDevice, st));
+        }
+        for (const Round& rd : rounds) {
+            ScanArgs sa{};
+            sa.codes = h->codes.as<uint8_t>();
+            sa.ids = h->ids.as<uint32_t>();
+            sa.qlut = h->qlut.p;
+            sa.tile_lut = h->tile_lut.p;
+            sa.row_query = h->row_query.as<uint32_t>();
+            sa.row_bias = h->row_bias.as<uint32_t>();
+            sa.jobs = h->jobs.as<ScanJob>() + rd.job_first;
+            sa.n_jobs = uint32_t(rd.n_jobs);
+            sa.cta_begin = h->round_begin.as<uint32_t>() + rd.begin_first;
+            sa.thr_key = h->sel.thr_key.as<uint64_t>();
+            sa.cand = h->sel.cand.as<uint64_t>();
+            sa.cand_count = h->sel.cand_count.as<uint32_t>();
+            sa.cap = cap;
+            sa.overflow = h->sel.overflow.as<uint32_t>();
+            sa.counters = h->counters.as<unsigned long long>();
+            const size_t e0 = h->timer.mark(st);
+            launch_scan(plan, ds, sa, rd.grid, st);
+            const size_t e1 = h->timer.mark(st);
+            launch_tighten(h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad, h->sel.cand.as<uint64_t>(),
+                           h->sel.cand_count.as<uint32_t>(), cap, h->sel.thr_key.as<uint64_t>(), nb, p.r, st);
+            const size_t e2 = h->timer.mark(st);
+            h->timer.span(1, e0, e1, rd.n_jobs);
+            h->timer.span(2, e1, e2);
+            h->stats.scan_launches += 1;
+            h->stats.segments += 1;
         }
         std::vector<uint32_t> ov(nb);
         QADC_CUDA_CHECK(cudaMemcpyAsync(ov.data(), h->sel.overflow.p, size_t(nb) * 4, cudaMemcpyDeviceToHost, st));
@@ -1131,8 +1156,9 @@ int qadc_ivf_probe_order(qadc_index* h, const float* queries, uint32_t nq, uint3
         h->order.ensure(size_t(nq) * a * 4);
         QADC_CUDA_CHECK(cudaMemcpyAsync(h->queries.p, queries, size_t(nq) * h->ds.dims * 4, cudaMemcpyHostToDevice, st));
         h->scratch.ensure(size_t(nq) * h->k_cells * 4);
+        h->cta_begin.ensure(size_t(nq) * 4);
         launch_ivf_probe(h->queries.as<float>(), h->coarse_t.as<float>(), h->ds.dims, h->k_cells, nq, a,
-                         h->scratch.as<float>(), h->order.as<uint32_t>(), st);
+                         h->scratch.as<float>(), h->cta_begin.as<uint32_t>(), h->order.as<uint32_t>(), st);
         QADC_CUDA_CHECK(cudaMemcpyAsync(order, h->order.p, size_t(nq) * a * 4, cudaMemcpyDeviceToHost, st));
         QADC_CUDA_CHECK(cudaStreamSynchronize(st));
     });

@@ -63,6 +63,8 @@ enum ScanVariant : uint32_t {
     VAR_U16X1 = 2,   // any width, u16 entries in smem, 1 row per lane, 32-row tile, int32 accumulate
     VAR_U8X1 = 3,    // any width, u8 (high-byte for u16 tables) conservative filter, 32-row tile
     VAR_F16X4H = 4,  // u16 tables, fp16 HIGH-BYTE conservative filter, 4 rows per lane (LDS.64), 128-row tile
+    VAR_F16X4H_C2 = 5, // same, 2 codes per warp step, 64-row tile (short row groups: IVF)
+    VAR_F16X4H_C4 = 6, // same, 4 codes per warp step, 32-row tile
     VAR_COUNT
 };
 
@@ -138,7 +140,8 @@ void launch_ivf_relayout(const qadc_spec& s, const DevSpec& ds, const uint8_t* d
                          const uint64_t* d_code_off, const uint64_t* d_count, uint32_t k_cells, uint64_t total_padded,
                          uint8_t* d_codes, cudaStream_t stream);
 void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t dims, uint32_t k_cells, uint32_t nq,
-                      uint32_t a, float* d_dist_scratch /* [nq][K] */, uint32_t* d_order, cudaStream_t stream);
+                      uint32_t a, float* d_dist_scratch /* [nq][K] */, uint32_t* d_redo /* [nq] */, uint32_t* d_order,
+                      cudaStream_t stream);
 void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* d_queries, const float* d_coarse,
                        const uint32_t* d_order, uint32_t n_pairs, uint32_t a, float* d_luts, float* d_pmin,
                        float* d_own_min, cudaStream_t stream);

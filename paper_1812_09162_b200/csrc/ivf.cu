@@ -105,12 +105,14 @@ ivf_coarse_dist_kernel(const float* __restrict__ queries, const float* __restric
 // index.hpp:261.  key = float bits << 32 | cell (distance >= +0, so float order == bit order).
 // dynamic smem: K keys (u64) + pow2(a) keys.
 __global__ void __launch_bounds__(256)
-ivf_probe_select_kernel(const float* __restrict__ dist, uint32_t k_cells, uint32_t a, uint32_t* __restrict__ order) {
+ivf_probe_select_kernel(const float* __restrict__ dist, uint32_t k_cells, uint32_t a, uint32_t* __restrict__ order,
+                        const uint32_t* __restrict__ only_flagged) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(sm_raw);
     uint64_t* best = keys + k_cells;
     __shared__ SelectScratch sc;
     const uint32_t qi = blockIdx.x;
+    if (only_flagged && !only_flagged[qi]) return; // the fast kernel already produced this query's order
     for (uint32_t c = threadIdx.x; c < k_cells; c += blockDim.x)
         keys[c] = (uint64_t(__float_as_uint(dist[size_t(qi) * k_cells + c])) << 32) | c;
     __syncthreads();
@@ -142,8 +144,83 @@ ivf_probe_select_kernel(const float* __restrict__ dist, uint32_t k_cells, uint32
     for (uint32_t i = threadIdx.x; i < a; i += blockDim.x) order[size_t(qi) * a + i] = uint32_t(best[i]);
 }
 
+// Fast path of the probe selection (a <= 256): threshold-and-compact instead of a full radix select.
+// Every thread takes the minimum of its strided share of the K keys; the a-th smallest of those 256
+// minima is a real key, hence an upper bound T on the a-th smallest key overall.  A second pass
+// compacts the (typically ~a) keys <= T, which are then sorted.  Exact: ties are part of the key
+// (distance bits << 32 | cell).  If more than PROBE_CAND keys pass (massive ties), the query is
+// flagged and redone by the radix kernel.
+static constexpr uint32_t PROBE_CAND = 2048;
+
+__global__ void __launch_bounds__(256)
+ivf_probe_select_fast_kernel(const float* __restrict__ dist, uint32_t k_cells, uint32_t a,
+                             uint32_t* __restrict__ order, uint32_t* __restrict__ redo) {
+    __shared__ uint64_t mins[256];
+    __shared__ uint64_t cand[PROBE_CAND];
+    __shared__ uint32_t s_cnt;
+    const uint32_t qi = blockIdx.x, tid = threadIdx.x;
+    const float* d = dist + size_t(qi) * k_cells;
+    uint64_t m = KEY_INF;
+    for (uint32_t c = tid; c < k_cells; c += 256) m = min(m, (uint64_t(__float_as_uint(d[c])) << 32) | c);
+    mins[tid] = m;
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+    for (uint32_t size = 2; size <= 256; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            if (tid < 128) {
+                const uint32_t lo = 2 * tid - (tid & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t x = mins[lo], y = mins[hi];
+                if ((x > y) == up) {
+                    mins[lo] = y;
+                    mins[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    const uint64_t T = mins[a - 1]; // a <= min(256, K) guaranteed by the launcher
+    for (uint32_t base = 0; base < k_cells; base += 256) {
+        const uint32_t c = base + tid;
+        const uint64_t k = c < k_cells ? ((uint64_t(__float_as_uint(d[c])) << 32) | c) : KEY_INF;
+        const bool take = k <= T;
+        const uint32_t bal = __ballot_sync(0xffffffffu, take);
+        if (bal) {
+            uint32_t start = 0;
+            if ((tid & 31) == 0) start = atomicAdd(&s_cnt, uint32_t(__popc(bal)));
+            start = __shfl_sync(0xffffffffu, start, 0);
+            const uint32_t slot = start + __popc(bal & ((1u << (tid & 31)) - 1u));
+            if (take && slot < PROBE_CAND) cand[slot] = k;
+        }
+    }
+    __syncthreads();
+    const uint32_t n = s_cnt;
+    if (n > PROBE_CAND) {
+        if (tid == 0) redo[qi] = 1u;
+        return;
+    }
+    uint32_t pow2 = 2;
+    while (pow2 < n) pow2 <<= 1;
+    for (uint32_t i = n + tid; i < pow2; i += 256) cand[i] = KEY_INF;
+    __syncthreads();
+    for (uint32_t size = 2; size <= pow2; size <<= 1)
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = tid; i < pow2 / 2; i += 256) {
+                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t x = cand[lo], y = cand[hi];
+                if ((x > y) == up) {
+                    cand[lo] = y;
+                    cand[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = tid; i < a; i += 256) order[size_t(qi) * a + i] = uint32_t(cand[i]);
+}
+
 void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t dims, uint32_t k_cells, uint32_t nq,
-                      uint32_t a, float* d_dist_scratch, uint32_t* d_order, cudaStream_t stream) {
+                      uint32_t a, float* d_dist_scratch, uint32_t* d_redo /* [nq] */, uint32_t* d_order,
+                      cudaStream_t stream) {
     if (nq == 0 || a == 0) return;
     uint32_t pow2 = 1;
     while (pow2 < a) pow2 <<= 1;
@@ -159,7 +236,15 @@ void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t 
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_probe_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_sel)));
-    ivf_probe_select_kernel<<<nq, 256, smem_sel, stream>>>(d_dist_scratch, k_cells, a, d_order);
+    const bool fast = a <= 256 && a <= k_cells && k_cells >= 256;
+    if (fast) {
+        QADC_CUDA_CHECK(cudaMemsetAsync(d_redo, 0, size_t(nq) * 4, stream));
+        ivf_probe_select_fast_kernel<<<nq, 256, 0, stream>>>(d_dist_scratch, k_cells, a, d_order, d_redo);
+        ++g_launches;
+        QADC_CUDA_CHECK(cudaGetLastError());
+    }
+    // radix select: the only path for large a / tiny K, the fallback of flagged queries otherwise
+    ivf_probe_select_kernel<<<nq, 256, smem_sel, stream>>>(d_dist_scratch, k_cells, a, d_order, fast ? d_redo : nullptr);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
@@ -203,16 +288,23 @@ ivf_tables_kernel(DevSpec ds, const float* __restrict__ codebook, const float* _
             luts[size_t(pair) * ds.E + e] = acc;
         }
         __syncthreads();
-        for (uint32_t j = threadIdx.x; j < ds.m; j += blockDim.x) {
+        // per-table minima, one warp per table (min is order-independent, so a tree is exact)
+        for (uint32_t j = threadIdx.x >> 5; j < ds.m; j += blockDim.x >> 5) {
             float mn = __int_as_float(0x7f800000);
             const float* t = lut + ds.ent_off[j];
-            for (uint32_t i = 0; i < (1u << ds.bits[j]); ++i) mn = (t[i] < mn) ? t[i] : mn;
-            pmin[j] = mn;
-            pmin_out[size_t(pair) * ds.m + j] = mn;
+            for (uint32_t i = threadIdx.x & 31; i < (1u << ds.bits[j]); i += 32) mn = (t[i] < mn) ? t[i] : mn;
+            for (int o = 16; o > 0; o >>= 1) {
+                const float other = __shfl_xor_sync(0xffffffffu, mn, o);
+                mn = (other < mn) ? other : mn;
+            }
+            if ((threadIdx.x & 31) == 0) {
+                pmin[j] = mn;
+                pmin_out[size_t(pair) * ds.m + j] = mn;
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            float s = 0.0f;
+            float s = 0.0f; // table-order fp32 sum (distance.hpp:28-32)
             for (uint32_t j = 0; j < ds.m; ++j) s = __fadd_rn(s, pmin[j]);
             own_min[pair] = s;
         }
@@ -344,12 +436,14 @@ ivf_quantize_kernel(DevSpec ds, const uint32_t* __restrict__ order, uint32_t a, 
                     const float* __restrict__ qparams, const uint32_t* __restrict__ pair_rank,
                     const uint32_t* __restrict__ cell_tile_base, uint32_t tq, void* __restrict__ qluts,
                     uint32_t* __restrict__ row_query, uint32_t* __restrict__ row_bias,
-                    uint32_t* __restrict__ pair_slot) {
-    const uint32_t pair = blockIdx.x;
+                    uint32_t* __restrict__ pair_slot, uint32_t n_pairs) {
+  for (uint32_t kk = 0; kk < IVF_PAIRS_PER_CTA; ++kk) {
+    const uint32_t pair = blockIdx.x * IVF_PAIRS_PER_CTA + kk;
+    if (pair >= n_pairs) return;
     const uint32_t rank = pair_rank[pair];
     if (rank == 0xFFFFFFFFu) { // empty list: skipped by the search loop (index.hpp:321)
         if (threadIdx.x == 0) pair_slot[pair] = 0xFFFFFFFFu;
-        return;
+        continue;
     }
     const uint32_t qi = pair / a;
     const uint32_t slot = cell_tile_base[order[pair]] * tq + rank;
@@ -373,6 +467,7 @@ ivf_quantize_kernel(DevSpec ds, const uint32_t* __restrict__ order, uint32_t a, 
         row_bias[slot] = bias;
         pair_slot[pair] = slot;
     }
+  }
 }
 
 void launch_ivf_quantize(const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a, const float* d_luts,
@@ -380,8 +475,9 @@ void launch_ivf_quantize(const DevSpec& ds, const uint32_t* d_order, uint32_t n_
                          const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base, uint32_t tq, void* d_qluts,
                          uint32_t* d_row_query, uint32_t* d_row_bias, uint32_t* d_pair_slot, cudaStream_t stream) {
     if (n_pairs == 0) return;
-    ivf_quantize_kernel<<<n_pairs, 256, 0, stream>>>(ds, d_order, a, d_luts, d_pmin, d_own_min, d_qparams, d_pair_rank,
-                                                     d_cell_tile_base, tq, d_qluts, d_row_query, d_row_bias, d_pair_slot);
+    ivf_quantize_kernel<<<(n_pairs + IVF_PAIRS_PER_CTA - 1) / IVF_PAIRS_PER_CTA, 256, 0, stream>>>(
+        ds, d_order, a, d_luts, d_pmin, d_own_min, d_qparams, d_pair_rank, d_cell_tile_base, tq, d_qluts, d_row_query,
+        d_row_bias, d_pair_slot, n_pairs);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }

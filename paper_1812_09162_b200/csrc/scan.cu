@@ -130,6 +130,7 @@ struct GeomRT {
 //   ROWB   bytes of one [entry] line in shared memory = TQ * sizeof(entry)
 
 struct PolF16x8 { // u8 tables only
+    static constexpr int CPW = 1;
     static constexpr int QPL = 8, TQ = 256, ROWB = 512, LOG_ROWB = 9, LANE_B = 16;
     static constexpr bool EXACT_FILTER = true;
     using Entry = __half;
@@ -163,6 +164,7 @@ struct PolF16x8 { // u8 tables only
 };
 
 struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
+    static constexpr int CPW = 1;
     static constexpr int QPL = 2, TQ = 64, ROWB = 256, LOG_ROWB = 8, LANE_B = 8;
     static constexpr bool EXACT_FILTER = true;
     using Entry = float;
@@ -184,8 +186,14 @@ struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
     static constexpr float BIG = 1.0e9f, HALF = 0.5f;
 };
 
-struct PolF16x4H { // u16 tables: fp16 image of the HIGH byte of every entry; conservative filter
-    static constexpr int QPL = 4, TQ = 128, ROWB = 256, LOG_ROWB = 8, LANE_B = 8;
+// u16 tables: fp16 image of the HIGH byte of every entry; conservative filter.  CPW = codes per warp
+// step: the warp's lanes split into CPW groups, each group walks a DIFFERENT code of the same list
+// against a tile of 128/CPW rows.  Bytes per wavefront and instructions per pair are unchanged, but
+// short row groups (IVF: ~40 (query, cell) pairs per cell) waste far fewer padded rows.
+template <int CPW_>
+struct PolF16x4H_T {
+    static constexpr int CPW = CPW_;
+    static constexpr int QPL = 4, TQ = 128 / CPW, ROWB = 256 / CPW, LOG_ROWB = (CPW == 1 ? 8 : CPW == 2 ? 7 : 6), LANE_B = 8;
     static constexpr bool EXACT_FILTER = false;
     using Entry = __half;
     struct Acc {
@@ -211,8 +219,12 @@ struct PolF16x4H { // u16 tables: fp16 image of the HIGH byte of every entry; co
     __device__ static float value(const Acc&, int) { return 0.f; } // never used: the filter is not exact
     static constexpr float BIG = 30000.0f, HALF = 0.5f;
 };
+using PolF16x4H = PolF16x4H_T<1>;
+using PolF16x4H_C2 = PolF16x4H_T<2>;
+using PolF16x4H_C4 = PolF16x4H_T<4>;
 
 struct PolU16x1 { // any width, u16 entries, int32 accumulate
+    static constexpr int CPW = 1;
     static constexpr int QPL = 1, TQ = 32, ROWB = 64, LOG_ROWB = 6, LANE_B = 2;
     static constexpr bool EXACT_FILTER = true;
     using Entry = unsigned short;
@@ -228,6 +240,7 @@ struct PolU16x1 { // any width, u16 entries, int32 accumulate
 };
 
 struct PolU8x1 { // any width; u16 tables keep only the HIGH byte: a conservative filter
+    static constexpr int CPW = 1;
     static constexpr int QPL = 1, TQ = 32, ROWB = 32, LOG_ROWB = 5, LANE_B = 1;
     static constexpr bool EXACT_FILTER = false;
     using Entry = unsigned char;
@@ -375,7 +388,9 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
         for (int s = 0; s < P::QPL; ++s) t[s] = P::BIG;
         P::init(acc0, t);
     }
-    const uint32_t lane_off = lane * P::LANE_B;
+    constexpr uint32_t LPC = 32 / P::CPW;             // lanes per code
+    const uint32_t lane_in = lane % LPC, lane_code = lane / LPC;
+    const uint32_t lane_off = lane_in * P::LANE_B;
     // per-warp queue of flagged pairs: ballot-compacted in the hot loop, resolved 32 at a time
     uint32_t* wq_row = reinterpret_cast<uint32_t*>(stage + NSTAGE * STAGE_BYTES) + warp * (WQ_CAP * 3);
     uint32_t* wq_idx = wq_row + WQ_CAP;
@@ -404,7 +419,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
             float t[P::QPL];
 #pragma unroll
             for (int s = 0; s < P::QPL; ++s) {
-                const uint32_t r = lane * P::QPL + s;
+                const uint32_t r = lane_in * P::QPL + s;
                 t[s] = P::BIG; // rows past the tile never admit
                 if (r < job.n_rows) {
                     const uint32_t row = job.row_begin + r;
@@ -462,7 +477,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                             if (qn + 32 > WQ_CAP) flush();
                             if (hs) {
                                 const uint32_t slot = qn + __popc(m & lanemask_lt);
-                                wq_row[slot] = job.row_begin + lane * P::QPL + sl;
+                                wq_row[slot] = job.row_begin + lane_in * P::QPL + sl;
                                 wq_idx[slot] = i;
                                 wq_val[slot] = P::value(acc, sl);
                             }
@@ -473,12 +488,13 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
             };
 
             if constexpr (!G::RUNTIME) {
-                for (uint32_t i0 = warp; i0 < cnt; i0 += SCAN_WARPS * CIF) {
+                for (uint32_t i0 = warp * P::CPW + lane_code; i0 < cnt + lane_code; i0 += SCAN_WARPS * P::CPW * CIF) {
+                    // (the loop bound is warp-uniform: i0 - lane_code is; lanes past the end are clamped + masked)
                     uint32_t cw[CIF][G::CW];
                     typename P::Acc acc[CIF];
 #pragma unroll
                     for (int c = 0; c < CIF; ++c) {
-                        const uint32_t i = min(i0 + c * SCAN_WARPS, cnt - 1); // clamp: duplicates are ignored below
+                        const uint32_t i = min(i0 + c * SCAN_WARPS * P::CPW, cnt - 1); // clamp: duplicates are ignored below
                         const uint32_t* src = reinterpret_cast<const uint32_t*>(sb + size_t(i) * G::STRIDE);
                         if constexpr (G::CW == 2) {
                             const uint2 v = *reinterpret_cast<const uint2*>(src);
@@ -504,18 +520,20 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                         }
                     });
 #pragma unroll
-                    for (int c = 0; c < CIF; ++c) flag(acc[c], i0 + c * SCAN_WARPS < cnt, i0 + c * SCAN_WARPS);
+                    for (int c = 0; c < CIF; ++c)
+                        flag(acc[c], i0 + c * SCAN_WARPS * P::CPW < cnt, i0 + c * SCAN_WARPS * P::CPW);
                 }
             } else {
                 // runtime geometry: any m / widths / code size that fits; one code per warp step
-                for (uint32_t i = warp; i < cnt; i += SCAN_WARPS) {
+                for (uint32_t iw = warp * P::CPW; iw < cnt; iw += SCAN_WARPS * P::CPW) {
+                    const uint32_t i = min(iw + lane_code, cnt - 1);
                     const uint8_t* code = reinterpret_cast<const uint8_t*>(sb + size_t(i) * stride);
                     typename P::Acc acc = acc0;
                     for (uint32_t j = 0; j < ds->m; ++j) {
                         const uint32_t idx = rt_sub_index(ds, code, j);
                         P::add(acc, tile + size_t(ds->ent_off[j] + idx) * P::ROWB + lane_off);
                     }
-                    flag(acc, true, i);
+                    flag(acc, iw + lane_code < cnt, i);
                 }
             }
             flush(); // queued pairs reference this stage buffer: resolve them before releasing it
@@ -540,6 +558,8 @@ const char* variant_name(uint32_t v) {
     case VAR_U16X1: return "u16x1 (u16 entries, 32-query tile, int32 accumulate)";
     case VAR_U8X1: return "u8x1 (high-byte filter, 32-query tile)";
     case VAR_F16X4H: return "f16x4h (u16 tables, fp16 high-byte filter + exact re-evaluation, 128-query tile, LDS.64)";
+    case VAR_F16X4H_C2: return "f16x4h-c2 (as f16x4h, 2 codes per warp step, 64-row tile)";
+    case VAR_F16X4H_C4: return "f16x4h-c4 (as f16x4h, 4 codes per warp step, 32-row tile)";
     }
     return "?";
 }
@@ -575,8 +595,12 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int cif) {
         case VAR_U16X1: set(VAR_U16X1, PolU16x1::TQ, smem_need<PolU16x1>(ds.E)); break;
         case VAR_U8X1: set(VAR_U8X1, PolU8x1::TQ, smem_need<PolU8x1>(ds.E)); break;
         case VAR_F16X4H:
+        case VAR_F16X4H_C2:
+        case VAR_F16X4H_C4:
             if (u8) throw Error(QADC_ERR_CONFIG, "scan: f16x4h is the 16-bit-table filter");
-            set(VAR_F16X4H, PolF16x4H::TQ, smem_need<PolF16x4H>(ds.E));
+            if (force_variant == VAR_F16X4H) set(VAR_F16X4H, PolF16x4H::TQ, smem_need<PolF16x4H>(ds.E));
+            else if (force_variant == VAR_F16X4H_C2) set(VAR_F16X4H_C2, PolF16x4H_C2::TQ, smem_need<PolF16x4H_C2>(ds.E));
+            else set(VAR_F16X4H_C4, PolF16x4H_C4::TQ, smem_need<PolF16x4H_C4>(ds.E));
             break;
         default: throw Error(QADC_ERR_CONFIG, "scan: unknown forced variant");
         }
@@ -636,6 +660,12 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, 
         if (G664::matches(ds)) return launch_one<PolF16x4H, G664>(plan, ds, args, grid, stream);
         if (G555::matches(ds)) return launch_one<PolF16x4H, G555>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_F16X4H_C2:
+        if (G655::matches(ds)) return launch_one<PolF16x4H_C2, G655>(plan, ds, args, grid, stream);
+        return launch_one<PolF16x4H_C2, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_F16X4H_C4:
+        if (G655::matches(ds)) return launch_one<PolF16x4H_C4, G655>(plan, ds, args, grid, stream);
+        return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
     default: throw Error(QADC_ERR_CONFIG, "scan: bad variant");
     }
 }

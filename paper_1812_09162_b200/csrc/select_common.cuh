@@ -27,9 +27,23 @@ __device__ uint64_t block_select_kth(KeyAt key_at, uint32_t total, uint32_t r, i
         __syncthreads();
         const uint64_t prefix = sc->prefix;
         const uint64_t himask = shift + 8 >= 64 ? 0ull : (~0ull << (shift + 8));
-        for (uint32_t i = threadIdx.x; i < total; i += blockDim.x) {
-            const uint64_t k = key_at(i);
-            if ((k & himask) == (prefix & himask)) atomicAdd(&sc->hist[(k >> shift) & 255u], 1u);
+        // Keys of one query share their leading bytes, so a plain histogram would hammer one bin with
+        // serialised same-address atomics: aggregate equal digits inside the warp first (one atomic per
+        // distinct digit per warp).  The loop bound is warp-uniform so that ballot/match are legal.
+        for (uint32_t base = 0; base < total; base += blockDim.x) {
+            const uint32_t i = base + threadIdx.x;
+            uint64_t k = 0;
+            bool live = i < total;
+            if (live) {
+                k = key_at(i);
+                live = (k & himask) == (prefix & himask);
+            }
+            const uint32_t digit = uint32_t(k >> shift) & 255u;
+            const uint32_t act = __ballot_sync(0xffffffffu, live);
+            if (live) {
+                const uint32_t peers = __match_any_sync(act, digit);
+                if ((threadIdx.x & 31u) == uint32_t(__ffs(peers) - 1)) atomicAdd(&sc->hist[digit], uint32_t(__popc(peers)));
+            }
         }
         __syncthreads();
         if (threadIdx.x < 32) { // lane l owns bins 8l..8l+7

@@ -73,7 +73,9 @@ static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n
 size_t tile_entry_bytes(ScanVariant v) {
     switch (v) {
     case VAR_F16X8:
-    case VAR_F16X4H: return 2;
+    case VAR_F16X4H:
+    case VAR_F16X4H_C2:
+    case VAR_F16X4H_C4: return 2;
     case VAR_F32X2: return 4;
     case VAR_U16X1: return 2;
     case VAR_U8X1: return 1;
@@ -85,7 +87,9 @@ void launch_pack_tiles(ScanVariant v, const void* qlut, uint32_t width, uint32_t
                        void* out, cudaStream_t stream) {
     switch (v) {
     case VAR_F16X8: return launch_pack<__half>(qlut, width, E, n_rows, tq, false, out, stream);
-    case VAR_F16X4H: return launch_pack<__half>(qlut, width, E, n_rows, tq, true, out, stream);
+    case VAR_F16X4H:
+    case VAR_F16X4H_C2:
+    case VAR_F16X4H_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, true, out, stream);
     case VAR_F32X2: return launch_pack<float>(qlut, width, E, n_rows, tq, false, out, stream);
     case VAR_U16X1: return launch_pack<unsigned short>(qlut, width, E, n_rows, tq, false, out, stream);
     case VAR_U8X1: return launch_pack<unsigned char>(qlut, width, E, n_rows, tq, false, out, stream);

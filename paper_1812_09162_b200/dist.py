@@ -52,23 +52,19 @@ def global_head(spec: QadcSpec, packed: np.ndarray, total: int, t_max: int = 409
     return packed[: packed_bytes(spec, n)], n
 
 
-class ShardedFlatIndex:
-    """A FlatIndex shard per rank plus the gather + merge exchange.
+class ShardedIndex:
+    """One index shard per rank (flat or IVF) plus the gather + merge exchange (NCCL all_gather of the per-rank
+    key lists, then the CUDA merge kernel qadc_merge_topk_device)."""
 
-    ``merge_fn`` exists so that the CPU (gloo) tests can exercise the host logic with a numpy merge; the
-    product path always uses the CUDA merge kernel (qadc_merge_topk_device)."""
-
-    def __init__(self, spec: QadcSpec, codebook, shard_packed, shard: ShardRange, head_packed, head_count, device,
-                 group=None):
+    def __init__(self, index, device, group=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = device
-        self.spec = spec
-        self.index = FlatIndex(spec, codebook, shard_packed, shard.count, base_id=shard.start,
-                               calib_packed=head_packed, calib_count=head_count, device=device)
+        self.spec = index.spec
+        self.index = index
 
     def search_device(self, d_queries, params: SearchParams, d_ids, d_dists, d_counts, stream=None):
         """All tensors are torch CUDA tensors on this rank's device; results are replicated on every rank."""
@@ -87,6 +83,15 @@ class ShardedFlatIndex:
 
     def close(self):
         self.index.close()
+
+
+class ShardedFlatIndex(ShardedIndex):
+    """A FlatIndex shard per rank: contiguous block-aligned code range, base_id, replicated global head."""
+
+    def __init__(self, spec: QadcSpec, codebook, shard_packed, shard: ShardRange, head_packed, head_count, device,
+                 group=None):
+        super().__init__(FlatIndex(spec, codebook, shard_packed, shard.count, base_id=shard.start,
+                                   calib_packed=head_packed, calib_count=head_count, device=device), device, group)
 
 
 def shard_ivf_lists(spec: QadcSpec, packed, list_byte_off, list_id_off, list_count, ids, rank: int, world: int,

@@ -444,3 +444,27 @@ def test_sharded_ivf_equals_unsharded(port, world):
     for qi in range(len(queries)):
         c = int(want[2][qi])
         assert np.array_equal(ids_g[qi, :c], want[0][qi, :c]) and bits_equal(dists_g[qi, :c], want[1][qi, :c])
+
+
+def test_ivf_probe_order_massive_ties(port):
+    """2100 coarse centroids of which 2080 coincide: every distance ties, the fast probe selection overflows its
+    candidate buffer and must fall back to the radix path; order is still (distance, cell) exact."""
+    dims, text, k_cells = 32, "8x{4,4}", 2100
+    rng = np.random.default_rng(31)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = rng.standard_normal(s.cb_floats).astype(np.float32)
+    coarse = np.tile(rng.standard_normal((1, dims)).astype(np.float32), (k_cells, 1))
+    coarse[:20] = rng.standard_normal((20, dims)).astype(np.float32) * 0.1
+    packed, boff, ioff, counts, ids = _ivf_lists(rng, s, k_cells, 6000)
+    queries = rng.standard_normal((5, dims)).astype(np.float32)
+    with qb.IvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids) as idx:
+        for a in (7, 64, 256):
+            order = idx.probe_order(queries, a)
+            for qi in range(5):
+                assert np.array_equal(order[qi], port.probe_order(dims, coarse, queries[qi], a))
+        want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=40, r=20, t=100)
+        got = idx.search(queries, qb.SearchParams(probes=40, r=20, t=100))
+        assert np.array_equal(got.counts, want[2])
+        for qi in range(5):
+            c = int(want[2][qi])
+            assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]) and bits_equal(got.dists[qi, :c], want[1][qi, :c])
