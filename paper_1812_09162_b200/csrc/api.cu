@@ -471,8 +471,13 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
             const ScanVariant cand[3] = {VAR_F16X4H, VAR_F16X4H_C2, VAR_F16X4H_C4};
             const uint32_t rows[3] = {128, 64, 32};
             double best = -1.0;
-            int pick = 0;
+            int pick = int(plan.variant) - int(VAR_F16X4H);
             for (int v = 0; v < 3; ++v) {
+                try {
+                    (void)plan_scan(ds, h->device, int(cand[v]), h->cif); // does this tile height fit shared memory?
+                } catch (const Error&) {
+                    continue;
+                }
                 double cost = 0.0;
                 for (uint32_t c = 0; c < K; ++c)
                     if (npairs[c])

@@ -65,6 +65,7 @@ enum ScanVariant : uint32_t {
     VAR_F16X4H = 4,  // u16 tables, fp16 HIGH-BYTE conservative filter, 4 rows per lane (LDS.64), 128-row tile
     VAR_F16X4H_C2 = 5, // same, 2 codes per warp step, 64-row tile (short row groups: IVF)
     VAR_F16X4H_C4 = 6, // same, 4 codes per warp step, 32-row tile
+    VAR_F16X4_C4 = 7,  // u8 tables exact in fp16, 4 codes per warp step, 32-row tile (large 8-bit tables: 8x{8})
     VAR_COUNT
 };
 

@@ -190,11 +190,12 @@ struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
 // step: the warp's lanes split into CPW groups, each group walks a DIFFERENT code of the same list
 // against a tile of 128/CPW rows.  Bytes per wavefront and instructions per pair are unchanged, but
 // short row groups (IVF: ~40 (query, cell) pairs per cell) waste far fewer padded rows.
-template <int CPW_>
+// HIGH = false is the exact twin for 8-bit tables (entries <= 255 are exact in fp16, as in f16x8).
+template <int CPW_, bool HIGH = true>
 struct PolF16x4H_T {
     static constexpr int CPW = CPW_;
     static constexpr int QPL = 4, TQ = 128 / CPW, ROWB = 256 / CPW, LOG_ROWB = (CPW == 1 ? 8 : CPW == 2 ? 7 : 6), LANE_B = 8;
-    static constexpr bool EXACT_FILTER = false;
+    static constexpr bool EXACT_FILTER = !HIGH;
     using Entry = __half;
     struct Acc {
         __half2 h[2];
@@ -216,12 +217,16 @@ struct PolF16x4H_T {
         const uint32_t* u = reinterpret_cast<const uint32_t*>(a.h);
         return (u[s >> 1] >> ((s & 1) * 16 + 15)) & 1u;
     }
-    __device__ static float value(const Acc&, int) { return 0.f; } // never used: the filter is not exact
+    // only used when the filter is exact (HIGH == false)
+    __device__ static float value(const Acc& a, int s) {
+        return (s & 1) ? __high2float(a.h[s >> 1]) : __low2float(a.h[s >> 1]);
+    }
     static constexpr float BIG = 30000.0f, HALF = 0.5f;
 };
 using PolF16x4H = PolF16x4H_T<1>;
 using PolF16x4H_C2 = PolF16x4H_T<2>;
 using PolF16x4H_C4 = PolF16x4H_T<4>;
+using PolF16x4_C4 = PolF16x4H_T<4, false>;
 
 struct PolU16x1 { // any width, u16 entries, int32 accumulate
     static constexpr int CPW = 1;
@@ -560,6 +565,7 @@ const char* variant_name(uint32_t v) {
     case VAR_F16X4H: return "f16x4h (u16 tables, fp16 high-byte filter + exact re-evaluation, 128-query tile, LDS.64)";
     case VAR_F16X4H_C2: return "f16x4h-c2 (as f16x4h, 2 codes per warp step, 64-row tile)";
     case VAR_F16X4H_C4: return "f16x4h-c4 (as f16x4h, 4 codes per warp step, 32-row tile)";
+    case VAR_F16X4_C4: return "f16x4-c4 (u8 tables exact in fp16, 4 codes per warp step, 32-row tile)";
     }
     return "?";
 }
@@ -594,6 +600,10 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int cif) {
         case VAR_F32X2: set(VAR_F32X2, PolF32x2::TQ, smem_need<PolF32x2>(ds.E)); break;
         case VAR_U16X1: set(VAR_U16X1, PolU16x1::TQ, smem_need<PolU16x1>(ds.E)); break;
         case VAR_U8X1: set(VAR_U8X1, PolU8x1::TQ, smem_need<PolU8x1>(ds.E)); break;
+        case VAR_F16X4_C4:
+            if (!u8) throw Error(QADC_ERR_CONFIG, "scan: f16x4-c4 needs 8-bit tables");
+            set(VAR_F16X4_C4, PolF16x4_C4::TQ, smem_need<PolF16x4_C4>(ds.E));
+            break;
         case VAR_F16X4H:
         case VAR_F16X4H_C2:
         case VAR_F16X4H_C4:
@@ -608,7 +618,10 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int cif) {
         return p;
     }
     if (u8 && fits(smem_need<PolF16x8>(ds.E))) set(VAR_F16X8, PolF16x8::TQ, smem_need<PolF16x8>(ds.E));
+    else if (u8 && fits(smem_need<PolF16x4_C4>(ds.E))) set(VAR_F16X4_C4, PolF16x4_C4::TQ, smem_need<PolF16x4_C4>(ds.E));
     else if (!u8 && fits(smem_need<PolF16x4H>(ds.E))) set(VAR_F16X4H, PolF16x4H::TQ, smem_need<PolF16x4H>(ds.E));
+    else if (!u8 && fits(smem_need<PolF16x4H_C2>(ds.E))) set(VAR_F16X4H_C2, PolF16x4H_C2::TQ, smem_need<PolF16x4H_C2>(ds.E));
+    else if (!u8 && fits(smem_need<PolF16x4H_C4>(ds.E))) set(VAR_F16X4H_C4, PolF16x4H_C4::TQ, smem_need<PolF16x4H_C4>(ds.E));
     else if (fits(smem_need<PolF32x2>(ds.E))) set(VAR_F32X2, PolF32x2::TQ, smem_need<PolF32x2>(ds.E));
     else if (fits(smem_need<PolU16x1>(ds.E))) set(VAR_U16X1, PolU16x1::TQ, smem_need<PolU16x1>(ds.E));
     else if (fits(smem_need<PolU8x1>(ds.E))) set(VAR_U8X1, PolU8x1::TQ, smem_need<PolU8x1>(ds.E));
@@ -665,7 +678,11 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, 
         return launch_one<PolF16x4H_C2, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4:
         if (G655::matches(ds)) return launch_one<PolF16x4H_C4, G655>(plan, ds, args, grid, stream);
+        if (G88::matches(ds)) return launch_one<PolF16x4H_C4, G88>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_F16X4_C4:
+        if (G8::matches(ds)) return launch_one<PolF16x4_C4, G8>(plan, ds, args, grid, stream);
+        return launch_one<PolF16x4_C4, GeomRT>(plan, ds, args, grid, stream);
     default: throw Error(QADC_ERR_CONFIG, "scan: bad variant");
     }
 }

@@ -75,7 +75,8 @@ size_t tile_entry_bytes(ScanVariant v) {
     case VAR_F16X8:
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
-    case VAR_F16X4H_C4: return 2;
+    case VAR_F16X4H_C4:
+    case VAR_F16X4_C4: return 2;
     case VAR_F32X2: return 4;
     case VAR_U16X1: return 2;
     case VAR_U8X1: return 1;
@@ -86,7 +87,8 @@ size_t tile_entry_bytes(ScanVariant v) {
 void launch_pack_tiles(ScanVariant v, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
                        void* out, cudaStream_t stream) {
     switch (v) {
-    case VAR_F16X8: return launch_pack<__half>(qlut, width, E, n_rows, tq, false, out, stream);
+    case VAR_F16X8:
+    case VAR_F16X4_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, false, out, stream);
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, true, out, stream);
