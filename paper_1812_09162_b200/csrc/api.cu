@@ -171,7 +171,7 @@ struct qadc_index {
     uint32_t seg0 = 4096;
     uint32_t seg_growth = 8;
     int force_variant = -1;
-    int cif = 2;
+    int cif = 0; // early-termination check point selector (see scan.cu launch_one)
     // workspace
     SelectBufs sel;
     DevBuf qlut, tile_lut, luts, calib_out, map, status, jobs, queries, out_ids, out_dists, out_counts, counters, scratch;
@@ -1037,7 +1037,7 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384));
         else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
         else if (n == "force_variant") h->force_variant = int(value);
-        else if (n == "cif") h->cif = int(value);
+        else if (n == "cif" || n == "early") h->cif = int(value);
         else if (n == "ivf_round0") h->ivf_round0 = uint32_t(std::max<int64_t>(value, 64));
         else throw Error(QADC_ERR_CONFIG, "set_option: unknown option " + n);
     });

@@ -92,7 +92,7 @@ struct ScanPlan {
     uint32_t tq;         // rows per tile
     uint32_t smem_bytes;
     uint32_t threads;
-    uint32_t cif; // codes in flight per warp (1, 2 or 4)
+    uint32_t cif; // early-termination check point selector: 0 none, 1 = M/2, 2 = 2M/3, 3 = 3M/4
 };
 
 // chooses the variant for a spec (throws config error if nothing fits shared memory)

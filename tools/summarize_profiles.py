@@ -72,13 +72,17 @@ if __name__ == "__main__":
     p = ROOT / "profiles"
     p.mkdir(exist_ok=True)
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    for rep, note in [(g / f"{tag}_scan_c2.ncu-rep", "ncu --set full --clock-control none, scan_kernel launch #16 of `python bench.py --steps 2 --warmup 3` (C2, 12x{6,5,5})"),
-                      (g / f"{tag}_scan_c1.ncu-rep", "ncu --set full --clock-control none, scan_kernel launch #12 of `python bench.py --workload c1 --steps 2 --warmup 3` (C1, 16x{4,4})")]:
-        if rep.exists():
-            summarize_rep(rep, p / (rep.stem + "_summary.txt"), note)
-    lc = g / f"{tag}_launches_c2.csv"
-    if lc.exists():
+    names = {"c1": "C1, 16x{4,4} N=1e6 Q=1e3", "c2": "C2, 12x{6,5,5} N=1e7 Q=1e4 (default bench)",
+             "c3": "C3, 8x{8,8} N=1e7 Q=1e4", "c4": "C4, 16x{4,4} N=2e8 Q=1e4", "c5": "C5, IVF K=16384 nprobe=64"}
+    for rep in sorted(g.glob(f"{tag}_scan_*.ncu-rep")):
+        w = rep.stem.split("_")[-1]
+        summarize_rep(rep, p / (rep.stem + "_summary.txt"),
+                      f"ncu --set full --clock-control none --import-source on, one scan_kernel launch of "
+                      f"`python bench.py --workload {w} --warmup 3` ({names.get(w, w)})")
+    for lc in sorted(g.glob(f"{tag}_launches_*.csv")):
+        w = lc.stem.split("_")[-1]
         (p / lc.name).write_text(lc.read_text())
-        summarize_launches(lc, p / f"{tag}_launch_share_c2.txt",
-                           "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 on `python bench.py --steps 2 --warmup 3 --no-cpu-baseline` "
-                           "(cold-cache, serialised per-launch times: compare SHARES, not absolutes)")
+        summarize_launches(lc, p / f"{tag}_launch_share_{w}.txt",
+                           f"ncu --metrics gpu__time_duration.sum --clock-control none on `python bench.py --workload {w} "
+                           f"--warmup 3 --no-cpu-baseline`, library kernels only (cold-cache, serialised per-launch times: "
+                           f"compare SHARES, not absolutes)")
