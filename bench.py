@@ -370,7 +370,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    st_acc = {"ms_scan": 0.0, "ms_lut": 0.0, "ms_select": 0.0, "launches": 0, "scan_launches": 0, "pairs": 0}
+    st_acc = {"ms_scan": 0.0, "ms_lut": 0.0, "ms_select": 0.0, "launches": 0, "scan_launches": 0, "pairs": 0,
+              "admitted": 0, "retries": 0}
     with ClockSampler(local_rank) as clocks:
         for _ in range(args.warmup):
             step()
@@ -393,6 +394,8 @@ def main():
             st_acc["launches"] += st.kernel_launches + (1 if sharded is not None else 0)  # + the merge kernel
             st_acc["scan_launches"] += st.scan_launches
             st_acc["pairs"] += st.pairs_scanned
+            st_acc["admitted"] += st.candidates
+            st_acc["retries"] += st.overflow_retries
         ev1.record()
         barrier()
         w1 = time.time()
@@ -458,6 +461,8 @@ def main():
                     "algorithmic_bytes_per_pair": 8,
                     "avg_launch_ms": st_acc["ms_scan"] / max(st_acc["scan_launches"], 1),
                     "stage_ms_per_step": {k: st_acc[k] / args.steps for k in ("ms_lut", "ms_scan", "ms_select")},
+                    "admitted_pairs_per_query": st_acc["admitted"] / args.steps / nq,
+                    "overflow_retries": st_acc["retries"],
                     "note": "codes are streamed once per query tile and reused from shared memory, so algorithmic bytes "
                             "exceed DRAM traffic; the kernel's real ceiling is the shared-memory pipe (profiles/)"}
         # the kernel's operative ceiling: table-lookup bytes through the shared-memory pipe (128 B/clk/SM)

@@ -13,7 +13,7 @@
  *
  * Parity status: PINNED.  tests/test_oracle_pins.py checks this restatement
  * against (a) the known-answer vectors held inline by the reference's own
- * tests (tests/golden/kat.json, transcribed with file:line), (b) golden
+ * tests (transcribed with file:line in tests/test_oracle_pins.py), (b) golden
  * input/output fixtures produced by running the unmodified reference headers
  * (oracle/_ref, built by oracle/Makefile from the sources where they lie), and
  * (c) when oracle/_ref is present, live differential runs against it.

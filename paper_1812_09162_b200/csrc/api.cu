@@ -171,7 +171,6 @@ struct qadc_index {
     uint32_t seg0 = 4096;
     uint32_t seg_growth = 8;
     int force_variant = -1;
-    int cif = 0; // early-termination check point selector (see scan.cu launch_one)
     // workspace
     SelectBufs sel;
     DevBuf qlut, tile_lut, luts, calib_out, map, status, jobs, queries, out_ids, out_dists, out_counts, counters, scratch;
@@ -187,7 +186,7 @@ namespace qadc {
 
 static constexpr uint64_t CODE_PAD = 1024; // device code arrays are padded to this many codes
 
-static ScanPlan plan_for(const qadc_index* h) { return plan_scan(h->ds, h->device, h->force_variant, h->cif); }
+static ScanPlan plan_for(const qadc_index* h) { return plan_scan(h->ds, h->device, h->force_variant); }
 
 // Geometric segment schedule: after n codes the R-th best of n bounds the admission
 // rate of the next codes by R/n, so each segment admits O(R * growth) candidates.
@@ -281,12 +280,11 @@ static bool scan_select_flat(qadc_index* h, const ScanPlan& plan, const uint8_t*
         a.cand_count = h->sel.cand_count.as<uint32_t>();
         a.cap = cap;
         a.overflow = h->sel.overflow.as<uint32_t>();
-        a.counters = h->counters.as<unsigned long long>();
         const size_t e0 = h->timer.mark(st);
         launch_scan(plan, h->ds, a, std::min<int>(grid, int(n)), st);
         const size_t e1 = h->timer.mark(st);
         launch_tighten(h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad, h->sel.cand.as<uint64_t>(),
-                       h->sel.cand_count.as<uint32_t>(), cap, h->sel.thr_key.as<uint64_t>(), nq, r, st);
+                       h->sel.cand_count.as<uint32_t>(), cap, h->sel.thr_key.as<uint64_t>(), nq, r, h->counters.as<unsigned long long>(), st);
         const size_t e2 = h->timer.mark(st);
         h->timer.span(1, e0, e1, bounds[si + 1] - bounds[si]);
         h->timer.span(2, e1, e2);
@@ -319,8 +317,11 @@ static void fill_empty_results(uint32_t nq, uint32_t r, uint32_t* d_ids, float* 
 
 static void check_status(qadc_index* h, cudaStream_t st) {
     int status = 0;
+    unsigned long long admitted = 0;
     QADC_CUDA_CHECK(cudaMemcpyAsync(&status, h->status.p, 4, cudaMemcpyDeviceToHost, st));
+    if (h->counters.p) QADC_CUDA_CHECK(cudaMemcpyAsync(&admitted, h->counters.p, 8, cudaMemcpyDeviceToHost, st));
     QADC_CUDA_CHECK(cudaStreamSynchronize(st));
+    h->stats.candidates = admitted;
     if (status == QADC_ERR_CALIBRATION) throw Error(QADC_ERR_CALIBRATION, "quantize_tables: d_max < d_min");
     if (status) throw Error(status, "device-side failure");
 }
@@ -344,6 +345,7 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
     const size_t wb = ds.word_width / 8;
     h->status.ensure(4);
     h->counters.ensure(16);
+    QADC_CUDA_CHECK(cudaMemsetAsync(h->counters.p, 0, 16, st));
     QADC_CUDA_CHECK(cudaMemsetAsync(h->status.p, 0, 4, st));
 
     // query batches bound the candidate-buffer footprint
@@ -422,6 +424,7 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
     uint32_t tq = plan.tq;
     h->status.ensure(4);
     h->counters.ensure(16);
+    QADC_CUDA_CHECK(cudaMemsetAsync(h->counters.p, 0, 16, st));
     QADC_CUDA_CHECK(cudaMemsetAsync(h->status.p, 0, 4, st));
     const int grid = h->num_sms;
 
@@ -474,7 +477,7 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
             int pick = int(plan.variant) - int(VAR_F16X4H);
             for (int v = 0; v < 3; ++v) {
                 try {
-                    (void)plan_scan(ds, h->device, int(cand[v]), h->cif); // does this tile height fit shared memory?
+                    (void)plan_scan(ds, h->device, int(cand[v])); // does this tile height fit shared memory?
                 } catch (const Error&) {
                     continue;
                 }
@@ -487,7 +490,7 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                     pick = v;
                 }
             }
-            plan = plan_scan(ds, h->device, int(cand[pick]), h->cif);
+            plan = plan_scan(ds, h->device, int(cand[pick]));
             tq = plan.tq;
         }
         h->stats.scan_variant = plan.variant;
@@ -622,12 +625,11 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
             sa.cand_count = h->sel.cand_count.as<uint32_t>();
             sa.cap = cap;
             sa.overflow = h->sel.overflow.as<uint32_t>();
-            sa.counters = h->counters.as<unsigned long long>();
             const size_t e0 = h->timer.mark(st);
             launch_scan(plan, ds, sa, rd.grid, st);
             const size_t e1 = h->timer.mark(st);
             launch_tighten(h->sel.top.as<uint64_t>(), h->sel.ntop.as<uint32_t>(), h->sel.kpad, h->sel.cand.as<uint64_t>(),
-                           h->sel.cand_count.as<uint32_t>(), cap, h->sel.thr_key.as<uint64_t>(), nb, p.r, st);
+                           h->sel.cand_count.as<uint32_t>(), cap, h->sel.thr_key.as<uint64_t>(), nb, p.r, h->counters.as<unsigned long long>(), st);
             const size_t e2 = h->timer.mark(st);
             h->timer.span(1, e0, e1, rd.n_jobs);
             h->timer.span(2, e1, e2);
@@ -935,7 +937,7 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
                 QADC_CUDA_CHECK(cudaMemcpyAsync(h.sel.cand.p, seed.data(), size_t(n_in) * 8, cudaMemcpyHostToDevice, st));
                 QADC_CUDA_CHECK(cudaMemcpyAsync(h.sel.cand_count.p, &n_in, 4, cudaMemcpyHostToDevice, st));
                 launch_tighten(h.sel.top.as<uint64_t>(), h.sel.ntop.as<uint32_t>(), h.sel.kpad, h.sel.cand.as<uint64_t>(),
-                               h.sel.cand_count.as<uint32_t>(), buf_cap, h.sel.thr_key.as<uint64_t>(), 1, cap, st);
+                               h.sel.cand_count.as<uint32_t>(), buf_cap, h.sel.thr_key.as<uint64_t>(), 1, cap, nullptr, st);
                 QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // seed vector goes out of scope
             }
             h.tile_lut.ensure(size_t(ds.E) * plan.tq * tile_entry_bytes(plan.variant));
@@ -967,11 +969,10 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
                         a.cand_count = h.sel.cand_count.as<uint32_t>();
                         a.cap = buf_cap;
                         a.overflow = h.sel.overflow.as<uint32_t>();
-                        a.counters = h.counters.as<unsigned long long>();
                         launch_scan(plan, ds, a, std::min<int>(grid, int(jobs.size())), st);
                         launch_tighten(h.sel.top.as<uint64_t>(), h.sel.ntop.as<uint32_t>(), h.sel.kpad,
                                        h.sel.cand.as<uint64_t>(), h.sel.cand_count.as<uint32_t>(), buf_cap,
-                                       h.sel.thr_key.as<uint64_t>(), 1, cap, st);
+                                       h.sel.thr_key.as<uint64_t>(), 1, cap, nullptr, st);
                         QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // jobs vector goes out of scope
                     }
                     uint32_t ov = 0;
@@ -1037,7 +1038,6 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384));
         else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
         else if (n == "force_variant") h->force_variant = int(value);
-        else if (n == "cif" || n == "early") h->cif = int(value);
         else if (n == "ivf_round0") h->ivf_round0 = uint32_t(std::max<int64_t>(value, 64));
         else throw Error(QADC_ERR_CONFIG, "set_option: unknown option " + n);
     });

@@ -84,7 +84,6 @@ struct ScanArgs {
     uint32_t* cand_count;      // [nq]
     uint32_t cap;
     uint32_t* overflow;        // [nq] set to 1 when a candidate did not fit
-    unsigned long long* counters; // [0] exact-admitted candidates, [1] slow-path entries
 };
 
 struct ScanPlan {
@@ -92,11 +91,10 @@ struct ScanPlan {
     uint32_t tq;         // rows per tile
     uint32_t smem_bytes;
     uint32_t threads;
-    uint32_t cif; // early-termination check point selector: 0 none, 1 = M/2, 2 = 2M/3, 3 = 3M/4
 };
 
 // chooses the variant for a spec (throws config error if nothing fits shared memory)
-ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int threads);
+ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant);
 void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
 
 // ---- LUT / calibration / quantization (lut.cu) ----
@@ -120,7 +118,8 @@ void launch_init_select(uint64_t* thr_key, uint32_t* cand_count, uint32_t* ntop,
                         cudaStream_t stream);
 // fold the new candidates of every query into its running top-r and refresh thr_key
 void launch_tighten(uint64_t* top, uint32_t* ntop, uint32_t kpad, uint64_t* cand, uint32_t* cand_count, uint32_t cap,
-                    uint64_t* thr_key, uint32_t nq, uint32_t r, cudaStream_t stream);
+                    uint64_t* thr_key, uint32_t nq, uint32_t r, unsigned long long* admitted /* optional counter */,
+                    cudaStream_t stream);
 // sort each query's top list and emit ids / unquantized distances / counts / keys
 void launch_finalize(const uint64_t* lists, const uint32_t* counts_in, uint32_t list_len, uint32_t nlists,
                      uint32_t nq, uint32_t r, const float* map, uint32_t flags, uint32_t qmax, uint32_t* out_ids,

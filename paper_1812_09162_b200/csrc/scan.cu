@@ -576,7 +576,7 @@ static uint32_t smem_need(uint32_t E) {
     return E * P::ROWB + NSTAGE * STAGE_BYTES + WQ_BYTES;
 }
 
-ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int cif) {
+ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
     int max_smem = 0;
     QADC_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     // static shared (DevSpec + ScanArgs + barriers) comes out of the same budget
@@ -584,7 +584,6 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, int cif) {
     if (ds.code_stride > 32) throw Error(QADC_ERR_CONFIG, "scan: codes wider than 256 bits are not supported");
     ScanPlan p{};
     p.threads = SCAN_THREADS;
-    p.cif = (cif >= 0 && cif <= 3) ? cif : 0; // early-termination check point selector
     auto fits = [&](uint32_t need) { return need <= budget; };
     auto set = [&](ScanVariant v, uint32_t tq, uint32_t need) {
         p.variant = v;

@@ -39,13 +39,15 @@ static constexpr int TIGHTEN_THREADS = 256;
 // One CTA per query.  dynamic smem: r keys.
 __global__ void __launch_bounds__(TIGHTEN_THREADS)
 tighten_kernel(uint64_t* __restrict__ top, uint32_t* __restrict__ ntop, uint32_t kpad, uint64_t* __restrict__ cand,
-               uint32_t* __restrict__ cand_count, uint32_t cap, uint64_t* __restrict__ thr_key, uint32_t r) {
+               uint32_t* __restrict__ cand_count, uint32_t cap, uint64_t* __restrict__ thr_key, uint32_t r,
+               unsigned long long* __restrict__ admitted) {
     extern __shared__ uint64_t keep[];
     __shared__ SelectScratch sc;
 
     const uint32_t q = blockIdx.x;
     const uint32_t n = min(cand_count[q], cap);
     if (n == 0) return;
+    if (admitted && threadIdx.x == 0) atomicAdd(admitted, (unsigned long long)n); // statistics only
     const uint32_t nt = ntop[q];
     const uint32_t total = nt + n;
     uint64_t* my_top = top + size_t(q) * kpad;
@@ -88,9 +90,10 @@ tighten_kernel(uint64_t* __restrict__ top, uint32_t* __restrict__ ntop, uint32_t
 }
 
 void launch_tighten(uint64_t* top, uint32_t* ntop, uint32_t kpad, uint64_t* cand, uint32_t* cand_count, uint32_t cap,
-                    uint64_t* thr_key, uint32_t nq, uint32_t r, cudaStream_t stream) {
+                    uint64_t* thr_key, uint32_t nq, uint32_t r, unsigned long long* admitted, cudaStream_t stream) {
     if (nq == 0) return;
-    tighten_kernel<<<nq, TIGHTEN_THREADS, size_t(r) * 8, stream>>>(top, ntop, kpad, cand, cand_count, cap, thr_key, r);
+    tighten_kernel<<<nq, TIGHTEN_THREADS, size_t(r) * 8, stream>>>(top, ntop, kpad, cand, cand_count, cap, thr_key, r,
+                                                                   admitted);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
