@@ -64,7 +64,7 @@ typedef struct qadc_spec {
     uint32_t cb_off[QADC_MAX_SUBS];
 } qadc_spec;
 
-/* SearchParams (index.hpp:20-32).  flags: bit 0 = fuse the final q*delta+d_min
+/* SearchParams (index.hpp:20-32).  flags: bit 1 = rerank (below); bit 0 = fuse the final q*delta+d_min
  * into one FMA like the reference's default -march=native build does
  * (distance.hpp:158-161); default 0 = unfused, matching the pinned oracle. */
 typedef struct qadc_search_params {
@@ -74,6 +74,9 @@ typedef struct qadc_search_params {
     uint32_t flags;
 } qadc_search_params;
 #define QADC_FLAG_FMA_UNQUANTIZE 1u
+/* SearchParams::rerank (index.hpp:24): re-order the final top-R by exact float ADC (index.hpp:53-67, 148-152,
+ * 377-386).  Only for unsharded handles (ids must address this handle's own codes); incompatible with d_out_keys. */
+#define QADC_FLAG_RERANK 2u
 
 /* counters of the last search on a handle (bench.py's gpu_launches comes from here) */
 typedef struct qadc_stats {

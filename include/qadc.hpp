@@ -125,10 +125,9 @@ inline std::vector<pqscan::SearchResult> split(uint32_t nq, uint32_t r, const st
 }
 inline qadc_search_params params_of(const pqscan::SearchParams& p) {
     p.validate();
-    if (p.rerank) throw pqscan::config_error("qadc: exact re-ranking is not part of the GPU path");
     if (p.forced_kernel == pqscan::KernelFamily::scalar_float)
         throw pqscan::config_error("qadc: the float-table scan is not part of the GPU path");
-    return qadc_search_params{p.probes, p.r, p.t, 0};
+    return qadc_search_params{p.probes, p.r, p.t, p.rerank ? QADC_FLAG_RERANK : 0u};
 }
 } // namespace detail
 

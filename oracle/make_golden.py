@@ -56,13 +56,14 @@ def flat_fixture(R: Oracle, name, dims, text, n_db, seed):
     # the natural vector family must agree with the normative scalar scan
     ids_v, dists_v, counts_v = R.flat_search(s, cb, packed, n_db, queries, r=r, t=t, family=1)
     assert np.array_equal(ids, ids_v) and np.array_equal(dists, dists_v) and np.array_equal(counts, counts_v)
+    ids_rr, dists_rr, counts_rr = R.flat_search(s, cb, packed, n_db, queries, r=r, t=t, family=0x100)  # rerank=true
     luts = np.stack([R.compute_tables(s, cb, q) for q in queries])
     prefix = np.stack([R.prefix_float(s, packed, n_db, lut, t) for lut in luts])
     sums = np.stack([R.adc_sums(s, packed, n_db, qlut[i], 0, n_db) for i in range(len(queries))])
     np.savez_compressed(
         GOLD / f"flat_{name}.npz", spec=text, dims=dims, codebook=cb, codes=codes, packed=packed, count=n_db,
         queries=queries, r=r, t=t, ids=ids, dists=dists, counts=counts, qlut=qlut, params=params, luts=luts,
-        prefix=prefix, sums=sums, vector_family=R.auto_family(s))
+        prefix=prefix, sums=sums, vector_family=R.auto_family(s), ids_rr=ids_rr, dists_rr=dists_rr)
     print(f"flat_{name}: {text} d={dims} n={n_db} family={R.auto_family(s)}")
 
 
@@ -148,6 +149,9 @@ def ivf_fixture(R: Oracle, name, dims, text, k_cells, n_db, probes, seed):
                                      family=1)
         assert np.array_equal(oi, oi2) and np.array_equal(od, od2) and np.array_equal(oc, oc2)
         out[f"ids_p{pr}"], out[f"dists_p{pr}"], out[f"counts_p{pr}"] = oi, od, oc
+    oi, od, oc = R.ivf_search(s, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=probes, r=50, t=200,
+                              family=0x100)  # rerank=true
+    out["ids_rr"], out["dists_rr"] = oi, od
     order = np.stack([R.probe_order(dims, coarse, q, probes) for q in queries])
     np.savez_compressed(
         GOLD / f"ivf_{name}.npz", spec=text, dims=dims, codebook=cb, coarse=coarse, packed=packed,

@@ -446,8 +446,30 @@ static int validate_params(uint32_t probes, uint32_t r, uint32_t t) {
 }
 
 /* FlatIndex::search for one query, index.hpp:110-145 */
+/* detail::rerank_by_float, index.hpp:53-67: order the final set by (exact float ADC, id) */
+typedef struct {
+    float d;
+    uint32_t id;
+} fent;
+static int cmp_fent(const void* a, const void* b) {
+    fent x = *(const fent*)a, y = *(const fent*)b;
+    if (x.d < y.d) return -1;
+    if (x.d > y.d) return 1;
+    return (x.id > y.id) - (x.id < y.id);
+}
+/* adc_scalar_float of the code at list position pos, distance.hpp:61-69 via FlatIndex::code_at (index.hpp:93-108) */
+static float float_adc_at(const orc_spec* s, const uint8_t* packed, uint64_t pos, const float* lut) {
+    float acc = 0.0f;
+    for (uint32_t r = 0; r < s->groups; ++r)
+        for (uint32_t k = 0; k < s->g; ++k) {
+            uint32_t j = r * s->g + k;
+            acc += lut[s->ent_off[j] + packed_index(s, packed, s->groups, pos, r, k)];
+        }
+    return acc;
+}
+
 static int flat_search_one(const orc_spec* s, const float* cb, const uint8_t* packed, uint64_t count,
-                           const float* query, uint32_t r, uint32_t t, uint32_t* out_ids, float* out_dists,
+                           const float* query, uint32_t r, uint32_t t, int rerank, uint32_t* out_ids, float* out_dists,
                            uint32_t* out_count, void* dbg_qlut, float* dbg_params) {
     *out_count = 0;
     if (count == 0) return ORC_OK;
@@ -471,6 +493,19 @@ static int flat_search_one(const orc_spec* s, const float* cb, const uint8_t* pa
             out_dists[i] = (float)h.e[i].dist * delta + own; /* unquantize, distance.hpp:158-161 */
         }
         *out_count = h.n;
+        if (rerank) { /* FlatIndex::rerank_exact, index.hpp:148-152 (ids are list positions) */
+            fent* fe = (fent*)malloc(sizeof(fent) * (h.n ? h.n : 1));
+            for (uint32_t i = 0; i < h.n; ++i) {
+                fe[i].id = out_ids[i];
+                fe[i].d = float_adc_at(s, packed, out_ids[i], lut);
+            }
+            qsort(fe, h.n, sizeof(fent), cmp_fent);
+            for (uint32_t i = 0; i < h.n; ++i) {
+                out_ids[i] = fe[i].id;
+                out_dists[i] = fe[i].d;
+            }
+            free(fe);
+        }
         if (dbg_qlut) memcpy(dbg_qlut, qlut, (size_t)s->total_entries * (s->word_width / 8));
         if (dbg_params) {
             dbg_params[0] = d_min;
@@ -494,6 +529,9 @@ typedef struct {
     uint64_t count;
     const float* queries;
     uint32_t nq, r, t;
+    int rerank;
+    const uint32_t* loc_cell; /* ivf locator: id -> cell, id -> position (index.hpp:366-375) */
+    const uint32_t* loc_pos;
     uint32_t* out_ids;
     float* out_dists;
     uint32_t* out_counts;
@@ -525,7 +563,7 @@ static void* worker(void* arg) {
             rc = ivf_search_one(J, query, J->out_ids + (size_t)q * J->r, J->out_dists + (size_t)q * J->r,
                                 J->out_counts + q);
         else
-            rc = flat_search_one(J->s, J->cb, J->packed, J->count, query, J->r, J->t, J->out_ids + (size_t)q * J->r,
+            rc = flat_search_one(J->s, J->cb, J->packed, J->count, query, J->r, J->t, J->rerank, J->out_ids + (size_t)q * J->r,
                                  J->out_dists + (size_t)q * J->r, J->out_counts + q,
                                  J->dbg_qlut ? (uint8_t*)J->dbg_qlut + (size_t)q * J->s->total_entries *
                                                                           (J->s->word_width / 8)
@@ -556,11 +594,11 @@ static int run_pool(job_t* J, int threads) {
 int orc_flat_search(const orc_spec* s, const float* codebook, const uint8_t* packed, uint64_t count,
                     const float* queries, uint32_t nq, uint32_t r, uint32_t t, int family, int threads,
                     uint32_t* out_ids, float* out_dists, uint32_t* out_counts, void* dbg_qlut, float* dbg_params) {
-    (void)family;
     int rc = validate_params(1, r, t);
     if (rc) return rc;
     job_t J;
     memset(&J, 0, sizeof J);
+    J.rerank = (family & 0x100) != 0; /* bit 8 of `family` = SearchParams::rerank */
     J.s = s;
     J.cb = codebook;
     J.packed = packed;
@@ -673,6 +711,22 @@ static int ivf_search_one(const job_t* J, const float* query, uint32_t* out_ids,
                 out_dists[i] = (float)h.e[i].dist * delta + d_min_global; /* index.hpp:337 */
             }
             *out_count = h.n;
+            if (J->rerank) { /* IvfIndex::rerank_exact, index.hpp:377-386 */
+                fent* fe = (fent*)malloc(sizeof(fent) * (h.n ? h.n : 1));
+                for (uint32_t i = 0; i < h.n; ++i) {
+                    const uint32_t id = out_ids[i], cell = J->loc_cell[id];
+                    uint32_t pi = 0;
+                    while (pi < a && order[pi] != cell) ++pi;
+                    fe[i].id = id;
+                    fe[i].d = float_adc_at(s, J->packed + J->list_byte_off[cell], J->loc_pos[id], tables + (size_t)pi * E);
+                }
+                qsort(fe, h.n, sizeof(fent), cmp_fent);
+                for (uint32_t i = 0; i < h.n; ++i) {
+                    out_ids[i] = fe[i].id;
+                    out_dists[i] = fe[i].d;
+                }
+                free(fe);
+            }
         }
     }
 done:
@@ -690,11 +744,29 @@ int orc_ivf_search(const orc_spec* s, const float* codebook, const float* coarse
                    const uint64_t* list_count, const uint32_t* ids, const float* queries, uint32_t nq,
                    uint32_t probes, uint32_t r, uint32_t t, int family, int threads, uint32_t* out_ids,
                    float* out_dists, uint32_t* out_counts) {
-    (void)family;
     int rc = validate_params(probes, r, t);
     if (rc) return rc;
+    /* IvfIndex constructor (index.hpp:169-177, 366-375): every id must be < total; build the locator */
+    uint64_t total = 0;
+    for (uint32_t c = 0; c < k_cells; ++c) total += list_count[c];
+    uint32_t* loc_cell = (uint32_t*)malloc(sizeof(uint32_t) * (total ? total : 1));
+    uint32_t* loc_pos = (uint32_t*)malloc(sizeof(uint32_t) * (total ? total : 1));
+    for (uint32_t c = 0; c < k_cells; ++c)
+        for (uint64_t p = 0; p < list_count[c]; ++p) {
+            uint32_t id = ids[list_id_off[c] + p];
+            if (id >= total) {
+                free(loc_cell);
+                free(loc_pos);
+                return fail(ORC_ERR_CORRUPTION, "ivf: vector id out of range");
+            }
+            loc_cell[id] = c;
+            loc_pos[id] = (uint32_t)p;
+        }
     job_t J;
     memset(&J, 0, sizeof J);
+    J.rerank = (family & 0x100) != 0;
+    J.loc_cell = loc_cell;
+    J.loc_pos = loc_pos;
     J.s = s;
     J.cb = codebook;
     J.packed = packed;
@@ -713,7 +785,10 @@ int orc_ivf_search(const orc_spec* s, const float* codebook, const float* coarse
     J.list_count = list_count;
     J.ids = ids;
     J.is_ivf = 1;
-    return run_pool(&J, threads);
+    rc = run_pool(&J, threads);
+    free(loc_cell);
+    free(loc_pos);
+    return rc;
 }
 
 /* ---------------------------------------------------------- handle variants -- */

@@ -124,9 +124,10 @@ void flatten_q(const orc_spec* s, const QuantizedTables& qt, void* out) {
 }
 
 std::optional<KernelFamily> family_of(const PqSpec& spec, int family) {
-    if (family == 0) return KernelFamily::scalar_quantized;
+    if ((family & 0xFF) == 0) return KernelFamily::scalar_quantized;
     return std::nullopt; // auto: natural vector family when the host has it
 }
+bool rerank_of(int family) { return (family & 0x100) != 0; } // bit 8 of `family` = SearchParams::rerank
 
 template <class F>
 void parallel_queries(uint32_t nq, int threads, F&& per_query) {
@@ -319,6 +320,7 @@ int orc_flat_search(const orc_spec* s, const float* codebook, const uint8_t* pac
         params.r = r;
         params.t = t;
         params.forced_kernel = family_of(spec, family);
+        params.rerank = rerank_of(family);
         params.validate();
         std::atomic<int> failed{0};
         std::string err;
@@ -390,6 +392,7 @@ int orc_ivf_search(const orc_spec* s, const float* codebook, const float* coarse
         params.r = r;
         params.t = t;
         params.forced_kernel = family_of(spec, family);
+        params.rerank = rerank_of(family);
         params.validate();
         std::atomic<int> failed{0};
         std::string err;
@@ -437,6 +440,7 @@ int orc_flat_search_h(void* hv, const float* queries, uint32_t nq, uint32_t r, u
         params.r = r;
         params.t = t;
         params.forced_kernel = family_of(h->spec, family);
+        params.rerank = rerank_of(family);
         params.validate();
         std::atomic<int> failed{0};
         std::string err;
@@ -484,6 +488,7 @@ int orc_ivf_search_h(void* hv, const float* queries, uint32_t nq, uint32_t probe
         params.r = r;
         params.t = t;
         params.forced_kernel = family_of(h->spec, family);
+        params.rerank = rerank_of(family);
         params.validate();
         std::atomic<int> failed{0};
         std::string err;

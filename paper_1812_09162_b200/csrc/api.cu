@@ -161,6 +161,7 @@ struct qadc_index {
     uint32_t k_cells = 0;
     DevBuf coarse, coarse_t, list_code_off, list_count_dev, calib_code_off, calib_count_dev;
     bool own_heads = true; // calibration heads alias the lists themselves (unsharded index)
+    DevBuf locator;        // ivf, unsharded: id -> device code position (IvfIndex::build_locator, index.hpp:366-375)
     std::vector<uint64_t> list_code_off_h, list_count_h;
     uint64_t total_codes = 0;
     uint32_t ivf_round0 = 512; // list positions scanned in the first round (then x seg_growth per round)
@@ -326,10 +327,21 @@ static void check_status(qadc_index* h, cudaStream_t st) {
     if (status) throw Error(status, "device-side failure");
 }
 
+static void check_rerank_args(const qadc_index* h, const qadc_search_params& p, const uint32_t* d_ids,
+                              const float* d_dists, const uint32_t* d_counts, const uint64_t* d_keys) {
+    if (!(p.flags & QADC_FLAG_RERANK)) return;
+    if (d_keys) throw Error(QADC_ERR_CONFIG, "rerank: re-ranking applies to a final result list, not to per-shard key lists");
+    if (!d_ids || !d_dists || !d_counts) throw Error(QADC_ERR_INPUT, "rerank: ids, dists and counts outputs are required");
+    if (h->kind == 0 && h->base_id != 0) throw Error(QADC_ERR_CONFIG, "rerank: not available on a database shard");
+    if (h->kind == 1 && !h->locator.p) throw Error(QADC_ERR_CONFIG, "rerank: not available on an IVF shard");
+}
+
 static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t nq, const qadc_search_params& p,
                                uint32_t* d_ids, float* d_dists, uint32_t* d_counts, uint64_t* d_keys, float* d_map,
                                cudaStream_t st) {
     validate_params(p, false);
+    check_rerank_args(h, p, d_ids, d_dists, d_counts, d_keys);
+    const bool rerank = (p.flags & QADC_FLAG_RERANK) != 0;
     h->stats = qadc_stats{};
     h->timer.reset();
     if (nq == 0) return;
@@ -367,6 +379,10 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
         la.qluts = h->qlut.p;
         la.map = h->map.as<float>();
         la.status = h->status.as<int>();
+        if (rerank) {
+            h->luts.ensure(size_t(nb) * ds.E * 4);
+            la.luts = h->luts.as<float>();
+        }
         const size_t t0 = h->timer.mark(st);
         launch_flat_tables(ds, la, st);
         const uint32_t ntiles = (nb + plan.tq - 1) / plan.tq;
@@ -387,6 +403,9 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
                         p.flags, ds.qmax, d_ids ? d_ids + size_t(q0) * p.r : nullptr,
                         d_dists ? d_dists + size_t(q0) * p.r : nullptr, d_counts ? d_counts + q0 : nullptr,
                         d_keys ? d_keys + size_t(q0) * p.r : nullptr, st);
+        if (rerank)
+            launch_rerank(ds, h->codes.as<uint8_t>(), h->luts.as<float>(), h->base_id, nullptr, nullptr, nullptr, 0, 0, nb,
+                          p.r, d_ids + size_t(q0) * p.r, d_dists + size_t(q0) * p.r, d_counts + q0, st);
         h->timer.span(2, f0, h->timer.mark(st));
         if (d_map)
             QADC_CUDA_CHECK(cudaMemcpyAsync(d_map + size_t(q0) * 2, h->map.p, size_t(nb) * 8, cudaMemcpyDeviceToDevice, st));
@@ -408,6 +427,8 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                               uint32_t* d_ids, float* d_dists, uint32_t* d_counts, uint64_t* d_keys, float* d_map,
                               cudaStream_t st) {
     validate_params(p, true);
+    check_rerank_args(h, p, d_ids, d_dists, d_counts, d_keys);
+    const bool rerank = (p.flags & QADC_FLAG_RERANK) != 0;
     h->stats = qadc_stats{};
     h->timer.reset();
     if (nq == 0) return;
@@ -653,6 +674,10 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                         p.flags, ds.qmax, d_ids ? d_ids + size_t(q0) * p.r : nullptr,
                         d_dists ? d_dists + size_t(q0) * p.r : nullptr, d_counts ? d_counts + q0 : nullptr,
                         d_keys ? d_keys + size_t(q0) * p.r : nullptr, st);
+        if (rerank)
+            launch_rerank(ds, h->codes.as<uint8_t>(), h->luts.as<float>(), 0, h->locator.as<uint32_t>(),
+                          h->list_code_off.as<uint64_t>(), h->order.as<uint32_t>(), K, a, nb, p.r,
+                          d_ids + size_t(q0) * p.r, d_dists + size_t(q0) * p.r, d_counts + q0, st);
         h->timer.span(2, f0, h->timer.mark(st));
         if (d_map)
             QADC_CUDA_CHECK(cudaMemcpyAsync(d_map + size_t(q0) * 2, h->map.p, size_t(nb) * 8, cudaMemcpyDeviceToDevice, st));
@@ -1145,6 +1170,21 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
             std::copy(ids + list_id_off[c], ids + list_id_off[c] + list_count[c], ids_padded.begin() + h->list_code_off_h[c]);
         h->ids.ensure(size_t(total_padded) * 4);
         QADC_CUDA_CHECK(cudaMemcpyAsync(h->ids.p, ids_padded.data(), size_t(total_padded) * 4, cudaMemcpyHostToDevice, st));
+        std::vector<uint32_t> loc;
+        if (!have_heads && total_padded < (uint64_t(1) << 32)) {
+            // IvfIndex::build_locator (index.hpp:366-375): ids must be < total ("vector id out of range" otherwise);
+            // the locator maps an id to its device code position for exact re-ranking.  Shards carry global ids and
+            // skip both.
+            loc.assign(std::max<uint64_t>(n_ids, 1), 0u);
+            for (uint32_t c = 0; c < k_cells; ++c)
+                for (uint64_t pp = 0; pp < list_count[c]; ++pp) {
+                    const uint32_t id = ids[list_id_off[c] + pp];
+                    if (id >= n_ids) throw Error(QADC_ERR_CORRUPTION, "ivf: vector id out of range");
+                    loc[id] = uint32_t(h->list_code_off_h[c] + pp);
+                }
+            h->locator.ensure(loc.size() * 4);
+            QADC_CUDA_CHECK(cudaMemcpyAsync(h->locator.p, loc.data(), loc.size() * 4, cudaMemcpyHostToDevice, st));
+        }
         QADC_CUDA_CHECK(cudaStreamSynchronize(st));
         *out = h.release();
     });

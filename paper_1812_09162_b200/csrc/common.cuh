@@ -159,6 +159,12 @@ void launch_ivf_seed(const DevSpec& ds, const uint8_t* d_codes, const uint32_t* 
                      const uint32_t* d_pair_slot, const void* d_qluts, const uint32_t* d_row_bias, uint32_t r,
                      uint32_t head, uint64_t* d_thr_key, cudaStream_t stream);
 
+// ---- exact re-ranking of the final top-R (rerank.cu) ----
+void launch_rerank(const DevSpec& ds, const uint8_t* d_codes, const float* d_luts, uint32_t base_id,
+                   const uint32_t* d_locator, const uint64_t* d_list_code_off, const uint32_t* d_order, uint32_t k_cells,
+                   uint32_t a, uint32_t nq, uint32_t r, uint32_t* d_ids, float* d_dists, const uint32_t* d_counts,
+                   cudaStream_t stream);
+
 // ---- layout (layout.cu) ----
 // reference PackedList bytes (device copy) -> linear device layout, padded with 0xFF codes up to n_padded
 void launch_relayout(const qadc_spec& s, const DevSpec& ds, const uint8_t* d_packed, uint64_t n, uint64_t n_padded,

@@ -46,13 +46,14 @@ class SearchParams:
     r: int = 100
     t: int = 400
     fma_unquantize: bool = False
+    rerank: bool = False  # exact re-ranking of the final top-R by float ADC (index.hpp:24)
 
     def c(self) -> QadcSearchParams:
         for name in ("probes", "r", "t"):
             v = getattr(self, name)
             if v < 0 or v > 0xFFFFFFFF:
                 raise QadcError(5, f"search: {name} out of range")
-        return QadcSearchParams(self.probes, self.r, self.t, 1 if self.fma_unquantize else 0)
+        return QadcSearchParams(self.probes, self.r, self.t, (1 if self.fma_unquantize else 0) | (2 if self.rerank else 0))
 
 
 @dataclass

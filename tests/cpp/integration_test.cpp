@@ -130,6 +130,11 @@ static void flat_checks() {
         }
         SearchResult one = gpu.search({queries.data(), d}, p);
         EXPECT(same(one, batch[0]), "flat %s single vs batch", text);
+        SearchParams pr = p; // exact re-ranking of the final set (index.hpp:148-152)
+        pr.rerank = true;
+        auto rr = gpu.search_batch(queries, 40, pr);
+        for (uint32_t q = 0; q < 40; ++q)
+            EXPECT(same(ref.search({queries.data() + size_t{q} * d, d}, pr), rr[q]), "flat %s rerank query %u differs", text, q);
         bool threw = false;
         try {
             SearchParams bad;
@@ -161,6 +166,11 @@ static void ivf_checks() {
         }
         EXPECT(ref.probe_order({queries.data(), d}, probes) == gpu.probe_order({queries.data(), d}, probes),
                "probe order differs at a=%u", probes);
+        p.rerank = true; // index.hpp:377-386
+        auto rr = gpu.search_batch(queries, 30, p);
+        for (uint32_t q = 0; q < 30; ++q)
+            EXPECT(same(ref.search({queries.data() + size_t{q} * d, d}, p), rr[q]), "ivf rerank probes=%u query %u differs",
+                   probes, q);
     }
     std::printf("ivf 12x{6,5,5} K=48: identical to IvfIndex::search at probes 1/6/48\n");
 }

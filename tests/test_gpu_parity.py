@@ -468,3 +468,53 @@ def test_ivf_probe_order_massive_ties(port):
         for qi in range(5):
             c = int(want[2][qi])
             assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]) and bits_equal(got.dists[qi, :c], want[1][qi, :c])
+
+
+# ------------------------------------------------------------------ rerank (N4) --
+
+@pytest.mark.parametrize("name", FLAT)
+def test_golden_flat_rerank(golden, name):
+    g = golden(name)
+    s = qb.allocate_dims(int(g["dims"]), str(g["spec"]))
+    with qb.FlatIndex(s, g["codebook"], g["packed"], int(g["count"])) as idx:
+        res = idx.search(g["queries"], qb.SearchParams(r=int(g["r"]), t=int(g["t"]), rerank=True))
+    assert np.array_equal(res.counts, g["counts"])
+    for qi in range(len(g["queries"])):
+        c = int(res.counts[qi])
+        assert np.array_equal(res.ids[qi, :c], g["ids_rr"][qi, :c]) and bits_equal(res.dists[qi, :c], g["dists_rr"][qi, :c])
+
+
+@pytest.mark.parametrize("name", ["ivf_irr655.npz", "ivf_pq16x4.npz"])
+def test_golden_ivf_rerank(golden, name):
+    g = golden(name)
+    s = qb.allocate_dims(int(g["dims"]), str(g["spec"]))
+    pr = int(g["probe_list"][1])
+    with qb.IvfIndex(s, g["codebook"], g["coarse"], g["packed"], g["list_byte_off"], g["list_id_off"],
+                     g["list_count"], g["list_ids"]) as idx:
+        res = idx.search(g["queries"], qb.SearchParams(probes=pr, r=int(g["r"]), t=int(g["t"]), rerank=True))
+    for qi in range(len(g["queries"])):
+        c = int(res.counts[qi])
+        assert np.array_equal(res.ids[qi, :c], g["ids_rr"][qi, :c]) and bits_equal(res.dists[qi, :c], g["dists_rr"][qi, :c])
+    bad = g["list_ids"].copy()
+    bad[3] = bad.size + 5
+    with pytest.raises(qb.QadcError) as e:  # index.hpp:372
+        qb.IvfIndex(s, g["codebook"], g["coarse"], g["packed"], g["list_byte_off"], g["list_id_off"], g["list_count"], bad)
+    assert e.value.kind == "corruption"
+
+
+def test_rerank_vs_oracle_and_shard_refusal(port):
+    rng = np.random.default_rng(17)
+    dims, text = 128, "16x{4,4}"
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+    n = 50000
+    pk = qb.pack_list(s, random_codes(s, n, seed=5))
+    queries = (rng.standard_normal((40, dims)) * 2).astype(np.float32)
+    want = port.flat_search(so, cb, pk, n, queries, r=100, t=400, family=0x100, threads=8)
+    with qb.FlatIndex(s, cb, pk, n) as idx:
+        got = idx.search(queries, qb.SearchParams(rerank=True))
+        assert np.array_equal(got.ids, want[0]) and bits_equal(got.dists, want[1])
+    with qb.FlatIndex(s, cb, pk, n, base_id=1000) as shard:
+        with pytest.raises(qb.QadcError) as e:
+            shard.search(queries, qb.SearchParams(rerank=True))
+        assert e.value.kind == "config"

@@ -285,3 +285,38 @@ def test_live_differential_scan_fn(port, ref):
             for fam in (0, 1):
                 b = ref.scan_quantized(s, pk, n, qlut, family=fam, **kw)
                 assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ------------------------------------------------------------------ rerank (N4) --
+
+@pytest.mark.parametrize("name", FLAT + IVF)
+def test_golden_rerank(port, golden, name):
+    """SearchParams::rerank (index.hpp:53-67, 148-152, 377-386): same set, ordered by exact float ADC."""
+    g = golden(name)
+    s = port.spec(int(g["dims"]), str(g["spec"]))
+    if name.startswith("flat"):
+        ids, dists, counts = port.flat_search(s, g["codebook"], g["packed"], int(g["count"]), g["queries"],
+                                              r=int(g["r"]), t=int(g["t"]), family=0x100)
+        base = g["ids"]
+    else:
+        pr = int(g["probe_list"][1])
+        ids, dists, counts = port.ivf_search(s, g["codebook"], g["coarse"], g["packed"], g["list_byte_off"],
+                                             g["list_id_off"], g["list_count"], g["list_ids"], g["queries"], probes=pr,
+                                             r=int(g["r"]), t=int(g["t"]), family=0x100)
+        base = g[f"ids_p{pr}"]
+    assert np.array_equal(ids, g["ids_rr"]) and dists.tobytes() == g["dists_rr"].tobytes()
+    for qi in range(len(ids)):
+        c = int(counts[qi])
+        assert set(ids[qi, :c].tolist()) == set(base[qi, :c].tolist())  # T/test_index.cpp:318-322
+        assert np.all(np.diff(dists[qi, :c]) >= 0)                        # T/test_index.cpp:325
+
+
+def test_ivf_id_out_of_range_is_corruption(port, golden):
+    g = golden("ivf_pq16x4.npz")  # index.hpp:372
+    s = port.spec(int(g["dims"]), str(g["spec"]))
+    bad = g["list_ids"].copy()
+    bad[3] = bad.size + 5
+    with pytest.raises(OracleError) as e:
+        port.ivf_search(s, g["codebook"], g["coarse"], g["packed"], g["list_byte_off"], g["list_id_off"],
+                        g["list_count"], bad, g["queries"], probes=2)
+    assert e.value.kind == "corruption"
