@@ -130,6 +130,13 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
                   const uint64_t* list_count, const uint32_t* ids, const uint8_t* calib_packed,
                   const uint64_t* calib_byte_off, const uint64_t* calib_count, int device, qadc_index** out);
 
+/* Open a QFLT (flat) or QIVF (IVF) container written by the reference (io.hpp:276-326) directly: headers are parsed on
+ * the host, the packed blocks go to the device as they are and are re-laid there.  load_flat_index / load_ivf_index
+ * + the FlatIndex / IvfIndex constructors in one call; same error classes (io 8, corruption 6, invalid_spec 3). */
+int qadc_open_file(const char* path, int device, qadc_index** out);
+/* kind: 0 flat, 1 ivf; count = total codes; cells = K (0 for flat).  Any output may be NULL. */
+int qadc_index_info(const qadc_index* h, int* kind, qadc_spec* spec, uint64_t* count, uint32_t* cells);
+
 void qadc_close(qadc_index* h);
 
 /* FlatIndex::search / IvfIndex::search over a batch (index.hpp:110, 276), host buffers.

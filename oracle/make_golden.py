@@ -64,6 +64,8 @@ def flat_fixture(R: Oracle, name, dims, text, n_db, seed):
         GOLD / f"flat_{name}.npz", spec=text, dims=dims, codebook=cb, codes=codes, packed=packed, count=n_db,
         queries=queries, r=r, t=t, ids=ids, dists=dists, counts=counts, qlut=qlut, params=params, luts=luts,
         prefix=prefix, sums=sums, vector_family=R.auto_family(s), ids_rr=ids_rr, dists_rr=dists_rr)
+    if name in ("pq16x4", "irr655", "pq16x4_short"):  # container fixtures written by the reference's io.hpp
+        R.save_flat(s, cb, packed, n_db, GOLD / f"flat_{name}.qflt")
     print(f"flat_{name}: {text} d={dims} n={n_db} family={R.auto_family(s)}")
 
 
@@ -158,6 +160,7 @@ def ivf_fixture(R: Oracle, name, dims, text, k_cells, n_db, probes, seed):
         list_byte_off=np.array(boff, np.uint64), list_id_off=np.array(ioff, np.uint64),
         list_count=np.array(counts, np.uint64), list_ids=ids, queries=queries, r=50, t=200,
         probe_list=np.array([1, probes, k_cells]), order=order, **out)
+    R.save_ivf(s, cb, coarse, packed, boff, ioff, counts, ids, GOLD / f"ivf_{name}.qivf")
     print(f"ivf_{name}: {text} K={k_cells} n={n_db} min/max list {min(counts)}/{max(counts)}")
 
 

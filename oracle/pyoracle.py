@@ -339,6 +339,22 @@ class Oracle:
                                         _p(asg, C.c_uint32)))
         return cent, asg
 
+    def save_flat(self, s: OrcSpec, codebook, packed, count: int, path: str):
+        assert self.kind == "reference"
+        cb, pk = _f32(codebook), np.ascontiguousarray(packed, dtype=np.uint8)
+        self._check(self.lib.ref_save_flat(C.byref(s), _p(cb, C.c_float), _p(pk, C.c_uint8), C.c_uint64(count),
+                                           str(path).encode()))
+
+    def save_ivf(self, s: OrcSpec, codebook, coarse, packed, list_byte_off, list_id_off, list_count, ids, path: str):
+        assert self.kind == "reference"
+        cb, co = _f32(codebook), _f32(coarse).reshape(-1, s.dims)
+        pk = np.ascontiguousarray(packed, dtype=np.uint8)
+        lbo, lio = np.ascontiguousarray(list_byte_off, dtype=np.uint64), np.ascontiguousarray(list_id_off, dtype=np.uint64)
+        lc, idv = np.ascontiguousarray(list_count, dtype=np.uint64), np.ascontiguousarray(ids, dtype=np.uint32)
+        self._check(self.lib.ref_save_ivf(C.byref(s), _p(cb, C.c_float), _p(co, C.c_float), C.c_uint32(co.shape[0]),
+                                          _p(pk, C.c_uint8), _p(lbo, C.c_uint64), _p(lio, C.c_uint64), _p(lc, C.c_uint64),
+                                          _p(idv, C.c_uint32), str(path).encode()))
+
     def auto_family(self, s: OrcSpec) -> str:
         assert self.kind == "reference"
         return self.lib.ref_auto_family(C.byref(s)).decode()

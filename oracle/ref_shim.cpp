@@ -536,6 +536,30 @@ int ref_kmeans(const float* points, uint64_t n, uint32_t dim, uint32_t k, uint32
     });
 }
 
+// save_flat_index / save_ivf_index (io.hpp:276-307): container fixtures written BY the reference
+int ref_save_flat(const orc_spec* s, const float* codebook, const uint8_t* packed, uint64_t count, const char* path) {
+    return guarded([&] {
+        FlatIndex index(codebook_of(s, codebook), list_of(s, packed, count, s->groups));
+        io::save_flat_index(path, index);
+    });
+}
+
+int ref_save_ivf(const orc_spec* s, const float* codebook, const float* coarse, uint32_t k_cells, const uint8_t* packed,
+                 const uint64_t* list_byte_off, const uint64_t* list_id_off, const uint64_t* list_count,
+                 const uint32_t* ids, const char* path) {
+    return guarded([&] {
+        std::vector<PackedList> lists(k_cells);
+        std::vector<std::vector<uint32_t>> lids(k_cells);
+        for (uint32_t c = 0; c < k_cells; ++c) {
+            lists[c] = list_of(s, packed + list_byte_off[c], list_count[c], s->groups);
+            lids[c].assign(ids + list_id_off[c], ids + list_id_off[c] + list_count[c]);
+        }
+        IvfIndex index(codebook_of(s, codebook), std::vector<float>(coarse, coarse + size_t{k_cells} * s->dims),
+                       std::move(lists), std::move(lids));
+        io::save_ivf_index(path, index);
+    });
+}
+
 // which family select_kernel picks on this host for the spec (kernels.hpp:114-129)
 const char* ref_auto_family(const orc_spec* s) {
     static thread_local std::string name;

@@ -6,5 +6,5 @@ helpers (``layout``), seeded synthetic inputs (``synth``) and the multi-GPU shar
 """
 from ._lib import QadcError, QadcSpec, build, lib  # noqa: F401
 from .index import (FlatIndex, IvfIndex, SearchParams, SearchResult, allocate_dims, encode, merge_topk_device,  # noqa: F401
-                    packed_bytes, scan_list)
+                    open_index, packed_bytes, scan_list)
 from .layout import pack_list, unpack_list  # noqa: F401

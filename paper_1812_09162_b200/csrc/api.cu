@@ -19,6 +19,7 @@ namespace qadc {
 
 void parse_spec(uint32_t dims, const std::string& text, qadc_spec& out);
 void validate_spec(const qadc_spec& s);
+int open_index_file(const char* path, int device, qadc_index** out);
 const char* variant_name(uint32_t v);
 
 static thread_local std::string g_error;
@@ -777,6 +778,24 @@ int qadc_flat_open(const qadc_spec* spec, const float* codebook, const uint8_t* 
         QADC_CUDA_CHECK(cudaStreamSynchronize(h->stream));
         *out = h.release();
     });
+}
+
+int qadc_open_file(const char* path, int device, qadc_index** out) {
+    int inner = QADC_OK;
+    const int rc = guarded([&] {
+        if (!path || !out) throw Error(QADC_ERR_INPUT, "null argument");
+        inner = open_index_file(path, device, out); // parse errors throw; open errors come back as a status
+    });
+    return rc != QADC_OK ? rc : inner;
+}
+
+int qadc_index_info(const qadc_index* h, int* kind, qadc_spec* spec, uint64_t* count, uint32_t* cells) {
+    if (!h) return QADC_ERR_INPUT;
+    if (kind) *kind = h->kind;
+    if (spec) *spec = h->spec;
+    if (count) *count = h->kind == 0 ? h->count : h->total_codes;
+    if (cells) *cells = h->k_cells;
+    return QADC_OK;
 }
 
 void qadc_close(qadc_index* h) {

@@ -247,6 +247,23 @@ class IvfIndex(_Index):
         return out
 
 
+def open_index(path: str, device: int = 0):
+    """load_flat_index / load_ivf_index (io.hpp:286-326) straight onto the GPU: opens a QFLT or QIVF container written
+    by the reference and returns a :class:`FlatIndex` or :class:`IvfIndex`."""
+    h = C.c_void_p()
+    check(lib().qadc_open_file(str(path).encode(), C.c_int(device), C.byref(h)))
+    kind, spec, count, cells = C.c_int(), QadcSpec(), C.c_uint64(), C.c_uint32()
+    check(lib().qadc_index_info(h, C.byref(kind), C.byref(spec), C.byref(count), C.byref(cells)))
+    obj = object.__new__(FlatIndex if kind.value == 0 else IvfIndex)
+    _Index.__init__(obj)
+    obj._h, obj.spec, obj.device = h, spec, device
+    if kind.value == 0:
+        obj.count = int(count.value)
+    else:
+        obj.total, obj.k_cells = int(count.value), int(cells.value)
+    return obj
+
+
 def scan_list(spec: QadcSpec, packed, count: int, qlut, *, rows=None, width=None, ids=None, base_id=0, acc_init=0,
               cap=100, heap_in=None, device=0):
     """The QuantizedScanFn contract (simd/kernels.hpp:49-50, scan_scalar.hpp:34-64) on the GPU.

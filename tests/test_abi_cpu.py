@@ -100,3 +100,50 @@ def test_cpp_binding_fails_loudly_without_gpu(L):
     out = subprocess.run([str(exe), "1"], capture_output=True, text=True, timeout=120)
     assert out.returncode != 0
     assert "no usable CUDA device" in out.stderr
+
+
+# ------------------------------------------------ N1: container loader, host-side parsing --
+
+def _open_raises(path):
+    import ctypes as C
+    h = C.c_void_p()
+    rc = qb.lib().qadc_open_file(str(path).encode(), 0, C.byref(h))
+    return rc, qb.lib().qadc_last_error().decode()
+
+
+def test_container_parse_errors(L, tmp_path):
+    """Header parsing mirrors io.hpp's error classes and happens before any device work (so it is testable here)."""
+    from pathlib import Path
+    gold = Path(__file__).resolve().parent / "golden"
+    good = (gold / "flat_pq16x4.qflt").read_bytes()
+    assert _open_raises(tmp_path / "missing.qflt")[0] == 8                      # io_error: cannot open
+    p = tmp_path / "x.bin"
+    p.write_bytes(b"NOPE" + good[4:])
+    assert _open_raises(p)[0] == 8                                              # bad magic (io.hpp:54-58)
+    p.write_bytes(good[:4] + (2).to_bytes(4, "little") + good[8:])
+    assert _open_raises(p)[0] == 8                                              # unsupported version (io.hpp:288-289)
+    p.write_bytes(good[: len(good) // 2])
+    assert _open_raises(p)[0] == 8                                              # truncated (io.hpp:39)
+    # QFLT(8) QADC(8) dims ngroups g widths(2) dim_alloc(16*4) codebook ... ; corrupt one dim_alloc entry
+    off = 8 + 8 + 12 + 2
+    bad = bytearray(good)
+    bad[off] ^= 1
+    p.write_bytes(bytes(bad))
+    assert _open_raises(p)[0] == 6                                              # allocation mismatch (io.hpp:191-192)
+    # flip a bit of the stored spec hash inside the QPKD header
+    q = good.index(b"QPKD")
+    bad = bytearray(good)
+    bad[q + 8] ^= 0x40
+    p.write_bytes(bytes(bad))
+    rc, msg = _open_raises(p)
+    assert rc == 6 and "hash" in msg                                            # io.hpp:258-259
+    bad = bytearray(good)
+    bad[q + 16] = 16                                                            # word width 8 -> 16
+    p.write_bytes(bytes(bad))
+    assert _open_raises(p)[0] == 6                                              # scheme mismatch (io.hpp:260-262)
+    bad = bytearray(good)
+    bad[q + 24] = 2                                                             # two lists in a flat index
+    p.write_bytes(bytes(bad))
+    assert _open_raises(p)[0] in (6, 8)                                         # io.hpp:293 (or EOF while reading list 2)
+    if L.qadc_device_count() <= 0:
+        assert _open_raises(gold / "flat_pq16x4.qflt")[0] == 20                 # a valid file still needs a device

@@ -518,3 +518,35 @@ def test_rerank_vs_oracle_and_shard_refusal(port):
         with pytest.raises(qb.QadcError) as e:
             shard.search(queries, qb.SearchParams(rerank=True))
         assert e.value.kind == "config"
+
+
+# ------------------------------------------------ N1: reference containers opened directly --
+
+@pytest.mark.parametrize("stem", ["flat_pq16x4", "flat_irr655", "flat_pq16x4_short"])
+def test_open_qflt_written_by_reference(golden, stem):
+    """QFLT written by the reference's save_flat_index (io.hpp:276-284): open directly, search, compare."""
+    from tests.conftest import GOLDEN
+    g = golden(stem + ".npz")
+    with qb.open_index(GOLDEN / (stem + ".qflt")) as idx:
+        assert isinstance(idx, qb.FlatIndex) and idx.size() == int(g["count"])
+        assert np.array_equal(idx.download_codes(0, idx.size()), g["codes"])
+        res = idx.search(g["queries"], qb.SearchParams(r=int(g["r"]), t=int(g["t"])))
+    assert np.array_equal(res.counts, g["counts"])
+    for qi in range(len(g["queries"])):
+        c = int(res.counts[qi])
+        assert np.array_equal(res.ids[qi, :c], g["ids"][qi, :c]) and bits_equal(res.dists[qi, :c], g["dists"][qi, :c])
+
+
+@pytest.mark.parametrize("stem", ["ivf_irr655", "ivf_pq16x4"])
+def test_open_qivf_written_by_reference(golden, stem):
+    from tests.conftest import GOLDEN
+    g = golden(stem + ".npz")
+    with qb.open_index(GOLDEN / (stem + ".qivf")) as idx:
+        assert isinstance(idx, qb.IvfIndex) and idx.cells() == len(g["list_count"]) and idx.size() == int(g["list_count"].sum())
+        for pr in g["probe_list"]:
+            res = idx.search(g["queries"], qb.SearchParams(probes=int(pr), r=int(g["r"]), t=int(g["t"])))
+            assert np.array_equal(res.counts, g[f"counts_p{pr}"])
+            for qi in range(len(g["queries"])):
+                c = int(res.counts[qi])
+                assert np.array_equal(res.ids[qi, :c], g[f"ids_p{pr}"][qi, :c])
+                assert bits_equal(res.dists[qi, :c], g[f"dists_p{pr}"][qi, :c])
