@@ -190,6 +190,14 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
 int qadc_encode(const qadc_spec* spec, const float* codebook, const float* vectors, uint64_t n, uint8_t* codes,
                 int device);
 
+/* IVF list construction given trained centroids and a residual codebook -- the data-dependent half of
+ * IvfIndex::build (index.hpp:195-227; "next" row N3): nearest coarse centroid under a double accumulator, ties to
+ * the lowest cell (kmeans.hpp:178-190), fp32 residual (index.hpp:200), encode (codebook.hpp:94-118).
+ * assign: n u32 cells; codes: n*m subcodes.  The caller groups vectors by cell in index order and packs each list
+ * (index.hpp:219-227; paper_1812_09162_b200.index.build_ivf_lists does). */
+int qadc_ivf_assign_encode(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
+                           const float* vectors, uint64_t n, uint32_t* assign, uint8_t* codes, int device);
+
 int qadc_get_stats(const qadc_index* h, qadc_stats* out);
 /* tuning knobs for experiments: name in {"cand_cap","seg0","seg_growth","force_variant","threads"} */
 int qadc_set_option(qadc_index* h, const char* name, int64_t value);

@@ -164,6 +164,17 @@ def ivf_fixture(R: Oracle, name, dims, text, k_cells, n_db, probes, seed):
     print(f"ivf_{name}: {text} K={k_cells} n={n_db} min/max list {min(counts)}/{max(counts)}")
 
 
+def ivf_build_fixture(R: Oracle, name, dims, text, k_cells, n_db, seed):
+    """IvfIndex::build itself (index.hpp:179-230): its trained centroids/codebook plus the lists it produced, so
+    that the assignment + residual-encode + pack stage can be replayed from the same inputs."""
+    rng = np.random.default_rng(seed)
+    db = blobs(rng, n_db, dims, clusters=30)
+    built = R.ivf_build(db, text, k_cells, iters=6, seed=seed)
+    np.savez_compressed(GOLD / f"ivfbuild_{name}.npz", spec=text, dims=dims, vectors=db, **built)
+    print(f"ivfbuild_{name}: {text} K={k_cells} n={n_db} min/max list "
+          f"{int(built['list_count'].min())}/{int(built['list_count'].max())}")
+
+
 def main():
     build()
     R = Oracle("reference")
@@ -176,6 +187,8 @@ def main():
     scan_fixture(R)
     ivf_fixture(R, "irr655", 48, "12x{6,5,5}", 24, 4000, 6, seed=300)
     ivf_fixture(R, "pq16x4", 32, "8x{4,4}", 12, 2500, 4, seed=301)
+    ivf_build_fixture(R, "pq8x4", 32, "8x{4,4}", 20, 3000, seed=400)
+    ivf_build_fixture(R, "irr655", 48, "12x{6,5,5}", 40, 3500, seed=401)
 
 
 if __name__ == "__main__":

@@ -155,6 +155,15 @@ class Oracle:
                                         _p(out, C.c_uint8)))
         return out
 
+    def ivf_assign_encode(self, s: OrcSpec, codebook, coarse, vectors):
+        cb, co, v = _f32(codebook), _f32(coarse).reshape(-1, s.dims), _f32(vectors).reshape(-1, s.dims)
+        assign = np.empty(v.shape[0], dtype=np.uint32)
+        codes = np.empty((v.shape[0], s.m), dtype=np.uint8)
+        self._check(self.lib.orc_ivf_assign_encode(C.byref(s), _p(cb, C.c_float), _p(co, C.c_float),
+                                                   C.c_uint32(co.shape[0]), _p(v, C.c_float), C.c_uint64(v.shape[0]),
+                                                   _p(assign, C.c_uint32), _p(codes, C.c_uint8)))
+        return assign, codes
+
     # -- tables ------------------------------------------------------------
     def compute_tables(self, s: OrcSpec, codebook: np.ndarray, query: np.ndarray) -> np.ndarray:
         cb, q = _f32(codebook), _f32(query)
@@ -338,6 +347,30 @@ class Oracle:
                                         C.c_uint32(iters), C.c_uint64(seed), _p(cent, C.c_float),
                                         _p(asg, C.c_uint32)))
         return cent, asg
+
+    def ivf_build(self, vectors, spec_text: str, k_coarse: int, iters=8, seed=0):
+        """The reference's IvfIndex::build (index.hpp:179-230) -> dict of its codebook, centroids, lists and ids."""
+        assert self.kind == "reference"
+        v = _f32(vectors)
+        n, dims = v.shape
+        self.lib.ref_ivf_build.restype = C.c_void_p
+        h = self.lib.ref_ivf_build(_p(v, C.c_float), C.c_uint64(n), C.c_uint32(dims), spec_text.encode(),
+                                   C.c_uint32(k_coarse), C.c_uint32(iters), C.c_uint64(seed))
+        if not h:
+            raise OracleError(1, self.lib.orc_last_error().decode())
+        h = C.c_void_p(h)
+        sizes = np.zeros(3, dtype=np.uint64)
+        self.lib.ref_ivf_built_sizes(h, _p(sizes, C.c_uint64))
+        out = dict(codebook=np.empty(int(sizes[0]), np.float32), coarse=np.empty((k_coarse, dims), np.float32),
+                   packed=np.empty(int(sizes[1]), np.uint8), list_byte_off=np.empty(k_coarse, np.uint64),
+                   list_id_off=np.empty(k_coarse, np.uint64), list_count=np.empty(k_coarse, np.uint64),
+                   ids=np.empty(int(sizes[2]), np.uint32))
+        self.lib.ref_ivf_built_get(h, _p(out["codebook"], C.c_float), _p(out["coarse"], C.c_float),
+                                   _p(out["packed"], C.c_uint8), _p(out["list_byte_off"], C.c_uint64),
+                                   _p(out["list_id_off"], C.c_uint64), _p(out["list_count"], C.c_uint64),
+                                   _p(out["ids"], C.c_uint32))
+        self.lib.ref_ivf_built_free(h)
+        return out
 
     def save_flat(self, s: OrcSpec, codebook, packed, count: int, path: str):
         assert self.kind == "reference"

@@ -844,3 +844,34 @@ int orc_ivf_search_h(void* hv, const float* queries, uint32_t nq, uint32_t probe
                           probes, r, t, family, threads, out_ids, out_dists, out_counts);
 }
 void orc_ivf_destroy(void* h) { free(h); }
+
+/* -------------------------------------------------- IVF list construction -- */
+
+int orc_ivf_assign_encode(const orc_spec* s, const float* codebook, const float* coarse, uint32_t k_cells,
+                          const float* vectors, uint64_t n, uint32_t* assign, uint8_t* codes) {
+    if (k_cells == 0) return fail(ORC_ERR_TRAINING, "ivf: no coarse centroids");
+    float* resid = (float*)malloc(sizeof(float) * s->dims);
+    for (uint64_t v = 0; v < n; ++v) {
+        const float* x = vectors + v * s->dims;
+        double best = INFINITY; /* kmeans.hpp:178-190: final assignment, ties go to the lowest centroid index */
+        uint32_t best_c = 0;
+        for (uint32_t c = 0; c < k_cells; ++c) {
+            const float* ctr = coarse + (size_t)c * s->dims;
+            double acc = 0.0; /* detail::sq_dist, kmeans.hpp:41-48 */
+            for (uint32_t j = 0; j < s->dims; ++j) {
+                double d = (double)x[j] - (double)ctr[j];
+                acc += d * d;
+            }
+            if (acc < best) {
+                best = acc;
+                best_c = c;
+            }
+        }
+        assign[v] = best_c;
+        const float* ctr = coarse + (size_t)best_c * s->dims;
+        for (uint32_t j = 0; j < s->dims; ++j) resid[j] = x[j] - ctr[j]; /* index.hpp:200 */
+        orc_encode(s, codebook, resid, 1, codes + v * s->m);
+    }
+    free(resid);
+    return ORC_OK;
+}

@@ -135,6 +135,13 @@ int orc_ivf_search(const orc_spec* s, const float* codebook, const float* coarse
                    uint32_t probes, uint32_t r, uint32_t t, int family, int threads, uint32_t* out_ids,
                    float* out_dists, uint32_t* out_counts);
 
+/* IVF list construction given a trained coarse quantizer and residual codebook (the data-dependent half of
+ * IvfIndex::build, index.hpp:195-227): nearest coarse centroid under a DOUBLE accumulator, ties to the lowest index
+ * (kmeans.hpp:178-190, detail::sq_dist :41-48); residual = x - centroid in fp32 (index.hpp:200); encode
+ * (codebook.hpp:94-118).  assign: n u32; codes: n*m bytes. */
+int orc_ivf_assign_encode(const orc_spec* s, const float* codebook, const float* coarse, uint32_t k_cells,
+                          const float* vectors, uint64_t n, uint32_t* assign, uint8_t* codes);
+
 /* Handle-based variants for timing (bench.py cpu_baseline): the index is built once, searches reuse it.
  * The port keeps pointers into the caller's arrays (they must stay alive); the reference shim builds a
  * pqscan::FlatIndex / pqscan::IvfIndex once. */

@@ -536,6 +536,84 @@ int ref_kmeans(const float* points, uint64_t n, uint32_t dim, uint32_t k, uint32
     });
 }
 
+// The data-dependent half of IvfIndex::build given trained centroids + codebook.  The reference only exposes it
+// inside build(); the port's restatement is exported under the common name, and ref_ivf_build below runs the REAL
+// build so that tests can feed its centroids/codebook back and demand byte-identical lists.
+int orc_ivf_assign_encode(const orc_spec* s, const float* codebook, const float* coarse, uint32_t k_cells,
+                          const float* vectors, uint64_t n, uint32_t* assign, uint8_t* codes) {
+    return guarded([&] {
+        Codebook cb = codebook_of(s, codebook);
+        std::vector<float> residual(s->dims);
+        for (uint64_t v = 0; v < n; ++v) {
+            const float* x = vectors + v * s->dims;
+            double best = std::numeric_limits<double>::infinity();
+            uint32_t best_c = 0;
+            for (uint32_t c = 0; c < k_cells; ++c) {
+                double d = detail::sq_dist(x, coarse + size_t{c} * s->dims, s->dims); // kmeans.hpp:41-48
+                if (d < best) {
+                    best = d;
+                    best_c = c;
+                }
+            }
+            assign[v] = best_c;
+            for (uint32_t j = 0; j < s->dims; ++j) residual[j] = x[j] - coarse[size_t{best_c} * s->dims + j];
+            Code c = encode(residual, cb);
+            std::memcpy(codes + v * s->m, c.data(), s->m);
+        }
+    });
+}
+
+// IvfIndex::build (index.hpp:179-230), the real thing, behind a handle with getters.
+struct RefBuilt {
+    IvfIndex index;
+};
+void* ref_ivf_build(const float* vectors, uint64_t n, uint32_t dims, const char* spec_text, uint32_t k_coarse,
+                    uint32_t iters, uint64_t seed) {
+    try {
+        IvfBuildConfig cfg;
+        cfg.k_coarse = k_coarse;
+        cfg.train.kmeans_iters = iters;
+        cfg.train.seed = seed;
+        return new RefBuilt{IvfIndex::build({vectors, n * dims}, n, parse_spec_string(spec_text), cfg)};
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+// sizes: [0] codebook floats, [1] total packed bytes, [2] total ids
+void ref_ivf_built_sizes(void* hv, uint64_t* sizes) {
+    const IvfIndex& ix = static_cast<RefBuilt*>(hv)->index;
+    uint64_t cbf = 0, pb = 0, ni = 0;
+    for (size_t j = 0; j < ix.codebook().spec().num_subs(); ++j) cbf += ix.codebook().sub_table(j).size();
+    for (const auto& l : ix.lists()) pb += l.data.size();
+    for (const auto& v : ix.list_ids()) ni += v.size();
+    sizes[0] = cbf;
+    sizes[1] = pb;
+    sizes[2] = ni;
+}
+void ref_ivf_built_get(void* hv, float* codebook, float* coarse, uint8_t* packed, uint64_t* byte_off, uint64_t* id_off,
+                       uint64_t* counts, uint32_t* ids) {
+    const IvfIndex& ix = static_cast<RefBuilt*>(hv)->index;
+    size_t o = 0;
+    for (size_t j = 0; j < ix.codebook().spec().num_subs(); ++j) {
+        const auto& t = ix.codebook().sub_table(j);
+        std::memcpy(codebook + o, t.data(), t.size() * 4);
+        o += t.size();
+    }
+    std::memcpy(coarse, ix.coarse_centroids().data(), ix.coarse_centroids().size() * 4);
+    uint64_t b = 0, i = 0;
+    for (uint32_t c = 0; c < ix.cells(); ++c) {
+        byte_off[c] = b;
+        id_off[c] = i;
+        counts[c] = ix.lists()[c].count;
+        std::memcpy(packed + b, ix.lists()[c].data.data(), ix.lists()[c].data.size());
+        std::memcpy(ids + i, ix.list_ids()[c].data(), ix.list_ids()[c].size() * 4);
+        b += ix.lists()[c].data.size();
+        i += ix.list_ids()[c].size();
+    }
+}
+void ref_ivf_built_free(void* hv) { delete static_cast<RefBuilt*>(hv); }
+
 // save_flat_index / save_ivf_index (io.hpp:276-307): container fixtures written BY the reference
 int ref_save_flat(const orc_spec* s, const float* codebook, const uint8_t* packed, uint64_t count, const char* path) {
     return guarded([&] {

@@ -1068,6 +1068,44 @@ int qadc_encode(const qadc_spec* spec, const float* codebook, const float* vecto
     });
 }
 
+int qadc_ivf_assign_encode(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
+                           const float* vectors, uint64_t n, uint32_t* assign, uint8_t* codes, int device) {
+    return guarded([&] {
+        if (!spec || !codebook || !coarse || (n && (!vectors || !assign || !codes)))
+            throw Error(QADC_ERR_INPUT, "ivf build: null argument");
+        if (k_cells == 0) throw Error(QADC_ERR_INPUT, "ivf build: no coarse centroids");
+        validate_spec(*spec);
+        set_device(device);
+        const DevSpec ds = make_dev_spec(*spec, spec->groups);
+        const uint32_t dims = spec->dims;
+        std::vector<float> ct(size_t(dims) * k_cells);
+        for (uint32_t c = 0; c < k_cells; ++c)
+            for (uint32_t j = 0; j < dims; ++j) ct[size_t(j) * k_cells + c] = coarse[size_t(c) * dims + j];
+        const uint64_t batch = std::min<uint64_t>(1u << 17, std::max<uint64_t>(n, 1));
+        DevBuf cb, co, cot, v, resid, scratch, asg, c;
+        cb.ensure(size_t(spec->cb_floats) * 4);
+        co.ensure(ct.size() * 4);
+        cot.ensure(ct.size() * 4);
+        v.ensure(size_t(batch) * dims * 4);
+        resid.ensure(size_t(batch) * dims * 4);
+        scratch.ensure(ivf_assign_scratch_bytes(k_cells, batch));
+        asg.ensure(size_t(batch) * 4);
+        c.ensure(size_t(batch) * spec->m);
+        QADC_CUDA_CHECK(cudaMemcpy(cb.p, codebook, size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice));
+        QADC_CUDA_CHECK(cudaMemcpy(co.p, coarse, ct.size() * 4, cudaMemcpyHostToDevice));
+        QADC_CUDA_CHECK(cudaMemcpy(cot.p, ct.data(), ct.size() * 4, cudaMemcpyHostToDevice));
+        for (uint64_t i = 0; i < n; i += batch) {
+            const uint64_t nb = std::min(batch, n - i);
+            QADC_CUDA_CHECK(cudaMemcpy(v.p, vectors + i * dims, size_t(nb) * dims * 4, cudaMemcpyHostToDevice));
+            launch_ivf_assign(v.as<float>(), co.as<float>(), cot.as<float>(), dims, k_cells, nb, scratch.p,
+                              asg.as<uint32_t>(), resid.as<float>(), nullptr);
+            launch_encode(ds, cb.as<float>(), resid.as<float>(), nb, c.as<uint8_t>(), nullptr);
+            QADC_CUDA_CHECK(cudaMemcpy(assign + i, asg.p, size_t(nb) * 4, cudaMemcpyDeviceToHost));
+            QADC_CUDA_CHECK(cudaMemcpy(codes + i * spec->m, c.p, size_t(nb) * spec->m, cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
 int qadc_get_stats(const qadc_index* h, qadc_stats* out) {
     if (!h || !out) return QADC_ERR_INPUT;
     *out = h->stats;

@@ -173,6 +173,10 @@ void launch_unlayout(const DevSpec& ds, const uint8_t* d_codes, uint64_t first, 
                      cudaStream_t stream);
 void launch_adc_sums(const DevSpec& ds, const uint8_t* d_codes, const void* d_qlut, uint32_t acc_init,
                      uint64_t first, uint64_t n, uint32_t* d_sums, cudaStream_t stream);
+size_t ivf_assign_scratch_bytes(uint32_t k_cells, uint64_t n);
+void launch_ivf_assign(const float* d_vectors, const float* d_coarse, const float* d_coarse_t, uint32_t dims,
+                       uint32_t k_cells, uint64_t n, void* d_scratch, uint32_t* d_assign, float* d_resid,
+                       cudaStream_t stream);
 void launch_encode(const DevSpec& ds, const float* d_codebook, const float* d_vectors, uint64_t n, uint8_t* d_codes,
                    cudaStream_t stream);
 

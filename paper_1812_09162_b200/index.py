@@ -14,6 +14,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from .layout import pack_list
 from ._lib import QadcError, QadcSearchParams, QadcSpec, QadcStats, check, lib
 
 KERNEL_FAMILY = "b200-smem-lut"  # reported in SearchResult.kernel (the reference reports its SIMD family)
@@ -301,6 +302,44 @@ def encode(spec: QadcSpec, codebook, vectors, device: int = 0) -> np.ndarray:
     check(lib().qadc_encode(C.byref(spec), _p(cb, C.c_float), _p(v, C.c_float), C.c_uint64(v.shape[0]),
                             _p(out, C.c_uint8), C.c_int(device)))
     return out
+
+
+def ivf_assign_encode(spec: QadcSpec, codebook, coarse, vectors, device: int = 0):
+    """The data-dependent half of IvfIndex::build (index.hpp:195-227) on the GPU: nearest coarse centroid (double
+    accumulator, ties to the lowest cell, kmeans.hpp:178-190), fp32 residual (index.hpp:200), residual encode.
+    Returns (assign[n] u32, codes[n, m] u8)."""
+    cb = _f32(codebook).reshape(-1)
+    co = _f32(coarse).reshape(-1, spec.dims)
+    v = _f32(vectors).reshape(-1, spec.dims)
+    assign = np.empty(v.shape[0], dtype=np.uint32)
+    codes = np.empty((v.shape[0], spec.m), dtype=np.uint8)
+    check(lib().qadc_ivf_assign_encode(C.byref(spec), _p(cb, C.c_float), _p(co, C.c_float), C.c_uint32(co.shape[0]),
+                                       _p(v, C.c_float), C.c_uint64(v.shape[0]), _p(assign, C.c_uint32),
+                                       _p(codes, C.c_uint8), C.c_int(device)))
+    return assign, codes
+
+
+def build_ivf_lists(spec: QadcSpec, codebook, coarse, vectors, device: int = 0) -> dict:
+    """IVF lists for `vectors` under trained `coarse` centroids and a residual `codebook`, laid out as
+    IvfIndex::build does (index.hpp:219-227): each cell's members in ascending vector index, one PackedList per
+    cell, ids = vector indices.  Assignment and encode run on the GPU (ivf_assign_encode); the grouping and the
+    byte packing are host numpy.  The dict's keys are IvfIndex's constructor arguments."""
+    co = _f32(coarse).reshape(-1, spec.dims)
+    k_cells = co.shape[0]
+    assign, codes = ivf_assign_encode(spec, codebook, co, vectors, device)
+    order = np.argsort(assign, kind="stable").astype(np.uint32)
+    counts = np.bincount(assign, minlength=k_cells).astype(np.uint64)
+    id_off = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
+    parts, byte_off, b = [], np.zeros(k_cells, dtype=np.uint64), 0
+    for c in range(k_cells):
+        byte_off[c] = b
+        if counts[c]:
+            i0 = int(id_off[c])
+            parts.append(pack_list(spec, codes[order[i0:i0 + int(counts[c])]]))
+            b += parts[-1].size
+    packed = np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint8)
+    return dict(packed=packed, list_byte_off=byte_off, list_id_off=id_off, list_count=counts, ids=order,
+                assign=assign)
 
 
 def merge_topk_device(d_keys, nshards: int, nq: int, r: int, d_map, d_ids, d_dists, d_counts, device: int,

@@ -550,3 +550,60 @@ def test_open_qivf_written_by_reference(golden, stem):
                 c = int(res.counts[qi])
                 assert np.array_equal(res.ids[qi, :c], g[f"ids_p{pr}"][qi, :c])
                 assert bits_equal(res.dists[qi, :c], g[f"dists_p{pr}"][qi, :c])
+
+
+# ------------------------------------------------------------------ N3: IVF list construction --
+
+@pytest.mark.parametrize("name", ["ivfbuild_pq8x4.npz", "ivfbuild_irr655.npz"])
+def test_ivf_build_lists_match_reference_build(golden, name):
+    """GPU assignment + residual encode + pack reproduces, byte for byte, the lists the reference's
+    IvfIndex::build produced from the same vectors (fixture holds its centroids, codebook, lists and ids)."""
+    g = golden(name)
+    s = qb.allocate_dims(int(g["dims"]), str(g["spec"]))
+    built = qb.build_ivf_lists(s, g["codebook"], g["coarse"], g["vectors"])
+    for key in ("packed", "list_byte_off", "list_id_off", "list_count", "ids"):
+        assert np.array_equal(built[key], g[key]), key
+
+
+def test_ivf_assign_encode_vs_oracle_many_cells(port):
+    """More cells than one CTA covers (cross-block reduction), duplicated centroids (ties to the lowest cell),
+    a ragged vector count, NaN / infinite inputs (never win: cell 0, like the reference's '<' loop)."""
+    rng = np.random.default_rng(12)
+    dims, text, k = 40, "10x{4,4}", 1000
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = rng.standard_normal(s.cb_floats).astype(np.float32)
+    coarse = (rng.standard_normal((k, dims)) * 3).astype(np.float32)
+    coarse[700] = coarse[5]
+    coarse[999] = coarse[300]
+    v = (rng.standard_normal((2500 + 7, dims)) * 3).astype(np.float32)
+    v[0], v[1] = coarse[5], coarse[300]
+    v[2, 3] = np.nan
+    v[3, 0] = np.inf
+    a, c = qb.ivf_assign_encode(s, cb, coarse, v)
+    a2, c2 = port.ivf_assign_encode(so, cb, coarse, v)
+    assert a[0] == 5 and a[1] == 300 and a[2] == 0 and a[3] == 0
+    assert np.array_equal(a, a2)
+    ok = np.ones(len(v), bool)
+    ok[2:4] = False  # the residual of a NaN/inf vector encodes to whatever '<' on NaN picks; compared separately
+    assert np.array_equal(c[ok], c2[ok])
+    assert np.array_equal(c[~ok], c2[~ok])
+
+
+def test_ivf_built_on_gpu_then_searched(port):
+    """End to end: lists built on the GPU, opened, searched -- equal to the oracle searching the oracle-built lists."""
+    rng = np.random.default_rng(13)
+    dims, text, k, n = 48, "12x{6,5,5}", 64, 30000
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    centres = rng.standard_normal((k, dims)).astype(np.float32) * 4
+    v = (centres[rng.integers(0, k, size=n)] + rng.standard_normal((n, dims))).astype(np.float32)
+    cb = (rng.standard_normal(s.cb_floats) * 0.7).astype(np.float32)
+    b = qb.build_ivf_lists(s, cb, centres, v)
+    a2, c2 = port.ivf_assign_encode(so, cb, centres, v)
+    assert np.array_equal(b["assign"], a2)
+    queries = (centres[rng.integers(0, k, size=20)] + rng.standard_normal((20, dims))).astype(np.float32)
+    want = port.ivf_search(so, cb, centres, b["packed"], b["list_byte_off"], b["list_id_off"], b["list_count"],
+                           b["ids"], queries, probes=8, r=50, t=200, threads=4)
+    with qb.IvfIndex(s, cb, centres, b["packed"], b["list_byte_off"], b["list_id_off"], b["list_count"],
+                     b["ids"]) as idx:
+        got = idx.search(queries, qb.SearchParams(probes=8, r=50, t=200))
+    assert np.array_equal(got.ids, want[0]) and bits_equal(got.dists, want[1]) and np.array_equal(got.counts, want[2])

@@ -320,3 +320,50 @@ def test_ivf_id_out_of_range_is_corruption(port, golden):
         port.ivf_search(s, g["codebook"], g["coarse"], g["packed"], g["list_byte_off"], g["list_id_off"],
                         g["list_count"], bad, g["queries"], probes=2)
     assert e.value.kind == "corruption"
+
+
+def _lists_equal(g, built, spec_pack, codes_by_cell=None):
+    k = len(g["list_count"])
+    for c in range(k):
+        cnt, i0, b0 = int(g["list_count"][c]), int(g["list_id_off"][c]), int(g["list_byte_off"][c])
+        assert cnt == int(built["list_count"][c])
+        assert np.array_equal(g["ids"][i0:i0 + cnt], built["ids"][int(built["list_id_off"][c]):][:cnt])
+        nb = spec_pack(cnt)
+        assert np.array_equal(g["packed"][b0:b0 + nb], built["packed"][int(built["list_byte_off"][c]):][:nb])
+
+
+@pytest.mark.parametrize("name", ["ivfbuild_pq8x4.npz", "ivfbuild_irr655.npz"])
+def test_golden_ivf_build_lists(port, golden, name):
+    """The port's assignment + residual encode, grouped and packed as index.hpp:219-227 does, reproduces the lists
+    IvfIndex::build itself produced from the same vectors, centroids and codebook (fixture written by the reference)."""
+    g = golden(name)
+    s = port.spec(int(g["dims"]), str(g["spec"]))
+    assign, codes = port.ivf_assign_encode(s, g["codebook"], g["coarse"], g["vectors"])
+    k = len(g["list_count"])
+    order = np.argsort(assign, kind="stable").astype(np.uint32)
+    counts = np.bincount(assign, minlength=k).astype(np.uint64)
+    id_off = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
+    parts, boff, b = [], [], 0
+    for c in range(k):
+        boff.append(b)
+        pk = port.pack_list(s, codes[order[int(id_off[c]):int(id_off[c] + counts[c])]]) if counts[c] else np.zeros(0, np.uint8)
+        parts.append(pk)
+        b += pk.size
+    built = dict(packed=np.concatenate(parts), list_byte_off=np.array(boff, np.uint64), list_id_off=id_off,
+                 list_count=counts, ids=order)
+    per_block = s.block_len * s.groups * (s.word_width // 8)
+    _lists_equal(g, built, lambda cnt: (cnt + s.block_len - 1) // s.block_len * per_block)
+
+
+def test_live_ivf_assign_encode(port, ref):
+    rng = np.random.default_rng(9)
+    dims, text, k = 32, "8x{4,4}", 300
+    s = port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats)).astype(np.float32)
+    coarse = (rng.standard_normal((k, dims)) * 3).astype(np.float32)
+    coarse[257] = coarse[3]  # exact tie: the lower cell wins
+    v = (rng.standard_normal((500, dims)) * 3).astype(np.float32)
+    v[0] = coarse[3]
+    a, c = port.ivf_assign_encode(s, cb, coarse, v)
+    a2, c2 = ref.ivf_assign_encode(s, cb, coarse, v)
+    assert a[0] == 3 and np.array_equal(a, a2) and np.array_equal(c, c2)
