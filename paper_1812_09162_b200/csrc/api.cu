@@ -154,7 +154,7 @@ struct qadc_index {
     cudaStream_t stream = nullptr;
     qadc_spec spec{};
     DevSpec ds{};
-    DevBuf codebook, codes, calib, ids;
+    DevBuf codebook, codebook_t, codes, calib, ids, slot_pair;
     uint64_t count = 0, count_padded = 0;
     uint32_t base_id = 0;
     uint32_t calib_count = 0;
@@ -476,8 +476,12 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->scratch.as<float>(), h->cta_begin.as<uint32_t>(),
                          h->order.as<uint32_t>(), st);
         const size_t t1 = h->timer.mark(st);
-        launch_ivf_tables(ds, h->codebook.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(), n_pairs, a,
-                          h->luts.as<float>(), h->pmin.as<float>(), h->own_min.as<float>(), st);
+        if (ivf_tables_tiled_supported(ds))
+            launch_ivf_tables_tiled(ds, h->codebook_t.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(),
+                                    n_pairs, a, h->luts.as<float>(), h->pmin.as<float>(), h->own_min.as<float>(), st);
+        else
+            launch_ivf_tables(ds, h->codebook.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(), n_pairs, a,
+                              h->luts.as<float>(), h->pmin.as<float>(), h->own_min.as<float>(), st);
         const size_t t2 = h->timer.mark(st);
         launch_ivf_calib(ds, h->own_heads ? h->codes.as<uint8_t>() : h->calib.as<uint8_t>(),
                          h->own_heads ? h->list_code_off.as<uint64_t>() : h->calib_code_off.as<uint64_t>(),
@@ -528,25 +532,22 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         h->row_query.ensure(std::max<size_t>(nslots * 4, 16));
         h->row_bias.ensure(std::max<size_t>(nslots * 4, 16));
         h->tile_lut.ensure(std::max<size_t>(nslots * ds.E * tile_entry_bytes(plan.variant), 16));
-        if (nslots) {
-            QADC_CUDA_CHECK(cudaMemsetAsync(h->row_query.p, 0xFF, nslots * 4, st));
-            QADC_CUDA_CHECK(cudaMemsetAsync(h->row_bias.p, 0, nslots * 4, st));
-            QADC_CUDA_CHECK(cudaMemsetAsync(h->qlut.p, 0, nslots * ds.E * wb, st));
-        }
+        h->slot_pair.ensure(std::max<size_t>(nslots * 4, 16));
         const size_t t4 = h->timer.mark(st);
-        launch_ivf_quantize(ds, h->order.as<uint32_t>(), n_pairs, a, h->luts.as<float>(), h->pmin.as<float>(),
-                            h->own_min.as<float>(), h->qparams.as<float>(), h->pair_rank.as<uint32_t>(),
-                            h->tile_base.as<uint32_t>(), tq, h->qlut.p, h->row_query.as<uint32_t>(),
-                            h->row_bias.as<uint32_t>(), h->pair_slot.as<uint32_t>(), st);
+        // quantize every tile's rows (padding rows: zero table, no query) and emit the scan's tile image
+        launch_ivf_quantize_pack(plan.variant, ds, h->order.as<uint32_t>(), n_pairs, a, h->luts.as<float>(),
+                                 h->pmin.as<float>(), h->own_min.as<float>(), h->qparams.as<float>(),
+                                 h->pair_rank.as<uint32_t>(), h->tile_base.as<uint32_t>(), tq, ntiles, h->qlut.p,
+                                 h->tile_lut.p, h->row_query.as<uint32_t>(), h->row_bias.as<uint32_t>(),
+                                 h->pair_slot.as<uint32_t>(), h->slot_pair.as<uint32_t>(), st);
         const size_t t5 = h->timer.mark(st);
-        launch_pack_tiles(plan.variant, h->qlut.p, ds.word_width, ds.E, uint32_t(nslots), tq, h->tile_lut.p, st);
-        const size_t t6 = h->timer.mark(st);
+        const size_t t6 = t5;
         h->timer.span(0, t0, t1, 101); // probe order
         h->timer.span(0, t1, t2, 102); // residual tables
         h->timer.span(0, t2, t3, 103); // calibration + grouping
         h->timer.span(0, t3, t4, 104); // host: tile layout, memsets
-        h->timer.span(0, t4, t5, 105); // quantize
-        h->timer.span(0, t5, t6, 106); // tile pack
+        h->timer.span(0, t4, t5, 105); // quantize + tile pack
+        (void)t6;
 
         h->sel.ensure(nb, p.r, cap);
         launch_init_select(h->sel.thr_key.as<uint64_t>(), h->sel.cand_count.as<uint32_t>(), h->sel.ntop.as<uint32_t>(),
@@ -1151,6 +1152,18 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
             if (!(codebook[i] - codebook[i] == 0.0f)) throw Error(QADC_ERR_CORRUPTION, "codebook: non-finite centroid component");
         h->codebook.ensure(size_t(spec->cb_floats) * 4);
         QADC_CUDA_CHECK(cudaMemcpyAsync(h->codebook.p, codebook, size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice, st));
+        {   // [sub][dim][entry] image of the codebook for the register-tiled table kernel (ivf_lut.cu)
+            std::vector<float> cbt(spec->cb_floats);
+            const DevSpec tds = make_dev_spec(*spec, spec->groups);
+            for (uint32_t j = 0; j < tds.m; ++j) {
+                const uint32_t nent = 1u << tds.bits[j], dsub = tds.dim_alloc[j];
+                for (uint32_t i = 0; i < nent; ++i)
+                    for (uint32_t t = 0; t < dsub; ++t)
+                        cbt[tds.cb_off[j] + size_t(t) * nent + i] = codebook[tds.cb_off[j] + size_t(i) * dsub + t];
+            }
+            h->codebook_t.ensure(size_t(spec->cb_floats) * 4);
+            QADC_CUDA_CHECK(cudaMemcpy(h->codebook_t.p, cbt.data(), size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice));
+        }
         const uint32_t d = spec->dims;
         // coarse centroids: row-major for the residuals, transposed [dims][K] for the probe kernel
         std::vector<float> ct(size_t(k_cells) * d);

@@ -145,6 +145,16 @@ void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t 
 void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* d_queries, const float* d_coarse,
                        const uint32_t* d_order, uint32_t n_pairs, uint32_t a, float* d_luts, float* d_pmin,
                        float* d_own_min, cudaStream_t stream);
+bool ivf_tables_tiled_supported(const DevSpec& ds);
+void launch_ivf_tables_tiled(const DevSpec& ds, const float* d_codebook_t, const float* d_queries,
+                             const float* d_coarse, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
+                             float* d_luts, float* d_pmin, float* d_own_min, cudaStream_t stream);
+void launch_ivf_quantize_pack(ScanVariant v, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
+                              const float* d_luts, const float* d_pmin, const float* d_own_min,
+                              const float* d_qparams, const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base,
+                              uint32_t tq, uint32_t ntiles, void* d_qluts, void* d_tile_lut, uint32_t* d_row_query,
+                              uint32_t* d_row_bias, uint32_t* d_pair_slot, uint32_t* d_slot_pair,
+                              cudaStream_t stream);
 void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_calib_codes, const uint64_t* d_calib_code_off,
                       const uint64_t* d_calib_count, const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq,
                       uint32_t a,

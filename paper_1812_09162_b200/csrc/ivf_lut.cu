@@ -1,0 +1,316 @@
+// ivf_lut.cu -- the table stage of IvfIndex::search at batch scale (index.hpp:282-288, 319-328).
+//
+// A batch of nq queries x a probes is nq*a independent table sets (6.4e5 of them at C5), i.e. more
+// bytes and flops than the probe-order stage.  Two kernels, both keeping the reference's fp32
+// operation order per table entry (compute_tables, distance.hpp:35-58; quantize_tables, :102-142):
+//
+//   ivf_tables_tiled_kernel   thread = table entry, register-tiled over TAB_PT (query, cell) pairs:
+//                             the entry's centroid lives in registers (loaded coalesced from the
+//                             [sub][dim][entry] transposed codebook), the pairs' residuals sit in
+//                             shared memory as [dim][pair] for 128-bit broadcast loads.
+//   ivf_quantize_pack_kernel  one CTA per LUT tile: quantizes the tile's rows against their
+//                             queries' shared bounds and writes BOTH images the scan uses -- the
+//                             [row][entry] table (exact re-evaluation, seeding) and the transposed,
+//                             variant-typed [entry][row] tile (tilepack.cu's layout) -- in one pass.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace qadc {
+
+static constexpr int TAB_PT = 16;   // pairs per CTA batch
+static constexpr int TAB_MAXD = 16; // widest subquantizer slice the register tile holds
+static constexpr uint32_t NONE32 = 0xFFFFFFFFu;
+
+__device__ __forceinline__ void fill_sub_of(const DevSpec& ds, uint8_t* sub_of) {
+    for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x) {
+        uint32_t j = 0;
+        while (j + 1 < ds.m && ds.ent_off[j + 1] <= e) ++j;
+        sub_of[e] = uint8_t(j);
+    }
+}
+
+// dynamic smem: res[dims][TAB_PT] | pmin_u[TAB_PT][m] (u32 bit patterns) | sub_of[E]
+__global__ void __launch_bounds__(256)
+ivf_tables_tiled_kernel(DevSpec ds, const float* __restrict__ codebook_t, const float* __restrict__ queries,
+                        const float* __restrict__ coarse, const uint32_t* __restrict__ order, uint32_t a,
+                        uint32_t n_pairs, float* __restrict__ luts, float* __restrict__ pmin_out,
+                        float* __restrict__ own_min) {
+    extern __shared__ __align__(16) float smf[];
+    float* res = smf;
+    uint32_t* pmin_u = reinterpret_cast<uint32_t*>(res + size_t(ds.dims) * TAB_PT);
+    uint8_t* sub_of = reinterpret_cast<uint8_t*>(pmin_u + size_t(ds.m) * TAB_PT);
+    __shared__ uint32_t s_q[TAB_PT], s_cell[TAB_PT];
+    const uint32_t pair0 = blockIdx.x * TAB_PT;
+    const uint32_t np = min(uint32_t(TAB_PT), n_pairs - pair0);
+    fill_sub_of(ds, sub_of);
+    if (threadIdx.x < TAB_PT) {
+        const uint32_t pair = pair0 + threadIdx.x;
+        s_q[threadIdx.x] = threadIdx.x < np ? pair / a : 0;
+        s_cell[threadIdx.x] = threadIdx.x < np ? order[pair] : 0;
+    }
+    for (uint32_t u = threadIdx.x; u < ds.m * TAB_PT; u += blockDim.x) pmin_u[u] = 0x7f800000u; // +inf
+    __syncthreads();
+    // residual = query - centroid (index.hpp:286), one fp32 subtraction per component
+    for (uint32_t p = 0; p < TAB_PT; ++p) {
+        const float* q = queries + size_t(s_q[p]) * ds.dims;
+        const float* c = coarse + size_t(s_cell[p]) * ds.dims;
+        for (uint32_t d = threadIdx.x; d < ds.dims; d += blockDim.x)
+            res[d * TAB_PT + p] = p < np ? __fsub_rn(q[d], c[d]) : 0.0f;
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x) {
+        const uint32_t j = sub_of[e];
+        const uint32_t dsub = ds.dim_alloc[j], nent = 1u << ds.bits[j];
+        const float* ct = codebook_t + ds.cb_off[j] + (e - ds.ent_off[j]);
+        float c[TAB_MAXD];
+#pragma unroll
+        for (int t = 0; t < TAB_MAXD; ++t) c[t] = uint32_t(t) < dsub ? ct[uint32_t(t) * nent] : 0.0f;
+        float acc[TAB_PT];
+#pragma unroll
+        for (int p = 0; p < TAB_PT; ++p) acc[p] = 0.0f;
+        const float4* rv = reinterpret_cast<const float4*>(res + size_t(ds.dim_off[j]) * TAB_PT);
+#pragma unroll
+        for (int t = 0; t < TAB_MAXD; ++t) {
+            if (uint32_t(t) < dsub) {
+#pragma unroll
+                for (int v = 0; v < TAB_PT / 4; ++v) {
+                    const float4 x = rv[t * (TAB_PT / 4) + v];
+                    float d;
+                    d = __fsub_rn(x.x, c[t]); acc[4 * v + 0] = __fadd_rn(acc[4 * v + 0], __fmul_rn(d, d));
+                    d = __fsub_rn(x.y, c[t]); acc[4 * v + 1] = __fadd_rn(acc[4 * v + 1], __fmul_rn(d, d));
+                    d = __fsub_rn(x.z, c[t]); acc[4 * v + 2] = __fadd_rn(acc[4 * v + 2], __fmul_rn(d, d));
+                    d = __fsub_rn(x.w, c[t]); acc[4 * v + 3] = __fadd_rn(acc[4 * v + 3], __fmul_rn(d, d));
+                }
+            }
+        }
+        // per-table minima (min is order independent; entries are >= +0 or NaN, for which the unsigned order
+        // of the bit patterns is the "x < best" rule started from +inf): reduce over the lanes of this warp
+        // that sit in the same table, then one shared-memory atomic per (pair, table, warp)
+        const uint32_t peers = __match_any_sync(__activemask(), j);
+        const bool leader = (threadIdx.x & 31) == uint32_t(__ffs(peers) - 1);
+        float* out = luts + size_t(pair0) * ds.E + e;
+#pragma unroll
+        for (int p = 0; p < TAB_PT; ++p) {
+            if (uint32_t(p) < np) out[size_t(p) * ds.E] = acc[p];
+            const uint32_t mn = __reduce_min_sync(peers, __float_as_uint(acc[p]));
+            if (leader) atomicMin(&pmin_u[p * ds.m + j], mn);
+        }
+    }
+    __syncthreads();
+    for (uint32_t u = threadIdx.x; u < np * ds.m; u += blockDim.x)
+        pmin_out[size_t(pair0) * ds.m + u] = __uint_as_float(pmin_u[u]);
+    if (threadIdx.x < np) { // table-order sum (DistanceTables::min_total, distance.hpp:28-32)
+        float s = 0.0f;
+        for (uint32_t j = 0; j < ds.m; ++j) s = __fadd_rn(s, __uint_as_float(pmin_u[threadIdx.x * ds.m + j]));
+        own_min[pair0 + threadIdx.x] = s;
+    }
+}
+
+bool ivf_tables_tiled_supported(const DevSpec& ds) {
+    for (uint32_t j = 0; j < ds.m; ++j)
+        if (ds.dim_alloc[j] > uint32_t(TAB_MAXD)) return false;
+    const size_t smem = sizeof(float) * TAB_PT * (size_t(ds.dims) + ds.m) + ds.E;
+    return smem <= 160 * 1024;
+}
+
+void launch_ivf_tables_tiled(const DevSpec& ds, const float* d_codebook_t, const float* d_queries,
+                             const float* d_coarse, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
+                             float* d_luts, float* d_pmin, float* d_own_min, cudaStream_t stream) {
+    if (n_pairs == 0) return;
+    const size_t smem = sizeof(float) * TAB_PT * (size_t(ds.dims) + ds.m) + ds.E;
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_tables_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ivf_tables_tiled_kernel<<<(n_pairs + TAB_PT - 1) / TAB_PT, 256, smem, stream>>>(
+        ds, d_codebook_t, d_queries, d_coarse, d_order, a, n_pairs, d_luts, d_pmin, d_own_min);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------- slot <-> pair map --
+
+__global__ void ivf_slot_map_kernel(const uint32_t* __restrict__ order, const uint32_t* __restrict__ pair_rank,
+                                    const uint32_t* __restrict__ cell_tile_base, uint32_t tq, uint32_t n_pairs,
+                                    uint32_t* __restrict__ pair_slot, uint32_t* __restrict__ slot_pair) {
+    const uint32_t pair = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pair >= n_pairs) return;
+    const uint32_t rank = pair_rank[pair];
+    if (rank == NONE32) { // empty list: skipped by the search loop (index.hpp:321)
+        pair_slot[pair] = NONE32;
+        return;
+    }
+    const uint32_t slot = cell_tile_base[order[pair]] * tq + rank;
+    pair_slot[pair] = slot;
+    slot_pair[slot] = pair;
+}
+
+// ------------------------------------------------------------ quantize + tile pack --
+
+// quantize_tables' entry rule (distance.hpp:117-124): fp32 saturation test, then
+// floor((double(p) - double(pmin)) / double(delta)).  The division is replaced by a multiplication with
+// rcp = RN(1/delta) whenever that provably gives the same floor: with Q = RN(x/delta) and y = RN(x*rcp),
+// |y - Q| <= 3*2^-53*Q < 2^-34 for Q < 2^17, so when y's fractional part is farther than 2^-30 from an
+// integer floor(y) == floor(Q).  Anything else (near-integers, huge or non-finite values) takes the division.
+__device__ __forceinline__ uint32_t quantize_entry_fast(float p, float pmin, float d_min, float d_max, float delta,
+                                                        double rcp, uint32_t qmax) {
+    if (delta <= 0.0f) return p == pmin ? 0u : qmax;
+    if (__fsub_rn(p, pmin) >= __fsub_rn(d_max, d_min)) return qmax;
+    if (p == pmin) return 0u; // every table's own minimum: x = 0 exactly
+    const double x = __dsub_rn(double(p), double(pmin));
+    const double y = __dmul_rn(x, rcp);
+    if (y >= 0.0 && y < 131072.0) {
+        const double k = floor(y);
+        const double f = __dsub_rn(y, k); // exact
+        if (f > 0x1p-30 && f < 1.0 - 0x1p-30) return k >= double(qmax) ? qmax : uint32_t(k);
+    }
+    const double q = floor(__ddiv_rn(x, double(delta)));
+    if (q >= double(qmax)) return qmax;
+    return uint32_t(q);
+}
+
+template <class Entry>
+__device__ __forceinline__ Entry tile_entry(uint32_t v, bool high_byte);
+template <>
+__device__ __forceinline__ __half tile_entry<__half>(uint32_t v, bool hb) {
+    return __uint2half_rn(hb ? v >> 8 : v); // exact: <= 255 whenever a half entry is used
+}
+template <>
+__device__ __forceinline__ float tile_entry<float>(uint32_t v, bool) { return float(v); }
+template <>
+__device__ __forceinline__ unsigned short tile_entry<unsigned short>(uint32_t v, bool) { return (unsigned short)v; }
+template <>
+__device__ __forceinline__ unsigned char tile_entry<unsigned char>(uint32_t v, bool hb) {
+    return (unsigned char)(hb ? v >> 8 : v);
+}
+
+static constexpr uint32_t QP_SLAB = 512; // entries per shared-memory panel
+
+// grid = tiles; block = 256.  dynamic smem: panel u16 [min(E, QP_SLAB)][tq + 2] | sub_of[E]
+template <class Entry>
+__global__ void __launch_bounds__(256)
+ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uint32_t a,
+                         const float* __restrict__ luts, const float* __restrict__ pmin,
+                         const float* __restrict__ own_min, const float* __restrict__ qparams, uint32_t tq,
+                         bool high_byte, void* __restrict__ qluts, Entry* __restrict__ tile_lut,
+                         uint32_t* __restrict__ row_query, uint32_t* __restrict__ row_bias) {
+    extern __shared__ __align__(16) unsigned short panel[];
+    const uint32_t slab_cap = min(ds.E, QP_SLAB), pitch = tq + 2;
+    uint8_t* sub_of = reinterpret_cast<uint8_t*>(panel + size_t(slab_cap) * pitch);
+    fill_sub_of(ds, sub_of);
+    __syncthreads();
+    const uint32_t tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (uint32_t e0 = 0; e0 < ds.E; e0 += slab_cap) {
+        const uint32_t ne = min(slab_cap, ds.E - e0);
+        for (uint32_t r = warp; r < tq; r += nwarps) {
+            const uint32_t slot = tile * tq + r;
+            const uint32_t pair = slot_pair[slot];
+            if (pair == NONE32) { // padding row: zero table, no query
+                for (uint32_t e = lane; e < ne; e += 32) {
+                    panel[e * pitch + r] = 0;
+                    if (ds.word_width == 8) reinterpret_cast<uint8_t*>(qluts)[size_t(slot) * ds.E + e0 + e] = 0;
+                    else reinterpret_cast<uint16_t*>(qluts)[size_t(slot) * ds.E + e0 + e] = 0;
+                }
+                if (e0 == 0 && lane == 0) {
+                    row_query[slot] = NONE32;
+                    row_bias[slot] = 0;
+                }
+                continue;
+            }
+            const uint32_t qi = pair / a;
+            const float d_min = qparams[size_t(qi) * 4 + 0], d_max = qparams[size_t(qi) * 4 + 1];
+            const float delta = qparams[size_t(qi) * 4 + 2];
+            const double rcp = delta > 0.0f ? __drcp_rn(double(delta)) : 0.0;
+            const float* lut = luts + size_t(pair) * ds.E + e0;
+            const float* pm = pmin + size_t(pair) * ds.m;
+            for (uint32_t eb = lane; eb < ne; eb += 128) { // four independent loads in flight per lane
+                float pv[4], pmv[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t e = eb + 32 * k;
+                    pv[k] = e < ne ? lut[e] : 0.0f;
+                    pmv[k] = e < ne ? pm[sub_of[e0 + e]] : 0.0f;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t e = eb + 32 * k;
+                    if (e >= ne) break;
+                    const uint32_t qv = quantize_entry_fast(pv[k], pmv[k], d_min, d_max, delta, rcp, ds.qmax);
+                    panel[e * pitch + r] = (unsigned short)qv;
+                    if (ds.word_width == 8) reinterpret_cast<uint8_t*>(qluts)[size_t(slot) * ds.E + e0 + e] = uint8_t(qv);
+                    else reinterpret_cast<uint16_t*>(qluts)[size_t(slot) * ds.E + e0 + e] = uint16_t(qv);
+                }
+            }
+            if (e0 == 0 && lane == 0) {
+                uint32_t bias = 0;
+                if (delta > 0.0f) { // float math, index.hpp:325-327
+                    const float b = floorf(__fdiv_rn(__fsub_rn(own_min[pair], d_min), delta));
+                    bias = b >= float(ds.qmax) ? ds.qmax : uint32_t(b);
+                }
+                row_query[slot] = qi;
+                row_bias[slot] = bias;
+            }
+        }
+        __syncthreads();
+        Entry* dst = tile_lut + (size_t(tile) * ds.E + e0) * tq;
+        if ((tq & (tq - 1)) == 0) {
+            const uint32_t lg = 31 - __clz(tq);
+            for (uint32_t u = threadIdx.x; u < ne * tq; u += blockDim.x)
+                dst[u] = tile_entry<Entry>(panel[(u >> lg) * pitch + (u & (tq - 1))], high_byte);
+        } else {
+            for (uint32_t u = threadIdx.x; u < ne * tq; u += blockDim.x)
+                dst[u] = tile_entry<Entry>(panel[(u / tq) * pitch + u % tq], high_byte);
+        }
+        __syncthreads();
+    }
+}
+
+template <class Entry>
+static void launch_qp(const DevSpec& ds, const uint32_t* slot_pair, uint32_t a, const float* luts, const float* pmin,
+                      const float* own_min, const float* qparams, uint32_t tq, bool hb, void* qluts, void* tile_lut,
+                      uint32_t* row_query, uint32_t* row_bias, uint32_t ntiles, cudaStream_t stream) {
+    const size_t smem = size_t(std::min(ds.E, QP_SLAB)) * (tq + 2) * sizeof(unsigned short) + ds.E;
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_quantize_pack_kernel<Entry>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    ivf_quantize_pack_kernel<Entry><<<ntiles, 256, smem, stream>>>(ds, slot_pair, a, luts, pmin, own_min, qparams, tq, hb,
+                                                                   qluts, static_cast<Entry*>(tile_lut), row_query,
+                                                                   row_bias);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_ivf_quantize_pack(ScanVariant v, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
+                              const float* d_luts, const float* d_pmin, const float* d_own_min,
+                              const float* d_qparams, const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base,
+                              uint32_t tq, uint32_t ntiles, void* d_qluts, void* d_tile_lut, uint32_t* d_row_query,
+                              uint32_t* d_row_bias, uint32_t* d_pair_slot, uint32_t* d_slot_pair,
+                              cudaStream_t stream) {
+    if (n_pairs == 0) return;
+    if (ntiles) QADC_CUDA_CHECK(cudaMemsetAsync(d_slot_pair, 0xFF, size_t(ntiles) * tq * 4, stream));
+    ivf_slot_map_kernel<<<(n_pairs + 255) / 256, 256, 0, stream>>>(d_order, d_pair_rank, d_cell_tile_base, tq, n_pairs,
+                                                                   d_pair_slot, d_slot_pair);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+    if (ntiles == 0) return;
+    const bool wide = ds.word_width == 16;
+    switch (v) {
+    case VAR_F16X8:
+    case VAR_F16X4_C4:
+        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, false, d_qluts, d_tile_lut,
+                                 d_row_query, d_row_bias, ntiles, stream);
+    case VAR_F16X4H:
+    case VAR_F16X4H_C2:
+    case VAR_F16X4H_C4:
+        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, wide, d_qluts, d_tile_lut,
+                                 d_row_query, d_row_bias, ntiles, stream);
+    case VAR_F32X2:
+        return launch_qp<float>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, false, d_qluts, d_tile_lut,
+                                d_row_query, d_row_bias, ntiles, stream);
+    case VAR_U16X1:
+        return launch_qp<unsigned short>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, false, d_qluts,
+                                         d_tile_lut, d_row_query, d_row_bias, ntiles, stream);
+    case VAR_U8X1:
+        return launch_qp<unsigned char>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, wide, d_qluts,
+                                        d_tile_lut, d_row_query, d_row_bias, ntiles, stream);
+    default: throw Error(QADC_ERR_CONFIG, "quantize_pack: bad variant");
+    }
+}
+
+} // namespace qadc
