@@ -165,7 +165,7 @@ struct qadc_index {
     DevBuf locator;        // ivf, unsharded: id -> device code position (IvfIndex::build_locator, index.hpp:366-375)
     std::vector<uint64_t> list_code_off_h, list_count_h;
     uint64_t total_codes = 0;
-    uint32_t ivf_round0 = 512; // list positions scanned in the first round (then x seg_growth per round)
+    uint32_t ivf_round0 = 4096; // list positions scanned in the first round (then x seg_growth per round)
     // ivf workspace
     DevBuf order, pmin, own_min, qparams, cell_npairs, pair_rank, pair_slot, tile_base, row_query, row_bias, cta_begin, round_begin;
     // options

@@ -84,6 +84,7 @@ struct ScanArgs {
     uint32_t* cand_count;      // [nq]
     uint32_t cap;
     uint32_t* overflow;        // [nq] set to 1 when a candidate did not fit
+    uint32_t tile_bufs;        // 1 or 2 LUT tile buffers in shared memory (filled in by launch_scan from the plan)
 };
 
 struct ScanPlan {
@@ -91,6 +92,7 @@ struct ScanPlan {
     uint32_t tq;         // rows per tile
     uint32_t smem_bytes;
     uint32_t threads;
+    uint32_t tile_bufs;  // 2 when a second LUT tile buffer fits: the next job's tile is prefetched
 };
 
 // chooses the variant for a spec (throws config error if nothing fits shared memory)

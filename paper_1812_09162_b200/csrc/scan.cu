@@ -331,11 +331,11 @@ template <class P, class G, int EARLY>
 __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param, ScanArgs args_param) {
     constexpr int CIF = 2; // codes in flight per lane group
     extern __shared__ __align__(1024) char smem[];
-    // dynamic smem: [0, E*ROWB) LUT tile | NSTAGE code stage buffers
+    // dynamic smem: tile_bufs x [E*ROWB) LUT tile | NSTAGE code stage buffers | per-warp queues
     __shared__ DevSpec s_ds;
     __shared__ ScanArgs s_args;
     __shared__ __align__(8) uint64_t s_full[NSTAGE], s_empty[NSTAGE];
-    __shared__ __align__(8) uint64_t s_tbar; // LUT tile arrival
+    __shared__ __align__(8) uint64_t s_tfull[2], s_tempty[2]; // LUT tile buffers: arrival / release
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
@@ -345,7 +345,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
             mbar_init(&s_full[i], 1);           // the producer's arrive.expect_tx
             mbar_init(&s_empty[i], SCAN_WARPS); // one arrival per consumer warp
         }
-        mbar_init(&s_tbar, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_tfull[i], 1);
+            mbar_init(&s_tempty[i], SCAN_WARPS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -354,8 +357,9 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
 
     const uint32_t E = G::RUNTIME ? ds->E : uint32_t(G::E);
     const uint32_t stride = ds->code_stride;
-    char* tile = smem;
-    char* stage = smem + size_t(E) * P::ROWB;
+    const uint32_t tile_bytes = E * P::ROWB;
+    const uint32_t tile_bufs = a->tile_bufs == 2 ? 2u : 1u;
+    char* stage = smem + size_t(tile_bufs) * tile_bytes;
     const uint32_t stage_codes = STAGE_BYTES / stride;
 
     // contiguous slice of the job list for this CTA
@@ -366,9 +370,25 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     if (warp == SCAN_WARPS) {
         if (lane != 0) return;
         uint32_t it = 0; // running stage-fill counter, mirrored by the consumers
+        uint32_t tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0; // LUT tiles issued so far
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
             const ScanJob job = a->jobs[ji];
             if (job.n_codes == 0 || job.n_rows == 0) continue;
+            if (job.row_begin != prev_rb || job.n_rows != prev_nr) {
+                // next LUT tile: the image [entry][row] was prepared up front (tilepack.cu / ivf_lut.cu), so it
+                // is a few bulk copies.  With two buffers it lands while the consumers still scan the
+                // previous job; with one, the wait below is the hand-over.
+                prev_rb = job.row_begin;
+                prev_nr = job.n_rows;
+                const uint32_t tb = tile_bufs == 2 ? (tseq & 1u) : 0u, use = tile_bufs == 2 ? (tseq >> 1) : tseq;
+                mbar_wait(&s_tempty[tb], (use & 1u) ^ 1u); // first use passes immediately
+                const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / P::TQ) * tile_bytes;
+                char* dst = smem + size_t(tb) * tile_bytes;
+                mbar_expect_tx(&s_tfull[tb], tile_bytes);
+                for (uint32_t off = 0; off < tile_bytes; off += 32768u)
+                    bulk_g2s(dst + off, src + off, min(32768u, tile_bytes - off), &s_tfull[tb]);
+                ++tseq;
+            }
             const uint8_t* gcodes = a->codes + job.code_off * stride;
             const uint32_t n_sub = (job.n_codes + stage_codes - 1) / stage_codes;
             for (uint32_t sub = 0; sub < n_sub; ++sub, ++it) {
@@ -386,7 +406,8 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
 
     // ============================ consumer warps ==============================================
     uint32_t cur_row_begin = 0xFFFFFFFFu, cur_n_rows = 0;
-    uint32_t tile_phase = 0, it = 0;
+    uint32_t tseq = 0, it = 0;
+    const char* tile = smem;
     typename P::Acc acc0;
     {
         float t[P::QPL];
@@ -410,17 +431,12 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
 
         // ---- (re)load the LUT tile when the row range changes ----
         if (job.row_begin != cur_row_begin || job.n_rows != cur_n_rows) {
-            consumer_sync(); // every consumer is done with the previous tile
+            if (tseq > 0) { // this warp is done with the previous tile's buffer
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_tempty[tile_bufs == 2 ? ((tseq - 1) & 1u) : 0u]);
+            }
             cur_row_begin = job.row_begin;
             cur_n_rows = job.n_rows;
-            // the tile image [entry][row] was prepared by tilepack.cu: bulk async copies, 32 KB each
-            if (tid == 0) {
-                const uint32_t tile_bytes = E * P::ROWB;
-                const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / P::TQ) * tile_bytes;
-                mbar_expect_tx(&s_tbar, tile_bytes);
-                for (uint32_t off = 0; off < tile_bytes; off += 32768u)
-                    bulk_g2s(tile + off, src + off, min(32768u, tile_bytes - off), &s_tbar);
-            }
             // per-lane accumulator start: bias - threshold - 1/2 (sign bit <=> admitted)
             float t[P::QPL];
 #pragma unroll
@@ -445,8 +461,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                 }
             }
             P::init(acc0, t);
-            mbar_wait(&s_tbar, tile_phase); // every thread observes the tile's arrival itself
-            tile_phase ^= 1u;
+            const uint32_t tb = tile_bufs == 2 ? (tseq & 1u) : 0u, use = tile_bufs == 2 ? (tseq >> 1) : tseq;
+            mbar_wait(&s_tfull[tb], use & 1u); // every thread observes the tile's arrival itself
+            tile = smem + size_t(tb) * tile_bytes;
+            ++tseq;
         }
 
         // ---- consume the job's codes stage by stage ----
@@ -615,6 +633,12 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
         default: throw Error(QADC_ERR_CONFIG, "scan: unknown forced variant");
         }
         if (!fits(p.smem_bytes)) throw Error(QADC_ERR_CONFIG, "scan: forced variant does not fit shared memory");
+        p.tile_bufs = 1;
+        const uint32_t tile_bytes = p.smem_bytes - (NSTAGE * STAGE_BYTES + WQ_BYTES);
+        if (fits(p.smem_bytes + tile_bytes)) {
+            p.tile_bufs = 2;
+            p.smem_bytes += tile_bytes;
+        }
         return p;
     }
     if (u8 && fits(smem_need<PolF16x8>(ds.E))) set(VAR_F16X8, PolF16x8::TQ, smem_need<PolF16x8>(ds.E));
@@ -628,6 +652,13 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
     else
         throw Error(QADC_ERR_CONFIG, "scan: the quantized tables of this spec (" + std::to_string(ds.E) +
                                          " entries) do not fit shared memory; no CPU fallback exists");
+    // a second tile buffer (the next job's tile lands while this one is scanned) whenever it fits
+    p.tile_bufs = 1;
+    const uint32_t tile_bytes = p.smem_bytes - (NSTAGE * STAGE_BYTES + WQ_BYTES);
+    if (fits(p.smem_bytes + tile_bytes)) {
+        p.tile_bufs = 2;
+        p.smem_bytes += tile_bytes;
+    }
     return p;
 }
 
@@ -651,8 +682,10 @@ static void launch_one(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& 
 
 // Compile-time geometries are instantiated only for the (policy, shape) pairs the planner
 // can actually pick for the named 64-bit specs; everything else runs the runtime geometry.
-void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
-    if (args.n_jobs == 0 || grid <= 0) return;
+void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_in, int grid, cudaStream_t stream) {
+    if (args_in.n_jobs == 0 || grid <= 0) return;
+    ScanArgs args = args_in;
+    args.tile_bufs = plan.tile_bufs;
     switch (plan.variant) {
     case VAR_F16X8:
         if (G44::matches(ds)) return launch_one<PolF16x8, G44>(plan, ds, args, grid, stream);
