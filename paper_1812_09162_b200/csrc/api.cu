@@ -155,6 +155,11 @@ struct qadc_index {
     qadc_spec spec{};
     DevSpec ds{};
     DevBuf codebook, codebook_t, codes, calib, ids, slot_pair;
+    DevBuf coarse_bf16, coarse_norm, coarse_mean, q_bf16, probe_eps; // tensor-core probe prefilter (ivf_probe_tc.cu)
+    double coarse_rmax = 0.0;
+    uint32_t dpad = 0;
+    bool probe_tc_ready = false;
+    int probe_tc = 1; // option: 0 = always the exact FP32 probe kernels
     uint64_t count = 0, count_padded = 0;
     uint32_t base_id = 0;
     uint32_t calib_count = 0;
@@ -424,6 +429,28 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
 
 // ------------------------------------------------------------------ IVF search --
 
+// probe order of nb queries into h->order; h->scratch holds the [nb][K] distance image
+static void ivf_probe_order_device(qadc_index* h, const float* dq, uint32_t nb, uint32_t a, cudaStream_t st) {
+    const DevSpec& ds = h->ds;
+    const uint32_t K = h->k_cells;
+    h->scratch.ensure(size_t(nb) * K * 4);
+    h->cta_begin.ensure(size_t(nb) * 4); // reused as the probe-selection redo flags
+    if (h->probe_tc && h->probe_tc_ready && ivf_probe_tc_supported(ds.dims, K, a)) {
+        h->q_bf16.ensure(size_t(nb) * h->dpad * 2);
+        h->probe_eps.ensure(size_t(nb) * 8);
+        launch_ivf_probe_tc(dq, h->coarse.as<float>(), h->coarse_bf16.as<uint16_t>(),
+                            h->coarse_norm.as<float>(), h->coarse_mean.as<double>(), h->coarse_rmax, ds.dims, h->dpad, K,
+                            nb, a, h->q_bf16.as<uint16_t>(), h->probe_eps.as<double>(),
+                            h->scratch.as<float>(), h->cta_begin.as<uint32_t>(), h->order.as<uint32_t>(), st);
+        // queries the prefilter could not decide (candidate overflow, non-finite input): exact kernels
+        launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->scratch.as<float>(),
+                         h->cta_begin.as<uint32_t>(), h->order.as<uint32_t>(), st, true);
+    } else {
+        launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->scratch.as<float>(),
+                         h->cta_begin.as<uint32_t>(), h->order.as<uint32_t>(), st);
+    }
+}
+
 static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq, const qadc_search_params& p,
                               uint32_t* d_ids, float* d_dists, uint32_t* d_counts, uint64_t* d_keys, float* d_map,
                               cudaStream_t st) {
@@ -471,10 +498,7 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         QADC_CUDA_CHECK(cudaMemsetAsync(h->cell_npairs.p, 0, size_t(K) * 4, st));
 
         const size_t t0 = h->timer.mark(st);
-        h->scratch.ensure(size_t(nb) * K * 4);
-        h->cta_begin.ensure(size_t(nb) * 4); // reused as the probe-selection redo flags
-        launch_ivf_probe(dq, h->coarse_t.as<float>(), ds.dims, K, nb, a, h->scratch.as<float>(), h->cta_begin.as<uint32_t>(),
-                         h->order.as<uint32_t>(), st);
+        ivf_probe_order_device(h, dq, nb, a, st);
         const size_t t1 = h->timer.mark(st);
         if (ivf_tables_tiled_supported(ds))
             launch_ivf_tables_tiled(ds, h->codebook_t.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(),
@@ -1121,6 +1145,7 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384));
         else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
         else if (n == "force_variant") h->force_variant = int(value);
+        else if (n == "probe_tc") h->probe_tc = int(value);
         else if (n == "ivf_round0") h->ivf_round0 = uint32_t(std::max<int64_t>(value, 64));
         else throw Error(QADC_ERR_CONFIG, "set_option: unknown option " + n);
     });
@@ -1174,6 +1199,21 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
         if (k_cells) {
             QADC_CUDA_CHECK(cudaMemcpyAsync(h->coarse.p, coarse, ct.size() * 4, cudaMemcpyHostToDevice, st));
             QADC_CUDA_CHECK(cudaMemcpyAsync(h->coarse_t.p, ct.data(), ct.size() * 4, cudaMemcpyHostToDevice, st));
+        }
+        if (k_cells >= 512) { // tensor-core probe prefilter: centred bf16 image of the centroids, |c'|^2, max |c'|
+            h->dpad = (d + 15) / 16 * 16;
+            std::vector<uint16_t> cb16;
+            std::vector<float> cn;
+            std::vector<double> mean;
+            h->probe_tc_ready = ivf_probe_tc_prepare(coarse, k_cells, d, h->dpad, cb16, cn, mean, h->coarse_rmax);
+            if (h->probe_tc_ready) {
+                h->coarse_bf16.ensure(cb16.size() * 2);
+                h->coarse_norm.ensure(cn.size() * 4);
+                h->coarse_mean.ensure(mean.size() * 8);
+                QADC_CUDA_CHECK(cudaMemcpy(h->coarse_bf16.p, cb16.data(), cb16.size() * 2, cudaMemcpyHostToDevice));
+                QADC_CUDA_CHECK(cudaMemcpy(h->coarse_norm.p, cn.data(), cn.size() * 4, cudaMemcpyHostToDevice));
+                QADC_CUDA_CHECK(cudaMemcpy(h->coarse_mean.p, mean.data(), mean.size() * 8, cudaMemcpyHostToDevice));
+            }
         }
         // every list starts on a 16-code boundary of the device array (bulk copies need 16-byte alignment)
         const uint64_t LIST_ALIGN = 16;
@@ -1270,10 +1310,7 @@ int qadc_ivf_probe_order(qadc_index* h, const float* queries, uint32_t nq, uint3
         h->queries.ensure(size_t(nq) * h->ds.dims * 4);
         h->order.ensure(size_t(nq) * a * 4);
         QADC_CUDA_CHECK(cudaMemcpyAsync(h->queries.p, queries, size_t(nq) * h->ds.dims * 4, cudaMemcpyHostToDevice, st));
-        h->scratch.ensure(size_t(nq) * h->k_cells * 4);
-        h->cta_begin.ensure(size_t(nq) * 4);
-        launch_ivf_probe(h->queries.as<float>(), h->coarse_t.as<float>(), h->ds.dims, h->k_cells, nq, a,
-                         h->scratch.as<float>(), h->cta_begin.as<uint32_t>(), h->order.as<uint32_t>(), st);
+        ivf_probe_order_device(h, h->queries.as<float>(), nq, a, st);
         QADC_CUDA_CHECK(cudaMemcpyAsync(order, h->order.p, size_t(nq) * a * 4, cudaMemcpyDeviceToHost, st));
         QADC_CUDA_CHECK(cudaStreamSynchronize(st));
     });

@@ -6,6 +6,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "qadc.h"
 
@@ -143,7 +144,16 @@ void launch_ivf_relayout(const qadc_spec& s, const DevSpec& ds, const uint8_t* d
                          uint8_t* d_codes, cudaStream_t stream);
 void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t dims, uint32_t k_cells, uint32_t nq,
                       uint32_t a, float* d_dist_scratch /* [nq][K] */, uint32_t* d_redo /* [nq] */, uint32_t* d_order,
-                      cudaStream_t stream);
+                      cudaStream_t stream, bool redo_only = false);
+// tensor-core prefilter of the probe order (ivf_probe_tc.cu)
+bool ivf_probe_tc_supported(uint32_t dims, uint32_t k_cells, uint32_t a);
+bool ivf_probe_tc_prepare(const float* coarse, uint32_t k_cells, uint32_t dims, uint32_t dpad,
+                          std::vector<uint16_t>& bf16_out, std::vector<float>& cnorm, std::vector<double>& mean,
+                          double& cmax);
+void launch_ivf_probe_tc(const float* d_queries, const float* d_coarse, const uint16_t* d_coarse_bf16 /* bf16 bits */,
+                         const float* d_cnorm, const double* d_mean, double cmax, uint32_t dims, uint32_t dpad,
+                         uint32_t k_cells, uint32_t nq, uint32_t a, uint16_t* d_qb /* bf16 bits */, double* d_eps2,
+                         float* d_approx, uint32_t* d_redo, uint32_t* d_order, cudaStream_t stream);
 void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* d_queries, const float* d_coarse,
                        const uint32_t* d_order, uint32_t n_pairs, uint32_t a, float* d_luts, float* d_pmin,
                        float* d_own_min, cudaStream_t stream);

@@ -70,9 +70,15 @@ static constexpr int PROBE_QT = 16;
 
 __global__ void __launch_bounds__(256)
 ivf_coarse_dist_kernel(const float* __restrict__ queries, const float* __restrict__ coarse_t, uint32_t dims,
-                       uint32_t k_cells, uint32_t nq, float* __restrict__ dist /* [nq][K] */) {
+                       uint32_t k_cells, uint32_t nq, float* __restrict__ dist /* [nq][K] */,
+                       const uint32_t* __restrict__ only_flagged) {
     extern __shared__ __align__(16) float qs[]; // [dims][PROBE_QT]
     const uint32_t q0 = blockIdx.y * PROBE_QT;
+    if (only_flagged) { // redo pass of the tensor-core prefilter: skip tiles without a flagged query
+        bool any = false;
+        for (uint32_t i = 0; i < PROBE_QT && q0 + i < nq; ++i) any |= only_flagged[q0 + i] != 0;
+        if (!any) return;
+    }
     for (uint32_t u = threadIdx.x; u < dims * PROBE_QT; u += blockDim.x) {
         const uint32_t qi = u % PROBE_QT, j = u / PROBE_QT;
         qs[u] = q0 + qi < nq ? queries[size_t(q0 + qi) * dims + j] : 0.0f;
@@ -220,7 +226,9 @@ ivf_probe_select_fast_kernel(const float* __restrict__ dist, uint32_t k_cells, u
 
 void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t dims, uint32_t k_cells, uint32_t nq,
                       uint32_t a, float* d_dist_scratch, uint32_t* d_redo /* [nq] */, uint32_t* d_order,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, bool redo_only) {
+    // redo_only: d_redo already flags the queries the tensor-core prefilter (ivf_probe_tc.cu) could not
+    // decide; only those get exact distances and the radix selection
     if (nq == 0 || a == 0) return;
     uint32_t pow2 = 1;
     while (pow2 < a) pow2 <<= 1;
@@ -232,11 +240,12 @@ void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t 
     if (smem_d > 200 * 1024) throw Error(QADC_ERR_CONFIG, "ivf probe: dims too large");
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_coarse_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_d)));
     const dim3 grid((k_cells + 255) / 256, (nq + PROBE_QT - 1) / PROBE_QT);
-    ivf_coarse_dist_kernel<<<grid, 256, smem_d, stream>>>(d_queries, d_coarse_t, dims, k_cells, nq, d_dist_scratch);
+    ivf_coarse_dist_kernel<<<grid, 256, smem_d, stream>>>(d_queries, d_coarse_t, dims, k_cells, nq, d_dist_scratch,
+                                                          redo_only ? d_redo : nullptr);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_probe_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_sel)));
-    const bool fast = a <= 256 && a <= k_cells && k_cells >= 256;
+    const bool fast = !redo_only && a <= 256 && a <= k_cells && k_cells >= 256;
     if (fast) {
         QADC_CUDA_CHECK(cudaMemsetAsync(d_redo, 0, size_t(nq) * 4, stream));
         ivf_probe_select_fast_kernel<<<nq, 256, 0, stream>>>(d_dist_scratch, k_cells, a, d_order, d_redo);
@@ -244,7 +253,8 @@ void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t 
         QADC_CUDA_CHECK(cudaGetLastError());
     }
     // radix select: the only path for large a / tiny K, the fallback of flagged queries otherwise
-    ivf_probe_select_kernel<<<nq, 256, smem_sel, stream>>>(d_dist_scratch, k_cells, a, d_order, fast ? d_redo : nullptr);
+    ivf_probe_select_kernel<<<nq, 256, smem_sel, stream>>>(d_dist_scratch, k_cells, a, d_order,
+                                                           fast || redo_only ? d_redo : nullptr);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }

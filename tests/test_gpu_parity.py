@@ -607,3 +607,58 @@ def test_ivf_built_on_gpu_then_searched(port):
                      b["ids"]) as idx:
         got = idx.search(queries, qb.SearchParams(probes=8, r=50, t=200))
     assert np.array_equal(got.ids, want[0]) and bits_equal(got.dists, want[1]) and np.array_equal(got.counts, want[2])
+
+
+# ------------------------------------------------------------------ probe order at scale (tensor-core prefilter) --
+
+def _empty_ivf(s, cb, coarse):
+    k = coarse.shape[0]
+    z64 = np.zeros(k, np.uint64)
+    return qb.IvfIndex(s, cb, coarse, np.zeros(0, np.uint8), z64, z64, z64, np.zeros(0, np.uint32))
+
+
+@pytest.mark.parametrize("offset,spread", [(0.0, 3.0), (100.0, 1.0), (-7.0, 0.01)])
+def test_probe_order_prefilter_is_exact(port, offset, spread):
+    """K >= 512 takes the bf16 tensor-core prefilter + exact re-evaluation (ivf_probe_tc.cu): the order must equal
+    the reference's probe_order bit for bit -- for centred data, data with a large common offset, and tightly
+    packed centroids; with exact ties (duplicated centroids: the lower cell first), for several probe counts,
+    and identically with the prefilter switched off."""
+    rng = np.random.default_rng(int(abs(offset) * 10 + spread * 100))
+    dims, text, k = 40, "10x{4,4}", 2048 + 3
+    s = qb.allocate_dims(dims, text)
+    cb = rng.standard_normal(s.cb_floats).astype(np.float32)
+    coarse = (offset + rng.standard_normal((k, dims)) * spread).astype(np.float32)
+    coarse[1500] = coarse[11]
+    coarse[2050] = coarse[11]
+    coarse[900] = coarse[33]
+    queries = (offset + rng.standard_normal((37, dims)) * spread).astype(np.float32)
+    queries[0] = coarse[11]
+    queries[1] = coarse[33] + np.float32(1e-3)
+    with _empty_ivf(s, cb, coarse) as idx:
+        for a in (1, 3, 64, 256):
+            got = idx.probe_order(queries, a)
+            idx.set_option("probe_tc", 0)
+            exact = idx.probe_order(queries, a)
+            idx.set_option("probe_tc", 1)
+            assert np.array_equal(got, exact), a
+            for qi in range(len(queries)):
+                assert np.array_equal(got[qi], port.probe_order(dims, coarse, queries[qi], a)), (a, qi)
+        assert idx.probe_order(queries, 3)[0].tolist() == [11, 1500, 2050]
+
+
+def test_probe_order_prefilter_overflow_falls_back(port):
+    """3000 identical centroids: every one of them is a candidate, the candidate buffer overflows and the query
+    is redone by the exact kernels (ties resolve to the lowest cells)."""
+    rng = np.random.default_rng(8)
+    dims, text, k = 32, "8x{4,4}", 4096
+    s = qb.allocate_dims(dims, text)
+    cb = rng.standard_normal(s.cb_floats).astype(np.float32)
+    coarse = (rng.standard_normal((k, dims)) * 2).astype(np.float32)
+    coarse[500:3500] = coarse[500]
+    queries = (rng.standard_normal((9, dims)) * 2).astype(np.float32)
+    queries[0] = coarse[500]
+    with _empty_ivf(s, cb, coarse) as idx:
+        got = idx.probe_order(queries, 32)
+    assert got[0].tolist() == list(range(500, 532))
+    for qi in range(len(queries)):
+        assert np.array_equal(got[qi], port.probe_order(dims, coarse, queries[qi], 32)), qi
