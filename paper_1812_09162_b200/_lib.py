@@ -7,12 +7,13 @@ entry point fails with QADC_ERR_CUDA when no CUDA device is usable.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import subprocess
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SO_PATH = PKG / "libqadc_b200.so"
+SO_PATH = Path(os.environ.get("QADC_LIB_PATH", PKG / "libqadc_b200.so"))  # override: A/B runs of two builds
 HEADER = ROOT / "include" / "qadc.h"
 
 QADC_MAX_SUBS = 64

@@ -523,6 +523,7 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
             // warp step) that minimises padded work = sum over cells of tiles * tile_rows * list_length
             const ScanVariant cand[3] = {VAR_F16X4H, VAR_F16X4H_C2, VAR_F16X4H_C4};
             const uint32_t rows[3] = {128, 64, 32};
+            const double per_pair[3] = {1.0 / 1.13, 1.0 / 1.18, 1.0 / 0.93}; // measured flat-scan rates (T pairs/s)
             double best = -1.0;
             int pick = int(plan.variant) - int(VAR_F16X4H);
             for (int v = 0; v < 3; ++v) {
@@ -535,7 +536,8 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                 for (uint32_t c = 0; c < K; ++c)
                     if (npairs[c])
                         cost += double((npairs[c] + rows[v] - 1) / rows[v]) * rows[v] * (double(h->list_count_h[c]) + 2048.0);
-                if (best < 0.0 || cost < best * 0.97) { // prefer the taller tile unless the gain is real
+                cost *= per_pair[v];
+                if (best < 0.0 || cost < best) {
                     best = cost;
                     pick = v;
                 }
@@ -644,6 +646,20 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                     while (cta + 1 < g) begins[bfirst + size_t(++cta)] = uint32_t(n);
                     begins[bfirst + size_t(g)] = uint32_t(n);
                     rounds.push_back(Round{first, n, bfirst, g});
+                    if (std::getenv("QADC_TRACE")) {
+                        uint64_t padded = 0, real = 0, mx = 0;
+                        for (size_t j = first; j < jobs.size(); ++j) {
+                            padded += uint64_t(jobs[j].n_codes) * tq;
+                            real += uint64_t(jobs[j].n_codes) * jobs[j].n_rows;
+                        }
+                        for (int c = 0; c < g; ++c) {
+                            uint64_t cs = 0;
+                            for (uint32_t j = begins[bfirst + c]; j < begins[bfirst + c + 1]; ++j) cs += cost[j];
+                            mx = std::max(mx, cs);
+                        }
+                        fprintf(stderr, "[qadc trace] round lo=%llu: %zu jobs, %.3e padded pairs, %.3e real, max CTA cost / mean = %.3f\n",
+                                (unsigned long long)lo, n, double(padded), double(real), double(mx) * g / double(total));
+                    }
                 }
                 if (hi == ~0ull) break;
                 lo = hi;

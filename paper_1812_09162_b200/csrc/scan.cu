@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     __shared__ ScanArgs s_args;
     __shared__ __align__(8) uint64_t s_full[NSTAGE], s_empty[NSTAGE];
     __shared__ __align__(8) uint64_t s_tfull[2], s_tempty[2]; // LUT tile buffers: arrival / release
+    __shared__ float s_thr[2][P::TQ];                          // per tile buffer: accumulator start of every row
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
             mbar_init(&s_empty[i], SCAN_WARPS); // one arrival per consumer warp
         }
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&s_tfull[i], 1);
+            mbar_init(&s_tfull[i], 2); // the tile's expect_tx + the accumulator starts' arrive
             mbar_init(&s_tempty[i], SCAN_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -367,12 +368,17 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     const uint32_t j_end = a->cta_begin ? a->cta_begin[blockIdx.x + 1] : uint32_t(uint64_t(a->n_jobs) * (blockIdx.x + 1) / gridDim.x);
 
     // ============================ producer warp: stream codes with TMA bulk copies ==========
+    // Lane 0 issues the copies; at a tile switch all 32 lanes gather the rows' accumulator starts
+    // (row -> query -> threshold is a chain of dependent global loads: done here, one tile ahead, it
+    // is off the consumers' critical path).
     if (warp == SCAN_WARPS) {
-        if (lane != 0) return;
         uint32_t it = 0; // running stage-fill counter, mirrored by the consumers
         uint32_t tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0; // LUT tiles issued so far
+        ScanJob cur{};
+        if (j_begin < j_end) cur = a->jobs[j_begin];
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
-            const ScanJob job = a->jobs[ji];
+            const ScanJob job = cur;
+            if (ji + 1 < j_end) cur = a->jobs[ji + 1]; // in flight while this job is issued
             if (job.n_codes == 0 || job.n_rows == 0) continue;
             if (job.row_begin != prev_rb || job.n_rows != prev_nr) {
                 // next LUT tile: the image [entry][row] was prepared up front (tilepack.cu / ivf_lut.cu), so it
@@ -382,23 +388,56 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                 prev_nr = job.n_rows;
                 const uint32_t tb = tile_bufs == 2 ? (tseq & 1u) : 0u, use = tile_bufs == 2 ? (tseq >> 1) : tseq;
                 mbar_wait(&s_tempty[tb], (use & 1u) ^ 1u); // first use passes immediately
-                const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / P::TQ) * tile_bytes;
-                char* dst = smem + size_t(tb) * tile_bytes;
-                mbar_expect_tx(&s_tfull[tb], tile_bytes);
-                for (uint32_t off = 0; off < tile_bytes; off += 32768u)
-                    bulk_g2s(dst + off, src + off, min(32768u, tile_bytes - off), &s_tfull[tb]);
+                if (lane == 0) {
+                    const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / P::TQ) * tile_bytes;
+                    char* dst = smem + size_t(tb) * tile_bytes;
+                    mbar_expect_tx(&s_tfull[tb], tile_bytes);
+                    for (uint32_t off = 0; off < tile_bytes; off += 32768u)
+                        bulk_g2s(dst + off, src + off, min(32768u, tile_bytes - off), &s_tfull[tb]);
+                }
+                __syncwarp(); // the buffer (and its s_thr row) is free: gather while the tile is in flight
+                // accumulator start per row: bias - threshold - 1/2 (sign bit <=> admitted)
+                for (uint32_t r = lane; r < uint32_t(P::TQ); r += 32) {
+                    float t = P::BIG; // rows past the tile / padding rows never admit
+                    if (r < job.n_rows) {
+                        const uint32_t row = job.row_begin + r;
+                        const uint32_t q = a->row_query ? a->row_query[row] : row;
+                        if (q != 0xFFFFFFFFu) {
+                            const uint64_t tk = a->thr_key[q];
+                            uint32_t thr = uint32_t(tk >> 32);
+                            uint32_t bias = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;
+                            if (tk == KEY_INF || thr >= ds->qmax) t = -P::BIG; // heap not full / worst saturated: admit all
+                            else {
+                                if (!P::EXACT_FILTER && ds->word_width == 16) {
+                                    thr >>= 8;
+                                    bias >>= 8;
+                                }
+                                t = float(bias) - float(thr) - P::HALF;
+                            }
+                        }
+                    }
+                    s_thr[tb][r] = t;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_tfull[tb]); // release: the s_thr stores above are visible to waiters
                 ++tseq;
             }
+            // the whole warp walks the stages in lockstep, all lanes polling the barrier; lane 0 alone issues the
+            // copies.  Measured on the 8x{8,8} scan: a long-lived split (lane 0 in the stage loop, 31 lanes
+            // parked at the next __syncwarp) costs 5 % of the kernel, a lane-0 poll + shuffle broadcast as much.
             const uint8_t* gcodes = a->codes + job.code_off * stride;
             const uint32_t n_sub = (job.n_codes + stage_codes - 1) / stage_codes;
             for (uint32_t sub = 0; sub < n_sub; ++sub, ++it) {
                 const uint32_t b = it % NSTAGE;
                 mbar_wait(&s_empty[b], ((it / NSTAGE) & 1u) ^ 1u); // first lap passes immediately
-                const uint32_t first = sub * stage_codes;
-                const uint32_t cnt = min(stage_codes, job.n_codes - first);
-                const uint32_t bytes = (cnt * stride + 15u) & ~15u;
-                mbar_expect_tx(&s_full[b], bytes);
-                bulk_g2s(stage + size_t(b) * STAGE_BYTES, gcodes + size_t(first) * stride, bytes, &s_full[b]);
+                if (lane == 0) {
+                    const uint32_t first = sub * stage_codes;
+                    const uint32_t cnt = min(stage_codes, job.n_codes - first);
+                    const uint32_t bytes = (cnt * stride + 15u) & ~15u;
+                    mbar_expect_tx(&s_full[b], bytes);
+                    bulk_g2s(stage + size_t(b) * STAGE_BYTES, gcodes + size_t(first) * stride, bytes, &s_full[b]);
+                }
+                __syncwarp();
             }
         }
         return;
@@ -425,11 +464,14 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     uint32_t qn = 0; // warp-uniform fill level
     const uint32_t lanemask_lt = (1u << lane) - 1u;
 
+    ScanJob cur{};
+    if (j_begin < j_end) cur = a->jobs[j_begin];
     for (uint32_t ji = j_begin; ji < j_end; ++ji) {
-        const ScanJob job = a->jobs[ji];
+        const ScanJob job = cur;
+        if (ji + 1 < j_end) cur = a->jobs[ji + 1]; // the next descriptor loads while this job is scanned
         if (job.n_codes == 0 || job.n_rows == 0) continue;
 
-        // ---- (re)load the LUT tile when the row range changes ----
+        // ---- switch to the next LUT tile when the row range changes ----
         if (job.row_begin != cur_row_begin || job.n_rows != cur_n_rows) {
             if (tseq > 0) { // this warp is done with the previous tile's buffer
                 __syncwarp();
@@ -437,34 +479,14 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
             }
             cur_row_begin = job.row_begin;
             cur_n_rows = job.n_rows;
-            // per-lane accumulator start: bias - threshold - 1/2 (sign bit <=> admitted)
-            float t[P::QPL];
-#pragma unroll
-            for (int s = 0; s < P::QPL; ++s) {
-                const uint32_t r = lane_in * P::QPL + s;
-                t[s] = P::BIG; // rows past the tile never admit
-                if (r < job.n_rows) {
-                    const uint32_t row = job.row_begin + r;
-                    const uint32_t q = a->row_query ? a->row_query[row] : row;
-                    if (q == 0xFFFFFFFFu) continue; // padding row of a partially filled tile
-                    const uint64_t tk = a->thr_key[q];
-                    uint32_t thr = uint32_t(tk >> 32);
-                    uint32_t bias = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;
-                    if (tk == KEY_INF || thr >= ds->qmax) t[s] = -P::BIG; // heap not full / worst saturated: admit all
-                    else {
-                        if (!P::EXACT_FILTER && ds->word_width == 16) {
-                            thr >>= 8;
-                            bias >>= 8;
-                        }
-                        t[s] = float(bias) - float(thr) - P::HALF;
-                    }
-                }
-            }
-            P::init(acc0, t);
             const uint32_t tb = tile_bufs == 2 ? (tseq & 1u) : 0u, use = tile_bufs == 2 ? (tseq >> 1) : tseq;
             mbar_wait(&s_tfull[tb], use & 1u); // every thread observes the tile's arrival itself
             tile = smem + size_t(tb) * tile_bytes;
             ++tseq;
+            float t[P::QPL]; // per-lane accumulator starts, gathered by the producer warp
+#pragma unroll
+            for (int sl = 0; sl < P::QPL; ++sl) t[sl] = s_thr[tb][lane_in * P::QPL + sl];
+            P::init(acc0, t);
         }
 
         // ---- consume the job's codes stage by stage ----
@@ -598,7 +620,7 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
     int max_smem = 0;
     QADC_CUDA_CHECK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     // static shared (DevSpec + ScanArgs + barriers) comes out of the same budget
-    const uint32_t budget = uint32_t(max_smem) - uint32_t(sizeof(DevSpec) + sizeof(ScanArgs) + 256);
+    const uint32_t budget = uint32_t(max_smem) - uint32_t(sizeof(DevSpec) + sizeof(ScanArgs) + 2 * 256 * sizeof(float) + 256);
     if (ds.code_stride > 32) throw Error(QADC_ERR_CONFIG, "scan: codes wider than 256 bits are not supported");
     ScanPlan p{};
     p.threads = SCAN_THREADS;
@@ -643,6 +665,11 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
     }
     if (u8 && fits(smem_need<PolF16x8>(ds.E))) set(VAR_F16X8, PolF16x8::TQ, smem_need<PolF16x8>(ds.E));
     else if (u8 && fits(smem_need<PolF16x4_C4>(ds.E))) set(VAR_F16X4_C4, PolF16x4_C4::TQ, smem_need<PolF16x4_C4>(ds.E));
+    // 64-row tiles first: measured 4 % faster than 128-row tiles on the flat 12x{6,5,5} scan (two tile buffers
+    // fit, and two codes per warp step halve the per-code bookkeeping); 32-row tiles pay ~37 % extra
+    // shared-memory wavefronts for bank conflicts between the four code groups of a warp
+    else if (!u8 && fits(2 * smem_need<PolF16x4H_C2>(ds.E) - (NSTAGE * STAGE_BYTES + WQ_BYTES)))
+        set(VAR_F16X4H_C2, PolF16x4H_C2::TQ, smem_need<PolF16x4H_C2>(ds.E));
     else if (!u8 && fits(smem_need<PolF16x4H>(ds.E))) set(VAR_F16X4H, PolF16x4H::TQ, smem_need<PolF16x4H>(ds.E));
     else if (!u8 && fits(smem_need<PolF16x4H_C2>(ds.E))) set(VAR_F16X4H_C2, PolF16x4H_C2::TQ, smem_need<PolF16x4H_C2>(ds.E));
     else if (!u8 && fits(smem_need<PolF16x4H_C4>(ds.E))) set(VAR_F16X4H_C4, PolF16x4H_C4::TQ, smem_need<PolF16x4H_C4>(ds.E));
