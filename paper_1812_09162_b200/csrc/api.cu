@@ -521,9 +521,19 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         if (h->force_variant < 0 && plan.variant >= VAR_F16X4H && plan.variant <= VAR_F16X4H_C4) {
             // rows per cell are known now: pick the tile height (128 / 64 / 32 rows, i.e. 1 / 2 / 4 codes per
             // warp step) that minimises padded work = sum over cells of tiles * tile_rows * list_length
-            const ScanVariant cand[3] = {VAR_F16X4H, VAR_F16X4H_C2, VAR_F16X4H_C4};
+            // 32-row tiles: the duplicated-line layout when two tile buffers of it fit, else the dense one
+            ScanVariant c32 = VAR_F16X4H_C4;
+            double rate32 = 0.93;
+            try {
+                if (plan_scan(ds, h->device, int(VAR_F16X4H_C4D)).tile_bufs == 2) {
+                    c32 = VAR_F16X4H_C4D;
+                    rate32 = 1.15;
+                }
+            } catch (const Error&) {
+            }
+            const ScanVariant cand[3] = {VAR_F16X4H, VAR_F16X4H_C2, c32};
             const uint32_t rows[3] = {128, 64, 32};
-            const double per_pair[3] = {1.0 / 1.13, 1.0 / 1.18, 1.0 / 0.93}; // measured flat-scan rates (T pairs/s)
+            const double per_pair[3] = {1.0 / 1.13, 1.0 / 1.18, 1.0 / rate32}; // measured flat-scan rates (T pairs/s)
             double best = -1.0;
             int pick = int(plan.variant) - int(VAR_F16X4H);
             for (int v = 0; v < 3; ++v) {

@@ -67,6 +67,8 @@ enum ScanVariant : uint32_t {
     VAR_F16X4H_C2 = 5, // same, 2 codes per warp step, 64-row tile (short row groups: IVF)
     VAR_F16X4H_C4 = 6, // same, 4 codes per warp step, 32-row tile
     VAR_F16X4_C4 = 7,  // u8 tables exact in fp16, 4 codes per warp step, 32-row tile (large 8-bit tables: 8x{8})
+    VAR_F16X4H_C4D = 8, // as C4 with every entry line stored twice (128 B): code groups 0/2 read the low copy,
+                        // 1/3 the high copy, so the four groups of a warp never share a bank
     VAR_COUNT
 };
 

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256)
 ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uint32_t a,
                          const float* __restrict__ luts, const float* __restrict__ pmin,
                          const float* __restrict__ own_min, const float* __restrict__ qparams, uint32_t tq,
-                         bool high_byte, void* __restrict__ qluts, Entry* __restrict__ tile_lut,
+                         bool high_byte, uint32_t copies, void* __restrict__ qluts, Entry* __restrict__ tile_lut,
                          uint32_t* __restrict__ row_query, uint32_t* __restrict__ row_bias) {
     extern __shared__ __align__(16) unsigned short panel[];
     const uint32_t slab_cap = min(ds.E, QP_SLAB), pitch = tq + 2;
@@ -250,14 +250,17 @@ ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uin
             }
         }
         __syncthreads();
-        Entry* dst = tile_lut + (size_t(tile) * ds.E + e0) * tq;
+        // copies == 2: every entry line twice back to back (VAR_F16X4H_C4D)
+        Entry* dst = tile_lut + (size_t(tile) * ds.E + e0) * tq * copies;
         if ((tq & (tq - 1)) == 0) {
             const uint32_t lg = 31 - __clz(tq);
-            for (uint32_t u = threadIdx.x; u < ne * tq; u += blockDim.x)
-                dst[u] = tile_entry<Entry>(panel[(u >> lg) * pitch + (u & (tq - 1))], high_byte);
+            for (uint32_t u = threadIdx.x; u < ne * tq * copies; u += blockDim.x) {
+                const uint32_t line = u >> lg; // entry * copies + copy
+                dst[u] = tile_entry<Entry>(panel[(copies == 2 ? line >> 1 : line) * pitch + (u & (tq - 1))], high_byte);
+            }
         } else {
-            for (uint32_t u = threadIdx.x; u < ne * tq; u += blockDim.x)
-                dst[u] = tile_entry<Entry>(panel[(u / tq) * pitch + u % tq], high_byte);
+            for (uint32_t u = threadIdx.x; u < ne * tq * copies; u += blockDim.x)
+                dst[u] = tile_entry<Entry>(panel[(u / tq / copies) * pitch + u % tq], high_byte);
         }
         __syncthreads();
     }
@@ -266,12 +269,13 @@ ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uin
 template <class Entry>
 static void launch_qp(const DevSpec& ds, const uint32_t* slot_pair, uint32_t a, const float* luts, const float* pmin,
                       const float* own_min, const float* qparams, uint32_t tq, bool hb, void* qluts, void* tile_lut,
-                      uint32_t* row_query, uint32_t* row_bias, uint32_t ntiles, cudaStream_t stream) {
+                      uint32_t* row_query, uint32_t* row_bias, uint32_t ntiles, cudaStream_t stream,
+                      uint32_t copies = 1) {
     const size_t smem = size_t(std::min(ds.E, QP_SLAB)) * (tq + 2) * sizeof(unsigned short) + ds.E;
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_quantize_pack_kernel<Entry>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ivf_quantize_pack_kernel<Entry><<<ntiles, 256, smem, stream>>>(ds, slot_pair, a, luts, pmin, own_min, qparams, tq, hb,
-                                                                   qluts, static_cast<Entry*>(tile_lut), row_query,
-                                                                   row_bias);
+                                                                   copies, qluts, static_cast<Entry*>(tile_lut),
+                                                                   row_query, row_bias);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
@@ -300,6 +304,9 @@ void launch_ivf_quantize_pack(ScanVariant v, const DevSpec& ds, const uint32_t* 
     case VAR_F16X4H_C4:
         return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, wide, d_qluts, d_tile_lut,
                                  d_row_query, d_row_bias, ntiles, stream);
+    case VAR_F16X4H_C4D:
+        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, wide, d_qluts, d_tile_lut,
+                                 d_row_query, d_row_bias, ntiles, stream, 2);
     case VAR_F32X2:
         return launch_qp<float>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, false, d_qluts, d_tile_lut,
                                 d_row_query, d_row_bias, ntiles, stream);

@@ -191,10 +191,16 @@ struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
 // against a tile of 128/CPW rows.  Bytes per wavefront and instructions per pair are unchanged, but
 // short row groups (IVF: ~40 (query, cell) pairs per cell) waste far fewer padded rows.
 // HIGH = false is the exact twin for 8-bit tables (entries <= 255 are exact in fp16, as in f16x8).
-template <int CPW_, bool HIGH = true>
+// DUP: every entry line is stored twice back to back (ROWB doubles); odd code groups read the second copy.
+// With four groups of 8 lanes x 8 B, groups 0/2 then only touch banks 0-15 and groups 1/3 banks 16-31: a warp
+// load is exactly two conflict-free wavefronts, where the dense layout needs 2.75 on average (the bank half
+// is the parity of a data-dependent entry index).
+template <int CPW_, bool HIGH = true, bool DUP_ = false>
 struct PolF16x4H_T {
     static constexpr int CPW = CPW_;
-    static constexpr int QPL = 4, TQ = 128 / CPW, ROWB = 256 / CPW, LOG_ROWB = (CPW == 1 ? 8 : CPW == 2 ? 7 : 6), LANE_B = 8;
+    static constexpr bool DUP = DUP_;
+    static constexpr int QPL = 4, TQ = 128 / CPW, ROWB = (256 / CPW) * (DUP ? 2 : 1),
+                         LOG_ROWB = (CPW == 1 ? 8 : CPW == 2 ? 7 : 6) + (DUP ? 1 : 0), LANE_B = 8;
     static constexpr bool EXACT_FILTER = !HIGH;
     using Entry = __half;
     struct Acc {
@@ -227,6 +233,12 @@ using PolF16x4H = PolF16x4H_T<1>;
 using PolF16x4H_C2 = PolF16x4H_T<2>;
 using PolF16x4H_C4 = PolF16x4H_T<4>;
 using PolF16x4_C4 = PolF16x4H_T<4, false>;
+using PolF16x4H_C4D = PolF16x4H_T<4, true, true>;
+
+template <class P, class = void>
+struct dup_of : std::false_type {};
+template <class P>
+struct dup_of<P, std::void_t<decltype(P::DUP)>> : std::bool_constant<P::DUP> {};
 
 struct PolU16x1 { // any width, u16 entries, int32 accumulate
     static constexpr int CPW = 1;
@@ -456,7 +468,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     }
     constexpr uint32_t LPC = 32 / P::CPW;             // lanes per code
     const uint32_t lane_in = lane % LPC, lane_code = lane / LPC;
-    const uint32_t lane_off = lane_in * P::LANE_B;
+    const uint32_t lane_off = lane_in * P::LANE_B + (dup_of<P>::value ? (lane_code & 1u) * (P::ROWB / 2) : 0u);
     // per-warp queue of flagged pairs: ballot-compacted in the hot loop, resolved 32 at a time
     uint32_t* wq_row = reinterpret_cast<uint32_t*>(stage + NSTAGE * STAGE_BYTES) + warp * (WQ_CAP * 3);
     uint32_t* wq_idx = wq_row + WQ_CAP;
@@ -607,6 +619,7 @@ const char* variant_name(uint32_t v) {
     case VAR_F16X4H_C2: return "f16x4h-c2 (as f16x4h, 2 codes per warp step, 64-row tile)";
     case VAR_F16X4H_C4: return "f16x4h-c4 (as f16x4h, 4 codes per warp step, 32-row tile)";
     case VAR_F16X4_C4: return "f16x4-c4 (u8 tables exact in fp16, 4 codes per warp step, 32-row tile)";
+    case VAR_F16X4H_C4D: return "f16x4h-c4d (as f16x4h-c4, entry lines duplicated: bank-conflict-free)";
     }
     return "?";
 }
@@ -647,8 +660,10 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
         case VAR_F16X4H:
         case VAR_F16X4H_C2:
         case VAR_F16X4H_C4:
+        case VAR_F16X4H_C4D:
             if (u8) throw Error(QADC_ERR_CONFIG, "scan: f16x4h is the 16-bit-table filter");
-            if (force_variant == VAR_F16X4H) set(VAR_F16X4H, PolF16x4H::TQ, smem_need<PolF16x4H>(ds.E));
+            if (force_variant == VAR_F16X4H_C4D) set(VAR_F16X4H_C4D, PolF16x4H_C4D::TQ, smem_need<PolF16x4H_C4D>(ds.E));
+            else if (force_variant == VAR_F16X4H) set(VAR_F16X4H, PolF16x4H::TQ, smem_need<PolF16x4H>(ds.E));
             else if (force_variant == VAR_F16X4H_C2) set(VAR_F16X4H_C2, PolF16x4H_C2::TQ, smem_need<PolF16x4H_C2>(ds.E));
             else set(VAR_F16X4H_C4, PolF16x4H_C4::TQ, smem_need<PolF16x4H_C4>(ds.E));
             break;
@@ -740,6 +755,9 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         if (G655::matches(ds)) return launch_one<PolF16x4H_C4, G655>(plan, ds, args, grid, stream);
         if (G88::matches(ds)) return launch_one<PolF16x4H_C4, G88>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_F16X4H_C4D:
+        if (G655::matches(ds)) return launch_one<PolF16x4H_C4D, G655>(plan, ds, args, grid, stream);
+        return launch_one<PolF16x4H_C4D, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4_C4:
         if (G8::matches(ds)) return launch_one<PolF16x4_C4, G8>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4_C4, GeomRT>(plan, ds, args, grid, stream);

@@ -34,7 +34,7 @@ static constexpr int PACK_E = 64;
 // grid = (ntiles, ceil(E / PACK_E)); block = 256.  rows [tile*TQ, tile*TQ + TQ) clipped to n_rows.
 template <class Entry>
 __global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width, uint32_t E, uint32_t n_rows,
-                                  uint32_t tq, bool high_byte, Entry* __restrict__ out) {
+                                  uint32_t tq, bool high_byte, uint32_t copies, Entry* __restrict__ out) {
     extern __shared__ unsigned short panel[]; // [PACK_E][tq + 1]
     const uint32_t tile = blockIdx.x, e0 = blockIdx.y * PACK_E;
     const uint32_t ne = min(uint32_t(PACK_E), E - e0);
@@ -51,21 +51,23 @@ __global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width,
         panel[el * pitch + r] = (unsigned short)v;
     }
     __syncthreads();
-    Entry* dst = out + (size_t(tile) * E + e0) * tq;
+    // copies == 2: every entry line twice back to back (VAR_F16X4H_C4D)
+    Entry* dst = out + (size_t(tile) * E + e0) * tq * copies;
     for (uint32_t u = threadIdx.x; u < ne * tq; u += blockDim.x) {
         const uint32_t r = u % tq, el = u / tq;
-        dst[size_t(el) * tq + r] = tile_convert<Entry>(panel[el * pitch + r], width, high_byte);
+        const Entry v = tile_convert<Entry>(panel[el * pitch + r], width, high_byte);
+        for (uint32_t c = 0; c < copies; ++c) dst[(size_t(el) * copies + c) * tq + r] = v;
     }
 }
 
 template <class Entry>
 static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq, bool hb,
-                        void* out, cudaStream_t stream) {
+                        void* out, cudaStream_t stream, uint32_t copies = 1) {
     const uint32_t ntiles = (n_rows + tq - 1) / tq;
     if (ntiles == 0) return;
     const dim3 grid(ntiles, (E + PACK_E - 1) / PACK_E);
     const size_t smem = size_t(PACK_E) * (tq + 1) * sizeof(unsigned short);
-    pack_tiles_kernel<Entry><<<grid, 256, smem, stream>>>(qlut, width, E, n_rows, tq, hb, static_cast<Entry*>(out));
+    pack_tiles_kernel<Entry><<<grid, 256, smem, stream>>>(qlut, width, E, n_rows, tq, hb, copies, static_cast<Entry*>(out));
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
@@ -77,6 +79,7 @@ size_t tile_entry_bytes(ScanVariant v) {
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4:
     case VAR_F16X4_C4: return 2;
+    case VAR_F16X4H_C4D: return 4; // two copies of a 2-byte entry
     case VAR_F32X2: return 4;
     case VAR_U16X1: return 2;
     case VAR_U8X1: return 1;
@@ -92,6 +95,7 @@ void launch_pack_tiles(ScanVariant v, const void* qlut, uint32_t width, uint32_t
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, true, out, stream);
+    case VAR_F16X4H_C4D: return launch_pack<__half>(qlut, width, E, n_rows, tq, true, out, stream, 2);
     case VAR_F32X2: return launch_pack<float>(qlut, width, E, n_rows, tq, false, out, stream);
     case VAR_U16X1: return launch_pack<unsigned short>(qlut, width, E, n_rows, tq, false, out, stream);
     case VAR_U8X1: return launch_pack<unsigned char>(qlut, width, E, n_rows, tq, false, out, stream);
