@@ -662,3 +662,44 @@ def test_probe_order_prefilter_overflow_falls_back(port):
     assert got[0].tolist() == list(range(500, 532))
     for qi in range(len(queries)):
         assert np.array_equal(got[qi], port.probe_order(dims, coarse, queries[qi], 32)), qi
+
+
+@pytest.mark.parametrize("dims,text,k_cells,n,probes,nq", [(96, "12x{6,5,5}", 1024, 400000, 24, 96),
+                                                           (128, "16x{4,4}", 600, 200000, 12, 70),
+                                                           (64, "8x{8,8}", 512, 120000, 9, 50)])
+def test_ivf_search_many_cells_vs_oracle(port, dims, text, k_cells, n, probes, nq):
+    """The batch-scale IVF stages -- tensor-core probe prefilter (K >= 512), register-tiled residual tables, fused
+    quantize + tile pack, 32/64-row tiles with two tile buffers -- against the oracle end to end, on clustered
+    queries (many queries share cells, so tiles are full) with a skewed list-length distribution."""
+    rng = np.random.default_rng(k_cells + probes)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 0.8).astype(np.float32)
+    coarse = (rng.standard_normal((k_cells, dims)) * 2 + 5.0).astype(np.float32)
+    # skewed list sizes: a few long lists, many short ones, two empty cells
+    w = rng.pareto(1.5, size=k_cells) + 0.05
+    w[[3, k_cells - 1]] = 0
+    assign = rng.choice(k_cells, size=n, p=w / w.sum())
+    codes = random_codes(s, n, seed=5)
+    order = np.argsort(assign, kind="stable")
+    counts = np.bincount(assign, minlength=k_cells).astype(np.uint64)
+    ioff = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
+    parts, boff, b = [], [], 0
+    for c in range(k_cells):
+        boff.append(b)
+        if counts[c]:
+            parts.append(qb.pack_list(s, codes[order[int(ioff[c]):int(ioff[c] + counts[c])]]))
+            b += parts[-1].size
+    packed, boff, ids = np.concatenate(parts), np.array(boff, np.uint64), order.astype(np.uint32)
+    hot = rng.integers(0, k_cells, size=6)
+    queries = (coarse[hot[rng.integers(0, 6, size=nq)]] + rng.standard_normal((nq, dims)) * 0.7).astype(np.float32)
+    with qb.IvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids) as idx:
+        for pr, r, t in [(probes, 100, 400), (3, 20, 60)]:
+            want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=pr, r=r, t=t, threads=8)
+            got = idx.search(queries, qb.SearchParams(probes=pr, r=r, t=t))
+            assert np.array_equal(got.counts, want[2]), (pr, r, t)
+            assert np.array_equal(got.ids, want[0]), (pr, r, t)
+            assert bits_equal(got.dists, want[1]), (pr, r, t)
+            rr = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=pr, r=r, t=t,
+                                 threads=8, family=0x100)
+            got_rr = idx.search(queries, qb.SearchParams(probes=pr, r=r, t=t, rerank=True))
+            assert np.array_equal(got_rr.ids, rr[0]) and bits_equal(got_rr.dists, rr[1]), ("rerank", pr)
