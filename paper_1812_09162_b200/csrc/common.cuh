@@ -174,10 +174,6 @@ void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_calib_codes, const uin
                       uint32_t a,
                       const float* d_luts, const float* d_own_min, uint32_t r, uint32_t t, float* d_qparams,
                       float* d_map, uint32_t* d_cell_npairs, uint32_t* d_pair_rank, cudaStream_t stream);
-void launch_ivf_quantize(const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a, const float* d_luts,
-                         const float* d_pmin, const float* d_own_min, const float* d_qparams,
-                         const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base, uint32_t tq, void* d_qluts,
-                         uint32_t* d_row_query, uint32_t* d_row_bias, uint32_t* d_pair_slot, cudaStream_t stream);
 void launch_ivf_seed(const DevSpec& ds, const uint8_t* d_codes, const uint32_t* d_ids, const uint64_t* d_list_code_off,
                      const uint64_t* d_list_count, const uint32_t* d_order, uint32_t nq, uint32_t a,
                      const uint32_t* d_pair_slot, const void* d_qluts, const uint32_t* d_row_bias, uint32_t r,

@@ -427,71 +427,6 @@ void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_codes, const uint64_t*
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
-// ------------------------------------------------------------------ quantization --
-
-__device__ __forceinline__ uint32_t ivf_quantize_entry(float p, float pmin, float d_min, float d_max, float delta,
-                                                       uint32_t qmax) { // distance.hpp:117-124
-    if (delta <= 0.0f) return p == pmin ? 0u : qmax;
-    if (__fsub_rn(p, pmin) >= __fsub_rn(d_max, d_min)) return qmax;
-    const double q = floor(__ddiv_rn(__dsub_rn(double(p), double(pmin)), double(delta)));
-    if (q >= double(qmax)) return qmax;
-    return uint32_t(q);
-}
-
-// One CTA per (query, probe) pair with a non-empty list: quantize its tables against the query's
-// shared bounds into LUT row `slot`, and derive the row's bias (index.hpp:322-328).
-__global__ void __launch_bounds__(256)
-ivf_quantize_kernel(DevSpec ds, const uint32_t* __restrict__ order, uint32_t a, const float* __restrict__ luts,
-                    const float* __restrict__ pmin, const float* __restrict__ own_min,
-                    const float* __restrict__ qparams, const uint32_t* __restrict__ pair_rank,
-                    const uint32_t* __restrict__ cell_tile_base, uint32_t tq, void* __restrict__ qluts,
-                    uint32_t* __restrict__ row_query, uint32_t* __restrict__ row_bias,
-                    uint32_t* __restrict__ pair_slot, uint32_t n_pairs) {
-  for (uint32_t kk = 0; kk < IVF_PAIRS_PER_CTA; ++kk) {
-    const uint32_t pair = blockIdx.x * IVF_PAIRS_PER_CTA + kk;
-    if (pair >= n_pairs) return;
-    const uint32_t rank = pair_rank[pair];
-    if (rank == 0xFFFFFFFFu) { // empty list: skipped by the search loop (index.hpp:321)
-        if (threadIdx.x == 0) pair_slot[pair] = 0xFFFFFFFFu;
-        continue;
-    }
-    const uint32_t qi = pair / a;
-    const uint32_t slot = cell_tile_base[order[pair]] * tq + rank;
-    const float d_min = qparams[size_t(qi) * 4 + 0], d_max = qparams[size_t(qi) * 4 + 1];
-    const float delta = qparams[size_t(qi) * 4 + 2];
-    const float* lut = luts + size_t(pair) * ds.E;
-    for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x) {
-        uint32_t j = 0;
-        while (j + 1 < ds.m && ds.ent_off[j + 1] <= e) ++j;
-        const uint32_t qv = ivf_quantize_entry(lut[e], pmin[size_t(pair) * ds.m + j], d_min, d_max, delta, ds.qmax);
-        if (ds.word_width == 8) reinterpret_cast<uint8_t*>(qluts)[size_t(slot) * ds.E + e] = uint8_t(qv);
-        else reinterpret_cast<uint16_t*>(qluts)[size_t(slot) * ds.E + e] = uint16_t(qv);
-    }
-    if (threadIdx.x == 0) {
-        uint32_t bias = 0;
-        if (delta > 0.0f) { // float math, index.hpp:325-327
-            const float b = floorf(__fdiv_rn(__fsub_rn(own_min[pair], d_min), delta));
-            bias = b >= float(ds.qmax) ? ds.qmax : uint32_t(b);
-        }
-        row_query[slot] = qi;
-        row_bias[slot] = bias;
-        pair_slot[pair] = slot;
-    }
-  }
-}
-
-void launch_ivf_quantize(const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a, const float* d_luts,
-                         const float* d_pmin, const float* d_own_min, const float* d_qparams,
-                         const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base, uint32_t tq, void* d_qluts,
-                         uint32_t* d_row_query, uint32_t* d_row_bias, uint32_t* d_pair_slot, cudaStream_t stream) {
-    if (n_pairs == 0) return;
-    ivf_quantize_kernel<<<(n_pairs + IVF_PAIRS_PER_CTA - 1) / IVF_PAIRS_PER_CTA, 256, 0, stream>>>(
-        ds, d_order, a, d_luts, d_pmin, d_own_min, d_qparams, d_pair_rank, d_cell_tile_base, tq, d_qluts, d_row_query,
-        d_row_bias, d_pair_slot, n_pairs);
-    ++g_launches;
-    QADC_CUDA_CHECK(cudaGetLastError());
-}
-
 // ------------------------------------------------------------- threshold seeding --
 
 // One CTA per query: exact quantized sums of the head of the first probed list that holds at

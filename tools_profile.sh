@@ -5,7 +5,7 @@ TAG=${1:-r01}
 set -x
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"
 $CMD > gpurun_out/${TAG}_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"qadc|scan_kernel|pack_tiles" -c 400 --csv --log-file gpurun_out/${TAG}_launches_c2.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"qadc|scan_kernel|pack_tiles|flat_tables|seed_topk|tighten|finalize|init_select" -c 400 --csv --log-file gpurun_out/${TAG}_launches_c2.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
 $CMD > gpurun_out/${TAG}_plain2.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 15 -c 1 -o gpurun_out/${TAG}_scan_c2 $CMD > gpurun_out/${TAG}_ncu_full.log 2>&1
 for W in c1 c3; do
@@ -16,7 +16,7 @@ ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s $
 done
 CMD5="python bench.py --workload c5 --steps 1 --warmup 3 --no-cpu-baseline"
 $CMD5 > gpurun_out/${TAG}_plain_c5.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ivf_|scan_kernel|tighten|pack_tiles|finalize|init_select" -s 1 -c 17 --csv --log-file gpurun_out/${TAG}_launches_c5.csv $CMD5 > gpurun_out/${TAG}_ncu_c5.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ivf_|probe_|scan_kernel|tighten|pack_tiles|finalize|init_select|seed" -s 1 -c 34 --csv --log-file gpurun_out/${TAG}_launches_c5.csv $CMD5 > gpurun_out/${TAG}_ncu_c5.log 2>&1
 $CMD5 > gpurun_out/${TAG}_plain_c5b.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 10 -c 1 -o gpurun_out/${TAG}_scan_c5 $CMD5 > gpurun_out/${TAG}_ncu_full_c5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 6 -c 1 -o gpurun_out/${TAG}_scan_c5 $CMD5 > gpurun_out/${TAG}_ncu_full_c5.log 2>&1
 ls -la gpurun_out | grep ${TAG}_ | tail -20
