@@ -88,6 +88,7 @@ struct ScanArgs {
     uint32_t cap;
     uint32_t* overflow;        // [nq] set to 1 when a candidate did not fit
     uint32_t tile_bufs;        // 1 or 2 LUT tile buffers in shared memory (filled in by launch_scan from the plan)
+    uint32_t filter_shift;     // conservative filters on 16-bit tables compare floor(x >> shift) (from the plan)
 };
 
 struct ScanPlan {
@@ -96,6 +97,11 @@ struct ScanPlan {
     uint32_t smem_bytes;
     uint32_t threads;
     uint32_t tile_bufs;  // 2 when a second LUT tile buffer fits: the next job's tile is prefetched
+    // Conservative fp16 filter on 16-bit tables: entries, bias and threshold are compared as floor(x >> shift).
+    // fp16 holds integers exactly up to 2048, so shift = 5 (11-bit entries) keeps every partial sum that can still
+    // be admitted exact; the shift grows with m so that m * (65535 >> shift) stays below the "admit all" sentinel.
+    // 8 for the u8-entry variant, 0 for exact variants and 8-bit tables.
+    uint32_t filter_shift;
 };
 
 // chooses the variant for a spec (throws config error if nothing fits shared memory)
@@ -132,7 +138,7 @@ void launch_finalize(const uint64_t* lists, const uint32_t* counts_in, uint32_t 
 
 // ---- tile-layout tables (tilepack.cu) ----
 size_t tile_entry_bytes(ScanVariant v);
-void launch_pack_tiles(ScanVariant v, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
+void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
                        void* out, cudaStream_t stream);
 
 // ---- dense head evaluation (seed.cu) ----
@@ -163,7 +169,7 @@ bool ivf_tables_tiled_supported(const DevSpec& ds);
 void launch_ivf_tables_tiled(const DevSpec& ds, const float* d_codebook_t, const float* d_queries,
                              const float* d_coarse, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
                              float* d_luts, float* d_pmin, float* d_own_min, cudaStream_t stream);
-void launch_ivf_quantize_pack(ScanVariant v, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
+void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
                               const float* d_luts, const float* d_pmin, const float* d_own_min,
                               const float* d_qparams, const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base,
                               uint32_t tq, uint32_t ntiles, void* d_qluts, void* d_tile_lut, uint32_t* d_row_query,

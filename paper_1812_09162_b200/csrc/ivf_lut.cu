@@ -168,18 +168,18 @@ __device__ __forceinline__ uint32_t quantize_entry_fast(float p, float pmin, flo
 }
 
 template <class Entry>
-__device__ __forceinline__ Entry tile_entry(uint32_t v, bool high_byte);
+__device__ __forceinline__ Entry tile_entry(uint32_t v, uint32_t shift);
 template <>
-__device__ __forceinline__ __half tile_entry<__half>(uint32_t v, bool hb) {
-    return __uint2half_rn(hb ? v >> 8 : v); // exact: <= 255 whenever a half entry is used
+__device__ __forceinline__ __half tile_entry<__half>(uint32_t v, uint32_t shift) {
+    return __uint2half_rn(v >> shift); // exact: <= 2047 whenever a half entry is used (ScanPlan::filter_shift)
 }
 template <>
-__device__ __forceinline__ float tile_entry<float>(uint32_t v, bool) { return float(v); }
+__device__ __forceinline__ float tile_entry<float>(uint32_t v, uint32_t) { return float(v); }
 template <>
-__device__ __forceinline__ unsigned short tile_entry<unsigned short>(uint32_t v, bool) { return (unsigned short)v; }
+__device__ __forceinline__ unsigned short tile_entry<unsigned short>(uint32_t v, uint32_t) { return (unsigned short)v; }
 template <>
-__device__ __forceinline__ unsigned char tile_entry<unsigned char>(uint32_t v, bool hb) {
-    return (unsigned char)(hb ? v >> 8 : v);
+__device__ __forceinline__ unsigned char tile_entry<unsigned char>(uint32_t v, uint32_t shift) {
+    return (unsigned char)(v >> shift);
 }
 
 static constexpr uint32_t QP_SLAB = 512; // entries per shared-memory panel
@@ -190,7 +190,8 @@ __global__ void __launch_bounds__(256)
 ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uint32_t a,
                          const float* __restrict__ luts, const float* __restrict__ pmin,
                          const float* __restrict__ own_min, const float* __restrict__ qparams, uint32_t tq,
-                         bool high_byte, uint32_t copies, void* __restrict__ qluts, Entry* __restrict__ tile_lut,
+                         uint32_t high_byte /* filter shift */, uint32_t copies, void* __restrict__ qluts,
+                         Entry* __restrict__ tile_lut,
                          uint32_t* __restrict__ row_query, uint32_t* __restrict__ row_bias) {
     extern __shared__ __align__(16) unsigned short panel[];
     const uint32_t slab_cap = min(ds.E, QP_SLAB), pitch = tq + 2;
@@ -268,7 +269,7 @@ ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uin
 
 template <class Entry>
 static void launch_qp(const DevSpec& ds, const uint32_t* slot_pair, uint32_t a, const float* luts, const float* pmin,
-                      const float* own_min, const float* qparams, uint32_t tq, bool hb, void* qluts, void* tile_lut,
+                      const float* own_min, const float* qparams, uint32_t tq, uint32_t hb, void* qluts, void* tile_lut,
                       uint32_t* row_query, uint32_t* row_bias, uint32_t ntiles, cudaStream_t stream,
                       uint32_t copies = 1) {
     const size_t smem = size_t(std::min(ds.E, QP_SLAB)) * (tq + 2) * sizeof(unsigned short) + ds.E;
@@ -280,7 +281,7 @@ static void launch_qp(const DevSpec& ds, const uint32_t* slot_pair, uint32_t a, 
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_ivf_quantize_pack(ScanVariant v, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
+void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
                               const float* d_luts, const float* d_pmin, const float* d_own_min,
                               const float* d_qparams, const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base,
                               uint32_t tq, uint32_t ntiles, void* d_qluts, void* d_tile_lut, uint32_t* d_row_query,
@@ -293,29 +294,30 @@ void launch_ivf_quantize_pack(ScanVariant v, const DevSpec& ds, const uint32_t* 
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
     if (ntiles == 0) return;
-    const bool wide = ds.word_width == 16;
+    const uint32_t fs = ds.word_width == 16 ? filter_shift : 0u;
     switch (v) {
     case VAR_F16X8:
     case VAR_F16X4_C4:
-        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, false, d_qluts, d_tile_lut,
+        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, 0, d_qluts, d_tile_lut,
                                  d_row_query, d_row_bias, ntiles, stream);
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4:
-        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, wide, d_qluts, d_tile_lut,
+        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, fs, d_qluts, d_tile_lut,
                                  d_row_query, d_row_bias, ntiles, stream);
     case VAR_F16X4H_C4D:
-        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, wide, d_qluts, d_tile_lut,
+        return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, fs, d_qluts, d_tile_lut,
                                  d_row_query, d_row_bias, ntiles, stream, 2);
     case VAR_F32X2:
-        return launch_qp<float>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, false, d_qluts, d_tile_lut,
+        return launch_qp<float>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, 0, d_qluts, d_tile_lut,
                                 d_row_query, d_row_bias, ntiles, stream);
     case VAR_U16X1:
-        return launch_qp<unsigned short>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, false, d_qluts,
+        return launch_qp<unsigned short>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, 0, d_qluts,
                                          d_tile_lut, d_row_query, d_row_bias, ntiles, stream);
     case VAR_U8X1:
-        return launch_qp<unsigned char>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, wide, d_qluts,
-                                        d_tile_lut, d_row_query, d_row_bias, ntiles, stream);
+        return launch_qp<unsigned char>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq,
+                                        ds.word_width == 16 ? 8u : 0u, d_qluts, d_tile_lut, d_row_query, d_row_bias,
+                                        ntiles, stream);
     default: throw Error(QADC_ERR_CONFIG, "quantize_pack: bad variant");
     }
 }

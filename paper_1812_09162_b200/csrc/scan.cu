@@ -227,7 +227,9 @@ struct PolF16x4H_T {
     __device__ static float value(const Acc& a, int s) {
         return (s & 1) ? __high2float(a.h[s >> 1]) : __low2float(a.h[s >> 1]);
     }
-    static constexpr float BIG = 30000.0f, HALF = 0.5f;
+    // HIGH: all terms are integers up to 2047, the start is bias' - thr' - 1 (sum' <= thr' <=> negative), every
+    // value in [-2048, 2047] is exact in fp16 and anything larger stays positive.  Exact twin: the usual - 1/2.
+    static constexpr float BIG = 30000.0f, HALF = HIGH ? 1.0f : 0.5f;
 };
 using PolF16x4H = PolF16x4H_T<1>;
 using PolF16x4H_C2 = PolF16x4H_T<2>;
@@ -421,8 +423,8 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                             if (tk == KEY_INF || thr >= ds->qmax) t = -P::BIG; // heap not full / worst saturated: admit all
                             else {
                                 if (!P::EXACT_FILTER && ds->word_width == 16) {
-                                    thr >>= 8;
-                                    bias >>= 8;
+                                    thr >>= a->filter_shift;
+                                    bias >>= a->filter_shift;
                                 }
                                 t = float(bias) - float(thr) - P::HALF;
                             }
@@ -637,6 +639,14 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
     if (ds.code_stride > 32) throw Error(QADC_ERR_CONFIG, "scan: codes wider than 256 bits are not supported");
     ScanPlan p{};
     p.threads = SCAN_THREADS;
+    auto filter_shift_for = [&](ScanVariant v) -> uint32_t {
+        if (ds.word_width != 16) return 0;
+        if (v == VAR_U8X1) return 8;
+        if (v != VAR_F16X4H && v != VAR_F16X4H_C2 && v != VAR_F16X4H_C4 && v != VAR_F16X4H_C4D) return 0;
+        uint32_t sh = 5;
+        while (sh < 8 && ds.m * (65535u >> sh) > 28000u) ++sh;
+        return sh;
+    };
     auto fits = [&](uint32_t need) { return need <= budget; };
     auto set = [&](ScanVariant v, uint32_t tq, uint32_t need) {
         p.variant = v;
@@ -671,6 +681,7 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
         }
         if (!fits(p.smem_bytes)) throw Error(QADC_ERR_CONFIG, "scan: forced variant does not fit shared memory");
         p.tile_bufs = 1;
+        p.filter_shift = filter_shift_for(p.variant);
         const uint32_t tile_bytes = p.smem_bytes - (NSTAGE * STAGE_BYTES + WQ_BYTES);
         if (fits(p.smem_bytes + tile_bytes)) {
             p.tile_bufs = 2;
@@ -696,6 +707,7 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant) {
                                          " entries) do not fit shared memory; no CPU fallback exists");
     // a second tile buffer (the next job's tile lands while this one is scanned) whenever it fits
     p.tile_bufs = 1;
+    p.filter_shift = filter_shift_for(p.variant);
     const uint32_t tile_bytes = p.smem_bytes - (NSTAGE * STAGE_BYTES + WQ_BYTES);
     if (fits(p.smem_bytes + tile_bytes)) {
         p.tile_bufs = 2;
@@ -728,6 +740,7 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
     if (args_in.n_jobs == 0 || grid <= 0) return;
     ScanArgs args = args_in;
     args.tile_bufs = plan.tile_bufs;
+    args.filter_shift = plan.filter_shift;
     switch (plan.variant) {
     case VAR_F16X8:
         if (G44::matches(ds)) return launch_one<PolF16x8, G44>(plan, ds, args, grid, stream);

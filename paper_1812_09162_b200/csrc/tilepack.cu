@@ -13,19 +13,19 @@
 namespace qadc {
 
 template <class Entry>
-__device__ __forceinline__ Entry tile_convert(uint32_t v, uint32_t width, bool high_byte);
+__device__ __forceinline__ Entry tile_convert(uint32_t v, uint32_t width, uint32_t shift);
 template <>
-__device__ __forceinline__ __half tile_convert<__half>(uint32_t v, uint32_t width, bool hb) {
-    return __uint2half_rn(hb && width == 16 ? v >> 8 : v); // exact: value <= 255 whenever a half entry is used
+__device__ __forceinline__ __half tile_convert<__half>(uint32_t v, uint32_t width, uint32_t shift) {
+    return __uint2half_rn(width == 16 ? v >> shift : v); // exact: value <= 2047 whenever a half entry is used
 }
 template <>
-__device__ __forceinline__ float tile_convert<float>(uint32_t v, uint32_t, bool) { return float(v); }
+__device__ __forceinline__ float tile_convert<float>(uint32_t v, uint32_t, uint32_t) { return float(v); }
 template <>
-__device__ __forceinline__ unsigned short tile_convert<unsigned short>(uint32_t v, uint32_t, bool) {
+__device__ __forceinline__ unsigned short tile_convert<unsigned short>(uint32_t v, uint32_t, uint32_t) {
     return (unsigned short)v;
 }
 template <>
-__device__ __forceinline__ unsigned char tile_convert<unsigned char>(uint32_t v, uint32_t width, bool) {
+__device__ __forceinline__ unsigned char tile_convert<unsigned char>(uint32_t v, uint32_t width, uint32_t) {
     return (unsigned char)(width == 16 ? v >> 8 : v);
 }
 
@@ -34,7 +34,8 @@ static constexpr int PACK_E = 64;
 // grid = (ntiles, ceil(E / PACK_E)); block = 256.  rows [tile*TQ, tile*TQ + TQ) clipped to n_rows.
 template <class Entry>
 __global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width, uint32_t E, uint32_t n_rows,
-                                  uint32_t tq, bool high_byte, uint32_t copies, Entry* __restrict__ out) {
+                                  uint32_t tq, uint32_t high_byte /* filter shift */, uint32_t copies,
+                                  Entry* __restrict__ out) {
     extern __shared__ unsigned short panel[]; // [PACK_E][tq + 1]
     const uint32_t tile = blockIdx.x, e0 = blockIdx.y * PACK_E;
     const uint32_t ne = min(uint32_t(PACK_E), E - e0);
@@ -61,7 +62,7 @@ __global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width,
 }
 
 template <class Entry>
-static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq, bool hb,
+static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq, uint32_t hb,
                         void* out, cudaStream_t stream, uint32_t copies = 1) {
     const uint32_t ntiles = (n_rows + tq - 1) / tq;
     if (ntiles == 0) return;
@@ -87,18 +88,18 @@ size_t tile_entry_bytes(ScanVariant v) {
     }
 }
 
-void launch_pack_tiles(ScanVariant v, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
-                       void* out, cudaStream_t stream) {
+void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, const void* qlut, uint32_t width, uint32_t E,
+                       uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     switch (v) {
     case VAR_F16X8:
-    case VAR_F16X4_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, false, out, stream);
+    case VAR_F16X4_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, 0, out, stream);
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
-    case VAR_F16X4H_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, true, out, stream);
-    case VAR_F16X4H_C4D: return launch_pack<__half>(qlut, width, E, n_rows, tq, true, out, stream, 2);
-    case VAR_F32X2: return launch_pack<float>(qlut, width, E, n_rows, tq, false, out, stream);
-    case VAR_U16X1: return launch_pack<unsigned short>(qlut, width, E, n_rows, tq, false, out, stream);
-    case VAR_U8X1: return launch_pack<unsigned char>(qlut, width, E, n_rows, tq, false, out, stream);
+    case VAR_F16X4H_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream);
+    case VAR_F16X4H_C4D: return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream, 2);
+    case VAR_F32X2: return launch_pack<float>(qlut, width, E, n_rows, tq, 0, out, stream);
+    case VAR_U16X1: return launch_pack<unsigned short>(qlut, width, E, n_rows, tq, 0, out, stream);
+    case VAR_U8X1: return launch_pack<unsigned char>(qlut, width, E, n_rows, tq, 8, out, stream);
     default: throw Error(QADC_ERR_CONFIG, "pack_tiles: bad variant");
     }
 }
