@@ -184,13 +184,43 @@ __device__ __forceinline__ unsigned char tile_entry<unsigned char>(uint32_t v, u
 
 static constexpr uint32_t QP_SLAB = 512; // entries per shared-memory panel
 
-// grid = tiles; block = 256.  dynamic smem: panel u16 [min(E, QP_SLAB)][tq + 2] | sub_of[E]
+// eight consecutive rows of one entry line, converted to the variant's entry type, as vector stores
+template <class Entry>
+__device__ __forceinline__ void store_rows8(Entry* dst, const uint32_t (&v)[8], uint32_t shift);
+template <>
+__device__ __forceinline__ void store_rows8<__half>(__half* dst, const uint32_t (&v)[8], uint32_t shift) {
+    __half2 h[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __halves2half2(tile_entry<__half>(v[2 * k], shift), tile_entry<__half>(v[2 * k + 1], shift));
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(h);
+}
+template <>
+__device__ __forceinline__ void store_rows8<float>(float* dst, const uint32_t (&v)[8], uint32_t) {
+    reinterpret_cast<float4*>(dst)[0] = make_float4(float(v[0]), float(v[1]), float(v[2]), float(v[3]));
+    reinterpret_cast<float4*>(dst)[1] = make_float4(float(v[4]), float(v[5]), float(v[6]), float(v[7]));
+}
+template <>
+__device__ __forceinline__ void store_rows8<unsigned short>(unsigned short* dst, const uint32_t (&v)[8], uint32_t) {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+}
+template <>
+__device__ __forceinline__ void store_rows8<unsigned char>(unsigned char* dst, const uint32_t (&v)[8], uint32_t shift) {
+    uint32_t w[2] = {0, 0};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w[k >> 2] |= ((v[k] >> shift) & 0xFFu) << (8 * (k & 3));
+    *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+}
+
+// grid = tiles; block = 256.  dynamic smem: panel u16 [min(E, QP_SLAB)][tq + 2] | sub_of[E].
+// Phase 1, warp per row: a lane quantizes two adjacent entries at a time (float2 load, one 32-bit store into the
+// [row][entry] table, two panel stores), four such pairs in flight.  Phase 2: a thread emits eight consecutive rows
+// of one entry line as a 16-byte store (twice for the duplicated-line layout).  E is even and tq a multiple of 8.
 template <class Entry>
 __global__ void __launch_bounds__(256)
 ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uint32_t a,
                          const float* __restrict__ luts, const float* __restrict__ pmin,
                          const float* __restrict__ own_min, const float* __restrict__ qparams, uint32_t tq,
-                         uint32_t high_byte /* filter shift */, uint32_t copies, void* __restrict__ qluts,
+                         uint32_t filter_shift, uint32_t copies, void* __restrict__ qluts,
                          Entry* __restrict__ tile_lut,
                          uint32_t* __restrict__ row_query, uint32_t* __restrict__ row_bias) {
     extern __shared__ __align__(16) unsigned short panel[];
@@ -199,16 +229,20 @@ ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uin
     fill_sub_of(ds, sub_of);
     __syncthreads();
     const uint32_t tile = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const bool wide = ds.word_width == 16;
     for (uint32_t e0 = 0; e0 < ds.E; e0 += slab_cap) {
         const uint32_t ne = min(slab_cap, ds.E - e0);
         for (uint32_t r = warp; r < tq; r += nwarps) {
             const uint32_t slot = tile * tq + r;
             const uint32_t pair = slot_pair[slot];
+            uint16_t* q16 = reinterpret_cast<uint16_t*>(qluts) + size_t(slot) * ds.E + e0;
+            uint8_t* q8 = reinterpret_cast<uint8_t*>(qluts) + size_t(slot) * ds.E + e0;
             if (pair == NONE32) { // padding row: zero table, no query
-                for (uint32_t e = lane; e < ne; e += 32) {
+                for (uint32_t e = 2 * lane; e < ne; e += 64) {
                     panel[e * pitch + r] = 0;
-                    if (ds.word_width == 8) reinterpret_cast<uint8_t*>(qluts)[size_t(slot) * ds.E + e0 + e] = 0;
-                    else reinterpret_cast<uint16_t*>(qluts)[size_t(slot) * ds.E + e0 + e] = 0;
+                    panel[(e + 1) * pitch + r] = 0;
+                    if (wide) *reinterpret_cast<uint32_t*>(q16 + e) = 0u;
+                    else *reinterpret_cast<uint16_t*>(q8 + e) = 0;
                 }
                 if (e0 == 0 && lane == 0) {
                     row_query[slot] = NONE32;
@@ -222,22 +256,28 @@ ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uin
             const double rcp = delta > 0.0f ? __drcp_rn(double(delta)) : 0.0;
             const float* lut = luts + size_t(pair) * ds.E + e0;
             const float* pm = pmin + size_t(pair) * ds.m;
-            for (uint32_t eb = lane; eb < ne; eb += 128) { // four independent loads in flight per lane
-                float pv[4], pmv[4];
+            for (uint32_t eb = 2 * lane; eb < ne; eb += 256) {
+                float2 pv[4];
+                float pm0[4], pm1[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const uint32_t e = eb + 32 * k;
-                    pv[k] = e < ne ? lut[e] : 0.0f;
-                    pmv[k] = e < ne ? pm[sub_of[e0 + e]] : 0.0f;
+                    const uint32_t e = eb + 64 * k;
+                    if (e < ne) {
+                        pv[k] = *reinterpret_cast<const float2*>(lut + e);
+                        pm0[k] = pm[sub_of[e0 + e]];
+                        pm1[k] = pm[sub_of[e0 + e + 1]];
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const uint32_t e = eb + 32 * k;
+                    const uint32_t e = eb + 64 * k;
                     if (e >= ne) break;
-                    const uint32_t qv = quantize_entry_fast(pv[k], pmv[k], d_min, d_max, delta, rcp, ds.qmax);
-                    panel[e * pitch + r] = (unsigned short)qv;
-                    if (ds.word_width == 8) reinterpret_cast<uint8_t*>(qluts)[size_t(slot) * ds.E + e0 + e] = uint8_t(qv);
-                    else reinterpret_cast<uint16_t*>(qluts)[size_t(slot) * ds.E + e0 + e] = uint16_t(qv);
+                    const uint32_t q0 = quantize_entry_fast(pv[k].x, pm0[k], d_min, d_max, delta, rcp, ds.qmax);
+                    const uint32_t q1 = quantize_entry_fast(pv[k].y, pm1[k], d_min, d_max, delta, rcp, ds.qmax);
+                    panel[e * pitch + r] = (unsigned short)q0;
+                    panel[(e + 1) * pitch + r] = (unsigned short)q1;
+                    if (wide) *reinterpret_cast<uint32_t*>(q16 + e) = q0 | (q1 << 16);
+                    else *reinterpret_cast<uint16_t*>(q8 + e) = uint16_t(q0 | (q1 << 8));
                 }
             }
             if (e0 == 0 && lane == 0) {
@@ -253,15 +293,19 @@ ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uin
         __syncthreads();
         // copies == 2: every entry line twice back to back (VAR_F16X4H_C4D)
         Entry* dst = tile_lut + (size_t(tile) * ds.E + e0) * tq * copies;
-        if ((tq & (tq - 1)) == 0) {
-            const uint32_t lg = 31 - __clz(tq);
-            for (uint32_t u = threadIdx.x; u < ne * tq * copies; u += blockDim.x) {
-                const uint32_t line = u >> lg; // entry * copies + copy
-                dst[u] = tile_entry<Entry>(panel[(copies == 2 ? line >> 1 : line) * pitch + (u & (tq - 1))], high_byte);
+        const uint32_t groups = tq >> 3, lg = 31 - __clz(groups); // 8-row groups per line (a power of two)
+        for (uint32_t u = threadIdx.x; u < ne * groups; u += blockDim.x) {
+            const uint32_t el = u >> lg, g = u & (groups - 1);
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(panel + el * pitch + g * 8); // 4-byte aligned: pitch even
+            uint32_t v[8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t w = src[k];
+                v[2 * k] = w & 0xFFFFu;
+                v[2 * k + 1] = w >> 16;
             }
-        } else {
-            for (uint32_t u = threadIdx.x; u < ne * tq * copies; u += blockDim.x)
-                dst[u] = tile_entry<Entry>(panel[(u / tq / copies) * pitch + u % tq], high_byte);
+            for (uint32_t c = 0; c < copies; ++c)
+                store_rows8<Entry>(dst + (size_t(el) * copies + c) * tq + g * 8, v, filter_shift);
         }
         __syncthreads();
     }
@@ -294,6 +338,8 @@ void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, const DevSpe
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
     if (ntiles == 0) return;
+    if (tq < 8 || (tq & (tq - 1)) != 0 || (ds.E & 1u))
+        throw Error(QADC_ERR_CONFIG, "quantize_pack: tile height must be a power of two >= 8 and E even");
     const uint32_t fs = ds.word_width == 16 ? filter_shift : 0u;
     switch (v) {
     case VAR_F16X8:

@@ -343,7 +343,7 @@ __device__ __forceinline__ void admit_entry(const DevSpec* ds, const ScanArgs* a
 
 template <class P, class G, int EARLY>
 __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param, ScanArgs args_param) {
-    constexpr int CIF = 2; // codes in flight per lane group
+    constexpr int CIF = 2; // codes in flight per lane group (4 was measured slower on every workload)
     extern __shared__ __align__(1024) char smem[];
     // dynamic smem: tile_bufs x [E*ROWB) LUT tile | NSTAGE code stage buffers | per-warp queues
     __shared__ DevSpec s_ds;
