@@ -154,7 +154,7 @@ struct qadc_index {
     cudaStream_t stream = nullptr;
     qadc_spec spec{};
     DevSpec ds{};
-    DevBuf codebook, codebook_t, codes, calib, ids, slot_pair;
+    DevBuf codebook, codebook_t, sub_of, codes, calib, ids, slot_pair;
     DevBuf coarse_bf16, coarse_norm, coarse_mean, q_bf16, probe_eps; // tensor-core probe prefilter (ivf_probe_tc.cu)
     double coarse_rmax = 0.0;
     uint32_t dpad = 0;
@@ -501,8 +501,9 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         ivf_probe_order_device(h, dq, nb, a, st);
         const size_t t1 = h->timer.mark(st);
         if (ivf_tables_tiled_supported(ds))
-            launch_ivf_tables_tiled(ds, h->codebook_t.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(),
-                                    n_pairs, a, h->luts.as<float>(), h->pmin.as<float>(), h->own_min.as<float>(), st);
+            launch_ivf_tables_tiled(ds, h->codebook_t.as<float>(), h->sub_of.as<uint8_t>(), dq, h->coarse.as<float>(),
+                                    h->order.as<uint32_t>(), n_pairs, a, h->luts.as<float>(), h->pmin.as<float>(),
+                                    h->own_min.as<float>(), st);
         else
             launch_ivf_tables(ds, h->codebook.as<float>(), dq, h->coarse.as<float>(), h->order.as<uint32_t>(), n_pairs, a,
                               h->luts.as<float>(), h->pmin.as<float>(), h->own_min.as<float>(), st);
@@ -1203,17 +1204,14 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
             if (!(codebook[i] - codebook[i] == 0.0f)) throw Error(QADC_ERR_CORRUPTION, "codebook: non-finite centroid component");
         h->codebook.ensure(size_t(spec->cb_floats) * 4);
         QADC_CUDA_CHECK(cudaMemcpyAsync(h->codebook.p, codebook, size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice, st));
-        {   // [sub][dim][entry] image of the codebook for the register-tiled table kernel (ivf_lut.cu)
-            std::vector<float> cbt(spec->cb_floats);
-            const DevSpec tds = make_dev_spec(*spec, spec->groups);
-            for (uint32_t j = 0; j < tds.m; ++j) {
-                const uint32_t nent = 1u << tds.bits[j], dsub = tds.dim_alloc[j];
-                for (uint32_t i = 0; i < nent; ++i)
-                    for (uint32_t t = 0; t < dsub; ++t)
-                        cbt[tds.cb_off[j] + size_t(t) * nent + i] = codebook[tds.cb_off[j] + size_t(i) * dsub + t];
-            }
-            h->codebook_t.ensure(size_t(spec->cb_floats) * 4);
-            QADC_CUDA_CHECK(cudaMemcpy(h->codebook_t.p, cbt.data(), size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice));
+        if (ivf_tables_tiled_supported(h->ds)) { // transposed codebook + entry map of the tiled table kernel (ivf_lut.cu)
+            std::vector<float> cbt;
+            std::vector<uint8_t> sub_of;
+            ivf_tables_tiled_prepare(h->ds, codebook, cbt, sub_of);
+            h->codebook_t.ensure(cbt.size() * 4);
+            h->sub_of.ensure(sub_of.size());
+            QADC_CUDA_CHECK(cudaMemcpy(h->codebook_t.p, cbt.data(), cbt.size() * 4, cudaMemcpyHostToDevice));
+            QADC_CUDA_CHECK(cudaMemcpy(h->sub_of.p, sub_of.data(), sub_of.size(), cudaMemcpyHostToDevice));
         }
         const uint32_t d = spec->dims;
         // coarse centroids: row-major for the residuals, transposed [dims][K] for the probe kernel

@@ -166,9 +166,11 @@ void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* 
                        const uint32_t* d_order, uint32_t n_pairs, uint32_t a, float* d_luts, float* d_pmin,
                        float* d_own_min, cudaStream_t stream);
 bool ivf_tables_tiled_supported(const DevSpec& ds);
-void launch_ivf_tables_tiled(const DevSpec& ds, const float* d_codebook_t, const float* d_queries,
-                             const float* d_coarse, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
-                             float* d_luts, float* d_pmin, float* d_own_min, cudaStream_t stream);
+void ivf_tables_tiled_prepare(const DevSpec& ds, const float* codebook, std::vector<float>& cb_tp,
+                              std::vector<uint8_t>& sub_of);
+void launch_ivf_tables_tiled(const DevSpec& ds, const float* d_codebook_tp, const uint8_t* d_sub_of,
+                             const float* d_queries, const float* d_coarse, const uint32_t* d_order, uint32_t n_pairs,
+                             uint32_t a, float* d_luts, float* d_pmin, float* d_own_min, cudaStream_t stream);
 void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
                               const float* d_luts, const float* d_pmin, const float* d_own_min,
                               const float* d_qparams, const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base,

@@ -30,20 +30,21 @@ __device__ __forceinline__ void fill_sub_of(const DevSpec& ds, uint8_t* sub_of) 
     }
 }
 
-// dynamic smem: res[dims][TAB_PT] | pmin_u[TAB_PT][m] (u32 bit patterns) | sub_of[E]
+// dynamic smem: res[dims][TAB_PT] | pmin_u[TAB_PT][m] (u32 bit patterns).
+// codebook_tp: [sub][TAB_MAXD][entries] zero padded (every entry has TAB_MAXD components at stride `entries`);
+// sub_of: entry -> subquantizer (bytes).  Both are built once per index (api.cu).
 __global__ void __launch_bounds__(256)
-ivf_tables_tiled_kernel(DevSpec ds, const float* __restrict__ codebook_t, const float* __restrict__ queries,
-                        const float* __restrict__ coarse, const uint32_t* __restrict__ order, uint32_t a,
-                        uint32_t n_pairs, float* __restrict__ luts, float* __restrict__ pmin_out,
-                        float* __restrict__ own_min) {
+ivf_tables_tiled_kernel(DevSpec ds, const float* __restrict__ codebook_tp, const uint8_t* __restrict__ sub_of,
+                        const float* __restrict__ queries, const float* __restrict__ coarse,
+                        const uint32_t* __restrict__ order, uint32_t a, uint32_t n_pairs, float* __restrict__ luts,
+                        float* __restrict__ pmin_out, float* __restrict__ own_min) {
     extern __shared__ __align__(16) float smf[];
     float* res = smf;
     uint32_t* pmin_u = reinterpret_cast<uint32_t*>(res + size_t(ds.dims) * TAB_PT);
-    uint8_t* sub_of = reinterpret_cast<uint8_t*>(pmin_u + size_t(ds.m) * TAB_PT);
     __shared__ uint32_t s_q[TAB_PT], s_cell[TAB_PT];
     const uint32_t pair0 = blockIdx.x * TAB_PT;
     const uint32_t np = min(uint32_t(TAB_PT), n_pairs - pair0);
-    fill_sub_of(ds, sub_of);
+    const uint32_t lane = threadIdx.x & 31;
     if (threadIdx.x < TAB_PT) {
         const uint32_t pair = pair0 + threadIdx.x;
         s_q[threadIdx.x] = threadIdx.x < np ? pair / a : 0;
@@ -52,20 +53,37 @@ ivf_tables_tiled_kernel(DevSpec ds, const float* __restrict__ codebook_t, const 
     for (uint32_t u = threadIdx.x; u < ds.m * TAB_PT; u += blockDim.x) pmin_u[u] = 0x7f800000u; // +inf
     __syncthreads();
     // residual = query - centroid (index.hpp:286), one fp32 subtraction per component
-    for (uint32_t p = 0; p < TAB_PT; ++p) {
-        const float* q = queries + size_t(s_q[p]) * ds.dims;
-        const float* c = coarse + size_t(s_cell[p]) * ds.dims;
-        for (uint32_t d = threadIdx.x; d < ds.dims; d += blockDim.x)
-            res[d * TAB_PT + p] = p < np ? __fsub_rn(q[d], c[d]) : 0.0f;
+    if ((ds.dims & 3u) == 0 && ((reinterpret_cast<uintptr_t>(queries) | reinterpret_cast<uintptr_t>(coarse)) & 15u) == 0) {
+        const uint32_t d4 = ds.dims >> 2;
+        for (uint32_t u = threadIdx.x; u < d4 * TAB_PT; u += blockDim.x) {
+            const uint32_t p = u / d4, j = (u - p * d4) * 4;
+            float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p < np) {
+                const float4 q = *reinterpret_cast<const float4*>(queries + size_t(s_q[p]) * ds.dims + j);
+                const float4 c = *reinterpret_cast<const float4*>(coarse + size_t(s_cell[p]) * ds.dims + j);
+                r = make_float4(__fsub_rn(q.x, c.x), __fsub_rn(q.y, c.y), __fsub_rn(q.z, c.z), __fsub_rn(q.w, c.w));
+            }
+            res[(j + 0) * TAB_PT + p] = r.x;
+            res[(j + 1) * TAB_PT + p] = r.y;
+            res[(j + 2) * TAB_PT + p] = r.z;
+            res[(j + 3) * TAB_PT + p] = r.w;
+        }
+    } else {
+        for (uint32_t p = 0; p < TAB_PT; ++p) {
+            const float* q = queries + size_t(s_q[p]) * ds.dims;
+            const float* c = coarse + size_t(s_cell[p]) * ds.dims;
+            for (uint32_t d = threadIdx.x; d < ds.dims; d += blockDim.x)
+                res[d * TAB_PT + p] = p < np ? __fsub_rn(q[d], c[d]) : 0.0f;
+        }
     }
     __syncthreads();
     for (uint32_t e = threadIdx.x; e < ds.E; e += blockDim.x) {
         const uint32_t j = sub_of[e];
         const uint32_t dsub = ds.dim_alloc[j], nent = 1u << ds.bits[j];
-        const float* ct = codebook_t + ds.cb_off[j] + (e - ds.ent_off[j]);
+        const float* ct = codebook_tp + size_t(ds.ent_off[j]) * TAB_MAXD + (e - ds.ent_off[j]);
         float c[TAB_MAXD];
 #pragma unroll
-        for (int t = 0; t < TAB_MAXD; ++t) c[t] = uint32_t(t) < dsub ? ct[uint32_t(t) * nent] : 0.0f;
+        for (int t = 0; t < TAB_MAXD; ++t) c[t] = ct[uint32_t(t) * nent]; // zero padded past dsub
         float acc[TAB_PT];
 #pragma unroll
         for (int p = 0; p < TAB_PT; ++p) acc[p] = 0.0f;
@@ -84,18 +102,33 @@ ivf_tables_tiled_kernel(DevSpec ds, const float* __restrict__ codebook_t, const 
                 }
             }
         }
-        // per-table minima (min is order independent; entries are >= +0 or NaN, for which the unsigned order
-        // of the bit patterns is the "x < best" rule started from +inf): reduce over the lanes of this warp
-        // that sit in the same table, then one shared-memory atomic per (pair, table, warp)
-        const uint32_t peers = __match_any_sync(__activemask(), j);
-        const bool leader = (threadIdx.x & 31) == uint32_t(__ffs(peers) - 1);
         float* out = luts + size_t(pair0) * ds.E + e;
+        if (np == TAB_PT) {
+#pragma unroll
+            for (int p = 0; p < TAB_PT; ++p) out[size_t(p) * ds.E] = acc[p];
+        } else {
+#pragma unroll
+            for (int p = 0; p < TAB_PT; ++p)
+                if (uint32_t(p) < np) out[size_t(p) * ds.E] = acc[p];
+        }
+        // per-table minima (min is order independent; entries are >= +0 or NaN, for which the unsigned order
+        // of the bit patterns is the "x < best" rule started from +inf): REDUX over the lanes of this warp that
+        // sit in the same table.  With >= TAB_PT such lanes, lane (first + p) keeps pair p's minimum and the
+        // group issues ONE shared atomic; smaller groups fall back to one atomic per pair by the group leader.
+        const uint32_t peers = __match_any_sync(__activemask(), j);
+        const uint32_t first = __ffs(peers) - 1, gsize = __popc(peers);
+        const bool wide_group = gsize >= uint32_t(TAB_PT);
+        uint32_t keep = 0x7f800000u;
 #pragma unroll
         for (int p = 0; p < TAB_PT; ++p) {
-            if (uint32_t(p) < np) out[size_t(p) * ds.E] = acc[p];
             const uint32_t mn = __reduce_min_sync(peers, __float_as_uint(acc[p]));
-            if (leader) atomicMin(&pmin_u[p * ds.m + j], mn);
+            if (wide_group) {
+                if (lane == first + uint32_t(p)) keep = mn;
+            } else if (lane == first) {
+                atomicMin(&pmin_u[p * ds.m + j], mn);
+            }
         }
+        if (wide_group && lane - first < uint32_t(TAB_PT)) atomicMin(&pmin_u[(lane - first) * ds.m + j], keep);
     }
     __syncthreads();
     for (uint32_t u = threadIdx.x; u < np * ds.m; u += blockDim.x)
@@ -110,18 +143,33 @@ ivf_tables_tiled_kernel(DevSpec ds, const float* __restrict__ codebook_t, const 
 bool ivf_tables_tiled_supported(const DevSpec& ds) {
     for (uint32_t j = 0; j < ds.m; ++j)
         if (ds.dim_alloc[j] > uint32_t(TAB_MAXD)) return false;
-    const size_t smem = sizeof(float) * TAB_PT * (size_t(ds.dims) + ds.m) + ds.E;
+    const size_t smem = sizeof(float) * TAB_PT * (size_t(ds.dims) + ds.m);
     return smem <= 160 * 1024;
 }
 
-void launch_ivf_tables_tiled(const DevSpec& ds, const float* d_codebook_t, const float* d_queries,
-                             const float* d_coarse, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
-                             float* d_luts, float* d_pmin, float* d_own_min, cudaStream_t stream) {
+// host side, once per index: zero-padded transposed codebook [sub][TAB_MAXD][entries] and the entry -> sub map
+void ivf_tables_tiled_prepare(const DevSpec& ds, const float* codebook, std::vector<float>& cb_tp,
+                              std::vector<uint8_t>& sub_of) {
+    cb_tp.assign(size_t(ds.E) * TAB_MAXD, 0.0f);
+    sub_of.assign(ds.E, 0);
+    for (uint32_t j = 0; j < ds.m; ++j) {
+        const uint32_t nent = 1u << ds.bits[j], dsub = ds.dim_alloc[j];
+        for (uint32_t i = 0; i < nent; ++i) {
+            sub_of[ds.ent_off[j] + i] = uint8_t(j);
+            for (uint32_t t = 0; t < dsub && t < uint32_t(TAB_MAXD); ++t)
+                cb_tp[size_t(ds.ent_off[j]) * TAB_MAXD + size_t(t) * nent + i] = codebook[ds.cb_off[j] + size_t(i) * dsub + t];
+        }
+    }
+}
+
+void launch_ivf_tables_tiled(const DevSpec& ds, const float* d_codebook_tp, const uint8_t* d_sub_of,
+                             const float* d_queries, const float* d_coarse, const uint32_t* d_order, uint32_t n_pairs,
+                             uint32_t a, float* d_luts, float* d_pmin, float* d_own_min, cudaStream_t stream) {
     if (n_pairs == 0) return;
-    const size_t smem = sizeof(float) * TAB_PT * (size_t(ds.dims) + ds.m) + ds.E;
+    const size_t smem = sizeof(float) * TAB_PT * (size_t(ds.dims) + ds.m);
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_tables_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ivf_tables_tiled_kernel<<<(n_pairs + TAB_PT - 1) / TAB_PT, 256, smem, stream>>>(
-        ds, d_codebook_t, d_queries, d_coarse, d_order, a, n_pairs, d_luts, d_pmin, d_own_min);
+        ds, d_codebook_tp, d_sub_of, d_queries, d_coarse, d_order, a, n_pairs, d_luts, d_pmin, d_own_min);
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
