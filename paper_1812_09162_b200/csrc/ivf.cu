@@ -350,57 +350,104 @@ ivf_calib_kernel(DevSpec ds, const uint8_t* __restrict__ codes, const uint64_t* 
                  float* __restrict__ qparams, float* __restrict__ map, uint32_t* __restrict__ cell_npairs,
                  uint32_t* __restrict__ pair_rank) {
     extern __shared__ float smf[];
-    float* prefix = smf;
-    uint32_t* start = reinterpret_cast<uint32_t*>(prefix + t); // a + 1 entries
-    __shared__ float s_dmin, s_dmax;
+    float* prefix = smf;                                       // t floats, padded to a power of two for the sort
+    uint32_t tpow = 1;
+    while (tpow < t) tpow <<= 1;
+    uint32_t* start = reinterpret_cast<uint32_t*>(prefix + tpow); // a + 1 entries
+    __shared__ float s_dmin;
     __shared__ uint32_t s_np;
-    const uint32_t qi = blockIdx.x;
+    __shared__ float w_min[8];
+    __shared__ uint32_t w_sum[8];
+    const uint32_t qi = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t* ord = order + size_t(qi) * a;
-    if (threadIdx.x == 0) {
-        float dmin = __int_as_float(0x7f800000); // index.hpp:301-302
-        uint32_t taken = 0;
-        for (uint32_t i = 0; i < a; ++i) {
+    // d_min_global = min over the probed cells of min_total() (index.hpp:301-302), and the prefix budget:
+    // cell i contributes min(count_i, t - taken) codes, i.e. taken_i = min(sum_{k<i} count_k, t) (index.hpp:305-306).
+    // Probes are walked in chunks of 256 with a block-wide exclusive scan.
+    float dmin = __int_as_float(0x7f800000);
+    uint32_t carry = 0; // codes taken by earlier chunks (saturated at t)
+    for (uint32_t base = 0; base < a; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        uint32_t cnt = 0;
+        if (i < a) {
             const float mt = own_min[size_t(qi) * a + i];
             dmin = (mt < dmin) ? mt : dmin;
-            start[i] = taken;
-            const uint64_t cnt = calib_count[ord[i]];
-            taken += uint32_t(min(cnt, uint64_t(t - taken))); // index.hpp:305-306
+            cnt = uint32_t(min(calib_count[ord[i]], uint64_t(t)));
         }
-        start[a] = taken;
-        s_dmin = dmin;
-        s_np = taken;
+        uint32_t incl = cnt; // inclusive warp scan, saturating at t keeps the sums small
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl = min(incl + v, t);
+        }
+        uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1); // saturated sum of the lanes before this one
+        if (lane == 0) excl = 0;
+        if (lane == 31) w_sum[warp] = incl;
+        __syncthreads();
+        uint32_t before = carry;
+        for (uint32_t w = 0; w < warp; ++w) before = min(before + w_sum[w], t);
+        if (i < a) start[i] = min(before + excl, t);
+        uint32_t total = carry;
+        for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) total = min(total + w_sum[w], t);
+        carry = total;
+        __syncthreads();
     }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float other = __shfl_xor_sync(0xffffffffu, dmin, o);
+        dmin = (other < dmin) ? other : dmin;
+    }
+    if (lane == 0) w_min[warp] = dmin;
     // row grouping: every probed, non-empty cell gets this pair as one LUT row
     for (uint32_t i = threadIdx.x; i < a; i += blockDim.x) {
         const uint32_t cell = ord[i];
         pair_rank[size_t(qi) * a + i] = list_count[cell] ? atomicAdd(&cell_npairs[cell], 1u) : 0xFFFFFFFFu;
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = w_min[0];
+        for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) m = (w_min[w] < m) ? w_min[w] : m;
+        s_dmin = m;
+        start[a] = carry;
+        s_np = carry;
+    }
+    __syncthreads();
     const uint32_t np = s_np;
     for (uint32_t p = threadIdx.x; p < np; p += blockDim.x) {
-        uint32_t i = 0;
-        while (start[i + 1] <= p) ++i; // the probe this prefix position falls into
+        uint32_t lo = 0, hi = a; // the probe this prefix position falls into: last i with start[i] <= p
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (start[mid] <= p) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t i = lo;
         const uint8_t* code = codes + (list_code_off[ord[i]] + (p - start[i])) * ds.code_stride;
         const float* lut = luts + (size_t(qi) * a + i) * ds.E;
         float acc = 0.0f;
         for (uint32_t j = 0; j < ds.m; ++j) acc = __fadd_rn(acc, lut[ds.ent_off[j] + code_field(ds, code, j)]);
         prefix[p] = acc;
     }
-    __syncthreads();
     float d_max = 0.0f;
     if (np) {
-        const uint32_t r_eff = min(r, np); // index.hpp:308
-        for (uint32_t i = threadIdx.x; i < np; i += blockDim.x) {
-            const float v = prefix[i];
-            uint32_t less = 0, leq = 0;
-            for (uint32_t k = 0; k < np; ++k) {
-                less += prefix[k] < v;
-                leq += prefix[k] <= v;
-            }
-            if (less <= r_eff - 1 && r_eff - 1 < leq) s_dmax = v;
-        }
+        // r_eff-th smallest of the prefix (index.hpp:308, calibrate_bounds): bitonic sort of the bit patterns
+        // (sums of non-negative terms: unsigned order == float order), padded with +inf
+        const uint32_t r_eff = min(r, np);
+        uint32_t npow = 2;
+        while (npow < np) npow <<= 1;
+        uint32_t* key = reinterpret_cast<uint32_t*>(prefix);
+        for (uint32_t i = np + threadIdx.x; i < npow; i += blockDim.x) key[i] = 0xFFFFFFFFu;
         __syncthreads();
-        d_max = s_dmax;
+        for (uint32_t size = 2; size <= npow; size <<= 1)
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                for (uint32_t i = threadIdx.x; i < npow / 2; i += blockDim.x) {
+                    const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const uint32_t x = key[lo], y = key[hi];
+                    if ((x > y) == up) {
+                        key[lo] = y;
+                        key[hi] = x;
+                    }
+                }
+                __syncthreads();
+            }
+        d_max = prefix[r_eff - 1];
     }
     if (threadIdx.x == 0) {
         float* o = qparams + size_t(qi) * 4;
@@ -419,7 +466,9 @@ void launch_ivf_calib(const DevSpec& ds, const uint8_t* d_codes, const uint64_t*
                       const float* d_luts, const float* d_own_min, uint32_t r, uint32_t t, float* d_qparams,
                       float* d_map, uint32_t* d_cell_npairs, uint32_t* d_pair_rank, cudaStream_t stream) {
     if (nq == 0) return;
-    const size_t smem = size_t(t) * 4 + size_t(a + 1) * 4;
+    size_t tpow = 1;
+    while (tpow < t) tpow <<= 1;
+    const size_t smem = tpow * 4 + size_t(a + 1) * 4;
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_calib_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ivf_calib_kernel<<<nq, 256, smem, stream>>>(ds, d_codes, d_list_code_off, d_calib_count, d_list_count, d_order, a, d_luts,
                                                 d_own_min, r, t, d_qparams, d_map, d_cell_npairs, d_pair_rank);
