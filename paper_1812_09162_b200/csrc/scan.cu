@@ -281,7 +281,8 @@ static constexpr int SCAN_THREADS = SCAN_CONSUMERS + 32;   // + one producer war
 static constexpr int STAGE_BYTES = 8192;                   // one code stage buffer
 static constexpr int NSTAGE = 4;
 static constexpr int WQ_CAP = 64;                          // per-warp queue of flagged (row, code) pairs
-static constexpr int WQ_BYTES = SCAN_WARPS * WQ_CAP * 12;  // row, stage index, accumulator value
+static constexpr int WQ_ENTRY = 28;                        // ref (8) + code copy (8) + row, stage index, value (4 each)
+static constexpr int WQ_BYTES = SCAN_WARPS * WQ_CAP * WQ_ENTRY;
 
 // --------------------------------------------------------- exact admission --
 
@@ -472,11 +473,32 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     const uint32_t lane_in = lane % LPC, lane_code = lane / LPC;
     const uint32_t lane_off = lane_in * P::LANE_B + (dup_of<P>::value ? (lane_code & 1u) * (P::ROWB / 2) : 0u);
     // per-warp queue of flagged pairs: ballot-compacted in the hot loop, resolved 32 at a time
-    uint32_t* wq_row = reinterpret_cast<uint32_t*>(stage + NSTAGE * STAGE_BYTES) + warp * (WQ_CAP * 3);
+    // 64-bit codes with a compile-time geometry (every named spec): the queue entry carries a copy of the code
+    // and a global id reference, so it outlives its stage buffer and job -- the queue is drained only when 32
+    // entries are waiting (full-warp admission) and once at the end.  Other shapes keep an index into the stage
+    // buffer and drain at every stage end.
+    constexpr bool COPY = !G::RUNTIME && G::CW == 2;
+    char* wq_base = stage + NSTAGE * STAGE_BYTES + size_t(warp) * (WQ_CAP * WQ_ENTRY);
+    uint64_t* wq_ref = reinterpret_cast<uint64_t*>(wq_base);
+    uint2* wq_code = reinterpret_cast<uint2*>(wq_ref + WQ_CAP);
+    uint32_t* wq_row = reinterpret_cast<uint32_t*>(wq_code + WQ_CAP);
     uint32_t* wq_idx = wq_row + WQ_CAP;
     float* wq_val = reinterpret_cast<float*>(wq_idx + WQ_CAP);
     uint32_t qn = 0; // warp-uniform fill level
     const uint32_t lanemask_lt = (1u << lane) - 1u;
+    auto flush_copy = [&]() {
+        __syncwarp();
+        for (uint32_t base = 0; base < qn; base += 32) {
+            const uint32_t e = base + lane;
+            if (e < qn) {
+                const uint64_t ref = wq_ref[e];
+                const uint32_t id = a->ids ? a->ids[ref] : uint32_t(ref);
+                admit_entry<P>(ds, a, wq_val[e], reinterpret_cast<const uint8_t*>(&wq_code[e]), wq_row[e], id);
+            }
+        }
+        __syncwarp();
+        qn = 0;
+    };
 
     ScanJob cur{};
     if (j_begin < j_end) cur = a->jobs[j_begin];
@@ -526,7 +548,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                 __syncwarp();
                 qn = 0;
             };
-            auto flag = [&](const typename P::Acc& acc, bool live, uint32_t i) {
+            auto flag = [&](const typename P::Acc& acc, bool live, uint32_t i, uint32_t c0, uint32_t c1) {
                 const bool h = live && P::any(acc);
                 if (__any_sync(0xffffffffu, h)) {
 #pragma unroll
@@ -534,12 +556,20 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                         const bool hs = h && P::hit(acc, sl);
                         const uint32_t m = __ballot_sync(0xffffffffu, hs);
                         if (m) {
-                            if (qn + 32 > WQ_CAP) flush();
+                            if (qn + 32 > WQ_CAP) {
+                                if constexpr (COPY) flush_copy();
+                                else flush();
+                            }
                             if (hs) {
                                 const uint32_t slot = qn + __popc(m & lanemask_lt);
                                 wq_row[slot] = job.row_begin + lane_in * P::QPL + sl;
-                                wq_idx[slot] = i;
                                 wq_val[slot] = P::value(acc, sl);
+                                if constexpr (COPY) {
+                                    wq_code[slot] = make_uint2(c0, c1);
+                                    wq_ref[slot] = a->ids ? job.ids_off + first + i : uint64_t(job.id_base + first + i);
+                                } else {
+                                    wq_idx[slot] = i;
+                                }
                             }
                             qn += __popc(m);
                         }
@@ -581,7 +611,8 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                     });
 #pragma unroll
                     for (int c = 0; c < CIF; ++c)
-                        flag(acc[c], i0 + c * SCAN_WARPS * P::CPW < cnt, i0 + c * SCAN_WARPS * P::CPW);
+                        flag(acc[c], i0 + c * SCAN_WARPS * P::CPW < cnt, i0 + c * SCAN_WARPS * P::CPW, cw[c][0],
+                             cw[c][G::CW > 1 ? 1 : 0]);
                 }
             } else {
                 // runtime geometry: any m / widths / code size that fits; one code per warp step
@@ -593,13 +624,15 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                         const uint32_t idx = rt_sub_index(ds, code, j);
                         P::add(acc, tile + size_t(ds->ent_off[j] + idx) * P::ROWB + lane_off);
                     }
-                    flag(acc, iw + lane_code < cnt, i);
+                    flag(acc, iw + lane_code < cnt, i, 0u, 0u);
                 }
             }
-            flush(); // queued pairs reference this stage buffer: resolve them before releasing it
+            if constexpr (!COPY) flush(); // queued pairs reference this stage buffer: resolve them before releasing it
+            __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[b]); // this warp is done with stage buffer b
         }
     }
+    if constexpr (COPY) flush_copy();
 }
 
 // ----------------------------------------------------------------- dispatch --
