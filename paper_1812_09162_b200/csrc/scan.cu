@@ -477,7 +477,9 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     // and a global id reference, so it outlives its stage buffer and job -- the queue is drained only when 32
     // entries are waiting (full-warp admission) and once at the end.  Other shapes keep an index into the stage
     // buffer and drain at every stage end.
-    constexpr bool COPY = !G::RUNTIME && G::CW == 2;
+    // (Exact-filter variants admit straight from the accumulator value and rarely need the code: they keep the
+    // cheaper stage-indexed entries; measured 4 % faster on the small-N 16x{4,4} workload.)
+    constexpr bool COPY = !G::RUNTIME && G::CW == 2 && !P::EXACT_FILTER;
     char* wq_base = stage + NSTAGE * STAGE_BYTES + size_t(warp) * (WQ_CAP * WQ_ENTRY);
     uint64_t* wq_ref = reinterpret_cast<uint64_t*>(wq_base);
     uint2* wq_code = reinterpret_cast<uint2*>(wq_ref + WQ_CAP);
