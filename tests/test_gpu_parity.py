@@ -703,3 +703,46 @@ def test_ivf_search_many_cells_vs_oracle(port, dims, text, k_cells, n, probes, n
                                  threads=8, family=0x100)
             got_rr = idx.search(queries, qb.SearchParams(probes=pr, r=r, t=t, rerank=True))
             assert np.array_equal(got_rr.ids, rr[0]) and bits_equal(got_rr.dists, rr[1]), ("rerank", pr)
+
+
+def test_full_size_c2_properties(port):
+    """BASELINE configs[1] at full size (12x{6,5,5}, d=96, N=1e7, Q=1e4 -- the default bench workload) through
+    size-independent properties: for every query the result is full, sorted by (distance, id) and duplicate free;
+    for a sample of queries the quantized tables equal the oracle's, every returned distance is the unquantized
+    oracle ADC sum of that code, and no code of a 100k uniform sample beats the R-th result; and two queries are
+    compared with the complete oracle search."""
+    dims, text, n, nq, r, t = 96, "12x{6,5,5}", 10_000_000, 10_000, 100, 400
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    from paper_1812_09162_b200.synth import train_codebook
+    cb = train_codebook(s, gaussian_mixture(20000, dims, seed=14), iters=3)
+    codes = random_codes(s, n, seed=16)
+    pk = qb.pack_list(s, codes)
+    queries = gaussian_mixture(nq, dims, seed=13)
+    with qb.FlatIndex(s, cb, pk, n) as idx:
+        res = idx.search(queries, qb.SearchParams(r=r, t=t))
+        check_q = np.arange(0, nq, 250)
+        _, qluts, _ = idx.tables(queries[check_q], qb.SearchParams(r=r, t=t))
+    assert np.all(res.counts == r)
+    assert np.all(np.diff(res.dists, axis=1) >= 0)
+    srt = np.sort(res.ids, axis=1)
+    assert np.all(srt[:, 1:] != srt[:, :-1])
+    bits = np.array(so.bits_list())
+    off = np.concatenate([[0], np.cumsum(1 << bits)[:-1]])
+    sample = np.random.default_rng(5).choice(n, size=100_000, replace=False)
+    for k, qi in enumerate(check_q):
+        lut = port.compute_tables(so, cb, queries[qi])
+        pre = port.prefix_float(so, pk, n, lut, t)
+        dmin, dmax = port.calibrate(so, lut, pre, r)
+        qlut, _, delta, own = port.quantize(so, lut, dmin, dmax, 16)
+        assert np.array_equal(qlut, qluts[k]), qi
+        q32 = qlut.astype(np.uint32)
+        sums = np.minimum(q32[off[None, :] + codes[res.ids[qi]].astype(np.int64)].sum(1), 65535)
+        want = (sums.astype(np.float32) * delta + own).astype(np.float32)
+        assert bits_equal(res.dists[qi], want), qi
+        keys = sums.astype(np.int64) << 32 | res.ids[qi].astype(np.int64)
+        assert np.all(np.diff(keys) > 0), qi
+        ssum = np.minimum(q32[off[None, :] + codes[sample].astype(np.int64)].sum(1), 65535)
+        skeys = ssum.astype(np.int64) << 32 | sample.astype(np.int64)
+        assert np.all(skeys[~np.isin(sample, res.ids[qi])] > keys[-1]), qi
+    ref = port.flat_search(so, cb, pk, n, queries[:2], r=r, t=t, threads=2)
+    assert np.array_equal(res.ids[:2], ref[0]) and bits_equal(res.dists[:2], ref[1])
