@@ -746,3 +746,38 @@ def test_full_size_c2_properties(port):
         assert np.all(skeys[~np.isin(sample, res.ids[qi])] > keys[-1]), qi
     ref = port.flat_search(so, cb, pk, n, queries[:2], r=r, t=t, threads=2)
     assert np.array_equal(res.ids[:2], ref[0]) and bits_equal(res.dists[:2], ref[1])
+
+
+def test_c5_shape_ivf_sampled_queries_vs_oracle(port):
+    """BASELINE configs[4] shape (K=16384 cells, d=128, 12x{6,5,5}, nprobe=64, R=100, t=400) on a smaller database
+    (8e6 codes, skewed list lengths) and 2000 queries: the probe order of every sampled query and its complete
+    result (ids, distances, counts) equal the oracle's.  This is the path the C5 bench line times: tensor-core probe
+    prefilter at the real K, 128k (query, cell) pairs of residual tables, fused quantize + pack, duplicated-line
+    32-row tiles, two scan rounds."""
+    rng = np.random.default_rng(55)
+    dims, text, k_cells, n, nq, probes = 128, "12x{6,5,5}", 16384, 8_000_000, 2000, 64
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    centres = (rng.standard_normal((64, dims)) * 3).astype(np.float32)
+    coarse = (centres[rng.integers(0, 64, size=k_cells)] + rng.standard_normal((k_cells, dims))).astype(np.float32)
+    cb = (rng.standard_normal(s.cb_floats) * 0.6).astype(np.float32)
+    w = rng.pareto(2.0, size=k_cells) + 0.2
+    counts = np.floor(w / w.sum() * n).astype(np.uint64)
+    counts[:5] = [0, 1, 15, 16, 17]  # empty / tiny lists next to the long ones
+    pbytes = np.array([qb.packed_bytes(s, int(c)) for c in counts], dtype=np.uint64)
+    boff = np.concatenate([[0], np.cumsum(pbytes)[:-1]]).astype(np.uint64)
+    ioff = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
+    packed = rng.integers(0, 256, size=int(pbytes.sum()), dtype=np.uint8)  # every {6,5,5} bit pattern is a valid code
+    ids = rng.permutation(int(counts.sum())).astype(np.uint32)
+    queries = (centres[rng.integers(0, 64, size=nq)] + rng.standard_normal((nq, dims)) * 1.2).astype(np.float32)
+    with qb.IvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids) as idx:
+        got = idx.search(queries, qb.SearchParams(probes=probes, r=100, t=400))
+        order = idx.probe_order(queries, probes)
+    assert np.all(np.diff(got.dists, axis=1)[got.counts == 100] >= 0)
+    sel = np.arange(0, nq, 67)
+    for qi in sel:
+        assert np.array_equal(order[qi], port.probe_order(dims, coarse, queries[qi], probes)), qi
+    want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries[sel], probes=probes, r=100, t=400,
+                           threads=8)
+    assert np.array_equal(got.counts[sel], want[2])
+    assert np.array_equal(got.ids[sel], want[0])
+    assert bits_equal(got.dists[sel], want[1])
