@@ -434,7 +434,7 @@ static void ivf_probe_order_device(qadc_index* h, const float* dq, uint32_t nb, 
     const DevSpec& ds = h->ds;
     const uint32_t K = h->k_cells;
     h->scratch.ensure(size_t(nb) * K * 4);
-    h->cta_begin.ensure(size_t(nb) * 4); // reused as the probe-selection redo flags
+    h->cta_begin.ensure((2 * size_t(nb) + 1) * 4); // reused as the probe-selection redo flags | list | count
     if (h->probe_tc && h->probe_tc_ready && ivf_probe_tc_supported(ds.dims, K, a)) {
         h->q_bf16.ensure(size_t(nb) * h->dpad * 2);
         h->probe_eps.ensure(size_t(nb) * 8);

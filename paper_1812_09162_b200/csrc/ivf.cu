@@ -71,21 +71,24 @@ static constexpr int PROBE_QT = 16;
 __global__ void __launch_bounds__(256)
 ivf_coarse_dist_kernel(const float* __restrict__ queries, const float* __restrict__ coarse_t, uint32_t dims,
                        uint32_t k_cells, uint32_t nq, float* __restrict__ dist /* [nq][K] */,
-                       const uint32_t* __restrict__ only_flagged) {
+                       const uint32_t* __restrict__ redo_list /* flags[nq] | list[nq] | count */) {
     extern __shared__ __align__(16) float qs[]; // [dims][PROBE_QT]
-    const uint32_t q0 = blockIdx.y * PROBE_QT;
-    if (only_flagged) { // redo pass of the tensor-core prefilter: skip tiles without a flagged query
-        bool any = false;
-        for (uint32_t i = 0; i < PROBE_QT && q0 + i < nq; ++i) any |= only_flagged[q0 + i] != 0;
-        if (!any) return;
-    }
+    __shared__ uint32_t s_qidx[PROBE_QT];
+    // redo pass of the tensor-core prefilter: the undecided queries come as a compact list, a small grid walks it
+    const uint32_t n_list = redo_list ? redo_list[2 * size_t(nq)] : nq;
+    for (uint32_t q0 = blockIdx.y * PROBE_QT; q0 < n_list; q0 += gridDim.y * PROBE_QT) {
+    __syncthreads(); // previous tile's shared data is no longer read
+    if (threadIdx.x < PROBE_QT)
+        s_qidx[threadIdx.x] = q0 + threadIdx.x < n_list ? (redo_list ? redo_list[nq + q0 + threadIdx.x] : q0 + threadIdx.x)
+                                                        : 0xFFFFFFFFu;
+    __syncthreads();
     for (uint32_t u = threadIdx.x; u < dims * PROBE_QT; u += blockDim.x) {
         const uint32_t qi = u % PROBE_QT, j = u / PROBE_QT;
-        qs[u] = q0 + qi < nq ? queries[size_t(q0 + qi) * dims + j] : 0.0f;
+        qs[u] = s_qidx[qi] != 0xFFFFFFFFu ? queries[size_t(s_qidx[qi]) * dims + j] : 0.0f;
     }
     __syncthreads();
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= k_cells) return;
+    if (c >= k_cells) continue;
     float acc[PROBE_QT];
 #pragma unroll
     for (int i = 0; i < PROBE_QT; ++i) acc[i] = 0.0f;
@@ -104,7 +107,8 @@ ivf_coarse_dist_kernel(const float* __restrict__ queries, const float* __restric
     }
 #pragma unroll
     for (int i = 0; i < PROBE_QT; ++i)
-        if (q0 + i < nq) dist[size_t(q0 + i) * k_cells + c] = acc[i];
+        if (s_qidx[i] != 0xFFFFFFFFu) dist[size_t(s_qidx[i]) * k_cells + c] = acc[i];
+    }
 }
 
 // One CTA (256 threads) per query: first a cells by (distance, cell) -- partial_sort on pairs,
@@ -239,7 +243,8 @@ void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t 
     const size_t smem_d = size_t(dims) * PROBE_QT * 4;
     if (smem_d > 200 * 1024) throw Error(QADC_ERR_CONFIG, "ivf probe: dims too large");
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_coarse_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_d)));
-    const dim3 grid((k_cells + 255) / 256, (nq + PROBE_QT - 1) / PROBE_QT);
+    const uint32_t q_tiles = (nq + PROBE_QT - 1) / PROBE_QT;
+    const dim3 grid((k_cells + 255) / 256, redo_only ? std::min<uint32_t>(q_tiles, 8u) : q_tiles);
     ivf_coarse_dist_kernel<<<grid, 256, smem_d, stream>>>(d_queries, d_coarse_t, dims, k_cells, nq, d_dist_scratch,
                                                           redo_only ? d_redo : nullptr);
     ++g_launches;

@@ -190,7 +190,10 @@ probe_select_tc_kernel(const float* __restrict__ approx, const double* __restric
     __syncthreads();
     const uint32_t n = s_cnt;
     if (n > TC_CAND || n < a) { // n < a only if the limit itself is NaN
-        if (tid == 0) redo[qi] = 1u;
+        if (tid == 0) { // flags[nq] | compact list[nq] | count
+            redo[qi] = 1u;
+            redo[gridDim.x + atomicAdd(&redo[2 * size_t(gridDim.x)], 1u)] = qi;
+        }
         return;
     }
     // the reference's distance (index.hpp:254-258): fp32, serial over the dims, unfused
@@ -248,7 +251,7 @@ void launch_ivf_probe_tc(const float* d_queries, const float* d_coarse, const ui
                          float* d_approx, uint32_t* d_redo, uint32_t* d_order, cudaStream_t stream) {
     const __nv_bfloat16* d_coarse_bf16 = reinterpret_cast<const __nv_bfloat16*>(d_coarse_bits);
     __nv_bfloat16* d_qb = reinterpret_cast<__nv_bfloat16*>(d_q_bits);
-    QADC_CUDA_CHECK(cudaMemsetAsync(d_redo, 0, size_t(nq) * 4, stream));
+    QADC_CUDA_CHECK(cudaMemsetAsync(d_redo, 0, (2 * size_t(nq) + 1) * 4, stream)); // flags | list | count
     probe_prep_queries_kernel<<<(nq * 32 + 255) / 256, 256, 0, stream>>>(d_queries, d_mean, dims, dpad, nq, cmax, d_qb,
                                                                         d_eps2);
     const dim3 grid((k_cells + GN - 1) / GN, (nq + GM - 1) / GM);
