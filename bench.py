@@ -46,7 +46,7 @@ WORKLOADS = {
     "c5": dict(kind="ivf", spec="12x{6,5,5}", dims=128, n=62_500_000, nq=10_000, data="random", k_cells=16384,
                probes=64),
 }
-R, T = 100, 400
+R, T = int(os.environ.get("QADC_BENCH_R", 100)), int(os.environ.get("QADC_BENCH_T", 400))  # BASELINE: R=100, t=400 (env: experiments only)
 
 
 def log(*a):
