@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -148,6 +149,9 @@ struct StageTimer {
 using namespace qadc;
 
 struct qadc_index {
+    // The handle is immutable after open, but every call uses its workspaces and stream: concurrent calls on one
+    // handle serialise here (the reference lets any number of threads call search on one index).
+    std::recursive_mutex mu;
     int kind = 0; // 0 flat, 1 ivf
     int device = 0;
     int num_sms = 0;
@@ -861,6 +865,7 @@ int qadc_search_batch_device(qadc_index* h, const float* d_queries, uint32_t nq,
                              uint64_t* d_out_keys, float* d_out_map, void* stream) {
     return guarded([&] {
         if (!h || !params || (nq && !d_queries)) throw Error(QADC_ERR_INPUT, "null argument");
+        std::lock_guard<std::recursive_mutex> lock(h->mu);
         set_device(h->device);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : h->stream;
         if (h->kind == 0)
@@ -875,6 +880,7 @@ int qadc_search_batch(qadc_index* h, const float* queries, uint32_t nq, const qa
     return guarded([&] {
         if (!h || !params || (nq && (!queries || !out_ids || !out_dists || !out_counts)))
             throw Error(QADC_ERR_INPUT, "null argument");
+        std::lock_guard<std::recursive_mutex> lock(h->mu);
         validate_params(*params, h->kind == 1);
         set_device(h->device);
         cudaStream_t st = h->stream;
@@ -915,6 +921,7 @@ int qadc_flat_tables(qadc_index* h, const float* queries, uint32_t nq, const qad
                      float* luts, void* qluts, float* calib) {
     return guarded([&] {
         if (!h || h->kind != 0 || !params || !queries) throw Error(QADC_ERR_INPUT, "tables: bad arguments");
+        std::lock_guard<std::recursive_mutex> lock(h->mu);
         validate_params(*params, false);
         set_device(h->device);
         if (nq == 0) return;
@@ -955,6 +962,7 @@ int qadc_flat_adc_sums(qadc_index* h, const void* qlut, uint32_t width, uint32_t
                        uint64_t n, uint32_t* sums) {
     return guarded([&] {
         if (!h || h->kind != 0 || !qlut || !sums) throw Error(QADC_ERR_INPUT, "adc_sums: bad arguments");
+        std::lock_guard<std::recursive_mutex> lock(h->mu);
         if (width != h->ds.word_width) throw Error(QADC_ERR_CONFIG, "scan: table width does not match the packing word width");
         if (first + n > h->count) throw Error(QADC_ERR_INPUT, "adc_sums: range exceeds list");
         set_device(h->device);
@@ -972,6 +980,7 @@ int qadc_flat_adc_sums(qadc_index* h, const void* qlut, uint32_t width, uint32_t
 int qadc_flat_download_codes(qadc_index* h, uint64_t first, uint64_t n, uint8_t* codes_out) {
     return guarded([&] {
         if (!h || h->kind != 0 || !codes_out) throw Error(QADC_ERR_INPUT, "download_codes: bad arguments");
+        std::lock_guard<std::recursive_mutex> lock(h->mu);
         if (first + n > h->count) throw Error(QADC_ERR_INPUT, "download_codes: range exceeds list");
         set_device(h->device);
         cudaStream_t st = h->stream;
@@ -1167,6 +1176,7 @@ int qadc_get_stats(const qadc_index* h, qadc_stats* out) {
 int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
     return guarded([&] {
         if (!h || !name) throw Error(QADC_ERR_INPUT, "set_option: null argument");
+        std::lock_guard<std::recursive_mutex> lock(h->mu);
         const std::string n(name);
         if (n == "cand_cap") h->cand_cap = uint32_t(std::max<int64_t>(value, 16));
         else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384));
@@ -1327,6 +1337,7 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
 int qadc_ivf_probe_order(qadc_index* h, const float* queries, uint32_t nq, uint32_t a, uint32_t* order) {
     return guarded([&] {
         if (!h || h->kind != 1 || (nq && (!queries || !order))) throw Error(QADC_ERR_INPUT, "probe_order: bad arguments");
+        std::lock_guard<std::recursive_mutex> lock(h->mu);
         set_device(h->device);
         a = std::min(a, h->k_cells);
         if (nq == 0 || a == 0) return;

@@ -781,3 +781,36 @@ def test_c5_shape_ivf_sampled_queries_vs_oracle(port):
     assert np.array_equal(got.counts[sel], want[2])
     assert np.array_equal(got.ids[sel], want[0])
     assert bits_equal(got.dists[sel], want[1])
+
+
+def test_concurrent_calls_on_one_handle_serialise():
+    """The reference lets any number of threads call search() on one index (the CLI's worker pool,
+    pqscan_cli.cpp:141-166).  A GPU handle owns workspaces and a stream, so concurrent calls must serialise inside
+    the library: every thread gets exactly the result a lone caller gets."""
+    import threading
+    rng = np.random.default_rng(21)
+    dims, text, n = 96, "12x{6,5,5}", 200_000
+    s = qb.allocate_dims(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+    pk = qb.pack_list(s, random_codes(s, n, seed=3))
+    batches = [(rng.standard_normal((nq, dims)) * 2).astype(np.float32) for nq in (1, 7, 64, 33, 1, 128, 5, 16)]
+    with qb.FlatIndex(s, cb, pk, n) as idx:
+        want = [idx.search(q) for q in batches]
+        got = [None] * len(batches)
+        errors = []
+
+        def work(k):
+            try:
+                for _ in range(3):
+                    got[k] = idx.search(batches[k])
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+
+        threads = [threading.Thread(target=work, args=(k,)) for k in range(len(batches))]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+    assert not errors, errors
+    for w, g in zip(want, got):
+        assert np.array_equal(w.ids, g.ids) and bits_equal(w.dists, g.dists) and np.array_equal(w.counts, g.counts)
