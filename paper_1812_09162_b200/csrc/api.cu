@@ -197,7 +197,9 @@ namespace qadc {
 
 static constexpr uint64_t CODE_PAD = 1024; // device code arrays are padded to this many codes
 
-static ScanPlan plan_for(const qadc_index* h) { return plan_scan(h->ds, h->device, h->force_variant); }
+static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true) {
+    return plan_scan(h->ds, h->device, h->force_variant, allow_merged);
+}
 
 // Geometric segment schedule: after n codes the R-th best of n bounds the admission
 // rate of the next codes by R/n, so each segment admits O(R * growth) candidates.
@@ -396,7 +398,7 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
         const size_t t0 = h->timer.mark(st);
         launch_flat_tables(ds, la, st);
         const uint32_t ntiles = (nb + plan.tq - 1) / plan.tq;
-        h->tile_lut.ensure(size_t(ntiles) * ds.E * plan.tq * tile_entry_bytes(plan.variant));
+        h->tile_lut.ensure(size_t(ntiles) * tile_entries(plan.variant, ds.E) * plan.tq * tile_entry_bytes(plan.variant));
         launch_pack_tiles(plan.variant, plan.filter_shift, h->qlut.p, ds.word_width, ds.E, nb, plan.tq, h->tile_lut.p, st);
         h->timer.span(0, t0, h->timer.mark(st));
         RowSet rows{h->qlut.p, h->tile_lut.p, nullptr, nullptr};
@@ -472,7 +474,7 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         h->stats.kernel_launches = g_launches;
         return;
     }
-    ScanPlan plan = plan_for(h);
+    ScanPlan plan = plan_for(h, false);
     const size_t wb = ds.word_width / 8;
     uint32_t tq = plan.tq;
     h->status.ensure(4);
@@ -1045,7 +1047,7 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
                                h.sel.cand_count.as<uint32_t>(), buf_cap, h.sel.thr_key.as<uint64_t>(), 1, cap, nullptr, st);
                 QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // seed vector goes out of scope
             }
-            h.tile_lut.ensure(size_t(ds.E) * plan.tq * tile_entry_bytes(plan.variant));
+            h.tile_lut.ensure(size_t(tile_entries(plan.variant, ds.E)) * plan.tq * tile_entry_bytes(plan.variant));
             launch_pack_tiles(plan.variant, plan.filter_shift, h.qlut.p, ds.word_width, ds.E, 1, plan.tq, h.tile_lut.p, st);
             RowSet rs{h.qlut.p, h.tile_lut.p, nullptr, bias.as<uint32_t>()};
             bool ok = true;

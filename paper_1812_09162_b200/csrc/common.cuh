@@ -67,6 +67,8 @@ enum ScanVariant : uint32_t {
     VAR_F16X4H_C2 = 5, // same, 2 codes per warp step, 64-row tile (short row groups: IVF)
     VAR_F16X4H_C4 = 6, // same, 4 codes per warp step, 32-row tile
     VAR_F16X4_C4 = 7,  // u8 tables exact in fp16, 4 codes per warp step, 32-row tile (large 8-bit tables: 8x{8})
+    VAR_F16X4_C4M = 9,  // 16x{4,4} scanned as 8x{8}: table j of the tile holds T[2j][b & 15] + T[2j+1][b >> 4] for
+                        // every byte b of the code (pair sums <= 510, exact in fp16) -- half the lookups per code
     VAR_F16X4H_C4D = 8, // as C4 with every entry line stored twice (128 B): code groups 0/2 read the low copy,
                         // 1/3 the high copy, so the four groups of a warp never share a bank
     VAR_COUNT
@@ -105,7 +107,9 @@ struct ScanPlan {
 };
 
 // chooses the variant for a spec (throws config error if nothing fits shared memory)
-ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant);
+// allow_merged: the caller packs its tiles with launch_pack_tiles (flat index, scan shim); the IVF batch path
+// writes tiles itself and does not produce the merged-pair layout.
+ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_merged = false);
 void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
 
 // ---- LUT / calibration / quantization (lut.cu) ----
@@ -138,6 +142,8 @@ void launch_finalize(const uint64_t* lists, const uint32_t* counts_in, uint32_t 
 
 // ---- tile-layout tables (tilepack.cu) ----
 size_t tile_entry_bytes(ScanVariant v);
+// entries of one LUT row in the tile image (the spec's E, except for the merged-pair layout)
+uint32_t tile_entries(ScanVariant v, uint32_t E);
 void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
                        void* out, cudaStream_t stream);
 

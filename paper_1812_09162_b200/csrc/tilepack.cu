@@ -73,8 +73,29 @@ static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
+// 16x{4,4} merged into 8 byte-indexed tables: entry (j, b) = T[2j][b & 15] + T[2j+1][b >> 4] (VAR_F16X4_C4M).
+// grid = (ntiles, 2048 / 64); block = 256; rows [tile*TQ, tile*TQ + TQ) clipped to n_rows; qlut is [row][256] u8.
+__global__ void pack_tiles_merged44_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint32_t tq,
+                                           __half* __restrict__ out) {
+    const uint32_t tile = blockIdx.x, e0 = blockIdx.y * 64;
+    __half* dst = out + (size_t(tile) * 2048 + e0) * tq;
+    for (uint32_t u = threadIdx.x; u < 64 * tq; u += blockDim.x) {
+        const uint32_t r = u % tq, e = e0 + u / tq;
+        const uint32_t row = tile * tq + r, j = e >> 8, b = e & 255u;
+        uint32_t v = 0;
+        if (row < n_rows) {
+            const uint8_t* t = qlut + size_t(row) * 256 + 32 * j;
+            v = uint32_t(t[b & 15u]) + uint32_t(t[16 + (b >> 4)]);
+        }
+        dst[u] = __uint2half_rn(v);
+    }
+}
+
+uint32_t tile_entries(ScanVariant v, uint32_t E) { return v == VAR_F16X4_C4M ? 2048u : E; }
+
 size_t tile_entry_bytes(ScanVariant v) {
     switch (v) {
+    case VAR_F16X4_C4M:
     case VAR_F16X8:
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
@@ -91,6 +112,16 @@ size_t tile_entry_bytes(ScanVariant v) {
 void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, const void* qlut, uint32_t width, uint32_t E,
                        uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     switch (v) {
+    case VAR_F16X4_C4M: {
+        if (width != 8 || E != 256) throw Error(QADC_ERR_CONFIG, "pack_tiles: merged layout is for 16x{4,4}");
+        const uint32_t ntiles = (n_rows + tq - 1) / tq;
+        if (ntiles == 0) return;
+        pack_tiles_merged44_kernel<<<dim3(ntiles, 2048 / 64), 256, 0, stream>>>(static_cast<const uint8_t*>(qlut), n_rows, tq,
+                                                                             static_cast<__half*>(out));
+        ++g_launches;
+        QADC_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
     case VAR_F16X8:
     case VAR_F16X4_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, 0, out, stream);
     case VAR_F16X4H:

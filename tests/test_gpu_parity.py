@@ -814,3 +814,38 @@ def test_concurrent_calls_on_one_handle_serialise():
     assert not errors, errors
     for w, g in zip(want, got):
         assert np.array_equal(w.ids, g.ids) and bits_equal(w.dists, g.dists) and np.array_equal(w.counts, g.counts)
+
+
+@pytest.mark.parametrize("dims,text,variants", [
+    (128, "16x{4,4}", [0, 1, 2, 3, 7, 9]),       # f16x8, f32x2, u16x1, u8x1, f16x4-c4, merged pair tables (default)
+    (96, "12x{6,5,5}", [1, 2, 3, 4, 5, 6, 8]),   # f32x2, u16x1, u8x1, f16x4h, -c2 (default), -c4, -c4d
+    (64, "8x{8,8}", [2, 3, 6]),                  # u16x1, u8x1, f16x4h-c4 (default)
+    (64, "8x{8}", [2, 3, 7]),                    # u16x1, u8x1, f16x4-c4
+])
+def test_every_scan_variant_is_exact(port, dims, text, variants):
+    """Each scan variant that can serve a spec (the planner's default and every fallback layout), forced through
+    qadc_set_option, returns the oracle's result bit for bit -- flat search with a ragged query count, and the
+    variant name reported by the library matches the one requested."""
+    rng = np.random.default_rng(len(text) + dims)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+    n, nq = 70_001, 77
+    pk = qb.pack_list(s, random_codes(s, n, seed=11))
+    queries = (rng.standard_normal((nq, dims)) * 2).astype(np.float32)
+    want = port.flat_search(so, cb, pk, n, queries, r=100, t=400, threads=8)
+    with qb.FlatIndex(s, cb, pk, n) as idx:
+        ran = 0
+        for v in [-1] + variants:
+            idx.set_option("force_variant", v)
+            try:
+                got = idx.search(queries, qb.SearchParams(r=100, t=400))
+            except qb.QadcError as e:  # a layout whose tables do not fit shared memory for this spec
+                assert e.kind == "config", (v, e)
+                continue
+            if v >= 0:
+                assert idx.stats().scan_variant == v
+            assert np.array_equal(got.ids, want[0]), v
+            assert bits_equal(got.dists, want[1]), v
+            assert np.array_equal(got.counts, want[2]), v
+            ran += 1
+        assert ran >= len(variants)  # the default plus all but at most one fallback must run
