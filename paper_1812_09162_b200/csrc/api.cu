@@ -399,7 +399,8 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
         launch_flat_tables(ds, la, st);
         const uint32_t ntiles = (nb + plan.tq - 1) / plan.tq;
         h->tile_lut.ensure(size_t(ntiles) * tile_entries(plan.variant, ds.E) * plan.tq * tile_entry_bytes(plan.variant));
-        launch_pack_tiles(plan.variant, plan.filter_shift, h->qlut.p, ds.word_width, ds.E, nb, plan.tq, h->tile_lut.p, st);
+        launch_pack_tiles(plan.variant, plan.filter_shift, tile_pair_layout(plan.variant, ds), h->qlut.p, ds.word_width, ds.E, nb,
+                          plan.tq, h->tile_lut.p, st);
         h->timer.span(0, t0, h->timer.mark(st));
         RowSet rows{h->qlut.p, h->tile_lut.p, nullptr, nullptr};
         const bool ok = scan_select_flat(h, plan, h->codes.as<uint8_t>(), h->count, h->base_id, rows, nb, p.r, cap,
@@ -578,7 +579,7 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         h->slot_pair.ensure(std::max<size_t>(nslots * 4, 16));
         const size_t t4 = h->timer.mark(st);
         // quantize every tile's rows (padding rows: zero table, no query) and emit the scan's tile image
-        launch_ivf_quantize_pack(plan.variant, plan.filter_shift, ds, h->order.as<uint32_t>(), n_pairs, a, h->luts.as<float>(),
+        launch_ivf_quantize_pack(plan.variant, plan.filter_shift, tile_pair_layout(plan.variant, ds), ds, h->order.as<uint32_t>(), n_pairs, a, h->luts.as<float>(),
                                  h->pmin.as<float>(), h->own_min.as<float>(), h->qparams.as<float>(),
                                  h->pair_rank.as<uint32_t>(), h->tile_base.as<uint32_t>(), tq, ntiles, h->qlut.p,
                                  h->tile_lut.p, h->row_query.as<uint32_t>(), h->row_bias.as<uint32_t>(),
@@ -1048,7 +1049,8 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
                 QADC_CUDA_CHECK(cudaStreamSynchronize(st)); // seed vector goes out of scope
             }
             h.tile_lut.ensure(size_t(tile_entries(plan.variant, ds.E)) * plan.tq * tile_entry_bytes(plan.variant));
-            launch_pack_tiles(plan.variant, plan.filter_shift, h.qlut.p, ds.word_width, ds.E, 1, plan.tq, h.tile_lut.p, st);
+            launch_pack_tiles(plan.variant, plan.filter_shift, tile_pair_layout(plan.variant, ds), h.qlut.p, ds.word_width, ds.E, 1,
+                              plan.tq, h.tile_lut.p, st);
             RowSet rs{h.qlut.p, h.tile_lut.p, nullptr, bias.as<uint32_t>()};
             bool ok = true;
             if (count) {

@@ -195,10 +195,16 @@ struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
 // With four groups of 8 lanes x 8 B, groups 0/2 then only touch banks 0-15 and groups 1/3 banks 16-31: a warp
 // load is exactly two conflict-free wavefronts, where the dense layout needs 2.75 on average (the bank half
 // is the parity of a data-dependent entry index).
-template <int CPW_, bool HIGH = true, bool DUP_ = false>
+// PAIR (32-row tiles, every table 256 entries): tables 2k / 2k+1 share 128-byte lines (low / high half) and the
+// odd code groups of a warp walk each table pair in swapped order (their code bytes are swapped pairwise once per
+// code), so at every step groups 0/2 and groups 1/3 read opposite bank halves: two conflict-free wavefronts per
+// warp load with NO extra shared memory -- what DUP buys with doubled lines, for the specs whose tables are too
+// large to double (8x{8,8}, 8x{8}, merged 16x{4,4}).
+template <int CPW_, bool HIGH = true, bool DUP_ = false, bool PAIR_ = false>
 struct PolF16x4H_T {
     static constexpr int CPW = CPW_;
     static constexpr bool DUP = DUP_;
+    static constexpr bool PAIR = PAIR_;
     static constexpr int QPL = 4, TQ = 128 / CPW, ROWB = (256 / CPW) * (DUP ? 2 : 1),
                          LOG_ROWB = (CPW == 1 ? 8 : CPW == 2 ? 7 : 6) + (DUP ? 1 : 0), LANE_B = 8;
     static constexpr bool EXACT_FILTER = !HIGH;
@@ -236,6 +242,13 @@ using PolF16x4H_C2 = PolF16x4H_T<2>;
 using PolF16x4H_C4 = PolF16x4H_T<4>;
 using PolF16x4_C4 = PolF16x4H_T<4, false>;
 using PolF16x4H_C4D = PolF16x4H_T<4, true, true>;
+using PolF16x4H_C4P = PolF16x4H_T<4, true, false, true>;
+using PolF16x4_C4P = PolF16x4H_T<4, false, false, true>;
+
+template <class P, class = void>
+struct pair_of : std::false_type {};
+template <class P>
+struct pair_of<P, std::void_t<decltype(P::PAIR)>> : std::bool_constant<P::PAIR> {};
 
 template <class P, class = void>
 struct dup_of : std::false_type {};
@@ -472,6 +485,12 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     constexpr uint32_t LPC = 32 / P::CPW;             // lanes per code
     const uint32_t lane_in = lane % LPC, lane_code = lane / LPC;
     const uint32_t lane_off = lane_in * P::LANE_B + (dup_of<P>::value ? (lane_code & 1u) * (P::ROWB / 2) : 0u);
+    // pair layout: even tables sit in the half (group parity), odd tables in the other one; odd groups see their
+    // code with adjacent bytes swapped
+    constexpr bool PAIR = pair_of<P>::value && !G::RUNTIME;
+    const uint32_t lane_off_a = lane_in * P::LANE_B + (lane_code & 1u) * P::ROWB;
+    const uint32_t lane_off_b = lane_in * P::LANE_B + ((lane_code & 1u) ^ 1u) * P::ROWB;
+    const uint32_t swap_sel = (lane_code & 1u) ? 0x2301u : 0x3210u;
     // per-warp queue of flagged pairs: ballot-compacted in the hot loop, resolved 32 at a time
     // 64-bit codes with a compile-time geometry (every named spec): the queue entry carries a copy of the code
     // and a global id reference, so it outlives its stage buffer and job -- the queue is drained only when 32
@@ -596,25 +615,34 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
 #pragma unroll
                             for (int k = 0; k < G::CW; ++k) cw[c][k] = src[k];
                         }
+                        if constexpr (PAIR) {
+#pragma unroll
+                            for (int k = 0; k < G::CW; ++k) cw[c][k] = __byte_perm(cw[c][k], 0u, swap_sel);
+                        }
                         acc[c] = acc0;
                     }
                     static_for<0, G::M>([&](auto J) {
                         constexpr int j = decltype(J)::value;
                         constexpr int bp = G::bitpos(j), nb = G::bits(j);
-                        constexpr int word = bp >> 5, sh = (bp & 31) - P::LOG_ROWB;
-                        constexpr uint32_t mask = ((1u << nb) - 1u) << P::LOG_ROWB;
-                        constexpr uint32_t imm = uint32_t(G::ent_off(j)) * P::ROWB;
+                        constexpr int logl = P::LOG_ROWB + (PAIR ? 1 : 0); // bytes per entry line (pair: two tables per line)
+                        constexpr int word = bp >> 5, sh = (bp & 31) - logl;
+                        constexpr uint32_t mask = ((1u << nb) - 1u) << logl;
+                        constexpr uint32_t imm = uint32_t(G::ent_off(PAIR ? (j & ~1) : j)) * P::ROWB;
+                        static_assert(!PAIR || (nb == 8 && (G::M & 1) == 0 && bp == 8 * j), "pair layout: 8-bit tables only");
 #pragma unroll
                         for (int c = 0; c < CIF; ++c) {
                             const uint32_t x = sh >= 0 ? (cw[c][word] >> (sh >= 0 ? sh : 0)) : (cw[c][word] << (sh < 0 ? -sh : 0));
-                            const uint32_t off = (x & mask) | lane_off;
+                            const uint32_t off = (x & mask) | (PAIR ? ((j & 1) ? lane_off_b : lane_off_a) : lane_off);
                             P::add(acc[c], tile + imm + off);
                         }
                     });
 #pragma unroll
-                    for (int c = 0; c < CIF; ++c)
-                        flag(acc[c], i0 + c * SCAN_WARPS * P::CPW < cnt, i0 + c * SCAN_WARPS * P::CPW, cw[c][0],
-                             cw[c][G::CW > 1 ? 1 : 0]);
+                    for (int c = 0; c < CIF; ++c) {
+                        // the queue keeps the code as stored (the byte swap is an involution)
+                        const uint32_t o0 = PAIR ? __byte_perm(cw[c][0], 0u, swap_sel) : cw[c][0];
+                        const uint32_t o1 = PAIR ? __byte_perm(cw[c][G::CW > 1 ? 1 : 0], 0u, swap_sel) : cw[c][G::CW > 1 ? 1 : 0];
+                        flag(acc[c], i0 + c * SCAN_WARPS * P::CPW < cnt, i0 + c * SCAN_WARPS * P::CPW, o0, o1);
+                    }
                 }
             } else {
                 // runtime geometry: any m / widths / code size that fits; one code per warp step
@@ -810,14 +838,15 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         return launch_one<PolF16x4H_C2, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4:
         if (G655::matches(ds)) return launch_one<PolF16x4H_C4, G655>(plan, ds, args, grid, stream);
-        if (G88::matches(ds)) return launch_one<PolF16x4H_C4, G88>(plan, ds, args, grid, stream);
+        if (G88::matches(ds)) return launch_one<PolF16x4H_C4P, G88>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4D:
         if (G655::matches(ds)) return launch_one<PolF16x4H_C4D, G655>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4D, GeomRT>(plan, ds, args, grid, stream);
-    case VAR_F16X4_C4M: return launch_one<PolF16x4_C4, G8>(plan, ds, args, grid, stream); // the code bytes ARE 8x{8} indices
+    // (G8 / G88 run the pair-interleaved tile layout: tile_pair_layout() in tilepack.cu makes the same choice)
+    case VAR_F16X4_C4M: return launch_one<PolF16x4_C4P, G8>(plan, ds, args, grid, stream); // the code bytes ARE 8x{8} indices
     case VAR_F16X4_C4:
-        if (G8::matches(ds)) return launch_one<PolF16x4_C4, G8>(plan, ds, args, grid, stream);
+        if (G8::matches(ds)) return launch_one<PolF16x4_C4P, G8>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4_C4, GeomRT>(plan, ds, args, grid, stream);
     default: throw Error(QADC_ERR_CONFIG, "scan: bad variant");
     }

@@ -34,7 +34,7 @@ static constexpr int PACK_E = 64;
 // grid = (ntiles, ceil(E / PACK_E)); block = 256.  rows [tile*TQ, tile*TQ + TQ) clipped to n_rows.
 template <class Entry>
 __global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width, uint32_t E, uint32_t n_rows,
-                                  uint32_t tq, uint32_t high_byte /* filter shift */, uint32_t copies,
+                                  uint32_t tq, uint32_t high_byte /* filter shift */, uint32_t copies, bool pair,
                                   Entry* __restrict__ out) {
     extern __shared__ unsigned short panel[]; // [PACK_E][tq + 1]
     const uint32_t tile = blockIdx.x, e0 = blockIdx.y * PACK_E;
@@ -53,32 +53,34 @@ __global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width,
     }
     __syncthreads();
     // copies == 2: every entry line twice back to back (VAR_F16X4H_C4D)
-    Entry* dst = out + (size_t(tile) * E + e0) * tq * copies;
+    // pair: entry lines permuted into the pair-interleaved order (common.cuh: pair_perm)
+    Entry* dst = out + size_t(tile) * E * tq * copies;
     for (uint32_t u = threadIdx.x; u < ne * tq; u += blockDim.x) {
         const uint32_t r = u % tq, el = u / tq;
         const Entry v = tile_convert<Entry>(panel[el * pitch + r], width, high_byte);
-        for (uint32_t c = 0; c < copies; ++c) dst[(size_t(el) * copies + c) * tq + r] = v;
+        const uint32_t line = pair ? pair_perm(e0 + el) : e0 + el;
+        for (uint32_t c = 0; c < copies; ++c) dst[(size_t(line) * copies + c) * tq + r] = v;
     }
 }
 
 template <class Entry>
 static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq, uint32_t hb,
-                        void* out, cudaStream_t stream, uint32_t copies = 1) {
+                        void* out, cudaStream_t stream, uint32_t copies = 1, bool pair = false) {
     const uint32_t ntiles = (n_rows + tq - 1) / tq;
     if (ntiles == 0) return;
     const dim3 grid(ntiles, (E + PACK_E - 1) / PACK_E);
     const size_t smem = size_t(PACK_E) * (tq + 1) * sizeof(unsigned short);
-    pack_tiles_kernel<Entry><<<grid, 256, smem, stream>>>(qlut, width, E, n_rows, tq, hb, copies, static_cast<Entry*>(out));
+    pack_tiles_kernel<Entry><<<grid, 256, smem, stream>>>(qlut, width, E, n_rows, tq, hb, copies, pair, static_cast<Entry*>(out));
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
 // 16x{4,4} merged into 8 byte-indexed tables: entry (j, b) = T[2j][b & 15] + T[2j+1][b >> 4] (VAR_F16X4_C4M).
 // grid = (ntiles, 2048 / 64); block = 256; rows [tile*TQ, tile*TQ + TQ) clipped to n_rows; qlut is [row][256] u8.
-__global__ void pack_tiles_merged44_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint32_t tq,
+__global__ void pack_tiles_merged44_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint32_t tq, bool pair,
                                            __half* __restrict__ out) {
     const uint32_t tile = blockIdx.x, e0 = blockIdx.y * 64;
-    __half* dst = out + (size_t(tile) * 2048 + e0) * tq;
+    __half* base = out + size_t(tile) * 2048 * tq;
     for (uint32_t u = threadIdx.x; u < 64 * tq; u += blockDim.x) {
         const uint32_t r = u % tq, e = e0 + u / tq;
         const uint32_t row = tile * tq + r, j = e >> 8, b = e & 255u;
@@ -87,8 +89,17 @@ __global__ void pack_tiles_merged44_kernel(const uint8_t* __restrict__ qlut, uin
             const uint8_t* t = qlut + size_t(row) * 256 + 32 * j;
             v = uint32_t(t[b & 15u]) + uint32_t(t[16 + (b >> 4)]);
         }
-        dst[u] = __uint2half_rn(v);
+        base[size_t(pair ? pair_perm(e) : e) * tq + r] = __uint2half_rn(v);
     }
+}
+
+bool tile_pair_layout(ScanVariant v, const DevSpec& ds) {
+    if (v == VAR_F16X4_C4M) return true; // the merged view is 8 tables of 256 entries
+    if (v != VAR_F16X4H_C4 && v != VAR_F16X4_C4) return false;
+    if (ds.m == 0 || (ds.m & 1u) || ds.E != ds.m * 256u || ds.code_stride != 8) return false;
+    for (uint32_t j = 0; j < ds.m; ++j)
+        if (ds.bits[j] != 8 || ds.bitpos[j] != 8 * j) return false;
+    return ds.m == 8; // the compile-time geometries that implement it (G8, G88)
 }
 
 uint32_t tile_entries(ScanVariant v, uint32_t E) { return v == VAR_F16X4_C4M ? 2048u : E; }
@@ -109,7 +120,7 @@ size_t tile_entry_bytes(ScanVariant v) {
     }
 }
 
-void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, const void* qlut, uint32_t width, uint32_t E,
+void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, bool pair, const void* qlut, uint32_t width, uint32_t E,
                        uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     switch (v) {
     case VAR_F16X4_C4M: {
@@ -117,16 +128,17 @@ void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, const void* qlut, u
         const uint32_t ntiles = (n_rows + tq - 1) / tq;
         if (ntiles == 0) return;
         pack_tiles_merged44_kernel<<<dim3(ntiles, 2048 / 64), 256, 0, stream>>>(static_cast<const uint8_t*>(qlut), n_rows, tq,
-                                                                             static_cast<__half*>(out));
+                                                                             pair, static_cast<__half*>(out));
         ++g_launches;
         QADC_CUDA_CHECK(cudaGetLastError());
         return;
     }
     case VAR_F16X8:
-    case VAR_F16X4_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, 0, out, stream);
+    case VAR_F16X4_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, 0, out, stream, 1, v == VAR_F16X4_C4 && pair);
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
-    case VAR_F16X4H_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream);
+    case VAR_F16X4H_C4:
+        return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream, 1, v == VAR_F16X4H_C4 && pair);
     case VAR_F16X4H_C4D: return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream, 2);
     case VAR_F32X2: return launch_pack<float>(qlut, width, E, n_rows, tq, 0, out, stream);
     case VAR_U16X1: return launch_pack<unsigned short>(qlut, width, E, n_rows, tq, 0, out, stream);
