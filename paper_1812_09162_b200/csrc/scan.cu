@@ -129,10 +129,18 @@ struct GeomRT {
 //   QPL    rows (queries) owned by one lane;   TQ = 32*QPL rows per tile
 //   ROWB   bytes of one [entry] line in shared memory = TQ * sizeof(entry)
 
-struct PolF16x8 { // u8 tables only
-    static constexpr int CPW = 1;
-    static constexpr int QPL = 8, TQ = 256, ROWB = 512, LOG_ROWB = 9, LANE_B = 16;
-    static constexpr bool EXACT_FILTER = true;
+// fp16 entries, 8 rows per lane (LDS.128).  CPW = 1: the 256-row tile of the u8 16x{4,4} scan.  CPW = 8: eight
+// code groups of 4 lanes against a 32-row tile -- the same tile image as the 4-rows-per-lane variants, but one
+// LDS.128 + 4 HADD2 per 8 rows instead of two LDS.64 + 4 HADD2, i.e. ~30 % fewer instructions per pair for the
+// 2048-entry specs, which are issue bound once the pair layout has removed their bank conflicts.
+// HIGH: conservative filter on the top bits of 16-bit tables (see PolF16x4H_T).  PAIR: pair-interleaved lines.
+template <int CPW_, bool HIGH, bool PAIR_>
+struct PolF16x8_T {
+    static constexpr int CPW = CPW_;
+    static constexpr bool PAIR = PAIR_;
+    static constexpr int QPL = 8, TQ = 256 / CPW, ROWB = 512 / CPW, LOG_ROWB = (CPW == 1 ? 9 : CPW == 2 ? 8 : CPW == 4 ? 7 : 6),
+                         LANE_B = 16;
+    static constexpr bool EXACT_FILTER = !HIGH;
     using Entry = __half;
     struct Acc {
         __half2 h[4];
@@ -160,8 +168,11 @@ struct PolF16x8 { // u8 tables only
     __device__ static float value(const Acc& a, int s) {
         return (s & 1) ? __high2float(a.h[s >> 1]) : __low2float(a.h[s >> 1]);
     }
-    static constexpr float BIG = 30000.0f, HALF = 0.5f;
+    static constexpr float BIG = 30000.0f, HALF = HIGH ? 1.0f : 0.5f;
 };
+using PolF16x8 = PolF16x8_T<1, false, false>;
+using PolF16x8_C8P = PolF16x8_T<8, false, true>;   // exact, 8-bit tables of 256 entries (8x{8}, merged 16x{4,4})
+using PolF16x8H_C8P = PolF16x8_T<8, true, true>;   // conservative, 16-bit tables of 256 entries (8x{8,8})
 
 struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
     static constexpr int CPW = 1;
@@ -838,15 +849,15 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         return launch_one<PolF16x4H_C2, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4:
         if (G655::matches(ds)) return launch_one<PolF16x4H_C4, G655>(plan, ds, args, grid, stream);
-        if (G88::matches(ds)) return launch_one<PolF16x4H_C4P, G88>(plan, ds, args, grid, stream);
+        if (G88::matches(ds)) return launch_one<PolF16x8H_C8P, G88>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4D:
         if (G655::matches(ds)) return launch_one<PolF16x4H_C4D, G655>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4D, GeomRT>(plan, ds, args, grid, stream);
     // (G8 / G88 run the pair-interleaved tile layout: tile_pair_layout() in tilepack.cu makes the same choice)
-    case VAR_F16X4_C4M: return launch_one<PolF16x4_C4P, G8>(plan, ds, args, grid, stream); // the code bytes ARE 8x{8} indices
+    case VAR_F16X4_C4M: return launch_one<PolF16x8_C8P, G8>(plan, ds, args, grid, stream); // the code bytes ARE 8x{8} indices
     case VAR_F16X4_C4:
-        if (G8::matches(ds)) return launch_one<PolF16x4_C4P, G8>(plan, ds, args, grid, stream);
+        if (G8::matches(ds)) return launch_one<PolF16x8_C8P, G8>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4_C4, GeomRT>(plan, ds, args, grid, stream);
     default: throw Error(QADC_ERR_CONFIG, "scan: bad variant");
     }
