@@ -134,12 +134,13 @@ struct GeomRT {
 // LDS.128 + 4 HADD2 per 8 rows instead of two LDS.64 + 4 HADD2, i.e. ~30 % fewer instructions per pair for the
 // 2048-entry specs, which are issue bound once the pair layout has removed their bank conflicts.
 // HIGH: conservative filter on the top bits of 16-bit tables (see PolF16x4H_T).  PAIR: pair-interleaved lines.
-template <int CPW_, bool HIGH, bool PAIR_>
+template <int CPW_, bool HIGH, bool PAIR_, bool DUP_ = false>
 struct PolF16x8_T {
     static constexpr int CPW = CPW_;
     static constexpr bool PAIR = PAIR_;
-    static constexpr int QPL = 8, TQ = 256 / CPW, ROWB = 512 / CPW, LOG_ROWB = (CPW == 1 ? 9 : CPW == 2 ? 8 : CPW == 4 ? 7 : 6),
-                         LANE_B = 16;
+    static constexpr bool DUP = DUP_; // every entry line twice, odd code groups read the second copy (see PolF16x4H_T)
+    static constexpr int QPL = 8, TQ = 256 / CPW, ROWB = (512 / CPW) * (DUP ? 2 : 1),
+                         LOG_ROWB = (CPW == 1 ? 9 : CPW == 2 ? 8 : CPW == 4 ? 7 : 6) + (DUP ? 1 : 0), LANE_B = 16;
     static constexpr bool EXACT_FILTER = !HIGH;
     using Entry = __half;
     struct Acc {
@@ -852,6 +853,8 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         if (G88::matches(ds)) return launch_one<PolF16x8H_C8P, G88>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4D:
+        // (the 8-rows-per-lane twin, PolF16x8H_C8D, is 8 % faster on a flat scan but 50 % slower on the IVF
+        // workload this variant exists for: with ~1 % of the warp steps flagged, 8 ballots per flagged step hurt)
         if (G655::matches(ds)) return launch_one<PolF16x4H_C4D, G655>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4D, GeomRT>(plan, ds, args, grid, stream);
     // (G8 / G88 run the pair-interleaved tile layout: tile_pair_layout() in tilepack.cu makes the same choice)
