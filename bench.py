@@ -466,14 +466,16 @@ def main():
                     "note": "codes are streamed once per query tile and reused from shared memory, so algorithmic bytes "
                             "exceed DRAM traffic; the kernel's real ceiling is the shared-memory pipe (profiles/)"}
         # the kernel's operative ceiling: table-lookup bytes through the shared-memory pipe (128 B/clk/SM)
-        entry_bytes = {0: 2, 1: 4, 2: 2, 3: 1, 4: 2, 5: 2, 6: 2, 7: 2}.get(int(idx.stats().scan_variant), 2)
+        variant = int(idx.stats().scan_variant)
+        entry_bytes = {0: 2, 1: 4, 2: 2, 3: 1, 4: 2, 5: 2, 6: 2, 7: 2, 8: 2, 9: 2}.get(variant, 2)
+        lookups = spec.m // 2 if variant == 9 else spec.m  # merged 16x{4,4}: one lookup per code byte (pair sums)
         sm_clock = (clk.get("sm_mhz") or 1965) * 1e6
         prop = torch.cuda.get_device_properties(dev)
         smem_peak = 128.0 * prop.multi_processor_count * sm_clock / 1e9
-        smem_ach = (st_acc["pairs"] * spec.m * entry_bytes / scan_s) / 1e9 if scan_s > 0 else None
+        smem_ach = (st_acc["pairs"] * lookups * entry_bytes / scan_s) / 1e9 if scan_s > 0 else None
         roofline["smem"] = {"bound": "shared-memory pipe", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
                             "frac": smem_ach / smem_peak if smem_ach else None,
-                            "bytes_per_pair": spec.m * entry_bytes,
+                            "bytes_per_pair": lookups * entry_bytes,
                             "peak_source": "128 B/clk/SM x SMs x sampled SM clock"}
         cpu_out = None
         if world == 1 and not args.no_cpu_baseline:

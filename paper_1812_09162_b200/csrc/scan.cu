@@ -694,9 +694,9 @@ const char* variant_name(uint32_t v) {
     case VAR_U8X1: return "u8x1 (high-byte filter, 32-query tile)";
     case VAR_F16X4H: return "f16x4h (u16 tables, fp16 high-byte filter + exact re-evaluation, 128-query tile, LDS.64)";
     case VAR_F16X4H_C2: return "f16x4h-c2 (as f16x4h, 2 codes per warp step, 64-row tile)";
-    case VAR_F16X4H_C4: return "f16x4h-c4 (as f16x4h, 4 codes per warp step, 32-row tile)";
-    case VAR_F16X4_C4: return "f16x4-c4 (u8 tables exact in fp16, 4 codes per warp step, 32-row tile)";
-    case VAR_F16X4_C4M: return "f16x4-c4m (16x{4,4} as 8 byte-indexed tables of pair sums, 4 codes per warp step, 32-row tile)";
+    case VAR_F16X4H_C4: return "f16x4h-c4 (as f16x4h, 32-row tile; 8x{8,8}: pair-interleaved lines, LDS.128, 8 codes per warp step)";
+    case VAR_F16X4_C4: return "f16x4-c4 (u8 tables exact in fp16, 32-row tile; 8x{8}: pair-interleaved lines, LDS.128, 8 codes per warp step)";
+    case VAR_F16X4_C4M: return "f16x4-c4m (16x{4,4} as 8 byte-indexed tables of pair sums; 32-row pair-interleaved tile, LDS.128, 8 codes per warp step)";
     case VAR_F16X4H_C4D: return "f16x4h-c4d (as f16x4h-c4, entry lines duplicated: bank-conflict-free)";
     }
     return "?";

@@ -20,3 +20,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"ivf_|probe_|
 $CMD5 > gpurun_out/${TAG}_plain_c5b.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:scan_kernel -s 6 -c 1 -o gpurun_out/${TAG}_scan_c5 $CMD5 > gpurun_out/${TAG}_ncu_full_c5.log 2>&1
 ls -la gpurun_out | grep ${TAG}_ | tail -20
+# summaries are produced here (the .ncu-rep files together exceed what gpurun copies back) and the reports dropped
+python tools/summarize_profiles.py ${TAG} && mkdir -p gpurun_out/${TAG}_summaries && cp profiles/${TAG}_* gpurun_out/${TAG}_summaries/
+rm -f gpurun_out/${TAG}_scan_*.ncu-rep
