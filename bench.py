@@ -467,8 +467,9 @@ def main():
                             "exceed DRAM traffic; the kernel's real ceiling is the shared-memory pipe (profiles/)"}
         # the kernel's operative ceiling: table-lookup bytes through the shared-memory pipe (128 B/clk/SM)
         variant = int(idx.stats().scan_variant)
-        entry_bytes = {0: 2, 1: 4, 2: 2, 3: 1, 4: 2, 5: 2, 6: 2, 7: 2, 8: 2, 9: 2}.get(variant, 2)
-        lookups = spec.m // 2 if variant == 9 else spec.m  # merged 16x{4,4}: one lookup per code byte (pair sums)
+        entry_bytes = {0: 2, 1: 4, 2: 2, 3: 1, 4: 2, 5: 2, 6: 2, 7: 2, 8: 2, 9: 2, 10: 2}.get(variant, 2)
+        # merged layouts: 16x{4,4} -> one lookup per code byte (pair sums); 12x{6,5,5} -> two lookups per 16-bit word
+        lookups = spec.m // 2 if variant == 9 else spec.m * 2 // 3 if variant == 10 else spec.m
         sm_clock = (clk.get("sm_mhz") or 1965) * 1e6
         prop = torch.cuda.get_device_properties(dev)
         smem_peak = 128.0 * prop.multi_processor_count * sm_clock / 1e9

@@ -67,10 +67,13 @@ enum ScanVariant : uint32_t {
     VAR_F16X4H_C2 = 5, // same, 2 codes per warp step, 64-row tile (short row groups: IVF)
     VAR_F16X4H_C4 = 6, // same, 4 codes per warp step, 32-row tile
     VAR_F16X4_C4 = 7,  // u8 tables exact in fp16, 4 codes per warp step, 32-row tile (large 8-bit tables: 8x{8})
-    VAR_F16X4_C4M = 9,  // 16x{4,4} scanned as 8x{8}: table j of the tile holds T[2j][b & 15] + T[2j+1][b >> 4] for
-                        // every byte b of the code (pair sums <= 510, exact in fp16) -- half the lookups per code
     VAR_F16X4H_C4D = 8, // as C4 with every entry line stored twice (128 B): code groups 0/2 read the low copy,
                         // 1/3 the high copy, so the four groups of a warp never share a bank
+    VAR_F16X4_C4M = 9,  // 16x{4,4} scanned as 8x{8}: table j of the tile holds T[2j][b & 15] + T[2j+1][b >> 4] for
+                        // every byte b of the code (pair sums <= 510, exact in fp16) -- half the lookups per code
+    VAR_F16X4H_C8Q = 10, // 12x{6,5,5} scanned as 8 lookups per code: per 16-bit word one 6-bit table and one 1024-entry
+                         // table of (5,5) pair sums; 16-row tile whose 128-byte lines hold the same entry of the four
+                         // words' tables (quad-interleaved); code groups walk the words in rotated order
     VAR_COUNT
 };
 
