@@ -187,6 +187,7 @@ struct PolF16x8_T {
 using PolF16x8 = PolF16x8_T<1, false, false>;
 using PolF16x8_C8P = PolF16x8_T<8, false, true>;   // exact, 8-bit tables of 256 entries (8x{8}, merged 16x{4,4})
 using PolF16x8H_C8P = PolF16x8_T<8, true, true>;   // conservative, 16-bit tables of 256 entries (8x{8,8})
+using PolF16x8H_C8D = PolF16x8_T<8, true, false, true>; // conservative, duplicated lines (E <= 512: IVF 12x{6,5,5})
 
 struct PolF32x2 { // u16 (or u8) tables, fp32 exact below 2^24
     static constexpr int CPW = 1;
@@ -651,6 +652,29 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
             auto flag = [&](const typename P::Acc& acc, bool live, uint32_t i, uint32_t c0, uint32_t c1) {
                 const bool h = live && P::any(acc);
                 if (__any_sync(0xffffffffu, h)) {
+                    if constexpr (COPY) {
+                        // sparse flags: one OR-reduction tells which of the lane's QPL slots is flagged anywhere in
+                        // the warp, and only those (typically one) pay a ballot
+                        uint32_t hits = 0;
+#pragma unroll
+                        for (int sl = 0; sl < P::QPL; ++sl) hits |= (h && P::hit(acc, sl)) ? (1u << sl) : 0u;
+                        uint32_t live_slots = __reduce_or_sync(0xffffffffu, hits);
+                        while (live_slots) {
+                            const uint32_t sl = __ffs(live_slots) - 1;
+                            live_slots &= live_slots - 1;
+                            const bool hs = (hits >> sl) & 1u;
+                            const uint32_t m = __ballot_sync(0xffffffffu, hs);
+                            if (qn + 32 > WQ_CAP) flush_copy();
+                            if (hs) {
+                                const uint32_t slot = qn + __popc(m & lanemask_lt);
+                                wq_row[slot] = job.row_begin + lane_in * P::QPL + sl;
+                                wq_code[slot] = make_uint2(c0, c1);
+                                wq_ref[slot] = a->ids ? job.ids_off + first + i : uint64_t(job.id_base + first + i);
+                            }
+                            qn += __popc(m);
+                        }
+                        return;
+                    }
 #pragma unroll
                     for (int sl = 0; sl < P::QPL; ++sl) {
                         const bool hs = h && P::hit(acc, sl);
@@ -952,7 +976,7 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
     case VAR_F16X4H_C4D:
         // (the 8-rows-per-lane twin, PolF16x8H_C8D, is 8 % faster on a flat scan but 50 % slower on the IVF
         // workload this variant exists for: with ~1 % of the warp steps flagged, 8 ballots per flagged step hurt)
-        if (G655::matches(ds)) return launch_one<PolF16x4H_C4D, G655>(plan, ds, args, grid, stream);
+        if (G655::matches(ds)) return launch_one<PolF16x8H_C8D, G655>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4D, GeomRT>(plan, ds, args, grid, stream);
     // (G8 / G88 run the pair-interleaved tile layout: tile_pair_layout() in tilepack.cu makes the same choice)
     case VAR_F16X4_C4M: return launch_one<PolF16x8_C8P, G8>(plan, ds, args, grid, stream); // the code bytes ARE 8x{8} indices
