@@ -652,51 +652,37 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
             auto flag = [&](const typename P::Acc& acc, bool live, uint32_t i, uint32_t c0, uint32_t c1) {
                 const bool h = live && P::any(acc);
                 if (__any_sync(0xffffffffu, h)) {
-                    if constexpr (COPY) {
-                        // sparse flags: one OR-reduction tells which of the lane's QPL slots is flagged anywhere in
-                        // the warp, and only those (typically one) pay a ballot
-                        uint32_t hits = 0;
+                    // sparse flags: one OR-reduction tells which of the lane's QPL slots is flagged anywhere in
+                    // the warp, and only those (typically one) pay a ballot
+                    uint32_t hits = 0;
 #pragma unroll
-                        for (int sl = 0; sl < P::QPL; ++sl) hits |= (h && P::hit(acc, sl)) ? (1u << sl) : 0u;
-                        uint32_t live_slots = __reduce_or_sync(0xffffffffu, hits);
-                        while (live_slots) {
-                            const uint32_t sl = __ffs(live_slots) - 1;
-                            live_slots &= live_slots - 1;
-                            const bool hs = (hits >> sl) & 1u;
-                            const uint32_t m = __ballot_sync(0xffffffffu, hs);
-                            if (qn + 32 > WQ_CAP) flush_copy();
-                            if (hs) {
-                                const uint32_t slot = qn + __popc(m & lanemask_lt);
-                                wq_row[slot] = job.row_begin + lane_in * P::QPL + sl;
+                    for (int sl = 0; sl < P::QPL; ++sl) hits |= (h && P::hit(acc, sl)) ? (1u << sl) : 0u;
+                    uint32_t live_slots = __reduce_or_sync(0xffffffffu, hits);
+                    while (live_slots) {
+                        const uint32_t sl = __ffs(live_slots) - 1;
+                        live_slots &= live_slots - 1;
+                        const bool hs = (hits >> sl) & 1u;
+                        const uint32_t m = __ballot_sync(0xffffffffu, hs);
+                        if (qn + 32 > WQ_CAP) {
+                            if constexpr (COPY) flush_copy();
+                            else flush();
+                        }
+                        if (hs) {
+                            const uint32_t slot = qn + __popc(m & lanemask_lt);
+                            wq_row[slot] = job.row_begin + lane_in * P::QPL + sl;
+                            if constexpr (COPY) { // the drain re-evaluates from the code: no accumulator value needed
                                 wq_code[slot] = make_uint2(c0, c1);
                                 wq_ref[slot] = a->ids ? job.ids_off + first + i : uint64_t(job.id_base + first + i);
-                            }
-                            qn += __popc(m);
-                        }
-                        return;
-                    }
+                            } else {
+                                float v = 0.0f;
 #pragma unroll
-                    for (int sl = 0; sl < P::QPL; ++sl) {
-                        const bool hs = h && P::hit(acc, sl);
-                        const uint32_t m = __ballot_sync(0xffffffffu, hs);
-                        if (m) {
-                            if (qn + 32 > WQ_CAP) {
-                                if constexpr (COPY) flush_copy();
-                                else flush();
+                                for (int k = 0; k < P::QPL; ++k)
+                                    if (uint32_t(k) == sl) v = P::value(acc, k);
+                                wq_val[slot] = v;
+                                wq_idx[slot] = i;
                             }
-                            if (hs) {
-                                const uint32_t slot = qn + __popc(m & lanemask_lt);
-                                wq_row[slot] = job.row_begin + lane_in * P::QPL + sl;
-                                wq_val[slot] = P::value(acc, sl);
-                                if constexpr (COPY) {
-                                    wq_code[slot] = make_uint2(c0, c1);
-                                    wq_ref[slot] = a->ids ? job.ids_off + first + i : uint64_t(job.id_base + first + i);
-                                } else {
-                                    wq_idx[slot] = i;
-                                }
-                            }
-                            qn += __popc(m);
                         }
+                        qn += __popc(m);
                     }
                 }
             };
