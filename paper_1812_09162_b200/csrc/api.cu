@@ -535,13 +535,13 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
             try {
                 if (plan_scan(ds, h->device, int(VAR_F16X4H_C4D)).tile_bufs == 2) {
                     c32 = VAR_F16X4H_C4D;
-                    rate32 = 1.15;
+                    rate32 = 1.25;
                 }
             } catch (const Error&) {
             }
             const ScanVariant cand[3] = {VAR_F16X4H, VAR_F16X4H_C2, c32};
             const uint32_t rows[3] = {128, 64, 32};
-            const double per_pair[3] = {1.0 / 1.13, 1.0 / 1.18, 1.0 / rate32}; // measured flat-scan rates (T pairs/s)
+            const double per_pair[3] = {1.0 / 1.13, 1.0 / 1.30, 1.0 / rate32}; // measured flat-scan rates (T pairs/s)
             double best = -1.0;
             int pick = int(plan.variant) - int(VAR_F16X4H);
             for (int v = 0; v < 3; ++v) {
