@@ -128,14 +128,19 @@ struct GeomRT {
 
 // 12x{6,5,5} seen as 4 words x {6-bit table, 1024-entry table of (5,5) pair sums}: 1088 quad lines per tile
 // (VAR_F16X4H_C8Q).  The hot loop has its own branch; exact re-evaluation uses the original geometry.
-struct GeomQ655 {
+// (12x{6,6,4} has the same merged view: 6 bits, then 10 bits = the 6-bit and the 4-bit subcode.)
+template <class ExactG>
+struct GeomQ6_10 {
     static constexpr bool RUNTIME = false;
     static constexpr int CW = 2, E = 1024 + 64, M = 8, STRIDE = 8, WORD = 16;
-    using Exact = GeomCT<16, 4, 6, 5, 5>;
+    using Exact = ExactG;
     __host__ __device__ static constexpr int bits(int) { return 0; }
     __host__ __device__ static constexpr int bitpos(int) { return 0; }
     __host__ __device__ static constexpr int ent_off(int) { return 0; }
 };
+
+using GeomQ655 = GeomQ6_10<GeomCT<16, 4, 6, 5, 5>>;
+using GeomQ664 = GeomQ6_10<GeomCT<16, 4, 6, 6, 4>>;
 
 // ------------------------------------------------------------------ policies --
 // A policy fixes how table entries live in shared memory and how a lane accumulates.
@@ -843,7 +848,8 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_
             set(VAR_F16X4_C4, PolF16x4_C4::TQ, smem_need<PolF16x4_C4>(ds.E));
             break;
         case VAR_F16X4H_C8Q:
-            if (!allow_merged || !G655::matches(ds)) throw Error(QADC_ERR_CONFIG, "scan: f16x4h-c8q is the flat 12x{6,5,5} layout");
+            if (!allow_merged || !(G655::matches(ds) || G664::matches(ds)))
+                throw Error(QADC_ERR_CONFIG, "scan: f16x4h-c8q is the flat 12x{6,5,5} / 12x{6,6,4} layout");
             set(VAR_F16X4H_C8Q, PolQ655::TQ, smem_need<PolQ655>(GeomQ655::E));
             break;
         case VAR_F16X4_C4M:
@@ -879,7 +885,7 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_
     else if (u8 && fits(smem_need<PolF16x8>(ds.E))) set(VAR_F16X8, PolF16x8::TQ, smem_need<PolF16x8>(ds.E));
     else if (u8 && fits(smem_need<PolF16x4_C4>(ds.E))) set(VAR_F16X4_C4, PolF16x4_C4::TQ, smem_need<PolF16x4_C4>(ds.E));
     // flat 12x{6,5,5}: the merged view (8 lookups per code instead of 12) -- measured 1.30 -> 1.78 T pairs/s on C2
-    else if (!u8 && allow_merged && G655::matches(ds) && fits(smem_need<PolQ655>(GeomQ655::E)))
+    else if (!u8 && allow_merged && (G655::matches(ds) || G664::matches(ds)) && fits(smem_need<PolQ655>(GeomQ655::E)))
         set(VAR_F16X4H_C8Q, PolQ655::TQ, smem_need<PolQ655>(GeomQ655::E));
     // 64-row tiles first: measured 4 % faster than 128-row tiles on the flat 12x{6,5,5} scan (two tile buffers
     // fit, and two codes per warp step halve the per-code bookkeeping); 32-row tiles pay ~37 % extra
@@ -958,7 +964,9 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         if (G655::matches(ds)) return launch_one<PolF16x4H_C4, G655>(plan, ds, args, grid, stream);
         if (G88::matches(ds)) return launch_one<PolF16x8H_C8P, G88>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
-    case VAR_F16X4H_C8Q: return launch_one<PolQ655, GeomQ655>(plan, ds, args, grid, stream);
+    case VAR_F16X4H_C8Q:
+        if (G664::matches(ds)) return launch_one<PolQ655, GeomQ664>(plan, ds, args, grid, stream);
+        return launch_one<PolQ655, GeomQ655>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4D:
         // (the 8-rows-per-lane twin, PolF16x8H_C8D, is 8 % faster on a flat scan but 50 % slower on the IVF
         // workload this variant exists for: with ~1 % of the warp steps flagged, 8 ballots per flagged step hurt)
