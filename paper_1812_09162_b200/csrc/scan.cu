@@ -128,19 +128,22 @@ struct GeomRT {
 
 // 12x{6,5,5} seen as 4 words x {6-bit table, 1024-entry table of (5,5) pair sums}: 1088 quad lines per tile
 // (VAR_F16X4H_C8Q).  The hot loop has its own branch; exact re-evaluation uses the original geometry.
-// (12x{6,6,4} has the same merged view: 6 bits, then 10 bits = the 6-bit and the 4-bit subcode.)
-template <class ExactG>
+// (12x{6,6,4} has the same merged view: 6 bits, then 10 bits = the 6-bit and the 4-bit subcode; 12x{5,5,5}: 5 bits,
+// then 10 bits.)  B0 = bits of a word's first subcode.
+template <class ExactG, int B0_>
 struct GeomQ6_10 {
     static constexpr bool RUNTIME = false;
-    static constexpr int CW = 2, E = 1024 + 64, M = 8, STRIDE = 8, WORD = 16;
+    static constexpr int B0 = B0_;
+    static constexpr int CW = 2, E = 1024 + (1 << B0), M = 8, STRIDE = 8, WORD = 16;
     using Exact = ExactG;
     __host__ __device__ static constexpr int bits(int) { return 0; }
     __host__ __device__ static constexpr int bitpos(int) { return 0; }
     __host__ __device__ static constexpr int ent_off(int) { return 0; }
 };
 
-using GeomQ655 = GeomQ6_10<GeomCT<16, 4, 6, 5, 5>>;
-using GeomQ664 = GeomQ6_10<GeomCT<16, 4, 6, 6, 4>>;
+using GeomQ655 = GeomQ6_10<GeomCT<16, 4, 6, 5, 5>, 6>;
+using GeomQ664 = GeomQ6_10<GeomCT<16, 4, 6, 6, 4>, 6>;
+using GeomQ555 = GeomQ6_10<GeomCT<16, 4, 5, 5, 5>, 5>;
 
 // ------------------------------------------------------------------ policies --
 // A policy fixes how table entries live in shared memory and how a lane accumulates.
@@ -724,11 +727,12 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                             const uint32_t hi = (quad_r & 2u) ? cw[c][0] : cw[c][1];
                             const uint32_t sh = (quad_r & 1u) * 16u;
                             const uint32_t wa = __funnelshift_r(lo, hi, sh), wb = __funnelshift_r(hi, lo, sh);
-                            constexpr uint32_t m10 = 1023u << 7, m6 = 63u << 7, base6 = 1024u * 128u;
-                            P::add(acc[c], tile + (((wa << 1) & m10) | quad_off[0]));
-                            P::add(acc[c], tile + (((wa >> 15) & m10) | quad_off[1]));
-                            P::add(acc[c], tile + (((wb << 1) & m10) | quad_off[2]));
-                            P::add(acc[c], tile + (((wb >> 15) & m10) | quad_off[3]));
+                            constexpr int b0 = G::RUNTIME ? 6 : (G::E - 1024 == 32 ? 5 : 6); // bits of a word's first subcode
+                            constexpr uint32_t m10 = 1023u << 7, m6 = ((1u << b0) - 1u) << 7, base6 = 1024u * 128u;
+                            P::add(acc[c], tile + (((wa << (7 - b0)) & m10) | quad_off[0]));
+                            P::add(acc[c], tile + (((wa >> (9 + b0)) & m10) | quad_off[1]));
+                            P::add(acc[c], tile + (((wb << (7 - b0)) & m10) | quad_off[2]));
+                            P::add(acc[c], tile + (((wb >> (9 + b0)) & m10) | quad_off[3]));
                             P::add(acc[c], tile + base6 + (((wa << 7) & m6) | quad_off[0]));
                             P::add(acc[c], tile + base6 + (((wa >> 9) & m6) | quad_off[1]));
                             P::add(acc[c], tile + base6 + (((wb << 7) & m6) | quad_off[2]));
@@ -848,8 +852,8 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_
             set(VAR_F16X4_C4, PolF16x4_C4::TQ, smem_need<PolF16x4_C4>(ds.E));
             break;
         case VAR_F16X4H_C8Q:
-            if (!allow_merged || !(G655::matches(ds) || G664::matches(ds)))
-                throw Error(QADC_ERR_CONFIG, "scan: f16x4h-c8q is the flat 12x{6,5,5} / 12x{6,6,4} layout");
+            if (!allow_merged || !(G655::matches(ds) || G664::matches(ds) || G555::matches(ds)))
+                throw Error(QADC_ERR_CONFIG, "scan: f16x4h-c8q is the flat 12x{6,5,5} / 12x{6,6,4} / 12x{5,5,5} layout");
             set(VAR_F16X4H_C8Q, PolQ655::TQ, smem_need<PolQ655>(GeomQ655::E));
             break;
         case VAR_F16X4_C4M:
@@ -885,7 +889,8 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_
     else if (u8 && fits(smem_need<PolF16x8>(ds.E))) set(VAR_F16X8, PolF16x8::TQ, smem_need<PolF16x8>(ds.E));
     else if (u8 && fits(smem_need<PolF16x4_C4>(ds.E))) set(VAR_F16X4_C4, PolF16x4_C4::TQ, smem_need<PolF16x4_C4>(ds.E));
     // flat 12x{6,5,5}: the merged view (8 lookups per code instead of 12) -- measured 1.30 -> 1.78 T pairs/s on C2
-    else if (!u8 && allow_merged && (G655::matches(ds) || G664::matches(ds)) && fits(smem_need<PolQ655>(GeomQ655::E)))
+    else if (!u8 && allow_merged && (G655::matches(ds) || G664::matches(ds) || G555::matches(ds)) &&
+             fits(smem_need<PolQ655>(GeomQ655::E)))
         set(VAR_F16X4H_C8Q, PolQ655::TQ, smem_need<PolQ655>(GeomQ655::E));
     // 64-row tiles first: measured 4 % faster than 128-row tiles on the flat 12x{6,5,5} scan (two tile buffers
     // fit, and two codes per warp step halve the per-code bookkeeping); 32-row tiles pay ~37 % extra
@@ -966,6 +971,7 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C8Q:
         if (G664::matches(ds)) return launch_one<PolQ655, GeomQ664>(plan, ds, args, grid, stream);
+        if (G555::matches(ds)) return launch_one<PolQ655, GeomQ555>(plan, ds, args, grid, stream);
         return launch_one<PolQ655, GeomQ655>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4D:
         // (the 8-rows-per-lane twin, PolF16x8H_C8D, is 8 % faster on a flat scan but 50 % slower on the IVF

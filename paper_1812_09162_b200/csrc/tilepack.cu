@@ -105,19 +105,20 @@ bool tile_pair_layout(ScanVariant v, const DevSpec& ds) {
 // 12x{6,5,5} merged for VAR_F16X4H_C8Q: per tile of 16 rows, 1024 + 64 lines of 128 bytes; line i of the first
 // section holds, for each word t = 0..3 (32 bytes = 16 rows each), (T[3t+1][i & 31] >> s) + (T[3t+2][i >> 5] >> s);
 // line i of the second section holds T[3t][i] >> s.  qlut is [row][512] u16; s = the plan's filter shift (6).
-// b1 = bits of the middle subcode (5 for {6,5,5}, 6 for {6,6,4}); a word's tables are 64, 2^b1 and 2^(10-b1) entries.
+// b0 / b1 = bits of a word's first / middle subcode ({6,5,5}: 6, 5; {6,6,4}: 6, 6; {5,5,5}: 5, 5); the word's tables
+// hold 2^b0, 2^b1 and 2^(10-b1) entries and the tile 1024 + 2^b0 quad lines.
 __global__ void pack_tiles_merged655_kernel(const uint16_t* __restrict__ qlut, uint32_t n_rows, uint32_t shift,
-                                            uint32_t b1, uint32_t E, __half* __restrict__ out) {
-    const uint32_t tile = blockIdx.x;
-    __half* base = out + size_t(tile) * 1088 * 64;
-    for (uint32_t u = blockIdx.y * blockDim.x + threadIdx.x; u < 1088u * 64u; u += gridDim.y * blockDim.x) {
+                                            uint32_t b0, uint32_t b1, uint32_t E, __half* __restrict__ out) {
+    const uint32_t tile = blockIdx.x, lines = 1024u + (1u << b0);
+    __half* base = out + size_t(tile) * lines * 64;
+    for (uint32_t u = blockIdx.y * blockDim.x + threadIdx.x; u < lines * 64u; u += gridDim.y * blockDim.x) {
         const uint32_t line = u >> 6, t = (u >> 4) & 3u, r = u & 15u;
         const uint32_t row = tile * 16 + r;
         uint32_t v = 0;
         if (row < n_rows) {
             const uint16_t* q = qlut + size_t(row) * E + t * (E / 4);
-            const uint32_t n1 = 1u << b1;
-            v = line < 1024 ? (uint32_t(q[64 + (line & (n1 - 1u))]) >> shift) + (uint32_t(q[64 + n1 + (line >> b1)]) >> shift)
+            const uint32_t n0 = 1u << b0, n1 = 1u << b1;
+            v = line < 1024 ? (uint32_t(q[n0 + (line & (n1 - 1u))]) >> shift) + (uint32_t(q[n0 + n1 + (line >> b1)]) >> shift)
                             : uint32_t(q[line - 1024]) >> shift;
         }
         base[u] = __uint2half_rn(v);
@@ -125,7 +126,7 @@ __global__ void pack_tiles_merged655_kernel(const uint16_t* __restrict__ qlut, u
 }
 
 uint32_t tile_entries(ScanVariant v, uint32_t E) {
-    return v == VAR_F16X4_C4M ? 2048u : v == VAR_F16X4H_C8Q ? 1088u : E;
+    return v == VAR_F16X4_C4M ? 2048u : v == VAR_F16X4H_C8Q ? (E == 384 ? 1056u : 1088u) : E;
 }
 
 size_t tile_entry_bytes(ScanVariant v) {
@@ -149,13 +150,13 @@ void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, bool pair, const vo
                        uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     switch (v) {
     case VAR_F16X4H_C8Q: {
-        if (width != 16 || (E != 512 && E != 576) || tq != 16)
-            throw Error(QADC_ERR_CONFIG, "pack_tiles: quad layout is for 12x{6,5,5} / 12x{6,6,4}");
+        if (width != 16 || (E != 512 && E != 576 && E != 384) || tq != 16)
+            throw Error(QADC_ERR_CONFIG, "pack_tiles: quad layout is for 12x{6,5,5} / 12x{6,6,4} / 12x{5,5,5}");
         const uint32_t ntiles = (n_rows + tq - 1) / tq;
         if (ntiles == 0) return;
         pack_tiles_merged655_kernel<<<dim3(ntiles, 17), 256, 0, stream>>>(static_cast<const uint16_t*>(qlut), n_rows,
-                                                                       filter_shift, E == 512 ? 5u : 6u, E,
-                                                                       static_cast<__half*>(out));
+                                                                       filter_shift, E == 384 ? 5u : 6u,
+                                                                       E == 576 ? 6u : 5u, E, static_cast<__half*>(out));
         ++g_launches;
         QADC_CUDA_CHECK(cudaGetLastError());
         return;
