@@ -851,3 +851,25 @@ def test_every_scan_variant_is_exact(port, dims, text, variants):
             assert np.array_equal(got.counts, want[2]), v
             ran += 1
         assert ran >= len(variants)  # the default plus all but at most one fallback must run
+
+
+@pytest.mark.parametrize("dims,text", [(128, "16x{4,4}"), (96, "12x{6,5,5}"), (64, "12x{6,6,4}"), (60, "12x{5,5,5}"),
+                                       (64, "8x{8,8}"), (64, "8x{8}")])
+def test_randomised_search_parameters_vs_oracle(port, dims, text):
+    """Random (n, nq, r, t) around the edges the planner's default variants see: one query, ragged tiles, r = 1,
+    r close to n, t = r and t > n, lists shorter than one stage buffer and longer than several segments."""
+    rng = np.random.default_rng(abs(hash(text)) % 9973)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 1.7).astype(np.float32)
+    for n, nq, r, t in [(1, 1, 1, 1), (17, 3, 5, 5), (700, 1, 100, 400), (5000, 33, 1, 1), (40000, 16, 250, 250),
+                        (300000, 47, 100, 400), (9000, 129, 1000, 5000), (70000, 5, 999, 1000)]:
+        pk = qb.pack_list(s, random_codes(s, n, seed=n))
+        queries = (rng.standard_normal((nq, dims)) * 1.7).astype(np.float32)
+        want = port.flat_search(so, cb, pk, n, queries, r=r, t=t, threads=8)
+        with qb.FlatIndex(s, cb, pk, n) as idx:
+            got = idx.search(queries, qb.SearchParams(r=r, t=t))
+        assert np.array_equal(got.counts, want[2]), (n, nq, r, t)
+        for qi in range(nq):
+            c = int(want[2][qi])
+            assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]), (n, nq, r, t, qi)
+            assert bits_equal(got.dists[qi, :c], want[1][qi, :c]), (n, nq, r, t, qi)
