@@ -532,6 +532,8 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
             // 32-row tiles: the duplicated-line layout when two tile buffers of it fit, else the dense one
             ScanVariant c32 = VAR_F16X4H_C4;
             double rate32 = 0.93;
+            if (tile_pair_layout(VAR_F16X4H_C4, ds)) rate32 = 1.25; // pair-interleaved lines: conflict free, no copies
+            else
             try {
                 if (plan_scan(ds, h->device, int(VAR_F16X4H_C4D)).tile_bufs == 2) {
                     c32 = VAR_F16X4H_C4D;

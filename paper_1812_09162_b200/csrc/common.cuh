@@ -149,14 +149,18 @@ size_t tile_entry_bytes(ScanVariant v);
 // 16x{4,4}): tables 2k and 2k+1 share 128-byte lines -- entry i of table 2k in the low half of line k*256 + i,
 // entry i of table 2k+1 in the high half.  Odd code groups of a warp walk each table pair in swapped order, so
 // at every step two groups read low halves and two read high halves: no bank conflicts (scan.cu).
-__host__ __device__ inline uint32_t pair_perm(uint32_t e) {
-    const uint32_t j = e >> 8, i = e & 255u;
-    return ((((j >> 1) << 8) + i) << 1) | (j & 1u);
+// The same interleave serves the irregular 16-bit specs on 32-row tiles with the pairing unit = one 16-bit WORD of
+// the code (words w and w ^ 1 have identical table sizes; odd code groups see their code with the 16-bit halves of
+// every 32-bit word swapped).  `block` = entries of one pairing unit: 256 (a table) or E / 4 (a word's tables).
+__host__ __device__ inline uint32_t pair_perm(uint32_t e, uint32_t block) {
+    const uint32_t u = e / block, i = e - u * block;
+    return ((((u >> 1) * block) + i) << 1) | (u & 1u);
 }
-bool tile_pair_layout(ScanVariant v, const DevSpec& ds);
+// 0 = dense lines; otherwise the pairing block of the tile layout the scan kernel expects for (variant, spec)
+uint32_t tile_pair_layout(ScanVariant v, const DevSpec& ds);
 // entries of one LUT row in the tile image (the spec's E, except for the merged-pair layout)
 uint32_t tile_entries(ScanVariant v, uint32_t E);
-void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, bool pair, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
+void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, uint32_t pair, const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq,
                        void* out, cudaStream_t stream);
 
 // ---- dense head evaluation (seed.cu) ----
@@ -189,7 +193,7 @@ void ivf_tables_tiled_prepare(const DevSpec& ds, const float* codebook, std::vec
 void launch_ivf_tables_tiled(const DevSpec& ds, const float* d_codebook_tp, const uint8_t* d_sub_of,
                              const float* d_queries, const float* d_coarse, const uint32_t* d_order, uint32_t n_pairs,
                              uint32_t a, float* d_luts, float* d_pmin, float* d_own_min, cudaStream_t stream);
-void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, bool pair, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
+void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, uint32_t pair, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
                               const float* d_luts, const float* d_pmin, const float* d_own_min,
                               const float* d_qparams, const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base,
                               uint32_t tq, uint32_t ntiles, void* d_qluts, void* d_tile_lut, uint32_t* d_row_query,

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(256)
 ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uint32_t a,
                          const float* __restrict__ luts, const float* __restrict__ pmin,
                          const float* __restrict__ own_min, const float* __restrict__ qparams, uint32_t tq,
-                         uint32_t filter_shift, uint32_t copies, bool pair, void* __restrict__ qluts,
+                         uint32_t filter_shift, uint32_t copies, uint32_t pair_block, void* __restrict__ qluts,
                          Entry* __restrict__ tile_lut,
                          uint32_t* __restrict__ row_query, uint32_t* __restrict__ row_bias) {
     extern __shared__ __align__(16) unsigned short panel[];
@@ -353,7 +353,7 @@ ivf_quantize_pack_kernel(DevSpec ds, const uint32_t* __restrict__ slot_pair, uin
                 v[2 * k] = w & 0xFFFFu;
                 v[2 * k + 1] = w >> 16;
             }
-            const uint32_t line = pair ? pair_perm(e0 + el) : e0 + el;
+            const uint32_t line = pair_block ? pair_perm(e0 + el, pair_block) : e0 + el;
             for (uint32_t c = 0; c < copies; ++c)
                 store_rows8<Entry>(dst + (size_t(line) * copies + c) * tq + g * 8, v, filter_shift);
         }
@@ -365,7 +365,7 @@ template <class Entry>
 static void launch_qp(const DevSpec& ds, const uint32_t* slot_pair, uint32_t a, const float* luts, const float* pmin,
                       const float* own_min, const float* qparams, uint32_t tq, uint32_t hb, void* qluts, void* tile_lut,
                       uint32_t* row_query, uint32_t* row_bias, uint32_t ntiles, cudaStream_t stream,
-                      uint32_t copies = 1, bool pair = false) {
+                      uint32_t copies = 1, uint32_t pair = 0) {
     const size_t smem = size_t(std::min(ds.E, QP_SLAB)) * (tq + 2) * sizeof(unsigned short) + ds.E;
     QADC_CUDA_CHECK(cudaFuncSetAttribute(ivf_quantize_pack_kernel<Entry>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     ivf_quantize_pack_kernel<Entry><<<ntiles, 256, smem, stream>>>(ds, slot_pair, a, luts, pmin, own_min, qparams, tq, hb,
@@ -375,7 +375,7 @@ static void launch_qp(const DevSpec& ds, const uint32_t* slot_pair, uint32_t a, 
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, bool pair, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
+void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, uint32_t pair, const DevSpec& ds, const uint32_t* d_order, uint32_t n_pairs, uint32_t a,
                               const float* d_luts, const float* d_pmin, const float* d_own_min,
                               const float* d_qparams, const uint32_t* d_pair_rank, const uint32_t* d_cell_tile_base,
                               uint32_t tq, uint32_t ntiles, void* d_qluts, void* d_tile_lut, uint32_t* d_row_query,
@@ -395,12 +395,12 @@ void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, bool pair, c
     case VAR_F16X8:
     case VAR_F16X4_C4:
         return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, 0, d_qluts, d_tile_lut,
-                                 d_row_query, d_row_bias, ntiles, stream, 1, v == VAR_F16X4_C4 && pair);
+                                 d_row_query, d_row_bias, ntiles, stream, 1, pair);
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4:
         return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, fs, d_qluts, d_tile_lut,
-                                 d_row_query, d_row_bias, ntiles, stream, 1, v == VAR_F16X4H_C4 && pair);
+                                 d_row_query, d_row_bias, ntiles, stream, 1, pair);
     case VAR_F16X4H_C4D:
         return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, fs, d_qluts, d_tile_lut,
                                  d_row_query, d_row_bias, ntiles, stream, 2);

@@ -570,7 +570,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     constexpr bool PAIR = pair_of<P>::value && !G::RUNTIME;
     const uint32_t lane_off_a = lane_in * P::LANE_B + (lane_code & 1u) * P::ROWB;
     const uint32_t lane_off_b = lane_in * P::LANE_B + ((lane_code & 1u) ^ 1u) * P::ROWB;
-    const uint32_t swap_sel = (lane_code & 1u) ? 0x2301u : 0x3210u;
+    // pairing unit: a 256-entry table (all-8-bit specs: odd groups swap adjacent code bytes) or one 16-bit word of an
+    // irregular spec (odd groups swap the 16-bit halves of every 32-bit code word)
+    constexpr bool PAIR_BYTES = G::RUNTIME || G::bits(0) == 8;
+    const uint32_t swap_sel = (lane_code & 1u) ? (PAIR_BYTES ? 0x2301u : 0x1032u) : 0x3210u;
     // quad layout (merged 12x{6,5,5}): rotation of this code group and the bank quarter it reads at step k
     constexpr bool QUAD = quad_of<P>::value;
     const uint32_t quad_r = lane_code & 3u;
@@ -745,12 +748,17 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                         constexpr int logl = P::LOG_ROWB + (PAIR ? 1 : 0); // bytes per entry line (pair: two tables per line)
                         constexpr int word = bp >> 5, sh = (bp & 31) - logl;
                         constexpr uint32_t mask = ((1u << nb) - 1u) << logl;
-                        constexpr uint32_t imm = uint32_t(G::ent_off(PAIR ? (j & ~1) : j)) * P::ROWB;
-                        static_assert(!PAIR || (nb == 8 && (G::M & 1) == 0 && bp == 8 * j), "pair layout: 8-bit tables only");
+                        // pair layout: unit u = table (8-bit specs) or code word; line = (u >> 1) * block + offset in unit
+                        constexpr int pblock = PAIR_BYTES ? 256 : G::ent_off(G::M / 4);
+                        constexpr int unit = G::ent_off(j) / pblock, within = G::ent_off(j) - unit * pblock;
+                        constexpr uint32_t imm = PAIR ? uint32_t((unit >> 1) * pblock + within) * 2u * P::ROWB
+                                                      : uint32_t(G::ent_off(j)) * P::ROWB;
+                        static_assert(!PAIR || PAIR_BYTES ? true : (G::M % 8 == 4 || G::M % 4 == 0), "pair layout: four code words");
+                        static_assert(!PAIR || !PAIR_BYTES || (nb == 8 && (G::M & 1) == 0 && bp == 8 * j), "pair layout: 8-bit tables");
 #pragma unroll
                         for (int c = 0; c < CIF; ++c) {
                             const uint32_t x = sh >= 0 ? (cw[c][word] >> (sh >= 0 ? sh : 0)) : (cw[c][word] << (sh < 0 ? -sh : 0));
-                            const uint32_t off = (x & mask) | (PAIR ? ((j & 1) ? lane_off_b : lane_off_a) : lane_off);
+                            const uint32_t off = (x & mask) | (PAIR ? ((unit & 1) ? lane_off_b : lane_off_a) : lane_off);
                             P::add(acc[c], tile + imm + off);
                         }
                     });
@@ -800,7 +808,7 @@ const char* variant_name(uint32_t v) {
     case VAR_U8X1: return "u8x1 (high-byte filter, 32-query tile)";
     case VAR_F16X4H: return "f16x4h (u16 tables, fp16 high-byte filter + exact re-evaluation, 128-query tile, LDS.64)";
     case VAR_F16X4H_C2: return "f16x4h-c2 (as f16x4h, 2 codes per warp step, 64-row tile)";
-    case VAR_F16X4H_C4: return "f16x4h-c4 (as f16x4h, 32-row tile; 8x{8,8}: pair-interleaved lines, LDS.128, 8 codes per warp step)";
+    case VAR_F16X4H_C4: return "f16x4h-c4 (as f16x4h, 32-row tile; named specs: pair-interleaved lines, LDS.128, 8 codes per warp step)";
     case VAR_F16X4_C4: return "f16x4-c4 (u8 tables exact in fp16, 32-row tile; 8x{8}: pair-interleaved lines, LDS.128, 8 codes per warp step)";
     case VAR_F16X4_C4M: return "f16x4-c4m (16x{4,4} as 8 byte-indexed tables of pair sums; 32-row pair-interleaved tile, LDS.128, 8 codes per warp step)";
     case VAR_F16X4H_C8Q: return "f16x4h-c8q (12x{6,5,5} as 4 x {6-bit table, (5,5) pair-sum table}: 8 lookups per code, quad-interleaved 16-row tile, LDS.128, 16 codes per warp step)";
@@ -966,7 +974,10 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         if (G655::matches(ds)) return launch_one<PolF16x4H_C2, G655>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C2, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4:
-        if (G655::matches(ds)) return launch_one<PolF16x4H_C4, G655>(plan, ds, args, grid, stream);
+        // irregular specs: word-pair interleaved lines (tile_pair_layout() makes the same choice), 8 rows per lane
+        if (G655::matches(ds)) return launch_one<PolF16x8H_C8P, G655>(plan, ds, args, grid, stream);
+        if (G664::matches(ds)) return launch_one<PolF16x8H_C8P, G664>(plan, ds, args, grid, stream);
+        if (G555::matches(ds)) return launch_one<PolF16x8H_C8P, G555>(plan, ds, args, grid, stream);
         if (G88::matches(ds)) return launch_one<PolF16x8H_C8P, G88>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C8Q:

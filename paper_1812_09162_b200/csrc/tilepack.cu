@@ -34,7 +34,7 @@ static constexpr int PACK_E = 64;
 // grid = (ntiles, ceil(E / PACK_E)); block = 256.  rows [tile*TQ, tile*TQ + TQ) clipped to n_rows.
 template <class Entry>
 __global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width, uint32_t E, uint32_t n_rows,
-                                  uint32_t tq, uint32_t high_byte /* filter shift */, uint32_t copies, bool pair,
+                                  uint32_t tq, uint32_t high_byte /* filter shift */, uint32_t copies, uint32_t pair,
                                   Entry* __restrict__ out) {
     extern __shared__ unsigned short panel[]; // [PACK_E][tq + 1]
     const uint32_t tile = blockIdx.x, e0 = blockIdx.y * PACK_E;
@@ -58,14 +58,14 @@ __global__ void pack_tiles_kernel(const void* __restrict__ qlut, uint32_t width,
     for (uint32_t u = threadIdx.x; u < ne * tq; u += blockDim.x) {
         const uint32_t r = u % tq, el = u / tq;
         const Entry v = tile_convert<Entry>(panel[el * pitch + r], width, high_byte);
-        const uint32_t line = pair ? pair_perm(e0 + el) : e0 + el;
+        const uint32_t line = pair ? pair_perm(e0 + el, pair) : e0 + el;
         for (uint32_t c = 0; c < copies; ++c) dst[(size_t(line) * copies + c) * tq + r] = v;
     }
 }
 
 template <class Entry>
 static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n_rows, uint32_t tq, uint32_t hb,
-                        void* out, cudaStream_t stream, uint32_t copies = 1, bool pair = false) {
+                        void* out, cudaStream_t stream, uint32_t copies = 1, uint32_t pair = 0) {
     const uint32_t ntiles = (n_rows + tq - 1) / tq;
     if (ntiles == 0) return;
     const dim3 grid(ntiles, (E + PACK_E - 1) / PACK_E);
@@ -77,7 +77,7 @@ static void launch_pack(const void* qlut, uint32_t width, uint32_t E, uint32_t n
 
 // 16x{4,4} merged into 8 byte-indexed tables: entry (j, b) = T[2j][b & 15] + T[2j+1][b >> 4] (VAR_F16X4_C4M).
 // grid = (ntiles, 2048 / 64); block = 256; rows [tile*TQ, tile*TQ + TQ) clipped to n_rows; qlut is [row][256] u8.
-__global__ void pack_tiles_merged44_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint32_t tq, bool pair,
+__global__ void pack_tiles_merged44_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint32_t tq, uint32_t pair,
                                            __half* __restrict__ out) {
     const uint32_t tile = blockIdx.x, e0 = blockIdx.y * 64;
     __half* base = out + size_t(tile) * 2048 * tq;
@@ -89,17 +89,29 @@ __global__ void pack_tiles_merged44_kernel(const uint8_t* __restrict__ qlut, uin
             const uint8_t* t = qlut + size_t(row) * 256 + 32 * j;
             v = uint32_t(t[b & 15u]) + uint32_t(t[16 + (b >> 4)]);
         }
-        base[size_t(pair ? pair_perm(e) : e) * tq + r] = __uint2half_rn(v);
+        base[size_t(pair ? pair_perm(e, pair) : e) * tq + r] = __uint2half_rn(v);
     }
 }
 
-bool tile_pair_layout(ScanVariant v, const DevSpec& ds) {
-    if (v == VAR_F16X4_C4M) return true; // the merged view is 8 tables of 256 entries
-    if (v != VAR_F16X4H_C4 && v != VAR_F16X4_C4) return false;
-    if (ds.m == 0 || (ds.m & 1u) || ds.E != ds.m * 256u || ds.code_stride != 8) return false;
-    for (uint32_t j = 0; j < ds.m; ++j)
-        if (ds.bits[j] != 8 || ds.bitpos[j] != 8 * j) return false;
-    return ds.m == 8; // the compile-time geometries that implement it (G8, G88)
+uint32_t tile_pair_layout(ScanVariant v, const DevSpec& ds) {
+    if (v == VAR_F16X4_C4M) return 256; // the merged view is 8 tables of 256 entries
+    if (v != VAR_F16X4H_C4 && v != VAR_F16X4_C4) return 0;
+    if (ds.m == 0 || ds.code_stride != 8) return 0;
+    bool bytes = ds.m == 8 && ds.E == 2048;
+    for (uint32_t j = 0; j < ds.m && bytes; ++j) bytes = ds.bits[j] == 8 && ds.bitpos[j] == 8 * j;
+    if (bytes) return 256; // G8 / G88
+    // G655 / G664 / G555 on the conservative 32-row variant: four 16-bit words with identical tables
+    if (v == VAR_F16X4H_C4 && ds.word_width == 16 && ds.m == 12 && ds.E % 4 == 0) {
+        for (uint32_t j = 0; j < 12; ++j) {
+            if (ds.bits[j] != ds.bits[j % 3]) return 0;
+            if (ds.bitpos[j] != 16 * (j / 3) + (j % 3 == 0 ? 0 : j % 3 == 1 ? ds.bits[0] : ds.bits[0] + ds.bits[1])) return 0;
+        }
+        const uint32_t b[3] = {ds.bits[0], ds.bits[1], ds.bits[2]};
+        const bool named = (b[0] == 6 && b[1] == 5 && b[2] == 5) || (b[0] == 6 && b[1] == 6 && b[2] == 4) ||
+                           (b[0] == 5 && b[1] == 5 && b[2] == 5);
+        return named ? ds.E / 4 : 0; // the compile-time geometries that implement it
+    }
+    return 0;
 }
 
 // 12x{6,5,5} merged for VAR_F16X4H_C8Q: per tile of 16 rows, 1024 + 64 lines of 128 bytes; line i of the first
@@ -146,7 +158,7 @@ size_t tile_entry_bytes(ScanVariant v) {
     }
 }
 
-void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, bool pair, const void* qlut, uint32_t width, uint32_t E,
+void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, uint32_t pair, const void* qlut, uint32_t width, uint32_t E,
                        uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     switch (v) {
     case VAR_F16X4H_C8Q: {
@@ -172,11 +184,11 @@ void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, bool pair, const vo
         return;
     }
     case VAR_F16X8:
-    case VAR_F16X4_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, 0, out, stream, 1, v == VAR_F16X4_C4 && pair);
+    case VAR_F16X4_C4: return launch_pack<__half>(qlut, width, E, n_rows, tq, 0, out, stream, 1, pair);
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4:
-        return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream, 1, v == VAR_F16X4H_C4 && pair);
+        return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream, 1, pair);
     case VAR_F16X4H_C4D: return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream, 2);
     case VAR_F32X2: return launch_pack<float>(qlut, width, E, n_rows, tq, 0, out, stream);
     case VAR_U16X1: return launch_pack<unsigned short>(qlut, width, E, n_rows, tq, 0, out, stream);
