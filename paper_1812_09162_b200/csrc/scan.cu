@@ -291,8 +291,6 @@ using PolF16x4H_C2 = PolF16x4H_T<2>;
 using PolF16x4H_C4 = PolF16x4H_T<4>;
 using PolF16x4_C4 = PolF16x4H_T<4, false>;
 using PolF16x4H_C4D = PolF16x4H_T<4, true, true>;
-using PolF16x4H_C4P = PolF16x4H_T<4, true, false, true>;
-using PolF16x4_C4P = PolF16x4H_T<4, false, false, true>;
 
 template <class P, class = void>
 struct pair_of : std::false_type {};
@@ -985,8 +983,9 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         if (G555::matches(ds)) return launch_one<PolQ655, GeomQ555>(plan, ds, args, grid, stream);
         return launch_one<PolQ655, GeomQ655>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4D:
-        // (the 8-rows-per-lane twin, PolF16x8H_C8D, is 8 % faster on a flat scan but 50 % slower on the IVF
-        // workload this variant exists for: with ~1 % of the warp steps flagged, 8 ballots per flagged step hurt)
+        // duplicated lines, 8 rows per lane (the 4-rows-per-lane twin was the choice while a flagged warp step cost
+        // one ballot per slot; with the sparse flag path this one is 13 % faster on the IVF workload).  Superseded
+        // as the IVF default by the word-pair layout of VAR_F16X4H_C4, kept as a selectable variant.
         if (G655::matches(ds)) return launch_one<PolF16x8H_C8D, G655>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4D, GeomRT>(plan, ds, args, grid, stream);
     // (G8 / G88 run the pair-interleaved tile layout: tile_pair_layout() in tilepack.cu makes the same choice)
