@@ -873,3 +873,35 @@ def test_randomised_search_parameters_vs_oracle(port, dims, text):
             c = int(want[2][qi])
             assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]), (n, nq, r, t, qi)
             assert bits_equal(got.dists[qi, :c], want[1][qi, :c]), (n, nq, r, t, qi)
+
+
+@pytest.mark.parametrize("dims,text,variants", [(96, "12x{6,5,5}", [1, 2, 4, 5, 6, 8]), (64, "12x{6,6,4}", [4, 5, 6]),
+                                                (60, "12x{5,5,5}", [4, 5, 6]), (64, "8x{8,8}", [2, 6]),
+                                                (64, "16x{4,4}", [0, 1, 7])])
+def test_every_ivf_tile_layout_is_exact(port, dims, text, variants):
+    """The IVF batch path writes its LUT tiles itself (fused quantize + pack): every tile layout it can be asked
+    for -- 128 / 64 / 32-row tiles, word-pair and byte-pair interleaved lines, duplicated lines, the fallbacks --
+    returns the oracle's result bit for bit."""
+    rng = np.random.default_rng(len(text) * 7 + dims)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    k_cells, n, nq, probes = 40, 60000, 90, 6
+    cb = (rng.standard_normal(s.cb_floats) * 1.2).astype(np.float32)
+    coarse = (rng.standard_normal((k_cells, dims)) * 3).astype(np.float32)
+    packed, boff, ioff, counts, ids = _ivf_lists(rng, s, k_cells, n, empty=(2,))
+    hot = rng.integers(0, k_cells, size=4)
+    queries = (coarse[hot[rng.integers(0, 4, size=nq)]] + rng.standard_normal((nq, dims))).astype(np.float32)
+    want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=probes, r=60, t=300, threads=8)
+    with qb.IvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids) as idx:
+        ran = 0
+        for v in [-1] + variants:
+            idx.set_option("force_variant", v)
+            try:
+                got = idx.search(queries, qb.SearchParams(probes=probes, r=60, t=300))
+            except qb.QadcError as e:
+                assert e.kind == "config", (v, e)
+                continue
+            assert np.array_equal(got.counts, want[2]), v
+            assert np.array_equal(got.ids, want[0]), v
+            assert bits_equal(got.dists, want[1]), v
+            ran += 1
+        assert ran >= 2
