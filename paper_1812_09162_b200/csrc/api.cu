@@ -541,12 +541,15 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
                 }
             } catch (const Error&) {
             }
-            const ScanVariant cand[3] = {VAR_F16X4H, VAR_F16X4H_C2, c32};
-            const uint32_t rows[3] = {128, 64, 32};
-            const double per_pair[3] = {1.0 / 1.13, 1.0 / 1.30, 1.0 / rate32}; // measured flat-scan rates (T pairs/s)
+            // 16-row tiles (quad lines) exist for the named irregular specs; every tile is also one more pass over its
+            // cell's codes and one more job, hence the larger per-tile constant below
+            const bool have16 = tile_pair_layout(VAR_F16X4H_C16Q, ds) != 0;
+            const ScanVariant cand[4] = {VAR_F16X4H, VAR_F16X4H_C2, c32, VAR_F16X4H_C16Q};
+            const uint32_t rows[4] = {128, 64, 32, 16};
+            const double per_pair[4] = {1.0 / 1.13, 1.0 / 1.30, 1.0 / rate32, 1.0 / 1.25}; // measured flat-scan rates (T pairs/s)
             double best = -1.0;
             int pick = int(plan.variant) - int(VAR_F16X4H);
-            for (int v = 0; v < 3; ++v) {
+            for (int v = 0; v < (have16 ? 4 : 3); ++v) {
                 try {
                     (void)plan_scan(ds, h->device, int(cand[v])); // does this tile height fit shared memory?
                 } catch (const Error&) {

@@ -74,6 +74,8 @@ enum ScanVariant : uint32_t {
     VAR_F16X4H_C8Q = 10, // 12x{6,5,5} scanned as 8 lookups per code: per 16-bit word one 6-bit table and one 1024-entry
                          // table of (5,5) pair sums; 16-row tile whose 128-byte lines hold the same entry of the four
                          // words' tables (quad-interleaved); code groups walk the words in rotated order
+    VAR_F16X4H_C16Q = 11, // irregular 16-bit specs on 16-row tiles: quad lines (the same entry of the four words' tables),
+                          // rotated codes, LDS.128, 16 codes per warp step -- the IVF layout with the least row padding
     VAR_COUNT
 };
 
@@ -152,9 +154,12 @@ size_t tile_entry_bytes(ScanVariant v);
 // The same interleave serves the irregular 16-bit specs on 32-row tiles with the pairing unit = one 16-bit WORD of
 // the code (words w and w ^ 1 have identical table sizes; odd code groups see their code with the 16-bit halves of
 // every 32-bit word swapped).  `block` = entries of one pairing unit: 256 (a table) or E / 4 (a word's tables).
+// Bit 31 of `block` selects the QUAD interleave instead (16-row tiles: four units per 128-byte line).
+static constexpr uint32_t TILE_QUAD = 0x80000000u;
 __host__ __device__ inline uint32_t pair_perm(uint32_t e, uint32_t block) {
-    const uint32_t u = e / block, i = e - u * block;
-    return ((((u >> 1) * block) + i) << 1) | (u & 1u);
+    const uint32_t b = block & ~TILE_QUAD, u = e / b, i = e - u * b;
+    if (block & TILE_QUAD) return (i << 2) | u;
+    return ((((u >> 1) * b) + i) << 1) | (u & 1u);
 }
 // 0 = dense lines; otherwise the pairing block of the tile layout the scan kernel expects for (variant, spec)
 uint32_t tile_pair_layout(ScanVariant v, const DevSpec& ds);

@@ -399,6 +399,7 @@ void launch_ivf_quantize_pack(ScanVariant v, uint32_t filter_shift, uint32_t pai
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4:
+    case VAR_F16X4H_C16Q:
         return launch_qp<__half>(ds, d_slot_pair, a, d_luts, d_pmin, d_own_min, d_qparams, tq, fs, d_qluts, d_tile_lut,
                                  d_row_query, d_row_bias, ntiles, stream, 1, pair);
     case VAR_F16X4H_C4D:

@@ -286,6 +286,24 @@ struct PolQ655 : PolF16x8_T<16, true, false> {
     static constexpr int TQ = 16, ROWB = 128, LOG_ROWB = 7, LANE_B = 16;
 };
 
+// The unmerged sibling for the IVF path (tiles of the merged view are 139 KB, far too much per (query, cell) row):
+// the same quad lines and rotated codes with the spec's own 12 tables -- a 16-row tile is E/4 lines of 128 bytes
+// (16 KB for 12x{6,5,5}), so a cell's last, partly filled tile wastes at most 15 rows instead of 31.
+struct PolQU : PolF16x8_T<16, true, false> {
+    static constexpr bool QUADU = true;
+    static constexpr int TQ = 16, ROWB = 128, LOG_ROWB = 7, LANE_B = 16;
+};
+template <class P, class = void>
+struct quadu_of : std::false_type {};
+template <class P>
+struct quadu_of<P, std::void_t<decltype(P::QUADU)>> : std::bool_constant<P::QUADU> {};
+// geometry view: a quarter of the entries per line set; the exact re-evaluation keeps the spec's geometry
+template <class Gx>
+struct GeomQU : Gx {
+    static constexpr int E = Gx::E / 4;
+    using Exact = Gx;
+};
+
 using PolF16x4H = PolF16x4H_T<1>;
 using PolF16x4H_C2 = PolF16x4H_T<2>;
 using PolF16x4H_C4 = PolF16x4H_T<4>;
@@ -574,6 +592,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
     const uint32_t swap_sel = (lane_code & 1u) ? (PAIR_BYTES ? 0x2301u : 0x1032u) : 0x3210u;
     // quad layout (merged 12x{6,5,5}): rotation of this code group and the bank quarter it reads at step k
     constexpr bool QUAD = quad_of<P>::value;
+    constexpr bool QUADU = quadu_of<P>::value && !G::RUNTIME;
     const uint32_t quad_r = lane_code & 3u;
     uint32_t quad_off[4];
 #pragma unroll
@@ -719,6 +738,19 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                         }
                         acc[c] = acc0;
                     }
+                    uint32_t orig[CIF][2]; // QUADU: the code as stored (the lookups use the rotated words)
+                    if constexpr (QUADU) {
+#pragma unroll
+                        for (int c = 0; c < CIF; ++c) {
+                            orig[c][0] = cw[c][0];
+                            orig[c][1] = cw[c][1];
+                            const uint32_t lo = (quad_r & 2u) ? cw[c][1] : cw[c][0];
+                            const uint32_t hi = (quad_r & 2u) ? cw[c][0] : cw[c][1];
+                            const uint32_t sh = (quad_r & 1u) * 16u;
+                            cw[c][0] = __funnelshift_r(lo, hi, sh);
+                            cw[c][1] = __funnelshift_r(hi, lo, sh);
+                        }
+                    }
                     if constexpr (QUAD) {
                         // word k of the rotated code = word (k + r) mod 4 of the stored one; per word the (5,5) pair
                         // index (bits 6..15) into the 1024-line section and the 6-bit index into the 64-line section
@@ -743,28 +775,33 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1) scan_kernel(DevSpec ds_param,
                     static_for<0, G::M>([&](auto J) {
                         constexpr int j = decltype(J)::value;
                         constexpr int bp = G::bitpos(j), nb = G::bits(j);
-                        constexpr int logl = P::LOG_ROWB + (PAIR ? 1 : 0); // bytes per entry line (pair: two tables per line)
+                        constexpr int logl = P::LOG_ROWB + (PAIR ? 1 : 0); // bytes per entry line (pair: two tables per line; quad: LOG_ROWB is the line)
                         constexpr int word = bp >> 5, sh = (bp & 31) - logl;
                         constexpr uint32_t mask = ((1u << nb) - 1u) << logl;
                         // pair layout: unit u = table (8-bit specs) or code word; line = (u >> 1) * block + offset in unit
                         constexpr int pblock = PAIR_BYTES ? 256 : G::ent_off(G::M / 4);
                         constexpr int unit = G::ent_off(j) / pblock, within = G::ent_off(j) - unit * pblock;
-                        constexpr uint32_t imm = PAIR ? uint32_t((unit >> 1) * pblock + within) * 2u * P::ROWB
-                                                      : uint32_t(G::ent_off(j)) * P::ROWB;
+                        constexpr uint32_t imm = PAIR    ? uint32_t((unit >> 1) * pblock + within) * 2u * P::ROWB
+                                                 : QUADU ? uint32_t(within) * P::ROWB // line = offset inside the word's tables
+                                                         : uint32_t(G::ent_off(j)) * P::ROWB;
                         static_assert(!PAIR || PAIR_BYTES ? true : (G::M % 8 == 4 || G::M % 4 == 0), "pair layout: four code words");
                         static_assert(!PAIR || !PAIR_BYTES || (nb == 8 && (G::M & 1) == 0 && bp == 8 * j), "pair layout: 8-bit tables");
 #pragma unroll
                         for (int c = 0; c < CIF; ++c) {
                             const uint32_t x = sh >= 0 ? (cw[c][word] >> (sh >= 0 ? sh : 0)) : (cw[c][word] << (sh < 0 ? -sh : 0));
-                            const uint32_t off = (x & mask) | (PAIR ? ((unit & 1) ? lane_off_b : lane_off_a) : lane_off);
+                            const uint32_t off = (x & mask) | (PAIR    ? ((unit & 1) ? lane_off_b : lane_off_a)
+                                                               : QUADU ? quad_off[unit & 3]
+                                                                       : lane_off);
                             P::add(acc[c], tile + imm + off);
                         }
                     });
 #pragma unroll
                     for (int c = 0; c < CIF; ++c) {
                         // the queue keeps the code as stored (the byte swap is an involution)
-                        const uint32_t o0 = PAIR ? __byte_perm(cw[c][0], 0u, swap_sel) : cw[c][0];
-                        const uint32_t o1 = PAIR ? __byte_perm(cw[c][G::CW > 1 ? 1 : 0], 0u, swap_sel) : cw[c][G::CW > 1 ? 1 : 0];
+                        const uint32_t o0 = QUADU ? orig[c][0] : PAIR ? __byte_perm(cw[c][0], 0u, swap_sel) : cw[c][0];
+                        const uint32_t o1 = QUADU  ? orig[c][1]
+                                            : PAIR ? __byte_perm(cw[c][G::CW > 1 ? 1 : 0], 0u, swap_sel)
+                                                   : cw[c][G::CW > 1 ? 1 : 0];
                         flag(acc[c], i0 + c * SCAN_WARPS * P::CPW < cnt, i0 + c * SCAN_WARPS * P::CPW, o0, o1);
                     }
                 }
@@ -810,6 +847,7 @@ const char* variant_name(uint32_t v) {
     case VAR_F16X4_C4: return "f16x4-c4 (u8 tables exact in fp16, 32-row tile; 8x{8}: pair-interleaved lines, LDS.128, 8 codes per warp step)";
     case VAR_F16X4_C4M: return "f16x4-c4m (16x{4,4} as 8 byte-indexed tables of pair sums; 32-row pair-interleaved tile, LDS.128, 8 codes per warp step)";
     case VAR_F16X4H_C8Q: return "f16x4h-c8q (12x{6,5,5} as 4 x {6-bit table, (5,5) pair-sum table}: 8 lookups per code, quad-interleaved 16-row tile, LDS.128, 16 codes per warp step)";
+    case VAR_F16X4H_C16Q: return "f16x4h-c16q (irregular 16-bit specs, 16-row tile of quad lines, rotated codes, LDS.128, 16 codes per warp step)";
     case VAR_F16X4H_C4D: return "f16x4h-c4d (as f16x4h-c4, entry lines duplicated: bank-conflict-free)";
     }
     return "?";
@@ -832,7 +870,7 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_
         if (ds.word_width != 16) return 0;
         if (v == VAR_U8X1) return 8;
         if (v == VAR_F16X4H_C8Q) return 6; // pair sums of 10-bit prefixes stay below 2048
-        if (v != VAR_F16X4H && v != VAR_F16X4H_C2 && v != VAR_F16X4H_C4 && v != VAR_F16X4H_C4D) return 0;
+        if (v != VAR_F16X4H && v != VAR_F16X4H_C2 && v != VAR_F16X4H_C4 && v != VAR_F16X4H_C4D && v != VAR_F16X4H_C16Q) return 0;
         uint32_t sh = 5;
         while (sh < 8 && ds.m * (65535u >> sh) > 28000u) ++sh;
         return sh;
@@ -856,6 +894,11 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_
         case VAR_F16X4_C4:
             if (!u8) throw Error(QADC_ERR_CONFIG, "scan: f16x4-c4 needs 8-bit tables");
             set(VAR_F16X4_C4, PolF16x4_C4::TQ, smem_need<PolF16x4_C4>(ds.E));
+            break;
+        case VAR_F16X4H_C16Q:
+            if (u8 || !(G655::matches(ds) || G664::matches(ds) || G555::matches(ds)))
+                throw Error(QADC_ERR_CONFIG, "scan: f16x4h-c16q is the 16-row layout of 12x{6,5,5} / 12x{6,6,4} / 12x{5,5,5}");
+            set(VAR_F16X4H_C16Q, PolQU::TQ, smem_need<PolQU>(ds.E / 4));
             break;
         case VAR_F16X4H_C8Q:
             if (!allow_merged || !(G655::matches(ds) || G664::matches(ds) || G555::matches(ds)))
@@ -978,6 +1021,10 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         if (G555::matches(ds)) return launch_one<PolF16x8H_C8P, G555>(plan, ds, args, grid, stream);
         if (G88::matches(ds)) return launch_one<PolF16x8H_C8P, G88>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C4, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_F16X4H_C16Q:
+        if (G664::matches(ds)) return launch_one<PolQU, GeomQU<G664>>(plan, ds, args, grid, stream);
+        if (G555::matches(ds)) return launch_one<PolQU, GeomQU<G555>>(plan, ds, args, grid, stream);
+        return launch_one<PolQU, GeomQU<G655>>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C8Q:
         if (G664::matches(ds)) return launch_one<PolQ655, GeomQ664>(plan, ds, args, grid, stream);
         if (G555::matches(ds)) return launch_one<PolQ655, GeomQ555>(plan, ds, args, grid, stream);

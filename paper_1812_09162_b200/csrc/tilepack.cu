@@ -95,13 +95,13 @@ __global__ void pack_tiles_merged44_kernel(const uint8_t* __restrict__ qlut, uin
 
 uint32_t tile_pair_layout(ScanVariant v, const DevSpec& ds) {
     if (v == VAR_F16X4_C4M) return 256; // the merged view is 8 tables of 256 entries
-    if (v != VAR_F16X4H_C4 && v != VAR_F16X4_C4) return 0;
+    if (v != VAR_F16X4H_C4 && v != VAR_F16X4_C4 && v != VAR_F16X4H_C16Q) return 0;
     if (ds.m == 0 || ds.code_stride != 8) return 0;
     bool bytes = ds.m == 8 && ds.E == 2048;
     for (uint32_t j = 0; j < ds.m && bytes; ++j) bytes = ds.bits[j] == 8 && ds.bitpos[j] == 8 * j;
     if (bytes) return 256; // G8 / G88
     // G655 / G664 / G555 on the conservative 32-row variant: four 16-bit words with identical tables
-    if (v == VAR_F16X4H_C4 && ds.word_width == 16 && ds.m == 12 && ds.E % 4 == 0) {
+    if ((v == VAR_F16X4H_C4 || v == VAR_F16X4H_C16Q) && ds.word_width == 16 && ds.m == 12 && ds.E % 4 == 0) {
         for (uint32_t j = 0; j < 12; ++j) {
             if (ds.bits[j] != ds.bits[j % 3]) return 0;
             if (ds.bitpos[j] != 16 * (j / 3) + (j % 3 == 0 ? 0 : j % 3 == 1 ? ds.bits[0] : ds.bits[0] + ds.bits[1])) return 0;
@@ -109,7 +109,8 @@ uint32_t tile_pair_layout(ScanVariant v, const DevSpec& ds) {
         const uint32_t b[3] = {ds.bits[0], ds.bits[1], ds.bits[2]};
         const bool named = (b[0] == 6 && b[1] == 5 && b[2] == 5) || (b[0] == 6 && b[1] == 6 && b[2] == 4) ||
                            (b[0] == 5 && b[1] == 5 && b[2] == 5);
-        return named ? ds.E / 4 : 0; // the compile-time geometries that implement it
+        if (!named) return 0; // the compile-time geometries that implement it
+        return v == VAR_F16X4H_C16Q ? (ds.E / 4) | TILE_QUAD : ds.E / 4;
     }
     return 0;
 }
@@ -149,6 +150,7 @@ size_t tile_entry_bytes(ScanVariant v) {
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4:
+    case VAR_F16X4H_C16Q:
     case VAR_F16X4_C4: return 2;
     case VAR_F16X4H_C4D: return 4; // two copies of a 2-byte entry
     case VAR_F32X2: return 4;
@@ -188,6 +190,7 @@ void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, uint32_t pair, cons
     case VAR_F16X4H:
     case VAR_F16X4H_C2:
     case VAR_F16X4H_C4:
+    case VAR_F16X4H_C16Q:
         return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream, 1, pair);
     case VAR_F16X4H_C4D: return launch_pack<__half>(qlut, width, E, n_rows, tq, filter_shift, out, stream, 2);
     case VAR_F32X2: return launch_pack<float>(qlut, width, E, n_rows, tq, 0, out, stream);

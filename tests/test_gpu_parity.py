@@ -818,7 +818,7 @@ def test_concurrent_calls_on_one_handle_serialise():
 
 @pytest.mark.parametrize("dims,text,variants", [
     (128, "16x{4,4}", [0, 1, 2, 3, 7, 9]),       # f16x8, f32x2, u16x1, u8x1, f16x4-c4, merged pair tables (default)
-    (96, "12x{6,5,5}", [1, 2, 3, 4, 5, 6, 8, 10]),   # f32x2, u16x1, u8x1, f16x4h, -c2, -c4, -c4d, merged quad
+    (96, "12x{6,5,5}", [1, 2, 3, 4, 5, 6, 8, 10, 11]),   # f32x2, u16x1, u8x1, f16x4h, -c2, -c4, -c4d, merged quad, 16-row quad
     (64, "12x{6,6,4}", [1, 2, 4, 5, 10]),        # f32x2, u16x1, f16x4h, -c2, merged quad (default)
     (60, "12x{5,5,5}", [1, 2, 4, 5, 10]),        # f32x2, u16x1, f16x4h, -c2, merged quad (default)
     (64, "8x{8,8}", [2, 3, 6]),                  # u16x1, u8x1, f16x4h-c4 (default)
@@ -875,8 +875,8 @@ def test_randomised_search_parameters_vs_oracle(port, dims, text):
             assert bits_equal(got.dists[qi, :c], want[1][qi, :c]), (n, nq, r, t, qi)
 
 
-@pytest.mark.parametrize("dims,text,variants", [(96, "12x{6,5,5}", [1, 2, 4, 5, 6, 8]), (64, "12x{6,6,4}", [4, 5, 6]),
-                                                (60, "12x{5,5,5}", [4, 5, 6]), (64, "8x{8,8}", [2, 6]),
+@pytest.mark.parametrize("dims,text,variants", [(96, "12x{6,5,5}", [1, 2, 4, 5, 6, 8, 11]), (64, "12x{6,6,4}", [4, 5, 6, 11]),
+                                                (60, "12x{5,5,5}", [4, 5, 6, 11]), (64, "8x{8,8}", [2, 6]),
                                                 (64, "16x{4,4}", [0, 1, 7])])
 def test_every_ivf_tile_layout_is_exact(port, dims, text, variants):
     """The IVF batch path writes its LUT tiles itself (fused quantize + pack): every tile layout it can be asked
