@@ -547,21 +547,26 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
             const ScanVariant cand[4] = {VAR_F16X4H, VAR_F16X4H_C2, c32, VAR_F16X4H_C16Q};
             const uint32_t rows[4] = {128, 64, 32, 16};
             const double per_pair[4] = {1.0 / 1.13, 1.0 / 1.30, 1.0 / rate32, 1.0 / 1.25}; // measured flat-scan rates (T pairs/s)
+            // one pass over the cells for all tile heights (this runs on the host between two kernels)
+            const int ncand = have16 ? 4 : 3;
+            double cost[4] = {0.0, 0.0, 0.0, 0.0};
+            for (uint32_t c = 0; c < K; ++c) {
+                const uint32_t np_c = npairs[c];
+                if (!np_c) continue;
+                const double w = double(h->list_count_h[c]) + 2048.0;
+                for (int v = 0; v < ncand; ++v) cost[v] += double((np_c + rows[v] - 1) & ~(rows[v] - 1)) * w;
+            }
             double best = -1.0;
             int pick = int(plan.variant) - int(VAR_F16X4H);
-            for (int v = 0; v < (have16 ? 4 : 3); ++v) {
+            for (int v = 0; v < ncand; ++v) {
                 try {
                     (void)plan_scan(ds, h->device, int(cand[v])); // does this tile height fit shared memory?
                 } catch (const Error&) {
                     continue;
                 }
-                double cost = 0.0;
-                for (uint32_t c = 0; c < K; ++c)
-                    if (npairs[c])
-                        cost += double((npairs[c] + rows[v] - 1) / rows[v]) * rows[v] * (double(h->list_count_h[c]) + 2048.0);
-                cost *= per_pair[v];
-                if (best < 0.0 || cost < best) {
-                    best = cost;
+                const double cst = cost[v] * per_pair[v];
+                if (best < 0.0 || cst < best) {
+                    best = cst;
                     pick = v;
                 }
             }
