@@ -905,3 +905,30 @@ def test_every_ivf_tile_layout_is_exact(port, dims, text, variants):
             assert bits_equal(got.dists, want[1]), v
             ran += 1
         assert ran >= 2
+
+
+@pytest.mark.parametrize("dims,text", [(96, "12x{6,5,5}"), (64, "12x{6,6,4}"), (60, "12x{5,5,5}"), (64, "8x{8,8}"),
+                                       (64, "16x{4,4}"), (32, "8x{8}")])
+def test_randomised_ivf_parameters_vs_oracle(port, dims, text):
+    """Random (cells, n, nq, probes, r, t) for the IVF batch path with the planner's own choices: few and many rows
+    per cell (every tile height gets picked somewhere), probes from 1 to all cells, r = 1 .. 300, t = r .. > n,
+    empty and one-code lists."""
+    rng = np.random.default_rng(abs(hash(text)) % 7919)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 1.3).astype(np.float32)
+    for k_cells, n, nq, probes, r, t in [(3, 50, 2, 3, 1, 1), (17, 4000, 40, 4, 10, 10), (64, 50000, 300, 2, 100, 400),
+                                         (600, 90000, 25, 37, 300, 300), (9, 30000, 513, 9, 50, 16000),
+                                         (200, 2500, 64, 200, 5, 40)]:
+        coarse = (rng.standard_normal((k_cells, dims)) * 3).astype(np.float32)
+        empty = (1,) if k_cells > 2 else ()
+        packed, boff, ioff, counts, ids = _ivf_lists(rng, s, k_cells, n, empty=empty)
+        hot = rng.integers(0, k_cells, size=max(2, k_cells // 8))
+        queries = (coarse[hot[rng.integers(0, len(hot), size=nq)]] + rng.standard_normal((nq, dims)) * 1.5).astype(np.float32)
+        want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=probes, r=r, t=t, threads=8)
+        with qb.IvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids) as idx:
+            got = idx.search(queries, qb.SearchParams(probes=probes, r=r, t=t))
+        assert np.array_equal(got.counts, want[2]), (k_cells, n, nq, probes, r, t)
+        for qi in range(nq):
+            c = int(want[2][qi])
+            assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]), (k_cells, n, nq, probes, r, t, qi)
+            assert bits_equal(got.dists[qi, :c], want[1][qi, :c]), (k_cells, n, nq, probes, r, t, qi)
