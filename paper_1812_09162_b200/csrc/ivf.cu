@@ -523,7 +523,12 @@ ivf_seed_kernel(DevSpec ds, const uint8_t* __restrict__ codes, const uint32_t* _
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint8_t* code = codes + (base + i) * ds.code_stride;
         uint32_t acc = bias;
-        for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + code_field(ds, code, j)];
+        if (ds.code_stride == 8) {
+            const uint2 cw = *reinterpret_cast<const uint2*>(code);
+            for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + code_field64(ds, cw.x, cw.y, j)];
+        } else {
+            for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + code_field(ds, code, j)];
+        }
         keys[i] = make_key(min(acc, ds.qmax), ids[base + i]);
     }
     __syncthreads();

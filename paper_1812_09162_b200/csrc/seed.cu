@@ -34,7 +34,12 @@ seed_topk_kernel(DevSpec ds, const uint8_t* __restrict__ codes, uint32_t n_head,
     for (uint32_t i = threadIdx.x; i < n_head; i += blockDim.x) {
         const uint8_t* code = codes + size_t(i) * ds.code_stride;
         uint32_t acc = bias;
-        for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + code_field(ds, code, j)];
+        if (ds.code_stride == 8) {
+            const uint2 cw = *reinterpret_cast<const uint2*>(code);
+            for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + code_field64(ds, cw.x, cw.y, j)];
+        } else {
+            for (uint32_t j = 0; j < ds.m; ++j) acc += table[ds.ent_off[j] + code_field(ds, code, j)];
+        }
         acc = min(acc, ds.qmax); // == the chain of saturating adds (all terms unsigned)
         keys[i] = make_key(acc, ids ? ids[i] : id_base + i);
     }

@@ -118,4 +118,11 @@ __device__ __forceinline__ uint32_t code_field(const DevSpec& ds, const uint8_t*
     return (w >> (bp & 31u)) & ((1u << ds.bits[j]) - 1u);
 }
 
+// the same for a 64-bit code already in two registers (one 8-byte load per code instead of one load per field)
+__device__ __forceinline__ uint32_t code_field64(const DevSpec& ds, uint32_t lo, uint32_t hi, uint32_t j) {
+    const uint32_t bp = ds.bitpos[j];
+    const uint32_t w = (bp >> 5) ? hi : lo;
+    return (w >> (bp & 31u)) & ((1u << ds.bits[j]) - 1u);
+}
+
 } // namespace qadc
