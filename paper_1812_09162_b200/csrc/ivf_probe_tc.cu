@@ -174,10 +174,11 @@ probe_select_tc_kernel(const float* __restrict__ approx, const double* __restric
             }
             __syncthreads();
         }
-    const double limit = double(mins[a - 1]) + eps2[qi]; // a <= min(256, K) guaranteed by the launcher
+    // a <= min(256, K) guaranteed by the launcher; rounded UP to fp32 (a superset of candidates is always safe)
+    const float limit = __double2float_ru(double(mins[a - 1]) + eps2[qi]);
     for (uint32_t base = 0; base < k_cells; base += 256) {
         const uint32_t c = base + tid;
-        const bool take = c < k_cells && !(double(d[c]) > limit); // NaN stays a candidate
+        const bool take = c < k_cells && !(d[c] > limit); // NaN stays a candidate
         const uint32_t bal = __ballot_sync(0xffffffffu, take);
         if (bal) {
             uint32_t start = 0;
