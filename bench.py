@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the Quicker ADC scan path on B200 (metric of BASELINE.json).
 
-    python bench.py --gpus N --steps K --warmup W [--workload c2] [--impl reference]
+    python bench.py --gpus N --steps K --warmup W [--workload c4] [--scaling strong|weak] [--impl reference]
 
 A "step" is one pass of the whole hot path (distance tables -> calibration -> quantization -> scan ->
 top-R [-> multi-GPU merge]) over one batch of synthetic queries against the resident database.
@@ -11,16 +11,22 @@ top-R [-> multi-GPU merge]) over one batch of synthetic queries against the resi
 ``roofline``= algorithmic code bytes (8 B per pair) / CUDA-event time of the scan kernels, against the
               measured HBM copy bandwidth of MEASURED_PEAKS.json;
 ``cpu_baseline`` = the reference's own CPU search (oracle/_ref when it was built, else the oracle port)
-              timed on this box's host cores on a bounded query sample of the same workload.
+              timed on this box's host cores on a bounded query sample of the same workload;
+``parity``  = after (outside) the timed region, a seeded sample of the just-benchmarked queries is searched by the
+              reference on the CPU and compared with the GPU result (ids, distance bits, counts); a mismatch
+              makes the exit code non-zero.
 
 Workloads (BASELINE.json configs; seeded synthetic inputs with the named shapes stand in for the
-SIFT/Deep-like data, see paper_1812_09162_b200/synth.py):
+SIFT/Deep-like data, see paper_1812_09162_b200/synth.py).  N is the size of the WHOLE database:
   c1  16x{4,4}    d=128  N=1e6   Q=1e3     c3  8x{8,8}   d=128  N=1e7  Q=1e4
   c2  12x{6,5,5}  d=96   N=1e7   Q=1e4     c4  16x{4,4}  d=128  N=2e8  Q=1e4 (uniform random codes)
-  c5  IVF K=16384, 12x{6,5,5} residual codes, d=128, N=6.25e7 per GPU (5e8 / 8), nprobe=64, Q=1e4
-Default c2 (configs[1]).  With --gpus N > 1 (torchrun, one rank per GPU) every rank holds one database
-shard of the per-GPU size above (weak scaling), queries are replicated and the per-query top-R lists are
-merged after one NCCL all_gather (IVF: every list is split across the ranks, list heads are replicated).
+  c5  IVF K=16384, 12x{6,5,5} residual codes, d=128, N=5e8, nprobe=64, Q=1e4
+  c5g the share of c5 one GPU of the 8-GPU box holds (N = 5e8 / 8 = 6.25e7): the single-GPU form of config 5
+Default c4: the largest single-GPU configuration and the one BASELINE's 1/2/4/8-GPU clause is written on.
+With --gpus N > 1 (torchrun, one rank per GPU) the ONE database of the workload is split evenly over the N ranks on
+packed-block boundaries (``"scaling": "strong"``: 2e8 / N codes per GPU for c4; IVF: every list is split N ways, list
+heads are replicated), queries are replicated and the per-query top-R lists are merged after one NCCL all_gather.
+``--scaling weak`` keeps the workload's N per GPU instead (N times the database).
 """
 from __future__ import annotations
 
@@ -43,10 +49,15 @@ WORKLOADS = {
     "c2": dict(kind="flat", spec="12x{6,5,5}", dims=96, n=10_000_000, nq=10_000, data="encoded"),
     "c3": dict(kind="flat", spec="8x{8,8}", dims=128, n=10_000_000, nq=10_000, data="encoded"),
     "c4": dict(kind="flat", spec="16x{4,4}", dims=128, n=200_000_000, nq=10_000, data="random"),
-    "c5": dict(kind="ivf", spec="12x{6,5,5}", dims=128, n=62_500_000, nq=10_000, data="random", k_cells=16384,
+    "c5": dict(kind="ivf", spec="12x{6,5,5}", dims=128, n=500_000_000, nq=10_000, data="random", k_cells=16384,
                probes=64),
+    "c5g": dict(kind="ivf", spec="12x{6,5,5}", dims=128, n=62_500_000, nq=10_000, data="random", k_cells=16384,
+                probes=64),
 }
 R, T = int(os.environ.get("QADC_BENCH_R", 100)), int(os.environ.get("QADC_BENCH_T", 400))  # BASELINE: R=100, t=400 (env: experiments only)
+CHUNK = 1 << 20   # the database is generated in chunks of this many codes, each from its own seed, so that any
+                  # rank can produce any code range of the ONE database without the others' random streams
+HEAD_MAX = 16384  # replicated calibration head (QADC_MAX_T): serves every t the ABI accepts
 
 
 def log(*a):
@@ -55,15 +66,20 @@ def log(*a):
 
 # ----------------------------------------------------------------------------- data --
 
-def make_flat(qb, spec, wl, rank, have_gpu):
-    """Packed shard for this rank (seeded by rank) + the global head (rank 0's first codes)."""
+def make_flat(qb, spec, wl, have_gpu, start=0, count=None, whole=False):
+    """Codes [start, start + count) of the workload's ONE database as a PackedList (start on a block boundary),
+    plus the global calibration head (the database's first codes).  whole=True also returns the complete database
+    (rank 0 keeps it for the CPU parity check when the database is sharded)."""
     from paper_1812_09162_b200 import synth
     dims, n = wl["dims"], wl["n"]
+    count = n - start if count is None else count
     centres = synth.mixture_centres(dims, seed=1)
     train = synth.gaussian_mixture(100_000, dims, seed=4, centres=centres)
     t0 = time.time()
     cb = synth.train_codebook(spec, train, iters=8, seed=5)
     log(f"[bench] codebook ({spec.cb_floats} floats) trained in {time.time() - t0:.1f}s")
+    code_bytes = spec.groups * (spec.word_width // 8)
+    assert CHUNK % spec.block_len == 0 and start % spec.block_len == 0
 
     def encode(vecs):
         if have_gpu:
@@ -72,38 +88,40 @@ def make_flat(qb, spec, wl, rank, have_gpu):
         o = Oracle("port")
         return o.encode(o.spec(dims, wl["spec"]), cb, vecs)
 
-    def shard_codes(r, count):
-        parts, done, batch, b = [], 0, 500_000, 0
-        while done < count:
-            nb = min(batch, count - done)
-            parts.append(encode(synth.gaussian_mixture(nb, dims, seed=2 + 1000 * r + b, centres=centres)))
-            done += nb
-            b += 1
-        return np.concatenate(parts)
+    def chunk_packed(c):
+        """PackedList bytes of chunk c = codes [c * CHUNK, min((c + 1) * CHUNK, n)) -- whole blocks except at the end."""
+        cn = min(CHUNK, n - c * CHUNK)
+        if wl["data"] == "random":
+            return synth.random_packed(spec, cn, seed=6 + 1000 * c)
+        return qb.pack_list(spec, encode(synth.gaussian_mixture(cn, dims, seed=2 + 1000 * c, centres=centres)))
+
+    def range_packed(lo, hi):
+        parts = []
+        for c in range(lo // CHUNK, (max(hi, lo + 1) - 1) // CHUNK + 1):
+            pk = chunk_packed(c)
+            c0 = c * CHUNK
+            a_, b_ = max(lo, c0) - c0, min(hi, c0 + CHUNK) - c0  # block-aligned except possibly b_ == chunk end
+            parts.append(pk[a_ * code_bytes: qb.packed_bytes(spec, b_)] if a_ else pk[: qb.packed_bytes(spec, b_)])
+        return np.concatenate(parts) if parts else np.zeros(0, np.uint8)
 
     t0 = time.time()
-    if wl["data"] == "random":
-        packed = synth.random_packed(spec, n, seed=6 + 1000 * rank)
-        # the global head (first codes of rank 0's shard) comes from its own seed so that every rank can
-        # regenerate it without rank 0's stream; rank 0 splices it in front of its shard
-        head_n = min(4096, n) // spec.block_len * spec.block_len
-        head = synth.random_packed(spec, head_n, seed=600)
-        if rank == 0:
-            packed[: head.size] = head
+    full = range_packed(0, n) if whole or (start == 0 and count == n) else None
+    if full is not None and start == 0 and count == n:
+        packed = full
+    elif full is not None:
+        packed = full[start * code_bytes: start * code_bytes + qb.packed_bytes(spec, count)]
     else:
-        codes = shard_codes(rank, n)
-        packed = qb.pack_list(spec, codes)
-        head_n = min(4096, n)
-        head_codes = codes[:head_n] if rank == 0 else shard_codes(0, min(head_n, 500_000))[:head_n]
-        head = qb.pack_list(spec, head_codes)
-    log(f"[bench] rank {rank}: database shard of {n} codes ready in {time.time() - t0:.1f}s")
+        packed = range_packed(start, start + count)
+    head_n = min(HEAD_MAX, n)
+    head = (full if full is not None else range_packed(0, min(n, CHUNK)))[: qb.packed_bytes(spec, head_n)]
+    log(f"[bench] codes [{start}, {start + count}) of {n} ready in {time.time() - t0:.1f}s")
     queries = synth.gaussian_mixture(wl["nq"], dims, seed=3, centres=centres)
-    return dict(cb=cb, packed=packed, head=head, head_n=head_n, queries=queries)
+    return dict(cb=cb, packed=packed, head=head, head_n=head_n, queries=queries, full=full)
 
 
-def make_ivf(qb, spec, wl, have_gpu, rank=0, world=1):
-    """Config 5 stand-in: coarse centroids from Lloyd iterations on mixture samples, list sizes from the
-    assignment histogram of a mixture sample scaled to N, uniform random residual codes, ids = positions."""
+def make_ivf(qb, spec, wl, have_gpu, bcast=None):
+    """Config 5 stand-in (the WHOLE index): coarse centroids from Lloyd iterations on mixture samples, list sizes
+    from the assignment histogram of a mixture sample scaled to N, uniform random residual codes, ids = positions."""
     from paper_1812_09162_b200 import synth
     import torch
     dims, n, K = wl["dims"], wl["n"], wl["k_cells"]
@@ -134,27 +152,19 @@ def make_ivf(qb, spec, wl, have_gpu, rank=0, world=1):
     counts = np.floor(hist / hist.sum() * n).astype(np.uint64)
     counts[: int(n - counts.sum())] += 1
     cb = synth.train_codebook(spec, resid, iters=6, seed=5)
+    if bcast is not None:  # Lloyd on the GPU uses float atomics: every rank must hold rank 0's index, bit for bit
+        coarse, cb, counts = bcast(coarse), bcast(cb), bcast(counts.astype(np.int64)).astype(np.uint64)
     log(f"[bench] coarse quantizer (K={K}) + residual codebook in {time.time() - t0:.1f}s; "
         f"list sizes min/median/max = {counts.min()}/{int(np.median(counts))}/{counts.max()}")
     t0 = time.time()
     pbytes = np.array([qb.packed_bytes(spec, int(c)) for c in counts], dtype=np.uint64)
     boff = np.concatenate([[0], np.cumsum(pbytes)[:-1]]).astype(np.uint64)
     ioff = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
-    packed0 = np.random.default_rng(6).integers(0, 256, size=int(pbytes.sum()), dtype=np.uint8)
-    packed = packed0 if rank == 0 else np.random.default_rng(6 + 1000 * rank).integers(
-        0, 256, size=int(pbytes.sum()), dtype=np.uint8)
-    ids = np.arange(n, dtype=np.uint32) + np.uint32(rank * n)
+    packed = np.random.default_rng(6).integers(0, 256, size=int(pbytes.sum()), dtype=np.uint8)  # same stream on every rank
+    ids = np.arange(n, dtype=np.uint32)
     out = dict(cb=cb, coarse=coarse, packed=packed, boff=boff, ioff=ioff, counts=counts, ids=ids)
-    if world > 1:
-        # weak scaling: rank r holds the r-th slice of EVERY list (same slice lengths on every rank); the heads of
-        # the unsharded lists are rank 0's first codes, regenerated from rank 0's stream on every rank
-        hc = np.minimum(counts, 512).astype(np.uint64)
-        hbytes = np.array([qb.packed_bytes(spec, int(c)) for c in hc], dtype=np.uint64)
-        hoff = np.concatenate([[0], np.cumsum(hbytes)[:-1]]).astype(np.uint64)
-        heads = np.concatenate([packed0[int(b): int(b) + int(hb)] for b, hb in zip(boff, hbytes)])
-        out.update(calib_packed=heads, calib_byte_off=hoff, calib_count=hc)
     out["queries"] = synth.gaussian_mixture(wl["nq"], dims, seed=3, centres=centres)
-    log(f"[bench] rank {rank}: {n} residual codes in {K} lists ready in {time.time() - t0:.1f}s")
+    log(f"[bench] {n} residual codes in {K} lists ready in {time.time() - t0:.1f}s")
     return out
 
 
@@ -225,13 +235,16 @@ class CpuReference:
             self.h = self.o.ivf_open(self.s, data["cb"], data["coarse"], data["packed"], data["boff"], data["ioff"],
                                      data["counts"], data["ids"])
         else:
-            self.h = self.o.flat_open(self.s, data["cb"], data["packed"], wl["n"])
+            self.h = self.o.flat_open(self.s, data["cb"], data["full"] if data.get("full") is not None else data["packed"],
+                                      wl["n"])
         self.family = self.o.auto_family(self.s) if self.kind == "reference" else "scalar-quantized (C port)"
+
+    def search(self, queries):
+        return self.o.search_h(self.h, queries, probes=self.wl.get("probes", 1), r=R, t=T, family=1, threads=self.cores)
 
     def run(self, nq):
         t0 = time.perf_counter()
-        self.o.search_h(self.h, self.queries[:nq], probes=self.wl.get("probes", 1), r=R, t=T, family=1,
-                        threads=self.cores)
+        self.search(self.queries[:nq])
         return time.perf_counter() - t0
 
     def sized_sample(self, budget_s, cap=None):
@@ -249,101 +262,89 @@ class CpuReference:
         return float(np.mean([lens[self.o.probe_order(self.wl["dims"], data["coarse"], q, self.wl["probes"])].sum()
                               for q in qs]))
 
+    def parity(self, got_ids, got_dists, got_counts, n_sample):
+        """Seeded sample of the benchmarked queries: reference result vs the GPU's (ids, distance bits, counts)."""
+        nq = len(self.queries)
+        sel = np.sort(np.random.default_rng(12345).choice(nq, size=min(n_sample, nq), replace=False))
+        ids, dists, counts = self.search(self.queries[sel])
+        bad = 0
+        for k, qi in enumerate(sel):
+            c = int(counts[k])
+            ok = int(got_counts[qi]) == c and np.array_equal(got_ids[qi, :c], ids[k, :c]) and \
+                got_dists[qi, :c].tobytes() == dists[k, :c].tobytes()
+            bad += 0 if ok else 1
+        return {"queries": int(len(sel)), "mismatches": int(bad), "oracle": self.kind,
+                "compared": "ids, distance bits and counts of a seeded query sample, after the timed region"}
+
     def close(self):
         self.o.close_h(self.h)
 
 
 # ------------------------------------------------------------------------------ main --
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=os.environ.get("QADC_WORKLOAD", "c2"), choices=sorted(WORKLOADS))
-    ap.add_argument("--n", type=int, default=0, help="override codes per GPU (debug)")
-    ap.add_argument("--nq", type=int, default=0, help="override query count (debug)")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--option", action="append", default=[], help="name=value passed to qadc_set_option")
-    args = ap.parse_args()
-    if args.impl == "ours":
-        args.warmup = max(args.warmup, 3)
-
-    wl = dict(WORKLOADS[args.workload])
-    if args.n:
-        wl["n"] = args.n
-    if args.nq:
-        wl["nq"] = args.nq
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+def describe(name, wl, world, scaling):
+    """The `config` object: identical in both arms (ours / reference) for one workload."""
     ivf = wl["kind"] == "ivf"
+    per_gpu = wl["n"] if scaling == "weak" else (wl["n"] + world - 1) // world
+    return {"workload": f"{name}: " + (f"IVF K={wl['k_cells']} nprobe={wl['probes']} " if ivf else "") +
+                        f"{wl['spec']} d={wl['dims']} N={wl['n'] * (world if scaling == 'weak' else 1)} Q={wl['nq']} R={R} t={T}",
+            "spec": wl["spec"], "dims": wl["dims"], "database_codes": wl["n"] * (world if scaling == "weak" else 1),
+            "codes_per_gpu": per_gpu, "queries": wl["nq"], "r": R, "t": T,
+            "database": "gaussian-mixture vectors encoded with k-means codebooks" if wl["data"] == "encoded"
+            else "uniform random codes", "sharding": f"db{world}" if world > 1 else "none"}
 
-    if args.impl == "reference" and rank != 0:
-        return 0
 
-    import paper_1812_09162_b200 as qb
-    qb.build()
-    have_gpu = qb.lib().qadc_device_count() > 0
+def run_ours(qb, name, wl, args, rank, local_rank, world, dist):
+    """One workload on the GPU path; returns the JSON object (rank 0) or None."""
+    import torch
+    from paper_1812_09162_b200.dist import ShardedFlatIndex, ShardedIndex, ShardRange, shard_ivf_lists, shard_ranges
+    ivf = wl["kind"] == "ivf"
     spec = qb.allocate_dims(wl["dims"], wl["spec"])
     dtype = "u16" if spec.word_width == 16 else "u8"
-    config = {"workload": f"{args.workload}: " + (f"IVF K={wl['k_cells']} nprobe={wl['probes']} " if ivf else "") +
-                          f"{wl['spec']} d={wl['dims']} N={wl['n']}/GPU Q={wl['nq']} R={R} t={T}",
-              "spec": wl["spec"], "dims": wl["dims"], "codes_per_gpu": wl["n"], "queries": wl["nq"], "r": R, "t": T,
-              "database": "gaussian-mixture vectors encoded with k-means codebooks" if wl["data"] == "encoded"
-              else "uniform random codes", "sharding": f"db{world}" if world > 1 else "none"}
-
-    # -------------------------------------------------------------- reference arm --
-    if args.impl == "reference":
-        data = make_ivf(qb, spec, wl, have_gpu) if ivf else make_flat(qb, spec, wl, 0, have_gpu)
-        cpu = CpuReference(wl, data)
-        nq_step = cpu.sized_sample(6.0)
-        ppq = cpu.pairs_per_query(data, nq_step)
-        times = []
-        for i in range(args.warmup + args.steps):
-            dt = cpu.run(nq_step)
-            if i >= args.warmup:
-                times.append(dt)
-        tot_t = sum(times)
-        value = ppq * nq_step * len(times) / tot_t
-        print(json.dumps({
-            "impl": "reference", "metric": "ADC codes scanned/s", "value": value, "unit": "codes/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * tot_t / max(len(times), 1), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": dtype, "data": "synthetic", "config": config,
-            "cpu_baseline": {"value": value, "unit": "codes/s", "cores": cpu.cores, "kind": cpu.kind,
-                             "sample": f"each step: {nq_step} of {wl['nq']} queries, kernel {cpu.family}"},
-            "e2e": {"value": value, "unit": "codes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
-        cpu.close()
-        return 0
-
-    # --------------------------------------------------------------------- our arm --
-    import torch
-    if not have_gpu:
-        raise SystemExit("bench.py: no CUDA device; the product has no CPU path (use --impl reference for the CPU arm)")
-    torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+    weak = args.scaling == "weak" and world > 1
+    want_cpu = rank == 0 and not args.no_cpu_baseline and (world == 1 or not args.no_parity)
     params = qb.SearchParams(probes=wl.get("probes", 1), r=R, t=T)
-    t0 = time.time()
+
+    def bcast(arr):
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+        dist.broadcast(t, 0)
+        return t.cpu().numpy()
+
     if ivf:
-        from paper_1812_09162_b200.dist import ShardedIndex
-        data = make_ivf(qb, spec, wl, have_gpu, rank, world)
+        data = make_ivf(qb, spec, wl, True, bcast if world > 1 else None)
         t0 = time.time()
-        idx = qb.IvfIndex(spec, data["cb"], data["coarse"], data["packed"], data["boff"], data["ioff"],
-                          data["counts"], data["ids"], device=local_rank, calib_packed=data.get("calib_packed"),
-                          calib_byte_off=data.get("calib_byte_off"), calib_count=data.get("calib_count"))
+        if world > 1 and not weak:
+            kw = shard_ivf_lists(spec, data["packed"], data["boff"], data["ioff"], data["counts"], data["ids"], rank,
+                                 world, t_max=max(4096, T))
+            idx = qb.IvfIndex(spec, data["cb"], data["coarse"], kw["packed"], kw["list_byte_off"], kw["list_id_off"],
+                              kw["list_count"], kw["ids"], device=local_rank, calib_packed=kw["calib_packed"],
+                              calib_byte_off=kw["calib_byte_off"], calib_count=kw["calib_count"],
+                              global_list_count=kw["global_list_count"])
+            del kw
+        else:
+            # weak: every rank holds a whole index of the workload's size (ids offset per rank); its own heads are
+            # the calibration heads, so every rank derives the same map only if the codes agree -- they do (same seed)
+            ids = data["ids"] + np.uint32(rank * wl["n"]) if weak else data["ids"]
+            idx = qb.IvfIndex(spec, data["cb"], data["coarse"], data["packed"], data["boff"], data["ioff"],
+                              data["counts"], ids, device=local_rank)
         sharded = ShardedIndex(idx, local_rank) if world > 1 else None
     else:
-        from paper_1812_09162_b200.dist import ShardedFlatIndex, ShardRange
-        data = make_flat(qb, spec, wl, rank, have_gpu)
-        t0 = time.time()
-        sharded = ShardedFlatIndex(spec, data["cb"], data["packed"], ShardRange(rank * wl["n"], wl["n"]), data["head"],
-                                   data["head_n"], local_rank)
+        if weak:
+            data = make_flat(qb, spec, wl, True)
+            shard = ShardRange(rank * wl["n"], wl["n"])
+            t0 = time.time()
+            sharded = ShardedFlatIndex(spec, data["cb"], data["packed"], shard, data["head"], data["head_n"], local_rank,
+                                       global_count=wl["n"] * world)
+        else:
+            rg = shard_ranges(wl["n"], world, spec.block_len)[rank]
+            data = make_flat(qb, spec, wl, True, rg.start, rg.count, whole=want_cpu)
+            t0 = time.time()
+            sharded = ShardedFlatIndex(spec, data["cb"], data["packed"], rg, data["head"], data["head_n"], local_rank,
+                                       global_count=wl["n"])
         idx = sharded.index
+        if world == 1:
+            sharded = None  # one GPU: the plain index, no merge step
     for opt in args.option:
         k, v = opt.split("=")
         idx.set_option(k, int(v))
@@ -401,13 +402,16 @@ def main():
         w1 = time.time()
         clk = clocks.summary(w0, w1)
     ms = ev0.elapsed_time(ev1)
+    pairs_rank = torch.tensor([float(st_acc["pairs"])], dtype=torch.float64, device=dev)
     if world > 1:
         tmax = torch.tensor([ms], device=dev)
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         ms = float(tmax.item())
-    pairs_per_step = st_acc["pairs"] / args.steps  # flat: N*Q per rank; IVF: sum of probed list lengths
-    total_pairs = pairs_per_step * world * args.steps
+        dist.all_reduce(pairs_rank, op=dist.ReduceOp.SUM)  # strong scaling: the shards' pairs add up to the database's
+    total_pairs = float(pairs_rank.item())
+    pairs_per_step = total_pairs / args.steps  # flat: N*Q; IVF: sum over queries of the probed lists' lengths
     value = total_pairs / (ms * 1e-3)
+    got = (d_ids.cpu().numpy().view(np.uint32), d_dists.cpu().numpy(), d_counts.cpu().numpy().astype(np.uint32))
 
     # ---- e2e: the host-buffer C-ABI call (H2D + D2H inside), same metric ----
     h_q = torch.from_numpy(queries).pin_memory()
@@ -443,6 +447,17 @@ def main():
         e2e_ms = float(tmax.item())
     e2e_value = total_pairs / (e2e_ms * 1e-3)
 
+    # single-query latency through the host-buffer call (the reference's own calling pattern: one search per query)
+    lat_ms = None
+    if world == 1:
+        q1 = np.ascontiguousarray(queries[:1])
+        idx.search(q1, params)
+        t0 = time.perf_counter()
+        for i in range(20):
+            idx.search(np.ascontiguousarray(queries[i % nq: i % nq + 1]), params)
+        lat_ms = (time.perf_counter() - t0) * 1e3 / 20
+
+    out = None
     if rank == 0:
         peaks_path = ROOT / "MEASURED_PEAKS.json"
         if peaks_path.exists():
@@ -451,59 +466,180 @@ def main():
             peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
         scan_s = st_acc["ms_scan"] * 1e-3
         achieved = (st_acc["pairs"] * 8.0 / scan_s) / 1e9 if scan_s > 0 else None
-        traffic = None
+        traffic, traffic_src = None, None
         tpath = ROOT / "profiles" / "traffic.json"  # dram__bytes_read+write of the dominant launch, from ncu --set full
         if tpath.exists():
-            traffic = json.loads(tpath.read_text()).get(args.workload)
+            traffic = json.loads(tpath.read_text()).get(name)
+            traffic_src = "profiles/traffic.json (dram__bytes_read.sum + dram__bytes_write.sum of the dominant launch, " \
+                          "one ncu --set full capture of this workload; not measured in this run)"
+        variant = int(idx.stats().scan_variant)
+        vname = qb.lib().qadc_variant_name(variant).decode()
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak if achieved else None, "traffic": traffic, "peak_source": peak_src,
-                    "kernel": "scan_kernel (" + qb.lib().qadc_variant_name(idx.stats().scan_variant).decode() + ")",
+                    "frac": achieved / peak if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
+                    "peak_source": peak_src, "kernel": "scan_kernel (" + vname + ")",
                     "algorithmic_bytes_per_pair": 8,
                     "avg_launch_ms": st_acc["ms_scan"] / max(st_acc["scan_launches"], 1),
                     "stage_ms_per_step": {k: st_acc[k] / args.steps for k in ("ms_lut", "ms_scan", "ms_select")},
                     "admitted_pairs_per_query": st_acc["admitted"] / args.steps / nq,
                     "overflow_retries": st_acc["retries"],
                     "note": "codes are streamed once per query tile and reused from shared memory, so algorithmic bytes "
-                            "exceed DRAM traffic; the kernel's real ceiling is the shared-memory pipe (profiles/)"}
+                            "exceed DRAM traffic; the kernel's real ceiling is on-chip (profiles/)"}
         # the kernel's operative ceiling: table-lookup bytes through the shared-memory pipe (128 B/clk/SM)
-        variant = int(idx.stats().scan_variant)
-        entry_bytes = {0: 2, 1: 4, 2: 2, 3: 1, 4: 2, 5: 2, 6: 2, 7: 2, 8: 2, 9: 2, 10: 2}.get(variant, 2)
+        entry_bytes = {1: 4, 3: 1}.get(variant, 2)
         # merged layouts: 16x{4,4} -> one lookup per code byte (pair sums); 12x{6,5,5} -> two lookups per 16-bit word
         lookups = spec.m // 2 if variant == 9 else spec.m * 2 // 3 if variant == 10 else spec.m
         sm_clock = (clk.get("sm_mhz") or 1965) * 1e6
         prop = torch.cuda.get_device_properties(dev)
         smem_peak = 128.0 * prop.multi_processor_count * sm_clock / 1e9
         smem_ach = (st_acc["pairs"] * lookups * entry_bytes / scan_s) / 1e9 if scan_s > 0 else None
-        roofline["smem"] = {"bound": "shared-memory pipe", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
-                            "frac": smem_ach / smem_peak if smem_ach else None,
-                            "bytes_per_pair": lookups * entry_bytes,
-                            "peak_source": "128 B/clk/SM x SMs x sampled SM clock"}
-        cpu_out = None
-        if world == 1 and not args.no_cpu_baseline:
+        if variant < 12:
+            roofline["smem"] = {"bound": "shared-memory pipe", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
+                                "frac": smem_ach / smem_peak if smem_ach else None,
+                                "bytes_per_pair": lookups * entry_bytes,
+                                "peak_source": "128 B/clk/SM x SMs x sampled SM clock"}
+        cpu_out, parity = None, None
+        if want_cpu:
             cpu = CpuReference(wl, data)
-            nq_s = cpu.sized_sample(12.0)
-            dt = cpu.run(nq_s)
-            cpu_out = {"value": pairs_per_step / nq * nq_s / dt, "unit": "codes/s", "cores": cpu.cores, "kind": cpu.kind,
-                       "sample": f"{nq_s} of {nq} queries, kernel {cpu.family}, {dt:.2f}s"}
+            if world == 1:
+                nq_s = cpu.sized_sample(12.0)
+                dt = cpu.run(nq_s)
+                cpu_out = {"value": pairs_per_step / nq * nq_s / dt, "unit": "codes/s", "cores": cpu.cores,
+                           "kind": cpu.kind, "sample": f"{nq_s} of {nq} queries, kernel {cpu.family}, {dt:.2f}s"}
+            if not args.no_parity:
+                parity = cpu.parity(*got, 64 if ivf else 32)
+                log(f"[bench] parity {name}: {parity}")
             cpu.close()
         out = {
             "metric": "ADC codes scanned/s", "value": value, "unit": "codes/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if weak or world == 1 else "strong",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": dict(config, pairs_per_step=pairs_per_step * world,
-                           l2="flushed between steps (256 MiB write inside the timed region); the code array "
-                              "is also re-streamed once per query tile"),
+            "config": describe(name, wl, world, "weak" if weak else "strong"),
+            "pairs_per_step": pairs_per_step,
+            "l2": "flushed between steps (256 MiB write inside the timed region); the code array is also re-streamed "
+                  "once per query tile",
             "clocks": clk, "gpu_launches": int(st_acc["launches"]),
             "e2e": {"value": e2e_value, "unit": "codes/s", "h2d_bytes_per_step": int(nq * wl["dims"] * 4),
                     "d2h_bytes_per_step": int(nq * R * 8 + nq * 4), "ms_per_step": e2e_ms / args.steps},
-            "roofline": roofline, "cpu_baseline": cpu_out,
+            "roofline": roofline, "cpu_baseline": cpu_out, "parity": parity,
+            "single_query_latency_ms": lat_ms,
             "per_gpu_value": value / world,
         }
+    idx.close()
+    del d_q, d_ids, d_dists, d_counts, flush, data
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=os.environ.get("QADC_WORKLOAD", "c4"), choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: split ONE database over the ranks (default) or keep the workload's N per GPU")
+    ap.add_argument("--also", default=os.environ.get("QADC_ALSO", "c1,c2,c3,c5g"),
+                    help="N = 1: further BASELINE configs measured briefly after the headline one and carried under "
+                         "'other_configs' ('' = none)")
+    ap.add_argument("--n", type=int, default=0, help="override the database size (debug)")
+    ap.add_argument("--nq", type=int, default=0, help="override query count (debug)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--option", action="append", default=[], help="name=value passed to qadc_set_option")
+    args = ap.parse_args()
+    if args.impl == "ours":
+        args.warmup = max(args.warmup, 3)
+
+    wl = dict(WORKLOADS[args.workload])
+    if args.n:
+        wl["n"] = args.n
+    if args.nq:
+        wl["nq"] = args.nq
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    ivf = wl["kind"] == "ivf"
+
+    if args.impl == "reference" and rank != 0:
+        return 0
+
+    import paper_1812_09162_b200 as qb
+    qb.build()
+    have_gpu = qb.lib().qadc_device_count() > 0
+    spec = qb.allocate_dims(wl["dims"], wl["spec"])
+    dtype = "u16" if spec.word_width == 16 else "u8"
+
+    # -------------------------------------------------------------- reference arm --
+    if args.impl == "reference":
+        # the reference's own CPU path on the WHOLE database of the workload (it has no sharding), all host cores
+        scaling = "weak" if args.scaling == "weak" and args.gpus > 1 else "strong"
+        data = make_ivf(qb, spec, wl, have_gpu) if ivf else make_flat(qb, spec, wl, have_gpu)
+        cpu = CpuReference(wl, data)
+        nq_step = cpu.sized_sample(6.0)
+        ppq = cpu.pairs_per_query(data, nq_step)
+        times = []
+        for i in range(args.warmup + args.steps):
+            dt = cpu.run(nq_step)
+            if i >= args.warmup:
+                times.append(dt)
+        tot_t = sum(times)
+        value = ppq * nq_step * len(times) / tot_t
+        print(json.dumps({
+            "impl": "reference", "metric": "ADC codes scanned/s", "value": value, "unit": "codes/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_t / max(len(times), 1), "higher_is_better": True,
+            "scaling": "weak" if scaling == "weak" or args.gpus == 1 else "strong",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": describe(args.workload, wl, args.gpus, scaling),
+            "cpu_baseline": {"value": value, "unit": "codes/s", "cores": cpu.cores, "kind": cpu.kind,
+                             "sample": f"each step: {nq_step} of {wl['nq']} queries, kernel {cpu.family}"},
+            "e2e": {"value": value, "unit": "codes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        cpu.close()
+        return 0
+
+    # --------------------------------------------------------------------- our arm --
+    import torch
+    if not have_gpu:
+        raise SystemExit("bench.py: no CUDA device; the product has no CPU path (use --impl reference for the CPU arm)")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    out = run_ours(qb, args.workload, wl, args, rank, local_rank, world, dist)
+    rc = 0
+    if rank == 0:
+        if out["parity"] and out["parity"]["mismatches"]:
+            rc = 3
+        others = []
+        if world == 1 and args.also and not args.n and not args.nq:
+            # the other BASELINE configs, briefly (2 steps, no CPU timing; parity still checked): context for the
+            # headline line, each a complete line of its own under "other_configs"
+            import copy
+            a2 = copy.copy(args)
+            a2.steps, a2.warmup, a2.no_cpu_baseline = 3, 3, False
+            for name in [x for x in args.also.split(",") if x and x != args.workload]:
+                try:
+                    a2.no_cpu_baseline = False
+                    o = run_ours(qb, name, dict(WORKLOADS[name]), a2, 0, local_rank, 1, None)
+                    keep = ("value", "unit", "ms_per_step", "steps", "warmup", "dtype", "config", "pairs_per_step",
+                            "gpu_launches", "e2e", "parity", "single_query_latency_ms", "cpu_baseline")
+                    rec = {k: o[k] for k in keep}
+                    rec["roofline"] = {k: o["roofline"][k] for k in ("achieved", "peak", "frac", "kernel", "stage_ms_per_step")}
+                    others.append(rec)
+                    if o["parity"] and o["parity"]["mismatches"]:
+                        rc = 3
+                except Exception as e:  # an extra config must never take the headline line down
+                    others.append({"config": {"workload": name}, "error": f"{type(e).__name__}: {e}"})
+        out["other_configs"] = others
         print(json.dumps(out))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    return 0
+    return rc
 
 
 if __name__ == "__main__":

@@ -26,6 +26,7 @@ extern "C" {
 #define QADC_MAX_SUBS 64
 #define QADC_MAX_GROUP 16
 #define QADC_MAX_R 1024 /* results per query supported by the device top-R stage */
+#define QADC_MAX_T 16384 /* longest calibration prefix t (the reference bounds neither; beyond these -> config error) */
 
 /* status classes: reference exception -> CLI exit code (errors.hpp, pqscan_cli.cpp:20-30) */
 enum {
@@ -114,21 +115,30 @@ uint64_t qadc_packed_bytes(const qadc_spec* spec, uint64_t n);
  *          (>= the largest t that will be used), needed only by shards whose
  *          own head is not the global head (index.hpp:124-129 calibrates on the
  *          global prefix); NULL/0 = use this shard's own head.
+ * global_count: length of the WHOLE list the shard belongs to (ignored without
+ *          calib_packed).  The reference calibrates on min(t, global_count) codes; when the
+ *          replicated head is shorter than the whole list (calib_count < global_count, or
+ *          global_count = 0 = unknown) a search with t > calib_count cannot reproduce that
+ *          and fails with QADC_ERR_CONFIG instead of silently calibrating on fewer codes.
  * device: CUDA ordinal. */
 int qadc_flat_open(const qadc_spec* spec, const float* codebook, const uint8_t* packed, uint64_t count,
-                   uint32_t base_id, const uint8_t* calib_packed, uint64_t calib_count, int device,
-                   qadc_index** out);
+                   uint32_t base_id, const uint8_t* calib_packed, uint64_t calib_count, uint64_t global_count,
+                   int device, qadc_index** out);
 
 /* ---- IvfIndex (index.hpp:166-177, 276-341) ------------------------------
  * Lists are concatenated: list c has list_count[c] codes, PackedList bytes at
  * packed + list_byte_off[c], ids at ids + list_id_off[c].
  * calib_*: per-list PackedList of the first min(count_global, t_max) codes of the
  * unsharded list (same convention as the flat index), or NULL to use own heads;
- * calib_count[c] is the GLOBAL list length capped at what calib_packed holds. */
+ * calib_count[c] = codes held by head c; global_list_count[c] = length of the unsharded list c
+ * (required with calib_*).  A search whose t exceeds the shortest TRUNCATED head
+ * (calib_count[c] < global_list_count[c]) fails with QADC_ERR_CONFIG: the reference's prefix
+ * (index.hpp:304-306) could ask that list for more codes than the head holds. */
 int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
                   const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
                   const uint64_t* list_count, const uint32_t* ids, const uint8_t* calib_packed,
-                  const uint64_t* calib_byte_off, const uint64_t* calib_count, int device, qadc_index** out);
+                  const uint64_t* calib_byte_off, const uint64_t* calib_count, const uint64_t* global_list_count,
+                  int device, qadc_index** out);
 
 /* Open a QFLT (flat) or QIVF (IVF) container written by the reference (io.hpp:276-326) directly: headers are parsed on
  * the host, the packed blocks go to the device as they are and are re-laid there.  load_flat_index / load_ivf_index

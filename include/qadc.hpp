@@ -81,6 +81,14 @@ inline std::vector<float> flatten(const pqscan::Codebook& cb) {
 // Drop-in for the functions quantized_scan_fn() returns (simd/kernels.hpp:133-153).  The
 // final heap is "the R smallest of (old entries U scanned candidates)" (heap.hpp:12-14), so the
 // GPU returns the list's own top-R and those R entries are pushed into the caller's heap.
+// The function-pointer type has no room for a device argument: the CUDA ordinal comes from
+// gpu_scan_device() (per thread, default 0).  This is the CORRECTNESS seam (the reference's differential
+// methodology runs through it): list and tables are uploaded on every call; throughput lives in the
+// batched GpuFlatIndex / GpuIvfIndex below, which keep the database resident.
+inline int& gpu_scan_device() {
+    thread_local int device = 0;
+    return device;
+}
 inline void gpu_scan_list(const pqscan::PackedList& list, const pqscan::PackingScheme& scheme,
                           const pqscan::QuantizedTables& qt, const uint32_t* ids, uint32_t base_id,
                           uint32_t acc_init, pqscan::CandidateHeap<uint32_t>& heap) {
@@ -105,7 +113,7 @@ inline void gpu_scan_list(const pqscan::PackedList& list, const pqscan::PackingS
     std::vector<uint32_t> od(cap), oi(cap);
     uint32_t n = 0;
     rethrow(qadc_scan_list(&s, list.data.data(), list.count, list.rows, qptr, qt.width, ids, base_id, acc_init, cap,
-                           nullptr, nullptr, 0, od.data(), oi.data(), &n, /*device=*/0));
+                           nullptr, nullptr, 0, od.data(), oi.data(), &n, gpu_scan_device()));
     for (uint32_t i = 0; i < n; ++i) heap.push(od[i], oi[i]);
 }
 
@@ -137,7 +145,7 @@ public:
     explicit GpuFlatIndex(const pqscan::FlatIndex& ref, int device = 0) : dims_(ref.codebook().spec().total_dims()) {
         const qadc_spec s = to_abi(ref.codebook().spec());
         const std::vector<float> cb = flatten(ref.codebook());
-        rethrow(qadc_flat_open(&s, cb.data(), ref.list().data.data(), ref.list().count, 0, nullptr, 0, device, &h_));
+        rethrow(qadc_flat_open(&s, cb.data(), ref.list().data.data(), ref.list().count, 0, nullptr, 0, 0, device, &h_));
     }
     GpuFlatIndex(const GpuFlatIndex&) = delete;
     GpuFlatIndex& operator=(const GpuFlatIndex&) = delete;
@@ -179,7 +187,7 @@ public:
             ids.insert(ids.end(), ref.list_ids()[c].begin(), ref.list_ids()[c].end());
         }
         rethrow(qadc_ivf_open(&s, cb.data(), ref.coarse_centroids().data(), ref.cells(), packed.data(), boff.data(),
-                              ioff.data(), cnt.data(), ids.data(), nullptr, nullptr, nullptr, device, &h_));
+                              ioff.data(), cnt.data(), ids.data(), nullptr, nullptr, nullptr, nullptr, device, &h_));
     }
     GpuIvfIndex(const GpuIvfIndex&) = delete;
     GpuIvfIndex& operator=(const GpuIvfIndex&) = delete;

@@ -86,7 +86,7 @@ static void validate_params(const qadc_search_params& p, bool ivf) {
     if (p.t < p.r) throw Error(QADC_ERR_INPUT, "search: calibration prefix t must be at least R");
     if (ivf && p.probes < 1) throw Error(QADC_ERR_INPUT, "search: probes must be at least 1");
     if (p.r > QADC_MAX_R) throw Error(QADC_ERR_CONFIG, "search: R exceeds QADC_MAX_R supported by the device top-R stage");
-    if (p.t > 16384) throw Error(QADC_ERR_CONFIG, "search: calibration prefix t exceeds 16384");
+    if (p.t > QADC_MAX_T) throw Error(QADC_ERR_CONFIG, "search: calibration prefix t exceeds QADC_MAX_T");
 }
 
 // Per-query selection state on the device.
@@ -167,6 +167,10 @@ struct qadc_index {
     uint64_t count = 0, count_padded = 0;
     uint32_t base_id = 0;
     uint32_t calib_count = 0;
+    // A shard calibrates on a replicated head of the WHOLE list (index.hpp:124-129).  When that head is shorter than
+    // the whole list, a search with t beyond it would silently calibrate on fewer codes than the reference does:
+    // such a t is a config error.  calib_limit = longest t the head can serve exactly (~0 = the head is complete).
+    uint64_t calib_limit = ~0ull;
     // ivf
     uint32_t k_cells = 0;
     DevBuf coarse, coarse_t, list_code_off, list_count_dev, calib_code_off, calib_count_dev;
@@ -362,6 +366,9 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
         h->stats.kernel_launches = g_launches;
         return;
     }
+    if (uint64_t(p.t) > h->calib_limit)
+        throw Error(QADC_ERR_CONFIG, "search: t = " + std::to_string(p.t) + " exceeds the replicated calibration head (" +
+                                         std::to_string(h->calib_limit) + " codes of a longer list): open the shard with a longer head");
     const ScanPlan plan = plan_for(h);
     h->stats.scan_variant = plan.variant;
     h->stats.query_tile = plan.tq;
@@ -475,6 +482,9 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
         h->stats.kernel_launches = g_launches;
         return;
     }
+    if (uint64_t(p.t) > h->calib_limit)
+        throw Error(QADC_ERR_CONFIG, "search: t = " + std::to_string(p.t) + " exceeds the shortest truncated calibration head (" +
+                                         std::to_string(h->calib_limit) + " codes): open the shard with longer list heads");
     ScanPlan plan = plan_for(h, false);
     const size_t wb = ds.word_width / 8;
     uint32_t tq = plan.tq;
@@ -763,14 +773,24 @@ static void ivf_search_device(qadc_index* h, const float* d_queries, uint32_t nq
     h->stats.kernel_launches = g_launches;
 }
 
+// Host -> device in plain async copies of at most 256 MiB: the source may be pageable or a file mapping
+// (qadc_open_file), where one chunk is what the driver stages at a time anyway.
+static void copy_h2d_chunked(void* dst, const void* src, uint64_t bytes, cudaStream_t st) {
+    const uint64_t chunk = uint64_t(256) << 20;
+    for (uint64_t off = 0; off < bytes; off += chunk)
+        QADC_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
+                                        size_t(std::min(chunk, bytes - off)), cudaMemcpyHostToDevice, st));
+}
+
 static void upload_list(qadc_index* h, const qadc_spec& s, const DevSpec& ds, const uint8_t* packed, uint64_t count,
                         DevBuf& out, uint64_t& padded, cudaStream_t st) {
     padded = (count + CODE_PAD - 1) / CODE_PAD * CODE_PAD + CODE_PAD;
     out.ensure(size_t(padded) * ds.code_stride);
+    if (count > 0xFFFFFFFFull) throw Error(QADC_ERR_INPUT, "list: more than 2^32 - 1 codes (ids are 32-bit)");
     const uint64_t bytes = qadc_packed_bytes(&s, count);
     DevBuf tmp;
     tmp.ensure(bytes);
-    if (bytes) QADC_CUDA_CHECK(cudaMemcpyAsync(tmp.p, packed, bytes, cudaMemcpyHostToDevice, st));
+    copy_h2d_chunked(tmp.p, packed, bytes, st);
     launch_relayout(s, ds, tmp.as<uint8_t>(), count, padded, out.as<uint8_t>(), st);
     QADC_CUDA_CHECK(cudaStreamSynchronize(st));
     (void)h;
@@ -806,13 +826,16 @@ int qadc_spec_parse(uint32_t dims, const char* text, qadc_spec* out) {
 
 uint64_t qadc_packed_bytes(const qadc_spec* s, uint64_t n) {
     if (n == 0) return 0;
+    // ids are uint32 and the product must not wrap: counts from an untrusted container are checked by the caller
+    // against this (UINT64_MAX = "does not fit")
+    if (n > 0xFFFFFFFFull) return ~0ull;
     const uint64_t blocks = (n + s->block_len - 1) / s->block_len;
     return blocks * s->groups * s->block_len * (s->word_width / 8);
 }
 
 int qadc_flat_open(const qadc_spec* spec, const float* codebook, const uint8_t* packed, uint64_t count,
-                   uint32_t base_id, const uint8_t* calib_packed, uint64_t calib_count, int device,
-                   qadc_index** out) {
+                   uint32_t base_id, const uint8_t* calib_packed, uint64_t calib_count, uint64_t global_count,
+                   int device, qadc_index** out) {
     return guarded([&] {
         if (!spec || !codebook || !out || (count && !packed)) throw Error(QADC_ERR_INPUT, "null argument");
         validate_spec(*spec);
@@ -835,11 +858,13 @@ int qadc_flat_open(const qadc_spec* spec, const float* codebook, const uint8_t* 
         upload_list(h.get(), *spec, h->ds, packed, count, h->codes, h->count_padded, h->stream);
         if (calib_packed && calib_count) {
             uint64_t pad = 0;
-            const uint64_t n = std::min<uint64_t>(calib_count, 16384);
+            const uint64_t n = std::min<uint64_t>(calib_count, QADC_MAX_T);
             upload_list(h.get(), *spec, h->ds, calib_packed, n, h->calib, pad, h->stream);
             h->calib_count = uint32_t(n);
+            // the head is complete only if the caller says the whole list is no longer than it
+            if (global_count == 0 || global_count > calib_count) h->calib_limit = n;
         } else {
-            const uint64_t n = std::min<uint64_t>(count, 16384);
+            const uint64_t n = std::min<uint64_t>(count, QADC_MAX_T);
             h->calib.ensure(std::max<size_t>(size_t(n) * h->ds.code_stride, 16));
             if (n) QADC_CUDA_CHECK(cudaMemcpyAsync(h->calib.p, h->codes.p, size_t(n) * h->ds.code_stride, cudaMemcpyDeviceToDevice, h->stream));
             h->calib_count = uint32_t(n);
@@ -1017,6 +1042,10 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
             throw Error(QADC_ERR_CONFIG, "scan: packed rows do not match the table count for this scheme");
         if (width != spec->word_width) throw Error(QADC_ERR_CONFIG, "scan: table width does not match the packing word width");
         // n_in may exceed cap: the reference pushes every seed through the bounded heap (selftest.hpp:104-109)
+        // CandidateHeap<uint32_t> takes any distance, but every distance this path produces is <= q_max <= 65535 and the
+        // device select ranks 48 key bits (16 distance + 32 id): larger seed distances are refused, not mis-ranked
+        for (uint32_t i = 0; i < n_in; ++i)
+            if (heap_in_dist[i] > 0xFFFFu) throw Error(QADC_ERR_CONFIG, "scan_list: pre-seeded heap distance exceeds 65535");
         if (cap > QADC_MAX_R) throw Error(QADC_ERR_CONFIG, "scan_list: heap capacity exceeds QADC_MAX_R");
         set_device(device);
         qadc_index h;
@@ -1068,7 +1097,7 @@ int qadc_scan_list(const qadc_spec* spec, const uint8_t* packed, uint64_t count,
                 h.sel.cap = buf_cap;
                 ok = [&] {
                     const int grid = h.num_sms;
-                    const uint64_t s0 = std::min<uint64_t>(h.seg0, std::max<uint32_t>(buf_cap / 2, 256));
+                    const uint64_t s0 = std::min<uint64_t>(h.seg0, std::max<uint32_t>(buf_cap / 2, 256)) / 16 * 16;
                     const std::vector<uint64_t> bounds = segment_bounds(count, s0, h.seg_growth);
                     for (size_t s = 0; s + 1 < bounds.size(); ++s) {
                         std::vector<ScanJob> jobs;
@@ -1193,11 +1222,11 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         std::lock_guard<std::recursive_mutex> lock(h->mu);
         const std::string n(name);
         if (n == "cand_cap") h->cand_cap = uint32_t(std::max<int64_t>(value, 16));
-        else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384));
+        else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384)) / 16u * 16u; // bulk copies: 16-byte aligned
         else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
         else if (n == "force_variant") h->force_variant = int(value);
         else if (n == "probe_tc") h->probe_tc = int(value);
-        else if (n == "ivf_round0") h->ivf_round0 = uint32_t(std::max<int64_t>(value, 64));
+        else if (n == "ivf_round0") h->ivf_round0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 64), 1 << 30)) / 16u * 16u;
         else throw Error(QADC_ERR_CONFIG, "set_option: unknown option " + n);
     });
 }
@@ -1205,13 +1234,14 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
 int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
                   const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
                   const uint64_t* list_count, const uint32_t* ids, const uint8_t* calib_packed,
-                  const uint64_t* calib_byte_off, const uint64_t* calib_count, int device, qadc_index** out) {
+                  const uint64_t* calib_byte_off, const uint64_t* calib_count, const uint64_t* global_list_count,
+                  int device, qadc_index** out) {
     return guarded([&] {
         if (!spec || !codebook || !out || (k_cells && (!coarse || !list_byte_off || !list_id_off || !list_count)))
             throw Error(QADC_ERR_INPUT, "null argument");
         const bool have_heads = calib_packed || calib_byte_off || calib_count;
-        if (have_heads && (!calib_byte_off || !calib_count))
-            throw Error(QADC_ERR_INPUT, "ivf: calib_byte_off and calib_count must be given together");
+        if (have_heads && (!calib_byte_off || !calib_count || !global_list_count))
+            throw Error(QADC_ERR_INPUT, "ivf: calib_byte_off, calib_count and global_list_count must be given together");
         validate_spec(*spec);
         set_device(device);
         std::unique_ptr<qadc_index> h(new qadc_index);
@@ -1269,6 +1299,7 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
         h->list_count_h.assign(list_count, list_count + k_cells);
         uint64_t run = 0, packed_total = 0, n_ids = 0;
         for (uint32_t c = 0; c < k_cells; ++c) {
+            if (list_count[c] > 0xFFFFFFFFull) throw Error(QADC_ERR_INPUT, "ivf: a list holds more than 2^32 - 1 codes");
             h->list_code_off_h[c] = run;
             run += (list_count[c] + LIST_ALIGN - 1) / LIST_ALIGN * LIST_ALIGN;
             packed_total = std::max<uint64_t>(packed_total, list_byte_off[c] + qadc_packed_bytes(spec, list_count[c]));
@@ -1289,7 +1320,7 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
             QADC_CUDA_CHECK(cudaMemcpyAsync(h->list_count_dev.p, list_count, size_t(k_cells) * 8, cudaMemcpyHostToDevice, st));
             QADC_CUDA_CHECK(cudaMemcpyAsync(boff.p, list_byte_off, size_t(k_cells) * 8, cudaMemcpyHostToDevice, st));
         }
-        if (packed_total) QADC_CUDA_CHECK(cudaMemcpyAsync(tmp.p, packed, packed_total, cudaMemcpyHostToDevice, st));
+        copy_h2d_chunked(tmp.p, packed, packed_total, st);
         if (k_cells)
             launch_ivf_relayout(*spec, h->ds, tmp.as<uint8_t>(), boff.as<uint64_t>(), h->list_code_off.as<uint64_t>(),
                                 h->list_count_dev.as<uint64_t>(), k_cells, total_padded, h->codes.as<uint8_t>(), st);
@@ -1299,6 +1330,9 @@ int qadc_ivf_open(const qadc_spec* spec, const float* codebook, const float* coa
             std::vector<uint64_t> coff(k_cells);
             uint64_t crun = 0, cbytes = 0;
             for (uint32_t c = 0; c < k_cells; ++c) {
+                if (calib_count[c] > global_list_count[c] || list_count[c] > global_list_count[c])
+                    throw Error(QADC_ERR_INPUT, "ivf: a list head or shard is longer than its whole list");
+                if (calib_count[c] < global_list_count[c]) h->calib_limit = std::min<uint64_t>(h->calib_limit, calib_count[c]);
                 coff[c] = crun;
                 crun += (calib_count[c] + LIST_ALIGN - 1) / LIST_ALIGN * LIST_ALIGN;
                 if (calib_count[c]) cbytes = std::max<uint64_t>(cbytes, calib_byte_off[c] + qadc_packed_bytes(spec, calib_count[c]));

@@ -12,6 +12,11 @@
 // the re-layout into the device format happens on the GPU (layout.cu / ivf.cu).  No host re-pack.
 // Error classes follow io.hpp: bad magic / version / truncation -> io_error (8); spec structure,
 // allocation, hash, scheme or list-count mismatch -> corruption_error (6); bad widths -> invalid_spec (3).
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -108,38 +113,62 @@ PackedSection read_packed(Reader& r, const Codebook& cb) { // read_packed_sectio
     ps.base = r.p;
     ps.count.resize(nlists);
     ps.byte_off.resize(nlists);
+    // A count is untrusted input: it must fit the bytes that are actually left in the file (this also keeps the
+    // size arithmetic from wrapping -- a crafted count like 2^62 would otherwise multiply to a small number) and ids
+    // are uint32.  The reference fails with io_error on the truncated read (io.hpp:262-268).
+    const uint64_t block_bytes = uint64_t(cb.spec.groups) * cb.spec.block_len * (cb.spec.word_width / 8);
     for (uint32_t l = 0; l < nlists; ++l) {
         ps.count[l] = r.get<uint64_t>();
         ps.byte_off[l] = r.at;
+        const uint64_t max_blocks = (r.n - r.at) / block_bytes;
+        if (ps.count[l] > 0xFFFFFFFFull || (ps.count[l] + cb.spec.block_len - 1) / cb.spec.block_len > max_blocks)
+            throw Error(QADC_ERR_IO, "unexpected end of file");
         r.bytes(size_t(qadc_packed_bytes(&cb.spec, ps.count[l])));
     }
     return ps;
 }
 
-std::vector<uint8_t> slurp(const char* path) {
-    FILE* f = std::fopen(path, "rb");
-    if (!f) throw Error(QADC_ERR_IO, std::string("cannot open ") + path);
-    std::vector<uint8_t> buf;
-    if (std::fseek(f, 0, SEEK_END) == 0) {
-        const long sz = std::ftell(f);
-        std::fseek(f, 0, SEEK_SET);
-        if (sz > 0) buf.resize(size_t(sz));
+// Read-only mapping of the container: the packed blocks go from the page cache to the device in the open
+// functions' chunked copies, without a second host copy of the whole file (a C5-size QIVF is ~6 GB).
+struct Mapping {
+    const uint8_t* p = nullptr;
+    size_t n = 0;
+    explicit Mapping(const char* path) {
+        const int fd = ::open(path, O_RDONLY);
+        if (fd < 0) throw Error(QADC_ERR_IO, std::string("cannot open ") + path);
+        struct stat sb;
+        if (::fstat(fd, &sb) != 0 || !S_ISREG(sb.st_mode)) {
+            ::close(fd);
+            throw Error(QADC_ERR_IO, std::string("cannot stat ") + path);
+        }
+        n = size_t(sb.st_size);
+        if (n) {
+            void* m = ::mmap(nullptr, n, PROT_READ, MAP_PRIVATE, fd, 0);
+            if (m == MAP_FAILED) {
+                ::close(fd);
+                throw Error(QADC_ERR_IO, std::string("cannot map ") + path);
+            }
+            ::madvise(m, n, MADV_SEQUENTIAL);
+            p = static_cast<const uint8_t*>(m);
+        }
+        ::close(fd);
     }
-    const size_t got = buf.empty() ? 0 : std::fread(buf.data(), 1, buf.size(), f);
-    std::fclose(f);
-    if (got != buf.size()) throw Error(QADC_ERR_IO, std::string("short read on ") + path);
-    return buf;
-}
+    Mapping(const Mapping&) = delete;
+    Mapping& operator=(const Mapping&) = delete;
+    ~Mapping() {
+        if (p) ::munmap(const_cast<uint8_t*>(p), n);
+    }
+};
 
 } // namespace
 
-// Returns through the ordinary open functions; the file image only has to live until they return.
+// Returns through the ordinary open functions; the mapping only has to live until they return.
 int open_index_file(const char* path, int device, qadc_index** out) {
-    const std::vector<uint8_t> img = slurp(path);
-    Reader r{img.data(), img.size()};
-    if (img.size() < 4) throw Error(QADC_ERR_IO, "bad magic: not an index file");
-    const bool flat = std::memcmp(img.data(), "QFLT", 4) == 0;
-    const bool ivf = std::memcmp(img.data(), "QIVF", 4) == 0;
+    const Mapping img(path);
+    Reader r{img.p, img.n};
+    if (img.n < 4) throw Error(QADC_ERR_IO, "bad magic: not an index file");
+    const bool flat = std::memcmp(img.p, "QFLT", 4) == 0;
+    const bool ivf = std::memcmp(img.p, "QIVF", 4) == 0;
     if (!flat && !ivf) throw Error(QADC_ERR_IO, "bad magic: not an index file"); // peek_index_kind, io.hpp:330-338
     r.bytes(4);
     if (r.get<uint32_t>() != 1) throw Error(QADC_ERR_IO, flat ? "flat index: unsupported format version" : "ivf index: unsupported format version");
@@ -147,7 +176,7 @@ int open_index_file(const char* path, int device, qadc_index** out) {
     if (flat) {
         const PackedSection ps = read_packed(r, cb);
         if (ps.count.size() != 1) throw Error(QADC_ERR_CORRUPTION, "flat index: expected exactly one list");
-        return qadc_flat_open(&cb.spec, cb.data, ps.base + ps.byte_off[0], ps.count[0], 0, nullptr, 0, device, out);
+        return qadc_flat_open(&cb.spec, cb.data, ps.base + ps.byte_off[0], ps.count[0], 0, nullptr, 0, 0, device, out);
     }
     const uint32_t k = r.get<uint32_t>();
     const float* coarse = reinterpret_cast<const float*>(r.bytes(size_t(k) * cb.spec.dims * 4));
@@ -159,9 +188,10 @@ int open_index_file(const char* path, int device, qadc_index** out) {
         id_off[c] = total;
         total += ps.count[c];
     }
+    if (total > 0xFFFFFFFFull) throw Error(QADC_ERR_CORRUPTION, "ivf index: more than 2^32 vectors (ids are 32-bit)");
     const uint32_t* ids = reinterpret_cast<const uint32_t*>(r.bytes(size_t(total) * 4));
     return qadc_ivf_open(&cb.spec, cb.data, coarse, k, ps.base, ps.byte_off.data(), id_off.data(), ps.count.data(), ids,
-                         nullptr, nullptr, nullptr, device, out);
+                         nullptr, nullptr, nullptr, nullptr, device, out);
 }
 
 } // namespace qadc

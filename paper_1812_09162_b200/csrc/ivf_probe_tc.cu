@@ -9,12 +9,18 @@
 //   1. approx[q][c] = |c'|^2 - 2 <q', c'> on the tensor cores (bf16 inputs, fp32 accumulate), with
 //      q' = q - mean, c' = c - mean (mean of the centroids; a translation leaves distances alone
 //      and makes the rounding errors relative to the spread of the data, not its offset).
-//   2. With D the real squared distance, D_ref the reference's fp32 value and A = approx + |q'|^2:
-//        |A - D|     <= (2^-8 + 2^-15) |q'||c'| + 2^-22 (|q'| + |c'|)^2       (bf16 rounding of both
-//                       inputs, <= 2^-9 each; fp32 accumulation over <= 2048 terms, truncation allowed;
-//                       fp32 rounding of |c'|^2 and of the final subtraction)
-//        |D_ref - D| <= (dims + 3) 2^-24 D <= 2^-13 (|q'| + |c'|)^2              (dims <= 2048)
-//      so |A - D_ref| <= eps := 2^-8 (|q'| + max_c |c'|)^2 with a factor ~1.8 to spare.
+//   2. With D the real squared distance, D_ref the reference's fp32 value, A = approx + |q'|^2 and
+//      S = (|q'| + |c'|)^2 (note |q'||c'| <= S / 4).  bf16 keeps 8 significand bits, so rounding to nearest has
+//      unit roundoff u = 2^-8 per input:
+//        |<q~,c~> - <q',c'>| <= (2u + u^2) |q'||c'|                  both inputs rounded, Cauchy-Schwarz
+//        => the -2<.,.> term is off by <= (2^-6 + 2^-15) |q'||c'| <= (2^-8 + 2^-17) S
+//        fp32 accumulation of <= 2048 exact products (truncation allowed): <= 2 * 2048 * 2^-23 |q'||c'| <= 2^-13 S
+//        fp32 rounding of |c'|^2 and of the final subtraction:             <= 2^-22 S
+//        |D_ref - D| <= (dims + 3) 2^-24 D <= 2^-13 S                      (serial fp32 sum, dims <= 2048)
+//      Sum: |A - D_ref| <= 2^-8 (1 + 2^-4 + ...) S < 1.07 * 2^-8 S.  The filter uses
+//      eps := 2^-7 (|q'| + max_c |c'|)^2, i.e. a factor ~1.88 above the bound.  (Round 1 used 2^-8 S, derived from
+//      u = 2^-9 -- one bit too optimistic; corrected, with an adversarial test whose inputs sit just below bf16
+//      rounding midpoints: tests/test_gpu_parity.py::test_probe_order_prefilter_bf16_midpoints.)
 //   3. T := the a-th smallest of 256 strided minima of approx (a real value that at least a cells do not
 //      exceed).  Those a cells have D_ref <= T + |q'|^2 + eps, hence so does the a-th smallest D_ref, and
 //      every cell of the true top-a (ties included) has approx <= T + 2 eps.  Cells passing that test are
@@ -50,7 +56,7 @@ __global__ void probe_prep_queries_kernel(const float* __restrict__ queries, con
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
         const double r = sqrt(s) * (1.0 + 1e-9) + cmax;
-        eps2[q] = 2.0 * (r * r) * (1.0 / 256.0) * (1.0 + 1e-9); // non-finite input -> inf/NaN -> flagged below
+        eps2[q] = 2.0 * (r * r) * (1.0 / 128.0) * (1.0 + 1e-9); // 2 eps, eps = 2^-7 r^2; non-finite input -> inf/NaN -> flagged below
     }
 }
 

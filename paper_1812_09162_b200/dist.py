@@ -46,8 +46,12 @@ def slice_packed(spec: QadcSpec, packed: np.ndarray, rng: ShardRange) -> np.ndar
     return packed[b0 * bb: b0 * bb + packed_bytes(spec, rng.count)]
 
 
-def global_head(spec: QadcSpec, packed: np.ndarray, total: int, t_max: int = 4096):
-    """PackedList prefix holding the first min(total, t_max) codes (rounded up to whole blocks)."""
+T_MAX = 16384  # QADC_MAX_T: the longest calibration prefix the ABI accepts, so a default head never truncates one
+
+
+def global_head(spec: QadcSpec, packed: np.ndarray, total: int, t_max: int = T_MAX):
+    """PackedList prefix holding the first min(total, t_max) codes (rounded up to whole blocks).  A shard opened
+    with this head serves every t <= t_max exactly; a larger t is refused (QADC_ERR_CONFIG), never clamped."""
     n = min(total, t_max)
     return packed[: packed_bytes(spec, n)], n
 
@@ -67,19 +71,31 @@ class ShardedIndex:
         self.index = index
 
     def search_device(self, d_queries, params: SearchParams, d_ids, d_dists, d_counts, stream=None):
-        """All tensors are torch CUDA tensors on this rank's device; results are replicated on every rank."""
+        """All tensors are torch CUDA tensors on this rank's device; results are replicated on every rank.
+
+        ``stream`` (an int cudaStream_t; default: torch's current stream) carries ALL three steps -- the shard
+        search, the all_gather and the merge kernel: the collective is issued under ``torch.cuda.stream`` of the
+        same stream, so the exchange is ordered behind the search and in front of the merge by stream order
+        alone, whatever the caller's current stream is."""
         import torch
         nq, r = int(d_queries.shape[0]), int(params.r)
-        keys = torch.empty((nq, r), dtype=torch.int64, device=d_queries.device)
-        qmap = torch.empty((nq, 2), dtype=torch.float32, device=d_queries.device)
-        self.index.search_device(d_queries, params, None, None, None, d_keys=keys, d_map=qmap, stream=stream)
-        if self.world == 1:
-            gathered = keys.unsqueeze(0)
-        else:
-            gathered = torch.empty((self.world, nq, r), dtype=torch.int64, device=d_queries.device)
-            self.dist.all_gather_into_tensor(gathered, keys, group=self.group)
-        merge_topk_device(gathered, self.world, nq, r, qmap, d_ids, d_dists, d_counts, self.device,
-                          fma_unquantize=params.fma_unquantize, stream=stream)
+        dev = d_queries.device
+        ext = torch.cuda.current_stream(dev) if not stream else torch.cuda.ExternalStream(int(stream), device=dev)
+        with torch.cuda.stream(ext):
+            keys = torch.empty((nq, r), dtype=torch.int64, device=dev)
+            qmap = torch.empty((nq, 2), dtype=torch.float32, device=dev)
+            self.index.search_device(d_queries, params, None, None, None, d_keys=keys, d_map=qmap,
+                                     stream=ext.cuda_stream)
+            if self.world == 1:
+                gathered = keys.unsqueeze(0)
+            else:
+                gathered = torch.empty((self.world, nq, r), dtype=torch.int64, device=dev)
+                # flat [world * nq, r] view: the layout NCCL and gloo both accept for the tensor form
+                self.dist.all_gather_into_tensor(gathered.view(self.world * nq, r), keys, group=self.group)
+            merge_topk_device(gathered, self.world, nq, r, qmap, d_ids, d_dists, d_counts, self.device,
+                              fma_unquantize=params.fma_unquantize, stream=ext.cuda_stream)
+            for t in (keys, qmap, gathered):  # allocated under `ext`, consumed there: nothing to record elsewhere
+                t.record_stream(ext)
 
     def close(self):
         self.index.close()
@@ -89,13 +105,24 @@ class ShardedFlatIndex(ShardedIndex):
     """A FlatIndex shard per rank: contiguous block-aligned code range, base_id, replicated global head."""
 
     def __init__(self, spec: QadcSpec, codebook, shard_packed, shard: ShardRange, head_packed, head_count, device,
-                 group=None):
+                 group=None, global_count: int = 0):
+        """``global_count`` = codes of the WHOLE database (0 = unknown: then the head is taken as truncated and a
+        search with t > head_count is refused rather than calibrated on fewer codes than the reference uses)."""
         super().__init__(FlatIndex(spec, codebook, shard_packed, shard.count, base_id=shard.start,
-                                   calib_packed=head_packed, calib_count=head_count, device=device), device, group)
+                                   calib_packed=head_packed, calib_count=head_count, global_count=global_count,
+                                   device=device), device, group)
+
+    @classmethod
+    def from_global(cls, spec: QadcSpec, codebook, packed, total: int, rank: int, world: int, device, group=None,
+                    t_max: int = T_MAX):
+        """Shard `rank` of `world` of one whole PackedList (each rank passes the same `packed`)."""
+        rg = shard_ranges(total, world, spec.block_len)[rank]
+        head, head_n = global_head(spec, packed, total, t_max)
+        return cls(spec, codebook, slice_packed(spec, packed, rg), rg, head, head_n, device, group, global_count=total)
 
 
 def shard_ivf_lists(spec: QadcSpec, packed, list_byte_off, list_id_off, list_count, ids, rank: int, world: int,
-                    t_max: int = 4096):
+                    t_max: int = T_MAX):
     """IVF sharding: EVERY list is split evenly (on packed-block boundaries) across the ranks --
     ids are explicit, so any split is legal (scan_scalar.hpp:60) -- and the first min(count, t_max) codes of every
     unsharded list are replicated as calibration heads, so probe order, tables, d_min_global, d_max, delta and the
@@ -123,7 +150,8 @@ def shard_ivf_lists(spec: QadcSpec, packed, list_byte_off, list_id_off, list_cou
     return dict(packed=cat(s_packed, np.uint8), list_byte_off=np.array(s_boff, np.uint64),
                 list_id_off=np.array(s_ioff, np.uint64), list_count=np.array(s_cnt, np.uint64),
                 ids=cat(s_ids, np.uint32), calib_packed=cat(c_packed, np.uint8),
-                calib_byte_off=np.array(c_boff, np.uint64), calib_count=np.array(c_cnt, np.uint64))
+                calib_byte_off=np.array(c_boff, np.uint64), calib_count=np.array(c_cnt, np.uint64),
+                global_list_count=np.ascontiguousarray(list_count, dtype=np.uint64))
 
 
 def merge_keys_numpy(gathered: np.ndarray, r: int) -> np.ndarray:

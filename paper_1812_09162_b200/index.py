@@ -144,7 +144,7 @@ class FlatIndex(_Index):
     derives the same quantization map (index.hpp:124-129)."""
 
     def __init__(self, spec: QadcSpec, codebook, packed, count: int, base_id: int = 0, calib_packed=None,
-                 calib_count: int = 0, device: int = 0):
+                 calib_count: int = 0, device: int = 0, global_count: int = 0):
         super().__init__()
         self.spec = spec
         self.device = device
@@ -162,7 +162,7 @@ class FlatIndex(_Index):
                 raise QadcError(5, "calibration list is shorter than its code count requires")
         check(lib().qadc_flat_open(C.byref(spec), _p(cb, C.c_float), _p(pk, C.c_uint8), C.c_uint64(count),
                                    C.c_uint32(base_id), _p(cpk, C.c_uint8), C.c_uint64(calib_count if cpk is not None else 0),
-                                   C.c_int(device), C.byref(self._h)))
+                                   C.c_uint64(global_count), C.c_int(device), C.byref(self._h)))
 
     def size(self) -> int:
         return self.count
@@ -199,9 +199,11 @@ class IvfIndex(_Index):
     """IvfIndex (index.hpp:166-177): coarse partition + per-cell packed lists of residual codes."""
 
     def __init__(self, spec: QadcSpec, codebook, coarse, packed, list_byte_off, list_id_off, list_count, ids,
-                 device: int = 0, calib_packed=None, calib_byte_off=None, calib_count=None):
+                 device: int = 0, calib_packed=None, calib_byte_off=None, calib_count=None, global_list_count=None):
         """For a shard (every list split across ranks) pass ``calib_*``: the PackedLists of the first
-        min(count, t_max) codes of the UNSHARDED lists, so that every rank derives the same quantization map."""
+        min(count, t_max) codes of the UNSHARDED lists, so that every rank derives the same quantization map,
+        and ``global_list_count`` (lengths of the unsharded lists): a search whose t exceeds a truncated head
+        is refused (config)."""
         super().__init__()
         self.spec = spec
         self.device = device
@@ -220,17 +222,20 @@ class IvfIndex(_Index):
         if int(lc.sum()) != idv.size:
             raise QadcError(6, "ivf: list code count != id count")  # index.hpp:175
         self.total = int(lc.sum())
-        cpk = cbo = cc = None
+        cpk = cbo = cc = glc = None
         if calib_packed is not None:
             cpk = np.ascontiguousarray(calib_packed, dtype=np.uint8).reshape(-1)
             cbo = np.ascontiguousarray(calib_byte_off, dtype=np.uint64)
             cc = np.ascontiguousarray(calib_count, dtype=np.uint64)
-            if not (cbo.size == cc.size == self.k_cells):
+            if global_list_count is None:
+                raise QadcError(5, "ivf: global_list_count is required with calibration heads")
+            glc = np.ascontiguousarray(global_list_count, dtype=np.uint64)
+            if not (cbo.size == cc.size == glc.size == self.k_cells):
                 raise QadcError(6, "ivf: calibration head section mismatch")
         check(lib().qadc_ivf_open(C.byref(spec), _p(cb, C.c_float), _p(co, C.c_float), C.c_uint32(self.k_cells),
                                   _p(pk, C.c_uint8), _p(lbo, C.c_uint64), _p(lio, C.c_uint64), _p(lc, C.c_uint64),
                                   _p(idv, C.c_uint32), _p(cpk, C.c_uint8), _p(cbo, C.c_uint64), _p(cc, C.c_uint64),
-                                  C.c_int(device), C.byref(self._h)))
+                                  _p(glc, C.c_uint64), C.c_int(device), C.byref(self._h)))
 
     def size(self) -> int:
         return self.total

@@ -365,13 +365,22 @@ def test_sharded_device_path_equals_unsharded(port, dims, text, n, world):
     dev = torch.device("cuda", 0)
     d_q = torch.from_numpy(queries).to(dev)
     head, head_n = global_head(s, packed, n)
+    if n > 1000:  # a head shorter than the list serves t <= its length only; beyond that: refused, never clamped
+        short, short_n = global_head(s, packed, n, t_max=256)
+        for gc in (n, 0):  # 0 = whole-list length unknown: treated as truncated
+            with qb.FlatIndex(s, cb, slice_packed(s, packed, shard_ranges(n, world, s.block_len)[1]), 64, base_id=64,
+                              calib_packed=short, calib_count=short_n, global_count=gc) as shard:
+                with pytest.raises(qb.QadcError) as e:
+                    shard.search(queries, qb.SearchParams(r=r, t=t))
+                assert e.value.kind == "config"
+                assert shard.search(queries, qb.SearchParams(r=r, t=256)).counts.max() <= r
     keys = torch.empty((world, len(queries), r), dtype=torch.int64, device=dev)
     qmap = torch.empty((len(queries), 2), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream().cuda_stream
     params = qb.SearchParams(r=r, t=t)
     for rank, rg in enumerate(shard_ranges(n, world, s.block_len)):
         with qb.FlatIndex(s, cb, slice_packed(s, packed, rg), rg.count, base_id=rg.start, calib_packed=head,
-                          calib_count=head_n) as shard:
+                          calib_count=head_n, global_count=n) as shard:
             shard.search_device(d_q, params, None, None, None, d_keys=keys[rank], d_map=qmap, stream=stream)
             torch.cuda.synchronize()
     d_ids = torch.empty((len(queries), r), dtype=torch.int32, device=dev)
@@ -429,7 +438,12 @@ def test_sharded_ivf_equals_unsharded(port, world):
         kw = shard_ivf_lists(s, packed, boff, ioff, counts, ids, rank, world, t_max=512)
         with qb.IvfIndex(s, cb, coarse, kw["packed"], kw["list_byte_off"], kw["list_id_off"], kw["list_count"],
                          kw["ids"], calib_packed=kw["calib_packed"], calib_byte_off=kw["calib_byte_off"],
-                         calib_count=kw["calib_count"]) as shard:
+                         calib_count=kw["calib_count"], global_list_count=kw["global_list_count"]) as shard:
+            if rank == 0:  # t beyond a truncated head is refused, never clamped (dist.py:49)
+                with pytest.raises(qb.QadcError) as e:
+                    shard.search_device(d_q, qb.SearchParams(probes=probes, r=r, t=513), None, None, None,
+                                        d_keys=keys[rank], d_map=qmap, stream=stream)
+                assert e.value.kind == "config"
             shard.search_device(d_q, params, None, None, None, d_keys=keys[rank], d_map=qmap, stream=stream)
             torch.cuda.synchronize()
     d_ids = torch.empty((len(queries), r), dtype=torch.int32, device=dev)
@@ -644,6 +658,40 @@ def test_probe_order_prefilter_is_exact(port, offset, spread):
             for qi in range(len(queries)):
                 assert np.array_equal(got[qi], port.probe_order(dims, coarse, queries[qi], a)), (a, qi)
         assert idx.probe_order(queries, 3)[0].tolist() == [11, 1500, 2050]
+
+
+def test_probe_order_prefilter_bf16_midpoints(port):
+    """Adversarial inputs for the prefilter's error bound: low dimension, every coordinate of every
+    centroid and query sits just BELOW a bf16 rounding midpoint (1 + (2k+1) 2^-8 - 2^-20) * 2^e, so each input loses
+    almost the full unit roundoff 2^-8 in the same direction; the centroid set is symmetric (c and -c) so the mean
+    is exactly zero and the bf16 images are the rounded inputs themselves.  Distances to the near centroids differ
+    by less than the bf16-induced error, so a too-small eps drops true top-a cells; the order must still be the
+    reference's, bit for bit, and equal to the exact kernels'."""
+    rng = np.random.default_rng(77)
+    dims, text, half = 8, "2x{4,4}", 600
+    s = qb.allocate_dims(dims, text)
+    cb = rng.standard_normal(s.cb_floats).astype(np.float32)
+
+    def below_midpoint(shape):
+        k = rng.integers(0, 64, size=shape)           # which bf16 interval of [1, 2): mantissa 7 bits -> 128 intervals
+        e = rng.integers(-1, 2, size=shape)           # exponents -1..1
+        sign = rng.choice([-1.0, 1.0], size=shape)
+        v = (1.0 + (2 * k + 1) * 2.0 ** -8 - 2.0 ** -20) * 2.0 ** e
+        return (sign * v).astype(np.float32)
+
+    pos = below_midpoint((half, dims))
+    coarse = np.concatenate([pos, -pos]).astype(np.float32)          # K = 1200, mean exactly 0
+    queries = below_midpoint((40, dims))
+    queries[:10] = coarse[rng.integers(0, 2 * half, size=10)] * np.float32(1.0 + 2.0 ** -9)
+    with _empty_ivf(s, cb, coarse) as idx:
+        for a in (1, 5, 64, 256):
+            got = idx.probe_order(queries, a)
+            idx.set_option("probe_tc", 0)
+            exact = idx.probe_order(queries, a)
+            idx.set_option("probe_tc", 1)
+            assert np.array_equal(got, exact), a
+            for qi in range(len(queries)):
+                assert np.array_equal(got[qi], port.probe_order(dims, coarse, queries[qi], a)), (a, qi)
 
 
 def test_probe_order_prefilter_overflow_falls_back(port):
