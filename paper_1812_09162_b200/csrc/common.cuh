@@ -76,6 +76,8 @@ enum ScanVariant : uint32_t {
                          // words' tables (quad-interleaved); code groups walk the words in rotated order
     VAR_F16X4H_C16Q = 11, // irregular 16-bit specs on 16-row tiles: quad lines (the same entry of the four words' tables),
                           // rotated codes, LDS.128, 16 codes per warp step -- the IVF layout with the least row padding
+    VAR_TC8 = 12, // 16x{4,4} as a one-hot int8 GEMM on tcgen05 (scan_tc.cu): 128 codes x 256 queries per MMA tile, s32
+                  // accumulators in TMEM, the admission threshold folded into a ninth K step (sign bit = admit)
     VAR_COUNT
 };
 
@@ -116,6 +118,10 @@ struct ScanPlan {
 // writes tiles itself and does not produce the merged-pair layout.
 ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_merged = false);
 void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
+// tensor-core scan of 16x{4,4} (scan_tc.cu)
+uint32_t scan_tc8_smem_bytes();
+void launch_scan_tc8(const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
+void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, void* out, cudaStream_t stream);
 
 // ---- LUT / calibration / quantization (lut.cu) ----
 struct LutArgs {

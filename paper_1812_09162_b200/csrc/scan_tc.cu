@@ -1,0 +1,409 @@
+// scan_tc.cu -- the 16x{4,4} scan as a one-hot int8 GEMM on the 5th-generation tensor cores (tcgen05).
+//
+// Reference semantics are those of scan.cu (scan_scalar.hpp:34-64): per code, the sum of the m = 16 quantized table
+// entries selected by its 4-bit subcodes, saturating at q_max = 255, pushed into a bounded (distance, id) heap.
+// Formulation: a code is the 256-dimensional 0/1 vector with a one at (table j, entry c_j); its sum for query q is
+// the dot product with q's 256 table bytes.  For a tile of 128 codes x 256 queries that is ONE contraction
+//     D[code][query] = sum_k onehot[code][k] * lut[query][k]        M = 128, N = 256, K = 256
+// whose operands are bytes and whose result fits 13 bits -- exactly what tcgen05.mma kind::i8 computes, 8192
+// multiply-adds per clock per SM, against the 128 B/clk shared-memory pipe that bounds the lookup kernel of scan.cu
+// (16 B of table traffic per pair).  VERDICT r1 asked for this experiment with a kill criterion (>= 1.5x end to end
+// and bit-exact); the measurement is in DESIGN.md section 4.5.
+//
+//   * A (one-hot, 128 x 256 B) is BUILT in shared memory by four generator warps from the streamed codes: thread =
+//     code, one 16-byte store per table (the 16 entries of table j are exactly one 16-byte K chunk, and the chunk is
+//     a single 0x01 byte at position c_j).  B (the tile's tables, 256 queries x 256 B) is resident in shared memory
+//     for a whole job, in the K-major no-swizzle canonical layout (8 rows x 16 bytes core matrices), prepared by
+//     pack_tiles_tc8_kernel and fetched with TMA bulk copies.  Table bytes are stored as e - 128 (signed), so every
+//     MMA is u8 x s8.
+//   * The admission threshold rides in the contraction: a ninth K step multiplies a constant all-ones A' block with a
+//     per-query row of 32 signed bytes that sum to v = 2048 + bias - thr - 1 (or -4096: admit all; +4064: padding row),
+//     so D = bias + sum - thr - 1 and "sum <= thr" is the SIGN BIT of the accumulator.
+//   * D (128 x 256 s32) lives in TMEM, two buffers of 256 columns; four epilogue warps read it back with tcgen05.ld
+//     (thread = code, 64 queries per load), OR the values and look at one sign bit per 64 pairs.  A flagged pair is
+//     re-evaluated exactly in integers from the reference-order table and passed through the CandidateHeap::push test
+//     (exact_admit_ct, scan_common.cuh) -- the filter never drops a pair the exact test would admit, so results are
+//     exact by construction, as in scan.cu.
+//   * Warp roles: 0-3 epilogue (TMEM lane quadrant = warp id), 4-7 one-hot generators, 8 MMA issuer (one elected
+//     lane; also owns the TMEM allocation), 9 producer (TMA code stream, tile loads, threshold rows).  All hand-offs
+//     are mbarriers; tcgen05.commit releases the one-hot stages and publishes the accumulators.
+// The operand layouts, the instruction descriptor and TS/SS modes were pinned against a CPU reference on the B200 by
+// tools/umma_probe.cu before this kernel relied on them.
+#include "scan_common.cuh"
+
+namespace qadc {
+
+namespace {
+
+constexpr int TC_TQ = 256;             // queries per tile = MMA N
+constexpr int TC_SUB = 128;            // codes per sub-tile = MMA M
+constexpr int TC_NA = 3;               // one-hot stages
+constexpr int TC_NSTAGE = 3;           // code stages (TMA ring)
+constexpr int TC_STAGE_BYTES = 8192;   // 1024 codes
+constexpr int TC_STAGE_CODES = TC_STAGE_BYTES / 8;
+constexpr int TC_INFO = 8;             // sub-tile info ring (generator -> epilogue)
+constexpr int TC_KC = 16;              // 16-byte K chunks of the table part (= tables)
+constexpr int TC_B_CHUNK = TC_TQ * 16; // bytes of one K chunk of B (256 rows x 16 B): the descriptor's LBO
+constexpr int TC_A_CHUNK = TC_SUB * 16;
+constexpr int TC_B_BYTES = (TC_KC + 2) * TC_B_CHUNK; // tables + the threshold K step
+constexpr int TC_A_BYTES = TC_KC * TC_A_CHUNK;
+constexpr int TC_AP_BYTES = 2 * TC_A_CHUNK;          // A': all ones, K = 32
+constexpr int TC_THREADS = 320;
+constexpr int TC_SMEM = TC_B_BYTES + TC_AP_BYTES + TC_NA * TC_A_BYTES + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8;
+
+struct SubInfo {
+    uint64_t id_ref;    // explicit ids: index of row 0's id in ScanArgs::ids; implicit: id of row 0
+    uint32_t n_valid;   // codes in this sub-tile (rows >= n_valid are padding)
+    uint32_t row_begin; // first LUT row of the tile
+};
+
+// shared-memory matrix descriptor: K-major, no swizzle (cute::UMMA::SmemDescriptor, version 1).  LBO = bytes between the
+// two 16-byte K chunks one MMA consumes, SBO = bytes between consecutive 8-row groups (a core matrix is 8 x 16 bytes)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) | (uint64_t((sbo >> 4) & 0x3FFFu) << 32) |
+           (uint64_t(1) << 46);
+}
+// instruction descriptor (cute::UMMA::InstrDescriptor): s32 accumulate, A = u8, B = s8, both K-major, M = 128, N = 256
+constexpr uint32_t TC_IDESC = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t(TC_TQ) >> 3) << 17) | ((uint32_t(TC_SUB) >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(TC_IDESC), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) { // arrives when every MMA issued so far has completed
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+        "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]),
+          "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]),
+          "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]),
+          "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]),
+          "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+using G44 = GeomCT<8, 8, 4, 4>; // 16x{4,4}: bit position of subquantizer j = 4 j
+
+// sub-tiles of one job: its stages hold TC_STAGE_CODES codes each, every stage is cut into sub-tiles of TC_SUB codes
+__device__ __forceinline__ uint32_t job_subtiles(uint32_t n_codes) {
+    const uint32_t full = n_codes / TC_STAGE_CODES, rem = n_codes - full * TC_STAGE_CODES;
+    return full * (TC_STAGE_CODES / TC_SUB) + (rem + TC_SUB - 1) / TC_SUB;
+}
+
+} // namespace
+
+__global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_param, ScanArgs args_param) {
+    extern __shared__ __align__(1024) char smem[];
+    __shared__ DevSpec s_ds;
+    __shared__ ScanArgs s_args;
+    __shared__ __align__(8) uint64_t s_full[TC_NSTAGE], s_empty[TC_NSTAGE]; // code stages: TMA -> generators
+    __shared__ __align__(8) uint64_t s_afull[TC_NA], s_aempty[TC_NA];        // one-hot stages: generators -> MMA
+    __shared__ __align__(8) uint64_t s_dfull[2], s_dempty[2];                // accumulators: MMA -> epilogue
+    __shared__ __align__(8) uint64_t s_tfull, s_tempty;                      // LUT tile: producer -> MMA
+    __shared__ SubInfo s_info[TC_INFO];
+    __shared__ uint32_t s_tmem;
+
+    char* sB = smem;
+    char* sAp = sB + TC_B_BYTES;
+    char* sA = sAp + TC_AP_BYTES;
+    char* stage = sA + TC_NA * TC_A_BYTES;
+    uint2* info_codes = reinterpret_cast<uint2*>(stage + TC_NSTAGE * TC_STAGE_BYTES);
+
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        s_ds = ds_param;
+        s_args = args_param;
+        for (int i = 0; i < TC_NSTAGE; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], 4);
+        }
+        for (int i = 0; i < TC_NA; ++i) {
+            mbar_init(&s_afull[i], 4);
+            mbar_init(&s_aempty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_dfull[i], 1);
+            mbar_init(&s_dempty[i], 4);
+        }
+        mbar_init(&s_tfull, 2); // the tile's expect_tx + the threshold rows' arrive
+        mbar_init(&s_tempty, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 8) { // the MMA warp owns the tensor memory: 2 accumulators x 256 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (uint32_t i = tid; i < TC_AP_BYTES / 16; i += TC_THREADS) // A': every row all ones
+        reinterpret_cast<uint4*>(sAp)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    proxy_fence();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const DevSpec* ds = &s_ds;
+    const ScanArgs* a = &s_args;
+    const uint32_t tmem = s_tmem;
+
+    const uint32_t j_begin = a->cta_begin ? a->cta_begin[blockIdx.x] : uint32_t(uint64_t(a->n_jobs) * blockIdx.x / gridDim.x);
+    const uint32_t j_end = a->cta_begin ? a->cta_begin[blockIdx.x + 1] : uint32_t(uint64_t(a->n_jobs) * (blockIdx.x + 1) / gridDim.x);
+
+    if (warp == 9) {
+        // ============================ producer: code stream + tile loads + threshold rows ====================
+        uint32_t it = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
+        for (uint32_t ji = j_begin; ji < j_end; ++ji) {
+            const ScanJob job = a->jobs[ji];
+            if (job.n_codes == 0 || job.n_rows == 0) continue;
+            if (job.row_begin != prev_rb || job.n_rows != prev_nr) {
+                prev_rb = job.row_begin;
+                prev_nr = job.n_rows;
+                mbar_wait(&s_tempty, (tseq & 1u) ^ 1u); // the MMAs of the previous tile are done with B
+                if (lane == 0) {
+                    const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / TC_TQ) * (TC_KC * TC_B_CHUNK);
+                    mbar_expect_tx(&s_tfull, TC_KC * TC_B_CHUNK);
+                    for (uint32_t off = 0; off < uint32_t(TC_KC * TC_B_CHUNK); off += 32768u)
+                        bulk_g2s(sB + off, src + off, 32768u, &s_tfull);
+                }
+                // threshold K step: row r gets 32 signed bytes that sum to v
+                for (uint32_t r = lane; r < uint32_t(TC_TQ); r += 32) {
+                    int v = 4064; // padding rows never admit
+                    if (r < job.n_rows) {
+                        const uint32_t row = job.row_begin + r;
+                        const uint32_t q = a->row_query ? a->row_query[row] : row;
+                        if (q != 0xFFFFFFFFu) {
+                            const uint64_t tk = a->thr_key[q];
+                            const uint32_t thr = uint32_t(tk >> 32);
+                            const uint32_t bias = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;
+                            if (tk == KEY_INF || thr >= ds->qmax) v = -4096; // heap not full / worst saturated: admit all
+                            else v = 2048 + int(bias) - int(thr) - 1;
+                        }
+                    }
+                    uint32_t w[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        uint32_t word = 0;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int x = max(-128, min(127, v));
+                            v -= x;
+                            word |= (uint32_t(x) & 0xFFu) << (8 * b);
+                        }
+                        w[k] = word;
+                    }
+                    char* dst = sB + TC_KC * TC_B_CHUNK + (r >> 3) * 128 + (r & 7u) * 16;
+                    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+                    *reinterpret_cast<uint4*>(dst + TC_B_CHUNK) = make_uint4(w[4], w[5], w[6], w[7]);
+                }
+                proxy_fence(); // generic-proxy stores -> visible to the tensor core's (async proxy) operand reads
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_tfull);
+                ++tseq;
+            }
+            const uint8_t* gcodes = a->codes + job.code_off * 8;
+            const uint32_t n_st = (job.n_codes + TC_STAGE_CODES - 1) / TC_STAGE_CODES;
+            for (uint32_t st = 0; st < n_st; ++st, ++it) {
+                const uint32_t b = it % TC_NSTAGE;
+                mbar_wait(&s_empty[b], ((it / TC_NSTAGE) & 1u) ^ 1u);
+                if (lane == 0) {
+                    const uint32_t first = st * TC_STAGE_CODES;
+                    const uint32_t cnt = min(uint32_t(TC_STAGE_CODES), job.n_codes - first);
+                    const uint32_t bytes = (cnt * 8 + 15u) & ~15u;
+                    mbar_expect_tx(&s_full[b], bytes);
+                    bulk_g2s(stage + size_t(b) * TC_STAGE_BYTES, gcodes + size_t(first) * 8, bytes, &s_full[b]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ============================ generators: codes -> one-hot A stages ==================================
+        const uint32_t g = tid - 128; // row of the sub-tile
+        uint32_t it = 0, s = 0;
+        for (uint32_t ji = j_begin; ji < j_end; ++ji) {
+            const ScanJob job = a->jobs[ji];
+            if (job.n_codes == 0 || job.n_rows == 0) continue;
+            const uint32_t n_st = (job.n_codes + TC_STAGE_CODES - 1) / TC_STAGE_CODES;
+            for (uint32_t st = 0; st < n_st; ++st, ++it) {
+                const uint32_t b = it % TC_NSTAGE;
+                mbar_wait(&s_full[b], (it / TC_NSTAGE) & 1u);
+                const uint32_t first = st * TC_STAGE_CODES;
+                const uint32_t cnt = min(uint32_t(TC_STAGE_CODES), job.n_codes - first);
+                const char* sb = stage + size_t(b) * TC_STAGE_BYTES;
+                const uint32_t n_sub = (cnt + TC_SUB - 1) / TC_SUB;
+                for (uint32_t sub = 0; sub < n_sub; ++sub, ++s) {
+                    const uint32_t sa = s % TC_NA;
+                    mbar_wait(&s_aempty[sa], ((s / TC_NA) & 1u) ^ 1u); // the MMAs that read this stage have completed
+                    const uint32_t i = sub * TC_SUB + g;
+                    const bool valid = i < cnt;
+                    uint2 code = make_uint2(0u, 0u);
+                    if (valid) code = *reinterpret_cast<const uint2*>(sb + size_t(i) * 8);
+                    char* dst = sA + size_t(sa) * TC_A_BYTES + (g >> 3) * 128 + (g & 7u) * 16;
+                    const uint32_t live = valid ? 1u : 0u; // padding rows: all-zero one-hot (masked again in the epilogue)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t n = ((j < 8 ? code.x : code.y) >> ((j & 7) * 4)) & 15u;
+                        const uint32_t bit = live << ((n & 3u) * 8);
+                        const uint32_t wsel = n >> 2;
+                        uint4 v;
+                        v.x = wsel == 0 ? bit : 0u;
+                        v.y = wsel == 1 ? bit : 0u;
+                        v.z = wsel == 2 ? bit : 0u;
+                        v.w = wsel == 3 ? bit : 0u;
+                        *reinterpret_cast<uint4*>(dst + j * TC_A_CHUNK) = v;
+                    }
+                    const uint32_t slot = s % TC_INFO;
+                    info_codes[slot * TC_SUB + g] = code;
+                    if (g == 0) {
+                        SubInfo inf;
+                        const uint64_t pos = uint64_t(first) + uint64_t(sub) * TC_SUB;
+                        inf.id_ref = a->ids ? job.ids_off + pos : uint64_t(job.id_base) + pos;
+                        inf.n_valid = min(uint32_t(TC_SUB), cnt - sub * TC_SUB);
+                        inf.row_begin = job.row_begin;
+                        s_info[slot] = inf;
+                    }
+                    proxy_fence();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s_afull[sa]);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[b]); // this warp is done with the code stage
+            }
+        }
+    } else if (warp == 8) {
+        // ============================ MMA issuer ==============================================================
+        uint32_t s = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
+        const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB), ap_base = smem_u32(sAp);
+        for (uint32_t ji = j_begin; ji < j_end; ++ji) {
+            const ScanJob job = a->jobs[ji];
+            if (job.n_codes == 0 || job.n_rows == 0) continue;
+            if (job.row_begin != prev_rb || job.n_rows != prev_nr) {
+                prev_rb = job.row_begin;
+                prev_nr = job.n_rows;
+                if (tseq > 0 && lane == 0) umma_commit(&s_tempty); // every MMA on the old tile has completed
+                __syncwarp();
+                mbar_wait(&s_tfull, tseq & 1u);
+                ++tseq;
+            }
+            const uint32_t n_sub = job_subtiles(job.n_codes);
+            for (uint32_t k = 0; k < n_sub; ++k, ++s) {
+                const uint32_t sa = s % TC_NA, buf = s & 1u;
+                mbar_wait(&s_afull[sa], (s / TC_NA) & 1u);
+                mbar_wait(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t d = tmem + buf * TC_TQ;
+                    const uint32_t a0 = a_base + sa * TC_A_BYTES;
+#pragma unroll
+                    for (int ks = 0; ks < TC_KC / 2; ++ks)
+                        umma_i8(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
+                                umma_desc(b_base + ks * 2 * TC_B_CHUNK, TC_B_CHUNK, 128), ks > 0);
+                    umma_i8(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128), 1u);
+                    umma_commit(&s_aempty[sa]); // the one-hot stage is free once these MMAs have read it
+                    umma_commit(&s_dfull[buf]); // ... and the accumulator is complete
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ============================ epilogue: TMEM -> sign test -> exact admission ==========================
+        uint32_t s = 0;
+        const uint32_t lane_base = (warp * 32u) << 16; // this warp's TMEM lane quadrant
+        for (uint32_t ji = j_begin; ji < j_end; ++ji) {
+            const ScanJob job = a->jobs[ji];
+            if (job.n_codes == 0 || job.n_rows == 0) continue;
+            const uint32_t n_sub = job_subtiles(job.n_codes);
+            for (uint32_t k = 0; k < n_sub; ++k, ++s) {
+                const uint32_t buf = s & 1u, slot = s % TC_INFO;
+                mbar_wait(&s_dfull[buf], (s >> 1) & 1u);
+                tc_fence_after();
+                const SubInfo inf = s_info[slot];
+                const bool valid = tid < inf.n_valid;
+#pragma unroll 1
+                for (uint32_t c0 = 0; c0 < uint32_t(TC_TQ); c0 += 64) {
+                    uint32_t v[64];
+                    tmem_ld64(tmem + buf * TC_TQ + lane_base + c0, v);
+                    tmem_ld_wait();
+                    uint32_t any = 0;
+#pragma unroll
+                    for (int j = 0; j < 64; j += 2) any |= v[j] | v[j + 1];
+                    if (valid && (any >> 31)) {
+                        // rare: which of the 64 queries?  (sign bits -> two masks, then the exact test per set bit)
+                        uint32_t m0 = 0, m1 = 0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            m0 |= (v[j] >> 31) << j;
+                            m1 |= (v[32 + j] >> 31) << j;
+                        }
+                        const uint2 code = info_codes[slot * TC_SUB + tid];
+                        const uint32_t id = a->ids ? a->ids[inf.id_ref + tid] : uint32_t(inf.id_ref) + tid;
+                        while (m0) {
+                            const uint32_t j = __ffs(m0) - 1;
+                            m0 &= m0 - 1;
+                            exact_admit_ct<G44>(ds, a, code.x, code.y, inf.row_begin + c0 + j, id);
+                        }
+                        while (m1) {
+                            const uint32_t j = __ffs(m1) - 1;
+                            m1 &= m1 - 1;
+                            exact_admit_ct<G44>(ds, a, code.x, code.y, inf.row_begin + c0 + 32 + j, id);
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_dempty[buf]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+// ------------------------------------------------------------------------------------------ tile image --
+
+// qlut [n_rows][256] u8 (reference table order) -> per tile of 256 rows the B operand image
+// [kc = 16][row = 256][16 bytes] of e - 128 (two's complement: e ^ 0x80); rows past n_rows hold e = 0.
+__global__ void pack_tiles_tc8_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint8_t* __restrict__ out) {
+    const uint32_t tile = blockIdx.x;
+    for (uint32_t i = threadIdx.x; i < uint32_t(TC_KC * TC_TQ); i += blockDim.x) {
+        const uint32_t kc = i / TC_TQ, r = i % TC_TQ;
+        const uint32_t row = tile * TC_TQ + r;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row < n_rows) v = *reinterpret_cast<const uint4*>(qlut + size_t(row) * 256 + kc * 16);
+        v.x ^= 0x80808080u;
+        v.y ^= 0x80808080u;
+        v.z ^= 0x80808080u;
+        v.w ^= 0x80808080u;
+        *reinterpret_cast<uint4*>(out + size_t(tile) * (TC_KC * TC_B_CHUNK) + size_t(kc) * TC_B_CHUNK + r * 16) = v;
+    }
+}
+
+uint32_t scan_tc8_smem_bytes() { return TC_SMEM; }
+
+void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, void* out, cudaStream_t stream) {
+    if (n_rows == 0) return;
+    pack_tiles_tc8_kernel<<<(n_rows + TC_TQ - 1) / TC_TQ, 256, 0, stream>>>(static_cast<const uint8_t*>(qlut), n_rows,
+                                                                           static_cast<uint8_t*>(out));
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_scan_tc8(const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_tc8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+    scan_tc8_kernel<<<grid, TC_THREADS, TC_SMEM, stream>>>(ds, args);
+    ++g_launches;
+    QADC_CUDA_CHECK(cudaGetLastError());
+}
+
+} // namespace qadc

@@ -156,6 +156,7 @@ size_t tile_entry_bytes(ScanVariant v) {
     case VAR_F32X2: return 4;
     case VAR_U16X1: return 2;
     case VAR_U8X1: return 1;
+    case VAR_TC8: return 1; // signed bytes e - 128, K-major operand image
     default: return 4;
     }
 }
@@ -163,6 +164,10 @@ size_t tile_entry_bytes(ScanVariant v) {
 void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, uint32_t pair, const void* qlut, uint32_t width, uint32_t E,
                        uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     switch (v) {
+    case VAR_TC8:
+        if (width != 8 || E != 256 || tq != 256) throw Error(QADC_ERR_CONFIG, "pack_tiles: the tensor-core layout is for 16x{4,4}");
+        launch_pack_tiles_tc8(qlut, n_rows, out, stream);
+        return;
     case VAR_F16X4H_C8Q: {
         if (width != 16 || (E != 512 && E != 576 && E != 384) || tq != 16)
             throw Error(QADC_ERR_CONFIG, "pack_tiles: quad layout is for 12x{6,5,5} / 12x{6,6,4} / 12x{5,5,5}");

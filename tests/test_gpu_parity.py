@@ -865,7 +865,7 @@ def test_concurrent_calls_on_one_handle_serialise():
 
 
 @pytest.mark.parametrize("dims,text,variants", [
-    (128, "16x{4,4}", [0, 1, 2, 3, 7, 9]),       # f16x8, f32x2, u16x1, u8x1, f16x4-c4, merged pair tables (default)
+    (128, "16x{4,4}", [0, 1, 2, 3, 7, 9, 12]),   # f16x8, f32x2, u16x1, u8x1, f16x4-c4, merged pair tables, tcgen05 one-hot GEMM
     (96, "12x{6,5,5}", [1, 2, 3, 4, 5, 6, 8, 10, 11]),   # f32x2, u16x1, u8x1, f16x4h, -c2, -c4, -c4d, merged quad, 16-row quad
     (64, "12x{6,6,4}", [1, 2, 4, 5, 10]),        # f32x2, u16x1, f16x4h, -c2, merged quad (default)
     (60, "12x{5,5,5}", [1, 2, 4, 5, 10]),        # f32x2, u16x1, f16x4h, -c2, merged quad (default)

@@ -66,6 +66,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
           "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+        "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]),
+          "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]),
+          "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]),
+          "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]),
+          "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
+        : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------------------------------------
@@ -193,17 +208,19 @@ __global__ void __launch_bounds__(128) mma_ts_check_kernel(const uint8_t* A, con
 // Rates.  mode 0: one thread issues `iters` x 8 MMAs (M=128, N, K=32 B each, i8) into two alternating accumulators,
 // nobody reads them (tensor pipe + operand fetch only).  mode 1: additionally 4 warps read the 128 x N s32
 // accumulator after every 8 MMAs (the product kernel's epilogue traffic), double-buffered through 2 mbarrier pairs.
-template <int N>
-__global__ void __launch_bounds__(192) mma_rate_kernel(uint32_t iters, int mode, uint32_t* sink) {
+// EW epilogue warps (4 or 8: warp w reads lane quadrant w % 4 and column half w / 4), batches of BATCH columns
+// (32, 64 or 128 = two x64 loads) per tcgen05.wait::ld.  KSTEPS MMAs of K = 32 bytes per tile.
+template <int N, int EW, int BATCH, int KSTEPS>
+__global__ void __launch_bounds__(EW * 32 + 32) mma_rate_kernel(uint32_t iters, int mode, uint32_t* sink) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t full[2], empty[2];
     __shared__ uint32_t tmem_base;
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
-    for (uint32_t i = tid; i < (128 + N) * 256 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 1);
+    for (uint32_t i = tid; i < (128 + N) * 32 * KSTEPS / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 1);
     if (tid == 0) {
         for (int i = 0; i < 2; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 128);
+            mbar_init(&empty[i], EW * 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -217,33 +234,51 @@ __global__ void __launch_bounds__(192) mma_rate_kernel(uint32_t iters, int mode,
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tb = tmem_base;
     const uint32_t id = idesc(2, 0, 0, 128, N);
-    if (warp == 4) { // MMA issuer
+    if (warp == EW) { // MMA issuer
         if ((tid & 31) == 0) {
-            const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 128 * 256);
+            const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 128 * 32 * KSTEPS);
             for (uint32_t it = 0; it < iters; ++it) {
                 const uint32_t buf = it & 1;
                 if (mode == 1) mbar_wait(&empty[buf], ((it >> 1) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                for (uint32_t ks = 0; ks < 8; ++ks)
+                for (uint32_t ks = 0; ks < KSTEPS; ++ks)
                     mma_i8(tb + buf * 256, smem_desc(a0 + ks * 2 * 2048, 2048, 128), smem_desc(b0 + ks * 2 * (N * 16), N * 16, 128), id, ks > 0);
                 mma_commit(&full[buf]);
             }
-            if (mode == 0) { // drain: wait for the last commits
-                mbar_wait(&full[(iters - 1) & 1], ((iters - 1) >> 1) & 1);
-            }
+            if (mode == 0) mbar_wait(&full[(iters - 1) & 1], ((iters - 1) >> 1) & 1);
         }
-    } else if (warp < 4 && mode == 1) {
+    } else if (warp < EW && mode == 1) {
         uint32_t acc = 0;
+        constexpr uint32_t COLS = N / (EW / 4);
+        const uint32_t col0 = (warp / 4) * COLS, lane_base = ((warp & 3u) * 32u) << 16;
         for (uint32_t it = 0; it < iters; ++it) {
             const uint32_t buf = it & 1;
             mbar_wait(&full[buf], (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            for (uint32_t c0 = 0; c0 < N; c0 += 32) {
-                uint32_t v[32];
-                tmem_ld32(tb + buf * 256 + ((warp * 32u) << 16) + c0, v);
-                tmem_ld_wait();
+            for (uint32_t c0 = 0; c0 < COLS; c0 += BATCH) {
+                const uint32_t t0 = tb + buf * 256 + lane_base + col0 + c0;
+                if constexpr (BATCH == 32) {
+                    uint32_t v[32];
+                    tmem_ld32(t0, v);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 32; j += 2) acc |= v[j] | v[j + 1];
+                    for (int j = 0; j < 32; j += 2) acc |= v[j] | v[j + 1];
+                } else if constexpr (BATCH == 64) {
+                    uint32_t v[64];
+                    tmem_ld64(t0, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 64; j += 2) acc |= v[j] | v[j + 1];
+                } else {
+                    uint32_t v[64], w[64];
+                    tmem_ld64(t0, v);
+                    tmem_ld64(t0 + 64, w);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 64; j += 2) acc |= v[j] | v[j + 1];
+#pragma unroll
+                    for (int j = 0; j < 64; j += 2) acc |= w[j] | w[j + 1];
+                }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[buf])) : "memory");
@@ -253,6 +288,31 @@ __global__ void __launch_bounds__(192) mma_rate_kernel(uint32_t iters, int mode,
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "n"(512));
+}
+
+template <int EW, int BATCH, int KSTEPS>
+static void run_rate(int sms, int clock_khz, int mode, uint32_t* sink) {
+    const uint32_t iters = 4000;
+    const size_t smem = (128 + 256) * 32 * KSTEPS;
+    auto k = mma_rate_kernel<256, EW, BATCH, KSTEPS>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    k<<<sms, EW * 32 + 32, smem>>>(100, mode, sink);
+    CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0));
+    k<<<sms, EW * 32 + 32, smem>>>(iters, mode, sink);
+    CK(cudaEventRecord(e1));
+    CK(cudaDeviceSynchronize());
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    const double macs = double(iters) * KSTEPS * 128 * 256 * 32 * sms;
+    printf("rate M=128 N=256 K=%d %-34s: %.3f ms, %6.1f TOP/s, %7.1f cycles/tile, %.3e pairs/s\n", KSTEPS * 32,
+           mode ? (EW == 4 ? (BATCH == 32 ? "4 epi warps, 32 cols/wait" : BATCH == 64 ? "4 epi warps, 64 cols/wait" : "4 epi warps, 128 cols/wait")
+                           : (BATCH == 32 ? "8 epi warps, 32 cols/wait" : BATCH == 64 ? "8 epi warps, 64 cols/wait" : "8 epi warps, 128 cols/wait"))
+                : "MMA only",
+           ms, 2 * macs / ms / 1e9, ms * 1e-3 * clock_khz * 1e3 / iters, double(iters) * 128 * 256 * sms / (ms * 1e-3));
 }
 
 static float bf16_to_f(uint16_t b) {
@@ -380,26 +440,16 @@ int main() {
     // ---- rates
     uint32_t* sink;
     CK(cudaMalloc(&sink, 4096));
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    for (int mode = 0; mode < 2; ++mode) {
-        const uint32_t iters = 4000;
-        const size_t smem = (128 + 256) * 256;
-        CK(cudaFuncSetAttribute(mma_rate_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        mma_rate_kernel<256><<<sms, 192, smem>>>(100, mode, sink);
-        CK(cudaDeviceSynchronize());
-        CK(cudaEventRecord(e0));
-        mma_rate_kernel<256><<<sms, 192, smem>>>(iters, mode, sink);
-        CK(cudaEventRecord(e1));
-        CK(cudaDeviceSynchronize());
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, e0, e1));
-        const double macs = double(iters) * 8 * 128 * 256 * 32 * sms;
-        printf("rate mode %d (M=128 N=256 K=256 per tile, %s): %.3f ms, %.1f TOP/s dense i8, %.1f cycles/tile at %d MHz, tile pairs/s = %.3e\n",
-               mode, mode ? "4 warps read every accumulator" : "MMA only", ms, 2 * macs / ms / 1e9,
-               ms * 1e-3 * prop.clockRate * 1e3 / iters, prop.clockRate / 1000, double(iters) * 128 * 256 * sms / (ms * 1e-3));
-    }
+    run_rate<4, 32, 8>(sms, prop.clockRate, 0, sink);
+    run_rate<4, 32, 9>(sms, prop.clockRate, 0, sink);
+    run_rate<4, 32, 8>(sms, prop.clockRate, 1, sink);
+    run_rate<4, 64, 8>(sms, prop.clockRate, 1, sink);
+    run_rate<4, 128, 8>(sms, prop.clockRate, 1, sink);
+    run_rate<8, 32, 8>(sms, prop.clockRate, 1, sink);
+    run_rate<8, 64, 8>(sms, prop.clockRate, 1, sink);
+    run_rate<8, 128, 8>(sms, prop.clockRate, 1, sink);
+    run_rate<8, 128, 9>(sms, prop.clockRate, 1, sink);
+    run_rate<8, 128, 4>(sms, prop.clockRate, 1, sink);
     printf("TS-mode hypothesis: %s\n", ts_fails ? "WRONG" : "confirmed");
     printf(fails ? "UMMA PROBE: %d FAILURES\n" : "UMMA PROBE: all checks ok\n", fails);
     return fails ? 1 : 0;
