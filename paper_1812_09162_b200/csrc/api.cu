@@ -186,6 +186,7 @@ struct qadc_index {
     uint32_t seg0 = 4096;
     uint32_t seg_growth = 8;
     int force_variant = -1;
+    uint32_t tc_debug = 0; // timing experiments on the tensor-core scan (results are wrong when non-zero)
     // workspace
     SelectBufs sel;
     DevBuf qlut, tile_lut, luts, calib_out, map, status, jobs, queries, out_ids, out_dists, out_counts, counters, scratch;
@@ -202,7 +203,9 @@ namespace qadc {
 static constexpr uint64_t CODE_PAD = 1024; // device code arrays are padded to this many codes
 
 static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true) {
-    return plan_scan(h->ds, h->device, h->force_variant, allow_merged);
+    ScanPlan p = plan_scan(h->ds, h->device, h->force_variant, allow_merged);
+    if (p.variant == VAR_TC8) p.filter_shift = h->tc_debug;
+    return p;
 }
 
 // Geometric segment schedule: after n codes the R-th best of n bounds the admission
@@ -1226,6 +1229,7 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
         else if (n == "force_variant") h->force_variant = int(value);
         else if (n == "probe_tc") h->probe_tc = int(value);
+        else if (n == "tc_debug") h->tc_debug = uint32_t(value);
         else if (n == "ivf_round0") h->ivf_round0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 64), 1 << 30)) / 16u * 16u;
         else throw Error(QADC_ERR_CONFIG, "set_option: unknown option " + n);
     });

@@ -20,13 +20,16 @@
 //     per-query row of 32 signed bytes that sum to v = 2048 + bias - thr - 1 (or -4096: admit all; +4064: padding row),
 //     so D = bias + sum - thr - 1 and "sum <= thr" is the SIGN BIT of the accumulator.
 //   * D (128 x 256 s32) lives in TMEM, two buffers of 256 columns; four epilogue warps read it back with tcgen05.ld
-//     (thread = code, 64 queries per load), OR the values and look at one sign bit per 64 pairs.  A flagged pair is
-//     re-evaluated exactly in integers from the reference-order table and passed through the CandidateHeap::push test
-//     (exact_admit_ct, scan_common.cuh) -- the filter never drops a pair the exact test would admit, so results are
-//     exact by construction, as in scan.cu.
-//   * Warp roles: 0-3 epilogue (TMEM lane quadrant = warp id), 4-7 one-hot generators, 8 MMA issuer (one elected
-//     lane; also owns the TMEM allocation), 9 producer (TMA code stream, tile loads, threshold rows).  All hand-offs
-//     are mbarriers; tcgen05.commit releases the one-hot stages and publishes the accumulators.
+//     (thread = code, 64 queries per load), OR the values and look at one sign bit per 64 pairs.  A flagged pair's
+//     accumulator is its exact sum; its (distance, id) key goes through the CandidateHeap::push test (heap.hpp:46-47)
+//     against the tile's threshold keys kept in shared memory.  Rows without a usable threshold (heap not full) are
+//     re-evaluated in integers from the reference-order table (exact_admit_ct, scan_common.cuh).  The sign test never
+//     drops a pair the exact test would admit, so results are exact by construction, as in scan.cu.
+//   * Warp roles: 0-7 epilogue (TMEM lane quadrant = warp id % 4, column half = warp id / 4), 8-11 one-hot
+//     generators, 12 MMA issuer (one elected lane; also owns the TMEM allocation), 13 producer (TMA code stream, tile
+//     loads, threshold rows).  All hand-offs are mbarriers; tcgen05.commit releases the one-hot stages and publishes
+//     the accumulators.  (Four epilogue warps were the bottleneck of the first version: 1970 cycles per sub-tile
+//     against 1205 of MMA, and the two did not overlap.)
 // The operand layouts, the instruction descriptor and TS/SS modes were pinned against a CPU reference on the B200 by
 // tools/umma_probe.cu before this kernel relied on them.
 #include "scan_common.cuh"
@@ -42,20 +45,34 @@ constexpr int TC_NSTAGE = 3;           // code stages (TMA ring)
 constexpr int TC_STAGE_BYTES = 8192;   // 1024 codes
 constexpr int TC_STAGE_CODES = TC_STAGE_BYTES / 8;
 constexpr int TC_INFO = 8;             // sub-tile info ring (generator -> epilogue)
+constexpr int TC_TKBUF = 4;            // per-tile threshold keys kept for the epilogue (it trails the producer by < 4 tiles)
 constexpr int TC_KC = 16;              // 16-byte K chunks of the table part (= tables)
 constexpr int TC_B_CHUNK = TC_TQ * 16; // bytes of one K chunk of B (256 rows x 16 B): the descriptor's LBO
 constexpr int TC_A_CHUNK = TC_SUB * 16;
 constexpr int TC_B_BYTES = (TC_KC + 2) * TC_B_CHUNK; // tables + the threshold K step
 constexpr int TC_A_BYTES = TC_KC * TC_A_CHUNK;
 constexpr int TC_AP_BYTES = 2 * TC_A_CHUNK;          // A': all ones, K = 32
-constexpr int TC_THREADS = 320;
-constexpr int TC_SMEM = TC_B_BYTES + TC_AP_BYTES + TC_NA * TC_A_BYTES + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8;
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13;
+constexpr int TC_THREADS = 14 * 32;
+constexpr int TC_WQ_CAP = 64;          // per-epilogue-warp queue of admitted (key, row) pairs
+constexpr int TC_SMEM = TC_B_BYTES + TC_AP_BYTES + TC_NA * TC_A_BYTES + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8 +
+                        TC_TKBUF * TC_TQ * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12;
 
 struct SubInfo {
     uint64_t id_ref;    // explicit ids: index of row 0's id in ScanArgs::ids; implicit: id of row 0
     uint32_t n_valid;   // codes in this sub-tile (rows >= n_valid are padding)
     uint32_t row_begin; // first LUT row of the tile
+    uint32_t tk_slot;   // which s_tk buffer holds this tile's threshold keys
+    uint32_t pad;
 };
+
+// the rare rows without a usable threshold (heap not full, or its worst entry saturated): integer re-evaluation from the
+// reference-order table.  One out-of-line copy: the epilogue's unrolled hit scan would otherwise carry 64 of them.
+__device__ __noinline__ void tc_exact_admit(const DevSpec* ds, const ScanArgs* a, uint32_t w0, uint32_t w1, uint32_t row,
+                                            uint32_t id) {
+    exact_admit_ct<GeomCT<8, 8, 4, 4>>(ds, a, w0, w1, row, id);
+}
 
 // shared-memory matrix descriptor: K-major, no swizzle (cute::UMMA::SmemDescriptor, version 1).  LBO = bytes between the
 // two 16-byte K chunks one MMA consumes, SBO = bytes between consecutive 8-row groups (a core matrix is 8 x 16 bytes)
@@ -122,6 +139,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     char* sA = sAp + TC_AP_BYTES;
     char* stage = sA + TC_NA * TC_A_BYTES;
     uint2* info_codes = reinterpret_cast<uint2*>(stage + TC_NSTAGE * TC_STAGE_BYTES);
+    uint64_t* s_tk = reinterpret_cast<uint64_t*>(info_codes + TC_INFO * TC_SUB); // [TC_TKBUF][TC_TQ] threshold keys per tile
+    uint64_t* s_wq_key = s_tk + TC_TKBUF * TC_TQ;                                  // [TC_EPI_WARPS][TC_WQ_CAP]
+    uint32_t* s_wq_row = reinterpret_cast<uint32_t*>(s_wq_key + TC_EPI_WARPS * TC_WQ_CAP);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
@@ -137,13 +157,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_dfull[i], 1);
-            mbar_init(&s_dempty[i], 4);
+            mbar_init(&s_dempty[i], TC_EPI_WARPS);
         }
         mbar_init(&s_tfull, 2); // the tile's expect_tx + the threshold rows' arrive
         mbar_init(&s_tempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 8) { // the MMA warp owns the tensor memory: 2 accumulators x 256 columns
+    if (warp == TC_MMA_WARP) { // the MMA warp owns the tensor memory: 2 accumulators x 256 columns
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "n"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -156,11 +176,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     const DevSpec* ds = &s_ds;
     const ScanArgs* a = &s_args;
     const uint32_t tmem = s_tmem;
+    const uint32_t dbg = a->filter_shift; // timing experiments (option tc_debug): 1 = epilogue reads nothing, 2 = generators store nothing, 4 = one MMA per sub-tile
 
     const uint32_t j_begin = a->cta_begin ? a->cta_begin[blockIdx.x] : uint32_t(uint64_t(a->n_jobs) * blockIdx.x / gridDim.x);
     const uint32_t j_end = a->cta_begin ? a->cta_begin[blockIdx.x + 1] : uint32_t(uint64_t(a->n_jobs) * (blockIdx.x + 1) / gridDim.x);
 
-    if (warp == 9) {
+    if (warp == TC_PROD_WARP) {
         // ============================ producer: code stream + tile loads + threshold rows ====================
         uint32_t it = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
@@ -177,8 +198,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         bulk_g2s(sB + off, src + off, 32768u, &s_tfull);
                 }
                 // threshold K step: row r gets 32 signed bytes that sum to v
+                uint64_t* tkb = s_tk + (tseq % TC_TKBUF) * TC_TQ;
                 for (uint32_t r = lane; r < uint32_t(TC_TQ); r += 32) {
                     int v = 4064; // padding rows never admit
+                    uint64_t tk_row = KEY_INF;
                     if (r < job.n_rows) {
                         const uint32_t row = job.row_begin + r;
                         const uint32_t q = a->row_query ? a->row_query[row] : row;
@@ -186,10 +209,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             const uint64_t tk = a->thr_key[q];
                             const uint32_t thr = uint32_t(tk >> 32);
                             const uint32_t bias = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;
+                            tk_row = tk;
                             if (tk == KEY_INF || thr >= ds->qmax) v = -4096; // heap not full / worst saturated: admit all
                             else v = 2048 + int(bias) - int(thr) - 1;
                         }
                     }
+                    tkb[r] = tk_row;
                     uint32_t w[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
@@ -226,13 +251,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 __syncwarp();
             }
         }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp >= TC_GEN_WARP0 && warp < TC_GEN_WARP0 + 4) {
         // ============================ generators: codes -> one-hot A stages ==================================
-        const uint32_t g = tid - 128; // row of the sub-tile
-        uint32_t it = 0, s = 0;
+        const uint32_t g = tid - TC_GEN_WARP0 * 32; // row of the sub-tile
+        uint32_t it = 0, s = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
             const ScanJob job = a->jobs[ji];
             if (job.n_codes == 0 || job.n_rows == 0) continue;
+            if (job.row_begin != prev_rb || job.n_rows != prev_nr) { // mirrors the producer's tile sequence
+                prev_rb = job.row_begin;
+                prev_nr = job.n_rows;
+                ++tseq;
+            }
             const uint32_t n_st = (job.n_codes + TC_STAGE_CODES - 1) / TC_STAGE_CODES;
             for (uint32_t st = 0; st < n_st; ++st, ++it) {
                 const uint32_t b = it % TC_NSTAGE;
@@ -249,6 +279,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     uint2 code = make_uint2(0u, 0u);
                     if (valid) code = *reinterpret_cast<const uint2*>(sb + size_t(i) * 8);
                     char* dst = sA + size_t(sa) * TC_A_BYTES + (g >> 3) * 128 + (g & 7u) * 16;
+                    if (!(dbg & 2u)) {
                     const uint32_t live = valid ? 1u : 0u; // padding rows: all-zero one-hot (masked again in the epilogue)
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
@@ -262,6 +293,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         v.w = wsel == 3 ? bit : 0u;
                         *reinterpret_cast<uint4*>(dst + j * TC_A_CHUNK) = v;
                     }
+                    }
                     const uint32_t slot = s % TC_INFO;
                     info_codes[slot * TC_SUB + g] = code;
                     if (g == 0) {
@@ -270,6 +302,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         inf.id_ref = a->ids ? job.ids_off + pos : uint64_t(job.id_base) + pos;
                         inf.n_valid = min(uint32_t(TC_SUB), cnt - sub * TC_SUB);
                         inf.row_begin = job.row_begin;
+                        inf.tk_slot = (tseq - 1) % TC_TKBUF;
+                        inf.pad = 0;
                         s_info[slot] = inf;
                     }
                     proxy_fence();
@@ -280,7 +314,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 if (lane == 0) mbar_arrive(&s_empty[b]); // this warp is done with the code stage
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == TC_MMA_WARP) {
         // ============================ MMA issuer ==============================================================
         uint32_t s = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
         const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB), ap_base = smem_u32(sAp);
@@ -306,6 +340,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     const uint32_t a0 = a_base + sa * TC_A_BYTES;
 #pragma unroll
                     for (int ks = 0; ks < TC_KC / 2; ++ks)
+                        if (ks == 0 || !(dbg & 4u))
                         umma_i8(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
                                 umma_desc(b_base + ks * 2 * TC_B_CHUNK, TC_B_CHUNK, 128), ks > 0);
                     umma_i8(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128), 1u);
@@ -318,7 +353,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     } else {
         // ============================ epilogue: TMEM -> sign test -> exact admission ==========================
         uint32_t s = 0;
-        const uint32_t lane_base = (warp * 32u) << 16; // this warp's TMEM lane quadrant
+        const uint32_t quad = warp & 3u, half_w = warp >> 2;   // TMEM lane quadrant, column half
+        const uint32_t rowi = quad * 32 + lane;                 // this thread's code (row of the sub-tile)
+        const uint32_t lane_base = (quad * 32u) << 16;
+        const uint32_t col_w = half_w * (TC_TQ / 2);
+        uint64_t* wq_key = s_wq_key + warp * TC_WQ_CAP;
+        uint32_t* wq_row = s_wq_row + warp * TC_WQ_CAP;
+        uint32_t qn = 0; // warp-uniform fill level of the queue
+        const uint32_t lt_mask = (1u << lane) - 1u;
+        auto drain = [&]() { // 32 admissions in flight at once (the atomics' round trips overlap)
+            __syncwarp();
+            for (uint32_t base = 0; base < qn; base += 32) {
+                const uint32_t e = base + lane;
+                if (e < qn) {
+                    const uint64_t key = wq_key[e];
+                    const uint32_t row = wq_row[e];
+                    const uint32_t q = a->row_query ? a->row_query[row] : row;
+                    const uint32_t at = atomicAdd(&a->cand_count[q], 1u);
+                    if (at < a->cap) a->cand[size_t(q) * a->cap + at] = key;
+                    else a->overflow[q] = 1u;
+                }
+            }
+            __syncwarp();
+            qn = 0;
+        };
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
             const ScanJob job = a->jobs[ji];
             if (job.n_codes == 0 || job.n_rows == 0) continue;
@@ -328,46 +386,99 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 mbar_wait(&s_dfull[buf], (s >> 1) & 1u);
                 tc_fence_after();
                 const SubInfo inf = s_info[slot];
-                const bool valid = tid < inf.n_valid;
+                const bool valid = rowi < inf.n_valid;
 #pragma unroll 1
-                for (uint32_t c0 = 0; c0 < uint32_t(TC_TQ); c0 += 64) {
+                for (uint32_t cb = 0; cb < uint32_t(TC_TQ / 2) && !(dbg & 1u); cb += 64) {
+                    const uint32_t c0 = col_w + cb;
                     uint32_t v[64];
                     tmem_ld64(tmem + buf * TC_TQ + lane_base + c0, v);
                     tmem_ld_wait();
-                    uint32_t any = 0;
+                    uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0; // four independent OR chains
 #pragma unroll
-                    for (int j = 0; j < 64; j += 2) any |= v[j] | v[j + 1];
-                    if (valid && (any >> 31)) {
-                        // rare: which of the 64 queries?  (sign bits -> two masks, then the exact test per set bit)
+                    for (int j = 0; j < 64; j += 8) {
+                        o0 |= v[j] | v[j + 1];
+                        o1 |= v[j + 2] | v[j + 3];
+                        o2 |= v[j + 4] | v[j + 5];
+                        o3 |= v[j + 6] | v[j + 7];
+                    }
+                    const uint32_t any = o0 | o1 | o2 | o3;
+                    if (__any_sync(0xffffffffu, valid && (any >> 31))) {
+                        // rare (warp-uniform branch): some sums of this batch are <= their query's threshold.  All lanes
+                        // turn their 64 sign bits into two masks; the warp then walks the UNION of flagged columns and
+                        // re-reads them from TMEM with one-column loads, four per wait (registers cannot be indexed
+                        // dynamically, and an unrolled 64-way test was measured 1.8x slower on the whole scan:
+                        // instruction-cache misses).  The accumulator IS the exact sum (D = bias + sum - thr - 1 with
+                        // thr < q_max: unsaturated), so the CandidateHeap::push test (heap.hpp:46-47) only needs the tile's
+                        // threshold key from shared memory.  Admitted keys go through a per-warp queue.
                         uint32_t m0 = 0, m1 = 0;
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             m0 |= (v[j] >> 31) << j;
                             m1 |= (v[32 + j] >> 31) << j;
                         }
-                        const uint2 code = info_codes[slot * TC_SUB + tid];
-                        const uint32_t id = a->ids ? a->ids[inf.id_ref + tid] : uint32_t(inf.id_ref) + tid;
-                        while (m0) {
-                            const uint32_t j = __ffs(m0) - 1;
-                            m0 &= m0 - 1;
-                            exact_admit_ct<G44>(ds, a, code.x, code.y, inf.row_begin + c0 + j, id);
-                        }
-                        while (m1) {
-                            const uint32_t j = __ffs(m1) - 1;
-                            m1 &= m1 - 1;
-                            exact_admit_ct<G44>(ds, a, code.x, code.y, inf.row_begin + c0 + 32 + j, id);
+                        if (!valid) m0 = m1 = 0u;
+                        const uint64_t* tks = s_tk + inf.tk_slot * TC_TQ;
+                        const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, inf.n_valid - 1)] : uint32_t(inf.id_ref) + rowi;
+#pragma unroll 1
+                        for (uint32_t hh = 0; hh < 2; ++hh) {
+                            const uint32_t mine = hh ? m1 : m0;
+                            uint32_t u = __reduce_or_sync(0xffffffffu, mine);
+                            while (u) {
+                                uint32_t jj[4], val[4];
+#pragma unroll
+                                for (int x = 0; x < 4; ++x) { // up to four flagged columns per TMEM round trip
+                                    jj[x] = u ? uint32_t(__ffs(u) - 1) : 0xFFFFFFFFu;
+                                    u &= u - 1; // (0 stays 0)
+                                }
+#pragma unroll
+                                for (int x = 0; x < 4; ++x) {
+                                    const uint32_t col = c0 + hh * 32 + (jj[x] == 0xFFFFFFFFu ? jj[0] : jj[x]);
+                                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(val[x]) : "r"(tmem + buf * TC_TQ + lane_base + col));
+                                }
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int x = 0; x < 4; ++x) {
+                                    const bool mineflag = jj[x] != 0xFFFFFFFFu && ((mine >> jj[x]) & 1u);
+                                    const uint32_t col = c0 + hh * 32 + (jj[x] & 31u);
+                                    uint64_t key = 0;
+                                    bool push = false;
+                                    if (mineflag) {
+                                        const uint64_t tk = tks[col];
+                                        const uint32_t thr = uint32_t(tk >> 32);
+                                        if (tk == KEY_INF || thr >= ds->qmax) {
+                                            const uint2 code = info_codes[slot * TC_SUB + rowi];
+                                            tc_exact_admit(ds, a, code.x, code.y, inf.row_begin + col, id);
+                                        } else {
+                                            key = make_key(uint32_t(int(val[x]) + int(thr) + 1), id);
+                                            push = key < tk;
+                                        }
+                                    }
+                                    const uint32_t bal = __ballot_sync(0xffffffffu, push);
+                                    if (bal) {
+                                        if (qn + 32 > uint32_t(TC_WQ_CAP)) drain();
+                                        if (push) {
+                                            const uint32_t e = qn + __popc(bal & lt_mask);
+                                            wq_key[e] = key;
+                                            wq_row[e] = inf.row_begin + col;
+                                        }
+                                        qn += __popc(bal);
+                                    }
+                                }
+                            }
                         }
                     }
                 }
+                if (qn >= 32) drain();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_dempty[buf]);
             }
         }
+        if (qn) drain();
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    if (warp == TC_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
 // ------------------------------------------------------------------------------------------ tile image --
