@@ -38,6 +38,9 @@ namespace qadc {
 
 namespace {
 
+#ifndef TC_PARK_NS
+#define TC_PARK_NS 0u
+#endif
 constexpr int TC_TQ = 256;             // queries per tile = MMA N
 constexpr int TC_SUB = 128;            // codes per sub-tile = MMA M
 constexpr int TC_NA = 3;               // one-hot stages
@@ -92,13 +95,28 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b,
 __device__ __forceinline__ void umma_commit(uint64_t* bar) { // arrives when every MMA issued so far has completed
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// mbarrier wait that parks the warp between polls (NANOSLEEP.SYNCS wakes on the barrier's phase change): ten of this
+// kernel's fourteen warps are waiting at any time, and a tight try_wait loop cost 22 % of all issued instructions
+__device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(addr), "r"(parity), "r"(TC_PARK_NS)
+            : "memory");
+    } while (!done);
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+// 128 consecutive columns, two per register: register i = low 16 bits of column 2i | low 16 bits of column 2i + 1 << 16
+// (every accumulator of this kernel fits 14 bits)
+__device__ __forceinline__ void tmem_ld128_pack16(uint32_t taddr, uint32_t (&v)[64]) {
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "tcgen05.ld.sync.aligned.32x32b.x64.pack::16b.b32 "
         "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
         "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
@@ -114,6 +132,19 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 using G44 = GeomCT<8, 8, 4, 4>; // 16x{4,4}: bit position of subquantizer j = 4 j
+
+// v[r] for a WARP-UNIFORM r: registers cannot be indexed dynamically, so this is a switch, which ptxas turns into a
+// six-level tree of uniform branches (~15 instructions, no divergence, no local memory)
+#define QADC_PICK4(b) case b: out = v[b]; break; case b + 1: out = v[b + 1]; break; case b + 2: out = v[b + 2]; break; case b + 3: out = v[b + 3]; break;
+#define QADC_PICK16(b) QADC_PICK4(b) QADC_PICK4(b + 4) QADC_PICK4(b + 8) QADC_PICK4(b + 12)
+__device__ __forceinline__ uint32_t pick64(const uint32_t (&v)[64], uint32_t r) {
+    uint32_t out = 0;
+    switch (r) {
+        QADC_PICK16(0) QADC_PICK16(16) QADC_PICK16(32) QADC_PICK16(48)
+    default: break;
+    }
+    return out;
+}
 
 // sub-tiles of one job: its stages hold TC_STAGE_CODES codes each, every stage is cut into sub-tiles of TC_SUB codes
 __device__ __forceinline__ uint32_t job_subtiles(uint32_t n_codes) {
@@ -190,7 +221,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             if (job.row_begin != prev_rb || job.n_rows != prev_nr) {
                 prev_rb = job.row_begin;
                 prev_nr = job.n_rows;
-                mbar_wait(&s_tempty, (tseq & 1u) ^ 1u); // the MMAs of the previous tile are done with B
+                mbar_wait_park(&s_tempty, (tseq & 1u) ^ 1u); // the MMAs of the previous tile are done with B
                 if (lane == 0) {
                     const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / TC_TQ) * (TC_KC * TC_B_CHUNK);
                     mbar_expect_tx(&s_tfull, TC_KC * TC_B_CHUNK);
@@ -240,7 +271,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             const uint32_t n_st = (job.n_codes + TC_STAGE_CODES - 1) / TC_STAGE_CODES;
             for (uint32_t st = 0; st < n_st; ++st, ++it) {
                 const uint32_t b = it % TC_NSTAGE;
-                mbar_wait(&s_empty[b], ((it / TC_NSTAGE) & 1u) ^ 1u);
+                mbar_wait_park(&s_empty[b], ((it / TC_NSTAGE) & 1u) ^ 1u);
                 if (lane == 0) {
                     const uint32_t first = st * TC_STAGE_CODES;
                     const uint32_t cnt = min(uint32_t(TC_STAGE_CODES), job.n_codes - first);
@@ -266,33 +297,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             const uint32_t n_st = (job.n_codes + TC_STAGE_CODES - 1) / TC_STAGE_CODES;
             for (uint32_t st = 0; st < n_st; ++st, ++it) {
                 const uint32_t b = it % TC_NSTAGE;
-                mbar_wait(&s_full[b], (it / TC_NSTAGE) & 1u);
+                mbar_wait_park(&s_full[b], (it / TC_NSTAGE) & 1u);
                 const uint32_t first = st * TC_STAGE_CODES;
                 const uint32_t cnt = min(uint32_t(TC_STAGE_CODES), job.n_codes - first);
                 const char* sb = stage + size_t(b) * TC_STAGE_BYTES;
                 const uint32_t n_sub = (cnt + TC_SUB - 1) / TC_SUB;
                 for (uint32_t sub = 0; sub < n_sub; ++sub, ++s) {
                     const uint32_t sa = s % TC_NA;
-                    mbar_wait(&s_aempty[sa], ((s / TC_NA) & 1u) ^ 1u); // the MMAs that read this stage have completed
+                    mbar_wait_park(&s_aempty[sa], ((s / TC_NA) & 1u) ^ 1u); // the MMAs that read this stage have completed
                     const uint32_t i = sub * TC_SUB + g;
                     const bool valid = i < cnt;
                     uint2 code = make_uint2(0u, 0u);
                     if (valid) code = *reinterpret_cast<const uint2*>(sb + size_t(i) * 8);
                     char* dst = sA + size_t(sa) * TC_A_BYTES + (g >> 3) * 128 + (g & 7u) * 16;
                     if (!(dbg & 2u)) {
-                    const uint32_t live = valid ? 1u : 0u; // padding rows: all-zero one-hot (masked again in the epilogue)
+                        // 16 stores of 16 bytes: table j's chunk is a 0x01 byte at position c_j.  (A 17-entry table of the
+                        // chunks in shared memory saves ALU work but its bank conflicts overload the shared-memory pipe the
+                        // MMA operands come through: measured 1.6x slower.)
+                        const uint32_t one = valid ? 1u : 0u; // padding rows: all zero (masked again in the epilogue)
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const uint32_t n = ((j < 8 ? code.x : code.y) >> ((j & 7) * 4)) & 15u;
-                        const uint32_t bit = live << ((n & 3u) * 8);
-                        const uint32_t wsel = n >> 2;
-                        uint4 v;
-                        v.x = wsel == 0 ? bit : 0u;
-                        v.y = wsel == 1 ? bit : 0u;
-                        v.z = wsel == 2 ? bit : 0u;
-                        v.w = wsel == 3 ? bit : 0u;
-                        *reinterpret_cast<uint4*>(dst + j * TC_A_CHUNK) = v;
-                    }
+                        for (int j = 0; j < 16; ++j) {
+                            const uint32_t cw = j < 8 ? code.x : code.y;
+                            constexpr int kShiftBase = 0;
+                            (void)kShiftBase;
+                            const int sh = (j & 7) * 4 - 3;                                      // 8 * nibble, in place
+                            const uint32_t n8 = (sh >= 0 ? cw >> (sh >= 0 ? sh : 0) : cw << 3) & 0x78u;
+                            const uint32_t bit = __funnelshift_l(0u, one, n8);                   // one << (n8 & 31)
+                            const uint32_t wsel = n8 >> 5;
+                            uint4 v;
+                            v.x = wsel == 0 ? bit : 0u;
+                            v.y = wsel == 1 ? bit : 0u;
+                            v.z = wsel == 2 ? bit : 0u;
+                            v.w = wsel == 3 ? bit : 0u;
+                            *reinterpret_cast<uint4*>(dst + j * TC_A_CHUNK) = v;
+                        }
                     }
                     const uint32_t slot = s % TC_INFO;
                     info_codes[slot * TC_SUB + g] = code;
@@ -306,7 +344,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         inf.pad = 0;
                         s_info[slot] = inf;
                     }
-                    proxy_fence();
+                    if (!(dbg & 16u)) proxy_fence();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&s_afull[sa]);
                 }
@@ -326,14 +364,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 prev_nr = job.n_rows;
                 if (tseq > 0 && lane == 0) umma_commit(&s_tempty); // every MMA on the old tile has completed
                 __syncwarp();
-                mbar_wait(&s_tfull, tseq & 1u);
+                mbar_wait_park(&s_tfull, tseq & 1u);
                 ++tseq;
             }
             const uint32_t n_sub = job_subtiles(job.n_codes);
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
                 const uint32_t sa = s % TC_NA, buf = s & 1u;
-                mbar_wait(&s_afull[sa], (s / TC_NA) & 1u);
-                mbar_wait(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
+                mbar_wait_park(&s_afull[sa], (s / TC_NA) & 1u);
+                mbar_wait_park(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t d = tmem + buf * TC_TQ;
@@ -383,95 +421,98 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             const uint32_t n_sub = job_subtiles(job.n_codes);
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
                 const uint32_t buf = s & 1u, slot = s % TC_INFO;
-                mbar_wait(&s_dfull[buf], (s >> 1) & 1u);
+                mbar_wait_park(&s_dfull[buf], (s >> 1) & 1u);
                 tc_fence_after();
                 const SubInfo inf = s_info[slot];
                 const bool valid = rowi < inf.n_valid;
-#pragma unroll 1
-                for (uint32_t cb = 0; cb < uint32_t(TC_TQ / 2) && !(dbg & 1u); cb += 64) {
-                    const uint32_t c0 = col_w + cb;
+                if (!(dbg & 1u)) {
+                    // this warp's 128 queries of the tile, two 16-bit sums per register
+                    const uint32_t c0 = col_w;
                     uint32_t v[64];
-                    tmem_ld64(tmem + buf * TC_TQ + lane_base + c0, v);
+                    tmem_ld128_pack16(tmem + buf * TC_TQ + lane_base + c0, v);
                     tmem_ld_wait();
-                    uint32_t o0 = 0, o1 = 0, o2 = 0, o3 = 0; // four independent OR chains
+                    // everything this warp needs from the accumulator is in registers now: hand the buffer back to the MMA
+                    // warp BEFORE looking at the values (admissions never touch tensor memory again)
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s_dempty[buf]);
+                    uint32_t g[4]; // OR of each group of 16 registers = 32 columns (four independent chains)
 #pragma unroll
-                    for (int j = 0; j < 64; j += 8) {
-                        o0 |= v[j] | v[j + 1];
-                        o1 |= v[j + 2] | v[j + 3];
-                        o2 |= v[j + 4] | v[j + 5];
-                        o3 |= v[j + 6] | v[j + 7];
+                    for (int k = 0; k < 4; ++k) {
+                        uint32_t o = 0;
+#pragma unroll
+                        for (int j = 0; j < 16; j += 2) o |= v[16 * k + j] | v[16 * k + j + 1];
+                        g[k] = o & 0x80008000u; // sign bits of the even / odd columns
                     }
-                    const uint32_t any = o0 | o1 | o2 | o3;
-                    if (__any_sync(0xffffffffu, valid && (any >> 31))) {
-                        // rare (warp-uniform branch): some sums of this batch are <= their query's threshold.  All lanes
-                        // turn their 64 sign bits into two masks; the warp then walks the UNION of flagged columns and
-                        // re-reads them from TMEM with one-column loads, four per wait (registers cannot be indexed
-                        // dynamically, and an unrolled 64-way test was measured 1.8x slower on the whole scan:
+                    const uint32_t any = g[0] | g[1] | g[2] | g[3];
+                    if (__any_sync(0xffffffffu, valid && any != 0u) && !(dbg & 8u)) {
+                        // rare (warp-uniform branch): some sums of this sub-tile are <= their query's threshold.  For each
+                        // group of 32 columns that is flagged anywhere in the warp, all lanes turn their 32 sign bits into a
+                        // mask (bit i = column 2i, bit 16 + i = column 2i + 1); the warp then walks the UNION of flagged
+                        // columns and re-reads them from TMEM with one-column loads, four per wait (registers cannot be
+                        // indexed dynamically, and an unrolled test per column was measured 1.8x slower on the whole scan:
                         // instruction-cache misses).  The accumulator IS the exact sum (D = bias + sum - thr - 1 with
                         // thr < q_max: unsaturated), so the CandidateHeap::push test (heap.hpp:46-47) only needs the tile's
                         // threshold key from shared memory.  Admitted keys go through a per-warp queue.
-                        uint32_t m0 = 0, m1 = 0;
+                        uint32_t m[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            m0 |= (v[j] >> 31) << j;
-                            m1 |= (v[32 + j] >> 31) << j;
+                        for (int k = 0; k < 4; ++k) {
+                            if (__any_sync(0xffffffffu, valid && g[k] != 0u)) {
+#pragma unroll
+                                for (int i = 0; i < 16; ++i) {
+                                    const uint32_t x = i == 15 ? v[16 * k + i] : (v[16 * k + i] >> (15 - i));
+                                    m[k] |= x & (0x00010001u << i);
+                                }
+                                if (!valid) m[k] = 0u;
+                            }
                         }
-                        if (!valid) m0 = m1 = 0u;
                         const uint64_t* tks = s_tk + inf.tk_slot * TC_TQ;
                         const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, inf.n_valid - 1)] : uint32_t(inf.id_ref) + rowi;
+                        // ONE copy of the column loop (the switch inside pick64 is ~200 instructions; sixteen inlined
+                        // copies of it thrashed the instruction cache)
 #pragma unroll 1
-                        for (uint32_t hh = 0; hh < 2; ++hh) {
-                            const uint32_t mine = hh ? m1 : m0;
+                        for (uint32_t hh = 0; hh < 4; ++hh) {
+                            const uint32_t mine = hh == 0 ? m[0] : hh == 1 ? m[1] : hh == 2 ? m[2] : m[3];
                             uint32_t u = __reduce_or_sync(0xffffffffu, mine);
                             while (u) {
-                                uint32_t jj[4], val[4];
-#pragma unroll
-                                for (int x = 0; x < 4; ++x) { // up to four flagged columns per TMEM round trip
-                                    jj[x] = u ? uint32_t(__ffs(u) - 1) : 0xFFFFFFFFu;
-                                    u &= u - 1; // (0 stays 0)
-                                }
-#pragma unroll
-                                for (int x = 0; x < 4; ++x) {
-                                    const uint32_t col = c0 + hh * 32 + (jj[x] == 0xFFFFFFFFu ? jj[0] : jj[x]);
-                                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(val[x]) : "r"(tmem + buf * TC_TQ + lane_base + col));
-                                }
-                                tmem_ld_wait();
-#pragma unroll
-                                for (int x = 0; x < 4; ++x) {
-                                    const bool mineflag = jj[x] != 0xFFFFFFFFu && ((mine >> jj[x]) & 1u);
-                                    const uint32_t col = c0 + hh * 32 + (jj[x] & 31u);
-                                    uint64_t key = 0;
-                                    bool push = false;
-                                    if (mineflag) {
-                                        const uint64_t tk = tks[col];
-                                        const uint32_t thr = uint32_t(tk >> 32);
-                                        if (tk == KEY_INF || thr >= ds->qmax) {
-                                            const uint2 code = info_codes[slot * TC_SUB + rowi];
-                                            tc_exact_admit(ds, a, code.x, code.y, inf.row_begin + col, id);
-                                        } else {
-                                            key = make_key(uint32_t(int(val[x]) + int(thr) + 1), id);
-                                            push = key < tk;
-                                        }
+                                const uint32_t b = uint32_t(__ffs(u) - 1);
+                                u &= u - 1;
+                                const uint32_t raw = pick64(v, hh * 16 + (b & 15u)); // columns 2i (low half) and 2i + 1
+                                const uint32_t val = (b >> 4) ? uint32_t(int(raw) >> 16) : uint32_t(int(raw << 16) >> 16);
+                                const uint32_t col = c0 + hh * 32 + 2 * (b & 15u) + (b >> 4);
+                                uint64_t key = 0;
+                                bool push = false;
+                                if ((mine >> b) & 1u) {
+                                    const uint64_t tk = tks[col];
+                                    const uint32_t thr = uint32_t(tk >> 32);
+                                    if (tk == KEY_INF || thr >= ds->qmax) {
+                                        const uint2 code = info_codes[slot * TC_SUB + rowi];
+                                        tc_exact_admit(ds, a, code.x, code.y, inf.row_begin + col, id);
+                                    } else {
+                                        key = make_key(uint32_t(int(val) + int(thr) + 1), id);
+                                        push = key < tk;
                                     }
-                                    const uint32_t bal = __ballot_sync(0xffffffffu, push);
-                                    if (bal) {
-                                        if (qn + 32 > uint32_t(TC_WQ_CAP)) drain();
-                                        if (push) {
-                                            const uint32_t e = qn + __popc(bal & lt_mask);
-                                            wq_key[e] = key;
-                                            wq_row[e] = inf.row_begin + col;
-                                        }
-                                        qn += __popc(bal);
+                                }
+                                const uint32_t bal = __ballot_sync(0xffffffffu, push);
+                                if (bal) {
+                                    if (qn + 32 > uint32_t(TC_WQ_CAP)) drain();
+                                    if (push) {
+                                        const uint32_t e = qn + __popc(bal & lt_mask);
+                                        wq_key[e] = key;
+                                        wq_row[e] = inf.row_begin + col;
                                     }
+                                    qn += __popc(bal);
                                 }
                             }
                         }
                     }
                 }
                 if (qn >= 32) drain();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&s_dempty[buf]);
+                if (dbg & 1u) { // (timing experiment: nothing was read)
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&s_dempty[buf]);
+                }
             }
         }
         if (qn) drain();
