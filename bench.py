@@ -492,6 +492,13 @@ def run_ours(qb, name, wl, args, rank, local_rank, world, dist):
         prop = torch.cuda.get_device_properties(dev)
         smem_peak = 128.0 * prop.multi_processor_count * sm_clock / 1e9
         smem_ach = (st_acc["pairs"] * lookups * entry_bytes / scan_s) / 1e9 if scan_s > 0 else None
+        if variant == 12:
+            # the tensor-core scan: one-hot int8 contraction, K = 256 table bytes + 32 threshold bytes per (code, query)
+            top = (st_acc["pairs"] * 2.0 * 288 / scan_s) / 1e12 if scan_s > 0 else None
+            roofline["tensor"] = {"bound": "tensor (tcgen05 kind::i8)", "achieved": top, "peak": 4492.0, "unit": "TOP/s",
+                                  "frac": top / 4492.0 if top else None, "ops_per_pair": 576,
+                                  "peak_source": "measured on this pool: back-to-back M=128 N=256 K=256 kind::i8 MMAs on all "
+                                                 "SMs, tools/umma_probe.cu (nominal dense int8: 4500 TOP/s)"}
         if variant < 12:
             roofline["smem"] = {"bound": "shared-memory pipe", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
                                 "frac": smem_ach / smem_peak if smem_ach else None,

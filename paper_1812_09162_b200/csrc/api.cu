@@ -202,8 +202,25 @@ namespace qadc {
 
 static constexpr uint64_t CODE_PAD = 1024; // device code arrays are padded to this many codes
 
-static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true) {
-    ScanPlan p = plan_scan(h->ds, h->device, h->force_variant, allow_merged);
+// nq = queries of the batch about to be scanned (0 = unknown / one list with one table set).
+// The tensor-core scan (scan_tc.cu) works on 256-query tiles and wants long code streams: it takes over from the
+// shared-memory kernel's 32-row tiles once a batch fills a good part of a tile and the list is long enough for its
+// big segments to dominate (measured: C4 2.85x faster, C1 -- 1e6 codes x 1e3 queries, launch bound -- 7 % slower,
+// a single query 2.2x slower).
+static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true, uint32_t nq = 0) {
+    int force = h->force_variant;
+    if (force < 0) {
+        if (const char* e = std::getenv("QADC_FORCE_VARIANT")) force = std::atoi(e); // tests: every entry point, one variant
+    }
+    if (force < 0 && allow_merged && h->kind == 0 && nq >= 96 && h->count >= (uint64_t(4) << 20)) {
+        try {
+            ScanPlan p = plan_scan(h->ds, h->device, int(VAR_TC8), true);
+            p.filter_shift = h->tc_debug;
+            return p;
+        } catch (const Error&) { // not 16x{4,4}
+        }
+    }
+    ScanPlan p = plan_scan(h->ds, h->device, force, allow_merged);
     if (p.variant == VAR_TC8) p.filter_shift = h->tc_debug;
     return p;
 }
@@ -372,7 +389,7 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
     if (uint64_t(p.t) > h->calib_limit)
         throw Error(QADC_ERR_CONFIG, "search: t = " + std::to_string(p.t) + " exceeds the replicated calibration head (" +
                                          std::to_string(h->calib_limit) + " codes of a longer list): open the shard with a longer head");
-    const ScanPlan plan = plan_for(h);
+    const ScanPlan plan = plan_for(h, true, nq);
     h->stats.scan_variant = plan.variant;
     h->stats.query_tile = plan.tq;
     const DevSpec& ds = h->ds;

@@ -90,6 +90,42 @@ def test_scan_fn_differential(port):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (pat, m, n, kw["cap"])
 
 
+def test_tensor_core_scan_through_scan_fn_contract(port, monkeypatch):
+    """The tcgen05 one-hot GEMM scan (scan_tc.cu, variant 12) forced onto the QuantizedScanFn entry point
+    (QADC_FORCE_VARIANT): the same differential as above for 16x{4,4} -- ragged list lengths (sub-tile and stage
+    tails), saturation-heavy tables, pre-seeded heaps, accumulator bias up to q_max + 1 (folded into the threshold
+    K step), both id modes, heaps that never fill (rows without a threshold take the exact re-evaluation), and the
+    all-zero / all-saturated corner tables of T/test_kernels.cpp:79-105, 135-159."""
+    monkeypatch.setenv("QADC_FORCE_VARIANT", "12")
+    rng = np.random.default_rng(4242)
+    s, so = qb.allocate_dims(128, "16x{4,4}"), port.spec(128, "16x{4,4}")
+    for trial in range(40):
+        if rng.integers(4) == 0:
+            qlut = (255 - rng.integers(0, 64, size=256)).astype(np.uint8)
+        elif rng.integers(3) == 0:
+            qlut = rng.integers(0, 24, size=256).astype(np.uint8)        # small sums: dense admissions, many ties
+        else:
+            qlut = rng.integers(0, 256, size=256).astype(np.uint8)
+        n = int([1, 127, 128, 129, 1023, 1024, 1025, 5000, 20000, 70001][trial % 10] + rng.integers(0, 3))
+        pk = qb.pack_list(s, random_codes(s, n, seed=int(rng.integers(1 << 30))))
+        kw = dict(cap=int([1, 7, 24, 100, 1000][trial % 5]),
+                  acc_init=int(rng.integers(257)) if rng.integers(3) == 0 else 0,
+                  base_id=int(rng.integers(100000)),
+                  ids=rng.integers(0, 1000000, size=n).astype(np.uint32) if rng.integers(2) else None,
+                  heap_in=[(int(rng.integers(256)), 2000000 + i) for i in range(int(rng.integers(4)))])
+        a = port.scan_quantized(so, pk, n, qlut, **kw)
+        b = qb.scan_list(s, pk, n, qlut, **kw)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (trial, n, kw["cap"], kw["acc_init"])
+    n = 30000
+    pk = qb.pack_list(s, random_codes(s, n, seed=3))
+    d, i = qb.scan_list(s, pk, n, np.zeros(256, np.uint8), cap=10, base_id=7)
+    assert d.tolist() == [0] * 10 and i.tolist() == list(range(7, 17))
+    d, i = qb.scan_list(s, pk, n, np.full(256, 255, np.uint8), cap=5, heap_in=[(9, 1), (8, 2), (7, 3), (6, 4), (5, 5)])
+    assert i.tolist() == [5, 4, 3, 2, 1]
+    d, i = qb.scan_list(s, pk, n, np.full(256, 255, np.uint8), cap=5)
+    assert d.tolist() == [255] * 5 and i.tolist() == [0, 1, 2, 3, 4]
+
+
 def test_scan_list_config_errors():
     # scan_scalar.hpp:23-27, 38-39; heap.hpp:27-28
     s = qb.allocate_dims(128, "16x{4,4}")
