@@ -171,6 +171,21 @@ int qadc_merge_topk_device(const uint64_t* d_keys, uint32_t nshards, uint32_t nq
                            uint32_t flags, uint32_t* d_out_ids, float* d_out_dists, uint32_t* d_out_counts,
                            int device, void* stream);
 
+/* ---- one process, several GPUs ----------------------------
+ * The reference is single-process; its multi-GPU drop-in is ONE handle that owns a shard per device: contiguous
+ * block-aligned code ranges scanned with base_id = range start (the chunked-scan contract, T/test_kernels.cpp:107-133),
+ * the whole list's calibration head replicated on every device (index.hpp:124-129), one ncclAllGather of the per-shard
+ * (distance << 32 | id) key lists and the merge kernel on devices[0].  NCCL is bound at run time (dlopen of
+ * libnccl.so.2); ndev = 1 works without it.  devices = NULL means ordinals 0..ndev-1. */
+typedef struct qadc_multi qadc_multi;
+int qadc_flat_open_sharded(const qadc_spec* spec, const float* codebook, const uint8_t* packed, uint64_t count, int ndev,
+                           const int* devices, qadc_multi** out);
+/* FlatIndex::search over a batch (index.hpp:110), host buffers, same output convention as qadc_search_batch */
+int qadc_multi_search_batch(qadc_multi* h, const float* queries, uint32_t nq, const qadc_search_params* params,
+                            uint32_t* out_ids, float* out_dists, uint32_t* out_counts);
+int qadc_multi_info(const qadc_multi* h, int* ndev, uint64_t* count, int* uses_nccl);
+void qadc_multi_close(qadc_multi* h);
+
 /* ---- debug / parity entry points ----------------------- */
 /* float LUTs (compute_tables, distance.hpp:35-58), calibration and quantized
  * LUTs (quantize_tables, distance.hpp:102-142) of a flat index.  Any output may

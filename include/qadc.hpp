@@ -147,9 +147,19 @@ public:
         const std::vector<float> cb = flatten(ref.codebook());
         rethrow(qadc_flat_open(&s, cb.data(), ref.list().data.data(), ref.list().count, 0, nullptr, 0, 0, device, &h_));
     }
+    // the same index sharded over ndev GPUs of this process (devices = nullptr: ordinals 0..ndev-1): contiguous
+    // block-aligned shards, replicated calibration head, one NCCL all_gather + merge per batch
+    GpuFlatIndex(const pqscan::FlatIndex& ref, int ndev, const int* devices) : dims_(ref.codebook().spec().total_dims()) {
+        const qadc_spec s = to_abi(ref.codebook().spec());
+        const std::vector<float> cb = flatten(ref.codebook());
+        rethrow(qadc_flat_open_sharded(&s, cb.data(), ref.list().data.data(), ref.list().count, ndev, devices, &m_));
+    }
     GpuFlatIndex(const GpuFlatIndex&) = delete;
     GpuFlatIndex& operator=(const GpuFlatIndex&) = delete;
-    ~GpuFlatIndex() { qadc_close(h_); }
+    ~GpuFlatIndex() {
+        qadc_close(h_);
+        qadc_multi_close(m_);
+    }
 
     pqscan::SearchResult search(std::span<const float> query, const pqscan::SearchParams& params) const {
         if (query.size() != dims_) throw pqscan::input_error("search: query has wrong dimension");
@@ -161,12 +171,14 @@ public:
         const qadc_search_params p = detail::params_of(params);
         std::vector<uint32_t> ids(size_t{nq} * p.r), counts(nq);
         std::vector<float> dists(size_t{nq} * p.r);
-        rethrow(qadc_search_batch(h_, queries.data(), nq, &p, ids.data(), dists.data(), counts.data()));
+        if (m_) rethrow(qadc_multi_search_batch(m_, queries.data(), nq, &p, ids.data(), dists.data(), counts.data()));
+        else rethrow(qadc_search_batch(h_, queries.data(), nq, &p, ids.data(), dists.data(), counts.data()));
         return detail::split(nq, p.r, ids, dists, counts);
     }
 
 private:
     qadc_index* h_ = nullptr;
+    qadc_multi* m_ = nullptr;
     uint32_t dims_;
 };
 

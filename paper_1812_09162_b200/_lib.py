@@ -97,6 +97,8 @@ def lib() -> C.CDLL:
         L.qadc_packed_bytes.argtypes = [C.POINTER(QadcSpec), C.c_uint64]
         L.qadc_close.restype = None
         L.qadc_close.argtypes = [C.c_void_p]
+        L.qadc_multi_close.restype = None
+        L.qadc_multi_close.argtypes = [C.c_void_p]
         _LIB = L
     return _LIB
 

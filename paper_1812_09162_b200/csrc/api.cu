@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -42,6 +43,9 @@ static int guarded(F&& f) {
         return QADC_ERR_CUDA;
     }
 }
+
+// the same status mapping for the other translation units' entry points (multi.cu)
+int multi_guarded(const std::function<void()>& f) { return guarded(f); }
 
 struct DevBuf {
     void* p = nullptr;

@@ -195,6 +195,57 @@ class FlatIndex(_Index):
         return out
 
 
+class MultiGpuFlatIndex:
+    """One process, several GPUs: FlatIndex sharded over ``ndev`` devices behind one handle (qadc_flat_open_sharded):
+    block-aligned shards with base ids, replicated calibration head, one NCCL all_gather + merge per batch."""
+
+    def __init__(self, spec: QadcSpec, codebook, packed, count: int, ndev: int = 1, devices=None):
+        self.spec, self.count, self._h = spec, int(count), C.c_void_p()
+        cb = _f32(codebook).reshape(-1)
+        if cb.size != spec.cb_floats:
+            raise QadcError(5, "codebook: table count does not match spec")
+        pk = np.ascontiguousarray(packed, dtype=np.uint8).reshape(-1)
+        if pk.size < packed_bytes(spec, count):
+            raise QadcError(5, "packed list is shorter than its code count requires")
+        dv = None if devices is None else np.ascontiguousarray(devices, dtype=np.int32)
+        check(lib().qadc_flat_open_sharded(C.byref(spec), _p(cb, C.c_float), _p(pk, C.c_uint8), C.c_uint64(count),
+                                           C.c_int(ndev), _p(dv, C.c_int), C.byref(self._h)))
+
+    def info(self):
+        ndev, count, nccl = C.c_int(), C.c_uint64(), C.c_int()
+        check(lib().qadc_multi_info(self._h, C.byref(ndev), C.byref(count), C.byref(nccl)))
+        return dict(ndev=ndev.value, count=int(count.value), uses_nccl=bool(nccl.value))
+
+    def search(self, queries, params: SearchParams | None = None) -> SearchResult:
+        params = params or SearchParams()
+        q = _f32(queries).reshape(-1, self.spec.dims)
+        nq, r = q.shape[0], max(int(params.r), 1)
+        ids = np.empty((nq, r), dtype=np.uint32)
+        dists = np.empty((nq, r), dtype=np.float32)
+        counts = np.zeros(nq, dtype=np.uint32)
+        cp = params.c()
+        check(lib().qadc_multi_search_batch(self._h, _p(q, C.c_float), C.c_uint32(nq), C.byref(cp), _p(ids, C.c_uint32),
+                                            _p(dists, C.c_float), _p(counts, C.c_uint32)))
+        return SearchResult(ids, dists, counts)
+
+    def close(self):
+        if self._h:
+            lib().qadc_multi_close(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class IvfIndex(_Index):
     """IvfIndex (index.hpp:166-177): coarse partition + per-cell packed lists of residual codes."""
 

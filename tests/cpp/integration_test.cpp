@@ -13,6 +13,8 @@
 
 using namespace pqscan;
 
+static void cudaGetDeviceCount_shim(int* n) { *n = qadc_device_count(); } // the ABI's own device probe (no CUDA headers here)
+
 static int g_fail = 0;
 #define EXPECT(cond, ...)                      \
     do {                                       \
@@ -142,6 +144,15 @@ static void flat_checks() {
             gpu.search({queries.data(), d}, bad);
         } catch (const input_error&) { threw = true; }
         EXPECT(threw, "flat %s: t < R must be an input_error", text);
+        // the one-process multi-GPU handle (qadc_flat_open_sharded) on the devices this box has: shards + replicated
+        // head + NCCL all_gather + merge must give the same lists
+        {
+            int ndev = 0;
+            cudaGetDeviceCount_shim(&ndev);
+            qadc::GpuFlatIndex multi(ref, ndev > 0 ? ndev : 1, nullptr);
+            auto mb = multi.search_batch(queries, 40, p);
+            for (uint32_t q = 0; q < 40; ++q) EXPECT(same(batch[q], mb[q]), "flat %s sharded(%d) query %u differs", text, ndev, q);
+        }
         std::printf("flat %s: 40 queries identical to FlatIndex::search\n", text);
     }
 }

@@ -435,6 +435,37 @@ def test_sharded_device_path_equals_unsharded(port, dims, text, n, world):
 
 # ------------------------------------------------ reference-side C++ binding (qadc.hpp) --
 
+def test_one_process_multi_gpu_handle(port):
+    """qadc_flat_open_sharded / qadc_multi_search_batch (the C++ single-process host: shards with base ids, replicated
+    calibration head, ncclAllGather, merge) on the devices of this box: same result as the plain FlatIndex and the
+    oracle; the exchange goes through NCCL whenever libnccl can be loaded; bad device lists are input errors."""
+    import torch  # noqa: F401  (loads the NCCL build the process shares)
+    rng = np.random.default_rng(12)
+    ndev = qb.lib().qadc_device_count()
+    for dims, text, n in [(128, "16x{4,4}", 120_000), (96, "12x{6,5,5}", 33_333), (64, "8x{8}", 100)]:
+        s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+        cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+        pk = qb.pack_list(s, random_codes(s, n, seed=31))
+        queries = (rng.standard_normal((50, dims)) * 2).astype(np.float32)
+        want = port.flat_search(so, cb, pk, n, queries, r=100, t=400, threads=8)
+        with qb.MultiGpuFlatIndex(s, cb, pk, n, ndev=ndev) as idx:
+            info = idx.info()
+            assert info["ndev"] == ndev and info["count"] == n and info["uses_nccl"]
+            for _ in range(2):
+                got = idx.search(queries, qb.SearchParams(r=100, t=400))
+                assert np.array_equal(got.counts, want[2])
+                for qi in range(len(queries)):
+                    c = int(want[2][qi])
+                    assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]) and bits_equal(got.dists[qi, :c], want[1][qi, :c])
+            with pytest.raises(qb.QadcError) as e:
+                idx.search(queries, qb.SearchParams(r=100, t=400, rerank=True))
+            assert e.value.kind == "config"
+    for bad in ([0, 0], [ndev], [-1]):
+        with pytest.raises(qb.QadcError) as e:
+            qb.MultiGpuFlatIndex(s, cb, pk, n, ndev=len(bad), devices=bad)
+        assert e.value.kind == "input"
+
+
 def test_cpp_integration_binary():
     """The reference's own C++ types (FlatIndex, IvfIndex, QuantizedScanFn, CandidateHeap) against the GPU path
     through include/qadc.hpp.  The binary is compiled in the build container against the unmodified reference
