@@ -474,7 +474,7 @@ static void ivf_probe_order_device(qadc_index* h, const float* dq, uint32_t nb, 
     h->scratch.ensure(size_t(nb) * K * 4);
     h->cta_begin.ensure((2 * size_t(nb) + 1) * 4); // reused as the probe-selection redo flags | list | count
     if (h->probe_tc && h->probe_tc_ready && ivf_probe_tc_supported(ds.dims, K, a)) {
-        h->q_bf16.ensure(size_t(nb) * h->dpad * 2);
+        h->q_bf16.ensure(ivf_probe_tc_query_image_elems(nb, h->dpad) * 2);
         h->probe_eps.ensure(size_t(nb) * 8);
         launch_ivf_probe_tc(dq, h->coarse.as<float>(), h->coarse_bf16.as<uint16_t>(),
                             h->coarse_norm.as<float>(), h->coarse_mean.as<double>(), h->coarse_rmax, ds.dims, h->dpad, K,

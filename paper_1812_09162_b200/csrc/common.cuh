@@ -188,6 +188,7 @@ void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t 
                       cudaStream_t stream, bool redo_only = false);
 // tensor-core prefilter of the probe order (ivf_probe_tc.cu)
 bool ivf_probe_tc_supported(uint32_t dims, uint32_t k_cells, uint32_t a);
+size_t ivf_probe_tc_query_image_elems(uint32_t nq, uint32_t dpad); // bf16 elements of the tiled query operand image
 bool ivf_probe_tc_prepare(const float* coarse, uint32_t k_cells, uint32_t dims, uint32_t dpad,
                           std::vector<uint16_t>& bf16_out, std::vector<float>& cnorm, std::vector<double>& mean,
                           double& cmax);

@@ -6,7 +6,8 @@
 // K cells matter, so this path first bounds every distance cheaply and then evaluates the
 // reference's exact arithmetic only where the bound cannot decide:
 //
-//   1. approx[q][c] = |c'|^2 - 2 <q', c'> on the tensor cores (bf16 inputs, fp32 accumulate), with
+//   1. approx[q][c] = |c'|^2 - 2 <q', c'> on the 5th-generation tensor cores (tcgen05.mma kind::f16: bf16 inputs, fp32
+//      accumulators in tensor memory; operands arrive as pre-tiled images through TMA bulk copies), with
 //      q' = q - mean, c' = c - mean (mean of the centroids; a translation leaves distances alone
 //      and makes the rounding errors relative to the spread of the data, not its offset).
 //   2. With D the real squared distance, D_ref the reference's fp32 value, A = approx + |q'|^2 and
@@ -30,6 +31,7 @@
 //      ties, non-finite input) is flagged and redone by the exact kernels.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
@@ -40,21 +42,32 @@ static constexpr uint32_t TC_CAND = 2048;
 
 // ---------------------------------------------------------------- query preparation --
 
-// One warp per query: q' = q - mean in double, bf16 image (zero padded to dpad), eps2 = 2 eps.
+// Operand images.  The MMA reads its operands from shared memory in the K-major no-swizzle canonical layout (core
+// matrices of 8 rows x 16 bytes); both operands are stored in GLOBAL memory already in that order, cut into slabs of
+// 128 K-elements, so that a tile slab is one contiguous block a single bulk copy brings in:
+//   image[tile][slab][kc = 16][row][8 elements],  rows = 128 (queries, A) or 256 (centroids, B), zero padded.
+static constexpr uint32_t PT_M = 128, PT_N = 256, PT_KS = 128; // tile rows (queries), tile columns (cells), K per slab
+__host__ __device__ inline size_t probe_image_index(uint32_t row, uint32_t k, uint32_t rows_per_tile, uint32_t nslab) {
+    const uint32_t tile = row / rows_per_tile, r = row % rows_per_tile, slab = k / PT_KS, kc = (k % PT_KS) / 8, e = k % 8;
+    return ((((size_t(tile) * nslab + slab) * 16 + kc) * rows_per_tile + r) * 8) + e;
+}
+
+// One warp per query row of the padded batch: q' = q - mean in double, bf16 image (zero padded), eps2 = 2 eps.
 __global__ void probe_prep_queries_kernel(const float* __restrict__ queries, const double* __restrict__ mean,
-                                          uint32_t dims, uint32_t dpad, uint32_t nq, double cmax,
+                                          uint32_t dims, uint32_t dpad, uint32_t nq, uint32_t nq_pad, double cmax,
                                           __nv_bfloat16* __restrict__ qb, double* __restrict__ eps2) {
     const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (q >= nq) return;
+    if (q >= nq_pad) return;
+    const uint32_t nslab = (dpad + PT_KS - 1) / PT_KS;
     double s = 0.0;
-    for (uint32_t j = lane; j < dpad; j += 32) {
+    for (uint32_t j = lane; j < nslab * PT_KS; j += 32) {
         double v = 0.0;
-        if (j < dims) v = double(queries[size_t(q) * dims + j]) - mean[j];
-        qb[size_t(q) * dpad + j] = __float2bfloat16_rn(float(v));
+        if (j < dims && q < nq) v = double(queries[size_t(q) * dims + j]) - mean[j];
+        qb[probe_image_index(q, j, PT_M, nslab)] = __float2bfloat16_rn(float(v));
         s += v * v;
     }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
+    if (lane == 0 && q < nq) {
         const double r = sqrt(s) * (1.0 + 1e-9) + cmax;
         eps2[q] = 2.0 * (r * r) * (1.0 / 128.0) * (1.0 + 1e-9); // 2 eps, eps = 2^-7 r^2; non-finite input -> inf/NaN -> flagged below
     }
@@ -62,90 +75,172 @@ __global__ void probe_prep_queries_kernel(const float* __restrict__ queries, con
 
 // ---------------------------------------------------------------- approximate distances --
 
-// C[q][c] = cn[c] - 2 * sum_k A[q][k] B[c][k];  A = queries (bf16, [nq][dpad]), B = centroids (bf16, [K][dpad]).
-// 256 threads = 8 warps as 4 (rows) x 2 (cols); CTA tile 128 x 128, k chunks of 64 through shared memory;
-// mma.sync.m16n8k16 bf16 -> fp32 (warp tile 32 x 64: 2 x 8 fragments).
-static constexpr int GM = 128, GN = 128, GK = 64, GPITCH = GK + 8;
+// out[q][c] = cn[c] - 2 * sum_k A[q][k] B[c][k] on tcgen05: CTA tile 128 queries x 256 cells, K in slabs of 128.
+//   warp 0   producer: one bulk copy per operand slab (A 32 KB, B 64 KB) into a 2-stage ring (UBLKCP + mbarrier)
+//   warp 1   MMA issuer (one elected lane): 8 x tcgen05.mma kind::f16 (M 128, N 256, K 16) per slab into one of two
+//            256-column fp32 accumulators in tensor memory; tcgen05.commit frees the stage / publishes the tile
+//   warps 2-9 epilogue (two per TMEM lane quadrant, 128 cells each): tcgen05.ld (thread = query row, 32 cells at a time),
+//            cn[c] - 2 acc, eight 16-byte stores = the row's 128 contiguous bytes (a shared-memory transpose so that a
+//            whole warp store is one row measured 1.4x slower than the mma.sync kernel it replaced: too few stores in flight)
+// Work items are (query tile, group of 8 cell tiles), walked persistently by gridDim.x CTAs.
+static constexpr uint32_t PT_THREADS = 320, PT_A_BYTES = 16 * PT_M * 16, PT_B_BYTES = 16 * PT_N * 16, PT_NGROUP = 8;
+static constexpr uint32_t PT_SMEM = 2 * (PT_A_BYTES + PT_B_BYTES);
 
-__device__ __forceinline__ void ldmatrix_x4(uint32_t (&r)[4], const void* p) {
-    const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+__device__ __forceinline__ uint32_t pt_smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void pt_mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(pt_smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+__device__ __forceinline__ void pt_mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done) : "r"(pt_smem_u32(bar)), "r"(parity) : "memory");
+    } while (!done);
 }
+__device__ __forceinline__ uint64_t pt_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) { // K-major, no swizzle, version 1
+    return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) | (uint64_t((sbo >> 4) & 0x3FFFu) << 32) |
+           (uint64_t(1) << 46);
+}
+// instruction descriptor: fp32 accumulate (1 << 4), A = B = bf16 (1 << 7, 1 << 10), K-major, N >> 3 at bit 17, M >> 4 at bit 24
+static constexpr uint32_t PT_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((PT_N >> 3) << 17) | ((PT_M >> 4) << 24);
 
-__global__ void __launch_bounds__(256)
-probe_approx_gemm_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat16* __restrict__ B,
+__global__ void __launch_bounds__(PT_THREADS, 1)
+probe_approx_umma_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat16* __restrict__ B,
                          const float* __restrict__ cn, uint32_t nq, uint32_t k_cells, uint32_t dpad,
                          float* __restrict__ out) {
-    __shared__ __align__(16) __nv_bfloat16 sa[GM * GPITCH];
-    __shared__ __align__(16) __nv_bfloat16 sb[GN * GPITCH];
+    extern __shared__ __align__(1024) char psm[];
+    __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_dfull[2], s_dempty[2];
+    __shared__ uint32_t s_tmem;
+    char* sA = psm;                                   // [2][PT_A_BYTES]
+    char* sB = psm + 2 * PT_A_BYTES;                  // [2][PT_B_BYTES]
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t wm = warp >> 1, wn = warp & 1;
-    const uint32_t row0 = blockIdx.y * GM, col0 = blockIdx.x * GN;
-    float acc[2][8][4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) acc[i][j][k] = 0.0f;
-    for (uint32_t k0 = 0; k0 < dpad; k0 += GK) {
-        // 128 rows x 64 bf16 = 128 x 8 uint4 per operand; 256 threads x 4 each
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-            const uint32_t u = tid + it * 256, r = u >> 3, cseg = u & 7;
-            uint4 va = make_uint4(0, 0, 0, 0), vb = make_uint4(0, 0, 0, 0);
-            if (k0 + cseg * 8 < dpad) {
-                if (row0 + r < nq) va = *reinterpret_cast<const uint4*>(A + size_t(row0 + r) * dpad + k0 + cseg * 8);
-                if (col0 + r < k_cells) vb = *reinterpret_cast<const uint4*>(B + size_t(col0 + r) * dpad + k0 + cseg * 8);
-            }
-            *reinterpret_cast<uint4*>(sa + r * GPITCH + cseg * 8) = va;
-            *reinterpret_cast<uint4*>(sb + r * GPITCH + cseg * 8) = vb;
+    const uint32_t nslab = (dpad + PT_KS - 1) / PT_KS;
+    const uint32_t mtiles = (nq + PT_M - 1) / PT_M, ntiles = (k_cells + PT_N - 1) / PT_N;
+    const uint32_t ngroups = (ntiles + PT_NGROUP - 1) / PT_NGROUP, n_items = mtiles * ngroups;
+    if (tid == 0) {
+        for (int i = 0; i < 2; ++i) {
+            pt_mbar_init(&s_full[i], 1);
+            pt_mbar_init(&s_empty[i], 1);
+            pt_mbar_init(&s_dfull[i], 1);
+            pt_mbar_init(&s_dempty[i], 8);
         }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < GK; kk += 16) {
-            uint32_t af[2][4];
-#pragma unroll
-            for (int i = 0; i < 2; ++i) // A fragment: 16 x 16 at rows wm*32 + i*16
-                ldmatrix_x4(af[i], sa + (wm * 32 + i * 16 + (lane & 15)) * GPITCH + kk + (lane >> 4) * 8);
-#pragma unroll
-            for (int jp = 0; jp < 4; ++jp) { // two 8-column B fragments per ldmatrix.x4
-                uint32_t bf[4];
-                const uint32_t n = wn * 64 + jp * 16 + (lane & 7) + ((lane >> 4) << 3);
-                ldmatrix_x4(bf, sb + n * GPITCH + kk + ((lane >> 3) & 1) * 8);
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    mma_bf16(acc[i][2 * jp + 0], af[i], bf[0], bf[1]);
-                    mma_bf16(acc[i][2 * jp + 1], af[i], bf[2], bf[3]);
-                }
-            }
-        }
-        __syncthreads();
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint32_t c = col0 + wn * 64 + j * 8 + (lane & 3) * 2;
-            const uint32_t r = row0 + wm * 32 + i * 16 + (lane >> 2);
-            if (c < k_cells) { // K is even or the last column is dropped below
-                const float n0 = cn[c], n1 = c + 1 < k_cells ? cn[c + 1] : 0.0f;
-                if (r < nq) {
-                    out[size_t(r) * k_cells + c] = n0 - 2.0f * acc[i][j][0];
-                    if (c + 1 < k_cells) out[size_t(r) * k_cells + c + 1] = n1 - 2.0f * acc[i][j][1];
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(pt_smem_u32(&s_tmem)), "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+
+    if (warp == 0) {
+        // ---- producer
+        uint32_t it = 0;
+        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+            const uint32_t mt = item / ngroups, g = item % ngroups;
+            for (uint32_t nt = g * PT_NGROUP; nt < min(ntiles, (g + 1) * PT_NGROUP); ++nt)
+                for (uint32_t sl = 0; sl < nslab; ++sl, ++it) {
+                    const uint32_t st = it & 1u;
+                    pt_mbar_wait(&s_empty[st], ((it >> 1) & 1u) ^ 1u);
+                    if (lane == 0) {
+                        const uint32_t bar = pt_smem_u32(&s_full[st]);
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(PT_A_BYTES + PT_B_BYTES) : "memory");
+                        const char* srcA = reinterpret_cast<const char*>(A) + (size_t(mt) * nslab + sl) * PT_A_BYTES;
+                        const char* srcB = reinterpret_cast<const char*>(B) + (size_t(nt) * nslab + sl) * PT_B_BYTES;
+                        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                         pt_smem_u32(sA + st * PT_A_BYTES)), "l"(srcA), "r"(PT_A_BYTES), "r"(bar) : "memory");
+                        for (uint32_t off = 0; off < PT_B_BYTES; off += 32768u)
+                            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                             pt_smem_u32(sB + st * PT_B_BYTES + off)), "l"(srcB + off), "r"(32768u), "r"(bar) : "memory");
+                    }
+                    __syncwarp();
                 }
-                if (r + 8 < nq) {
-                    out[size_t(r + 8) * k_cells + c] = n0 - 2.0f * acc[i][j][2];
-                    if (c + 1 < k_cells) out[size_t(r + 8) * k_cells + c + 1] = n1 - 2.0f * acc[i][j][3];
+        }
+    } else if (warp == 1) {
+        // ---- MMA issuer
+        uint32_t it = 0, tile = 0;
+        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+            const uint32_t g = item % ngroups;
+            for (uint32_t nt = g * PT_NGROUP; nt < min(ntiles, (g + 1) * PT_NGROUP); ++nt, ++tile) {
+                const uint32_t buf = tile & 1u;
+                pt_mbar_wait(&s_dempty[buf], ((tile >> 1) & 1u) ^ 1u);
+                for (uint32_t sl = 0; sl < nslab; ++sl, ++it) {
+                    const uint32_t st = it & 1u;
+                    pt_mbar_wait(&s_full[st], (it >> 1) & 1u);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    if (lane == 0) {
+                        const uint32_t ksteps = min(PT_KS, dpad - sl * PT_KS) / 16;
+                        const uint32_t a0 = pt_smem_u32(sA + st * PT_A_BYTES), b0 = pt_smem_u32(sB + st * PT_B_BYTES);
+                        for (uint32_t ks = 0; ks < ksteps; ++ks) {
+                            const uint64_t da = pt_desc(a0 + ks * 2 * (PT_M * 16), PT_M * 16, 128);
+                            const uint64_t db = pt_desc(b0 + ks * 2 * (PT_N * 16), PT_N * 16, 128);
+                            const uint32_t acc = (sl | ks) != 0u;
+                            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                                         ::"r"(tmem + buf * PT_N), "l"(da), "l"(db), "r"(PT_IDESC), "r"(acc) : "memory");
+                        }
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(pt_smem_u32(&s_empty[st])) : "memory");
+                        if (sl + 1 == nslab)
+                            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(pt_smem_u32(&s_dfull[buf])) : "memory");
+                    }
+                    __syncwarp();
                 }
             }
         }
+    } else {
+        // ---- epilogue (warps 2..9: TMEM lane quadrant = warp & 3, column half = (warp - 2) / 4)
+        const uint32_t quad = warp & 3u, chalf = (warp - 2) >> 2;
+        const bool vec_ok = (k_cells & 3u) == 0;
+        uint32_t tile = 0;
+        for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+            const uint32_t mt = item / ngroups, g = item % ngroups;
+            for (uint32_t nt = g * PT_NGROUP; nt < min(ntiles, (g + 1) * PT_NGROUP); ++nt, ++tile) {
+                const uint32_t buf = tile & 1u;
+                pt_mbar_wait(&s_dfull[buf], (tile >> 1) & 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t q = mt * PT_M + quad * 32 + lane;
+                for (uint32_t c0 = chalf * (PT_N / 2); c0 < (chalf + 1) * (PT_N / 2); c0 += 32) {
+                    uint32_t v[32];
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+                          "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+                          "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+                          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                        : "r"(tmem + buf * PT_N + ((quad * 32u) << 16) + c0));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    const uint32_t c = nt * PT_N + c0; // first of this thread's 32 consecutive cells
+                    if (q < nq) {
+                        float* dst = out + size_t(q) * k_cells + c;
+                        if (vec_ok && c + 32 <= k_cells) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) {
+                                const float4 n4 = *reinterpret_cast<const float4*>(cn + c + j); // same address in every lane
+                                float4 o;
+                                o.x = n4.x - 2.0f * __uint_as_float(v[j]);
+                                o.y = n4.y - 2.0f * __uint_as_float(v[j + 1]);
+                                o.z = n4.z - 2.0f * __uint_as_float(v[j + 2]);
+                                o.w = n4.w - 2.0f * __uint_as_float(v[j + 3]);
+                                *reinterpret_cast<float4*>(dst + j) = o;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (c + j < k_cells) dst[j] = cn[c + j] - 2.0f * __uint_as_float(v[j]);
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(pt_smem_u32(&s_dempty[buf])) : "memory");
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
 // ---------------------------------------------------------------- candidates -> exact order --
@@ -251,7 +346,12 @@ bool ivf_probe_tc_supported(uint32_t dims, uint32_t k_cells, uint32_t a) {
     return a >= 1 && a <= 256 && k_cells >= 512 && a * 4 <= k_cells && dims <= 2048;
 }
 
-// d_coarse_bf16 [K][dpad], d_cnorm [K], d_mean [dims] come from ivf_probe_tc_prepare (host, at open).
+// d_coarse_bf16 (tiled image), d_cnorm [K], d_mean [dims] come from ivf_probe_tc_prepare (host, at open).
+size_t ivf_probe_tc_query_image_elems(uint32_t nq, uint32_t dpad) {
+    const uint32_t nslab = (dpad + PT_KS - 1) / PT_KS;
+    return size_t((nq + PT_M - 1) / PT_M) * nslab * 16 * PT_M * 8;
+}
+
 void launch_ivf_probe_tc(const float* d_queries, const float* d_coarse, const uint16_t* d_coarse_bits,
                          const float* d_cnorm, const double* d_mean, double cmax, uint32_t dims, uint32_t dpad,
                          uint32_t k_cells, uint32_t nq, uint32_t a, uint16_t* d_q_bits, double* d_eps2,
@@ -259,10 +359,17 @@ void launch_ivf_probe_tc(const float* d_queries, const float* d_coarse, const ui
     const __nv_bfloat16* d_coarse_bf16 = reinterpret_cast<const __nv_bfloat16*>(d_coarse_bits);
     __nv_bfloat16* d_qb = reinterpret_cast<__nv_bfloat16*>(d_q_bits);
     QADC_CUDA_CHECK(cudaMemsetAsync(d_redo, 0, (2 * size_t(nq) + 1) * 4, stream)); // flags | list | count
-    probe_prep_queries_kernel<<<(nq * 32 + 255) / 256, 256, 0, stream>>>(d_queries, d_mean, dims, dpad, nq, cmax, d_qb,
-                                                                        d_eps2);
-    const dim3 grid((k_cells + GN - 1) / GN, (nq + GM - 1) / GM);
-    probe_approx_gemm_kernel<<<grid, 256, 0, stream>>>(d_qb, d_coarse_bf16, d_cnorm, nq, k_cells, dpad, d_approx);
+    const uint32_t nq_pad = (nq + PT_M - 1) / PT_M * PT_M;
+    probe_prep_queries_kernel<<<(nq_pad * 32 + 255) / 256, 256, 0, stream>>>(d_queries, d_mean, dims, dpad, nq, nq_pad, cmax,
+                                                                            d_qb, d_eps2);
+    int dev = 0, sms = 0;
+    QADC_CUDA_CHECK(cudaGetDevice(&dev));
+    QADC_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const uint32_t mtiles = nq_pad / PT_M, ntiles = (k_cells + PT_N - 1) / PT_N;
+    const uint32_t n_items = mtiles * ((ntiles + PT_NGROUP - 1) / PT_NGROUP);
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(probe_approx_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(PT_SMEM)));
+    probe_approx_umma_kernel<<<std::min<uint32_t>(uint32_t(sms), n_items), PT_THREADS, PT_SMEM, stream>>>(
+        d_qb, d_coarse_bf16, d_cnorm, nq, k_cells, dpad, d_approx);
     probe_select_tc_kernel<<<nq, 256, size_t(dims) * 4, stream>>>(d_approx, d_eps2, d_queries, d_coarse, dims, k_cells, a,
                                                                  d_order, d_redo);
     g_launches += 3;
@@ -281,7 +388,8 @@ bool ivf_probe_tc_prepare(const float* coarse, uint32_t k_cells, uint32_t dims, 
         mean[j] /= double(std::max<uint32_t>(k_cells, 1));
         if (!(mean[j] - mean[j] == 0.0)) return false;
     }
-    bf16_out.assign(size_t(k_cells) * dpad, 0);
+    const uint32_t nslab = (dpad + PT_KS - 1) / PT_KS;
+    bf16_out.assign(size_t((k_cells + PT_N - 1) / PT_N) * nslab * 16 * PT_N * 8, 0); // tiled operand image, zero padded
     cnorm.assign(k_cells, 0.0f);
     cmax = 0.0;
     for (uint32_t c = 0; c < k_cells; ++c) {
@@ -293,7 +401,7 @@ bool ivf_probe_tc_prepare(const float* coarse, uint32_t k_cells, uint32_t dims, 
             uint32_t bits;
             std::memcpy(&bits, &f, 4);
             bits += 0x7FFFu + ((bits >> 16) & 1u); // round to nearest even (finite inputs)
-            bf16_out[size_t(c) * dpad + j] = uint16_t(bits >> 16);
+            bf16_out[probe_image_index(c, j, PT_N, nslab)] = uint16_t(bits >> 16);
         }
         if (!(s - s == 0.0)) return false;
         cnorm[c] = float(s);
