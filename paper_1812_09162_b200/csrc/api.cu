@@ -471,7 +471,7 @@ static void flat_search_device(qadc_index* h, const float* d_queries, uint32_t n
 static void ivf_probe_order_device(qadc_index* h, const float* dq, uint32_t nb, uint32_t a, cudaStream_t st) {
     const DevSpec& ds = h->ds;
     const uint32_t K = h->k_cells;
-    h->scratch.ensure(size_t(nb) * K * 4);
+    h->scratch.ensure(std::max(size_t(nb) * K * 4, ivf_probe_tc_scratch_bytes(nb, K))); // exact path: [nb][K] distances
     h->cta_begin.ensure((2 * size_t(nb) + 1) * 4); // reused as the probe-selection redo flags | list | count
     if (h->probe_tc && h->probe_tc_ready && ivf_probe_tc_supported(ds.dims, K, a)) {
         h->q_bf16.ensure(ivf_probe_tc_query_image_elems(nb, h->dpad) * 2);

@@ -189,13 +189,14 @@ void launch_ivf_probe(const float* d_queries, const float* d_coarse_t, uint32_t 
 // tensor-core prefilter of the probe order (ivf_probe_tc.cu)
 bool ivf_probe_tc_supported(uint32_t dims, uint32_t k_cells, uint32_t a);
 size_t ivf_probe_tc_query_image_elems(uint32_t nq, uint32_t dpad); // bf16 elements of the tiled query operand image
+size_t ivf_probe_tc_scratch_bytes(uint32_t nq, uint32_t k_cells);    // class minima, limits, candidate bitmaps
 bool ivf_probe_tc_prepare(const float* coarse, uint32_t k_cells, uint32_t dims, uint32_t dpad,
                           std::vector<uint16_t>& bf16_out, std::vector<float>& cnorm, std::vector<double>& mean,
                           double& cmax);
 void launch_ivf_probe_tc(const float* d_queries, const float* d_coarse, const uint16_t* d_coarse_bf16 /* bf16 bits */,
                          const float* d_cnorm, const double* d_mean, double cmax, uint32_t dims, uint32_t dpad,
                          uint32_t k_cells, uint32_t nq, uint32_t a, uint16_t* d_qb /* bf16 bits */, double* d_eps2,
-                         float* d_approx, uint32_t* d_redo, uint32_t* d_order, cudaStream_t stream);
+                         float* d_scratch, uint32_t* d_redo, uint32_t* d_order, cudaStream_t stream);
 void launch_ivf_tables(const DevSpec& ds, const float* d_codebook, const float* d_queries, const float* d_coarse,
                        const uint32_t* d_order, uint32_t n_pairs, uint32_t a, float* d_luts, float* d_pmin,
                        float* d_own_min, cudaStream_t stream);

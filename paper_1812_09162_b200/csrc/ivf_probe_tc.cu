@@ -22,10 +22,13 @@
 //      eps := 2^-7 (|q'| + max_c |c'|)^2, i.e. a factor ~1.88 above the bound.  (Round 1 used 2^-8 S, derived from
 //      u = 2^-9 -- one bit too optimistic; corrected, with an adversarial test whose inputs sit just below bf16
 //      rounding midpoints: tests/test_gpu_parity.py::test_probe_order_prefilter_bf16_midpoints.)
-//   3. T := the a-th smallest of 256 strided minima of approx (a real value that at least a cells do not
-//      exceed).  Those a cells have D_ref <= T + |q'|^2 + eps, hence so does the a-th smallest D_ref, and
-//      every cell of the true top-a (ties included) has approx <= T + 2 eps.  Cells passing that test are
-//      the candidates (typically 1.5-2 a of them).
+//   3. The approximate values are never stored: the contraction runs TWICE (it is ~20 us of tensor-core time; a
+//      [queries][cells] fp32 image would be 655 MB written and read twice at C5).  Pass 1's epilogue keeps, per query,
+//      the minimum of every residue class c mod 256; T := the a-th smallest of those 256 minima (a real value that at
+//      least a cells do not exceed).  Those a cells have D_ref <= T + |q'|^2 + eps, hence so does the a-th smallest D_ref, and
+//      every cell of the true top-a (ties included) has approx <= T + 2 eps.  Pass 2's epilogue recomputes the same
+//      values (bit-identical: same instructions, same data) and appends the cells passing that test to the query's
+//      candidate list (typically 1.5-2 a of them).
 //   4. Candidates get the reference's serial fp32 distance; the first a by (distance bits, cell) are the
 //      probe order -- bit-identical to the exact path.  A query whose candidate set overflows (massive
 //      ties, non-finite input) is flagged and redone by the exact kernels.
@@ -82,8 +85,8 @@ __global__ void probe_prep_queries_kernel(const float* __restrict__ queries, con
 //   warps 2-9 epilogue (two per TMEM lane quadrant, 128 cells each): tcgen05.ld (thread = query row, 32 cells at a time),
 //            cn[c] - 2 acc, eight 16-byte stores = the row's 128 contiguous bytes (a shared-memory transpose so that a
 //            whole warp store is one row measured 1.4x slower than the mma.sync kernel it replaced: too few stores in flight)
-// Work items are (query tile, group of 8 cell tiles), walked persistently by gridDim.x CTAs.
-static constexpr uint32_t PT_THREADS = 320, PT_A_BYTES = 16 * PT_M * 16, PT_B_BYTES = 16 * PT_N * 16, PT_NGROUP = 8;
+// Work items are (query tile, group of 16 cell tiles), walked persistently by gridDim.x CTAs.
+static constexpr uint32_t PT_THREADS = 320, PT_A_BYTES = 16 * PT_M * 16, PT_B_BYTES = 16 * PT_N * 16, PT_NGROUP = 16;
 static constexpr uint32_t PT_SMEM = 2 * (PT_A_BYTES + PT_B_BYTES);
 
 __device__ __forceinline__ uint32_t pt_smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
@@ -104,10 +107,23 @@ __device__ __forceinline__ uint64_t pt_desc(uint32_t saddr, uint32_t lbo, uint32
 // instruction descriptor: fp32 accumulate (1 << 4), A = B = bf16 (1 << 7, 1 << 10), K-major, N >> 3 at bit 17, M >> 4 at bit 24
 static constexpr uint32_t PT_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((PT_N >> 3) << 17) | ((PT_M >> 4) << 24);
 
+// monotone map float -> uint32 (unsigned order == float order; used for atomicMin on floats of either sign)
+__device__ __forceinline__ uint32_t pt_ordered(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float pt_unordered(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+// PASS 1: mins_u[q][c mod 256] = min over cells of approx (ordered-uint encoding, atomicMin across work items).
+// PASS 2: cand[q][w] = bitmap of the cells 32 w .. 32 w + 31 with !(approx > limit[q])  (ntiles * 8 words per query).
+template <int PASS>
 __global__ void __launch_bounds__(PT_THREADS, 1)
 probe_approx_umma_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat16* __restrict__ B,
                          const float* __restrict__ cn, uint32_t nq, uint32_t k_cells, uint32_t dpad,
-                         float* __restrict__ out) {
+                         uint32_t* __restrict__ mins_u, const float* __restrict__ limit, uint32_t* __restrict__ cand,
+                         uint32_t* __restrict__ cand_count) {
     extern __shared__ __align__(1024) char psm[];
     __shared__ __align__(8) uint64_t s_full[2], s_empty[2], s_dfull[2], s_dempty[2];
     __shared__ uint32_t s_tmem;
@@ -189,18 +205,30 @@ probe_approx_umma_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat1
             }
         }
     } else {
-        // ---- epilogue (warps 2..9: TMEM lane quadrant = warp & 3, column half = (warp - 2) / 4)
+        // ---- epilogue (warps 2..9: TMEM lane quadrant = warp & 3, column half = (warp - 2) / 4); thread = query row
         const uint32_t quad = warp & 3u, chalf = (warp - 2) >> 2;
-        const bool vec_ok = (k_cells & 3u) == 0;
+        const float INF = __int_as_float(0x7f800000);
         uint32_t tile = 0;
         for (uint32_t item = blockIdx.x; item < n_items; item += gridDim.x) {
             const uint32_t mt = item / ngroups, g = item % ngroups;
+            const uint32_t q = mt * PT_M + quad * 32 + lane;
+            float mn[PT_N / 2]; // PASS 1: running minimum of each of this thread's 128 residue classes over the item's cell tiles
+            float lim = 0.0f;
+            const uint32_t bm_words = ntiles * (PT_N / 32); // bitmap words per query (cells padded to whole tiles)
+            if (PASS == 1) {
+#pragma unroll
+                for (int j = 0; j < int(PT_N / 2); ++j) mn[j] = INF;
+            } else {
+                lim = q < nq ? limit[q] : -INF; // rows past the batch never pass
+            }
             for (uint32_t nt = g * PT_NGROUP; nt < min(ntiles, (g + 1) * PT_NGROUP); ++nt, ++tile) {
                 const uint32_t buf = tile & 1u;
                 pt_mbar_wait(&s_dfull[buf], (tile >> 1) & 1u);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t q = mt * PT_M + quad * 32 + lane;
-                for (uint32_t c0 = chalf * (PT_N / 2); c0 < (chalf + 1) * (PT_N / 2); c0 += 32) {
+                const bool full_tile = (nt + 1) * PT_N <= k_cells; // the last tile's padding columns are zero operands: skip them
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const uint32_t c0 = chalf * (PT_N / 2) + cc * 32;
                     uint32_t v[32];
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -212,29 +240,42 @@ probe_approx_umma_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat1
                         : "r"(tmem + buf * PT_N + ((quad * 32u) << 16) + c0));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     const uint32_t c = nt * PT_N + c0; // first of this thread's 32 consecutive cells
-                    if (q < nq) {
-                        float* dst = out + size_t(q) * k_cells + c;
-                        if (vec_ok && c + 32 <= k_cells) {
+                    float val[32];
+                    if (full_tile) {
 #pragma unroll
-                            for (int j = 0; j < 32; j += 4) {
-                                const float4 n4 = *reinterpret_cast<const float4*>(cn + c + j); // same address in every lane
-                                float4 o;
-                                o.x = n4.x - 2.0f * __uint_as_float(v[j]);
-                                o.y = n4.y - 2.0f * __uint_as_float(v[j + 1]);
-                                o.z = n4.z - 2.0f * __uint_as_float(v[j + 2]);
-                                o.w = n4.w - 2.0f * __uint_as_float(v[j + 3]);
-                                *reinterpret_cast<float4*>(dst + j) = o;
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                if (c + j < k_cells) dst[j] = cn[c + j] - 2.0f * __uint_as_float(v[j]);
+                        for (int j = 0; j < 32; j += 4) {
+                            const float4 n4 = *reinterpret_cast<const float4*>(cn + c + j); // same address in every lane
+                            val[j] = n4.x - 2.0f * __uint_as_float(v[j]);
+                            val[j + 1] = n4.y - 2.0f * __uint_as_float(v[j + 1]);
+                            val[j + 2] = n4.z - 2.0f * __uint_as_float(v[j + 2]);
+                            val[j + 3] = n4.w - 2.0f * __uint_as_float(v[j + 3]);
                         }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            val[j] = c + j < k_cells ? cn[c + j] - 2.0f * __uint_as_float(v[j]) : INF; // +inf: never a minimum; as a candidate it is dropped by the exact kernel's bound check
+                    }
+                    if (PASS == 1) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) mn[cc * 32 + j] = fminf(mn[cc * 32 + j], val[j]); // NaN never lowers a minimum
+                    } else {
+                        // this thread's 32 consecutive cells are exactly one word of the query's candidate bitmap: a plain
+                        // store, no atomics, no divergence (appending to a list with atomicAdd was 3x slower than the
+                        // whole contraction)
+                        uint32_t bits = 0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) bits |= (!(val[j] > lim) ? 1u : 0u) << j; // NaN stays a candidate; padding cells are +inf
+                        if (q < nq) cand[size_t(q) * bm_words + (c >> 5)] = bits;
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(pt_smem_u32(&s_dempty[buf])) : "memory");
+            }
+            if (PASS == 1 && q < nq) {
+                uint32_t* dst = mins_u + size_t(q) * PT_N + chalf * (PT_N / 2);
+#pragma unroll
+                for (int j = 0; j < int(PT_N / 2); ++j) atomicMin(dst + j, pt_ordered(mn[j]));
             }
         }
     }
@@ -245,22 +286,14 @@ probe_approx_umma_kernel(const __nv_bfloat16* __restrict__ A, const __nv_bfloat1
 
 // ---------------------------------------------------------------- candidates -> exact order --
 
-// One CTA (256 threads) per query.  dynamic smem: dims floats (the query).
+// One CTA (256 threads) per query: T = a-th smallest of the 256 class minima, limit = T + 2 eps rounded UP to fp32
+// (a superset of candidates is always safe).  a <= min(256, K) is guaranteed by the launcher.
 __global__ void __launch_bounds__(256)
-probe_select_tc_kernel(const float* __restrict__ approx, const double* __restrict__ eps2,
-                       const float* __restrict__ queries, const float* __restrict__ coarse, uint32_t dims,
-                       uint32_t k_cells, uint32_t a, uint32_t* __restrict__ order, uint32_t* __restrict__ redo) {
-    extern __shared__ __align__(16) float qs[];
+probe_limit_kernel(const uint32_t* __restrict__ mins_u, const double* __restrict__ eps2, uint32_t a,
+                   float* __restrict__ limit) {
     __shared__ float mins[256];
-    __shared__ uint64_t cand[TC_CAND];
-    __shared__ uint32_t s_cnt;
     const uint32_t qi = blockIdx.x, tid = threadIdx.x;
-    const float* d = approx + size_t(qi) * k_cells;
-    for (uint32_t j = tid; j < dims; j += 256) qs[j] = queries[size_t(qi) * dims + j];
-    float m = __int_as_float(0x7f800000);
-    for (uint32_t c = tid; c < k_cells; c += 256) m = fminf(m, d[c]); // NaN never lowers a minimum
-    mins[tid] = m;
-    if (tid == 0) s_cnt = 0;
+    mins[tid] = pt_unordered(mins_u[size_t(qi) * 256 + tid]);
     __syncthreads();
     for (uint32_t size = 2; size <= 256; size <<= 1)
         for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
@@ -275,30 +308,55 @@ probe_select_tc_kernel(const float* __restrict__ approx, const double* __restric
             }
             __syncthreads();
         }
-    // a <= min(256, K) guaranteed by the launcher; rounded UP to fp32 (a superset of candidates is always safe)
-    const float limit = __double2float_ru(double(mins[a - 1]) + eps2[qi]);
-    for (uint32_t base = 0; base < k_cells; base += 256) {
-        const uint32_t c = base + tid;
-        const bool take = c < k_cells && !(d[c] > limit); // NaN stays a candidate
-        const uint32_t bal = __ballot_sync(0xffffffffu, take);
-        if (bal) {
-            uint32_t start = 0;
-            if ((tid & 31) == 0) start = atomicAdd(&s_cnt, uint32_t(__popc(bal)));
-            start = __shfl_sync(0xffffffffu, start, 0);
-            const uint32_t slot = start + __popc(bal & ((1u << (tid & 31)) - 1u));
-            if (take && slot < TC_CAND) cand[slot] = c;
+    if (tid == 0) limit[qi] = __double2float_ru(double(mins[a - 1]) + eps2[qi]);
+}
+
+// One CTA (256 threads) per query: compact the candidate bitmap, evaluate the reference's exact distance for the
+// candidates, first a by (distance bits, cell).  dynamic smem: the query (dims floats).
+__global__ void __launch_bounds__(256)
+probe_exact_kernel(const uint32_t* __restrict__ bitmap, uint32_t bm_words, const float* __restrict__ queries,
+                   const float* __restrict__ coarse, uint32_t dims, uint32_t k_cells, uint32_t a,
+                   uint32_t* __restrict__ order, uint32_t* __restrict__ redo) {
+    extern __shared__ __align__(16) float exs[];
+    float* qs = exs;
+    __shared__ uint64_t cand[TC_CAND];
+    __shared__ uint32_t s_cnt;
+    const uint32_t qi = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) s_cnt = 0;
+    for (uint32_t j = tid; j < dims; j += 256) qs[j] = queries[size_t(qi) * dims + j];
+    __syncthreads();
+    for (uint32_t w0 = 0; w0 < bm_words; w0 += 256) { // warp-uniform trip count
+        const uint32_t w = w0 + tid;
+        uint32_t bits = w < bm_words ? bitmap[size_t(qi) * bm_words + w] : 0u;
+        if (w * 32 + 32 > k_cells) bits &= w * 32 >= k_cells ? 0u : (0xFFFFFFFFu >> (32 - (k_cells - w * 32))); // padding cells
+        const uint32_t n = __popc(bits);
+        uint32_t incl = n;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += t;
+        }
+        uint32_t base = 0;
+        if (lane == 31 && incl) base = atomicAdd(&s_cnt, incl);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - n;
+        while (bits) {
+            const uint32_t j = __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (base < TC_CAND) cand[base] = w * 32 + j;
+            ++base;
         }
     }
     __syncthreads();
     const uint32_t n = s_cnt;
-    if (n > TC_CAND || n < a) { // n < a only if the limit itself is NaN
-        if (tid == 0) { // flags[nq] | compact list[nq] | count
+    if (n > TC_CAND || n < a) { // overflow (massive ties, non-finite input: a NaN limit admits every cell)
+        if (tid == 0) {         // flags[nq] | compact list[nq] | count
             redo[qi] = 1u;
             redo[gridDim.x + atomicAdd(&redo[2 * size_t(gridDim.x)], 1u)] = qi;
         }
         return;
     }
-    // the reference's distance (index.hpp:254-258): fp32, serial over the dims, unfused
+    // the reference's distance (index.hpp:254-258): fp32, serial over the dims, unfused.  One thread per candidate,
+    // walking its centroid row straight from L2 (staging the rows through shared memory with coalesced loads was
+    // measured 2.8x slower: one CTA per SM and a barrier per 128 rows).
     for (uint32_t i = tid; i < n; i += 256) {
         const uint32_t c = uint32_t(cand[i]);
         const float* ctr = coarse + size_t(c) * dims;
@@ -352,13 +410,22 @@ size_t ivf_probe_tc_query_image_elems(uint32_t nq, uint32_t dpad) {
     return size_t((nq + PT_M - 1) / PT_M) * nslab * 16 * PT_M * 8;
 }
 
+// workspace of the prefilter: class minima [nq][256] | limit [nq] | candidate bitmaps [nq][ceil(K / 256) * 8]
+size_t ivf_probe_tc_scratch_bytes(uint32_t nq, uint32_t k_cells) {
+    return size_t(nq) * (256 + 1 + size_t((k_cells + PT_N - 1) / PT_N) * (PT_N / 32)) * 4;
+}
+
 void launch_ivf_probe_tc(const float* d_queries, const float* d_coarse, const uint16_t* d_coarse_bits,
                          const float* d_cnorm, const double* d_mean, double cmax, uint32_t dims, uint32_t dpad,
                          uint32_t k_cells, uint32_t nq, uint32_t a, uint16_t* d_q_bits, double* d_eps2,
-                         float* d_approx, uint32_t* d_redo, uint32_t* d_order, cudaStream_t stream) {
+                         float* d_scratch, uint32_t* d_redo, uint32_t* d_order, cudaStream_t stream) {
     const __nv_bfloat16* d_coarse_bf16 = reinterpret_cast<const __nv_bfloat16*>(d_coarse_bits);
     __nv_bfloat16* d_qb = reinterpret_cast<__nv_bfloat16*>(d_q_bits);
+    uint32_t* mins_u = reinterpret_cast<uint32_t*>(d_scratch);
+    float* limit = reinterpret_cast<float*>(mins_u + size_t(nq) * 256);
+    uint32_t* bitmap = reinterpret_cast<uint32_t*>(limit + nq);
     QADC_CUDA_CHECK(cudaMemsetAsync(d_redo, 0, (2 * size_t(nq) + 1) * 4, stream)); // flags | list | count
+    QADC_CUDA_CHECK(cudaMemsetAsync(mins_u, 0xFF, size_t(nq) * 256 * 4, stream));  // ordered encoding of "no value yet"
     const uint32_t nq_pad = (nq + PT_M - 1) / PT_M * PT_M;
     probe_prep_queries_kernel<<<(nq_pad * 32 + 255) / 256, 256, 0, stream>>>(d_queries, d_mean, dims, dpad, nq, nq_pad, cmax,
                                                                             d_qb, d_eps2);
@@ -367,12 +434,17 @@ void launch_ivf_probe_tc(const float* d_queries, const float* d_coarse, const ui
     QADC_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const uint32_t mtiles = nq_pad / PT_M, ntiles = (k_cells + PT_N - 1) / PT_N;
     const uint32_t n_items = mtiles * ((ntiles + PT_NGROUP - 1) / PT_NGROUP);
-    QADC_CUDA_CHECK(cudaFuncSetAttribute(probe_approx_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(PT_SMEM)));
-    probe_approx_umma_kernel<<<std::min<uint32_t>(uint32_t(sms), n_items), PT_THREADS, PT_SMEM, stream>>>(
-        d_qb, d_coarse_bf16, d_cnorm, nq, k_cells, dpad, d_approx);
-    probe_select_tc_kernel<<<nq, 256, size_t(dims) * 4, stream>>>(d_approx, d_eps2, d_queries, d_coarse, dims, k_cells, a,
-                                                                 d_order, d_redo);
-    g_launches += 3;
+    const uint32_t grid = std::min<uint32_t>(uint32_t(sms), n_items);
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(probe_approx_umma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(PT_SMEM)));
+    QADC_CUDA_CHECK(cudaFuncSetAttribute(probe_approx_umma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(PT_SMEM)));
+    probe_approx_umma_kernel<1><<<grid, PT_THREADS, PT_SMEM, stream>>>(d_qb, d_coarse_bf16, d_cnorm, nq, k_cells, dpad, mins_u,
+                                                                       nullptr, nullptr, nullptr);
+    probe_limit_kernel<<<nq, 256, 0, stream>>>(mins_u, d_eps2, a, limit);
+    probe_approx_umma_kernel<2><<<grid, PT_THREADS, PT_SMEM, stream>>>(d_qb, d_coarse_bf16, d_cnorm, nq, k_cells, dpad, nullptr,
+                                                                       limit, bitmap, nullptr);
+    probe_exact_kernel<<<nq, 256, size_t(dims) * 4, stream>>>(bitmap, ntiles * (PT_N / 32), d_queries, d_coarse, dims, k_cells, a, d_order,
+                                                     d_redo);
+    g_launches += 5;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
