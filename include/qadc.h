@@ -223,6 +223,17 @@ int qadc_encode(const qadc_spec* spec, const float* codebook, const float* vecto
 int qadc_ivf_assign_encode(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
                            const float* vectors, uint64_t n, uint32_t* assign, uint8_t* codes, int device);
 
+/* The whole data-dependent half of IvfIndex::build on the GPU (index.hpp:195-227): assignment, residuals, encode AND
+ * the per-list grouping + packing (:219-227: every cell's members in ascending vector index, one PackedList per cell,
+ * ids = vector indices).  Outputs are exactly qadc_ivf_open's arguments: list_count / list_byte_off / list_id_off
+ * (k_cells each), ids (n), packed (caller buffer of packed_cap >= qadc_ivf_build_packed_bound(spec, n, k_cells) bytes;
+ * *packed_bytes = bytes written).  assign (optional, n u32) receives the cells. */
+uint64_t qadc_ivf_build_packed_bound(const qadc_spec* spec, uint64_t n, uint32_t k_cells);
+int qadc_ivf_build_lists(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
+                         const float* vectors, uint64_t n, uint64_t* list_count, uint64_t* list_byte_off,
+                         uint64_t* list_id_off, uint32_t* ids, uint8_t* packed, uint64_t packed_cap, uint64_t* packed_bytes,
+                         uint32_t* assign, int device);
+
 int qadc_get_stats(const qadc_index* h, qadc_stats* out);
 /* tuning knobs for experiments: name in {"cand_cap","seg0","seg_growth","force_variant","threads"} */
 int qadc_set_option(qadc_index* h, const char* name, int64_t value);

@@ -1234,6 +1234,81 @@ int qadc_ivf_assign_encode(const qadc_spec* spec, const float* codebook, const f
     });
 }
 
+uint64_t qadc_ivf_build_packed_bound(const qadc_spec* s, uint64_t n, uint32_t k_cells) {
+    const uint64_t block_bytes = uint64_t(s->groups) * s->block_len * (s->word_width / 8);
+    return (n / s->block_len + k_cells) * block_bytes; // every list wastes less than one block
+}
+
+int qadc_ivf_build_lists(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
+                         const float* vectors, uint64_t n, uint64_t* list_count, uint64_t* list_byte_off,
+                         uint64_t* list_id_off, uint32_t* ids, uint8_t* packed, uint64_t packed_cap, uint64_t* packed_bytes,
+                         uint32_t* assign, int device) {
+    return guarded([&] {
+        if (!spec || !codebook || !coarse || !list_count || !list_byte_off || !list_id_off || !packed_bytes ||
+            (n && (!vectors || !ids || !packed)))
+            throw Error(QADC_ERR_INPUT, "ivf build: null argument");
+        if (k_cells == 0) throw Error(QADC_ERR_INPUT, "ivf build: no coarse centroids");
+        if (n > 0xFFFFFFFFull) throw Error(QADC_ERR_INPUT, "ivf build: more than 2^32 - 1 vectors (ids are 32-bit)");
+        validate_spec(*spec);
+        if (packed_cap < qadc_ivf_build_packed_bound(spec, n, k_cells))
+            throw Error(QADC_ERR_INPUT, "ivf build: packed buffer smaller than qadc_ivf_build_packed_bound()");
+        set_device(device);
+        const DevSpec ds = make_dev_spec(*spec, spec->groups);
+        const uint32_t dims = spec->dims;
+        std::vector<float> ct(size_t(dims) * k_cells);
+        for (uint32_t c = 0; c < k_cells; ++c)
+            for (uint32_t j = 0; j < dims; ++j) ct[size_t(j) * k_cells + c] = coarse[size_t(c) * dims + j];
+        const uint64_t batch = std::min<uint64_t>(1u << 17, std::max<uint64_t>(n, 1));
+        DevBuf cb, co, cot, v, resid, scratch, asg, codes, counts, id_off, byte_off, totals, order, pk, status;
+        cb.ensure(size_t(spec->cb_floats) * 4);
+        co.ensure(ct.size() * 4);
+        cot.ensure(ct.size() * 4);
+        v.ensure(size_t(batch) * dims * 4);
+        resid.ensure(size_t(batch) * dims * 4);
+        scratch.ensure(ivf_assign_scratch_bytes(k_cells, batch));
+        asg.ensure(std::max<size_t>(size_t(n) * 4, 16));
+        codes.ensure(std::max<size_t>(size_t(n) * spec->m, 16));
+        counts.ensure(size_t(k_cells) * 8);
+        id_off.ensure(size_t(k_cells) * 8);
+        byte_off.ensure(size_t(k_cells) * 8);
+        totals.ensure(16);
+        order.ensure(std::max<size_t>(size_t(n) * 4, 16));
+        pk.ensure(std::max<uint64_t>(packed_cap, 16));
+        status.ensure(4);
+        QADC_CUDA_CHECK(cudaMemset(status.p, 0, 4));
+        QADC_CUDA_CHECK(cudaMemcpy(cb.p, codebook, size_t(spec->cb_floats) * 4, cudaMemcpyHostToDevice));
+        QADC_CUDA_CHECK(cudaMemcpy(co.p, coarse, ct.size() * 4, cudaMemcpyHostToDevice));
+        QADC_CUDA_CHECK(cudaMemcpy(cot.p, ct.data(), ct.size() * 4, cudaMemcpyHostToDevice));
+        for (uint64_t i = 0; i < n; i += batch) { // vectors stream through; assignments and codes stay on the device
+            const uint64_t nb = std::min(batch, n - i);
+            QADC_CUDA_CHECK(cudaMemcpy(v.p, vectors + i * dims, size_t(nb) * dims * 4, cudaMemcpyHostToDevice));
+            launch_ivf_assign(v.as<float>(), co.as<float>(), cot.as<float>(), dims, k_cells, nb, scratch.p,
+                              asg.as<uint32_t>() + i, resid.as<float>(), nullptr);
+            launch_encode(ds, cb.as<float>(), resid.as<float>(), nb, codes.as<uint8_t>() + i * spec->m, nullptr);
+        }
+        launch_ivf_group_pack(*spec, ds, asg.as<uint32_t>(), codes.as<uint8_t>(), n, k_cells,
+                              counts.as<unsigned long long>(), id_off.as<unsigned long long>(),
+                              byte_off.as<unsigned long long>(), totals.as<unsigned long long>(), order.as<uint32_t>(),
+                              pk.as<uint8_t>(), status.as<int>(), nullptr);
+        unsigned long long tot[2] = {0, 0};
+        int st = 0;
+        QADC_CUDA_CHECK(cudaMemcpy(tot, totals.p, 16, cudaMemcpyDeviceToHost));
+        QADC_CUDA_CHECK(cudaMemcpy(&st, status.p, 4, cudaMemcpyDeviceToHost));
+        if (st) throw Error(st, "ivf build: assignment out of range");
+        if (tot[0] != n || tot[1] > packed_cap) throw Error(QADC_ERR_CUDA, "ivf build: internal size mismatch");
+        static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
+        QADC_CUDA_CHECK(cudaMemcpy(list_count, counts.p, size_t(k_cells) * 8, cudaMemcpyDeviceToHost));
+        QADC_CUDA_CHECK(cudaMemcpy(list_id_off, id_off.p, size_t(k_cells) * 8, cudaMemcpyDeviceToHost));
+        QADC_CUDA_CHECK(cudaMemcpy(list_byte_off, byte_off.p, size_t(k_cells) * 8, cudaMemcpyDeviceToHost));
+        if (n) {
+            QADC_CUDA_CHECK(cudaMemcpy(ids, order.p, size_t(n) * 4, cudaMemcpyDeviceToHost));
+            QADC_CUDA_CHECK(cudaMemcpy(packed, pk.p, size_t(tot[1]), cudaMemcpyDeviceToHost));
+            if (assign) QADC_CUDA_CHECK(cudaMemcpy(assign, asg.p, size_t(n) * 4, cudaMemcpyDeviceToHost));
+        }
+        *packed_bytes = tot[1];
+    });
+}
+
 int qadc_get_stats(const qadc_index* h, qadc_stats* out) {
     if (!h || !out) return QADC_ERR_INPUT;
     *out = h->stats;

@@ -240,6 +240,10 @@ size_t ivf_assign_scratch_bytes(uint32_t k_cells, uint64_t n);
 void launch_ivf_assign(const float* d_vectors, const float* d_coarse, const float* d_coarse_t, uint32_t dims,
                        uint32_t k_cells, uint64_t n, void* d_scratch, uint32_t* d_assign, float* d_resid,
                        cudaStream_t stream);
+void launch_ivf_group_pack(const qadc_spec& spec, const DevSpec& ds, const uint32_t* d_assign, const uint8_t* d_codes, uint64_t n,
+                           uint32_t k_cells, unsigned long long* d_counts, unsigned long long* d_id_off,
+                           unsigned long long* d_byte_off, unsigned long long* d_totals, uint32_t* d_order, uint8_t* d_packed,
+                           int* d_status, cudaStream_t stream);
 void launch_encode(const DevSpec& ds, const float* d_codebook, const float* d_vectors, uint64_t n, uint8_t* d_codes,
                    cudaStream_t stream);
 

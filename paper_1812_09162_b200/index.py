@@ -378,24 +378,29 @@ def ivf_assign_encode(spec: QadcSpec, codebook, coarse, vectors, device: int = 0
 def build_ivf_lists(spec: QadcSpec, codebook, coarse, vectors, device: int = 0) -> dict:
     """IVF lists for `vectors` under trained `coarse` centroids and a residual `codebook`, laid out as
     IvfIndex::build does (index.hpp:219-227): each cell's members in ascending vector index, one PackedList per
-    cell, ids = vector indices.  Assignment and encode run on the GPU (ivf_assign_encode); the grouping and the
-    byte packing are host numpy.  The dict's keys are IvfIndex's constructor arguments."""
+    cell, ids = vector indices.  Everything runs on the GPU behind the C ABI (qadc_ivf_build_lists): assignment,
+    residuals, encode, a stable grouping by cell and the packing into the reference's transposed blocks.  The dict's
+    keys are IvfIndex's constructor arguments (+ ``assign``)."""
+    cb = _f32(codebook).reshape(-1)
     co = _f32(coarse).reshape(-1, spec.dims)
-    k_cells = co.shape[0]
-    assign, codes = ivf_assign_encode(spec, codebook, co, vectors, device)
-    order = np.argsort(assign, kind="stable").astype(np.uint32)
-    counts = np.bincount(assign, minlength=k_cells).astype(np.uint64)
-    id_off = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
-    parts, byte_off, b = [], np.zeros(k_cells, dtype=np.uint64), 0
-    for c in range(k_cells):
-        byte_off[c] = b
-        if counts[c]:
-            i0 = int(id_off[c])
-            parts.append(pack_list(spec, codes[order[i0:i0 + int(counts[c])]]))
-            b += parts[-1].size
-    packed = np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint8)
-    return dict(packed=packed, list_byte_off=byte_off, list_id_off=id_off, list_count=counts, ids=order,
-                assign=assign)
+    v = _f32(vectors).reshape(-1, spec.dims)
+    n, k_cells = v.shape[0], co.shape[0]
+    L = lib()
+    L.qadc_ivf_build_packed_bound.restype = C.c_uint64
+    cap = int(L.qadc_ivf_build_packed_bound(C.byref(spec), C.c_uint64(n), C.c_uint32(k_cells)))
+    counts = np.zeros(k_cells, dtype=np.uint64)
+    byte_off = np.zeros(k_cells, dtype=np.uint64)
+    id_off = np.zeros(k_cells, dtype=np.uint64)
+    ids = np.zeros(n, dtype=np.uint32)
+    assign = np.zeros(n, dtype=np.uint32)
+    packed = np.zeros(max(cap, 1), dtype=np.uint8)
+    nbytes = C.c_uint64(0)
+    check(L.qadc_ivf_build_lists(C.byref(spec), _p(cb, C.c_float), _p(co, C.c_float), C.c_uint32(k_cells),
+                                 _p(v, C.c_float), C.c_uint64(n), _p(counts, C.c_uint64), _p(byte_off, C.c_uint64),
+                                 _p(id_off, C.c_uint64), _p(ids, C.c_uint32), _p(packed, C.c_uint8), C.c_uint64(cap),
+                                 C.byref(nbytes), _p(assign, C.c_uint32), C.c_int(device)))
+    return dict(packed=packed[: nbytes.value].copy(), list_byte_off=byte_off, list_id_off=id_off, list_count=counts,
+                ids=ids, assign=assign)
 
 
 def merge_topk_device(d_keys, nshards: int, nq: int, r: int, d_map, d_ids, d_dists, d_counts, device: int,

@@ -646,6 +646,35 @@ def test_ivf_build_lists_match_reference_build(golden, name):
         assert np.array_equal(built[key], g[key]), key
 
 
+def test_ivf_build_lists_grouping_and_packing_many_cells():
+    """qadc_ivf_build_lists (device histogram + scans + stable grouping + pack kernel) against the host restatement of
+    index.hpp:219-227 on the same assignment: more cells than vectors in places (empty lists), ragged tails in every
+    block size / word width, ids ascending inside every list, offsets consistent with qadc_packed_bytes."""
+    rng = np.random.default_rng(33)
+    for dims, text, k, n in [(40, "10x{4,4}", 1000, 2500 + 7), (48, "6x{6,5,5}", 300, 20_011), (32, "4x{8}", 70, 5_000),
+                             (64, "8x{8,8}", 17, 33)]:
+        s = qb.allocate_dims(dims, text)
+        cb = rng.standard_normal(s.cb_floats).astype(np.float32)
+        coarse = (rng.standard_normal((k, dims)) * 3).astype(np.float32)
+        v = (rng.standard_normal((n, dims)) * 3).astype(np.float32)
+        built = qb.build_ivf_lists(s, cb, coarse, v)
+        assign, codes = qb.ivf_assign_encode(s, cb, coarse, v)
+        assert np.array_equal(built["assign"], assign)
+        order = np.argsort(assign, kind="stable").astype(np.uint32)
+        counts = np.bincount(assign, minlength=k).astype(np.uint64)
+        assert np.array_equal(built["list_count"], counts) and np.array_equal(built["ids"], order)
+        id_off = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
+        assert np.array_equal(built["list_id_off"], id_off)
+        b = 0
+        for c in range(k):
+            assert int(built["list_byte_off"][c]) == b
+            i0, cnt = int(id_off[c]), int(counts[c])
+            want = qb.pack_list(s, codes[order[i0:i0 + cnt]]) if cnt else np.zeros(0, np.uint8)
+            assert np.array_equal(built["packed"][b:b + want.size], want), (text, c)
+            b += qb.packed_bytes(s, cnt)
+        assert built["packed"].size == b
+
+
 def test_ivf_assign_encode_vs_oracle_many_cells(port):
     """More cells than one CTA covers (cross-block reduction), duplicated centroids (ties to the lowest cell),
     a ragged vector count, NaN / infinite inputs (never win: cell 0, like the reference's '<' loop)."""
