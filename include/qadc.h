@@ -25,7 +25,7 @@ extern "C" {
 
 #define QADC_MAX_SUBS 64
 #define QADC_MAX_GROUP 16
-#define QADC_MAX_R 1024 /* results per query supported by the device top-R stage */
+#define QADC_MAX_R 16384 /* results per query supported by the device top-R stage (round 1: 1024) */
 #define QADC_MAX_T 16384 /* longest calibration prefix t (the reference bounds neither; beyond these -> config error) */
 
 /* status classes: reference exception -> CLI exit code (errors.hpp, pqscan_cli.cpp:20-30) */

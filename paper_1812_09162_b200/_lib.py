@@ -18,7 +18,7 @@ HEADER = ROOT / "include" / "qadc.h"
 
 QADC_MAX_SUBS = 64
 QADC_MAX_GROUP = 16
-QADC_MAX_R = 1024
+QADC_MAX_R = 16384
 
 ERR_KINDS = {3: "invalid_spec", 4: "training", 5: "input", 6: "corruption", 7: "config", 8: "io", 9: "calibration",
              20: "cuda"}

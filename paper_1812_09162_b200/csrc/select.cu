@@ -92,6 +92,8 @@ tighten_kernel(uint64_t* __restrict__ top, uint32_t* __restrict__ ntop, uint32_t
 void launch_tighten(uint64_t* top, uint32_t* ntop, uint32_t kpad, uint64_t* cand, uint32_t* cand_count, uint32_t cap,
                     uint64_t* thr_key, uint32_t nq, uint32_t r, unsigned long long* admitted, cudaStream_t stream) {
     if (nq == 0) return;
+    if (size_t(r) * 8 > 48 * 1024) // R above 6144: opt in to the larger dynamic shared memory (QADC_MAX_R * 8 = 128 KB)
+        QADC_CUDA_CHECK(cudaFuncSetAttribute(tighten_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(r) * 8)));
     tighten_kernel<<<nq, TIGHTEN_THREADS, size_t(r) * 8, stream>>>(top, ntop, kpad, cand, cand_count, cap, thr_key, r,
                                                                    admitted);
     ++g_launches;

@@ -200,6 +200,40 @@ def test_flat_search_vs_oracle(port, dims, text):
                     assert np.array_equal(got.ids[qi, :c], ref2[0][qi, :c]) and bits_equal(got.dists[qi, :c], ref2[1][qi, :c])
 
 
+@pytest.mark.parametrize("dims,text,n,r,t", [(64, "16x{4,4}", 30_000, 1500, 2000), (48, "12x{6,5,5}", 20_000, 7000, 9000),
+                                            (64, "8x{8}", 9_000, 16384, 16384)])
+def test_large_r_and_t_vs_oracle(port, dims, text, n, r, t):
+    """R and t far above the paper's 100 / 400 (the reference bounds neither, index.hpp:27-31; the device top-R stage
+    goes to QADC_MAX_R = QADC_MAX_T = 16384): heaps that stay unfilled for most of the list, candidate-buffer retries,
+    R > N; flat and IVF."""
+    rng = np.random.default_rng(r)
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+    pk = qb.pack_list(s, random_codes(s, n, seed=r))
+    queries = (rng.standard_normal((6, dims)) * 2).astype(np.float32)
+    want = port.flat_search(so, cb, pk, n, queries, r=r, t=t, threads=6)
+    with qb.FlatIndex(s, cb, pk, n) as idx:
+        got = idx.search(queries, qb.SearchParams(r=r, t=t))
+        with pytest.raises(qb.QadcError) as e:
+            idx.search(queries, qb.SearchParams(r=16385, t=16385))
+        assert e.value.kind == "config"
+    assert np.array_equal(got.counts, want[2])
+    for qi in range(len(queries)):
+        c = int(want[2][qi])
+        assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]) and bits_equal(got.dists[qi, :c], want[1][qi, :c])
+    k_cells = 12
+    coarse = (rng.standard_normal((k_cells, dims)) * 3).astype(np.float32)
+    packed, boff, ioff, counts, ids = _ivf_lists(rng, s, k_cells, n)
+    rr, tt = min(r, 3000), min(t, 4000)
+    want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=5, r=rr, t=tt, threads=6)
+    with qb.IvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids) as idx:
+        got = idx.search(queries, qb.SearchParams(probes=5, r=rr, t=tt))
+    assert np.array_equal(got.counts, want[2])
+    for qi in range(len(queries)):
+        c = int(want[2][qi])
+        assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]) and bits_equal(got.dists[qi, :c], want[1][qi, :c])
+
+
 def test_search_errors_and_empty():
     s = qb.allocate_dims(64, "16x{4,4}")
     cb = np.zeros(s.cb_floats, np.float32)

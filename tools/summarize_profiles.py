@@ -18,6 +18,10 @@ KEYS = [
     "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
     "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__warps_eligible.avg.per_cycle_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg", "sm__pipe_tensor_subpipe_hmma_cycles_active_realtime.avg",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "smsp__sass_inst_executed_op_tmem_ldt.sum",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed", "sm__cycles_active.avg",
 ]
 
 
@@ -74,10 +78,14 @@ if __name__ == "__main__":
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     names = {"c1": "C1, 16x{4,4} N=1e6 Q=1e3", "c2": "C2, 12x{6,5,5} N=1e7 Q=1e4 (default bench)",
              "c3": "C3, 8x{8,8} N=1e7 Q=1e4", "c4": "C4, 16x{4,4} N=2e8 Q=1e4", "c5": "C5, IVF K=16384 nprobe=64"}
+    for rep in sorted(g.glob(f"{tag}_probe_*.ncu-rep")):
+        summarize_rep(rep, p / (rep.stem + "_summary.txt"),
+                      "ncu --set full --clock-control none --import-source on, the two probe_approx_umma_kernel launches "
+                      "(class minima, candidate bitmaps) of `python bench.py --workload c5g --warmup 3`")
     for rep in sorted(g.glob(f"{tag}_scan_*.ncu-rep")):
         w = rep.stem.split("_")[-1]
         summarize_rep(rep, p / (rep.stem + "_summary.txt"),
-                      f"ncu --set full --clock-control none --import-source on, one scan_kernel launch of "
+                      f"ncu --set full --clock-control none --import-source on, one scan launch of "
                       f"`python bench.py --workload {w} --warmup 3` ({names.get(w, w)})")
     for lc in sorted(g.glob(f"{tag}_launches_*.csv")):
         w = lc.stem.split("_")[-1]
