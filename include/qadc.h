@@ -234,6 +234,11 @@ int qadc_ivf_build_lists(const qadc_spec* spec, const float* codebook, const flo
                          uint64_t* list_id_off, uint32_t* ids, uint8_t* packed, uint64_t packed_cap, uint64_t* packed_bytes,
                          uint32_t* assign, int device);
 
+/* Guard-zone check of every device buffer (enabled by the environment variable QADC_DEBUG_CANARY; returns 1 when on):
+ * buffers verified so far and guard bytes found overwritten (must stay 0).  Stands in for compute-sanitizer memcheck,
+ * which the GPU pool refuses. */
+int qadc_debug_canary(uint64_t* buffers_checked, uint64_t* bytes_corrupted);
+
 int qadc_get_stats(const qadc_index* h, qadc_stats* out);
 /* tuning knobs for experiments: name in {"cand_cap","seg0","seg_growth","force_variant","threads"} */
 int qadc_set_option(qadc_index* h, const char* name, int64_t value);
