@@ -51,6 +51,10 @@ WORKLOADS = {
     "c4": dict(kind="flat", spec="16x{4,4}", dims=128, n=200_000_000, nq=10_000, data="random"),
     "c5": dict(kind="ivf", spec="12x{6,5,5}", dims=128, n=500_000_000, nq=10_000, data="random", k_cells=16384,
                probes=64),
+    # the paper's 128-bit configurations at the C2/C3 size, uniform random codes
+    "w44": dict(kind="flat", spec="32x{4,4}", dims=128, n=10_000_000, nq=10_000, data="random"),
+    "w655": dict(kind="flat", spec="24x{6,5,5}", dims=96, n=10_000_000, nq=10_000, data="random"),
+    "w88": dict(kind="flat", spec="16x{8,8}", dims=128, n=10_000_000, nq=10_000, data="random"),
     "c5g": dict(kind="ivf", spec="12x{6,5,5}", dims=128, n=62_500_000, nq=10_000, data="random", k_cells=16384,
                 probes=64),
 }

@@ -683,6 +683,11 @@ using G664 = GeomCT<16, 4, 6, 6, 4>;  // 12x{6,6,4}
 using G555 = GeomCT<16, 4, 5, 5, 5>;  // 12x{5,5,5}
 using G88 = GeomCT<16, 4, 8, 8>;      // 8x{8,8}
 using G8 = GeomCT<8, 8, 8>;           // 8x{8}
+// the paper's 128-bit configurations
+using G44W = GeomCT<8, 16, 4, 4>;     // 32x{4,4}
+using G655W = GeomCT<16, 8, 6, 5, 5>; // 24x{6,5,5}
+using G664W = GeomCT<16, 8, 6, 6, 4>; // 24x{6,6,4}
+using G88W = GeomCT<16, 8, 8, 8>;     // 16x{8,8}
 
 const char* variant_name(uint32_t v) {
     switch (v) {
@@ -866,7 +871,9 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         if (G88::matches(ds)) return launch_one<PolU16x1, G88>(plan, ds, args, grid, stream);
         if (G8::matches(ds)) return launch_one<PolU16x1, G8>(plan, ds, args, grid, stream);
         return launch_one<PolU16x1, GeomRT>(plan, ds, args, grid, stream);
-    case VAR_U8X1: return launch_one<PolU8x1, GeomRT>(plan, ds, args, grid, stream);
+    case VAR_U8X1:
+        if (G88W::matches(ds)) return launch_one<PolU8x1, G88W>(plan, ds, args, grid, stream);
+        return launch_one<PolU8x1, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H:
         if (G655::matches(ds)) return launch_one<PolF16x4H, G655>(plan, ds, args, grid, stream);
         if (G664::matches(ds)) return launch_one<PolF16x4H, G664>(plan, ds, args, grid, stream);
@@ -874,6 +881,8 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
         return launch_one<PolF16x4H, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C2:
         if (G655::matches(ds)) return launch_one<PolF16x4H_C2, G655>(plan, ds, args, grid, stream);
+        if (G655W::matches(ds)) return launch_one<PolF16x4H_C2, G655W>(plan, ds, args, grid, stream);
+        if (G664W::matches(ds)) return launch_one<PolF16x4H_C2, G664W>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4H_C2, GeomRT>(plan, ds, args, grid, stream);
     case VAR_F16X4H_C4:
         // irregular specs: word-pair interleaved lines (tile_pair_layout() makes the same choice), 8 rows per lane
@@ -900,6 +909,7 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
     case VAR_F16X4_C4M: return launch_one<PolF16x8_C8P, G8>(plan, ds, args, grid, stream); // the code bytes ARE 8x{8} indices
     case VAR_F16X4_C4:
         if (G8::matches(ds)) return launch_one<PolF16x8_C8P, G8>(plan, ds, args, grid, stream);
+        if (G44W::matches(ds)) return launch_one<PolF16x4_C4, G44W>(plan, ds, args, grid, stream);
         return launch_one<PolF16x4_C4, GeomRT>(plan, ds, args, grid, stream);
     default: throw Error(QADC_ERR_CONFIG, "scan: bad variant");
     }

@@ -168,7 +168,8 @@ def test_whole_vs_chunked_scan(port):
 
 
 SPECS = [(128, "16x{4,4}"), (96, "12x{6,5,5}"), (128, "8x{8,8}"), (128, "8x{8}"), (128, "12x{6,6,4}"),
-         (120, "12x{5,5,5}"), (128, "12x{6,5,5}"), (64, "32x{4,4}"), (64, "4x{4,4,4,4}")]
+         (120, "12x{5,5,5}"), (128, "12x{6,5,5}"), (64, "32x{4,4}"), (64, "4x{4,4,4,4}"), (96, "24x{6,5,5}"),
+         (96, "24x{6,6,4}"), (128, "16x{8,8}")]  # incl. the paper's 128-bit configurations
 
 
 @pytest.mark.parametrize("dims,text", SPECS)
