@@ -287,6 +287,45 @@ def test_live_differential_scan_fn(port, ref):
                 assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+@pytest.mark.parametrize("dims,text,k_cells,n", [(64, "16x{4,4}", 24, 9000), (48, "12x{6,5,5}", 40, 12000),
+                                                   (64, "8x{8,8}", 9, 2500), (32, "4x{8}", 15, 3000), (48, "6x{6,6,4}", 50, 700)])
+def test_live_differential_ivf(port, ref, dims, text, k_cells, n):
+    """The port's IvfIndex::search (shared quantization map + per-cell bias, index.hpp:276-341) against the unmodified
+    reference, live: random coarse centroids and residual codebooks, ragged lists incl. empty / 1-code / shorter than t
+    and R, probes 1 .. > K, both kernel families (normative scalar and the reference's auto SIMD choice), ids, distance
+    bits and counts; and the probe order of every query (index.hpp:247-265), ties included."""
+    rng = np.random.default_rng(k_cells * 1000 + n)
+    sp, sr = port.spec(dims, text), ref.spec(dims, text)
+    cb = (rng.normal(size=sp.cb_floats) * 1.5).astype(np.float32)
+    coarse = (rng.normal(size=(k_cells, dims)) * 3).astype(np.float32)
+    coarse[k_cells - 1] = coarse[0]  # an exact tie in the probe order: the lower cell first
+    assign = rng.integers(0, k_cells, size=n)
+    assign[assign == 3] = 4          # cell 3 stays empty
+    assign[:1] = 5
+    codes = np.stack([rng.integers(0, 1 << b, size=n) for b in sp.bits_list()], 1).astype(np.uint8)
+    packed, ids, boff, ioff, counts = [], [], [], [], []
+    b = i = 0
+    for c in range(k_cells):
+        members = np.nonzero(assign == c)[0].astype(np.uint32)
+        pk = port.pack_list(sp, codes[members])
+        boff.append(b); ioff.append(i); counts.append(len(members)); packed.append(pk); ids.append(members)
+        b += pk.size; i += len(members)
+    packed = np.concatenate(packed) if b else np.zeros(0, np.uint8)
+    ids = np.concatenate(ids)
+    args = (packed, np.array(boff, np.uint64), np.array(ioff, np.uint64), np.array(counts, np.uint64), ids)
+    queries = (rng.normal(size=(7, dims)) * 3).astype(np.float32)
+    queries[0] = coarse[0]
+    for q in queries:
+        for a in (1, 3, k_cells, k_cells + 5):
+            assert np.array_equal(port.probe_order(dims, coarse, q, a), ref.probe_order(dims, coarse, q, a))
+    for probes, r, t in [(1, 10, 20), (3, 100, 400), (k_cells // 2, 50, 50), (k_cells + 3, 300, 1000)]:
+        want = port.ivf_search(sp, cb, coarse, *args, queries, probes=probes, r=r, t=t, threads=2)
+        for fam in (0, 1):
+            got = ref.ivf_search(sr, cb, coarse, *args, queries, probes=probes, r=r, t=t, family=fam, threads=2)
+            for x, y in zip(want, got):
+                assert x.tobytes() == y.tobytes(), (probes, r, t, fam)
+
+
 # ------------------------------------------------------------------ rerank (N4) --
 
 @pytest.mark.parametrize("name", FLAT + IVF)
