@@ -401,6 +401,7 @@ def run_ours(qb, name, wl, args, rank, local_rank, world, dist):
             st_acc["pairs"] += st.pairs_scanned
             st_acc["admitted"] += st.candidates
             st_acc["retries"] += st.overflow_retries
+            st_acc["variant"] = int(st.scan_variant)  # the timed batch's kernel (later one-query calls may plan another)
         ev1.record()
         barrier()
         w1 = time.time()
@@ -476,7 +477,7 @@ def run_ours(qb, name, wl, args, rank, local_rank, world, dist):
             traffic = json.loads(tpath.read_text()).get(name)
             traffic_src = "profiles/traffic.json (dram__bytes_read.sum + dram__bytes_write.sum of the dominant launch, " \
                           "one ncu --set full capture of this workload; not measured in this run)"
-        variant = int(idx.stats().scan_variant)
+        variant = int(st_acc.get("variant", idx.stats().scan_variant))
         vname = qb.lib().qadc_variant_name(variant).decode()
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak if achieved else None, "traffic": traffic, "traffic_source": traffic_src,
