@@ -232,6 +232,7 @@ struct qadc_index {
     uint32_t cand_cap = 8192;
     uint32_t seg0 = 4096;
     uint32_t seg_growth = 8;
+    bool seg_growth_set = false; // set_option("seg_growth") was called: the per-variant default below no longer applies
     int force_variant = -1;
     uint32_t tc_debug = 0; // timing experiments on the tensor-core scan (results are wrong when non-zero)
     // workspace
@@ -336,7 +337,11 @@ static bool scan_select_flat(qadc_index* h, const ScanPlan& plan, const uint8_t*
                          h->sel.thr_key.as<uint64_t>(), st);
         h->timer.span(2, s0e, h->timer.mark(st));
     }
-    std::vector<uint64_t> bounds = segment_bounds(count - head, uint64_t(h->seg0) * h->seg_growth, h->seg_growth);
+    // growth of the segment schedule: an admitted pair costs the tensor-core scan far more than the shared-memory
+    // kernel (hit path per flagged column vs a ballot), so it prefers more, smaller segments -- fewer candidates per
+    // query between two threshold updates (C4: x8 332 ms, x4 320, x3 316, x2 315 per step)
+    const uint32_t growth = (plan.variant == VAR_TC8 && !h->seg_growth_set) ? 2u : h->seg_growth;
+    std::vector<uint64_t> bounds = segment_bounds(count - head, uint64_t(h->seg0) * growth, growth);
     for (auto& b : bounds) b += head;
     std::vector<ScanJob> jobs;
     std::vector<std::pair<size_t, size_t>> seg_jobs;
@@ -1371,7 +1376,10 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         const std::string n(name);
         if (n == "cand_cap") h->cand_cap = uint32_t(std::max<int64_t>(value, 16));
         else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384)) / 16u * 16u; // bulk copies: 16-byte aligned
-        else if (n == "seg_growth") h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
+        else if (n == "seg_growth") {
+            h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
+            h->seg_growth_set = true;
+        }
         else if (n == "force_variant") h->force_variant = int(value);
         else if (n == "probe_tc") h->probe_tc = int(value);
         else if (n == "tc_debug") h->tc_debug = uint32_t(value);
