@@ -253,14 +253,14 @@ static constexpr uint64_t CODE_PAD = 1024; // device code arrays are padded to t
 // nq = queries of the batch about to be scanned (0 = unknown / one list with one table set).
 // The tensor-core scan (scan_tc.cu) works on 256-query tiles and wants long code streams: it takes over from the
 // shared-memory kernel's 32-row tiles once a batch fills a good part of a tile and the list is long enough for its
-// big segments to dominate (measured: C4 2.85x faster, C1 -- 1e6 codes x 1e3 queries, launch bound -- 7 % slower,
-// a single query 2.2x slower).
+// segments to amortise its tile loads (measured: C4 3.1x faster; C1 -- 1e6 codes x 1e3 queries, launch bound -- 2 %
+// faster; a single query over 2e8 codes 2.2x slower: a 256-query tile for one query wastes the tensor core).
 static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true, uint32_t nq = 0) {
     int force = h->force_variant;
     if (force < 0) {
         if (const char* e = std::getenv("QADC_FORCE_VARIANT")) force = std::atoi(e); // tests: every entry point, one variant
     }
-    if (force < 0 && allow_merged && h->kind == 0 && nq >= 96 && h->count >= (uint64_t(4) << 20)) {
+    if (force < 0 && allow_merged && h->kind == 0 && nq >= 96 && h->count >= (uint64_t(1) << 18)) {
         try {
             ScanPlan p = plan_scan(h->ds, h->device, int(VAR_TC8), true);
             p.filter_shift = h->tc_debug;
