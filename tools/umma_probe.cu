@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(128) mma_check_kernel(const uint8_t* A, const 
         uint32_t v[32];
         tmem_ld32(tb + ((warp * 32u) << 16) + c0, v);
         tmem_ld_wait();
-        for (int j = 0; j < 32; ++j) D[size_t(tid) * N + c0 + j] = v[j];
+        for (int j = 0; j < 32; ++j)
+            if (c0 + j < N) D[size_t(tid) * N + c0 + j] = v[j];
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -197,7 +198,70 @@ __global__ void __launch_bounds__(128) mma_ts_check_kernel(const uint8_t* A, con
         uint32_t v[32];
         tmem_ld32(tb + ((warp * 32u) << 16) + c0, v);
         tmem_ld_wait();
-        for (int j = 0; j < 32; ++j) D[size_t(tid) * N + c0 + j] = v[j];
+        for (int j = 0; j < 32; ++j)
+            if (c0 + j < N) D[size_t(tid) * N + c0 + j] = v[j];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "n"(512));
+}
+
+
+// ---------------------------------------------------------------------------------------------------------------
+// Test 1c: 2:4-sparse kind::i8.  Logical A [128][64] with at most two non-zeros per group of four K elements is
+// stored compressed (32 bytes per row, the dense K = 32 tile layout) + 4 metadata bits per group in tensor memory
+// (lane = row, two columns = 64 bits per row per instruction).  `hyp` selects the metadata encoding under test.
+__device__ __forceinline__ void mma_i8_sp(uint32_t d, uint64_t a, uint64_t b, uint32_t e_tmem, uint32_t id, uint32_t acc) {
+    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\ntcgen05.mma.sp.cta_group::1.kind::i8 [%0], %1, %2, [%3], %4, p;\n}\n"
+                 ::"r"(d), "l"(a), "l"(b), "r"(e_tmem), "r"(id), "r"(acc) : "memory");
+}
+__global__ void __launch_bounds__(128) mma_sp_check_kernel(const uint8_t* Ac, const uint32_t* meta /* [128][2] */, const uint8_t* B,
+                                                           uint32_t N, uint32_t id, uint32_t* D) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    uint8_t* sa = sm;             // 128 x 32 B
+    uint8_t* sb = sm + 128 * 32;  // N x 64 B
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    for (uint32_t i = tid; i < 128 * 32; i += 128) {
+        const uint32_t row = i / 32, kb = i % 32;
+        sa[(kb / 16) * (128 * 16) + (row / 8) * 128 + (row % 8) * 16 + kb % 16] = Ac[i];
+    }
+    for (uint32_t i = tid; i < N * 64; i += 128) {
+        const uint32_t row = i / 64, kb = i % 64;
+        sb[(kb / 16) * (N * 16) + (row / 8) * 128 + (row % 8) * 16 + kb % 16] = B[i];
+    }
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tb = tmem_base, e_col = 256;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(tb + ((warp * 32u) << 16) + e_col),
+                 "r"(meta[tid * 2]), "r"(meta[tid * 2 + 1]) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 0) {
+        mma_i8_sp(tb, smem_desc(smem_u32(sa), 128 * 16, 128), smem_desc(smem_u32(sb), N * 16, 128), tb + e_col, id, 0);
+        mma_commit(&bar);
+    }
+    mbar_wait(&bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (uint32_t c0 = 0; c0 < N; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tb + ((warp * 32u) << 16) + c0, v);
+        tmem_ld_wait();
+        for (int j = 0; j < 32; ++j)
+            if (c0 + j < N) D[size_t(tid) * N + c0 + j] = v[j];
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -315,6 +379,54 @@ static void run_rate(int sms, int clock_khz, int mode, uint32_t* sink) {
            ms, 2 * macs / ms / 1e9, ms * 1e-3 * clock_khz * 1e3 / iters, double(iters) * 128 * 256 * sms / (ms * 1e-3));
 }
 
+
+// Rate of the sparse form: per tile NSP sparse MMAs (K = 64 logical each) + one dense K = 32 MMA into alternating
+// accumulators of N columns (N = 240 leaves 32 TMEM columns for two metadata stages), nobody reads them.
+template <int N, int NSP>
+__global__ void __launch_bounds__(64) mma_sp_rate_kernel(uint32_t iters) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t full[2];
+    __shared__ uint32_t tmem_base;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    for (uint32_t i = tid; i < (128 * 32 + N * 64) * NSP / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 1);
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "n"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tb = tmem_base;
+    for (int c = 0; c < 32; c += 2) // metadata: every group keeps positions (0, 1): nibble 0x4
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(tb + ((warp * 32u) << 16) + 480 + c), "r"(0x44444444u), "r"(0x44444444u) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (tid == 32) {
+        const uint32_t a0 = smem_u32(sm), b0 = smem_u32(sm + 128 * 32 * NSP);
+        const uint32_t id_sp = idesc(2, 0, 1, 128, N) | (1u << 2), id_d = idesc(2, 0, 1, 128, N);
+        for (uint32_t it = 0; it < iters; ++it) {
+            const uint32_t buf = it & 1;
+            for (uint32_t ks = 0; ks < NSP; ++ks)
+                mma_i8_sp(tb + buf * N, smem_desc(a0 + ks * 2 * 2048, 2048, 128), smem_desc(b0 + ks * 4 * (N * 16), N * 16, 128),
+                          tb + 480 + (ks & 7) * 2, id_sp, ks > 0);
+            mma_i8(tb + buf * N, smem_desc(a0, 2048, 128), smem_desc(b0, N * 16, 128), id_d, 1);
+            mma_commit(&full[buf]);
+        }
+        mbar_wait(&full[(iters - 1) & 1], ((iters - 1) >> 1) & 1);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "n"(512));
+}
+
 static float bf16_to_f(uint16_t b) {
     uint32_t u = uint32_t(b) << 16;
     float f;
@@ -399,6 +511,55 @@ int main() {
             ts_fails += bad != 0;
             cudaFree(dA); cudaFree(dB); cudaFree(dD);
         }
+
+    // ---- 2:4 sparse i8 check, several metadata encodings
+    for (int hyp = 0; hyp < 4; ++hyp)
+        for (uint32_t N : {64u, 240u}) {
+            std::vector<uint8_t> A(128 * 64, 0), Ac(128 * 32), B(N * 64);
+            std::vector<uint32_t> meta(128 * 2, 0);
+            for (auto& x : B) x = rand() & 255;
+            for (uint32_t r = 0; r < 128; ++r)
+                for (uint32_t g = 0; g < 16; ++g) {
+                    uint32_t i0 = rand() % 3, i1 = i0 + 1 + rand() % (3 - i0);
+                    const uint8_t v0 = rand() & 255, v1 = rand() & 255;
+                    A[r * 64 + 4 * g + i0] = v0;
+                    A[r * 64 + 4 * g + i1] = v1;
+                    Ac[r * 32 + 2 * g] = v0;
+                    Ac[r * 32 + 2 * g + 1] = v1;
+                    const uint32_t nib = (hyp & 1) ? (i1 | (i0 << 2)) : (i0 | (i1 << 2));
+                    const uint32_t gg = (hyp & 2) ? (g ^ 8) : g;
+                    meta[r * 2 + gg / 8] |= nib << (4 * (gg % 8));
+                }
+            uint8_t *dA, *dB;
+            uint32_t *dD, *dM;
+            CK(cudaMalloc(&dA, Ac.size()));
+            CK(cudaMalloc(&dB, B.size()));
+            CK(cudaMalloc(&dM, meta.size() * 4));
+            CK(cudaMalloc(&dD, 128 * N * 4));
+            CK(cudaMemcpy(dA, Ac.data(), Ac.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dB, B.data(), B.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dM, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice));
+            CK(cudaMemset(dD, 0xEE, 128 * N * 4));
+            const size_t smem = 128 * 32 + N * 64;
+            CK(cudaFuncSetAttribute(mma_sp_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            mma_sp_check_kernel<<<1, 128, smem>>>(dA, dM, dB, N, idesc(2, 0, 1, 128, N) | (1u << 2), dD);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) {
+                printf("i8 SPARSE hyp %d N=%3u: CUDA error %s\n", hyp, N, cudaGetErrorString(e));
+                return 3;
+            }
+            std::vector<int32_t> D(128 * N);
+            CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
+            long bad = 0;
+            for (uint32_t r = 0; r < 128; ++r)
+                for (uint32_t c = 0; c < N; ++c) {
+                    int32_t s2 = 0;
+                    for (uint32_t k = 0; k < 64; ++k) s2 += int32_t(A[r * 64 + k]) * int32_t(int8_t(B[c * 64 + k]));
+                    bad += s2 != D[r * N + c];
+                }
+            printf("i8 SPARSE 2:4 (K=64) hyp %d N=%3u: %s (%ld mismatches; D[0][0]=%d D[5][7]=%d)\n", hyp, N, bad ? "no" : "MATCH", bad, D[0], D[5 * N + 7]);
+            cudaFree(dA); cudaFree(dB); cudaFree(dD); cudaFree(dM);
+        }
     // ---- bf16 checks (K elements = Kbytes / 2)
     for (uint32_t N : {64u, 256u})
         for (uint32_t Kb : {32u, 256u}) {
@@ -450,6 +611,25 @@ int main() {
     run_rate<8, 128, 8>(sms, prop.clockRate, 1, sink);
     run_rate<8, 128, 9>(sms, prop.clockRate, 1, sink);
     run_rate<8, 128, 4>(sms, prop.clockRate, 1, sink);
+    {
+        const uint32_t iters = 4000;
+        const size_t smem = (128 * 32 + 240 * 64) * 4;
+        auto k = mma_sp_rate_kernel<240, 4>;
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        k<<<sms, 64, smem>>>(100);
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventRecord(e0));
+        k<<<sms, 64, smem>>>(iters);
+        CK(cudaEventRecord(e1));
+        CK(cudaDeviceSynchronize());
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        printf("rate SPARSE M=128 N=240 K=256 (4 sparse K=64 MMAs) + dense K=32: %.3f ms, %7.1f cycles/tile, %.3e pairs/s\n", ms,
+               ms * 1e-3 * prop.clockRate * 1e3 / iters, double(iters) * 128 * 240 * sms / (ms * 1e-3));
+    }
     printf("TS-mode hypothesis: %s\n", ts_fails ? "WRONG" : "confirmed");
     printf(fails ? "UMMA PROBE: %d FAILURES\n" : "UMMA PROBE: all checks ok\n", fails);
     return fails ? 1 : 0;
