@@ -78,6 +78,9 @@ enum ScanVariant : uint32_t {
                           // rotated codes, LDS.128, 16 codes per warp step -- the IVF layout with the least row padding
     VAR_TC8 = 12, // 16x{4,4} as a one-hot int8 GEMM on tcgen05 (scan_tc.cu): 128 codes x 256 queries per MMA tile, s32
                   // accumulators in TMEM, the admission threshold folded into a ninth K step (sign bit = admit)
+    VAR_TC8S = 13, // the same with 2:4-SPARSE MMAs: a one-hot row has one non-zero per 16 K bytes, so A is stored compressed
+                   // (two kept bytes per group of four + 4 metadata bits in tensor memory) and every MMA covers 64 logical K
+                   // at the cost of 32: 240-query tiles (24 TMEM columns go to the metadata stages)
     VAR_COUNT
 };
 
@@ -119,9 +122,10 @@ struct ScanPlan {
 ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_merged = false);
 void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
 // tensor-core scan of 16x{4,4} (scan_tc.cu)
-uint32_t scan_tc8_smem_bytes();
-void launch_scan_tc8(const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
-void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, void* out, cudaStream_t stream);
+uint32_t scan_tc8_smem_bytes(bool sparse);
+uint32_t scan_tc8_tile_rows(bool sparse);
+void launch_scan_tc8(bool sparse, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
+void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream);
 
 // ---- LUT / calibration / quantization (lut.cu) ----
 struct LutArgs {

@@ -41,26 +41,30 @@ namespace {
 #ifndef TC_PARK_NS
 #define TC_PARK_NS 0u
 #endif
-constexpr int TC_TQ = 256;             // queries per tile = MMA N
+// queries per tile = MMA N: 256 dense; 240 for the 2:4-sparse form (it needs 24 TMEM columns for its metadata stages)
+__host__ __device__ constexpr int tc_tq(bool sp) { return sp ? 240 : 256; }
 constexpr int TC_SUB = 128;            // codes per sub-tile = MMA M
-constexpr int TC_NA = 3;               // one-hot stages
+__host__ __device__ constexpr int tc_na(bool sp) { return sp ? 4 : 3; } // one-hot stages (sparse: 16 KB each + 8 metadata columns)
 constexpr int TC_NSTAGE = 3;           // code stages (TMA ring)
 constexpr int TC_STAGE_BYTES = 8192;   // 1024 codes
 constexpr int TC_STAGE_CODES = TC_STAGE_BYTES / 8;
 constexpr int TC_INFO = 8;             // sub-tile info ring (generator -> epilogue)
 constexpr int TC_TKBUF = 4;            // per-tile threshold keys kept for the epilogue (it trails the producer by < 4 tiles)
 constexpr int TC_KC = 16;              // 16-byte K chunks of the table part (= tables)
-constexpr int TC_B_CHUNK = TC_TQ * 16; // bytes of one K chunk of B (256 rows x 16 B): the descriptor's LBO
+__host__ __device__ constexpr int tc_b_chunk(bool sp) { return tc_tq(sp) * 16; } // bytes of one K chunk of B (TQ rows x 16 B): the descriptor's LBO
 constexpr int TC_A_CHUNK = TC_SUB * 16;
-constexpr int TC_B_BYTES = (TC_KC + 2) * TC_B_CHUNK; // tables + the threshold K step
-constexpr int TC_A_BYTES = TC_KC * TC_A_CHUNK;
+__host__ __device__ constexpr int tc_b_bytes(bool sp) { return (TC_KC + 2) * tc_b_chunk(sp); } // tables + the threshold K step
+__host__ __device__ constexpr int tc_a_bytes(bool sp) { return (sp ? TC_KC / 2 : TC_KC) * TC_A_CHUNK; } // sparse: two kept bytes per group of four
+constexpr uint32_t TC_ECOL = 480;      // sparse: first TMEM column of the metadata stages (8 columns each)
 constexpr int TC_AP_BYTES = 2 * TC_A_CHUNK;          // A': all ones, K = 32
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13;
 constexpr int TC_THREADS = 14 * 32;
 constexpr int TC_WQ_CAP = 64;          // per-epilogue-warp queue of admitted (key, row) pairs
-constexpr int TC_SMEM = TC_B_BYTES + TC_AP_BYTES + TC_NA * TC_A_BYTES + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8 +
-                        TC_TKBUF * TC_TQ * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12;
+__host__ __device__ constexpr int tc_smem(bool sp) {
+    return tc_b_bytes(sp) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8 +
+           TC_TKBUF * 256 * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12;
+}
 
 struct SubInfo {
     uint64_t id_ref;    // explicit ids: index of row 0's id in ScanArgs::ids; implicit: id of row 0
@@ -83,13 +87,25 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) | (uint64_t((sbo >> 4) & 0x3FFFu) << 32) |
            (uint64_t(1) << 46);
 }
-// instruction descriptor (cute::UMMA::InstrDescriptor): s32 accumulate, A = u8, B = s8, both K-major, M = 128, N = 256
-constexpr uint32_t TC_IDESC = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t(TC_TQ) >> 3) << 17) | ((uint32_t(TC_SUB) >> 4) << 24);
+// instruction descriptor (cute::UMMA::InstrDescriptor): s32 accumulate, A = u8, B = s8, both K-major, M = 128, N = TQ;
+// bit 2 = A is 2:4 sparse
+__host__ __device__ constexpr uint32_t tc_idesc(bool sp, bool sparse_instr) {
+    return (sparse_instr ? 4u : 0u) | (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t(tc_tq(sp)) >> 3) << 17) | ((uint32_t(TC_SUB) >> 4) << 24);
+}
 
-__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(TC_IDESC), "r"(accumulate)
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// 2:4-sparse A: 32 compressed bytes per row per instruction = 64 logical K; metadata (4 bits per group of four: the two
+// kept positions, idx0 | idx1 << 2) in tensor memory, lane = row, two columns per instruction (pinned by tools/umma_probe.cu)
+__device__ __forceinline__ void umma_i8_sp(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t e_tmem, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\ntcgen05.mma.sp.cta_group::1.kind::i8 [%0], %1, %2, [%3], %4, p;\n}\n" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(e_tmem), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) { // arrives when every MMA issued so far has completed
@@ -154,12 +170,16 @@ __device__ __forceinline__ uint32_t job_subtiles(uint32_t n_codes) {
 
 } // namespace
 
+template <bool SP>
 __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_param, ScanArgs args_param) {
+    constexpr int TC_TQ = tc_tq(SP), TC_B_CHUNK = tc_b_chunk(SP), TC_B_BYTES = tc_b_bytes(SP), TC_A_BYTES = tc_a_bytes(SP);
+    constexpr int TC_NA = tc_na(SP);
+    constexpr uint32_t TC_IDESC = tc_idesc(SP, false), TC_IDESC_SP = tc_idesc(SP, true);
     extern __shared__ __align__(1024) char smem[];
     __shared__ DevSpec s_ds;
     __shared__ ScanArgs s_args;
     __shared__ __align__(8) uint64_t s_full[TC_NSTAGE], s_empty[TC_NSTAGE]; // code stages: TMA -> generators
-    __shared__ __align__(8) uint64_t s_afull[TC_NA], s_aempty[TC_NA];        // one-hot stages: generators -> MMA
+    __shared__ __align__(8) uint64_t s_afull[tc_na(SP)], s_aempty[tc_na(SP)]; // one-hot stages: generators -> MMA
     __shared__ __align__(8) uint64_t s_dfull[2], s_dempty[2];                // accumulators: MMA -> epilogue
     __shared__ __align__(8) uint64_t s_tfull, s_tempty;                      // LUT tile: producer -> MMA
     __shared__ SubInfo s_info[TC_INFO];
@@ -171,7 +191,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     char* stage = sA + TC_NA * TC_A_BYTES;
     uint2* info_codes = reinterpret_cast<uint2*>(stage + TC_NSTAGE * TC_STAGE_BYTES);
     uint64_t* s_tk = reinterpret_cast<uint64_t*>(info_codes + TC_INFO * TC_SUB); // [TC_TKBUF][TC_TQ] threshold keys per tile
-    uint64_t* s_wq_key = s_tk + TC_TKBUF * TC_TQ;                                  // [TC_EPI_WARPS][TC_WQ_CAP]
+    uint64_t* s_wq_key = s_tk + TC_TKBUF * 256;                                    // [TC_EPI_WARPS][TC_WQ_CAP]
     uint32_t* s_wq_row = reinterpret_cast<uint32_t*>(s_wq_key + TC_EPI_WARPS * TC_WQ_CAP);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -226,10 +246,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / TC_TQ) * (TC_KC * TC_B_CHUNK);
                     mbar_expect_tx(&s_tfull, TC_KC * TC_B_CHUNK);
                     for (uint32_t off = 0; off < uint32_t(TC_KC * TC_B_CHUNK); off += 32768u)
-                        bulk_g2s(sB + off, src + off, 32768u, &s_tfull);
+                        bulk_g2s(sB + off, src + off, min(32768u, uint32_t(TC_KC * TC_B_CHUNK) - off), &s_tfull);
                 }
                 // threshold K step: row r gets 32 signed bytes that sum to v
-                uint64_t* tkb = s_tk + (tseq % TC_TKBUF) * TC_TQ;
+                uint64_t* tkb = s_tk + (tseq % TC_TKBUF) * 256;
                 for (uint32_t r = lane; r < uint32_t(TC_TQ); r += 32) {
                     int v = 4064; // padding rows never admit
                     uint64_t tk_row = KEY_INF;
@@ -302,7 +322,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 const uint32_t cnt = min(uint32_t(TC_STAGE_CODES), job.n_codes - first);
                 const char* sb = stage + size_t(b) * TC_STAGE_BYTES;
                 const uint32_t n_sub = (cnt + TC_SUB - 1) / TC_SUB;
-                for (uint32_t sub = 0; sub < n_sub; ++sub, ++s) {
+                // one sub-tile's operand: everything except the fences and the hand-over (two sub-tiles share those below)
+                auto emit = [&](uint32_t sub, uint32_t s) {
                     const uint32_t sa = s % TC_NA;
                     mbar_wait_park(&s_aempty[sa], ((s / TC_NA) & 1u) ^ 1u); // the MMAs that read this stage have completed
                     const uint32_t i = sub * TC_SUB + g;
@@ -310,6 +331,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     uint2 code = make_uint2(0u, 0u);
                     if (valid) code = *reinterpret_cast<const uint2*>(sb + size_t(i) * 8);
                     char* dst = sA + size_t(sa) * TC_A_BYTES + (g >> 3) * 128 + (g & 7u) * 16;
+                    if constexpr (SP) {
+                        // 2:4-sparse one-hot row: per group of four K bytes two bytes are kept.  Table j's chunk shrinks to
+                        // 8 bytes (a 0x01 at byte 2g or 2g + 1, g = c_j >> 2) + 16 metadata bits (nibble g = the kept
+                        // positions (p, p + 1), or (2, 3) for p = 3; every other group keeps (0, 1) = 0x4).  Per MMA
+                        // (K = 64 = four tables): two 16-byte stores and two metadata columns, lane = row.
+                        const uint32_t one = valid ? 1u : 0u;
+                        uint32_t meta[8];
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) {
+                            uint32_t w[8], m16[4];
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                const int j = 4 * ks + t;
+                                const uint32_t cw = j < 8 ? code.x : code.y;
+                                const uint32_t n = (cw >> ((j & 7) * 4)) & 15u;
+                                const uint32_t p = n & 3u, g4 = n >> 2;
+                                const uint32_t sh = 16u * g4 + (p == 3u ? 8u : 0u);  // bit position of the 0x01 in the 64-bit word
+                                w[2 * t] = __funnelshift_lc(0u, one, sh);
+                                w[2 * t + 1] = __funnelshift_lc(0u, one, sh - 32u);
+                                const uint32_t nib = (0xEE94u >> (4u * p)) & 15u;     // (0,1) (1,2) (2,3) (2,3)
+                                m16[t] = 0x4444u ^ ((nib ^ 4u) << (4u * g4));
+                            }
+                            *reinterpret_cast<uint4*>(dst + (2 * ks) * TC_A_CHUNK) = make_uint4(w[0], w[1], w[2], w[3]);
+                            *reinterpret_cast<uint4*>(dst + (2 * ks + 1) * TC_A_CHUNK) = make_uint4(w[4], w[5], w[6], w[7]);
+                            meta[2 * ks] = m16[0] | (m16[1] << 16);
+                            meta[2 * ks + 1] = m16[2] | (m16[3] << 16);
+                        }
+                        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                                         tmem + (((warp & 3u) * 32u) << 16) + TC_ECOL + sa * 8),
+                                     "r"(meta[0]), "r"(meta[1]), "r"(meta[2]), "r"(meta[3]), "r"(meta[4]), "r"(meta[5]), "r"(meta[6]), "r"(meta[7])
+                                     : "memory");
+                    } else
                     if (!(dbg & 2u)) {
                         // 16 stores of 16 bytes: table j's chunk is a 0x01 byte at position c_j.  (A 17-entry table of the
                         // chunks in shared memory saves ALU work but its bank conflicts overload the shared-memory pipe the
@@ -343,9 +396,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         inf.pad = 0;
                         s_info[slot] = inf;
                     }
+                };
+                // sub-tiles go out in pairs: the store fences and the mbarrier hand-over are pure latency for a generator
+                // warp (one per scheduler), and with one pair of fences per two sub-tiles it keeps ahead of the sparse MMAs
+                for (uint32_t sub = 0; sub < n_sub; sub += 2, s += 2) {
+                    const bool two = sub + 1 < n_sub;
+                    emit(sub, s);
+                    if (two) emit(sub + 1, s + 1);
+                    if constexpr (SP) {
+                        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                        tc_fence_before();
+                    }
                     if (!(dbg & 16u)) proxy_fence();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&s_afull[sa]);
+                    if (lane == 0) {
+                        mbar_arrive(&s_afull[s % TC_NA]);
+                        if (two) mbar_arrive(&s_afull[(s + 1) % TC_NA]);
+                    }
+                    if (!two) s -= 1; // (the loop adds 2)
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[b]); // this warp is done with the code stage
@@ -375,12 +443,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 if (lane == 0) {
                     const uint32_t d = tmem + buf * TC_TQ;
                     const uint32_t a0 = a_base + sa * TC_A_BYTES;
+                    if constexpr (SP) {
 #pragma unroll
-                    for (int ks = 0; ks < TC_KC / 2; ++ks)
-                        if (ks == 0 || !(dbg & 4u))
-                        umma_i8(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
-                                umma_desc(b_base + ks * 2 * TC_B_CHUNK, TC_B_CHUNK, 128), ks > 0);
-                    umma_i8(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128), 1u);
+                        for (int ks = 0; ks < 4; ++ks) // four 2:4-sparse MMAs of 64 logical K (= four tables) each
+                            if (ks == 0 || !(dbg & 4u))
+                                umma_i8_sp(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
+                                           umma_desc(b_base + ks * 4 * TC_B_CHUNK, TC_B_CHUNK, 128), tmem + TC_ECOL + sa * 8 + 2 * ks,
+                                           TC_IDESC_SP, ks > 0);
+                    } else {
+#pragma unroll
+                        for (int ks = 0; ks < TC_KC / 2; ++ks)
+                            if (ks == 0 || !(dbg & 4u))
+                                umma_i8(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
+                                        umma_desc(b_base + ks * 2 * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, ks > 0);
+                    }
+                    umma_i8(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, 1u);
                     umma_commit(&s_aempty[sa]); // the one-hot stage is free once these MMAs have read it
                     umma_commit(&s_dfull[buf]); // ... and the accumulator is complete
                 }
@@ -430,6 +507,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     uint32_t v[64];
                     tmem_ld128_pack16(tmem + buf * TC_TQ + lane_base + c0, v);
                     tmem_ld_wait();
+                    if constexpr (SP) { // a warp owns 120 of the tile's 240 queries: the load's last 8 columns are not its own
+                        v[60] = v[61] = v[62] = v[63] = 0u;
+                    }
                     // everything this warp needs from the accumulator is in registers now: hand the buffer back to the MMA
                     // warp BEFORE looking at the values (admissions never touch tensor memory again)
                     tc_fence_before();
@@ -465,7 +545,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                 if (!valid) m[k] = 0u;
                             }
                         }
-                        const uint64_t* tks = s_tk + inf.tk_slot * TC_TQ;
+                        const uint64_t* tks = s_tk + inf.tk_slot * 256;
                         const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, inf.n_valid - 1)] : uint32_t(inf.id_ref) + rowi;
                         // ONE copy of the column loop (the switch inside pick64 is ~200 instructions; sixteen inlined
                         // copies of it thrashed the instruction cache)
@@ -523,38 +603,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
 
 // ------------------------------------------------------------------------------------------ tile image --
 
-// qlut [n_rows][256] u8 (reference table order) -> per tile of 256 rows the B operand image
-// [kc = 16][row = 256][16 bytes] of e - 128 (two's complement: e ^ 0x80); rows past n_rows hold e = 0.
-__global__ void pack_tiles_tc8_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint8_t* __restrict__ out) {
+// qlut [n_rows][256] u8 (reference table order) -> per tile of tq rows the B operand image
+// [kc = 16][row = tq][16 bytes] of e - 128 (two's complement: e ^ 0x80); rows past n_rows hold e = 0.
+__global__ void pack_tiles_tc8_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint32_t tq, uint8_t* __restrict__ out) {
     const uint32_t tile = blockIdx.x;
-    for (uint32_t i = threadIdx.x; i < uint32_t(TC_KC * TC_TQ); i += blockDim.x) {
-        const uint32_t kc = i / TC_TQ, r = i % TC_TQ;
-        const uint32_t row = tile * TC_TQ + r;
+    for (uint32_t i = threadIdx.x; i < uint32_t(TC_KC) * tq; i += blockDim.x) {
+        const uint32_t kc = i / tq, r = i % tq;
+        const uint32_t row = tile * tq + r;
         uint4 v = make_uint4(0, 0, 0, 0);
         if (row < n_rows) v = *reinterpret_cast<const uint4*>(qlut + size_t(row) * 256 + kc * 16);
         v.x ^= 0x80808080u;
         v.y ^= 0x80808080u;
         v.z ^= 0x80808080u;
         v.w ^= 0x80808080u;
-        *reinterpret_cast<uint4*>(out + size_t(tile) * (TC_KC * TC_B_CHUNK) + size_t(kc) * TC_B_CHUNK + r * 16) = v;
+        *reinterpret_cast<uint4*>(out + size_t(tile) * (TC_KC * tq * 16) + size_t(kc) * (tq * 16) + r * 16) = v;
     }
 }
 
-uint32_t scan_tc8_smem_bytes() { return TC_SMEM; }
+uint32_t scan_tc8_smem_bytes(bool sparse) { return sparse ? tc_smem(true) : tc_smem(false); }
+uint32_t scan_tc8_tile_rows(bool sparse) { return tc_tq(sparse); }
 
-void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, void* out, cudaStream_t stream) {
+void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     if (n_rows == 0) return;
-    pack_tiles_tc8_kernel<<<(n_rows + TC_TQ - 1) / TC_TQ, 256, 0, stream>>>(static_cast<const uint8_t*>(qlut), n_rows,
-                                                                           static_cast<uint8_t*>(out));
+    pack_tiles_tc8_kernel<<<(n_rows + tq - 1) / tq, 256, 0, stream>>>(static_cast<const uint8_t*>(qlut), n_rows, tq,
+                                                                      static_cast<uint8_t*>(out));
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_scan_tc8(const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
-    QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_tc8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
-    scan_tc8_kernel<<<grid, TC_THREADS, TC_SMEM, stream>>>(ds, args);
+void launch_scan_tc8(bool sparse, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
+    if (sparse) {
+        QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_tc8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(true)));
+        scan_tc8_kernel<true><<<grid, TC_THREADS, tc_smem(true), stream>>>(ds, args);
+    } else {
+        QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_tc8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(false)));
+        scan_tc8_kernel<false><<<grid, TC_THREADS, tc_smem(false), stream>>>(ds, args);
+    }
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
 } // namespace qadc
+

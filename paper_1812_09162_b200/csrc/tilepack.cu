@@ -156,7 +156,8 @@ size_t tile_entry_bytes(ScanVariant v) {
     case VAR_F32X2: return 4;
     case VAR_U16X1: return 2;
     case VAR_U8X1: return 1;
-    case VAR_TC8: return 1; // signed bytes e - 128, K-major operand image
+    case VAR_TC8:
+    case VAR_TC8S: return 1; // signed bytes e - 128, K-major operand image
     default: return 4;
     }
 }
@@ -165,8 +166,10 @@ void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, uint32_t pair, cons
                        uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     switch (v) {
     case VAR_TC8:
-        if (width != 8 || E != 256 || tq != 256) throw Error(QADC_ERR_CONFIG, "pack_tiles: the tensor-core layout is for 16x{4,4}");
-        launch_pack_tiles_tc8(qlut, n_rows, out, stream);
+    case VAR_TC8S:
+        if (width != 8 || E != 256 || tq != scan_tc8_tile_rows(v == VAR_TC8S))
+            throw Error(QADC_ERR_CONFIG, "pack_tiles: the tensor-core layout is for 16x{4,4}");
+        launch_pack_tiles_tc8(qlut, n_rows, tq, out, stream);
         return;
     case VAR_F16X4H_C8Q: {
         if (width != 16 || (E != 512 && E != 576 && E != 384) || tq != 16)
