@@ -41,6 +41,15 @@ namespace {
 #ifndef TC_PARK_NS
 #define TC_PARK_NS 0u
 #endif
+// -DTC_PROFILE: lane 0 of one warp per role accumulates clock64() spans around its waits and prints them for CTA 0 at the
+// end of every long launch (build: make EXTRA=-DTC_PROFILE; the numbers behind DESIGN.md section 4.5's stall table)
+#ifdef TC_PROFILE
+#define TC_PROF_DECL(n) long long prof_t[n] = {}; long long prof_c = clock64(); long long prof_start = prof_c
+#define TC_PROF(i) do { const long long now_ = clock64(); prof_t[i] += now_ - prof_c; prof_c = now_; } while (0)
+#else
+#define TC_PROF_DECL(n)
+#define TC_PROF(i)
+#endif
 // queries per tile = MMA N: 256 dense; 240 for the 2:4-sparse form (it needs 24 TMEM columns for its metadata stages)
 __host__ __device__ constexpr int tc_tq(bool sp) { return sp ? 240 : 256; }
 constexpr int TC_SUB = 128;            // codes per sub-tile = MMA M
@@ -306,6 +315,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         // ============================ generators: codes -> one-hot A stages ==================================
         const uint32_t g = tid - TC_GEN_WARP0 * 32; // row of the sub-tile
         uint32_t it = 0, s = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
+        TC_PROF_DECL(5);
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
             const ScanJob job = a->jobs[ji];
             if (job.n_codes == 0 || job.n_rows == 0) continue;
@@ -317,7 +327,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             const uint32_t n_st = (job.n_codes + TC_STAGE_CODES - 1) / TC_STAGE_CODES;
             for (uint32_t st = 0; st < n_st; ++st, ++it) {
                 const uint32_t b = it % TC_NSTAGE;
+                TC_PROF(0);
                 mbar_wait_park(&s_full[b], (it / TC_NSTAGE) & 1u);
+                TC_PROF(1);
                 const uint32_t first = st * TC_STAGE_CODES;
                 const uint32_t cnt = min(uint32_t(TC_STAGE_CODES), job.n_codes - first);
                 const char* sb = stage + size_t(b) * TC_STAGE_BYTES;
@@ -325,38 +337,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 // one sub-tile's operand: everything except the fences and the hand-over (two sub-tiles share those below)
                 auto emit = [&](uint32_t sub, uint32_t s) {
                     const uint32_t sa = s % TC_NA;
+                    TC_PROF(0);
                     mbar_wait_park(&s_aempty[sa], ((s / TC_NA) & 1u) ^ 1u); // the MMAs that read this stage have completed
+                    TC_PROF(2);
                     const uint32_t i = sub * TC_SUB + g;
                     const bool valid = i < cnt;
                     uint2 code = make_uint2(0u, 0u);
                     if (valid) code = *reinterpret_cast<const uint2*>(sb + size_t(i) * 8);
                     char* dst = sA + size_t(sa) * TC_A_BYTES + (g >> 3) * 128 + (g & 7u) * 16;
                     if constexpr (SP) {
-                        // 2:4-sparse one-hot row: per group of four K bytes two bytes are kept.  Table j's chunk shrinks to
-                        // 8 bytes (a 0x01 at byte 2g or 2g + 1, g = c_j >> 2) + 16 metadata bits (nibble g = the kept
-                        // positions (p, p + 1), or (2, 3) for p = 3; every other group keeps (0, 1) = 0x4).  Per MMA
-                        // (K = 64 = four tables): two 16-byte stores and two metadata columns, lane = row.
-                        const uint32_t one = valid ? 1u : 0u;
+                        // 2:4-sparse one-hot row.  The K order is ours to choose (pack_tiles_tc8_kernel lays B out to match), and
+                        // it is chosen so that the operand is a handful of shifts per table: K step ks covers the tables
+                        // ks, ks + 4, ks + 8, ks + 12 (the nibbles at bit 4 ks of the code's four 16-bit quarters); entry n of
+                        // a table sits in group n >> 2 at position 2 (n & 1) + ((n >> 1) & 1).  The kept pair of EVERY group of
+                        // the table is (0, 1) if n is even and (2, 3) if n is odd -- the other groups' kept bytes are zero, so
+                        // which positions they claim does not matter -- hence 16 metadata bits 0x4444 or 0xEEEE per table and
+                        // the single 0x01 at compressed byte n >> 1.  Per K step: two 16-byte stores + two metadata columns.
+                        const uint64_t one = valid ? 1ull : 0ull;
                         uint32_t meta[8];
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks) {
-                            uint32_t w[8], m16[4];
+                            uint64_t w[4];
 #pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                const int j = 4 * ks + t;
-                                const uint32_t cw = j < 8 ? code.x : code.y;
-                                const uint32_t n = (cw >> ((j & 7) * 4)) & 15u;
-                                const uint32_t p = n & 3u, g4 = n >> 2;
-                                const uint32_t sh = 16u * g4 + (p == 3u ? 8u : 0u);  // bit position of the 0x01 in the 64-bit word
-                                w[2 * t] = __funnelshift_lc(0u, one, sh);
-                                w[2 * t + 1] = __funnelshift_lc(0u, one, sh - 32u);
-                                const uint32_t nib = (0xEE94u >> (4u * p)) & 15u;     // (0,1) (1,2) (2,3) (2,3)
-                                m16[t] = 0x4444u ^ ((nib ^ 4u) << (4u * g4));
+                            for (int c = 0; c < 4; ++c) {
+                                const uint32_t cw = c < 2 ? code.x : code.y;
+                                const int lo = 4 * ks + 16 * (c & 1) + 1;                                 // bit position of n >> 1
+                                const uint32_t sh = (lo >= 3 ? cw >> (lo >= 3 ? lo - 3 : 0) : cw << (3 - lo)) & 0x38u; // 8 (n >> 1)
+                                w[c] = one << sh;
                             }
-                            *reinterpret_cast<uint4*>(dst + (2 * ks) * TC_A_CHUNK) = make_uint4(w[0], w[1], w[2], w[3]);
-                            *reinterpret_cast<uint4*>(dst + (2 * ks + 1) * TC_A_CHUNK) = make_uint4(w[4], w[5], w[6], w[7]);
-                            meta[2 * ks] = m16[0] | (m16[1] << 16);
-                            meta[2 * ks + 1] = m16[2] | (m16[3] << 16);
+                            *reinterpret_cast<uint4*>(dst + (2 * ks) * TC_A_CHUNK) =
+                                make_uint4(uint32_t(w[0]), uint32_t(w[0] >> 32), uint32_t(w[1]), uint32_t(w[1] >> 32));
+                            *reinterpret_cast<uint4*>(dst + (2 * ks + 1) * TC_A_CHUNK) =
+                                make_uint4(uint32_t(w[2]), uint32_t(w[2] >> 32), uint32_t(w[3]), uint32_t(w[3] >> 32));
+                            meta[2 * ks] = ((code.x >> (4 * ks)) & 0x00010001u) * 0xAAAAu + 0x44444444u;
+                            meta[2 * ks + 1] = ((code.y >> (4 * ks)) & 0x00010001u) * 0xAAAAu + 0x44444444u;
                         }
                         asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
                                          tmem + (((warp & 3u) * 32u) << 16) + TC_ECOL + sa * 8),
@@ -403,26 +417,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     const bool two = sub + 1 < n_sub;
                     emit(sub, s);
                     if (two) emit(sub + 1, s + 1);
+                    TC_PROF(0);
                     if constexpr (SP) {
                         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                         tc_fence_before();
                     }
+                    TC_PROF(3);
                     if (!(dbg & 16u)) proxy_fence();
                     __syncwarp();
                     if (lane == 0) {
                         mbar_arrive(&s_afull[s % TC_NA]);
                         if (two) mbar_arrive(&s_afull[(s + 1) % TC_NA]);
                     }
+                    TC_PROF(4);
                     if (!two) s -= 1; // (the loop adds 2)
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[b]); // this warp is done with the code stage
             }
         }
+#ifdef TC_PROFILE
+        if (blockIdx.x == 0 && tid == TC_GEN_WARP0 * 32 && s > 2000)
+            printf("tc-prof gen: subtiles %u total %lld | work %lld wait-codes %lld wait-aempty %lld wait-st %lld fence+arrive %lld (cycles per sub-tile: %lld)\n",
+                   s, clock64() - prof_start, prof_t[0], prof_t[1], prof_t[2], prof_t[3], prof_t[4], (clock64() - prof_start) / s);
+#endif
     } else if (warp == TC_MMA_WARP) {
         // ============================ MMA issuer ==============================================================
         uint32_t s = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
         const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB), ap_base = smem_u32(sAp);
+        TC_PROF_DECL(3);
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
             const ScanJob job = a->jobs[ji];
             if (job.n_codes == 0 || job.n_rows == 0) continue;
@@ -437,8 +460,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             const uint32_t n_sub = job_subtiles(job.n_codes);
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
                 const uint32_t sa = s % TC_NA, buf = s & 1u;
+                TC_PROF(0);
                 mbar_wait_park(&s_afull[sa], (s / TC_NA) & 1u);
+                TC_PROF(1);
                 mbar_wait_park(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
+                TC_PROF(2);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t d = tmem + buf * TC_TQ;
@@ -464,6 +490,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 __syncwarp();
             }
         }
+#ifdef TC_PROFILE
+        if (blockIdx.x == 0 && lane == 0 && s > 2000)
+            printf("tc-prof mma: subtiles %u total %lld | issue %lld wait-afull %lld wait-dempty %lld\n", s, clock64() - prof_start,
+                   prof_t[0], prof_t[1], prof_t[2]);
+#endif
     } else {
         // ============================ epilogue: TMEM -> sign test -> exact admission ==========================
         uint32_t s = 0;
@@ -474,6 +505,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         uint64_t* wq_key = s_wq_key + warp * TC_WQ_CAP;
         uint32_t* wq_row = s_wq_row + warp * TC_WQ_CAP;
         uint32_t qn = 0; // warp-uniform fill level of the queue
+        TC_PROF_DECL(3);
         const uint32_t lt_mask = (1u << lane) - 1u;
         auto drain = [&]() { // 32 admissions in flight at once (the atomics' round trips overlap)
             __syncwarp();
@@ -497,7 +529,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             const uint32_t n_sub = job_subtiles(job.n_codes);
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
                 const uint32_t buf = s & 1u, slot = s % TC_INFO;
+                TC_PROF(0);
                 mbar_wait_park(&s_dfull[buf], (s >> 1) & 1u);
+                TC_PROF(1);
                 tc_fence_after();
                 const SubInfo inf = s_info[slot];
                 const bool valid = rowi < inf.n_valid;
@@ -507,6 +541,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     uint32_t v[64];
                     tmem_ld128_pack16(tmem + buf * TC_TQ + lane_base + c0, v);
                     tmem_ld_wait();
+                    TC_PROF(2);
                     if constexpr (SP) { // a warp owns 120 of the tile's 240 queries: the load's last 8 columns are not its own
                         v[60] = v[61] = v[62] = v[63] = 0u;
                     }
@@ -595,6 +630,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             }
         }
         if (qn) drain();
+#ifdef TC_PROFILE
+        if (blockIdx.x == 0 && tid == 0 && s > 2000)
+            printf("tc-prof epi: subtiles %u total %lld | work %lld wait-dfull %lld tmem-load %lld\n", s, clock64() - prof_start, prof_t[0],
+                   prof_t[1], prof_t[2]);
+#endif
     }
     tc_fence_before();
     __syncthreads();
@@ -605,13 +645,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
 
 // qlut [n_rows][256] u8 (reference table order) -> per tile of tq rows the B operand image
 // [kc = 16][row = tq][16 bytes] of e - 128 (two's complement: e ^ 0x80); rows past n_rows hold e = 0.
-__global__ void pack_tiles_tc8_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint32_t tq, uint8_t* __restrict__ out) {
+// Dense: chunk kc = table kc in entry order.  Sparse (the generator's K order): chunk 4 ks + c = table ks + 4 c, and byte
+// 4 g + p of the chunk = entry 4 g + 2 (p & 1) + (p >> 1).
+__global__ void pack_tiles_tc8_kernel(const uint8_t* __restrict__ qlut, uint32_t n_rows, uint32_t tq, uint32_t sparse,
+                                      uint8_t* __restrict__ out) {
     const uint32_t tile = blockIdx.x;
     for (uint32_t i = threadIdx.x; i < uint32_t(TC_KC) * tq; i += blockDim.x) {
         const uint32_t kc = i / tq, r = i % tq;
         const uint32_t row = tile * tq + r;
+        const uint32_t table = sparse ? (kc >> 2) + 4 * (kc & 3u) : kc;
         uint4 v = make_uint4(0, 0, 0, 0);
-        if (row < n_rows) v = *reinterpret_cast<const uint4*>(qlut + size_t(row) * 256 + kc * 16);
+        if (row < n_rows) v = *reinterpret_cast<const uint4*>(qlut + size_t(row) * 256 + table * 16);
+        if (sparse) { // within every group of four entries: (e0, e1, e2, e3) -> (e0, e2, e1, e3)
+            v.x = __byte_perm(v.x, 0u, 0x3120);
+            v.y = __byte_perm(v.y, 0u, 0x3120);
+            v.z = __byte_perm(v.z, 0u, 0x3120);
+            v.w = __byte_perm(v.w, 0u, 0x3120);
+        }
         v.x ^= 0x80808080u;
         v.y ^= 0x80808080u;
         v.z ^= 0x80808080u;
@@ -626,7 +676,7 @@ uint32_t scan_tc8_tile_rows(bool sparse) { return tc_tq(sparse); }
 void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     if (n_rows == 0) return;
     pack_tiles_tc8_kernel<<<(n_rows + tq - 1) / tq, 256, 0, stream>>>(static_cast<const uint8_t*>(qlut), n_rows, tq,
-                                                                      static_cast<uint8_t*>(out));
+                                                                      tq == uint32_t(tc_tq(true)) ? 1u : 0u, static_cast<uint8_t*>(out));
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());
 }
