@@ -262,7 +262,7 @@ static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true, uint32_t
     }
     if (force < 0 && allow_merged && h->kind == 0 && nq >= 96 && h->count >= (uint64_t(1) << 18)) {
         try {
-            ScanPlan p = plan_scan(h->ds, h->device, int(VAR_TC8), true);
+            ScanPlan p = plan_scan(h->ds, h->device, int(VAR_TC8S), true);
             p.filter_shift = h->tc_debug;
             return p;
         } catch (const Error&) { // not 16x{4,4}
