@@ -269,7 +269,7 @@ static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true, uint32_t
         }
     }
     ScanPlan p = plan_scan(h->ds, h->device, force, allow_merged);
-    if (p.variant == VAR_TC8 || p.variant == VAR_TC8S) p.filter_shift = h->tc_debug;
+    if (is_tc8(p.variant)) p.filter_shift = h->tc_debug;
     return p;
 }
 
@@ -340,7 +340,7 @@ static bool scan_select_flat(qadc_index* h, const ScanPlan& plan, const uint8_t*
     // growth of the segment schedule: an admitted pair costs the tensor-core scan far more than the shared-memory
     // kernel (hit path per flagged column vs a ballot), so it prefers more, smaller segments -- fewer candidates per
     // query between two threshold updates (C4: x8 332 ms, x4 320, x3 316, x2 315 per step)
-    const uint32_t growth = ((plan.variant == VAR_TC8 || plan.variant == VAR_TC8S) && !h->seg_growth_set) ? 2u : h->seg_growth;
+    const uint32_t growth = (is_tc8(plan.variant) && !h->seg_growth_set) ? 2u : h->seg_growth;
     std::vector<uint64_t> bounds = segment_bounds(count - head, uint64_t(h->seg0) * growth, growth);
     for (auto& b : bounds) b += head;
     std::vector<ScanJob> jobs;

@@ -81,6 +81,8 @@ enum ScanVariant : uint32_t {
     VAR_TC8S = 13, // the same with 2:4-SPARSE MMAs: a one-hot row has one non-zero per 16 K bytes, so A is stored compressed
                    // (two kept bytes per group of four + 4 metadata bits in tensor memory) and every MMA covers 64 logical K
                    // at the cost of 32: 240-query tiles (24 TMEM columns go to the metadata stages)
+    VAR_TC8P = 14, // the sparse form on CTA PAIRS (cta_group::2, clusters of two): M = 256 codes per MMA, each SM holds and
+                   // reads only half of the tile's tables (the single-CTA form is bound by those shared-memory reads)
     VAR_COUNT
 };
 
@@ -122,9 +124,11 @@ struct ScanPlan {
 ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_merged = false);
 void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
 // tensor-core scan of 16x{4,4} (scan_tc.cu)
-uint32_t scan_tc8_smem_bytes(bool sparse);
-uint32_t scan_tc8_tile_rows(bool sparse);
-void launch_scan_tc8(bool sparse, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
+inline bool is_tc8(int variant) { return variant == VAR_TC8 || variant == VAR_TC8S || variant == VAR_TC8P; }
+inline int tc8_mode(int variant) { return variant - int(VAR_TC8); } // 0 dense, 1 sparse, 2 sparse on CTA pairs
+uint32_t scan_tc8_smem_bytes(int mode);
+uint32_t scan_tc8_tile_rows(int mode);
+void launch_scan_tc8(int mode, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
 void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream);
 
 // ---- LUT / calibration / quantization (lut.cu) ----

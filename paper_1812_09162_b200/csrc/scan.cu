@@ -704,6 +704,7 @@ const char* variant_name(uint32_t v) {
     case VAR_F16X4H_C16Q: return "f16x4h-c16q (irregular 16-bit specs, 16-row tile of quad lines, rotated codes, LDS.128, 16 codes per warp step)";
     case VAR_F16X4H_C4D: return "f16x4h-c4d (as f16x4h-c4, entry lines duplicated: bank-conflict-free)";
     case VAR_TC8: return "tc8 (16x{4,4} as a one-hot int8 GEMM on tcgen05: 128 codes x 256 queries per tile, s32 accumulators in TMEM, threshold folded into the contraction)";
+    case VAR_TC8P: return "tc8p (the tc8s contraction on CTA pairs: tcgen05 cta_group::2, 256 codes x 240 queries per MMA, each SM holds half of the tile's tables)";
     case VAR_TC8S: return "tc8s (16x{4,4} as a 2:4-sparse one-hot int8 GEMM on tcgen05: 128 codes x 240 queries per tile, compressed A + metadata in TMEM, s32 accumulators in TMEM, threshold folded into the contraction)";
     }
     return "?";
@@ -762,13 +763,14 @@ ScanPlan plan_scan(const DevSpec& ds, int device, int force_variant, bool allow_
             set(VAR_F16X4H_C8Q, PolQ655::TQ, smem_need<PolQ655>(GeomQ655::E));
             break;
         case VAR_TC8:
-        case VAR_TC8S: {
-            const bool sp = force_variant == VAR_TC8S;
+        case VAR_TC8S:
+        case VAR_TC8P: {
+            const int mode = tc8_mode(force_variant);
             if (!allow_merged || !G44::matches(ds)) throw Error(QADC_ERR_CONFIG, "scan: tc8 is the flat 16x{4,4} layout");
-            if (!fits(scan_tc8_smem_bytes(sp))) throw Error(QADC_ERR_CONFIG, "scan: tc8 does not fit shared memory");
-            p.variant = sp ? VAR_TC8S : VAR_TC8;
-            p.tq = scan_tc8_tile_rows(sp);
-            p.smem_bytes = scan_tc8_smem_bytes(sp);
+            if (!fits(scan_tc8_smem_bytes(mode))) throw Error(QADC_ERR_CONFIG, "scan: tc8 does not fit shared memory");
+            p.variant = ScanVariant(force_variant);
+            p.tq = scan_tc8_tile_rows(mode);
+            p.smem_bytes = scan_tc8_smem_bytes(mode);
             p.tile_bufs = 1;
             p.filter_shift = 0;
             return p;
@@ -860,8 +862,9 @@ void launch_scan(const ScanPlan& plan, const DevSpec& ds, const ScanArgs& args_i
     args.tile_bufs = plan.tile_bufs;
     args.filter_shift = plan.filter_shift;
     switch (plan.variant) {
-    case VAR_TC8: return launch_scan_tc8(false, ds, args, grid, stream);
-    case VAR_TC8S: return launch_scan_tc8(true, ds, args, grid, stream);
+    case VAR_TC8:
+    case VAR_TC8S:
+    case VAR_TC8P: return launch_scan_tc8(tc8_mode(plan.variant), ds, args, grid, stream);
     case VAR_F16X8:
         if (G44::matches(ds)) return launch_one<PolF16x8, G44>(plan, ds, args, grid, stream);
         return launch_one<PolF16x8, GeomRT>(plan, ds, args, grid, stream);

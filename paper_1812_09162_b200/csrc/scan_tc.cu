@@ -60,9 +60,11 @@ constexpr int TC_STAGE_CODES = TC_STAGE_BYTES / 8;
 constexpr int TC_INFO = 8;             // sub-tile info ring (generator -> epilogue)
 constexpr int TC_TKBUF = 4;            // per-tile threshold keys kept for the epilogue (it trails the producer by < 4 tiles)
 constexpr int TC_KC = 16;              // 16-byte K chunks of the table part (= tables)
-__host__ __device__ constexpr int tc_b_chunk(bool sp) { return tc_tq(sp) * 16; } // bytes of one K chunk of B (TQ rows x 16 B): the descriptor's LBO
+// B rows one CTA holds: the whole tile, or half of it for a CTA pair (cta_group::2 reads the other half from the peer)
+__host__ __device__ constexpr int tc_brows(bool sp, bool pair = false) { return pair ? tc_tq(sp) / 2 : tc_tq(sp); }
+__host__ __device__ constexpr int tc_b_chunk(bool sp, bool pair = false) { return tc_brows(sp, pair) * 16; } // bytes of one K chunk of B (rows x 16 B): the descriptor's LBO
 constexpr int TC_A_CHUNK = TC_SUB * 16;
-__host__ __device__ constexpr int tc_b_bytes(bool sp) { return (TC_KC + 2) * tc_b_chunk(sp); } // tables + the threshold K step
+__host__ __device__ constexpr int tc_b_bytes(bool sp, bool pair = false) { return (TC_KC + 2) * tc_b_chunk(sp, pair); } // tables + the threshold K step
 __host__ __device__ constexpr int tc_a_bytes(bool sp) { return (sp ? TC_KC / 2 : TC_KC) * TC_A_CHUNK; } // sparse: two kept bytes per group of four
 constexpr uint32_t TC_ECOL = 480;      // sparse: first TMEM column of the metadata stages (8 columns each)
 constexpr int TC_AP_BYTES = 2 * TC_A_CHUNK;          // A': all ones, K = 32
@@ -70,8 +72,8 @@ constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13;
 constexpr int TC_THREADS = 14 * 32;
 constexpr int TC_WQ_CAP = 64;          // per-epilogue-warp queue of admitted (key, row) pairs
-__host__ __device__ constexpr int tc_smem(bool sp) {
-    return tc_b_bytes(sp) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8 +
+__host__ __device__ constexpr int tc_smem(bool sp, bool pair = false) {
+    return tc_b_bytes(sp, pair) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8 +
            TC_TKBUF * 256 * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12;
 }
 
@@ -98,31 +100,88 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 }
 // instruction descriptor (cute::UMMA::InstrDescriptor): s32 accumulate, A = u8, B = s8, both K-major, M = 128, N = TQ;
 // bit 2 = A is 2:4 sparse
-__host__ __device__ constexpr uint32_t tc_idesc(bool sp, bool sparse_instr) {
-    return (sparse_instr ? 4u : 0u) | (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t(tc_tq(sp)) >> 3) << 17) | ((uint32_t(TC_SUB) >> 4) << 24);
+__host__ __device__ constexpr uint32_t tc_idesc(bool sp, bool sparse_instr, bool pair = false) {
+    return (sparse_instr ? 4u : 0u) | (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t(tc_tq(sp)) >> 3) << 17) |
+           ((uint32_t(pair ? 2 * TC_SUB : TC_SUB) >> 4) << 24);
 }
 
+template <bool PAIR = false>
 __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
-        : "memory");
+    if constexpr (PAIR)
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+            : "memory");
+    else
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+            : "memory");
 }
 // 2:4-sparse A: 32 compressed bytes per row per instruction = 64 logical K; metadata (4 bits per group of four: the two
 // kept positions, idx0 | idx1 << 2) in tensor memory, lane = row, two columns per instruction (pinned by tools/umma_probe.cu)
+template <bool PAIR = false>
 __device__ __forceinline__ void umma_i8_sp(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t e_tmem, uint32_t idesc,
                                            uint32_t accumulate) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\ntcgen05.mma.sp.cta_group::1.kind::i8 [%0], %1, %2, [%3], %4, p;\n}\n" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(e_tmem), "r"(idesc), "r"(accumulate)
-        : "memory");
+    if constexpr (PAIR)
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\ntcgen05.mma.sp.cta_group::2.kind::i8 [%0], %1, %2, [%3], %4, p;\n}\n" ::"r"(d_tmem),
+            "l"(a), "l"(b), "r"(e_tmem), "r"(idesc), "r"(accumulate)
+            : "memory");
+    else
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %5, 0;\ntcgen05.mma.sp.cta_group::1.kind::i8 [%0], %1, %2, [%3], %4, p;\n}\n" ::"r"(d_tmem),
+            "l"(a), "l"(b), "r"(e_tmem), "r"(idesc), "r"(accumulate)
+            : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar) { // arrives when every MMA issued so far has completed
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+// arrives when every MMA issued so far has completed; CTA pair: on the barrier at this offset in BOTH CTAs
+template <bool PAIR = false>
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    if constexpr (PAIR)
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         smem_u32(bar)),
+                     "h"(uint16_t(3))
+                     : "memory");
+    else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// ---- CTA pair plumbing: rank in the cluster, cluster-wide barrier, arrive on a barrier of the LEADER CTA (rank 0)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// (default .release.cta semantics, as CUTLASS's ClusterBarrier::arrive(cta_id): what the arrivals publish -- the one-hot
+// stage and its metadata -- is read by the arriving CTA's OWN tensor core, the barrier only orders the leader's issue
+// after it; a .release.cluster arrive was measured at ~400 cycles per hand-over)
+template <bool PAIR>
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar, uint32_t rank = 0) {
+    if (PAIR && rank != 0) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(0u));
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+    } else {
+        mbar_arrive(bar);
+    }
 }
 // mbarrier wait that parks the warp between polls (NANOSLEEP.SYNCS wakes on the barrier's phase change): ten of this
 // kernel's fourteen warps are waiting at any time, and a tight try_wait loop cost 22 % of all issued instructions
 __device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(addr), "r"(parity), "r"(TC_PARK_NS)
+            : "memory");
+    } while (!done);
+}
+// the same for a barrier other CTAs of the cluster arrive on (kept apart so that its semantics can be changed in one place)
+__device__ __forceinline__ void mbar_wait_park_cluster(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t done;
     do {
@@ -172,18 +231,23 @@ __device__ __forceinline__ uint32_t pick64(const uint32_t (&v)[64], uint32_t r) 
 }
 
 // sub-tiles of one job: its stages hold TC_STAGE_CODES codes each, every stage is cut into sub-tiles of TC_SUB codes
-__device__ __forceinline__ uint32_t job_subtiles(uint32_t n_codes) {
+// (CTA pair: a step covers 2 x TC_SUB codes, the CTA of rank r takes the r-th half)
+__device__ __forceinline__ uint32_t job_subtiles(uint32_t n_codes, uint32_t step = TC_SUB) {
     const uint32_t full = n_codes / TC_STAGE_CODES, rem = n_codes - full * TC_STAGE_CODES;
-    return full * (TC_STAGE_CODES / TC_SUB) + (rem + TC_SUB - 1) / TC_SUB;
+    return full * (TC_STAGE_CODES / step) + (rem + step - 1) / step;
 }
 
 } // namespace
 
-template <bool SP>
+template <bool SP, bool PAIR>
 __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_param, ScanArgs args_param) {
-    constexpr int TC_TQ = tc_tq(SP), TC_B_CHUNK = tc_b_chunk(SP), TC_B_BYTES = tc_b_bytes(SP), TC_A_BYTES = tc_a_bytes(SP);
+    static_assert(SP || !PAIR, "the CTA-pair form is built for the sparse operand only");
+    constexpr int TC_TQ = tc_tq(SP), TC_BROWS = tc_brows(SP, PAIR), TC_B_CHUNK = tc_b_chunk(SP, PAIR), TC_B_BYTES = tc_b_bytes(SP, PAIR),
+                  TC_A_BYTES = tc_a_bytes(SP);
     constexpr int TC_NA = tc_na(SP);
-    constexpr uint32_t TC_IDESC = tc_idesc(SP, false), TC_IDESC_SP = tc_idesc(SP, true);
+    constexpr uint32_t TC_IDESC = tc_idesc(SP, false, PAIR), TC_IDESC_SP = tc_idesc(SP, true, PAIR);
+    constexpr uint32_t TC_STEP = PAIR ? 2 * TC_SUB : TC_SUB; // codes per MMA step of the CTA (pair)
+    constexpr uint32_t NCTA = PAIR ? 2 : 1;
     extern __shared__ __align__(1024) char smem[];
     __shared__ DevSpec s_ds;
     __shared__ ScanArgs s_args;
@@ -191,6 +255,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     __shared__ __align__(8) uint64_t s_afull[tc_na(SP)], s_aempty[tc_na(SP)]; // one-hot stages: generators -> MMA
     __shared__ __align__(8) uint64_t s_dfull[2], s_dempty[2];                // accumulators: MMA -> epilogue
     __shared__ __align__(8) uint64_t s_tfull, s_tempty;                      // LUT tile: producer -> MMA
+    __shared__ __align__(8) uint64_t s_tload;                                // CTA pair: this CTA's half of the tile has landed
     __shared__ SubInfo s_info[TC_INFO];
     __shared__ uint32_t s_tmem;
 
@@ -204,6 +269,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     uint32_t* s_wq_row = reinterpret_cast<uint32_t*>(s_wq_key + TC_EPI_WARPS * TC_WQ_CAP);
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // CTA pair: both CTAs walk the same jobs; rank r generates, holds and post-processes the r-th 128 codes of every step
+    // and holds the r-th half of the tile's B rows; the leader (rank 0) issues the MMAs for both.  Barriers the leader's
+    // MMA warp waits on (afull, dempty, tfull) live in the leader and count arrivals from both CTAs; barriers the tensor
+    // core signals (aempty, dfull, tempty) exist in both CTAs and get multicast commits.
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
     if (tid == 0) {
         s_ds = ds_param;
         s_args = args_param;
@@ -212,34 +282,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             mbar_init(&s_empty[i], 4);
         }
         for (int i = 0; i < TC_NA; ++i) {
-            mbar_init(&s_afull[i], 4);
+            mbar_init(&s_afull[i], 4 * NCTA);
             mbar_init(&s_aempty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_dfull[i], 1);
-            mbar_init(&s_dempty[i], TC_EPI_WARPS);
+            mbar_init(&s_dempty[i], TC_EPI_WARPS * NCTA);
         }
-        mbar_init(&s_tfull, 2); // the tile's expect_tx + the threshold rows' arrive
+        mbar_init(&s_tfull, 2); // the tile's expect_tx + the threshold rows' arrive (CTA pair: one arrive per CTA)
         mbar_init(&s_tempty, 1);
+        mbar_init(&s_tload, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == TC_MMA_WARP) { // the MMA warp owns the tensor memory: 2 accumulators x 256 columns
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "n"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "n"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)), "n"(512));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     for (uint32_t i = tid; i < TC_AP_BYTES / 16; i += TC_THREADS) // A': every row all ones
         reinterpret_cast<uint4*>(sAp)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
     proxy_fence();
     tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync_all(); // the peer's barriers are initialised before anything arrives on them
     tc_fence_after();
     const DevSpec* ds = &s_ds;
     const ScanArgs* a = &s_args;
     const uint32_t tmem = s_tmem;
     const uint32_t dbg = a->filter_shift; // timing experiments (option tc_debug): 1 = epilogue reads nothing, 2 = generators store nothing, 4 = one MMA per sub-tile
 
-    const uint32_t j_begin = a->cta_begin ? a->cta_begin[blockIdx.x] : uint32_t(uint64_t(a->n_jobs) * blockIdx.x / gridDim.x);
-    const uint32_t j_end = a->cta_begin ? a->cta_begin[blockIdx.x + 1] : uint32_t(uint64_t(a->n_jobs) * (blockIdx.x + 1) / gridDim.x);
+    const uint32_t unit = blockIdx.x / NCTA, n_units = gridDim.x / NCTA; // a CTA, or a CTA pair
+    const uint32_t j_begin = (a->cta_begin && !PAIR) ? a->cta_begin[unit] : uint32_t(uint64_t(a->n_jobs) * unit / n_units);
+    const uint32_t j_end = (a->cta_begin && !PAIR) ? a->cta_begin[unit + 1] : uint32_t(uint64_t(a->n_jobs) * (unit + 1) / n_units);
 
     if (warp == TC_PROD_WARP) {
         // ============================ producer: code stream + tile loads + threshold rows ====================
@@ -252,10 +330,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 prev_nr = job.n_rows;
                 mbar_wait_park(&s_tempty, (tseq & 1u) ^ 1u); // the MMAs of the previous tile are done with B
                 if (lane == 0) {
-                    const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / TC_TQ) * (TC_KC * TC_B_CHUNK);
-                    mbar_expect_tx(&s_tfull, TC_KC * TC_B_CHUNK);
-                    for (uint32_t off = 0; off < uint32_t(TC_KC * TC_B_CHUNK); off += 32768u)
-                        bulk_g2s(sB + off, src + off, min(32768u, uint32_t(TC_KC * TC_B_CHUNK) - off), &s_tfull);
+                    if constexpr (PAIR) { // this CTA's rows of every K chunk: 16 pieces of the [kc][TQ rows][16 B] image
+                        const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / TC_TQ) * (TC_KC * TC_TQ * 16) +
+                                          size_t(rank) * TC_B_CHUNK;
+                        mbar_expect_tx(&s_tload, TC_KC * TC_B_CHUNK);
+                        for (uint32_t kc = 0; kc < uint32_t(TC_KC); ++kc)
+                            bulk_g2s(sB + kc * TC_B_CHUNK, src + size_t(kc) * (TC_TQ * 16), TC_B_CHUNK, &s_tload);
+                    } else {
+                        const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / TC_TQ) * (TC_KC * TC_B_CHUNK);
+                        mbar_expect_tx(&s_tfull, TC_KC * TC_B_CHUNK);
+                        for (uint32_t off = 0; off < uint32_t(TC_KC * TC_B_CHUNK); off += 32768u)
+                            bulk_g2s(sB + off, src + off, min(32768u, uint32_t(TC_KC * TC_B_CHUNK) - off), &s_tfull);
+                    }
                 }
                 // threshold K step: row r gets 32 signed bytes that sum to v
                 uint64_t* tkb = s_tk + (tseq % TC_TKBUF) * 256;
@@ -287,13 +373,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         }
                         w[k] = word;
                     }
-                    char* dst = sB + TC_KC * TC_B_CHUNK + (r >> 3) * 128 + (r & 7u) * 16;
+                    if (PAIR && r / uint32_t(TC_BROWS) != rank) continue; // (the keys above are kept for the whole tile)
+                    const uint32_t rl = PAIR ? r % uint32_t(TC_BROWS) : r;
+                    char* dst = sB + TC_KC * TC_B_CHUNK + (rl >> 3) * 128 + (rl & 7u) * 16;
                     *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
                     *reinterpret_cast<uint4*>(dst + TC_B_CHUNK) = make_uint4(w[4], w[5], w[6], w[7]);
                 }
                 proxy_fence(); // generic-proxy stores -> visible to the tensor core's (async proxy) operand reads
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&s_tfull);
+                if constexpr (PAIR) { // tell the leader once this CTA's half (bulk copies + threshold rows) is in place
+                    mbar_wait_park(&s_tload, tseq & 1u);
+                    if (lane == 0) mbar_arrive_leader<true>(&s_tfull, rank);
+                } else {
+                    if (lane == 0) mbar_arrive(&s_tfull);
+                }
                 ++tseq;
             }
             const uint8_t* gcodes = a->codes + job.code_off * 8;
@@ -333,14 +426,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 const uint32_t first = st * TC_STAGE_CODES;
                 const uint32_t cnt = min(uint32_t(TC_STAGE_CODES), job.n_codes - first);
                 const char* sb = stage + size_t(b) * TC_STAGE_BYTES;
-                const uint32_t n_sub = (cnt + TC_SUB - 1) / TC_SUB;
+                const uint32_t n_sub = (cnt + TC_STEP - 1) / TC_STEP;
                 // one sub-tile's operand: everything except the fences and the hand-over (two sub-tiles share those below)
                 auto emit = [&](uint32_t sub, uint32_t s) {
                     const uint32_t sa = s % TC_NA;
                     TC_PROF(0);
                     mbar_wait_park(&s_aempty[sa], ((s / TC_NA) & 1u) ^ 1u); // the MMAs that read this stage have completed
                     TC_PROF(2);
-                    const uint32_t i = sub * TC_SUB + g;
+                    const uint32_t sub_g = PAIR ? 2 * sub + rank : sub; // which 128 codes of the stage
+                    const uint32_t i = sub_g * TC_SUB + g;
                     const bool valid = i < cnt;
                     uint2 code = make_uint2(0u, 0u);
                     if (valid) code = *reinterpret_cast<const uint2*>(sb + size_t(i) * 8);
@@ -365,6 +459,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                 const uint32_t sh = (lo >= 3 ? cw >> (lo >= 3 ? lo - 3 : 0) : cw << (3 - lo)) & 0x38u; // 8 (n >> 1)
                                 w[c] = one << sh;
                             }
+                            if (dbg & 2u) continue; // (timing experiment: nothing stored)
                             *reinterpret_cast<uint4*>(dst + (2 * ks) * TC_A_CHUNK) =
                                 make_uint4(uint32_t(w[0]), uint32_t(w[0] >> 32), uint32_t(w[1]), uint32_t(w[1] >> 32));
                             *reinterpret_cast<uint4*>(dst + (2 * ks + 1) * TC_A_CHUNK) =
@@ -402,9 +497,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     info_codes[slot * TC_SUB + g] = code;
                     if (g == 0) {
                         SubInfo inf;
-                        const uint64_t pos = uint64_t(first) + uint64_t(sub) * TC_SUB;
+                        const uint64_t pos = uint64_t(first) + uint64_t(sub_g) * TC_SUB;
                         inf.id_ref = a->ids ? job.ids_off + pos : uint64_t(job.id_base) + pos;
-                        inf.n_valid = min(uint32_t(TC_SUB), cnt - sub * TC_SUB);
+                        inf.n_valid = sub_g * TC_SUB < cnt ? min(uint32_t(TC_SUB), cnt - sub_g * TC_SUB) : 0u;
                         inf.row_begin = job.row_begin;
                         inf.tk_slot = (tseq - 1) % TC_TKBUF;
                         inf.pad = 0;
@@ -426,8 +521,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     if (!(dbg & 16u)) proxy_fence();
                     __syncwarp();
                     if (lane == 0) {
-                        mbar_arrive(&s_afull[s % TC_NA]);
-                        if (two) mbar_arrive(&s_afull[(s + 1) % TC_NA]);
+                        mbar_arrive_leader<PAIR>(&s_afull[s % TC_NA], rank);
+                        if (two) mbar_arrive_leader<PAIR>(&s_afull[(s + 1) % TC_NA], rank);
                     }
                     TC_PROF(4);
                     if (!two) s -= 1; // (the loop adds 2)
@@ -441,8 +536,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             printf("tc-prof gen: subtiles %u total %lld | work %lld wait-codes %lld wait-aempty %lld wait-st %lld fence+arrive %lld (cycles per sub-tile: %lld)\n",
                    s, clock64() - prof_start, prof_t[0], prof_t[1], prof_t[2], prof_t[3], prof_t[4], (clock64() - prof_start) / s);
 #endif
-    } else if (warp == TC_MMA_WARP) {
-        // ============================ MMA issuer ==============================================================
+    } else if (warp == TC_MMA_WARP && rank == 0) {
+        // ============================ MMA issuer (CTA pair: the leader's, for both CTAs) =======================
         uint32_t s = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
         const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB), ap_base = smem_u32(sAp);
         TC_PROF_DECL(3);
@@ -452,18 +547,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             if (job.row_begin != prev_rb || job.n_rows != prev_nr) {
                 prev_rb = job.row_begin;
                 prev_nr = job.n_rows;
-                if (tseq > 0 && lane == 0) umma_commit(&s_tempty); // every MMA on the old tile has completed
+                if (tseq > 0 && lane == 0) umma_commit<PAIR>(&s_tempty); // every MMA on the old tile has completed
                 __syncwarp();
-                mbar_wait_park(&s_tfull, tseq & 1u);
+                if constexpr (PAIR) mbar_wait_park_cluster(&s_tfull, tseq & 1u);
+                else mbar_wait_park(&s_tfull, tseq & 1u);
                 ++tseq;
             }
-            const uint32_t n_sub = job_subtiles(job.n_codes);
+            const uint32_t n_sub = job_subtiles(job.n_codes, TC_STEP);
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
                 const uint32_t sa = s % TC_NA, buf = s & 1u;
                 TC_PROF(0);
-                mbar_wait_park(&s_afull[sa], (s / TC_NA) & 1u);
+                if constexpr (PAIR) mbar_wait_park_cluster(&s_afull[sa], (s / TC_NA) & 1u);
+                else mbar_wait_park(&s_afull[sa], (s / TC_NA) & 1u);
                 TC_PROF(1);
-                mbar_wait_park(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
+                if constexpr (PAIR) mbar_wait_park_cluster(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
+                else mbar_wait_park(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
                 TC_PROF(2);
                 tc_fence_after();
                 if (lane == 0) {
@@ -473,7 +571,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks) // four 2:4-sparse MMAs of 64 logical K (= four tables) each
                             if (ks == 0 || !(dbg & 4u))
-                                umma_i8_sp(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
+                                umma_i8_sp<PAIR>(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
                                            umma_desc(b_base + ks * 4 * TC_B_CHUNK, TC_B_CHUNK, 128), tmem + TC_ECOL + sa * 8 + 2 * ks,
                                            TC_IDESC_SP, ks > 0);
                     } else {
@@ -483,9 +581,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                 umma_i8(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
                                         umma_desc(b_base + ks * 2 * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, ks > 0);
                     }
-                    umma_i8(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, 1u);
-                    umma_commit(&s_aempty[sa]); // the one-hot stage is free once these MMAs have read it
-                    umma_commit(&s_dfull[buf]); // ... and the accumulator is complete
+                    umma_i8<PAIR>(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, 1u);
+                    umma_commit<PAIR>(&s_aempty[sa]); // the one-hot stage is free once these MMAs have read it
+                    umma_commit<PAIR>(&s_dfull[buf]); // ... and the accumulator is complete
                 }
                 __syncwarp();
             }
@@ -495,7 +593,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             printf("tc-prof mma: subtiles %u total %lld | issue %lld wait-afull %lld wait-dempty %lld\n", s, clock64() - prof_start,
                    prof_t[0], prof_t[1], prof_t[2]);
 #endif
-    } else {
+    } else if (warp < TC_EPI_WARPS) {
         // ============================ epilogue: TMEM -> sign test -> exact admission ==========================
         uint32_t s = 0;
         const uint32_t quad = warp & 3u, half_w = warp >> 2;   // TMEM lane quadrant, column half
@@ -526,7 +624,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
             const ScanJob job = a->jobs[ji];
             if (job.n_codes == 0 || job.n_rows == 0) continue;
-            const uint32_t n_sub = job_subtiles(job.n_codes);
+            const uint32_t n_sub = job_subtiles(job.n_codes, TC_STEP);
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
                 const uint32_t buf = s & 1u, slot = s % TC_INFO;
                 TC_PROF(0);
@@ -549,7 +647,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     // warp BEFORE looking at the values (admissions never touch tensor memory again)
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&s_dempty[buf]);
+                    if (lane == 0) mbar_arrive_leader<PAIR>(&s_dempty[buf], rank);
                     uint32_t g[4]; // OR of each group of 16 registers = 32 columns (four independent chains)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -581,7 +679,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             }
                         }
                         const uint64_t* tks = s_tk + inf.tk_slot * 256;
-                        const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, inf.n_valid - 1)] : uint32_t(inf.id_ref) + rowi;
+                        const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, max(inf.n_valid, 1u) - 1u)] : uint32_t(inf.id_ref) + rowi;
                         // ONE copy of the column loop (the switch inside pick64 is ~200 instructions; sixteen inlined
                         // copies of it thrashed the instruction cache)
 #pragma unroll 1
@@ -625,7 +723,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 if (dbg & 1u) { // (timing experiment: nothing was read)
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&s_dempty[buf]);
+                    if (lane == 0) mbar_arrive_leader<PAIR>(&s_dempty[buf], rank);
                 }
             }
         }
@@ -638,7 +736,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == TC_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    if constexpr (PAIR) {
+        cluster_sync_all(); // neither CTA leaves (or frees tensor memory) while the other may still arrive on its barriers
+        if (warp == TC_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    } else {
+        if (warp == TC_MMA_WARP) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    }
 }
 
 // ------------------------------------------------------------------------------------------ tile image --
@@ -670,8 +773,9 @@ __global__ void pack_tiles_tc8_kernel(const uint8_t* __restrict__ qlut, uint32_t
     }
 }
 
-uint32_t scan_tc8_smem_bytes(bool sparse) { return sparse ? tc_smem(true) : tc_smem(false); }
-uint32_t scan_tc8_tile_rows(bool sparse) { return tc_tq(sparse); }
+// mode: 0 dense, 1 2:4-sparse, 2 2:4-sparse on CTA pairs
+uint32_t scan_tc8_smem_bytes(int mode) { return mode == 2 ? tc_smem(true, true) : mode == 1 ? tc_smem(true) : tc_smem(false); }
+uint32_t scan_tc8_tile_rows(int mode) { return tc_tq(mode != 0); }
 
 void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
     if (n_rows == 0) return;
@@ -681,13 +785,36 @@ void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, void*
     QADC_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_scan_tc8(bool sparse, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
-    if (sparse) {
-        QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_tc8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(true)));
-        scan_tc8_kernel<true><<<grid, TC_THREADS, tc_smem(true), stream>>>(ds, args);
+void launch_scan_tc8(int mode, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream) {
+    if (mode == 2) {
+        // CTA pairs: clusters of two, at most one pair per TPC; `grid` arrives as min(SMs, jobs)
+        int dev = 0, sms = 0;
+        QADC_CUDA_CHECK(cudaGetDevice(&dev));
+        QADC_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        const int pairs = std::max(1, std::min(grid, sms / 2));
+        auto kern = scan_tc8_kernel<true, true>;
+        QADC_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(true, true)));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(2 * pairs));
+        cfg.blockDim = dim3(TC_THREADS);
+        cfg.dynamicSmemBytes = tc_smem(true, true);
+        cfg.stream = stream;
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = 2;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        QADC_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ds, args));
+    } else if (mode == 1) {
+        auto kern = scan_tc8_kernel<true, false>;
+        QADC_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(true)));
+        kern<<<grid, TC_THREADS, tc_smem(true), stream>>>(ds, args);
     } else {
-        QADC_CUDA_CHECK(cudaFuncSetAttribute(scan_tc8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(false)));
-        scan_tc8_kernel<false><<<grid, TC_THREADS, tc_smem(false), stream>>>(ds, args);
+        auto kern = scan_tc8_kernel<false, false>;
+        QADC_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem(false)));
+        kern<<<grid, TC_THREADS, tc_smem(false), stream>>>(ds, args);
     }
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());

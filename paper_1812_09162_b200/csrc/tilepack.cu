@@ -157,7 +157,8 @@ size_t tile_entry_bytes(ScanVariant v) {
     case VAR_U16X1: return 2;
     case VAR_U8X1: return 1;
     case VAR_TC8:
-    case VAR_TC8S: return 1; // signed bytes e - 128, K-major operand image
+    case VAR_TC8S:
+    case VAR_TC8P: return 1; // signed bytes e - 128, K-major operand image
     default: return 4;
     }
 }
@@ -167,7 +168,8 @@ void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, uint32_t pair, cons
     switch (v) {
     case VAR_TC8:
     case VAR_TC8S:
-        if (width != 8 || E != 256 || tq != scan_tc8_tile_rows(v == VAR_TC8S))
+    case VAR_TC8P:
+        if (width != 8 || E != 256 || tq != scan_tc8_tile_rows(tc8_mode(v)))
             throw Error(QADC_ERR_CONFIG, "pack_tiles: the tensor-core layout is for 16x{4,4}");
         launch_pack_tiles_tc8(qlut, n_rows, tq, out, stream);
         return;

@@ -90,7 +90,7 @@ def test_scan_fn_differential(port):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), (pat, m, n, kw["cap"])
 
 
-@pytest.mark.parametrize("variant", [12, 13])
+@pytest.mark.parametrize("variant", [12, 13, 14])
 def test_tensor_core_scan_through_scan_fn_contract(port, monkeypatch, variant):
     """The tcgen05 one-hot GEMM scan (scan_tc.cu, variants 12 = dense and 13 = 2:4 sparse) forced onto the QuantizedScanFn entry point
     (QADC_FORCE_VARIANT): the same differential as above for 16x{4,4} -- ragged list lengths (sub-tile and stage
@@ -997,7 +997,7 @@ def test_concurrent_calls_on_one_handle_serialise():
 
 
 @pytest.mark.parametrize("dims,text,variants", [
-    (128, "16x{4,4}", [0, 1, 2, 3, 7, 9, 12, 13]),   # f16x8, f32x2, u16x1, u8x1, f16x4-c4, merged pair tables, tcgen05 one-hot GEMM (dense, 2:4 sparse)
+    (128, "16x{4,4}", [0, 1, 2, 3, 7, 9, 12, 13, 14]),   # f16x8, f32x2, u16x1, u8x1, f16x4-c4, merged pair tables, tcgen05 one-hot GEMM (dense, 2:4 sparse, sparse on CTA pairs)
     (96, "12x{6,5,5}", [1, 2, 3, 4, 5, 6, 8, 10, 11]),   # f32x2, u16x1, u8x1, f16x4h, -c2, -c4, -c4d, merged quad, 16-row quad
     (64, "12x{6,6,4}", [1, 2, 4, 5, 10]),        # f32x2, u16x1, f16x4h, -c2, merged quad (default)
     (60, "12x{5,5,5}", [1, 2, 4, 5, 10]),        # f32x2, u16x1, f16x4h, -c2, merged quad (default)
