@@ -504,18 +504,19 @@ def run_ours(qb, name, wl, args, rank, local_rank, world, dist):
                                   "frac": top / 4492.0 if top else None, "ops_per_pair": 576,
                                   "peak_source": "measured on this pool: back-to-back M=128 N=256 K=256 kind::i8 MMAs on all "
                                                  "SMs, tools/umma_probe.cu (nominal dense int8: 4500 TOP/s)"}
-        if variant == 13:
+        if variant in (13, 14):
             # the 2:4-sparse form: same contraction (576 logical ops per pair), half of the table part's products skipped.
             # Ceiling = the MMA-only rate of the kernel's own instruction sequence (4 sparse K = 64 + 1 dense K = 32,
             # M = 128, N = 240), measured with nothing else running: 731 cycles per tile per SM.
             sm_n = prop.multi_processor_count
-            peak_pairs = 128.0 * 240.0 * sm_n * sm_clock / 731.0
+            mma_cycles = 731.0 if variant == 13 else 647.0  # (14: the CTA-pair form, tools/umma2_probe.cu)
+            peak_pairs = 128.0 * 240.0 * sm_n * sm_clock / mma_cycles
             top = (st_acc["pairs"] * 576.0 / scan_s) / 1e12 if scan_s > 0 else None
             roofline["tensor"] = {"bound": "tensor (tcgen05 kind::i8, 2:4 sparse)", "achieved": top,
                                   "peak": peak_pairs * 576.0 / 1e12, "unit": "TOP/s (dense-equivalent)",
                                   "frac": top / (peak_pairs * 576.0 / 1e12) if top else None, "ops_per_pair": 576,
                                   "peak_source": "measured on this pool: the kernel's MMA sequence back to back on all SMs, "
-                                                 "731 cycles per 128 x 240 tile (tools/umma_probe.cu); the dense kind::i8 peak "
+                                                 f"{mma_cycles:.0f} cycles per 128 x 240 tile per SM (tools/umma_probe.cu, umma2_probe.cu); the dense kind::i8 peak "
                                                  "measured the same way is 4492 TOP/s"}
         if variant < 12:
             roofline["smem"] = {"bound": "shared-memory pipe", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",

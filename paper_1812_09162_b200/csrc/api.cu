@@ -262,7 +262,10 @@ static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true, uint32_t
     }
     if (force < 0 && allow_merged && h->kind == 0 && nq >= 96 && h->count >= (uint64_t(1) << 18)) {
         try {
-            ScanPlan p = plan_scan(h->ds, h->device, int(VAR_TC8S), true);
+            // dense (256-query tiles) or 2:4 sparse (240-query tiles, a tile step costs ~5/6 of a dense one: 1090 vs 1309
+            // cycles per 128 codes measured on C4): whichever needs less tensor time for this batch
+            const uint64_t t_dense = (nq + 255) / 256, t_sparse = (nq + 239) / 240;
+            ScanPlan p = plan_scan(h->ds, h->device, int(t_sparse * 5 <= t_dense * 6 ? VAR_TC8S : VAR_TC8), true);
             p.filter_shift = h->tc_debug;
             return p;
         } catch (const Error&) { // not 16x{4,4}

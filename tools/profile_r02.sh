@@ -5,11 +5,11 @@ TAG=${1:-r02}
 LIB='qadc|scan_|pack_tiles|flat_tables|seed_topk|tighten|finalize|init_select|probe_|ivf_'
 C4="python bench.py --workload c4 --steps 1 --warmup 3 --also '' --no-cpu-baseline --no-parity"
 C5="python bench.py --workload c5g --steps 1 --warmup 3 --also '' --no-cpu-baseline --no-parity"
-# C4 (the headline): every library launch of the first step, then the big segment of the tensor-core scan in full
+# C4 (the headline): every library launch of the first step (15 segments), then the 6.7e7-code segment of the tensor-core scan in full
 eval $C4 > gpurun_out/${TAG}_plain_c4.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$LIB" -c 16 --csv --log-file gpurun_out/${TAG}_launches_c4.csv bash -c "$C4" > gpurun_out/${TAG}_ncu_launch_c4.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$LIB" -c 40 --csv --log-file gpurun_out/${TAG}_launches_c4.csv bash -c "$C4" > gpurun_out/${TAG}_ncu_launch_c4.log 2>&1
 eval $C4 > gpurun_out/${TAG}_plain_c4b.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:scan_tc8 -s 4 -c 1 -o gpurun_out/${TAG}_scan_c4 bash -c "$C4" > gpurun_out/${TAG}_ncu_full_c4.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:scan_tc8 -s 13 -c 1 -o gpurun_out/${TAG}_scan_c4 bash -c "$C4" > gpurun_out/${TAG}_ncu_full_c4.log 2>&1
 # C5 (IVF): launch list of one step, the first scan round and the probe contraction in full
 eval $C5 > gpurun_out/${TAG}_plain_c5.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"$LIB" -s 1 -c 40 --csv --log-file gpurun_out/${TAG}_launches_c5.csv bash -c "$C5" > gpurun_out/${TAG}_ncu_launch_c5.log 2>&1
