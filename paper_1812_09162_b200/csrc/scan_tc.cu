@@ -41,6 +41,12 @@ namespace {
 #ifndef TC_PARK_NS
 #define TC_PARK_NS 0u
 #endif
+#ifndef TC_SPIN
+#define TC_SPIN 0 // 1: mbarrier waits spin on test_wait instead of the (parking) try_wait
+#endif
+#ifndef TC_GEN_GROUP
+#define TC_GEN_GROUP 2 // sub-tiles a generator warp emits per hand-over (1 or 2)
+#endif
 // -DTC_PROFILE: lane 0 of one warp per role accumulates clock64() spans around its waits and prints them for CTA 0 at the
 // end of every long launch (build: make EXTRA=-DTC_PROFILE; the numbers behind DESIGN.md section 4.5's stall table)
 #ifdef TC_PROFILE
@@ -69,8 +75,8 @@ __host__ __device__ constexpr int tc_a_bytes(bool sp) { return (sp ? TC_KC / 2 :
 constexpr uint32_t TC_ECOL = 480;      // sparse: first TMEM column of the metadata stages (8 columns each)
 constexpr int TC_AP_BYTES = 2 * TC_A_CHUNK;          // A': all ones, K = 32
 constexpr int TC_EPI_WARPS = 8;
-constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13;
-constexpr int TC_THREADS = 14 * 32;
+constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13, TC_MMA_WARP2 = 14;
+constexpr int TC_THREADS = 15 * 32;
 constexpr int TC_WQ_CAP = 64;          // per-epilogue-warp queue of admitted (key, row) pairs
 __host__ __device__ constexpr int tc_smem(bool sp, bool pair = false) {
     return tc_b_bytes(sp, pair) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8 +
@@ -145,6 +151,48 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     else
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// The same three instructions for a CONVERGED warp: every lane executes the statement with warp-uniform operands and
+// elect.sync picks the one lane that issues.  Inside `if (lane == 0)` the compiler cannot see that the operands are uniform
+// and wraps every tcgen05 instruction in an ELECT / R2UR.BROADCAST / BRA.U.ANY loop (~20 dependent instructions each).
+#define QADC_ELECT_PRED ".reg .pred p, q;\nelect.sync _|q, 0xffffffff;\n"
+template <bool PAIR>
+__device__ __forceinline__ void umma_i8_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accumulate) {
+    if constexpr (PAIR)
+        asm volatile("{\n" QADC_ELECT_PRED "setp.ne.b32 p, %4, 0;\n@q tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+                     "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+                     : "memory");
+    else
+        asm volatile("{\n" QADC_ELECT_PRED "setp.ne.b32 p, %4, 0;\n@q tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+                     "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+                     : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void umma_i8_sp_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t e_tmem, uint32_t idesc,
+                                                 uint32_t accumulate) {
+    if constexpr (PAIR)
+        asm volatile("{\n" QADC_ELECT_PRED "setp.ne.b32 p, %5, 0;\n@q tcgen05.mma.sp.cta_group::2.kind::i8 [%0], %1, %2, [%3], %4, p;\n}\n" ::"r"(
+                         d_tmem),
+                     "l"(a), "l"(b), "r"(e_tmem), "r"(idesc), "r"(accumulate)
+                     : "memory");
+    else
+        asm volatile("{\n" QADC_ELECT_PRED "setp.ne.b32 p, %5, 0;\n@q tcgen05.mma.sp.cta_group::1.kind::i8 [%0], %1, %2, [%3], %4, p;\n}\n" ::"r"(
+                         d_tmem),
+                     "l"(a), "l"(b), "r"(e_tmem), "r"(idesc), "r"(accumulate)
+                     : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+    if constexpr (PAIR)
+        asm volatile("{\n" QADC_ELECT_PRED
+                     "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+                         smem_u32(bar)),
+                     "h"(uint16_t(3))
+                     : "memory");
+    else
+        asm volatile("{\n" QADC_ELECT_PRED "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                         smem_u32(bar))
+                     : "memory");
+}
 // ---- CTA pair plumbing: rank in the cluster, cluster-wide barrier, arrive on a barrier of the LEADER CTA (rank 0)
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
@@ -172,6 +220,14 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar, uint32_t rank 
 __device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
     const uint32_t addr = smem_u32(bar);
     uint32_t done;
+#if TC_SPIN
+    do { // non-blocking probe in a tight loop: lowest wake-up latency, costs issue slots
+        asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done)
+                     : "r"(addr), "r"(parity)
+                     : "memory");
+    } while (!done);
+#else
     do {
         asm volatile(
             "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\nselp.u32 %0, 1, 0, p;\n}\n"
@@ -179,6 +235,7 @@ __device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
             : "r"(addr), "r"(parity), "r"(TC_PARK_NS)
             : "memory");
     } while (!done);
+#endif
 }
 // the same for a barrier other CTAs of the cluster arrive on (kept apart so that its semantics can be changed in one place)
 __device__ __forceinline__ void mbar_wait_park_cluster(uint64_t* bar, uint32_t parity) {
@@ -258,6 +315,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     __shared__ __align__(8) uint64_t s_tload;                                // CTA pair: this CTA's half of the tile has landed
     __shared__ SubInfo s_info[TC_INFO];
     __shared__ uint32_t s_tmem;
+#ifdef TC_PROFILE
+    __shared__ long long s_stamp[3][8]; // per step (ring): MMAs committed | epilogue warp 0 past dfull | ... released the buffer
+#endif
 
     char* sB = smem;
     char* sAp = sB + TC_B_BYTES;
@@ -290,7 +350,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             mbar_init(&s_dempty[i], TC_EPI_WARPS * NCTA);
         }
         mbar_init(&s_tfull, 2); // the tile's expect_tx + the threshold rows' arrive (CTA pair: one arrive per CTA)
-        mbar_init(&s_tempty, 1);
+        mbar_init(&s_tempty, SP ? 2 : 1); // one commit per MMA warp
         mbar_init(&s_tload, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -508,8 +568,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 };
                 // sub-tiles go out in pairs: the store fences and the mbarrier hand-over are pure latency for a generator
                 // warp (one per scheduler), and with one pair of fences per two sub-tiles it keeps ahead of the sparse MMAs
-                for (uint32_t sub = 0; sub < n_sub; sub += 2, s += 2) {
-                    const bool two = sub + 1 < n_sub;
+                for (uint32_t sub = 0; sub < n_sub; sub += TC_GEN_GROUP, s += TC_GEN_GROUP) {
+                    const bool two = TC_GEN_GROUP == 2 && sub + 1 < n_sub;
                     emit(sub, s);
                     if (two) emit(sub + 1, s + 1);
                     TC_PROF(0);
@@ -525,7 +585,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         if (two) mbar_arrive_leader<PAIR>(&s_afull[(s + 1) % TC_NA], rank);
                     }
                     TC_PROF(4);
-                    if (!two) s -= 1; // (the loop adds 2)
+                    if (TC_GEN_GROUP == 2 && !two) s -= 1; // (the loop adds 2)
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[b]); // this warp is done with the code stage
@@ -536,11 +596,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             printf("tc-prof gen: subtiles %u total %lld | work %lld wait-codes %lld wait-aempty %lld wait-st %lld fence+arrive %lld (cycles per sub-tile: %lld)\n",
                    s, clock64() - prof_start, prof_t[0], prof_t[1], prof_t[2], prof_t[3], prof_t[4], (clock64() - prof_start) / s);
 #endif
-    } else if (warp == TC_MMA_WARP && rank == 0) {
-        // ============================ MMA issuer (CTA pair: the leader's, for both CTAs) =======================
+    } else if ((warp == TC_MMA_WARP || (SP && warp == TC_MMA_WARP2)) && rank == 0) {
+        // ============================ MMA issuers (CTA pair: the leader's, for both CTAs) ======================
+        // Two warps, one per accumulator buffer (even / odd steps).  A single issuer spends ~570 cycles per step outside
+        // the MMAs themselves (barrier waits, fences, the commits, the compiler's elect loops around every uniform-datapath
+        // instruction) while the tensor queue holds only a few MMAs: measured, the pipe idled 44 % of the time.  With two
+        // issuers one's bookkeeping overlaps the other's MMAs; tcgen05.commit tracks the issuing thread's own MMAs, which is
+        // exactly the per-buffer completion the barriers need.
+        const uint32_t my_buf = warp == TC_MMA_WARP ? 0u : 1u;
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0), dbg_u = __shfl_sync(0xffffffffu, dbg, 0);
         uint32_t s = 0, tseq = 0, prev_rb = 0xFFFFFFFFu, prev_nr = 0;
         const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB), ap_base = smem_u32(sAp);
         TC_PROF_DECL(3);
+#ifdef TC_PROFILE
+        long long lat_rel = 0, t_mma = 0, t_commit = 0;
+#endif
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
             const ScanJob job = a->jobs[ji];
             if (job.n_codes == 0 || job.n_rows == 0) continue;
@@ -556,6 +626,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             const uint32_t n_sub = job_subtiles(job.n_codes, TC_STEP);
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
                 const uint32_t sa = s % TC_NA, buf = s & 1u;
+                if (SP && buf != my_buf) continue; // (dense: one issuer -- alternating accumulators per MMA cost it 10 %)
                 TC_PROF(0);
                 if constexpr (PAIR) mbar_wait_park_cluster(&s_afull[sa], (s / TC_NA) & 1u);
                 else mbar_wait_park(&s_afull[sa], (s / TC_NA) & 1u);
@@ -563,35 +634,59 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 if constexpr (PAIR) mbar_wait_park_cluster(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
                 else mbar_wait_park(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
                 TC_PROF(2);
+#ifdef TC_PROFILE
+                if (lane == 0 && s >= 2) { lat_rel += clock64() - s_stamp[2][(s - 2) & 7u]; }
+#endif
                 tc_fence_after();
-                if (lane == 0) {
+                if constexpr (SP) {
+                    // converged issue (see umma_*_elect): sa / buf come from the loop counter of a uniform loop, and the shuffle
+                    // tells the compiler so
+                    const uint32_t sa_u = __shfl_sync(0xffffffffu, sa, 0), buf_u = __shfl_sync(0xffffffffu, buf, 0);
+                    const uint32_t d = tmem_u + buf_u * TC_TQ;
+                    const uint32_t a0 = a_base + sa_u * TC_A_BYTES;
+#ifdef TC_PROFILE
+                    const long long t_m0 = clock64();
+#endif
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) // four 2:4-sparse MMAs of 64 logical K (= four tables) each
+                        if (ks == 0 || !(dbg_u & 4u))
+                            umma_i8_sp_elect<PAIR>(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
+                                                   umma_desc(b_base + ks * 4 * TC_B_CHUNK, TC_B_CHUNK, 128),
+                                                   tmem_u + TC_ECOL + sa_u * 8 + 2 * ks, TC_IDESC_SP, ks > 0);
+                    if (!(dbg_u & 32u)) // (timing experiment: no threshold step)
+                        umma_i8_elect<PAIR>(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128),
+                                            TC_IDESC, 1u);
+#ifdef TC_PROFILE
+                    const long long t_c0 = clock64();
+                    t_mma += t_c0 - t_m0;
+#endif
+                    umma_commit_elect<PAIR>(&s_aempty[sa_u]); // the one-hot stage is free once these MMAs have read it
+                    umma_commit_elect<PAIR>(&s_dfull[buf_u]); // ... and the accumulator is complete
+#ifdef TC_PROFILE
+                    if (lane == 0) {
+                        s_stamp[0][s & 7u] = clock64();
+                        t_commit += s_stamp[0][s & 7u] - t_c0;
+                    }
+#endif
+                } else if (lane == 0) {
                     const uint32_t d = tmem + buf * TC_TQ;
                     const uint32_t a0 = a_base + sa * TC_A_BYTES;
-                    if constexpr (SP) {
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) // four 2:4-sparse MMAs of 64 logical K (= four tables) each
-                            if (ks == 0 || !(dbg & 4u))
-                                umma_i8_sp<PAIR>(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
-                                           umma_desc(b_base + ks * 4 * TC_B_CHUNK, TC_B_CHUNK, 128), tmem + TC_ECOL + sa * 8 + 2 * ks,
-                                           TC_IDESC_SP, ks > 0);
-                    } else {
-#pragma unroll
-                        for (int ks = 0; ks < TC_KC / 2; ++ks)
-                            if (ks == 0 || !(dbg & 4u))
-                                umma_i8(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
-                                        umma_desc(b_base + ks * 2 * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, ks > 0);
-                    }
-                    umma_i8<PAIR>(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, 1u);
-                    umma_commit<PAIR>(&s_aempty[sa]); // the one-hot stage is free once these MMAs have read it
-                    umma_commit<PAIR>(&s_dfull[buf]); // ... and the accumulator is complete
+                    for (int ks = 0; ks < TC_KC / 2; ++ks)
+                        if (ks == 0 || !(dbg & 4u))
+                            umma_i8(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
+                                    umma_desc(b_base + ks * 2 * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, ks > 0);
+                    umma_i8(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128), TC_IDESC, 1u);
+                    umma_commit(&s_aempty[sa]); // the one-hot stage is free once these MMAs have read it
+                    umma_commit(&s_dfull[buf]); // ... and the accumulator is complete
                 }
                 __syncwarp();
             }
         }
 #ifdef TC_PROFILE
-        if (blockIdx.x == 0 && lane == 0 && s > 2000)
-            printf("tc-prof mma: subtiles %u total %lld | issue %lld wait-afull %lld wait-dempty %lld\n", s, clock64() - prof_start,
-                   prof_t[0], prof_t[1], prof_t[2]);
+        if (blockIdx.x == 0 && lane == 0 && s > 2000 && my_buf == 0)
+            printf("tc-prof mma: subtiles %u total %lld | issue %lld (the MMAs %lld, the commits %lld) wait-afull %lld wait-dempty %lld | release(s-2) -> past dempty(s) %lld\n", s,
+                   clock64() - prof_start, prof_t[0], t_mma, t_commit, prof_t[1], prof_t[2], lat_rel);
 #endif
     } else if (warp < TC_EPI_WARPS) {
         // ============================ epilogue: TMEM -> sign test -> exact admission ==========================
@@ -604,6 +699,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         uint32_t* wq_row = s_wq_row + warp * TC_WQ_CAP;
         uint32_t qn = 0; // warp-uniform fill level of the queue
         TC_PROF_DECL(3);
+#ifdef TC_PROFILE
+        long long lat_wake = 0, lat_read = 0;
+#endif
         const uint32_t lt_mask = (1u << lane) - 1u;
         auto drain = [&]() { // 32 admissions in flight at once (the atomics' round trips overlap)
             __syncwarp();
@@ -630,6 +728,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 TC_PROF(0);
                 mbar_wait_park(&s_dfull[buf], (s >> 1) & 1u);
                 TC_PROF(1);
+#ifdef TC_PROFILE
+                if (tid == 0) { s_stamp[1][s & 7u] = clock64(); lat_wake += s_stamp[1][s & 7u] - s_stamp[0][s & 7u]; }
+#endif
                 tc_fence_after();
                 const SubInfo inf = s_info[slot];
                 const bool valid = rowi < inf.n_valid;
@@ -648,6 +749,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_leader<PAIR>(&s_dempty[buf], rank);
+#ifdef TC_PROFILE
+                    if (tid == 0) { s_stamp[2][s & 7u] = clock64(); lat_read += s_stamp[2][s & 7u] - s_stamp[1][s & 7u]; }
+#endif
                     uint32_t g[4]; // OR of each group of 16 registers = 32 columns (four independent chains)
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -730,8 +834,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         if (qn) drain();
 #ifdef TC_PROFILE
         if (blockIdx.x == 0 && tid == 0 && s > 2000)
-            printf("tc-prof epi: subtiles %u total %lld | work %lld wait-dfull %lld tmem-load %lld\n", s, clock64() - prof_start, prof_t[0],
-                   prof_t[1], prof_t[2]);
+            printf("tc-prof epi: subtiles %u total %lld | work %lld wait-dfull %lld tmem-load %lld | commit(s) -> past dfull(s) %lld, -> released %lld\n", s,
+                   clock64() - prof_start, prof_t[0], prof_t[1], prof_t[2], lat_wake, lat_read);
 #endif
     }
     tc_fence_before();
