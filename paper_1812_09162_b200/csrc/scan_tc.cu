@@ -26,10 +26,12 @@
 //     re-evaluated in integers from the reference-order table (exact_admit_ct, scan_common.cuh).  The sign test never
 //     drops a pair the exact test would admit, so results are exact by construction, as in scan.cu.
 //   * Warp roles: 0-7 epilogue (TMEM lane quadrant = warp id % 4, column half = warp id / 4), 8-11 one-hot
-//     generators, 12 MMA issuer (one elected lane; also owns the TMEM allocation), 13 producer (TMA code stream, tile
-//     loads, threshold rows).  All hand-offs are mbarriers; tcgen05.commit releases the one-hot stages and publishes
-//     the accumulators.  (Four epilogue warps were the bottleneck of the first version: 1970 cycles per sub-tile
-//     against 1205 of MMA, and the two did not overlap.)
+//     generators, 12 and 14 MMA issuers (sparse forms: one per accumulator buffer; 12 also owns the TMEM allocation),
+//     13 producer (TMA code stream, tile loads, threshold rows).  All hand-offs are mbarriers; tcgen05.commit releases
+//     the one-hot stages and publishes the accumulators.  (Four epilogue warps were the bottleneck of the first
+//     version: 1970 cycles per sub-tile against 1205 of MMA, and the two did not overlap.)
+//   * Three instantiations: dense (variant 12), 2:4 sparse (13: compressed one-hot + metadata in TMEM, 240-query
+//     tiles), and the sparse form on CTA pairs (14: cta_group::2, M = 256, each SM holds half of the tile's tables).
 // The operand layouts, the instruction descriptor and TS/SS modes were pinned against a CPU reference on the B200 by
 // tools/umma_probe.cu before this kernel relied on them.
 #include "scan_common.cuh"
