@@ -773,9 +773,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         // thr < q_max: unsaturated), so the CandidateHeap::push test (heap.hpp:46-47) only needs the tile's
                         // threshold key from shared memory.  Admitted keys go through a per-warp queue.
                         uint32_t m[4] = {0u, 0u, 0u, 0u};
+                        uint32_t gany = 0; // groups flagged anywhere in the warp (warp-uniform)
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             if (__any_sync(0xffffffffu, valid && g[k] != 0u)) {
+                                gany |= 1u << k;
 #pragma unroll
                                 for (int i = 0; i < 16; ++i) {
                                     const uint32_t x = i == 15 ? v[16 * k + i] : (v[16 * k + i] >> (15 - i));
@@ -789,7 +791,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         // ONE copy of the column loop (the switch inside pick64 is ~200 instructions; sixteen inlined
                         // copies of it thrashed the instruction cache)
 #pragma unroll 1
-                        for (uint32_t hh = 0; hh < 4; ++hh) {
+                        for (; gany; gany &= gany - 1u) { // only the flagged groups (usually one)
+                            const uint32_t hh = uint32_t(__ffs(gany) - 1);
                             const uint32_t mine = hh == 0 ? m[0] : hh == 1 ? m[1] : hh == 2 ? m[2] : m[3];
                             uint32_t u = __reduce_or_sync(0xffffffffu, mine);
                             while (u) {
