@@ -80,9 +80,10 @@ constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13, TC_MMA_WARP2 = 14;
 constexpr int TC_THREADS = 15 * 32;
 constexpr int TC_WQ_CAP = 64;          // per-epilogue-warp queue of admitted (key, row) pairs
+constexpr int TC_DUMP_BYTES = 16 * 32 * 4; // sparse forms: per-epilogue-warp scratch for one flagged group of 16 registers x 32 lanes
 __host__ __device__ constexpr int tc_smem(bool sp, bool pair = false) {
     return tc_b_bytes(sp, pair) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8 +
-           TC_TKBUF * 256 * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12;
+           TC_TKBUF * 256 * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12 + (sp ? TC_EPI_WARPS * TC_DUMP_BYTES : 0);
 }
 
 struct SubInfo {
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     uint64_t* s_tk = reinterpret_cast<uint64_t*>(info_codes + TC_INFO * TC_SUB); // [TC_TKBUF][TC_TQ] threshold keys per tile
     uint64_t* s_wq_key = s_tk + TC_TKBUF * 256;                                    // [TC_EPI_WARPS][TC_WQ_CAP]
     uint32_t* s_wq_row = reinterpret_cast<uint32_t*>(s_wq_key + TC_EPI_WARPS * TC_WQ_CAP);
+    uint4* s_dump = reinterpret_cast<uint4*>(s_wq_row + TC_EPI_WARPS * TC_WQ_CAP); // (sparse forms only) [TC_EPI_WARPS][4][32]
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // CTA pair: both CTAs walk the same jobs; rank r generates, holds and post-processes the r-th 128 codes of every step
@@ -795,10 +797,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             const uint32_t hh = uint32_t(__ffs(gany) - 1);
                             const uint32_t mine = hh == 0 ? m[0] : hh == 1 ? m[1] : hh == 2 ? m[2] : m[3];
                             uint32_t u = __reduce_or_sync(0xffffffffu, mine);
+                            uint4* dump = s_dump + warp * (TC_DUMP_BYTES / 16);
+                            if constexpr (SP) {
+                                // registers cannot be indexed dynamically: the flagged group's 16 registers go to this warp's
+                                // scratch ([quad of registers][lane]: conflict-free 16-byte stores) and are read back by index
+                                // (each lane reads only what it wrote).  The 64-way switch this replaces is 2 KB of rarely
+                                // executed code, i.e. instruction-cache misses every time the path is taken.
+                                switch (hh) {
+#define QADC_DUMP16(k0)                                                                              \
+    dump[0 * 32 + lane] = make_uint4(v[k0 + 0], v[k0 + 1], v[k0 + 2], v[k0 + 3]);                    \
+    dump[1 * 32 + lane] = make_uint4(v[k0 + 4], v[k0 + 5], v[k0 + 6], v[k0 + 7]);                    \
+    dump[2 * 32 + lane] = make_uint4(v[k0 + 8], v[k0 + 9], v[k0 + 10], v[k0 + 11]);                  \
+    dump[3 * 32 + lane] = make_uint4(v[k0 + 12], v[k0 + 13], v[k0 + 14], v[k0 + 15]);
+                                case 0: QADC_DUMP16(0) break;
+                                case 1: QADC_DUMP16(16) break;
+                                case 2: QADC_DUMP16(32) break;
+                                default: QADC_DUMP16(48) break;
+#undef QADC_DUMP16
+                                }
+                            }
                             while (u) {
                                 const uint32_t b = uint32_t(__ffs(u) - 1);
                                 u &= u - 1;
-                                const uint32_t raw = pick64(v, hh * 16 + (b & 15u)); // columns 2i (low half) and 2i + 1
+                                uint32_t raw; // columns 2i (low half) and 2i + 1
+                                if constexpr (SP) raw = reinterpret_cast<const uint32_t*>(dump + ((b & 15u) >> 2) * 32 + lane)[b & 3u];
+                                else raw = pick64(v, hh * 16 + (b & 15u));
                                 const uint32_t val = (b >> 4) ? uint32_t(int(raw) >> 16) : uint32_t(int(raw << 16) >> 16);
                                 const uint32_t col = c0 + hh * 32 + 2 * (b & 15u) + (b >> 4);
                                 uint64_t key = 0;
