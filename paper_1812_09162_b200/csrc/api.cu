@@ -232,6 +232,7 @@ struct qadc_index {
     uint32_t cand_cap = 8192;
     uint32_t seg0 = 4096;
     uint32_t seg_growth = 8;
+    uint32_t seg_growth_pct = 0; // experiment: non-integer growth of the flat schedule, in percent (0 = use seg_growth)
     bool seg_growth_set = false; // set_option("seg_growth") was called: the per-variant default below no longer applies
     int force_variant = -1;
     uint32_t tc_debug = 0; // timing experiments on the tensor-core scan (results are wrong when non-zero)
@@ -282,14 +283,16 @@ static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true, uint32_t
 
 // Geometric segment schedule: after n codes the R-th best of n bounds the admission
 // rate of the next codes by R/n, so each segment admits O(R * growth) candidates.
-static std::vector<uint64_t> segment_bounds(uint64_t count, uint64_t seg0, uint64_t growth) {
+// (growth in percent: 200 = every segment twice as long as the one before; lengths stay multiples of 256 codes)
+static std::vector<uint64_t> segment_bounds(uint64_t count, uint64_t seg0, uint64_t growth, uint64_t growth_pct = 0) {
     std::vector<uint64_t> b{0};
     uint64_t len = std::max<uint64_t>(seg0, 256);
+    const uint64_t pct = growth_pct ? std::max<uint64_t>(growth_pct, 110) : std::max<uint64_t>(growth, 2) * 100;
     while (b.back() < count) {
         uint64_t next = std::min(count, b.back() + len);
         if (count - next < len / 2) next = count; // do not leave a tiny tail segment
         b.push_back(next);
-        len *= std::max<uint64_t>(growth, 2);
+        len = (len * pct / 100 + 255) / 256 * 256;
     }
     return b;
 }
@@ -348,7 +351,7 @@ static bool scan_select_flat(qadc_index* h, const ScanPlan& plan, const uint8_t*
     // kernel (hit path per flagged column vs a ballot), so it prefers more, smaller segments -- fewer candidates per
     // query between two threshold updates (C4: x8 332 ms, x4 320, x3 316, x2 315 per step)
     const uint32_t growth = (is_tc8(plan.variant) && !h->seg_growth_set) ? 2u : h->seg_growth;
-    std::vector<uint64_t> bounds = segment_bounds(count - head, uint64_t(h->seg0) * growth, growth);
+    std::vector<uint64_t> bounds = segment_bounds(count - head, uint64_t(h->seg0) * growth, growth, h->seg_growth_pct);
     for (auto& b : bounds) b += head;
     std::vector<ScanJob> jobs;
     std::vector<std::pair<size_t, size_t>> seg_jobs;
@@ -1383,6 +1386,7 @@ int qadc_set_option(qadc_index* h, const char* name, int64_t value) {
         const std::string n(name);
         if (n == "cand_cap") h->cand_cap = uint32_t(std::max<int64_t>(value, 16));
         else if (n == "seg0") h->seg0 = uint32_t(std::min<int64_t>(std::max<int64_t>(value, 256), 16384)) / 16u * 16u; // bulk copies: 16-byte aligned
+        else if (n == "seg_growth_pct") h->seg_growth_pct = uint32_t(std::max<int64_t>(value, 0));
         else if (n == "seg_growth") {
             h->seg_growth = uint32_t(std::max<int64_t>(value, 2));
             h->seg_growth_set = true;
