@@ -269,7 +269,7 @@ static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true, uint32_t
             // 2e8 243.0 vs 253.7 -- the pair's hand-overs cross SMs, which only pays once segments are long)
             const uint64_t t_dense = (nq + 255) / 256, t_sparse = (nq + 239) / 240;
             const bool sparse = t_sparse * 5 <= t_dense * 6;
-            const int v = !sparse ? int(VAR_TC8) : h->count >= 60000000ull ? int(VAR_TC8P) : int(VAR_TC8S);
+            const int v = !sparse ? int(VAR_TC8) : (h->count >= 60000000ull && nq > 240) ? int(VAR_TC8P) : int(VAR_TC8S);
             ScanPlan p = plan_scan(h->ds, h->device, v, true);
             p.filter_shift = h->tc_debug;
             return p;

@@ -128,8 +128,9 @@ inline bool is_tc8(int variant) { return variant == VAR_TC8 || variant == VAR_TC
 inline int tc8_mode(int variant) { return variant - int(VAR_TC8); } // 0 dense, 1 sparse, 2 sparse on CTA pairs
 uint32_t scan_tc8_smem_bytes(int mode);
 uint32_t scan_tc8_tile_rows(int mode);
+uint32_t scan_tc8_pack_rows(int mode);
 void launch_scan_tc8(int mode, const DevSpec& ds, const ScanArgs& args, int grid, cudaStream_t stream);
-void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream);
+void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, uint32_t images_per_tile, void* out, cudaStream_t stream);
 
 // ---- LUT / calibration / quantization (lut.cu) ----
 struct LutArgs {

@@ -81,9 +81,13 @@ constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13, TC_MMA_WARP
 constexpr int TC_THREADS = 15 * 32;
 constexpr int TC_WQ_CAP = 64;          // per-epilogue-warp queue of admitted (key, row) pairs
 constexpr int TC_DUMP_BYTES = 16 * 32 * 4; // sparse forms: per-epilogue-warp scratch for one flagged group of 16 registers x 32 lanes
+// query tiles per job: the CTA-pair form keeps TWO tiles' tables resident (its B halves are small enough) and runs every
+// one-hot stage against both, one tile per accumulator buffer -- half the generator work, stores and hand-overs per pair
+__host__ __device__ constexpr int tc_nt(bool pair) { return pair ? 2 : 1; }
 __host__ __device__ constexpr int tc_smem(bool sp, bool pair = false) {
-    return tc_b_bytes(sp, pair) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES + TC_INFO * TC_SUB * 8 +
-           TC_TKBUF * 256 * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12 + (sp ? TC_EPI_WARPS * TC_DUMP_BYTES : 0);
+    return tc_nt(pair) * tc_b_bytes(sp, pair) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES +
+           TC_INFO * TC_SUB * 8 + TC_TKBUF * tc_nt(pair) * 256 * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12 +
+           (sp ? TC_EPI_WARPS * TC_DUMP_BYTES : 0);
 }
 
 struct SubInfo {
@@ -308,6 +312,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     constexpr uint32_t TC_IDESC = tc_idesc(SP, false, PAIR), TC_IDESC_SP = tc_idesc(SP, true, PAIR);
     constexpr uint32_t TC_STEP = PAIR ? 2 * TC_SUB : TC_SUB; // codes per MMA step of the CTA (pair)
     constexpr uint32_t NCTA = PAIR ? 2 : 1;
+    constexpr uint32_t NT = tc_nt(PAIR);          // query tiles per job = consumers of one one-hot stage
+    constexpr uint32_t TK_STRIDE = NT * 256;      // threshold keys per s_tk slot
     extern __shared__ __align__(1024) char smem[];
     __shared__ DevSpec s_ds;
     __shared__ ScanArgs s_args;
@@ -323,12 +329,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
 #endif
 
     char* sB = smem;
-    char* sAp = sB + TC_B_BYTES;
+    char* sAp = sB + NT * TC_B_BYTES;
     char* sA = sAp + TC_AP_BYTES;
     char* stage = sA + TC_NA * TC_A_BYTES;
     uint2* info_codes = reinterpret_cast<uint2*>(stage + TC_NSTAGE * TC_STAGE_BYTES);
     uint64_t* s_tk = reinterpret_cast<uint64_t*>(info_codes + TC_INFO * TC_SUB); // [TC_TKBUF][TC_TQ] threshold keys per tile
-    uint64_t* s_wq_key = s_tk + TC_TKBUF * 256;                                    // [TC_EPI_WARPS][TC_WQ_CAP]
+    uint64_t* s_wq_key = s_tk + TC_TKBUF * TK_STRIDE;                              // [TC_EPI_WARPS][TC_WQ_CAP]
     uint32_t* s_wq_row = reinterpret_cast<uint32_t*>(s_wq_key + TC_EPI_WARPS * TC_WQ_CAP);
     uint4* s_dump = reinterpret_cast<uint4*>(s_wq_row + TC_EPI_WARPS * TC_WQ_CAP); // (sparse forms only) [TC_EPI_WARPS][4][32]
 
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         }
         for (int i = 0; i < TC_NA; ++i) {
             mbar_init(&s_afull[i], 4 * NCTA);
-            mbar_init(&s_aempty[i], 1);
+            mbar_init(&s_aempty[i], NT); // one commit per consumer of the stage
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_dfull[i], 1);
@@ -394,12 +400,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 prev_nr = job.n_rows;
                 mbar_wait_park(&s_tempty, (tseq & 1u) ^ 1u); // the MMAs of the previous tile are done with B
                 if (lane == 0) {
-                    if constexpr (PAIR) { // this CTA's rows of every K chunk: 16 pieces of the [kc][TQ rows][16 B] image
-                        const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / TC_TQ) * (TC_KC * TC_TQ * 16) +
-                                          size_t(rank) * TC_B_CHUNK;
-                        mbar_expect_tx(&s_tload, TC_KC * TC_B_CHUNK);
-                        for (uint32_t kc = 0; kc < uint32_t(TC_KC); ++kc)
-                            bulk_g2s(sB + kc * TC_B_CHUNK, src + size_t(kc) * (TC_TQ * 16), TC_B_CHUNK, &s_tload);
+                    if constexpr (PAIR) { // this CTA's rows of every K chunk: 16 pieces of each [kc][TQ rows][16 B] image
+                        mbar_expect_tx(&s_tload, NT * TC_KC * TC_B_CHUNK);
+                        for (uint32_t ti = 0; ti < NT; ++ti) {
+                            const char* src = reinterpret_cast<const char*>(a->tile_lut) +
+                                              size_t(job.row_begin / TC_TQ + ti) * (TC_KC * TC_TQ * 16) + size_t(rank) * TC_B_CHUNK;
+                            for (uint32_t kc = 0; kc < uint32_t(TC_KC); ++kc)
+                                bulk_g2s(sB + ti * TC_B_BYTES + kc * TC_B_CHUNK, src + size_t(kc) * (TC_TQ * 16), TC_B_CHUNK, &s_tload);
+                        }
                     } else {
                         const char* src = reinterpret_cast<const char*>(a->tile_lut) + size_t(job.row_begin / TC_TQ) * (TC_KC * TC_B_CHUNK);
                         mbar_expect_tx(&s_tfull, TC_KC * TC_B_CHUNK);
@@ -408,8 +416,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     }
                 }
                 // threshold K step: row r gets 32 signed bytes that sum to v
-                uint64_t* tkb = s_tk + (tseq % TC_TKBUF) * 256;
-                for (uint32_t r = lane; r < uint32_t(TC_TQ); r += 32) {
+                uint64_t* tkb = s_tk + (tseq % TC_TKBUF) * TK_STRIDE;
+                for (uint32_t r = lane; r < NT * uint32_t(TC_TQ); r += 32) {
                     int v = 4064; // padding rows never admit
                     uint64_t tk_row = KEY_INF;
                     if (r < job.n_rows) {
@@ -437,9 +445,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         }
                         w[k] = word;
                     }
-                    if (PAIR && r / uint32_t(TC_BROWS) != rank) continue; // (the keys above are kept for the whole tile)
-                    const uint32_t rl = PAIR ? r % uint32_t(TC_BROWS) : r;
-                    char* dst = sB + TC_KC * TC_B_CHUNK + (rl >> 3) * 128 + (rl & 7u) * 16;
+                    const uint32_t ti = r / uint32_t(TC_TQ), rr = r - ti * uint32_t(TC_TQ); // tile of the job, row of the tile
+                    if (PAIR && rr / uint32_t(TC_BROWS) != rank) continue; // (the keys above are kept for the whole tile)
+                    const uint32_t rl = PAIR ? rr % uint32_t(TC_BROWS) : rr;
+                    char* dst = sB + ti * TC_B_BYTES + TC_KC * TC_B_CHUNK + (rl >> 3) * 128 + (rl & 7u) * 16;
                     *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
                     *reinterpret_cast<uint4*>(dst + TC_B_CHUNK) = make_uint4(w[4], w[5], w[6], w[7]);
                 }
@@ -627,13 +636,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 else mbar_wait_park(&s_tfull, tseq & 1u);
                 ++tseq;
             }
-            const uint32_t n_sub = job_subtiles(job.n_codes, TC_STEP);
+            // s counts UNITS = (step, tile of the job): accumulator buffer = s & 1 (NT = 2: the tile; NT = 1: step parity)
+            const uint32_t n_sub = job_subtiles(job.n_codes, TC_STEP) * NT;
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
-                const uint32_t sa = s % TC_NA, buf = s & 1u;
+                const uint32_t sa = (s / NT) % TC_NA, buf = s & 1u;
                 if (SP && buf != my_buf) continue; // (dense: one issuer -- alternating accumulators per MMA cost it 10 %)
                 TC_PROF(0);
-                if constexpr (PAIR) mbar_wait_park_cluster(&s_afull[sa], (s / TC_NA) & 1u);
-                else mbar_wait_park(&s_afull[sa], (s / TC_NA) & 1u);
+                if constexpr (PAIR) mbar_wait_park_cluster(&s_afull[sa], ((s / NT) / TC_NA) & 1u);
+                else mbar_wait_park(&s_afull[sa], ((s / NT) / TC_NA) & 1u);
                 TC_PROF(1);
                 if constexpr (PAIR) mbar_wait_park_cluster(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
                 else mbar_wait_park(&s_dempty[buf], ((s >> 1) & 1u) ^ 1u);
@@ -648,6 +658,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     const uint32_t sa_u = __shfl_sync(0xffffffffu, sa, 0), buf_u = __shfl_sync(0xffffffffu, buf, 0);
                     const uint32_t d = tmem_u + buf_u * TC_TQ;
                     const uint32_t a0 = a_base + sa_u * TC_A_BYTES;
+                    const uint32_t b0 = b_base + (NT == 2 ? buf_u * uint32_t(TC_B_BYTES) : 0u); // this unit's tile
 #ifdef TC_PROFILE
                     const long long t_m0 = clock64();
 #endif
@@ -655,10 +666,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     for (int ks = 0; ks < 4; ++ks) // four 2:4-sparse MMAs of 64 logical K (= four tables) each
                         if (ks == 0 || !(dbg_u & 4u))
                             umma_i8_sp_elect<PAIR>(d, umma_desc(a0 + ks * 2 * TC_A_CHUNK, TC_A_CHUNK, 128),
-                                                   umma_desc(b_base + ks * 4 * TC_B_CHUNK, TC_B_CHUNK, 128),
+                                                   umma_desc(b0 + ks * 4 * TC_B_CHUNK, TC_B_CHUNK, 128),
                                                    tmem_u + TC_ECOL + sa_u * 8 + 2 * ks, TC_IDESC_SP, ks > 0);
                     if (!(dbg_u & 32u)) // (timing experiment: no threshold step)
-                        umma_i8_elect<PAIR>(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b_base + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128),
+                        umma_i8_elect<PAIR>(d, umma_desc(ap_base, TC_A_CHUNK, 128), umma_desc(b0 + TC_KC * TC_B_CHUNK, TC_B_CHUNK, 128),
                                             TC_IDESC, 1u);
 #ifdef TC_PROFILE
                     const long long t_c0 = clock64();
@@ -726,9 +737,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         for (uint32_t ji = j_begin; ji < j_end; ++ji) {
             const ScanJob job = a->jobs[ji];
             if (job.n_codes == 0 || job.n_rows == 0) continue;
-            const uint32_t n_sub = job_subtiles(job.n_codes, TC_STEP);
+            const uint32_t n_sub = job_subtiles(job.n_codes, TC_STEP) * NT; // units, as in the MMA warps
             for (uint32_t k = 0; k < n_sub; ++k, ++s) {
-                const uint32_t buf = s & 1u, slot = s % TC_INFO;
+                const uint32_t buf = s & 1u, slot = (s / NT) % TC_INFO;
+                const uint32_t toff = NT == 2 ? buf * uint32_t(TC_TQ) : 0u; // first row of this unit's tile within the job
                 TC_PROF(0);
                 mbar_wait_park(&s_dfull[buf], (s >> 1) & 1u);
                 TC_PROF(1);
@@ -788,7 +800,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                 if (!valid) m[k] = 0u;
                             }
                         }
-                        const uint64_t* tks = s_tk + inf.tk_slot * 256;
+                        const uint64_t* tks = s_tk + inf.tk_slot * TK_STRIDE + toff;
                         const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, max(inf.n_valid, 1u) - 1u)] : uint32_t(inf.id_ref) + rowi;
                         // ONE copy of the column loop (the switch inside pick64 is ~200 instructions; sixteen inlined
                         // copies of it thrashed the instruction cache)
@@ -831,7 +843,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                     const uint32_t thr = uint32_t(tk >> 32);
                                     if (tk == KEY_INF || thr >= ds->qmax) {
                                         const uint2 code = info_codes[slot * TC_SUB + rowi];
-                                        tc_exact_admit(ds, a, code.x, code.y, inf.row_begin + col, id);
+                                        tc_exact_admit(ds, a, code.x, code.y, inf.row_begin + toff + col, id);
                                     } else {
                                         key = make_key(uint32_t(int(val) + int(thr) + 1), id);
                                         push = key < tk;
@@ -843,7 +855,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                     if (push) {
                                         const uint32_t e = qn + __popc(bal & lt_mask);
                                         wq_key[e] = key;
-                                        wq_row[e] = inf.row_begin + col;
+                                        wq_row[e] = inf.row_begin + toff + col;
                                     }
                                     qn += __popc(bal);
                                 }
@@ -907,11 +919,14 @@ __global__ void pack_tiles_tc8_kernel(const uint8_t* __restrict__ qlut, uint32_t
 
 // mode: 0 dense, 1 2:4-sparse, 2 2:4-sparse on CTA pairs
 uint32_t scan_tc8_smem_bytes(int mode) { return mode == 2 ? tc_smem(true, true) : mode == 1 ? tc_smem(true) : tc_smem(false); }
-uint32_t scan_tc8_tile_rows(int mode) { return tc_tq(mode != 0); }
+uint32_t scan_tc8_tile_rows(int mode) { return tc_tq(mode != 0) * tc_nt(mode == 2); } // rows of a JOB's tile (pair form: two images)
+uint32_t scan_tc8_pack_rows(int mode) { return tc_tq(mode != 0); }                     // rows of one packed tile image
 
-void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, void* out, cudaStream_t stream) {
+// `images_per_tile` consecutive images make one job tile: the image count is rounded up to a whole number of them
+void launch_pack_tiles_tc8(const void* qlut, uint32_t n_rows, uint32_t tq, uint32_t images_per_tile, void* out, cudaStream_t stream) {
     if (n_rows == 0) return;
-    pack_tiles_tc8_kernel<<<(n_rows + tq - 1) / tq, 256, 0, stream>>>(static_cast<const uint8_t*>(qlut), n_rows, tq,
+    const uint32_t images = ((n_rows + tq - 1) / tq + images_per_tile - 1) / images_per_tile * images_per_tile;
+    pack_tiles_tc8_kernel<<<images, 256, 0, stream>>>(static_cast<const uint8_t*>(qlut), n_rows, tq,
                                                                       tq == uint32_t(tc_tq(true)) ? 1u : 0u, static_cast<uint8_t*>(out));
     ++g_launches;
     QADC_CUDA_CHECK(cudaGetLastError());

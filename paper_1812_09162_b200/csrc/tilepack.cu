@@ -171,7 +171,7 @@ void launch_pack_tiles(ScanVariant v, uint32_t filter_shift, uint32_t pair, cons
     case VAR_TC8P:
         if (width != 8 || E != 256 || tq != scan_tc8_tile_rows(tc8_mode(v)))
             throw Error(QADC_ERR_CONFIG, "pack_tiles: the tensor-core layout is for 16x{4,4}");
-        launch_pack_tiles_tc8(qlut, n_rows, tq, out, stream);
+        launch_pack_tiles_tc8(qlut, n_rows, scan_tc8_pack_rows(tc8_mode(v)), tq / scan_tc8_pack_rows(tc8_mode(v)), out, stream);
         return;
     case VAR_F16X4H_C8Q: {
         if (width != 16 || (E != 512 && E != 576 && E != 384) || tq != 16)
