@@ -424,11 +424,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         const uint32_t row = job.row_begin + r;
                         const uint32_t q = a->row_query ? a->row_query[row] : row;
                         if (q != 0xFFFFFFFFu) {
-                            const uint64_t tk = a->thr_key[q];
-                            const uint32_t thr = uint32_t(tk >> 32);
+                            uint64_t tk = a->thr_key[q];
+                            uint32_t thr = uint32_t(tk >> 32);
                             const uint32_t bias = a->row_bias ? min(a->row_bias[row], ds->qmax) : 0u;
+                            // Ties cannot win where ids only grow: with implicit ids every code of this tile run has an id
+                            // >= job.id_base, and if that exceeds the id of the heap's worst entry, a sum EQUAL to the
+                            // threshold gives key > worst key -- CandidateHeap::push rejects it (heap.hpp:46-47).  The
+                            // effective threshold is then (thr - 1, any id): with 8-bit sums about half of the pairs at or
+                            // below the threshold sit exactly on it, and each would cost the epilogue an admission attempt.
+                            if (tk != KEY_INF && thr < ds->qmax && a->ids == nullptr && job.id_base > uint32_t(tk)) {
+                                if (thr == 0) {
+                                    tk = 0; // nothing is below a zero threshold: never admit (v stays at the padding value)
+                                } else {
+                                    thr -= 1;
+                                    tk = make_key(thr, 0xFFFFFFFFu);
+                                }
+                            }
                             tk_row = tk;
-                            if (tk == KEY_INF || thr >= ds->qmax) v = -4096; // heap not full / worst saturated: admit all
+                            if (tk == 0) v = 4064;
+                            else if (tk == KEY_INF || thr >= ds->qmax) v = -4096; // heap not full / worst saturated: admit all
                             else v = 2048 + int(bias) - int(thr) - 1;
                         }
                     }
