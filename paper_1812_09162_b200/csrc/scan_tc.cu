@@ -762,13 +762,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                 if (tid == 0) { s_stamp[1][s & 7u] = clock64(); lat_wake += s_stamp[1][s & 7u] - s_stamp[0][s & 7u]; }
 #endif
                 tc_fence_after();
-                const SubInfo inf = s_info[slot];
-                const bool valid = rowi < inf.n_valid;
                 if (!(dbg & 1u)) {
-                    // this warp's 128 queries of the tile, two 16-bit sums per register
+                    // this warp's 128 queries of the tile, two 16-bit sums per register (the sub-tile's info is fetched
+                    // while the tensor-memory load is in flight)
                     const uint32_t c0 = col_w;
                     uint32_t v[64];
                     tmem_ld128_pack16(tmem + buf * TC_TQ + lane_base + c0, v);
+                    const SubInfo inf = s_info[slot];
+                    const bool valid = rowi < inf.n_valid;
                     tmem_ld_wait();
                     TC_PROF(2);
                     if constexpr (SP) { // a warp owns 120 of the tile's 240 queries: the load's last 8 columns are not its own
