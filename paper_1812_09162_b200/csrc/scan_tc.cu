@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     __shared__ __align__(8) uint64_t s_tload;                                // CTA pair: this CTA's half of the tile has landed
     __shared__ SubInfo s_info[TC_INFO];
     __shared__ uint32_t s_tmem;
+    __shared__ uint32_t s_wqn[TC_EPI_WARPS]; // admission queues' fill levels while lanes push on their own
 #ifdef TC_PROFILE
     __shared__ long long s_stamp[3][8]; // per step (ring): MMAs committed | epilogue warp 0 past dfull | ... released the buffer
 #endif
@@ -801,6 +802,83 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         // instruction-cache misses).  The accumulator IS the exact sum (D = bias + sum - thr - 1 with
                         // thr < q_max: unsaturated), so the CandidateHeap::push test (heap.hpp:46-47) only needs the tile's
                         // threshold key from shared memory.  Admitted keys go through a per-warp queue.
+                        if constexpr (SP) {
+                            // LANE-LOCAL admission (sparse forms): every lane with flagged sums walks its own hits -- masks,
+                            // the group's registers through its own scratch slots, the threshold test -- with no votes or
+                            // reductions in the loop, and reserves queue slots with a shared-memory atomic.  (The warp-uniform
+                            // walk over the union of flagged columns below cost ~1000 cycles per visit.)
+                            uint32_t m[4];
+                            uint32_t todo = 0;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                m[k] = 0u;
+                                if (valid && g[k] != 0u) {
+#pragma unroll
+                                    for (int i = 0; i < 16; ++i) {
+                                        const uint32_t x = i == 15 ? v[16 * k + i] : (v[16 * k + i] >> (15 - i));
+                                        m[k] |= x & (0x00010001u << i);
+                                    }
+                                    todo |= 1u << k;
+                                }
+                            }
+                            const uint64_t* tks = s_tk + inf.tk_slot * TK_STRIDE + toff;
+                            const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, max(inf.n_valid, 1u) - 1u)] : uint32_t(inf.id_ref) + rowi;
+                            uint4* dump = s_dump + warp * (TC_DUMP_BYTES / 16);
+                            uint32_t* wqn = &s_wqn[warp];
+                            if (lane == 0) *wqn = qn;
+                            __syncwarp();
+                            uint32_t mcur = 0, kcur = 0;
+                            for (;;) {
+                                bool blocked = false; // the queue is full: drain it (warp-wide) and come back
+                                while ((todo | mcur) != 0u && !blocked) {
+                                    if (mcur == 0u) { // open this lane's next flagged group: its 16 registers go to the scratch
+                                        kcur = uint32_t(__ffs(todo) - 1);
+                                        todo &= todo - 1u;
+                                        mcur = kcur == 0 ? m[0] : kcur == 1 ? m[1] : kcur == 2 ? m[2] : m[3];
+                                        switch (kcur) {
+#define QADC_DUMP16(k0)                                                                              \
+    dump[0 * 32 + lane] = make_uint4(v[k0 + 0], v[k0 + 1], v[k0 + 2], v[k0 + 3]);                    \
+    dump[1 * 32 + lane] = make_uint4(v[k0 + 4], v[k0 + 5], v[k0 + 6], v[k0 + 7]);                    \
+    dump[2 * 32 + lane] = make_uint4(v[k0 + 8], v[k0 + 9], v[k0 + 10], v[k0 + 11]);                  \
+    dump[3 * 32 + lane] = make_uint4(v[k0 + 12], v[k0 + 13], v[k0 + 14], v[k0 + 15]);
+                                        case 0: QADC_DUMP16(0) break;
+                                        case 1: QADC_DUMP16(16) break;
+                                        case 2: QADC_DUMP16(32) break;
+                                        default: QADC_DUMP16(48) break;
+#undef QADC_DUMP16
+                                        }
+                                    }
+                                    const uint32_t b = uint32_t(__ffs(mcur) - 1);
+                                    const uint32_t raw = reinterpret_cast<const uint32_t*>(dump + ((b & 15u) >> 2) * 32 + lane)[b & 3u];
+                                    const uint32_t val = (b >> 4) ? uint32_t(int(raw) >> 16) : uint32_t(int(raw << 16) >> 16);
+                                    const uint32_t col = c0 + kcur * 32 + 2 * (b & 15u) + (b >> 4);
+                                    const uint64_t tk = tks[col];
+                                    const uint32_t thr = uint32_t(tk >> 32);
+                                    if (tk == KEY_INF || thr >= ds->qmax) {
+                                        const uint2 code = info_codes[slot * TC_SUB + rowi];
+                                        tc_exact_admit(ds, a, code.x, code.y, inf.row_begin + toff + col, id);
+                                    } else {
+                                        const uint64_t key = make_key(uint32_t(int(val) + int(thr) + 1), id);
+                                        if (key < tk) {
+                                            const uint32_t e = atomicAdd(wqn, 1u);
+                                            if (e >= uint32_t(TC_WQ_CAP)) {
+                                                blocked = true; // (the bit stays set: retried after the drain)
+                                                continue;
+                                            }
+                                            wq_key[e] = key;
+                                            wq_row[e] = inf.row_begin + toff + col;
+                                        }
+                                    }
+                                    mcur &= mcur - 1u;
+                                }
+                                __syncwarp();
+                                qn = min(*wqn, uint32_t(TC_WQ_CAP));
+                                if (!__any_sync(0xffffffffu, (todo | mcur) != 0u)) break;
+                                drain();
+                                if (lane == 0) *wqn = 0u;
+                                __syncwarp();
+                            }
+                        } else {
                         uint32_t m[4] = {0u, 0u, 0u, 0u};
                         uint32_t gany = 0; // groups flagged anywhere in the warp (warp-uniform)
 #pragma unroll
@@ -876,6 +954,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                 }
                             }
                         }
+                        } // (dense form)
                     }
                 }
                 if (qn >= 32) drain();
