@@ -263,13 +263,14 @@ static ScanPlan plan_for(const qadc_index* h, bool allow_merged = true, uint32_t
     }
     if (force < 0 && allow_merged && h->kind == 0 && nq >= 96 && h->count >= (uint64_t(1) << 18)) {
         try {
-            // dense (256-query tiles) or 2:4 sparse (240-query tiles, a tile step costs ~4/5 of a dense one: 1040 vs 1309
-            // cycles per 128 codes measured on C4): whichever needs less tensor time for this batch.  From 8 Mi codes and
-            // more than one tile on, the sparse form runs on CTA pairs with two tiles per job (measured, 1e4 queries:
-            // 4e6 codes 11.46 vs 11.39 ms, 1.25e7 22.5 vs 23.0, 2.5e7 36.6 vs 38.4, 5e7 62.5 vs 68.2, 2e8 204 vs 242)
+            // dense (256-query tiles) or 2:4 sparse (240-query tiles; a tile step costs ~4/5 of a dense one -- C4 242 vs
+            // 305 ms -- and its admission path is the cheaper one): whichever needs less tensor time for this batch (C1, 1000
+            // queries: 5 sparse tiles 0.92 ms, 4 dense ones 1.10).  From 8 Mi codes and ten tiles on, the sparse form runs
+            // on CTA pairs with two tiles per job (measured, 1e4 queries: 4e6 codes 11.46 vs 11.39 ms, 1.25e7 22.5 vs 23.0,
+            // 2.5e7 36.6 vs 38.4, 5e7 62.5 vs 68.2, 2e8 204 vs 240; 2e7 codes x 2000 queries = 9 tiles: 7.26 vs 6.79)
             const uint64_t t_dense = (nq + 255) / 256, t_sparse = (nq + 239) / 240;
-            const bool sparse = t_sparse * 5 <= t_dense * 6;
-            const int v = !sparse ? int(VAR_TC8) : (h->count >= (8ull << 20) && nq > 240) ? int(VAR_TC8P) : int(VAR_TC8S);
+            const bool sparse = t_sparse * 4 <= t_dense * 5;
+            const int v = !sparse ? int(VAR_TC8) : (h->count >= (8ull << 20) && t_sparse >= 10) ? int(VAR_TC8P) : int(VAR_TC8S);
             ScanPlan p = plan_scan(h->ds, h->device, v, true);
             p.filter_shift = h->tc_debug;
             return p;
