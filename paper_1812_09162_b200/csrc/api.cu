@@ -351,7 +351,8 @@ static bool scan_select_flat(qadc_index* h, const ScanPlan& plan, const uint8_t*
     // growth of the segment schedule: an admitted pair costs the tensor-core scan far more than the shared-memory
     // kernel (hit path per flagged column vs a ballot), so it prefers more, smaller segments -- fewer candidates per
     // query between two threshold updates (C4: x8 332 ms, x4 320, x3 316, x2 315 per step)
-    const uint32_t growth = (is_tc8(plan.variant) && !h->seg_growth_set) ? 2u : h->seg_growth;
+    // (small searches are launch-latency bound and take x4: C1, 1e6 codes x 1e3 queries, 0.84 vs 0.92 ms; 4e6 x 1e4: 9.77 vs 9.42)
+    const uint32_t growth = (is_tc8(plan.variant) && !h->seg_growth_set) ? (uint64_t(nq) * count < 10000000000ull ? 4u : 2u) : h->seg_growth;
     std::vector<uint64_t> bounds = segment_bounds(count - head, uint64_t(h->seg0) * growth, growth, h->seg_growth_pct);
     for (auto& b : bounds) b += head;
     std::vector<ScanJob> jobs;
