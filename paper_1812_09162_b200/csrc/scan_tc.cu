@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     // MMA warp waits on (afull, dempty, tfull) live in the leader and count arrivals from both CTAs; barriers the tensor
     // core signals (aempty, dfull, tempty) exist in both CTAs and get multicast commits.
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    if (tid < uint32_t(TC_EPI_WARPS)) s_wqn[tid] = 0u;
     if (tid == 0) {
         s_ds = ds_param;
         s_args = args_param;
@@ -746,6 +747,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     else a->overflow[q] = 1u;
                 }
             }
+            if (lane == 0) s_wqn[warp] = 0u;
             __syncwarp();
             qn = 0;
         };
@@ -813,20 +815,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             for (int k = 0; k < 4; ++k) {
                                 m[k] = 0u;
                                 if (valid && g[k] != 0u) {
+                                    uint32_t part[4] = {0u, 0u, 0u, 0u}; // four short OR chains instead of one of sixteen
 #pragma unroll
                                     for (int i = 0; i < 16; ++i) {
                                         const uint32_t x = i == 15 ? v[16 * k + i] : (v[16 * k + i] >> (15 - i));
-                                        m[k] |= x & (0x00010001u << i);
+                                        part[i & 3] |= x & (0x00010001u << i);
                                     }
+                                    m[k] = (part[0] | part[1]) | (part[2] | part[3]);
                                     todo |= 1u << k;
                                 }
                             }
                             const uint64_t* tks = s_tk + inf.tk_slot * TK_STRIDE + toff;
                             const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, max(inf.n_valid, 1u) - 1u)] : uint32_t(inf.id_ref) + rowi;
                             uint4* dump = s_dump + warp * (TC_DUMP_BYTES / 16);
-                            uint32_t* wqn = &s_wqn[warp];
-                            if (lane == 0) *wqn = qn;
-                            __syncwarp();
+                            uint32_t* wqn = &s_wqn[warp]; // == qn here (kept in step by drain())
                             uint32_t mcur = 0, kcur = 0;
                             for (;;) {
                                 bool blocked = false; // the queue is full: drain it (warp-wide) and come back
@@ -872,11 +874,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                     mcur &= mcur - 1u;
                                 }
                                 __syncwarp();
-                                qn = min(*wqn, uint32_t(TC_WQ_CAP));
-                                if (!__any_sync(0xffffffffu, (todo | mcur) != 0u)) break;
+                                const uint32_t cnt = *wqn; // > capacity <=> some lane could not push and waits for a drain
+                                qn = min(cnt, uint32_t(TC_WQ_CAP));
+                                if (cnt <= uint32_t(TC_WQ_CAP)) break;
                                 drain();
-                                if (lane == 0) *wqn = 0u;
-                                __syncwarp();
                             }
                         } else {
                         uint32_t m[4] = {0u, 0u, 0u, 0u};
