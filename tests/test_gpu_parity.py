@@ -1033,6 +1033,37 @@ def test_every_scan_variant_is_exact(port, dims, text, variants):
         assert ran >= len(variants)  # the default plus all but at most one fallback must run
 
 
+@pytest.mark.parametrize("variant", [12, 13, 14])
+@pytest.mark.parametrize("distinct,r,cand_cap", [(40, 100, 0), (3, 257, 0), (500, 1000, 512)])
+def test_tensor_core_search_with_massive_ties(port, variant, distinct, r, cand_cap):
+    """Flat search through each tensor-core form over a list made of a handful of DISTINCT codes repeated -- every
+    quantized sum ties with thousands of others, so the result is decided by ids alone (heap.hpp:46-47).  Covers the
+    threshold rows that exclude ties where ids only grow, the lane-local admission queues (dense admissions, queue-full
+    retries) and, with a small candidate buffer, the overflow retry; 700 queries = a ragged last tile and, for the pair
+    form, an odd number of 240-query tiles (its second tile of the last job is half padding)."""
+    rng = np.random.default_rng(distinct * 7 + r)
+    dims, text = 64, "16x{4,4}"
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+    n, nq = 300_007, 700
+    pool = random_codes(s, distinct, seed=distinct)
+    codes = pool[rng.integers(0, distinct, size=n)]
+    pk = qb.pack_list(s, codes)
+    queries = (rng.standard_normal((nq, dims)) * 2).astype(np.float32)
+    want = port.flat_search(so, cb, pk, n, queries, r=r, t=max(r, 400), threads=8)
+    with qb.FlatIndex(s, cb, pk, n) as idx:
+        idx.set_option("force_variant", variant)
+        if cand_cap:
+            idx.set_option("cand_cap", cand_cap)
+        got = idx.search(queries, qb.SearchParams(r=r, t=max(r, 400)))
+        assert idx.stats().scan_variant == variant
+        if cand_cap:
+            assert idx.stats().overflow_retries >= 1
+    assert np.array_equal(got.ids, want[0])
+    assert bits_equal(got.dists, want[1])
+    assert np.array_equal(got.counts, want[2])
+
+
 @pytest.mark.parametrize("dims,text", [(128, "16x{4,4}"), (96, "12x{6,5,5}"), (64, "12x{6,6,4}"), (60, "12x{5,5,5}"),
                                        (64, "8x{8,8}"), (64, "8x{8}")])
 def test_randomised_search_parameters_vs_oracle(port, dims, text):
