@@ -728,6 +728,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         const uint32_t col_w = half_w * (TC_TQ / 2);
         uint64_t* wq_key = s_wq_key + warp * TC_WQ_CAP;
         uint32_t* wq_row = s_wq_row + warp * TC_WQ_CAP;
+        uint32_t* wq_id = reinterpret_cast<uint32_t*>(s_dump + warp * (TC_DUMP_BYTES / 16)); // (sparse forms) [TC_WQ_CAP]
         uint32_t qn = 0; // warp-uniform fill level of the queue
         TC_PROF_DECL(3);
 #ifdef TC_PROFILE
@@ -739,12 +740,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             for (uint32_t base = 0; base < qn; base += 32) {
                 const uint32_t e = base + lane;
                 if (e < qn) {
-                    const uint64_t key = wq_key[e];
-                    const uint32_t row = wq_row[e];
-                    const uint32_t q = a->row_query ? a->row_query[row] : row;
-                    const uint32_t at = atomicAdd(&a->cand_count[q], 1u);
-                    if (at < a->cap) a->cand[size_t(q) * a->cap + at] = key;
-                    else a->overflow[q] = 1u;
+                    if constexpr (SP) {
+                        // sparse forms: the queue holds COORDINATES (code, table row, id) of flagged pairs; the sum is
+                        // recomputed from the reference-order table -- 16 independent byte loads -- and goes through the
+                        // CandidateHeap::push test against the query's current key (exact_admit_ct, scan_common.cuh)
+                        const uint64_t code = wq_key[e];
+                        tc_exact_admit(ds, a, uint32_t(code), uint32_t(code >> 32), wq_row[e], wq_id[e]);
+                    } else {
+                        const uint64_t key = wq_key[e];
+                        const uint32_t row = wq_row[e];
+                        const uint32_t q = a->row_query ? a->row_query[row] : row;
+                        const uint32_t at = atomicAdd(&a->cand_count[q], 1u);
+                        if (at < a->cap) a->cand[size_t(q) * a->cap + at] = key;
+                        else a->overflow[q] = 1u;
+                    }
                 }
             }
             if (lane == 0) s_wqn[warp] = 0u;
@@ -825,52 +834,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                     todo |= 1u << k;
                                 }
                             }
-                            const uint64_t* tks = s_tk + inf.tk_slot * TK_STRIDE + toff;
+                            // the visit only queues coordinates: no accumulator value is needed again (drain() recomputes the
+                            // sum), so there is no register indexing, no threshold lookup and no compare on this path
                             const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, max(inf.n_valid, 1u) - 1u)] : uint32_t(inf.id_ref) + rowi;
-                            uint4* dump = s_dump + warp * (TC_DUMP_BYTES / 16);
+                            const uint2 code2 = info_codes[slot * TC_SUB + rowi];
+                            const uint64_t code = (uint64_t(code2.y) << 32) | code2.x;
+                            const uint32_t rowbase = inf.row_begin + toff + c0;
                             uint32_t* wqn = &s_wqn[warp]; // == qn here (kept in step by drain())
                             uint32_t mcur = 0, kcur = 0;
                             for (;;) {
                                 bool blocked = false; // the queue is full: drain it (warp-wide) and come back
                                 while ((todo | mcur) != 0u && !blocked) {
-                                    if (mcur == 0u) { // open this lane's next flagged group: its 16 registers go to the scratch
+                                    if (mcur == 0u) { // this lane's next flagged group
                                         kcur = uint32_t(__ffs(todo) - 1);
                                         todo &= todo - 1u;
                                         mcur = kcur == 0 ? m[0] : kcur == 1 ? m[1] : kcur == 2 ? m[2] : m[3];
-                                        switch (kcur) {
-#define QADC_DUMP16(k0)                                                                              \
-    dump[0 * 32 + lane] = make_uint4(v[k0 + 0], v[k0 + 1], v[k0 + 2], v[k0 + 3]);                    \
-    dump[1 * 32 + lane] = make_uint4(v[k0 + 4], v[k0 + 5], v[k0 + 6], v[k0 + 7]);                    \
-    dump[2 * 32 + lane] = make_uint4(v[k0 + 8], v[k0 + 9], v[k0 + 10], v[k0 + 11]);                  \
-    dump[3 * 32 + lane] = make_uint4(v[k0 + 12], v[k0 + 13], v[k0 + 14], v[k0 + 15]);
-                                        case 0: QADC_DUMP16(0) break;
-                                        case 1: QADC_DUMP16(16) break;
-                                        case 2: QADC_DUMP16(32) break;
-                                        default: QADC_DUMP16(48) break;
-#undef QADC_DUMP16
-                                        }
                                     }
                                     const uint32_t b = uint32_t(__ffs(mcur) - 1);
-                                    const uint32_t raw = reinterpret_cast<const uint32_t*>(dump + ((b & 15u) >> 2) * 32 + lane)[b & 3u];
-                                    const uint32_t val = (b >> 4) ? uint32_t(int(raw) >> 16) : uint32_t(int(raw << 16) >> 16);
-                                    const uint32_t col = c0 + kcur * 32 + 2 * (b & 15u) + (b >> 4);
-                                    const uint64_t tk = tks[col];
-                                    const uint32_t thr = uint32_t(tk >> 32);
-                                    if (tk == KEY_INF || thr >= ds->qmax) {
-                                        const uint2 code = info_codes[slot * TC_SUB + rowi];
-                                        tc_exact_admit(ds, a, code.x, code.y, inf.row_begin + toff + col, id);
-                                    } else {
-                                        const uint64_t key = make_key(uint32_t(int(val) + int(thr) + 1), id);
-                                        if (key < tk) {
-                                            const uint32_t e = atomicAdd(wqn, 1u);
-                                            if (e >= uint32_t(TC_WQ_CAP)) {
-                                                blocked = true; // (the bit stays set: retried after the drain)
-                                                continue;
-                                            }
-                                            wq_key[e] = key;
-                                            wq_row[e] = inf.row_begin + toff + col;
-                                        }
+                                    const uint32_t e = atomicAdd(wqn, 1u);
+                                    if (e >= uint32_t(TC_WQ_CAP)) {
+                                        blocked = true; // (the bit stays set: retried after the drain)
+                                        continue;
                                     }
+                                    wq_key[e] = code;
+                                    wq_row[e] = rowbase + kcur * 32 + 2 * (b & 15u) + (b >> 4);
+                                    wq_id[e] = id;
                                     mcur &= mcur - 1u;
                                 }
                                 __syncwarp();
