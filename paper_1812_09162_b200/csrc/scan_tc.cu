@@ -756,7 +756,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     }
                 }
             }
-            if (lane == 0) s_wqn[warp] = 0u;
             __syncwarp();
             qn = 0;
         };
@@ -804,7 +803,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         g[k] = o & 0x80008000u; // sign bits of the even / odd columns
                     }
                     const uint32_t any = g[0] | g[1] | g[2] | g[3];
-                    if (__any_sync(0xffffffffu, valid && any != 0u) && !(dbg & 8u)) {
+                    const uint32_t hit_lanes = __ballot_sync(0xffffffffu, valid && any != 0u);
+                    if (hit_lanes != 0u && !(dbg & 8u)) {
                         // rare (warp-uniform branch): some sums of this sub-tile are <= their query's threshold.  For each
                         // group of 32 columns that is flagged anywhere in the warp, all lanes turn their 32 sign bits into a
                         // mask (bit i = column 2i, bit 16 + i = column 2i + 1); the warp then walks the UNION of flagged
@@ -840,7 +840,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             const uint2 code2 = info_codes[slot * TC_SUB + rowi];
                             const uint64_t code = (uint64_t(code2.y) << 32) | code2.x;
                             const uint32_t rowbase = inf.row_begin + toff + c0;
-                            uint32_t* wqn = &s_wqn[warp]; // == qn here (kept in step by drain())
+                            uint32_t* wqn = &s_wqn[warp];
+                            // the common case -- ONE lane has flagged sums and they fit the queue: it takes the next slots
+                            // itself, no atomic and no round trip through shared memory for the fill level
+                            const uint32_t n_mine = uint32_t(__popc(m[0]) + __popc(m[1]) + __popc(m[2]) + __popc(m[3]));
+                            const uint32_t n_one = __shfl_sync(0xffffffffu, n_mine, __ffs(hit_lanes) - 1);
+                            if ((hit_lanes & (hit_lanes - 1u)) == 0u && qn + n_one <= uint32_t(TC_WQ_CAP)) {
+                                uint32_t e = qn;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    for (uint32_t mk = m[k]; mk != 0u; mk &= mk - 1u, ++e) {
+                                        const uint32_t b = uint32_t(__ffs(mk) - 1);
+                                        wq_key[e] = code;
+                                        wq_row[e] = rowbase + k * 32 + 2 * (b & 15u) + (b >> 4);
+                                        wq_id[e] = id;
+                                    }
+                                qn += n_one;
+                                __syncwarp();
+                            } else {
+                            if (lane == 0) *wqn = qn; // the shared fill level is only kept for this path
+                            __syncwarp();
                             uint32_t mcur = 0, kcur = 0;
                             for (;;) {
                                 bool blocked = false; // the queue is full: drain it (warp-wide) and come back
@@ -866,6 +885,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                 qn = min(cnt, uint32_t(TC_WQ_CAP));
                                 if (cnt <= uint32_t(TC_WQ_CAP)) break;
                                 drain();
+                                if (lane == 0) *wqn = 0u;
+                                __syncwarp();
+                            }
                             }
                         } else {
                         uint32_t m[4] = {0u, 0u, 0u, 0u};
