@@ -22,9 +22,10 @@
 //   * D (128 x 256 s32) lives in TMEM, two buffers of 256 columns; four epilogue warps read it back with tcgen05.ld
 //     (thread = code, 64 queries per load), OR the values and look at one sign bit per 64 pairs.  A flagged pair's
 //     accumulator is its exact sum; its (distance, id) key goes through the CandidateHeap::push test (heap.hpp:46-47)
-//     against the tile's threshold keys kept in shared memory.  Rows without a usable threshold (heap not full) are
-//     re-evaluated in integers from the reference-order table (exact_admit_ct, scan_common.cuh).  The sign test never
-//     drops a pair the exact test would admit, so results are exact by construction, as in scan.cu.
+//     against the tile's threshold keys kept in shared memory (dense form), or the pair's coordinates are queued and
+//     its sum is recomputed from the reference-order table, 32 pairs at a time (sparse forms; exact_admit_ct,
+//     scan_common.cuh, which also serves rows without a usable threshold).  The sign test never drops a pair the
+//     exact test would admit, so results are exact by construction, as in scan.cu.
 //   * Warp roles: 0-7 epilogue (TMEM lane quadrant = warp id % 4, column half = warp id / 4), 8-11 one-hot
 //     generators, 12 and 14 MMA issuers (sparse forms: one per accumulator buffer; 12 also owns the TMEM allocation),
 //     13 producer (TMA code stream, tile loads, threshold rows).  All hand-offs are mbarriers; tcgen05.commit releases
@@ -80,14 +81,14 @@ constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13, TC_MMA_WARP2 = 14;
 constexpr int TC_THREADS = 15 * 32;
 constexpr int TC_WQ_CAP = 64;          // per-epilogue-warp queue of admitted (key, row) pairs
-constexpr int TC_DUMP_BYTES = 16 * 32 * 4; // sparse forms: per-epilogue-warp scratch for one flagged group of 16 registers x 32 lanes
+constexpr int TC_WQ_ID_BYTES = TC_WQ_CAP * 4; // sparse forms: the queue entries' ids (their entries are coordinates: code, row, id)
 // query tiles per job: the CTA-pair form keeps TWO tiles' tables resident (its B halves are small enough) and runs every
 // one-hot stage against both, one tile per accumulator buffer -- half the generator work, stores and hand-overs per pair
 __host__ __device__ constexpr int tc_nt(bool pair) { return pair ? 2 : 1; }
 __host__ __device__ constexpr int tc_smem(bool sp, bool pair = false) {
     return tc_nt(pair) * tc_b_bytes(sp, pair) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES +
            TC_INFO * TC_SUB * 8 + TC_TKBUF * tc_nt(pair) * 256 * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12 +
-           (sp ? TC_EPI_WARPS * TC_DUMP_BYTES : 0);
+           (sp ? TC_EPI_WARPS * TC_WQ_ID_BYTES : 0);
 }
 
 struct SubInfo {
@@ -337,7 +338,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     uint64_t* s_tk = reinterpret_cast<uint64_t*>(info_codes + TC_INFO * TC_SUB); // [TC_TKBUF][TC_TQ] threshold keys per tile
     uint64_t* s_wq_key = s_tk + TC_TKBUF * TK_STRIDE;                              // [TC_EPI_WARPS][TC_WQ_CAP]
     uint32_t* s_wq_row = reinterpret_cast<uint32_t*>(s_wq_key + TC_EPI_WARPS * TC_WQ_CAP);
-    uint4* s_dump = reinterpret_cast<uint4*>(s_wq_row + TC_EPI_WARPS * TC_WQ_CAP); // (sparse forms only) [TC_EPI_WARPS][4][32]
+    uint32_t* s_wq_id = s_wq_row + TC_EPI_WARPS * TC_WQ_CAP;                         // (sparse forms only) [TC_EPI_WARPS][TC_WQ_CAP]
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // CTA pair: both CTAs walk the same jobs; rank r generates, holds and post-processes the r-th 128 codes of every step
@@ -728,7 +729,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         const uint32_t col_w = half_w * (TC_TQ / 2);
         uint64_t* wq_key = s_wq_key + warp * TC_WQ_CAP;
         uint32_t* wq_row = s_wq_row + warp * TC_WQ_CAP;
-        uint32_t* wq_id = reinterpret_cast<uint32_t*>(s_dump + warp * (TC_DUMP_BYTES / 16)); // (sparse forms) [TC_WQ_CAP]
+        uint32_t* wq_id = s_wq_id + warp * TC_WQ_CAP;
         uint32_t qn = 0; // warp-uniform fill level of the queue
         TC_PROF_DECL(3);
 #ifdef TC_PROFILE
@@ -814,10 +815,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         // thr < q_max: unsaturated), so the CandidateHeap::push test (heap.hpp:46-47) only needs the tile's
                         // threshold key from shared memory.  Admitted keys go through a per-warp queue.
                         if constexpr (SP) {
-                            // LANE-LOCAL admission (sparse forms): every lane with flagged sums walks its own hits -- masks,
-                            // the group's registers through its own scratch slots, the threshold test -- with no votes or
-                            // reductions in the loop, and reserves queue slots with a shared-memory atomic.  (The warp-uniform
-                            // walk over the union of flagged columns below cost ~1000 cycles per visit.)
+                            // LANE-LOCAL admission (sparse forms): every lane with flagged sums turns its sign bits into column
+                            // masks and queues the pairs' COORDINATES (code, table row, id); drain() recomputes their sums
+                            // exactly.  No votes or reductions in the loop.  (The warp-uniform walk over the union of flagged
+                            // columns of the dense form below costs ~1000 cycles per visit.)
                             uint32_t m[4];
                             uint32_t todo = 0;
 #pragma unroll
@@ -913,31 +914,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             const uint32_t hh = uint32_t(__ffs(gany) - 1);
                             const uint32_t mine = hh == 0 ? m[0] : hh == 1 ? m[1] : hh == 2 ? m[2] : m[3];
                             uint32_t u = __reduce_or_sync(0xffffffffu, mine);
-                            uint4* dump = s_dump + warp * (TC_DUMP_BYTES / 16);
-                            if constexpr (SP) {
-                                // registers cannot be indexed dynamically: the flagged group's 16 registers go to this warp's
-                                // scratch ([quad of registers][lane]: conflict-free 16-byte stores) and are read back by index
-                                // (each lane reads only what it wrote).  The 64-way switch this replaces is 2 KB of rarely
-                                // executed code, i.e. instruction-cache misses every time the path is taken.
-                                switch (hh) {
-#define QADC_DUMP16(k0)                                                                              \
-    dump[0 * 32 + lane] = make_uint4(v[k0 + 0], v[k0 + 1], v[k0 + 2], v[k0 + 3]);                    \
-    dump[1 * 32 + lane] = make_uint4(v[k0 + 4], v[k0 + 5], v[k0 + 6], v[k0 + 7]);                    \
-    dump[2 * 32 + lane] = make_uint4(v[k0 + 8], v[k0 + 9], v[k0 + 10], v[k0 + 11]);                  \
-    dump[3 * 32 + lane] = make_uint4(v[k0 + 12], v[k0 + 13], v[k0 + 14], v[k0 + 15]);
-                                case 0: QADC_DUMP16(0) break;
-                                case 1: QADC_DUMP16(16) break;
-                                case 2: QADC_DUMP16(32) break;
-                                default: QADC_DUMP16(48) break;
-#undef QADC_DUMP16
-                                }
-                            }
                             while (u) {
                                 const uint32_t b = uint32_t(__ffs(u) - 1);
                                 u &= u - 1;
-                                uint32_t raw; // columns 2i (low half) and 2i + 1
-                                if constexpr (SP) raw = reinterpret_cast<const uint32_t*>(dump + ((b & 15u) >> 2) * 32 + lane)[b & 3u];
-                                else raw = pick64(v, hh * 16 + (b & 15u));
+                                const uint32_t raw = pick64(v, hh * 16 + (b & 15u)); // columns 2i (low half) and 2i + 1
                                 const uint32_t val = (b >> 4) ? uint32_t(int(raw) >> 16) : uint32_t(int(raw << 16) >> 16);
                                 const uint32_t col = c0 + hh * 32 + 2 * (b & 15u) + (b >> 4);
                                 uint64_t key = 0;
