@@ -67,7 +67,6 @@ constexpr int TC_NSTAGE = 3;           // code stages (TMA ring)
 constexpr int TC_STAGE_BYTES = 8192;   // 1024 codes
 constexpr int TC_STAGE_CODES = TC_STAGE_BYTES / 8;
 constexpr int TC_INFO = 8;             // sub-tile info ring (generator -> epilogue)
-constexpr int TC_TKBUF = 4;            // per-tile threshold keys kept for the epilogue (it trails the producer by < 4 tiles)
 constexpr int TC_KC = 16;              // 16-byte K chunks of the table part (= tables)
 // B rows one CTA holds: the whole tile, or half of it for a CTA pair (cta_group::2 reads the other half from the peer)
 __host__ __device__ constexpr int tc_brows(bool sp, bool pair = false) { return pair ? tc_tq(sp) / 2 : tc_tq(sp); }
@@ -81,22 +80,19 @@ constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_GEN_WARP0 = 8, TC_MMA_WARP = 12, TC_PROD_WARP = 13, TC_MMA_WARP2 = 14;
 constexpr int TC_THREADS = 15 * 32;
 constexpr int TC_WQ_CAP = 64;          // per-epilogue-warp queue of admitted (key, row) pairs
-constexpr int TC_WQ_ID_BYTES = TC_WQ_CAP * 4; // sparse forms: the queue entries' ids (their entries are coordinates: code, row, id)
 // query tiles per job: the CTA-pair form keeps TWO tiles' tables resident (its B halves are small enough) and runs every
 // one-hot stage against both, one tile per accumulator buffer -- half the generator work, stores and hand-overs per pair
 __host__ __device__ constexpr int tc_nt(bool pair) { return pair ? 2 : 1; }
 __host__ __device__ constexpr int tc_smem(bool sp, bool pair = false) {
     return tc_nt(pair) * tc_b_bytes(sp, pair) + TC_AP_BYTES + tc_na(sp) * tc_a_bytes(sp) + TC_NSTAGE * TC_STAGE_BYTES +
-           TC_INFO * TC_SUB * 8 + TC_TKBUF * tc_nt(pair) * 256 * 8 + TC_EPI_WARPS * TC_WQ_CAP * 12 +
-           (sp ? TC_EPI_WARPS * TC_WQ_ID_BYTES : 0);
+           TC_INFO * TC_SUB * 8 + TC_EPI_WARPS * TC_WQ_CAP * 16;
 }
 
 struct SubInfo {
     uint64_t id_ref;    // explicit ids: index of row 0's id in ScanArgs::ids; implicit: id of row 0
     uint32_t n_valid;   // codes in this sub-tile (rows >= n_valid are padding)
     uint32_t row_begin; // first LUT row of the tile
-    uint32_t tk_slot;   // which s_tk buffer holds this tile's threshold keys
-    uint32_t pad;
+    uint32_t pad[2];
 };
 
 // the rare rows without a usable threshold (heap not full, or its worst entry saturated): integer re-evaluation from the
@@ -282,19 +278,6 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 
 using G44 = GeomCT<8, 8, 4, 4>; // 16x{4,4}: bit position of subquantizer j = 4 j
 
-// v[r] for a WARP-UNIFORM r: registers cannot be indexed dynamically, so this is a switch, which ptxas turns into a
-// six-level tree of uniform branches (~15 instructions, no divergence, no local memory)
-#define QADC_PICK4(b) case b: out = v[b]; break; case b + 1: out = v[b + 1]; break; case b + 2: out = v[b + 2]; break; case b + 3: out = v[b + 3]; break;
-#define QADC_PICK16(b) QADC_PICK4(b) QADC_PICK4(b + 4) QADC_PICK4(b + 8) QADC_PICK4(b + 12)
-__device__ __forceinline__ uint32_t pick64(const uint32_t (&v)[64], uint32_t r) {
-    uint32_t out = 0;
-    switch (r) {
-        QADC_PICK16(0) QADC_PICK16(16) QADC_PICK16(32) QADC_PICK16(48)
-    default: break;
-    }
-    return out;
-}
-
 // sub-tiles of one job: its stages hold TC_STAGE_CODES codes each, every stage is cut into sub-tiles of TC_SUB codes
 // (CTA pair: a step covers 2 x TC_SUB codes, the CTA of rank r takes the r-th half)
 __device__ __forceinline__ uint32_t job_subtiles(uint32_t n_codes, uint32_t step = TC_SUB) {
@@ -314,7 +297,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     constexpr uint32_t TC_STEP = PAIR ? 2 * TC_SUB : TC_SUB; // codes per MMA step of the CTA (pair)
     constexpr uint32_t NCTA = PAIR ? 2 : 1;
     constexpr uint32_t NT = tc_nt(PAIR);          // query tiles per job = consumers of one one-hot stage
-    constexpr uint32_t TK_STRIDE = NT * 256;      // threshold keys per s_tk slot
     extern __shared__ __align__(1024) char smem[];
     __shared__ DevSpec s_ds;
     __shared__ ScanArgs s_args;
@@ -335,10 +317,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
     char* sA = sAp + TC_AP_BYTES;
     char* stage = sA + TC_NA * TC_A_BYTES;
     uint2* info_codes = reinterpret_cast<uint2*>(stage + TC_NSTAGE * TC_STAGE_BYTES);
-    uint64_t* s_tk = reinterpret_cast<uint64_t*>(info_codes + TC_INFO * TC_SUB); // [TC_TKBUF][TC_TQ] threshold keys per tile
-    uint64_t* s_wq_key = s_tk + TC_TKBUF * TK_STRIDE;                              // [TC_EPI_WARPS][TC_WQ_CAP]
+    uint64_t* s_wq_key = reinterpret_cast<uint64_t*>(info_codes + TC_INFO * TC_SUB); // [TC_EPI_WARPS][TC_WQ_CAP] queued codes
     uint32_t* s_wq_row = reinterpret_cast<uint32_t*>(s_wq_key + TC_EPI_WARPS * TC_WQ_CAP);
-    uint32_t* s_wq_id = s_wq_row + TC_EPI_WARPS * TC_WQ_CAP;                         // (sparse forms only) [TC_EPI_WARPS][TC_WQ_CAP]
+    uint32_t* s_wq_id = s_wq_row + TC_EPI_WARPS * TC_WQ_CAP;
 
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // CTA pair: both CTAs walk the same jobs; rank r generates, holds and post-processes the r-th 128 codes of every step
@@ -419,10 +400,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     }
                 }
                 // threshold K step: row r gets 32 signed bytes that sum to v
-                uint64_t* tkb = s_tk + (tseq % TC_TKBUF) * TK_STRIDE;
                 for (uint32_t r = lane; r < NT * uint32_t(TC_TQ); r += 32) {
                     int v = 4064; // padding rows never admit
-                    uint64_t tk_row = KEY_INF;
                     if (r < job.n_rows) {
                         const uint32_t row = job.row_begin + r;
                         const uint32_t q = a->row_query ? a->row_query[row] : row;
@@ -434,7 +413,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             // >= job.id_base, and if that exceeds the id of the heap's worst entry, a sum EQUAL to the
                             // threshold gives key > worst key -- CandidateHeap::push rejects it (heap.hpp:46-47).  The
                             // effective threshold is then (thr - 1, any id): with 8-bit sums about half of the pairs at or
-                            // below the threshold sit exactly on it, and each would cost the epilogue an admission attempt.
+                            // below the threshold sit exactly on it, and each would cost the epilogue an admission attempt (drain() tests
+                            // against the REAL key, so a pair that slips through is still judged correctly).
                             if (tk != KEY_INF && thr < ds->qmax && a->ids == nullptr && job.id_base > uint32_t(tk)) {
                                 if (thr == 0) {
                                     tk = 0; // nothing is below a zero threshold: never admit (v stays at the padding value)
@@ -443,13 +423,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                     tk = make_key(thr, 0xFFFFFFFFu);
                                 }
                             }
-                            tk_row = tk;
                             if (tk == 0) v = 4064;
                             else if (tk == KEY_INF || thr >= ds->qmax) v = -4096; // heap not full / worst saturated: admit all
                             else v = 2048 + int(bias) - int(thr) - 1;
                         }
                     }
-                    tkb[r] = tk_row;
                     uint32_t w[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
@@ -591,8 +569,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         inf.id_ref = a->ids ? job.ids_off + pos : uint64_t(job.id_base) + pos;
                         inf.n_valid = sub_g * TC_SUB < cnt ? min(uint32_t(TC_SUB), cnt - sub_g * TC_SUB) : 0u;
                         inf.row_begin = job.row_begin;
-                        inf.tk_slot = (tseq - 1) % TC_TKBUF;
-                        inf.pad = 0;
+                        inf.pad[0] = inf.pad[1] = 0;
                         s_info[slot] = inf;
                     }
                 };
@@ -741,20 +718,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
             for (uint32_t base = 0; base < qn; base += 32) {
                 const uint32_t e = base + lane;
                 if (e < qn) {
-                    if constexpr (SP) {
-                        // sparse forms: the queue holds COORDINATES (code, table row, id) of flagged pairs; the sum is
-                        // recomputed from the reference-order table -- 16 independent byte loads -- and goes through the
-                        // CandidateHeap::push test against the query's current key (exact_admit_ct, scan_common.cuh)
-                        const uint64_t code = wq_key[e];
-                        tc_exact_admit(ds, a, uint32_t(code), uint32_t(code >> 32), wq_row[e], wq_id[e]);
-                    } else {
-                        const uint64_t key = wq_key[e];
-                        const uint32_t row = wq_row[e];
-                        const uint32_t q = a->row_query ? a->row_query[row] : row;
-                        const uint32_t at = atomicAdd(&a->cand_count[q], 1u);
-                        if (at < a->cap) a->cand[size_t(q) * a->cap + at] = key;
-                        else a->overflow[q] = 1u;
-                    }
+                    // the queue holds COORDINATES (code, table row, id) of flagged pairs; the sum is recomputed from the
+                    // reference-order table -- 16 independent byte loads -- and goes through the CandidateHeap::push test
+                    // against the query's current key (exact_admit_ct, scan_common.cuh)
+                    const uint64_t code = wq_key[e];
+                    tc_exact_admit(ds, a, uint32_t(code), uint32_t(code >> 32), wq_row[e], wq_id[e]);
                 }
             }
             __syncwarp();
@@ -814,11 +782,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                         // instruction-cache misses).  The accumulator IS the exact sum (D = bias + sum - thr - 1 with
                         // thr < q_max: unsaturated), so the CandidateHeap::push test (heap.hpp:46-47) only needs the tile's
                         // threshold key from shared memory.  Admitted keys go through a per-warp queue.
-                        if constexpr (SP) {
-                            // LANE-LOCAL admission (sparse forms): every lane with flagged sums turns its sign bits into column
+                        {
+                            // LANE-LOCAL admission: every lane with flagged sums turns its sign bits into column
                             // masks and queues the pairs' COORDINATES (code, table row, id); drain() recomputes their sums
-                            // exactly.  No votes or reductions in the loop.  (The warp-uniform walk over the union of flagged
-                            // columns of the dense form below costs ~1000 cycles per visit.)
+                            // exactly.  No votes or reductions in the loop.  (A warp-uniform walk over the union of flagged
+                            // columns, picking values out of the registers, cost ~1000 cycles per visit.)
                             uint32_t m[4];
                             uint32_t todo = 0;
 #pragma unroll
@@ -890,62 +858,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                                 __syncwarp();
                             }
                             }
-                        } else {
-                        uint32_t m[4] = {0u, 0u, 0u, 0u};
-                        uint32_t gany = 0; // groups flagged anywhere in the warp (warp-uniform)
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            if (__any_sync(0xffffffffu, valid && g[k] != 0u)) {
-                                gany |= 1u << k;
-#pragma unroll
-                                for (int i = 0; i < 16; ++i) {
-                                    const uint32_t x = i == 15 ? v[16 * k + i] : (v[16 * k + i] >> (15 - i));
-                                    m[k] |= x & (0x00010001u << i);
-                                }
-                                if (!valid) m[k] = 0u;
-                            }
                         }
-                        const uint64_t* tks = s_tk + inf.tk_slot * TK_STRIDE + toff;
-                        const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, max(inf.n_valid, 1u) - 1u)] : uint32_t(inf.id_ref) + rowi;
-                        // ONE copy of the column loop (the switch inside pick64 is ~200 instructions; sixteen inlined
-                        // copies of it thrashed the instruction cache)
-#pragma unroll 1
-                        for (; gany; gany &= gany - 1u) { // only the flagged groups (usually one)
-                            const uint32_t hh = uint32_t(__ffs(gany) - 1);
-                            const uint32_t mine = hh == 0 ? m[0] : hh == 1 ? m[1] : hh == 2 ? m[2] : m[3];
-                            uint32_t u = __reduce_or_sync(0xffffffffu, mine);
-                            while (u) {
-                                const uint32_t b = uint32_t(__ffs(u) - 1);
-                                u &= u - 1;
-                                const uint32_t raw = pick64(v, hh * 16 + (b & 15u)); // columns 2i (low half) and 2i + 1
-                                const uint32_t val = (b >> 4) ? uint32_t(int(raw) >> 16) : uint32_t(int(raw << 16) >> 16);
-                                const uint32_t col = c0 + hh * 32 + 2 * (b & 15u) + (b >> 4);
-                                uint64_t key = 0;
-                                bool push = false;
-                                if ((mine >> b) & 1u) {
-                                    const uint64_t tk = tks[col];
-                                    const uint32_t thr = uint32_t(tk >> 32);
-                                    if (tk == KEY_INF || thr >= ds->qmax) {
-                                        const uint2 code = info_codes[slot * TC_SUB + rowi];
-                                        tc_exact_admit(ds, a, code.x, code.y, inf.row_begin + toff + col, id);
-                                    } else {
-                                        key = make_key(uint32_t(int(val) + int(thr) + 1), id);
-                                        push = key < tk;
-                                    }
-                                }
-                                const uint32_t bal = __ballot_sync(0xffffffffu, push);
-                                if (bal) {
-                                    if (qn + 32 > uint32_t(TC_WQ_CAP)) drain();
-                                    if (push) {
-                                        const uint32_t e = qn + __popc(bal & lt_mask);
-                                        wq_key[e] = key;
-                                        wq_row[e] = inf.row_begin + toff + col;
-                                    }
-                                    qn += __popc(bal);
-                                }
-                            }
-                        }
-                        } // (dense form)
                     }
                 }
                 if (qn >= 32) drain();
