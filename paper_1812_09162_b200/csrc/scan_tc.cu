@@ -774,14 +774,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                     const uint32_t any = g[0] | g[1] | g[2] | g[3];
                     const uint32_t hit_lanes = __ballot_sync(0xffffffffu, valid && any != 0u);
                     if (hit_lanes != 0u && !(dbg & 8u)) {
-                        // rare (warp-uniform branch): some sums of this sub-tile are <= their query's threshold.  For each
-                        // group of 32 columns that is flagged anywhere in the warp, all lanes turn their 32 sign bits into a
-                        // mask (bit i = column 2i, bit 16 + i = column 2i + 1); the warp then walks the UNION of flagged
-                        // columns and re-reads them from TMEM with one-column loads, four per wait (registers cannot be
-                        // indexed dynamically, and an unrolled test per column was measured 1.8x slower on the whole scan:
-                        // instruction-cache misses).  The accumulator IS the exact sum (D = bias + sum - thr - 1 with
-                        // thr < q_max: unsaturated), so the CandidateHeap::push test (heap.hpp:46-47) only needs the tile's
-                        // threshold key from shared memory.  Admitted keys go through a per-warp queue.
+                        // rare (warp-uniform branch): some sums of this sub-tile are <= their query's threshold (D = bias + sum -
+                        // thr - 1 is negative).  Nothing but the sign is used from here on.
                         {
                             // LANE-LOCAL admission: every lane with flagged sums turns its sign bits into column
                             // masks and queues the pairs' COORDINATES (code, table row, id); drain() recomputes their sums
