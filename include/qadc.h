@@ -180,7 +180,15 @@ int qadc_merge_topk_device(const uint64_t* d_keys, uint32_t nshards, uint32_t nq
 typedef struct qadc_multi qadc_multi;
 int qadc_flat_open_sharded(const qadc_spec* spec, const float* codebook, const uint8_t* packed, uint64_t count, int ndev,
                            const int* devices, qadc_multi** out);
-/* FlatIndex::search over a batch (index.hpp:110), host buffers, same output convention as qadc_search_batch */
+/* The same for IvfIndex (index.hpp:166-177, 276-341; arguments as qadc_ivf_open): EVERY list is split evenly on
+ * packed-block boundaries (ids are explicit, so any split is legal: scan_scalar.hpp:60) and the first
+ * min(count, QADC_MAX_T) codes of every unsharded list are replicated as calibration heads, so probe order, tables,
+ * d_min_global, d_max, delta and the biases come out identical on every device. */
+int qadc_ivf_open_sharded(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
+                          const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
+                          const uint64_t* list_count, const uint32_t* ids, int ndev, const int* devices, qadc_multi** out);
+/* FlatIndex::search / IvfIndex::search over a batch (index.hpp:110, 276), host buffers, same output convention as
+ * qadc_search_batch */
 int qadc_multi_search_batch(qadc_multi* h, const float* queries, uint32_t nq, const qadc_search_params* params,
                             uint32_t* out_ids, float* out_dists, uint32_t* out_counts);
 int qadc_multi_info(const qadc_multi* h, int* ndev, uint64_t* count, int* uses_nccl);

@@ -186,6 +186,43 @@ private:
 class GpuIvfIndex {
 public:
     explicit GpuIvfIndex(const pqscan::IvfIndex& ref, int device = 0) : dims_(ref.dims()), cells_(ref.cells()) {
+        open(ref, device, 0, nullptr);
+    }
+    // every list split over `ndev` GPUs of this process (devices = nullptr: ordinals 0..ndev-1): qadc_ivf_open_sharded
+    GpuIvfIndex(const pqscan::IvfIndex& ref, int ndev, const int* devices) : dims_(ref.dims()), cells_(ref.cells()) {
+        open(ref, 0, ndev, devices);
+    }
+    GpuIvfIndex(const GpuIvfIndex&) = delete;
+    GpuIvfIndex& operator=(const GpuIvfIndex&) = delete;
+    ~GpuIvfIndex() {
+        qadc_close(h_);
+        qadc_multi_close(m_);
+    }
+
+    pqscan::SearchResult search(std::span<const float> query, const pqscan::SearchParams& params) const {
+        if (query.size() != dims_) throw pqscan::input_error("search: query has wrong dimension");
+        return search_batch(query, 1, params)[0];
+    }
+    std::vector<pqscan::SearchResult> search_batch(std::span<const float> queries, uint32_t nq,
+                                                   const pqscan::SearchParams& params) const {
+        if (queries.size() != size_t{nq} * dims_) throw pqscan::input_error("search: query has wrong dimension");
+        const qadc_search_params p = detail::params_of(params);
+        std::vector<uint32_t> ids(size_t{nq} * p.r), counts(nq);
+        std::vector<float> dists(size_t{nq} * p.r);
+        if (m_) rethrow(qadc_multi_search_batch(m_, queries.data(), nq, &p, ids.data(), dists.data(), counts.data()));
+        else rethrow(qadc_search_batch(h_, queries.data(), nq, &p, ids.data(), dists.data(), counts.data()));
+        return detail::split(nq, p.r, ids, dists, counts);
+    }
+    std::vector<uint32_t> probe_order(std::span<const float> query, uint32_t a) const {
+        if (query.size() != dims_) throw pqscan::input_error("probe_order: query has wrong dimension");
+        if (!h_) throw pqscan::config_error("probe_order: not available on a sharded index");
+        std::vector<uint32_t> order(std::min(a, cells_)); // index.hpp:250
+        rethrow(qadc_ivf_probe_order(h_, query.data(), 1, a, order.data()));
+        return order;
+    }
+
+private:
+    void open(const pqscan::IvfIndex& ref, int device, int ndev, const int* devices) {
         const qadc_spec s = to_abi(ref.codebook().spec());
         const std::vector<float> cb = flatten(ref.codebook());
         std::vector<uint8_t> packed;
@@ -198,35 +235,15 @@ public:
             packed.insert(packed.end(), ref.lists()[c].data.begin(), ref.lists()[c].data.end());
             ids.insert(ids.end(), ref.list_ids()[c].begin(), ref.list_ids()[c].end());
         }
-        rethrow(qadc_ivf_open(&s, cb.data(), ref.coarse_centroids().data(), ref.cells(), packed.data(), boff.data(),
-                              ioff.data(), cnt.data(), ids.data(), nullptr, nullptr, nullptr, nullptr, device, &h_));
+        if (ndev > 0)
+            rethrow(qadc_ivf_open_sharded(&s, cb.data(), ref.coarse_centroids().data(), ref.cells(), packed.data(), boff.data(),
+                                          ioff.data(), cnt.data(), ids.data(), ndev, devices, &m_));
+        else
+            rethrow(qadc_ivf_open(&s, cb.data(), ref.coarse_centroids().data(), ref.cells(), packed.data(), boff.data(),
+                                  ioff.data(), cnt.data(), ids.data(), nullptr, nullptr, nullptr, nullptr, device, &h_));
     }
-    GpuIvfIndex(const GpuIvfIndex&) = delete;
-    GpuIvfIndex& operator=(const GpuIvfIndex&) = delete;
-    ~GpuIvfIndex() { qadc_close(h_); }
-
-    pqscan::SearchResult search(std::span<const float> query, const pqscan::SearchParams& params) const {
-        if (query.size() != dims_) throw pqscan::input_error("search: query has wrong dimension");
-        return search_batch(query, 1, params)[0];
-    }
-    std::vector<pqscan::SearchResult> search_batch(std::span<const float> queries, uint32_t nq,
-                                                   const pqscan::SearchParams& params) const {
-        if (queries.size() != size_t{nq} * dims_) throw pqscan::input_error("search: query has wrong dimension");
-        const qadc_search_params p = detail::params_of(params);
-        std::vector<uint32_t> ids(size_t{nq} * p.r), counts(nq);
-        std::vector<float> dists(size_t{nq} * p.r);
-        rethrow(qadc_search_batch(h_, queries.data(), nq, &p, ids.data(), dists.data(), counts.data()));
-        return detail::split(nq, p.r, ids, dists, counts);
-    }
-    std::vector<uint32_t> probe_order(std::span<const float> query, uint32_t a) const {
-        if (query.size() != dims_) throw pqscan::input_error("probe_order: query has wrong dimension");
-        std::vector<uint32_t> order(std::min(a, cells_)); // index.hpp:250
-        rethrow(qadc_ivf_probe_order(h_, query.data(), 1, a, order.data()));
-        return order;
-    }
-
-private:
     qadc_index* h_ = nullptr;
+    qadc_multi* m_ = nullptr;
     uint32_t dims_, cells_;
 };
 

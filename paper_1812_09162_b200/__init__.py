@@ -5,6 +5,6 @@ the ctypes loader, the host-side mirror of the reference interface (``index``), 
 helpers (``layout``), seeded synthetic inputs (``synth``) and the multi-GPU shard/merge glue (``dist``).
 """
 from ._lib import QadcError, QadcSpec, build, lib  # noqa: F401
-from .index import (FlatIndex, IvfIndex, MultiGpuFlatIndex, SearchParams, SearchResult, allocate_dims, build_ivf_lists, encode,  # noqa: F401
+from .index import (FlatIndex, IvfIndex, MultiGpuFlatIndex, MultiGpuIvfIndex, SearchParams, SearchResult, allocate_dims, build_ivf_lists, encode,  # noqa: F401
                     ivf_assign_encode, merge_topk_device, open_index, packed_bytes, scan_list)
 from .layout import pack_list, unpack_list  # noqa: F401

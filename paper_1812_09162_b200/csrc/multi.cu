@@ -97,7 +97,8 @@ struct qadc_multi {
     std::vector<int> devices;
     std::vector<qadc_index*> shards;
     std::vector<cudaStream_t> streams;
-    std::vector<ncclComm_t> comms; // empty: single device without NCCL
+    std::vector<ncclComm_t> comms; // empty: single device without NCCL, or the same-device test mode
+    bool local_gather = false;     // QADC_MULTI_SAME_DEVICE_TEST: the shards share a device, the exchange is device-to-device copies
     std::vector<DevMem> queries, keys, map, gathered;
     DevMem out_ids, out_dists, out_counts; // on devices[0]
     std::string error;
@@ -114,6 +115,52 @@ struct qadc_multi {
     }
 };
 
+// Test hook: with QADC_MULTI_SAME_DEVICE_TEST=1 a device may be listed several times, so that the sharding arithmetic of
+// this host (ranges, base ids, replicated heads, gather order, merge) runs with ndev > 1 on a one-GPU box; the exchange
+// is then a device-to-device copy instead of ncclAllGather (NCCL refuses two ranks on one device).
+static bool same_device_test() {
+    const char* e = std::getenv("QADC_MULTI_SAME_DEVICE_TEST");
+    return e && e[0] == '1';
+}
+
+// devices[] -> m->devices, streams, NCCL communicators
+static void multi_setup_devices(qadc_multi* m, int ndev, const int* devices) {
+    int visible = 0;
+    if (cudaGetDeviceCount(&visible) != cudaSuccess || visible == 0)
+        throw Error(QADC_ERR_CUDA, "no usable CUDA device (this library has no CPU fallback)");
+    m->ndev = ndev;
+    for (int i = 0; i < ndev; ++i) {
+        const int d = devices ? devices[i] : i;
+        if (d < 0 || d >= visible) throw Error(QADC_ERR_INPUT, "open_sharded: device ordinal out of range");
+        if (std::find(m->devices.begin(), m->devices.end(), d) != m->devices.end()) {
+            if (!same_device_test()) throw Error(QADC_ERR_INPUT, "open_sharded: a device is listed twice (one shard per GPU)");
+            m->local_gather = true;
+        }
+        m->devices.push_back(d);
+    }
+}
+
+static void multi_setup_exchange(qadc_multi* m) {
+    const int ndev = m->ndev;
+    m->streams.assign(ndev, nullptr);
+    for (int i = 0; i < ndev; ++i) {
+        QADC_CUDA_CHECK(cudaSetDevice(m->devices[i]));
+        QADC_CUDA_CHECK(cudaStreamCreateWithFlags(&m->streams[i], cudaStreamNonBlocking));
+    }
+    if (m->local_gather) {
+        // (test mode: no communicator)
+    } else if (nccl().ok()) {
+        m->comms.assign(ndev, nullptr);
+        nccl_check(nccl().CommInitAll(m->comms.data(), ndev, m->devices.data()), "ncclCommInitAll");
+    } else if (ndev > 1) {
+        throw Error(QADC_ERR_CUDA, "open_sharded: libnccl.so.2 could not be loaded; the multi-GPU exchange needs NCCL");
+    }
+    m->queries.resize(ndev);
+    m->keys.resize(ndev);
+    m->map.resize(ndev);
+    m->gathered.resize(ndev);
+}
+
 namespace qadc {
 int multi_guarded(const std::function<void()>& f); // api.cu: maps exceptions to status codes + qadc_last_error
 }
@@ -125,20 +172,10 @@ int qadc_flat_open_sharded(const qadc_spec* spec, const float* codebook, const u
     return multi_guarded([&] {
         if (!spec || !codebook || !out || (count && !packed)) throw Error(QADC_ERR_INPUT, "null argument");
         if (ndev < 1) throw Error(QADC_ERR_INPUT, "open_sharded: ndev must be at least 1");
-        int visible = 0;
-        if (cudaGetDeviceCount(&visible) != cudaSuccess || visible == 0)
-            throw Error(QADC_ERR_CUDA, "no usable CUDA device (this library has no CPU fallback)");
         std::unique_ptr<qadc_multi> m(new qadc_multi);
-        m->ndev = ndev;
         m->spec = *spec;
         m->count = count;
-        for (int i = 0; i < ndev; ++i) {
-            const int d = devices ? devices[i] : i;
-            if (d < 0 || d >= visible) throw Error(QADC_ERR_INPUT, "open_sharded: device ordinal out of range");
-            if (std::find(m->devices.begin(), m->devices.end(), d) != m->devices.end())
-                throw Error(QADC_ERR_INPUT, "open_sharded: a device is listed twice (one shard per GPU)");
-            m->devices.push_back(d);
-        }
+        multi_setup_devices(m.get(), ndev, devices);
         // contiguous block-aligned shards (the partition of paper_1812_09162_b200/dist.py::shard_ranges)
         const uint64_t bl = spec->block_len, blocks = (count + bl - 1) / bl;
         const uint64_t block_bytes = uint64_t(spec->groups) * bl * (spec->word_width / 8);
@@ -152,21 +189,65 @@ int qadc_flat_open_sharded(const qadc_spec* spec, const float* codebook, const u
                                           ndev > 1 ? packed : nullptr, ndev > 1 ? head_n : 0, count, m->devices[i], &m->shards[i]);
             if (rc != QADC_OK) throw Error(rc, qadc_last_error());
         }
-        m->streams.assign(ndev, nullptr);
+        multi_setup_exchange(m.get());
+        *out = m.release();
+    });
+}
+
+// IvfIndex over several GPUs behind one handle: EVERY list is split evenly on packed-block boundaries (ids are explicit,
+// so any split is legal: scan_scalar.hpp:60) and the first min(count, QADC_MAX_T) codes of every unsharded list are
+// replicated as calibration heads, so that probe order, tables, d_min_global, d_max, delta and the biases come out
+// identical on every shard (index.hpp:276-341) -- the partition of paper_1812_09162_b200/dist.py::shard_ivf_lists.
+int qadc_ivf_open_sharded(const qadc_spec* spec, const float* codebook, const float* coarse, uint32_t k_cells,
+                          const uint8_t* packed, const uint64_t* list_byte_off, const uint64_t* list_id_off,
+                          const uint64_t* list_count, const uint32_t* ids, int ndev, const int* devices, qadc_multi** out) {
+    return multi_guarded([&] {
+        if (!spec || !codebook || !out || (k_cells && (!coarse || !list_byte_off || !list_id_off || !list_count)))
+            throw Error(QADC_ERR_INPUT, "null argument");
+        if (ndev < 1) throw Error(QADC_ERR_INPUT, "open_sharded: ndev must be at least 1");
+        std::unique_ptr<qadc_multi> m(new qadc_multi);
+        m->spec = *spec;
+        multi_setup_devices(m.get(), ndev, devices);
+        const uint64_t bl = spec->block_len;
+        const uint64_t block_bytes = uint64_t(spec->groups) * bl * (spec->word_width / 8);
+        uint64_t total = 0;
+        for (uint32_t c = 0; c < k_cells; ++c) total += list_count[c];
+        m->count = total;
+        if (total && (!packed || !ids)) throw Error(QADC_ERR_INPUT, "null argument");
+        // the replicated heads (only needed when the lists are really split)
+        std::vector<uint8_t> head_packed;
+        std::vector<uint64_t> head_off(k_cells), head_cnt(k_cells), global_cnt(list_count, list_count + k_cells);
+        if (ndev > 1)
+            for (uint32_t c = 0; c < k_cells; ++c) {
+                const uint64_t hn = std::min<uint64_t>(list_count[c], QADC_MAX_T);
+                const uint64_t hb = (hn + bl - 1) / bl * block_bytes;
+                head_off[c] = head_packed.size();
+                head_cnt[c] = hn;
+                head_packed.insert(head_packed.end(), packed + list_byte_off[c], packed + list_byte_off[c] + hb);
+            }
+        m->shards.assign(ndev, nullptr);
         for (int i = 0; i < ndev; ++i) {
-            QADC_CUDA_CHECK(cudaSetDevice(m->devices[i]));
-            QADC_CUDA_CHECK(cudaStreamCreateWithFlags(&m->streams[i], cudaStreamNonBlocking));
+            std::vector<uint8_t> sp;
+            std::vector<uint32_t> sid;
+            std::vector<uint64_t> boff(k_cells), ioff(k_cells), cnt(k_cells);
+            for (uint32_t c = 0; c < k_cells; ++c) {
+                const uint64_t n = list_count[c], blocks = (n + bl - 1) / bl;
+                const uint64_t b0 = blocks * uint64_t(i) / uint64_t(ndev), b1 = blocks * uint64_t(i + 1) / uint64_t(ndev);
+                const uint64_t start = std::min(b0 * bl, n), end = std::min(b1 * bl, n);
+                boff[c] = sp.size();
+                ioff[c] = sid.size();
+                cnt[c] = end - start;
+                const uint8_t* src = packed + list_byte_off[c];
+                sp.insert(sp.end(), src + b0 * block_bytes, src + b1 * block_bytes);
+                sid.insert(sid.end(), ids + list_id_off[c] + start, ids + list_id_off[c] + end);
+            }
+            const int rc = qadc_ivf_open(spec, codebook, coarse, k_cells, sp.data(), boff.data(), ioff.data(), cnt.data(), sid.data(),
+                                         ndev > 1 ? head_packed.data() : nullptr, ndev > 1 ? head_off.data() : nullptr,
+                                         ndev > 1 ? head_cnt.data() : nullptr, ndev > 1 ? global_cnt.data() : nullptr,
+                                         m->devices[i], &m->shards[i]);
+            if (rc != QADC_OK) throw Error(rc, qadc_last_error());
         }
-        if (nccl().ok()) {
-            m->comms.assign(ndev, nullptr);
-            nccl_check(nccl().CommInitAll(m->comms.data(), ndev, m->devices.data()), "ncclCommInitAll");
-        } else if (ndev > 1) {
-            throw Error(QADC_ERR_CUDA, "open_sharded: libnccl.so.2 could not be loaded; the multi-GPU exchange needs NCCL");
-        }
-        m->queries.resize(ndev);
-        m->keys.resize(ndev);
-        m->map.resize(ndev);
-        m->gathered.resize(ndev);
+        multi_setup_exchange(m.get());
         *out = m.release();
     });
 }
@@ -222,9 +303,15 @@ int qadc_multi_search_batch(qadc_multi* m, const float* queries, uint32_t nq, co
                 nccl_check(nccl().AllGather(m->keys[i].p, m->gathered[i].p, nr, /*ncclUint64*/ 5, m->comms[i], m->streams[i]),
                            "ncclAllGather");
             nccl_check(nccl().GroupEnd(), "ncclGroupEnd");
-        } else {
+        } else { // one device (or the same-device test mode): the "gather" is device-to-device copies in rank order
+            for (int i = 1; i < ndev; ++i) {
+                QADC_CUDA_CHECK(cudaSetDevice(m->devices[i]));
+                QADC_CUDA_CHECK(cudaStreamSynchronize(m->streams[i]));
+            }
             QADC_CUDA_CHECK(cudaSetDevice(m->devices[0]));
-            QADC_CUDA_CHECK(cudaMemcpyAsync(m->gathered[0].p, m->keys[0].p, nr * 8, cudaMemcpyDeviceToDevice, m->streams[0]));
+            for (int i = 0; i < ndev; ++i)
+                QADC_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(m->gathered[0].p) + size_t(i) * nr * 8, m->keys[i].p, nr * 8,
+                                                cudaMemcpyDeviceToDevice, m->streams[0]));
         }
         // merge on device 0 (every rank holds the gathered lists; the reference's caller wants ONE result)
         const int rc = qadc_merge_topk_device(static_cast<const uint64_t*>(m->gathered[0].p), uint32_t(ndev), nq, r,

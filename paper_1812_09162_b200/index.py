@@ -239,6 +239,32 @@ class MultiGpuFlatIndex:
     def __exit__(self, *exc):
         self.close()
 
+
+class MultiGpuIvfIndex(MultiGpuFlatIndex):
+    """One process, several GPUs: IvfIndex with every list split over ``ndev`` devices behind one handle
+    (qadc_ivf_open_sharded): replicated list heads, one NCCL all_gather + merge per batch."""
+
+    def __init__(self, spec: QadcSpec, codebook, coarse, packed, list_byte_off, list_id_off, list_count, ids,
+                 ndev: int = 1, devices=None):
+        self.spec, self._h = spec, C.c_void_p()
+        cb = _f32(codebook).reshape(-1)
+        if cb.size != spec.cb_floats:
+            raise QadcError(5, "codebook: table count does not match spec")
+        co = _f32(coarse).reshape(-1, spec.dims)
+        k = co.shape[0]
+        pk = np.ascontiguousarray(packed, dtype=np.uint8).reshape(-1)
+        boff = np.ascontiguousarray(list_byte_off, dtype=np.uint64)
+        ioff = np.ascontiguousarray(list_id_off, dtype=np.uint64)
+        cnt = np.ascontiguousarray(list_count, dtype=np.uint64)
+        idv = np.ascontiguousarray(ids, dtype=np.uint32)
+        if not (len(boff) == len(ioff) == len(cnt) == k):
+            raise QadcError(5, "ivf: one offset / count per coarse centroid is required")
+        self.count = int(cnt.sum())
+        dv = None if devices is None else np.ascontiguousarray(devices, dtype=np.int32)
+        check(lib().qadc_ivf_open_sharded(C.byref(spec), _p(cb, C.c_float), _p(co, C.c_float), C.c_uint32(k),
+                                          _p(pk, C.c_uint8), _p(boff, C.c_uint64), _p(ioff, C.c_uint64), _p(cnt, C.c_uint64),
+                                          _p(idv, C.c_uint32), C.c_int(ndev), _p(dv, C.c_int), C.byref(self._h)))
+
     def __del__(self):
         try:
             self.close()

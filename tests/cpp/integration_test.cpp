@@ -7,6 +7,7 @@
 // the place of the SIMD kernels, then compares FlatIndex::search / IvfIndex::search with their GPU
 // counterparts on indexes BUILT BY THE REFERENCE (k-means training, encode, pack).  Exit code 0 = all equal.
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 
 #include "qadc.hpp"
@@ -149,7 +150,10 @@ static void flat_checks() {
         {
             int ndev = 0;
             cudaGetDeviceCount_shim(&ndev);
-            qadc::GpuFlatIndex multi(ref, ndev > 0 ? ndev : 1, nullptr);
+            const char* same_env = std::getenv("QADC_MULTI_SAME_DEVICE_TEST"); // three shards on one device (test hook)
+            const int three[3] = {0, 0, 0};
+            const bool dup = same_env && same_env[0] == '1';
+            qadc::GpuFlatIndex multi(ref, dup ? 3 : (ndev > 0 ? ndev : 1), dup ? three : nullptr);
             auto mb = multi.search_batch(queries, 40, p);
             for (uint32_t q = 0; q < 40; ++q) EXPECT(same(batch[q], mb[q]), "flat %s sharded(%d) query %u differs", text, ndev, q);
         }
@@ -183,7 +187,21 @@ static void ivf_checks() {
             EXPECT(same(ref.search({queries.data() + size_t{q} * d, d}, p), rr[q]), "ivf rerank probes=%u query %u differs",
                    probes, q);
     }
-    std::printf("ivf 12x{6,5,5} K=48: identical to IvfIndex::search at probes 1/6/48\n");
+    { // the one-process multi-GPU handle for IVF (qadc_ivf_open_sharded): every list split over the devices of this box
+      // (three shards on one device under QADC_MULTI_SAME_DEVICE_TEST=1, which the Python test sets)
+        int ndev = 0;
+        cudaGetDeviceCount_shim(&ndev);
+        const char* same_env = std::getenv("QADC_MULTI_SAME_DEVICE_TEST");
+        const int three[3] = {0, 0, 0};
+        const bool dup = same_env && same_env[0] == '1';
+        qadc::GpuIvfIndex multi(ref, dup ? 3 : (ndev > 0 ? ndev : 1), dup ? three : nullptr);
+        SearchParams p;
+        p.probes = 6;
+        auto mb = multi.search_batch(queries, 30, p);
+        for (uint32_t q = 0; q < 30; ++q)
+            EXPECT(same(ref.search({queries.data() + size_t{q} * d, d}, p), mb[q]), "ivf sharded query %u differs", q);
+    }
+    std::printf("ivf 12x{6,5,5} K=48: identical to IvfIndex::search at probes 1/6/48 (+ sharded handle)\n");
 }
 
 int main(int argc, char** argv) {

@@ -511,9 +511,55 @@ def test_cpp_integration_binary():
     exe = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "integration_test"
     if not exe.exists():
         pytest.skip("oracle/_ref/integration_test was not built (no reference tree at build time)")
-    out = subprocess.run([str(exe), "25"], capture_output=True, text=True, timeout=900)
-    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
-    assert "INTEGRATION OK" in out.stdout
+    import os
+    for extra in ({}, {"QADC_MULTI_SAME_DEVICE_TEST": "1"}):  # second run: the sharded handles split 3 ways on one device
+        out = subprocess.run([str(exe), "25"], capture_output=True, text=True, timeout=900, env={**os.environ, **extra})
+        assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+        assert "INTEGRATION OK" in out.stdout
+
+
+def test_one_process_sharding_arithmetic_on_one_device(port, monkeypatch):
+    """qadc_flat_open_sharded / qadc_ivf_open_sharded with ndev = 3 on ONE device (test hook
+    QADC_MULTI_SAME_DEVICE_TEST: duplicate ordinals allowed, the exchange is a device-to-device copy instead of
+    ncclAllGather): block-aligned ranges with base ids, every IVF list split three ways, replicated calibration heads,
+    gather order and merge -- same result as the oracle, incl. lists shorter than a block and t beyond short lists."""
+    monkeypatch.setenv("QADC_MULTI_SAME_DEVICE_TEST", "1")
+    rng = np.random.default_rng(77)
+    for dims, text, n in [(128, "16x{4,4}", 100_003), (96, "12x{6,5,5}", 20_000), (64, "8x{8}", 70)]:
+        s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+        cb = (rng.standard_normal(s.cb_floats) * 2).astype(np.float32)
+        pk = qb.pack_list(s, random_codes(s, n, seed=5))
+        queries = (rng.standard_normal((33, dims)) * 2).astype(np.float32)
+        want = port.flat_search(so, cb, pk, n, queries, r=50, t=300, threads=8)
+        with qb.MultiGpuFlatIndex(s, cb, pk, n, ndev=3, devices=[0, 0, 0]) as idx:
+            assert idx.info() == dict(ndev=3, count=n, uses_nccl=False)
+            got = idx.search(queries, qb.SearchParams(r=50, t=300))
+        assert np.array_equal(got.counts, want[2]) and np.array_equal(got.ids, want[0]) and bits_equal(got.dists, want[1])
+    dims, text, k_cells, n = 64, "12x{6,5,5}", 24, 30_000
+    s, so = qb.allocate_dims(dims, text), port.spec(dims, text)
+    cb = (rng.standard_normal(s.cb_floats) * 1.5).astype(np.float32)
+    coarse = (rng.standard_normal((k_cells, dims)) * 3).astype(np.float32)
+    assign = rng.integers(0, k_cells - 2, size=n)  # two empty lists
+    assign[:5] = k_cells - 2                        # and one of five codes
+    codes = random_codes(s, n, seed=8)
+    packed, ids, boff, ioff, counts = [], [], [], [], []
+    b = i = 0
+    for c in range(k_cells):
+        members = np.nonzero(assign == c)[0].astype(np.uint32)
+        lp = qb.pack_list(s, codes[members])
+        boff.append(b); ioff.append(i); counts.append(len(members)); packed.append(lp); ids.append(members)
+        b += lp.size; i += len(members)
+    packed, ids = np.concatenate(packed), np.concatenate(ids)
+    queries = (rng.standard_normal((40, dims)) * 3).astype(np.float32)
+    for probes, r, t in [(5, 60, 250), (24, 100, 2000)]:
+        want = port.ivf_search(so, cb, coarse, packed, boff, ioff, counts, ids, queries, probes=probes, r=r, t=t, threads=8)
+        with qb.MultiGpuIvfIndex(s, cb, coarse, packed, boff, ioff, counts, ids, ndev=3, devices=[0, 0, 0]) as idx:
+            assert idx.info()["ndev"] == 3 and idx.info()["count"] == n
+            got = idx.search(queries, qb.SearchParams(probes=probes, r=r, t=t))
+        assert np.array_equal(got.counts, want[2])
+        for qi in range(len(queries)):
+            c = int(want[2][qi])
+            assert np.array_equal(got.ids[qi, :c], want[0][qi, :c]) and bits_equal(got.dists[qi, :c], want[1][qi, :c])
 
 
 @pytest.mark.parametrize("world", [2, 5])
