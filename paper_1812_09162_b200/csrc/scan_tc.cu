@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
         uint32_t* wq_row = s_wq_row + warp * TC_WQ_CAP;
         uint32_t* wq_id = s_wq_id + warp * TC_WQ_CAP;
         uint32_t qn = 0; // warp-uniform fill level of the queue
+        const uint32_t* ids_ptr = a->ids;
         TC_PROF_DECL(3);
 #ifdef TC_PROFILE
         long long lat_wake = 0, lat_read = 0;
@@ -799,7 +800,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             }
                             // the visit only queues coordinates: no accumulator value is needed again (drain() recomputes the
                             // sum), so there is no register indexing, no threshold lookup and no compare on this path
-                            const uint32_t id = a->ids ? a->ids[inf.id_ref + min(rowi, max(inf.n_valid, 1u) - 1u)] : uint32_t(inf.id_ref) + rowi;
+                            const uint32_t id = ids_ptr ? ids_ptr[inf.id_ref + min(rowi, max(inf.n_valid, 1u) - 1u)] : uint32_t(inf.id_ref) + rowi;
                             const uint2 code2 = info_codes[slot * TC_SUB + rowi];
                             const uint64_t code = (uint64_t(code2.y) << 32) | code2.x;
                             const uint32_t rowbase = inf.row_begin + toff + c0;
@@ -810,14 +811,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan_tc8_kernel(DevSpec ds_para
                             const uint32_t n_one = __shfl_sync(0xffffffffu, n_mine, __ffs(hit_lanes) - 1);
                             if ((hit_lanes & (hit_lanes - 1u)) == 0u && qn + n_one <= uint32_t(TC_WQ_CAP)) {
                                 uint32_t e = qn;
-#pragma unroll
-                                for (int k = 0; k < 4; ++k)
-                                    for (uint32_t mk = m[k]; mk != 0u; mk &= mk - 1u, ++e) {
+                                for (uint32_t t = todo; t != 0u; t &= t - 1u) { // (one copy of the loop: flagged groups only)
+                                    const uint32_t k = uint32_t(__ffs(t) - 1);
+                                    uint32_t mk = k == 0 ? m[0] : k == 1 ? m[1] : k == 2 ? m[2] : m[3];
+                                    for (; mk != 0u; mk &= mk - 1u, ++e) {
                                         const uint32_t b = uint32_t(__ffs(mk) - 1);
                                         wq_key[e] = code;
                                         wq_row[e] = rowbase + k * 32 + 2 * (b & 15u) + (b >> 4);
                                         wq_id[e] = id;
                                     }
+                                }
                                 qn += n_one;
                                 __syncwarp();
                             } else {
